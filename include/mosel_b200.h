@@ -1,0 +1,144 @@
+/* mosel_b200.h — C-ABI of the B200 (sm_100a) hot path of MOSEL-style
+ * modality-aware serving (arXiv 2310.18481; reference package `modserve`).
+ *
+ * The reference is pure Python and has no FFI layer; its
+ * worker seam is a table lookup.  Each entry point below replaces one
+ * reference interface, cited file:line into /root/reference/pkg/src/modserve:
+ *
+ *   ms_policy_select  <- scheduler.py:382-425 apply_policy(OPTIMIZED) on a
+ *                        one-job scope (+ :202-233 detect_violation /
+ *                        compute_budget, :236-326 reassign_optimized,
+ *                        :366-379 try_upgrade); closed form SURVEY §8a P5.
+ *   ms_compact_index  <- strategy.py:54-60 Strategy.make canonical (mask,
+ *   ms_gather_rows       batch) grouping + sim.py:372-377 part loop: turns
+ *   ms_compact           per-request masks into modality-grouped sub-batches.
+ *   ms_gemm_plan_*    <- sim.py:374 profile.part_latency_us(mask, batch)
+ *   ms_gemm_run          stand-in: the per-modality encoders (dense layers,
+ *   ms_op_* / ms_program_run   implicit-GEMM convolutions) and late fusion +
+ *                        head; dropped modalities = all_mask & ~mask
+ *                        (profile.py:157-159) contribute nothing.
+ *   ms_event_* (profiler) <- profile.py:338-356 save_profile producer: the
+ *                        latency table is refreshed from CUDA-event timings.
+ *
+ * Conventions: every call is stream-ordered on the `stream` argument
+ * (a cudaStream_t passed as void*), takes caller-owned device pointers,
+ * performs no allocation and returns an int status: 0 = MS_OK; nonzero maps
+ * to the reference's ValueError family on the Python side; the message is
+ * available from ms_last_error().  Plans/ops are caller-allocated opaque
+ * blobs of MS_GEMM_PLAN_BYTES / MS_OP_BYTES bytes (64-byte aligned).
+ */
+#ifndef MOSEL_B200_H
+#define MOSEL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define MS_OK 0
+#define MS_ERR_INVALID 1
+#define MS_ERR_CUDA 2
+
+#define MS_GEMM_PLAN_BYTES 1024
+#define MS_OP_BYTES 1152
+
+#define MS_DROP (-1)
+
+typedef struct MsSegment {
+  int n_begin;   /* first output column of this segment */
+  int n_end;     /* one past the last */
+  void* ptr;     /* destination base */
+  long long ldd; /* destination row stride (elements) */
+  int col0;      /* destination column of n_begin */
+  int pad_;
+} MsSegment;
+
+int ms_abi_version(void);
+const char* ms_last_error(void);
+int ms_device_sync(void);
+
+/* ---- policy step (one warp per job) --------------------
+ * lat_us[N*C] / credit[N*C]: per-job frontier (ascending latency, strictly
+ * increasing credit), n_cand[N] valid entries, deadline_us[N];
+ * est = round_half_even(lat * factor); B = deadline - dispatch_us.
+ * choice[N] = index into the frontier or MS_DROP. credit may be NULL. */
+int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t* n_cand, int C,
+                     const int64_t* deadline_us, int64_t dispatch_us, double factor, int N,
+                     int32_t* choice, void* stream);
+
+/* ---- request compaction ----------------------------
+ * mask[N] (bit k = modality k present) ->
+ *   idx[K*N]   : idx[k*N + j] = j-th request (ascending) that has modality k
+ *   inv[K*N]   : inv[k*N + i] = position of request i in idx_k, or -1
+ *   counts[K]  : |idx_k|
+ *   combo_offsets[2^K + 1], perm[N]: stable counting sort of requests by mask */
+int ms_compact_index(const uint16_t* mask, int N, int K, int32_t* idx, int32_t* inv, int32_t* counts,
+                     int32_t* combo_offsets, int32_t* perm, void* stream);
+/* dst[j] = src[slot ? slot[idx[j]] : idx[j]] for j < *count (count read on
+ * device); rows of row_bytes (multiple of 16), vectorised 16-B copies. */
+int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
+                   const int32_t* count, int max_rows, void* dst, void* stream);
+/* index + one gather per modality (X[k]/G[k]/row_bytes[k], K <= 8) */
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_bytes,
+               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
+               int32_t* combo_offsets, int32_t* perm, void* stream);
+
+/* ---- tcgen05 GEMM plans (encoders, fusion head) -----------------------
+ * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL. */
+int ms_gemm_plan_dense(void* plan, const void* A, int M, int K, long long lda, const void* W, int N,
+                       int K_pad, int BN, const float* bias, int relu, int out_fp32, void* D,
+                       long long ldd, int col0, int nseg, const MsSegment* segs);
+/* implicit-GEMM conv over NHWC bf16 input [n_img, H, W, C] (channel stride
+ * c_stride); weights [Cout, KH*KW*ceil64(C)] tap-major, each tap's channels
+ * zero-padded to a multiple of 64; output pixel-major [n_img*OH*OW, ...].
+ * (bn, bh, bw) is the output-pixel block one 128-row tile covers. */
+int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
+                      int KH, int KW, int stride, int pad, const void* Wt, int Cout, int BN,
+                      const float* bias, int relu, void* D, long long ldd, int col0, int nseg,
+                      const MsSegment* segs, int bn, int bh, int bw);
+/* masked late-fusion concat GEMM: row i, K slice k*F..(k+1)*F reads
+ * feat[k][inv[k*inv_ld + i]] or zeros when inv == -1. */
+int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
+                        int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
+                        int out_fp32, void* D, long long ldd, int col0);
+int ms_gemm_run(const void* plan, void* stream);
+int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
+
+/* ---- HBM-bound ops (NHWC bf16) ---------------------------------------- */
+/* max (is_max=1) or average (count includes padding) pooling, k x k */
+int ms_pool2d(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride,
+              int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, void* stream);
+/* conv im2col for small-channel first layers: out[pixel, (kh*KW+kw)*C + c],
+ * zero for columns >= KH*KW*C up to K_pad */
+int ms_im2col(const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride, int pad,
+              void* out, int K_pad, void* stream);
+/* global average pool + TSN segment consensus: X[(r*S + s)*HW + p, C] ->
+ * Y[r, C] = mean over s, p */
+int ms_segment_mean(const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld, void* stream);
+
+/* ---- op programs: a whole encoder forward as one native call ---------- */
+int ms_op_gemm(void* op, const void* plan);
+int ms_op_pool2d(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k,
+                 int stride, int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0);
+int ms_op_im2col(void* op, const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride,
+                 int pad, void* out, int K_pad);
+int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld);
+int ms_program_run(const void* ops, int n_ops, void* stream);
+
+/* ---- profiler timing (CUDA events) ------------------------------------ */
+int ms_event_create(void** ev);
+int ms_event_destroy(void* ev);
+int ms_event_record(void* ev, void* stream);
+int ms_event_elapsed_us(void* start, void* stop, double* us);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOSEL_B200_H */

@@ -1,0 +1,487 @@
+// tcgen05/TMEM GEMM for the per-modality encoders and the fusion head.
+//
+//   D[m, n] = act( sum_k A[m, k] * W[n, k] + bias[n] )      bf16 in, fp32 acc
+//
+// One 128 x BN output tile per CTA (UMMA M=128, cta_group::1, N = BN <= 256),
+// K in blocks of 64 bf16 (one 128-byte swizzle row).  Warp roles:
+//   warp 0      : TMA producer (A and W tiles; W always by TMA)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  : epilogue (TMEM -> regs -> bias/ReLU -> global); in
+//                 GATHER mode they are also the A producers (cp.async)
+// A-operand modes:
+//   DENSE  : A is a row-major [M, K] matrix, 2-D TMA box {64, 128}
+//   CONV   : implicit-GEMM convolution over NHWC input. The M tile is a
+//            (bn images x bh rows x bw cols) block of output pixels; each
+//            K block is one (tap, 64-channel chunk) and is ONE 4-D TMA box
+//            {64, bw*s, bh*s, bn} with element strides {1, s, s, 1} at the
+//            tap-shifted coordinate.  TMA zero-fills out-of-bounds
+//            coordinates, which implements the convolution padding and the
+//            channel tail for free.
+//   GATHER : masked late-fusion concat.  Row i, K block kb reads modality
+//            k = kb*64 / F from its compacted feature buffer at row inv_k[i];
+//            absent modalities (inv = -1) are zero-filled — exactly
+//            "skipping those K columns".
+// The epilogue routes 32-column chunks to up to 4 destination segments so
+// merged 1x1 branch GEMMs write straight into Inception concat slices.
+#include <cstdio>
+#include <cstring>
+
+#include "mosel_b200.h"
+#include "ptx.cuh"
+#include "runtime.h"
+
+namespace mosel {
+
+constexpr int kThreads = 192;
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
+
+enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2 };
+
+struct Seg {
+  int n_begin, n_end;
+  void* ptr;
+  long long ldd;
+  int col0;
+  int pad_;
+};
+
+struct GemmParams {
+  int mode;
+  int M;       // DENSE/GATHER rows
+  int N;       // valid output columns
+  int BN;      // tile width (multiple of 32, <= 256)
+  int num_kb;  // K blocks
+  int stages;
+  int a_bytes;  // bytes of one A TMA box (CONV: bn*bh*bw*128)
+  int b_bytes;
+  // CONV geometry
+  int n_img, OH, OW, stride, pad, KW, cchunks, bn, bh, bw, tiles_w, tiles_h;
+  // GATHER
+  const __nv_bfloat16* feat[4];
+  const int32_t* inv;  // [n_mod, inv_ld]
+  int inv_ld, feat_dim, n_mod;
+  // epilogue
+  const float* bias;
+  int relu, out_fp32, nseg, pad_;
+  Seg seg[4];
+};
+
+struct alignas(64) GemmPlan {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  GemmParams p;
+  int grid_x, grid_y, smem_bytes, tmem_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stages = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + stages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + stages * p.b_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* acc_full = empty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tile = blockIdx.x;
+  const int n_tile = blockIdx.y;
+
+  if (threadIdx.x == 0) {
+    const uint32_t full_count = (p.mode == MODE_GATHER) ? 1 + 128 : 1;
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], full_count);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    if (p.mode != MODE_GATHER) tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)p.BN) tmem_cols <<= 1;
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // CONV tile origin
+  int n0 = 0, oh0 = 0, ow0 = 0;
+  if (p.mode == MODE_CONV) {
+    const int tw = m_tile % p.tiles_w;
+    const int th = (m_tile / p.tiles_w) % p.tiles_h;
+    const int tn = m_tile / (p.tiles_w * p.tiles_h);
+    n0 = tn * p.bn;
+    oh0 = th * p.bh;
+    ow0 = tw * p.bw;
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int s = 0;
+      uint32_t phase = 0;
+      const uint32_t tx = (p.mode == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        mbar_wait(&empty[s], phase ^ 1);
+        const uint32_t a_dst = smem_addr(smA + s * kABytes);
+        const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
+        mbar_arrive_expect_tx(&full[s], tx);
+        if (p.mode == MODE_DENSE) {
+          tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
+        } else if (p.mode == MODE_CONV) {
+          const int tap = kb / p.cchunks;
+          const int cc = kb - tap * p.cchunks;
+          const int kh = tap / p.KW;
+          const int kw = tap - kh * p.KW;
+          tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 * p.stride - p.pad + kw,
+                      oh0 * p.stride - p.pad + kh, n0);
+        }
+        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)p.BN);
+    int s = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < p.num_kb; ++kb) {
+      mbar_wait(&full[s], phase);
+      tc_fence_after();
+      if (p.mode == MODE_GATHER) fence_proxy_async_smem();
+      if (lane == 0) {
+        const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
+        const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
+          umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+    if (lane == 0) umma_commit(acc_full);
+    __syncwarp();
+  } else {
+    // ------------------------------------- warps 2..5: gather + epilogue
+    const int q = warp & 3;              // TMEM lane quarter of this warp
+    const int r = q * 32 + lane;         // tile row owned by this thread
+    if (p.mode == MODE_GATHER) {
+      const int row = m_tile * kBM + r;
+      const __nv_bfloat16* src_row[4];
+      for (int k = 0; k < 4; ++k) {
+        src_row[k] = nullptr;
+        if (k < p.n_mod && row < p.M) {
+          const int j = p.inv[(long long)k * p.inv_ld + row];
+          if (j >= 0) src_row[k] = p.feat[k] + (long long)j * p.feat_dim;
+        }
+      }
+      const int kb_per_mod = p.feat_dim / kBK;
+      int s = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        mbar_wait(&empty[s], phase ^ 1);
+        const int k = kb / kb_per_mod;
+        const int off = (kb - k * kb_per_mod) * kBK;
+        const __nv_bfloat16* src = (k < 4) ? src_row[k] : nullptr;
+        const uint32_t dst = smem_addr(smA + s * kABytes) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t phys = (uint32_t)(c ^ (r & 7));
+          cp_async_16(dst + phys * 16, src ? (const void*)(src + off + c * 8) : (const void*)p.feat[0],
+                      src ? 16u : 0u);
+        }
+        cp_async_mbar_arrive_noinc(&full[s]);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    }
+
+    // output row for this thread (or -1)
+    long long out_row = -1;
+    if (p.mode == MODE_CONV) {
+      const int per_img = p.bh * p.bw;
+      if (r < p.bn * per_img) {
+        const int i = r / per_img;
+        const int y = (r - i * per_img) / p.bw;
+        const int x = r - i * per_img - y * p.bw;
+        const int n = n0 + i, oh = oh0 + y, ow = ow0 + x;
+        if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
+      }
+    } else {
+      const int row = m_tile * kBM + r;
+      if (row < p.M) out_row = row;
+    }
+
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int n_first = n_tile * p.BN;
+    for (int c = 0; c < p.BN / 32; ++c) {
+      const int nb = n_first + c * 32;
+      if (nb >= p.N) break;  // warp-uniform
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
+      tmem_wait_ld();
+      if (out_row < 0) continue;
+      int sg = 0;
+      while (sg + 1 < p.nseg && nb >= p.seg[sg].n_end) ++sg;
+      const Seg& S = p.seg[sg];
+      const long long base = out_row * S.ldd + S.col0 + (nb - S.n_begin);
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float x = __uint_as_float(v[j]);
+        const int n = nb + j;
+        if (p.bias != nullptr && n < p.N) x += p.bias[n];
+        if (p.relu) x = fmaxf(x, 0.0f);
+        f[j] = x;
+      }
+      if (p.out_fp32) {
+        float* dst = reinterpret_cast<float*>(S.ptr) + base;
+        const int lim = min(32, p.N - nb);
+        for (int j = 0; j < lim; ++j) dst[j] = f[j];
+      } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(S.ptr) + base;
+        if (nb + 32 <= p.N) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            d4[j] = make_uint4(pack_bf16x2(f[8 * j + 0], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                               pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+          }
+        } else {
+          for (int j = 0; j < p.N - nb; ++j) dst[j] = __float2bfloat16_rn(f[j]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+// ==================================================================== host
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+static int encode_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims,
+                      const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estride) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return set_error(MS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box,
+                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char msg[160];
+    snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (%d) rank=%d", (int)r, rank);
+    return set_error(MS_ERR_INVALID, msg);
+  }
+  return MS_OK;
+}
+
+static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int BN, int num_kb, int grid_x) {
+  GemmParams& p = P->p;
+  if (BN % 32 != 0 || BN < 32 || BN > 256) return set_error(MS_ERR_INVALID, "BN must be a multiple of 32 in [32, 256]");
+  if (K_pad % kBK != 0) return set_error(MS_ERR_INVALID, "weight K must be padded to a multiple of 64");
+  cuuint64_t dims[2] = {(cuuint64_t)K_pad, (cuuint64_t)N_rows_w};
+  cuuint64_t strides[1] = {(cuuint64_t)K_pad * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)BN};
+  cuuint32_t es[2] = {1, 1};
+  int rc = encode_map(&P->tmB, 2, W, dims, strides, box, es);
+  if (rc) return rc;
+  p.BN = BN;
+  p.num_kb = num_kb;
+  p.b_bytes = BN * kBK * 2;
+  const int per_stage = kABytes + p.b_bytes;
+  int stages = (200 * 1024) / per_stage;
+  if (stages > 8) stages = 8;
+  if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
+  p.stages = stages;
+  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 1) * 8 + 16;
+  P->grid_x = grid_x;
+  P->grid_y = (p.N + BN - 1) / BN;
+  int tc = 32;
+  while (tc < BN) tc <<= 1;
+  P->tmem_cols = tc;
+  return MS_OK;
+}
+
+static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D, long long ldd, int col0) {
+  if (nseg <= 0 || segs == nullptr) {
+    p.nseg = 1;
+    p.seg[0] = Seg{0, p.N, D, ldd, col0, 0};
+    return;
+  }
+  p.nseg = nseg;
+  for (int i = 0; i < nseg && i < 4; ++i)
+    p.seg[i] = Seg{segs[i].n_begin, segs[i].n_end, segs[i].ptr, segs[i].ldd, segs[i].col0, 0};
+}
+
+static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
+  static int attr_set = 0;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = 1;
+  }
+  dim3 grid(P->grid_x, P->grid_y);
+  gemm_tc_kernel<<<grid, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, P->p);
+  return check_launch("gemm_tc_kernel");
+}
+
+}  // namespace mosel
+
+using namespace mosel;
+
+static_assert(sizeof(GemmPlan) <= MS_GEMM_PLAN_BYTES, "MS_GEMM_PLAN_BYTES too small");
+
+extern "C" {
+
+int ms_gemm_plan_dense(void* plan, const void* A, int M, int K, long long lda, const void* W, int N, int K_pad,
+                       int BN, const float* bias, int relu, int out_fp32, void* D, long long ldd, int col0,
+                       int nseg, const MsSegment* segs) {
+  if (plan == nullptr || A == nullptr || W == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
+  if (M <= 0 || N <= 0 || K <= 0 || K > K_pad) return set_error(MS_ERR_INVALID, "bad dense GEMM shape");
+  if ((lda * 2) % 16 != 0) return set_error(MS_ERR_INVALID, "lda*2 must be a multiple of 16");
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  memset(P, 0, sizeof(GemmPlan));
+  GemmParams& p = P->p;
+  p.mode = MODE_DENSE;
+  p.M = M;
+  p.N = N;
+  p.bias = bias;
+  p.relu = relu;
+  p.out_fp32 = out_fp32;
+  p.a_bytes = kABytes;
+  set_segments(p, nseg, segs, D, ldd, col0);
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+  cuuint32_t es[2] = {1, 1};
+  int rc = encode_map(&P->tmA, 2, A, dims, strides, box, es);
+  if (rc) return rc;
+  return finish_plan(P, W, K_pad, N, BN, K_pad / kBK, (M + kBM - 1) / kBM);
+}
+
+int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride, int KH,
+                      int KW, int stride, int pad, const void* Wt, int Cout, int BN, const float* bias, int relu,
+                      void* D, long long ldd, int col0, int nseg, const MsSegment* segs, int bn, int bh, int bw) {
+  if (plan == nullptr || X == nullptr || Wt == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
+  if (stride < 1 || stride > 2 || bn * bh * bw > kBM || bn < 1 || bh < 1 || bw < 1)
+    return set_error(MS_ERR_INVALID, "bad conv tile / stride");
+  if ((c_stride * 2) % 16 != 0) return set_error(MS_ERR_INVALID, "channel stride*2 must be a multiple of 16");
+  const int OH = (H + 2 * pad - KH) / stride + 1;
+  const int OW = (W_in + 2 * pad - KW) / stride + 1;
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  memset(P, 0, sizeof(GemmPlan));
+  GemmParams& p = P->p;
+  p.mode = MODE_CONV;
+  p.N = Cout;
+  p.bias = bias;
+  p.relu = relu;
+  p.n_img = n_img;
+  p.OH = OH;
+  p.OW = OW;
+  p.stride = stride;
+  p.pad = pad;
+  p.KW = KW;
+  p.cchunks = (C + kBK - 1) / kBK;
+  p.bn = bn;
+  p.bh = bh;
+  p.bw = bw;
+  p.tiles_w = (OW + bw - 1) / bw;
+  p.tiles_h = (OH + bh - 1) / bh;
+  p.a_bytes = bn * bh * bw * kBK * 2;
+  p.M = n_img * OH * OW;
+  set_segments(p, nseg, segs, D, ldd, col0);
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W_in, (cuuint64_t)H, (cuuint64_t)n_img};
+  cuuint64_t strides[3] = {(cuuint64_t)c_stride * 2, (cuuint64_t)c_stride * 2 * W_in,
+                           (cuuint64_t)c_stride * 2 * W_in * H};
+  cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es);
+  if (rc) return rc;
+  const int num_kb = KH * KW * p.cchunks;
+  const int tiles_n = (n_img + bn - 1) / bn;
+  return finish_plan(P, Wt, num_kb * kBK, Cout, BN, num_kb, tiles_n * p.tiles_h * p.tiles_w);
+}
+
+int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
+                        int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
+                        int out_fp32, void* D, long long ldd, int col0) {
+  if (plan == nullptr || feat == nullptr || inv == nullptr || W == nullptr)
+    return set_error(MS_ERR_INVALID, "null pointer");
+  if (n_mod < 1 || n_mod > 4 || feat_dim % kBK != 0 || M <= 0)
+    return set_error(MS_ERR_INVALID, "gather GEMM needs 1..4 modalities and feat_dim % 64 == 0");
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  memset(P, 0, sizeof(GemmPlan));
+  GemmParams& p = P->p;
+  p.mode = MODE_GATHER;
+  p.M = M;
+  p.N = N;
+  p.bias = bias;
+  p.relu = relu;
+  p.out_fp32 = out_fp32;
+  p.inv = inv;
+  p.inv_ld = inv_ld;
+  p.n_mod = n_mod;
+  p.feat_dim = feat_dim;
+  for (int k = 0; k < n_mod; ++k) p.feat[k] = reinterpret_cast<const __nv_bfloat16*>(feat[k]);
+  for (int k = n_mod; k < 4; ++k) p.feat[k] = p.feat[0];
+  set_segments(p, 0, nullptr, D, ldd, col0);
+  const int K = n_mod * feat_dim;
+  return finish_plan(P, W, K, N, BN, K / kBK, (M + kBM - 1) / kBM);
+}
+
+int ms_gemm_run(const void* plan, void* stream) {
+  if (plan == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  return launch_plan(reinterpret_cast<const GemmPlan*>(plan), reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes) {
+  const GemmPlan* P = reinterpret_cast<const GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  if (grid_x) *grid_x = P->grid_x;
+  if (grid_y) *grid_y = P->grid_y;
+  if (stages) *stages = P->p.stages;
+  if (smem_bytes) *smem_bytes = P->smem_bytes;
+  return MS_OK;
+}
+
+}  // extern "C"

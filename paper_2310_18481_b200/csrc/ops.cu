@@ -1,0 +1,318 @@
+// HBM-bound NHWC ops around the encoder GEMMs (pooling, first-layer im2col,
+// global-pool + segment consensus), the op-program runner that executes a
+// whole encoder forward in one native call, CUDA-event helpers for the
+// profiler, and the error plumbing.
+#include <cstdio>
+#include <cstring>
+
+#include "mosel_b200.h"
+#include "ptx.cuh"
+#include "runtime.h"
+
+namespace mosel {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    char msg[256];
+    snprintf(msg, sizeof msg, "%s: %s", what, cudaGetErrorString(e));
+    return set_error(MS_ERR_CUDA, msg);
+  }
+  return MS_OK;
+}
+
+// ----------------------------------------------------------------- pooling
+// one thread = one output pixel x 8 channels (16-B vectors)
+__global__ void pool2d_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H, int W, int C,
+                              long long xcs, int k, int stride, int pad, int OH, int OW, int is_max,
+                              __nv_bfloat16* __restrict__ Y, long long ycs, int ycol0) {
+  const int cg = C / 8;
+  const long long total = (long long)n_img * OH * OW * cg;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(t % cg);
+    long long pix = t / cg;
+    const int ow = (int)(pix % OW);
+    const int oh = (int)((pix / OW) % OH);
+    const int n = (int)(pix / ((long long)OW * OH));
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = is_max ? -INFINITY : 0.0f;
+    const int h0 = oh * stride - pad, w0 = ow * stride - pad;
+    for (int dy = 0; dy < k; ++dy) {
+      const int h = h0 + dy;
+      if (h < 0 || h >= H) continue;
+      for (int dx = 0; dx < k; ++dx) {
+        const int w = w0 + dx;
+        if (w < 0 || w >= W) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(X + (((long long)n * H + h) * W + w) * xcs + g * 8);
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float f = __bfloat162float(e[j]);
+          acc[j] = is_max ? fmaxf(acc[j], f) : acc[j] + f;
+        }
+      }
+    }
+    const float scale = is_max ? 1.0f : 1.0f / (float)(k * k);
+    uint4 o;
+    o.x = pack_bf16x2(acc[0] * scale, acc[1] * scale);
+    o.y = pack_bf16x2(acc[2] * scale, acc[3] * scale);
+    o.z = pack_bf16x2(acc[4] * scale, acc[5] * scale);
+    o.w = pack_bf16x2(acc[6] * scale, acc[7] * scale);
+    *reinterpret_cast<uint4*>(Y + pix * ycs + ycol0 + g * 8) = o;
+  }
+}
+
+static int pool_out(int in, int k, int stride, int pad, int ceil_mode) {
+  const int span = in + 2 * pad - k;
+  int o = (ceil_mode ? (span + stride - 1) / stride : span / stride) + 1;
+  // a window must start inside the (left-padded) input
+  if (ceil_mode && (o - 1) * stride >= in + pad) --o;
+  return o;
+}
+
+// -------------------------------------------------------------- im2col
+__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H, int W, int C, int KH,
+                              int KW, int stride, int pad, int OH, int OW, __nv_bfloat16* __restrict__ out,
+                              int K_pad) {
+  const long long total = (long long)n_img * OH * OW * K_pad;
+  const int kreal = KH * KW * C;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int kk = (int)(t % K_pad);
+    const long long pix = t / K_pad;
+    __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
+    if (kk < kreal) {
+      const int c = kk % C;
+      const int tap = kk / C;
+      const int kw = tap % KW, kh = tap / KW;
+      const int ow = (int)(pix % OW);
+      const int oh = (int)((pix / OW) % OH);
+      const int n = (int)(pix / ((long long)OW * OH));
+      const int h = oh * stride - pad + kh, w = ow * stride - pad + kw;
+      if (h >= 0 && h < H && w >= 0 && w < W) v = X[(((long long)n * H + h) * W + w) * C + c];
+    }
+    out[t] = v;
+  }
+}
+
+// ----------------------------------------- global pool + segment consensus
+__global__ void segment_mean_kernel(const __nv_bfloat16* __restrict__ X, int n_req, int S, int HW, int C,
+                                    __nv_bfloat16* __restrict__ Y, long long y_ld) {
+  const int cg = C / 8;
+  const long long total = (long long)n_req * cg;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(t % cg);
+    const long long r = t / cg;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long rows = (long long)S * HW;
+    const __nv_bfloat16* base = X + r * rows * C + g * 8;
+    for (long long p = 0; p < rows; ++p) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + p * C);
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(e[j]);
+    }
+    const float s = 1.0f / (float)rows;
+    uint4 o;
+    o.x = pack_bf16x2(acc[0] * s, acc[1] * s);
+    o.y = pack_bf16x2(acc[2] * s, acc[3] * s);
+    o.z = pack_bf16x2(acc[4] * s, acc[5] * s);
+    o.w = pack_bf16x2(acc[6] * s, acc[7] * s);
+    *reinterpret_cast<uint4*>(Y + r * y_ld + g * 8) = o;
+  }
+}
+
+static int grid_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  const long long cap = 148LL * 16;  // 16 resident 256-thread CTAs per SM
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---------------------------------------------------------- op programs
+enum OpKind : int { OP_GEMM = 1, OP_POOL = 2, OP_IM2COL = 3, OP_SEGMEAN = 4 };
+
+struct PoolArgs {
+  const void* X;
+  void* Y;
+  long long xcs, ycs;
+  int n_img, H, W, C, k, stride, pad, ceil_mode, is_max, ycol0;
+};
+struct Im2colArgs {
+  const void* X;
+  void* out;
+  int n_img, H, W, C, KH, KW, stride, pad, K_pad;
+};
+struct SegArgs {
+  const void* X;
+  void* Y;
+  long long y_ld;
+  int n_req, S, HW, C;
+};
+
+struct alignas(64) Op {
+  int kind;
+  int pad_[15];
+  union {
+    unsigned char plan[MS_GEMM_PLAN_BYTES];
+    PoolArgs pool;
+    Im2colArgs im2col;
+    SegArgs seg;
+  } u;
+};
+static_assert(sizeof(Op) <= MS_OP_BYTES, "MS_OP_BYTES too small");
+
+static int run_pool(const PoolArgs& a, cudaStream_t st) {
+  if (a.C % 8 != 0 || a.xcs % 8 != 0 || a.ycs % 8 != 0 || a.ycol0 % 8 != 0)
+    return set_error(MS_ERR_INVALID, "pool2d needs channel counts/strides multiple of 8");
+  const int OH = pool_out(a.H, a.k, a.stride, a.pad, a.ceil_mode);
+  const int OW = pool_out(a.W, a.k, a.stride, a.pad, a.ceil_mode);
+  const long long work = (long long)a.n_img * OH * OW * (a.C / 8);
+  pool2d_kernel<<<grid_for(work, 256), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H, a.W, a.C, a.xcs, a.k, a.stride, a.pad, OH, OW,
+      a.is_max, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0);
+  return check_launch("pool2d_kernel");
+}
+
+static int run_im2col(const Im2colArgs& a, cudaStream_t st) {
+  const int OH = (a.H + 2 * a.pad - a.KH) / a.stride + 1;
+  const int OW = (a.W + 2 * a.pad - a.KW) / a.stride + 1;
+  const long long work = (long long)a.n_img * OH * OW * a.K_pad;
+  im2col_kernel<<<grid_for(work, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H,
+                                                      a.W, a.C, a.KH, a.KW, a.stride, a.pad, OH, OW,
+                                                      reinterpret_cast<__nv_bfloat16*>(a.out), a.K_pad);
+  return check_launch("im2col_kernel");
+}
+
+static int run_segmean(const SegArgs& a, cudaStream_t st) {
+  if (a.C % 8 != 0 || a.y_ld % 8 != 0) return set_error(MS_ERR_INVALID, "segment_mean needs C % 8 == 0");
+  const long long work = (long long)a.n_req * (a.C / 8);
+  segment_mean_kernel<<<grid_for(work, 128), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_req,
+                                                            a.S, a.HW, a.C, reinterpret_cast<__nv_bfloat16*>(a.Y),
+                                                            a.y_ld);
+  return check_launch("segment_mean_kernel");
+}
+
+}  // namespace mosel
+
+using namespace mosel;
+
+extern "C" {
+
+int ms_abi_version(void) { return 1; }
+const char* ms_last_error(void) { return g_err; }
+int ms_device_sync(void) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_error(MS_ERR_CUDA, cudaGetErrorString(e));
+  return MS_OK;
+}
+
+int ms_pool2d(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride, int pad,
+              int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, void* stream) {
+  PoolArgs a{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0};
+  return run_pool(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_im2col(const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride, int pad, void* out,
+              int K_pad, void* stream) {
+  Im2colArgs a{X, out, n_img, H, W, C, KH, KW, stride, pad, K_pad};
+  return run_im2col(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_segment_mean(const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld, void* stream) {
+  SegArgs a{X, Y, y_ld, n_req, S, HW, C};
+  return run_segmean(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_op_gemm(void* op, const void* plan) {
+  if (!op || !plan) return set_error(MS_ERR_INVALID, "null op/plan");
+  Op* o = reinterpret_cast<Op*>(op);
+  memset(o, 0, sizeof(Op));
+  o->kind = OP_GEMM;
+  memcpy(o->u.plan, plan, MS_GEMM_PLAN_BYTES);
+  return MS_OK;
+}
+
+int ms_op_pool2d(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride,
+                 int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  Op* o = reinterpret_cast<Op*>(op);
+  memset(o, 0, sizeof(Op));
+  o->kind = OP_POOL;
+  o->u.pool = PoolArgs{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0};
+  return MS_OK;
+}
+
+int ms_op_im2col(void* op, const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride, int pad,
+                 void* out, int K_pad) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  Op* o = reinterpret_cast<Op*>(op);
+  memset(o, 0, sizeof(Op));
+  o->kind = OP_IM2COL;
+  o->u.im2col = Im2colArgs{X, out, n_img, H, W, C, KH, KW, stride, pad, K_pad};
+  return MS_OK;
+}
+
+int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  Op* o = reinterpret_cast<Op*>(op);
+  memset(o, 0, sizeof(Op));
+  o->kind = OP_SEGMEAN;
+  o->u.seg = SegArgs{X, Y, y_ld, n_req, S, HW, C};
+  return MS_OK;
+}
+
+int ms_program_run(const void* ops, int n_ops, void* stream) {
+  const Op* o = reinterpret_cast<const Op*>(ops);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n_ops; ++i) {
+    int rc = MS_OK;
+    switch (o[i].kind) {
+      case OP_GEMM: rc = ms_gemm_run(o[i].u.plan, stream); break;
+      case OP_POOL: rc = run_pool(o[i].u.pool, st); break;
+      case OP_IM2COL: rc = run_im2col(o[i].u.im2col, st); break;
+      case OP_SEGMEAN: rc = run_segmean(o[i].u.seg, st); break;
+      default: rc = set_error(MS_ERR_INVALID, "unknown op kind");
+    }
+    if (rc != MS_OK) return rc;
+  }
+  return MS_OK;
+}
+
+int ms_event_create(void** ev) {
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return set_error(MS_ERR_CUDA, "cudaEventCreate failed");
+  *ev = reinterpret_cast<void*>(e);
+  return MS_OK;
+}
+int ms_event_destroy(void* ev) {
+  cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+  return MS_OK;
+}
+int ms_event_record(void* ev, void* stream) {
+  if (cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return set_error(MS_ERR_CUDA, "cudaEventRecord failed");
+  return MS_OK;
+}
+int ms_event_elapsed_us(void* start, void* stop, double* us) {
+  float ms = 0.0f;
+  if (cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)) != cudaSuccess ||
+      cudaEventElapsedTime(&ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(stop)) !=
+          cudaSuccess)
+    return set_error(MS_ERR_CUDA, "cudaEventElapsedTime failed");
+  *us = 1000.0 * (double)ms;
+  return MS_OK;
+}
+
+}  // extern "C"

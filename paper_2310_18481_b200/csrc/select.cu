@@ -1,0 +1,246 @@
+// Selection half of the hot path on the device:
+//   * ms_policy_select — the per-job policy step, one warp per
+//     job, bit-exact with apply_policy(OPTIMIZED) on a one-job scope
+//     (reference scheduler.py:382-425).
+//   * ms_compact_index / ms_gather_rows — request compaction: per-request
+//     modality masks -> per-modality stable index lists (warp ballot + popc
+//     prefix sums), inverse maps, a stable counting sort by combo
+//     (strategy.py:54-60 canonical order), and vectorised row gathers into
+//     contiguous modality-grouped sub-batches.
+#include <cstdint>
+
+#include "mosel_b200.h"
+#include "ptx.cuh"
+#include "runtime.h"
+
+namespace mosel {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// est = round-half-even(lat * factor) exactly as Python's round(int * float):
+// the product is one IEEE fp64 multiply (no FMA contraction possible here).
+__device__ __forceinline__ long long estimate_us(long long lat, double factor) {
+  return __double2ll_rn(__dmul_rn((double)lat, factor));
+}
+
+__global__ void policy_select_kernel(const int64_t* __restrict__ lat_us, const int32_t* __restrict__ n_cand, int C,
+                                     const int64_t* __restrict__ deadline_us, long long dispatch_us, double factor,
+                                     int N, int32_t* __restrict__ choice) {
+  const int job = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (job >= N) return;  // warp-uniform
+  const int n = n_cand[job];
+  const long long budget = (long long)deadline_us[job] - dispatch_us;
+  const int64_t* row = lat_us + (long long)job * C;
+  int best = -1;
+  long long est0 = 0, est_top = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < n;
+    const long long e = valid ? estimate_us(row[i], factor) : 0;
+    const unsigned fit = __ballot_sync(kFull, valid && e <= budget);
+    if (fit) best = base + 31 - __clz(fit);
+    if (base == 0) est0 = __shfl_sync(kFull, e, 0);
+    if (n - 1 - base < 32) est_top = __shfl_sync(kFull, e, (n - 1 - base) & 31);
+  }
+  if (lane != 0) return;
+  int out;
+  if (n <= 0) {
+    out = MS_DROP;
+  } else if (est_top <= budget) {
+    out = n - 1;  // no violation: stays at the highest-accuracy candidate
+  } else if (budget <= 0) {
+    out = MS_DROP;  // compute_budget: unsavable
+  } else if ((est0 + 999) / 1000 > budget / 1000) {
+    out = MS_DROP;  // knapsack 1 ms grid: fastest rounds up past floor(B)
+  } else {
+    out = best;  // optimum then try_upgrade: largest est <= B
+  }
+  choice[job] = out;
+}
+
+// ---------------------------------------------------------------- compaction
+constexpr int kCompactThreads = 1024;
+constexpr int kMaxK = 8;
+
+__global__ void __launch_bounds__(kCompactThreads)
+    compact_index_kernel(const uint16_t* __restrict__ mask, int N, int K, int32_t* __restrict__ idx,
+                         int32_t* __restrict__ inv, int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                         int32_t* __restrict__ perm) {
+  __shared__ int s_excl[kMaxK][32];
+  __shared__ int s_tot[kMaxK];
+  __shared__ int s_base[kMaxK];
+  __shared__ int s_hist[1 << kMaxK];
+  __shared__ int s_cursor[1 << kMaxK];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int bins = 1 << K;
+  const unsigned lt = (1u << lane) - 1u;
+
+  if (t < K) s_base[t] = 0;
+  for (int b = t; b < bins; b += kCompactThreads) s_hist[b] = 0;
+  __syncthreads();
+
+  // ---- per-modality stable index lists + combo histogram
+  for (int c0 = 0; c0 < N; c0 += kCompactThreads) {
+    const int i = c0 + t;
+    const int m = (i < N) ? (int)mask[i] : 0;
+    if (i < N) atomicAdd(&s_hist[m & (bins - 1)], 1);
+    unsigned bal[kMaxK];
+    for (int k = 0; k < K; ++k) {
+      bal[k] = __ballot_sync(kFull, i < N && ((m >> k) & 1));
+      if (lane == 0) s_excl[k][warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    if (warp < K) {  // warp k scans the 32 warp totals of modality k
+      const int k = warp;
+      const int v = s_excl[k][lane];
+      int incl = v;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
+      }
+      s_excl[k][lane] = incl - v;
+      if (lane == 31) s_tot[k] = incl;
+    }
+    __syncthreads();
+    if (i < N) {
+      for (int k = 0; k < K; ++k) {
+        if ((m >> k) & 1) {
+          const int pos = s_base[k] + s_excl[k][warp] + __popc(bal[k] & lt);
+          idx[(long long)k * N + pos] = i;
+          inv[(long long)k * N + i] = pos;
+        } else {
+          inv[(long long)k * N + i] = -1;
+        }
+      }
+    }
+    __syncthreads();
+    if (t < K) s_base[t] += s_tot[t];
+    __syncthreads();
+  }
+  if (t < K) counts[t] = s_base[t];
+
+  // ---- exclusive scan of the combo histogram -> offsets (bins <= 256)
+  if (t == 0) {
+    int acc = 0;
+    for (int b = 0; b < bins; ++b) {
+      offsets[b] = acc;
+      s_cursor[b] = acc;
+      acc += s_hist[b];
+    }
+    offsets[bins] = acc;
+  }
+  __syncthreads();
+
+  // ---- stable placement by mask (match_any ranks within the warp)
+  for (int c0 = 0; c0 < N; c0 += kCompactThreads) {
+    const int i = c0 + t;
+    const int m = (i < N) ? (int)mask[i] & (bins - 1) : bins;  // sentinel bin for tail lanes
+    const unsigned peers = __match_any_sync(kFull, m);
+    const int rank = __popc(peers & lt);
+    const int leader = __ffs(peers) - 1;
+    // serialise warps in order so earlier warps claim earlier slots
+    for (int w = 0; w < kCompactThreads / 32; ++w) {
+      if (warp == w && i < N) {
+        int slot_base = 0;
+        if (lane == leader) slot_base = atomicAdd(&s_cursor[m], __popc(peers));
+        slot_base = __shfl_sync(peers, slot_base, leader);
+        perm[slot_base + rank] = i;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// dst[j] = src[slot ? slot[idx[j]] : idx[j]], j < *count; blockIdx.y = row
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_vecs, const int32_t* __restrict__ slot,
+                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
+                                   uint4* __restrict__ dst) {
+  const int n = *count;
+  for (int j = blockIdx.y; j < n; j += gridDim.y) {
+    int r = idx[j];
+    if (slot) r = slot[r];
+    const uint4* s = src + (long long)r * row_vecs;
+    uint4* d = dst + (long long)j * row_vecs;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; v + 3 * step < row_vecs; v += 4 * step) {
+      const uint4 a = __ldcs(s + v), b = __ldcs(s + v + step), c = __ldcs(s + v + 2 * step),
+                  e = __ldcs(s + v + 3 * step);
+      d[v] = a;
+      d[v + step] = b;
+      d[v + 2 * step] = c;
+      d[v + 3 * step] = e;
+    }
+    for (; v < row_vecs; v += step) d[v] = __ldcs(s + v);
+  }
+}
+
+static int gather_launch(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
+                         const int32_t* count, int max_rows, void* dst, cudaStream_t st) {
+  if (row_bytes % 16 != 0) return set_error(MS_ERR_INVALID, "row_bytes must be a multiple of 16");
+  if (max_rows <= 0) return MS_OK;
+  const long long vecs = row_bytes / 16;
+  long long bx = (vecs + 256 * 4 - 1) / (256 * 4);
+  if (bx > 512) bx = 512;
+  if (bx < 1) bx = 1;
+  int gy = max_rows < 65535 ? max_rows : 65535;
+  dim3 grid((unsigned)bx, (unsigned)gy);
+  gather_rows_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), vecs, slot, idx, count,
+                                           reinterpret_cast<uint4*>(dst));
+  return check_launch("gather_rows_kernel");
+}
+
+}  // namespace mosel
+
+using namespace mosel;
+
+extern "C" {
+
+int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t* n_cand, int C,
+                     const int64_t* deadline_us, int64_t dispatch_us, double factor, int N, int32_t* choice,
+                     void* stream) {
+  (void)credit;  // frontier credits are strictly increasing: the argmax is the largest feasible index
+  if (N < 0 || C < 1) return set_error(MS_ERR_INVALID, "policy_select: bad shape");
+  if (N == 0) return MS_OK;
+  if (!lat_us || !n_cand || !deadline_us || !choice) return set_error(MS_ERR_INVALID, "policy_select: null pointer");
+  if (!(factor > 0.0)) return set_error(MS_ERR_INVALID, "policy_select: factor must be positive");
+  const int threads = 256;
+  const long long warps = N;
+  const int blocks = (int)((warps * 32 + threads - 1) / threads);
+  policy_select_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      lat_us, n_cand, C, deadline_us, (long long)dispatch_us, factor, N, choice);
+  return check_launch("policy_select_kernel");
+}
+
+int ms_compact_index(const uint16_t* mask, int N, int K, int32_t* idx, int32_t* inv, int32_t* counts,
+                     int32_t* combo_offsets, int32_t* perm, void* stream) {
+  if (K < 1 || K > kMaxK) return set_error(MS_ERR_INVALID, "compact: K must be in 1..8");
+  if (N < 0) return set_error(MS_ERR_INVALID, "compact: N must be >= 0");
+  if (!mask && N > 0) return set_error(MS_ERR_INVALID, "compact: null mask");
+  compact_index_kernel<<<1, kCompactThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(mask, N, K, idx, inv,
+                                                                                         counts, combo_offsets, perm);
+  return check_launch("compact_index_kernel");
+}
+
+int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
+                   const int32_t* count, int max_rows, void* dst, void* stream) {
+  if (!src || !idx || !count || !dst) return set_error(MS_ERR_INVALID, "gather_rows: null pointer");
+  return gather_launch(src, row_bytes, slot, idx, count, max_rows, dst, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_bytes,
+               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
+               int32_t* combo_offsets, int32_t* perm, void* stream) {
+  int rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
+  if (rc) return rc;
+  for (int k = 0; k < K; ++k) {
+    if (X == nullptr || G == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
+    rc = gather_launch(X[k], row_bytes[k], slot, idx + (long long)k * N, counts + k, N, G[k],
+                       reinterpret_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+  }
+  return MS_OK;
+}
+
+}  // extern "C"

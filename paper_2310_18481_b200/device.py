@@ -1,0 +1,316 @@
+"""ctypes binding of the C-ABI library ``libmosel_b200.so``.
+
+This is the same binding a maintainer of the reference would add (see
+INTEGRATION.md): plain pointers and sizes, a ``cudaStream_t`` per call, an
+``int`` status mapped to ``ValueError`` subclasses.  PyTorch provides device
+memory and the current stream only.  There is no fallback: if the library
+or a CUDA device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libmosel_b200.so"
+GEMM_PLAN_BYTES = 1024
+OP_BYTES = 1152
+DROP = -1
+
+_lib = None
+
+
+class DeviceError(ValueError):
+    """A C-ABI call returned a nonzero status."""
+
+
+class Segment(C.Structure):
+    _fields_ = [("n_begin", C.c_int), ("n_end", C.c_int), ("ptr", C.c_void_p),
+                ("ldd", C.c_longlong), ("col0", C.c_int), ("pad_", C.c_int)]
+
+
+_P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
+_SIGS = {
+    "ms_abi_version": ([], C.c_int),
+    "ms_last_error": ([], C.c_char_p),
+    "ms_device_sync": ([], C.c_int),
+    "ms_policy_select": ([_P, _P, _P, _I, _P, C.c_int64, _D, _I, _P, _P], C.c_int),
+    "ms_compact_index": ([_P, _I, _I, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_gather_rows": ([_P, _LL, _P, _P, _P, _I, _P, _P], C.c_int),
+    "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_gemm_plan_dense": ([_P, _P, _I, _I, _LL, _P, _I, _I, _I, _P, _I, _I, _P, _LL, _I, _I, _P],
+                           C.c_int),
+    "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
+                           _I, _I, _P, _I, _I, _I], C.c_int),
+    "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
+                            C.c_int),
+    "ms_gemm_run": ([_P, _P], C.c_int),
+    "ms_gemm_plan_info": ([_P, _P, _P, _P, _P], C.c_int),
+    "ms_pool2d": ([_P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P], C.c_int),
+    "ms_im2col": ([_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P], C.c_int),
+    "ms_segment_mean": ([_P, _I, _I, _I, _I, _P, _LL, _P], C.c_int),
+    "ms_op_gemm": ([_P, _P], C.c_int),
+    "ms_op_pool2d": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I], C.c_int),
+    "ms_op_im2col": ([_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I], C.c_int),
+    "ms_op_segment_mean": ([_P, _P, _I, _I, _I, _I, _P, _LL], C.c_int),
+    "ms_program_run": ([_P, _I, _P], C.c_int),
+    "ms_event_create": ([_P], C.c_int),
+    "ms_event_destroy": ([_P], C.c_int),
+    "ms_event_record": ([_P, _P], C.c_int),
+    "ms_event_elapsed_us": ([_P, _P, _P], C.c_int),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def lib():
+    """Load (once) and return the library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2310_18481_b200.build`")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(h, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = h
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().ms_last_error().decode(errors="replace")
+        raise DeviceError(f"{what}: {msg} (status {rc})")
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 hot path needs a CUDA device; there is no CPU fallback")
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    return t.data_ptr()
+
+
+def sync() -> None:
+    check(lib().ms_device_sync(), "ms_device_sync")
+
+
+# ------------------------------------------------------------------ policy
+
+
+def policy_select(lat_us, credit, n_cand, deadline_us, dispatch_us: int, factor: float,
+                  device=None, out=None, stream=None):
+    """Device P5 over an SoA table. Accepts numpy or torch inputs; returns a
+    numpy int32 array (or fills the CUDA tensor ``out`` without syncing)."""
+    torch = _torch()
+    dev = device or torch.device("cuda")
+
+    def as_dev(a, dt):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=dev, dtype=dt).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+
+    lat = as_dev(lat_us, torch.int64)
+    n = lat.shape[0]
+    cand = as_dev(n_cand, torch.int32)
+    dl = as_dev(deadline_us, torch.int64)
+    cr = as_dev(credit, torch.int32) if credit is not None else None
+    res = out if out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+    check(lib().ms_policy_select(ptr(lat), ptr(cr), ptr(cand), int(lat.shape[1]), ptr(dl),
+                                 int(dispatch_us), float(factor), int(n), ptr(res),
+                                 stream_ptr(stream)), "ms_policy_select")
+    if out is not None:
+        return out
+    return res.cpu().numpy()
+
+
+# -------------------------------------------------------------- compaction
+
+
+def compact_index(mask, n_modalities: int, stream=None):
+    """Device G1/G2 index build. ``mask`` is a CUDA uint16/int tensor [N].
+    Returns (idx[K,N], inv[K,N], counts[K], combo_offsets[2^K+1], perm[N])."""
+    torch = _torch()
+    m = mask.to(torch.int16).contiguous() if mask.dtype != torch.int16 else mask.contiguous()
+    n = m.shape[0]
+    k = n_modalities
+    dev = m.device
+    idx = torch.full((k, max(n, 1)), -1, dtype=torch.int32, device=dev)
+    inv = torch.empty((k, max(n, 1)), dtype=torch.int32, device=dev)
+    counts = torch.empty(k, dtype=torch.int32, device=dev)
+    offs = torch.empty((1 << k) + 1, dtype=torch.int32, device=dev)
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    check(lib().ms_compact_index(ptr(m), n, k, ptr(idx), ptr(inv), ptr(counts), ptr(offs),
+                                 ptr(perm), stream_ptr(stream)), "ms_compact_index")
+    return idx[:, :n], inv[:, :n], counts, offs, perm[:n]
+
+
+def gather_rows(src, idx, count, max_rows: int, dst, slot=None, stream=None):
+    row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+    check(lib().ms_gather_rows(ptr(src), row_bytes, ptr(slot), ptr(idx), ptr(count), int(max_rows),
+                               ptr(dst), stream_ptr(stream)), "ms_gather_rows")
+    return dst
+
+
+# ------------------------------------------------------------------ GEMMs
+
+
+class GemmPlan:
+    """An opaque 64-byte-aligned plan blob plus the tensors it points at
+    (kept alive for the plan's lifetime)."""
+
+    def __init__(self):
+        self._raw = C.create_string_buffer(GEMM_PLAN_BYTES + 64)
+        addr = C.addressof(self._raw)
+        self.addr = (addr + 63) & ~63
+        self.keep = []
+
+    def run(self, stream=None):
+        check(lib().ms_gemm_run(self.addr, stream_ptr(stream)), "ms_gemm_run")
+
+    def info(self):
+        vals = [C.c_int() for _ in range(4)]
+        check(lib().ms_gemm_plan_info(self.addr, *[C.byref(v) for v in vals]), "ms_gemm_plan_info")
+        return {k: v.value for k, v in zip(("grid_x", "grid_y", "stages", "smem_bytes"), vals)}
+
+
+def _segments(segs):
+    if not segs:
+        return 0, None
+    arr = (Segment * len(segs))()
+    for i, (nb, ne, t, ldd, col0) in enumerate(segs):
+        arr[i] = Segment(nb, ne, ptr(t), ldd, col0, 0)
+    return len(segs), arr
+
+
+def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col0=0, ldd=None,
+               segs=None, M=None):
+    """D = act(A[M,K] @ W[N,K_pad]^T + bias); A row stride = A.stride(0)."""
+    p = GemmPlan()
+    m = A.shape[0] if M is None else M
+    k = A.shape[1] if K is None else K
+    nseg, sarr = _segments(segs)
+    check(lib().ms_gemm_plan_dense(p.addr, ptr(A), m, k, A.stride(0), ptr(W), W.shape[0], W.shape[1],
+                                   BN, ptr(bias), int(relu), int(out_fp32), ptr(D),
+                                   D.stride(0) if ldd is None else ldd, col0, nseg, sarr),
+          "ms_gemm_plan_dense")
+    p.keep = [A, W, bias, D, segs]
+    return p
+
+
+def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, bias, D, *, ldd,
+              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16)):
+    p = GemmPlan()
+    nseg, sarr = _segments(segs)
+    bn, bh, bw = tile
+    check(lib().ms_gemm_plan_conv(p.addr, ptr(X), n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad,
+                                  ptr(Wt), Cout, BN, ptr(bias), int(relu), ptr(D), ldd, col0, nseg,
+                                  sarr, bn, bh, bw), "ms_gemm_plan_conv")
+    p.keep = [X, Wt, bias, D, segs]
+    return p
+
+
+def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_fp32=False):
+    p = GemmPlan()
+    arr = (C.c_void_p * len(feats))(*[ptr(f) for f in feats])
+    check(lib().ms_gemm_plan_gather(p.addr, arr, ptr(inv), inv.stride(0), len(feats), feat_dim, M,
+                                    ptr(W), W.shape[0], BN, ptr(bias), int(relu), int(out_fp32),
+                                    ptr(D), D.stride(0), 0), "ms_gemm_plan_gather")
+    p.keep = [feats, inv, W, bias, D, arr]
+    return p
+
+
+# -------------------------------------------------------------- op programs
+
+
+class Program:
+    """A native op list (ms_program_run): one call runs a whole encoder."""
+
+    def __init__(self):
+        self.ops = []  # (kind, args)
+        self.keep = []
+        self._buf = None
+        self._addr = 0
+
+    def gemm(self, plan: GemmPlan):
+        self.ops.append(("gemm", plan))
+        self.keep.append(plan)
+
+    def pool(self, X, n_img, H, W, C_, x_cs, k, stride, pad, ceil_mode, is_max, Y, y_cs, y_col0):
+        self.ops.append(("pool", (ptr(X), n_img, H, W, C_, x_cs, k, stride, pad, int(ceil_mode),
+                                  int(is_max), ptr(Y), y_cs, y_col0)))
+        self.keep += [X, Y]
+
+    def im2col(self, X, n_img, H, W, C_, KH, KW, stride, pad, out, K_pad):
+        self.ops.append(("im2col", (ptr(X), n_img, H, W, C_, KH, KW, stride, pad, ptr(out), K_pad)))
+        self.keep += [X, out]
+
+    def segment_mean(self, X, n_req, S, HW, C_, Y, y_ld):
+        self.ops.append(("segmean", (ptr(X), n_req, S, HW, C_, ptr(Y), y_ld)))
+        self.keep += [X, Y]
+
+    def seal(self):
+        n = len(self.ops)
+        self._buf = C.create_string_buffer(OP_BYTES * max(n, 1) + 64)
+        self._addr = (C.addressof(self._buf) + 63) & ~63
+        L = lib()
+        for i, (kind, a) in enumerate(self.ops):
+            at = self._addr + i * OP_BYTES
+            if kind == "gemm":
+                check(L.ms_op_gemm(at, a.addr), "ms_op_gemm")
+            elif kind == "pool":
+                check(L.ms_op_pool2d(at, *a), "ms_op_pool2d")
+            elif kind == "im2col":
+                check(L.ms_op_im2col(at, *a), "ms_op_im2col")
+            else:
+                check(L.ms_op_segment_mean(at, *a), "ms_op_segment_mean")
+        return self
+
+    def run(self, stream=None):
+        if self._buf is None:
+            self.seal()
+        check(lib().ms_program_run(self._addr, len(self.ops), stream_ptr(stream)), "ms_program_run")
+
+    @property
+    def n_launches(self) -> int:
+        return len(self.ops)
+
+
+# ------------------------------------------------------------------ events
+
+
+class Event:
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib().ms_event_create(C.byref(h)), "ms_event_create")
+        self.h = h
+
+    def record(self, stream=None):
+        check(lib().ms_event_record(self.h, stream_ptr(stream)), "ms_event_record")
+
+    def elapsed_us(self, end: "Event") -> float:
+        out = C.c_double()
+        check(lib().ms_event_elapsed_us(self.h, end.h, C.byref(out)), "ms_event_elapsed_us")
+        return out.value
+
+    def __del__(self):
+        try:
+            if _lib is not None and self.h:
+                _lib.ms_event_destroy(self.h)
+        except Exception:
+            pass

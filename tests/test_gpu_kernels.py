@@ -1,0 +1,249 @@
+"""Kernel-level parity on the B200, through the C-ABI library.
+
+Integer work (policy, compaction, gathers) is bit-exact against the oracle
+and the reference golden vectors; tensor-core work is compared with a plain
+PyTorch fp32 reference of the same op on the same bf16 inputs.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import selection as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2310_18481_b200 import build, device
+    build.build()
+    device.lib()
+    return device
+
+
+def test_policy_select_bit_exact_vs_reference_golden(dev):
+    cases = json.loads((GOLDEN / "policy_cases.json").read_text())
+    # group by (dispatch, factor) so each launch has one scalar pair
+    groups = {}
+    for c in cases:
+        groups.setdefault((c["dispatch_us"], c["factor"]), []).append(c)
+    mismatches = 0
+    for (dispatch, factor), cs in groups.items():
+        width = max(len(c["lat_us"]) for c in cs)
+        lat = np.zeros((len(cs), width), dtype=np.int64)
+        cr = np.zeros((len(cs), width), dtype=np.int32)
+        for i, c in enumerate(cs):
+            lat[i, : len(c["lat_us"])] = c["lat_us"]
+            cr[i, : len(c["credit"])] = c["credit"]
+        ncand = np.array([len(c["lat_us"]) for c in cs], dtype=np.int32)
+        dl = np.array([c["deadline_us"] for c in cs], dtype=np.int64)
+        got = dev.policy_select(lat, cr, ncand, dl, dispatch, factor)
+        exp = np.array([c["expected"] for c in cs], dtype=np.int32)
+        mismatches += int((got != exp).sum())
+    assert mismatches == 0, f"{mismatches} of {len(cases)} policy choices differ from the reference"
+
+
+def test_policy_select_batched_random_vs_oracle(dev):
+    rng = np.random.default_rng(3)
+    n, width = 4096, 40  # > 32 candidates exercises the multi-round warp path
+    lat = np.sort(rng.integers(1_000, 400_000, size=(n, width)), axis=1).astype(np.int64)
+    lat += np.arange(width)  # strictly increasing
+    ncand = rng.integers(0, width + 1, size=n).astype(np.int32)
+    dl = rng.integers(-5_000, 500_000, size=n).astype(np.int64)
+    for factor in (0.5, 1.0, 1.37, 2.5):
+        got = dev.policy_select(lat, None, ncand, dl, 0, factor)
+        exp = orc.policy_select(lat, ncand, dl, 0, factor)
+        assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("n,k", [(0, 3), (1, 1), (7, 2), (256, 3), (1000, 4), (1025, 3), (3000, 4), (517, 8)])
+def test_compact_index_bit_exact(dev, n, k):
+    rng = np.random.default_rng(n * 31 + k)
+    masks = rng.integers(1, 1 << k, size=n).astype(np.int64)
+    m_dev = torch.as_tensor(masks.astype(np.int16)).cuda()
+    idx, inv, counts, offs, perm = dev.compact_index(m_dev, k)
+    e_idx, e_inv, e_counts = orc.compact(masks, k)
+    assert counts.cpu().numpy().tolist() == e_counts.tolist()
+    for kk in range(k):
+        c = int(e_counts[kk])
+        assert np.array_equal(idx[kk, :c].cpu().numpy(), e_idx[kk])
+        assert np.array_equal(inv[kk].cpu().numpy(), e_inv[kk])
+    e_perm, e_offs, _ = orc.group_free_masks(masks if n else np.zeros(0, np.int64), 4)
+    if n:
+        bins = 1 << k
+        ref_perm = np.argsort(masks, kind="stable")
+        ref_offs = np.concatenate([[0], np.cumsum(np.bincount(masks, minlength=bins))])
+        assert np.array_equal(perm.cpu().numpy(), ref_perm)
+        assert np.array_equal(offs.cpu().numpy(), ref_offs)
+
+
+def test_gather_rows_with_slots(dev):
+    rng = np.random.default_rng(0)
+    pool = torch.randn(50, 3, 40, dtype=torch.float32, device="cuda").to(torch.bfloat16)
+    idx = torch.tensor([3, 1, 4, 1, 5], dtype=torch.int32, device="cuda")
+    slot = torch.as_tensor(rng.permutation(50).astype(np.int32)).cuda()
+    count = torch.tensor([4], dtype=torch.int32, device="cuda")
+    dst = torch.zeros(5, 3, 40, dtype=torch.bfloat16, device="cuda")
+    dev.gather_rows(pool, idx, count, 5, dst, slot=slot)
+    torch.cuda.synchronize()
+    exp = pool[slot[idx[:4].long()].long()]
+    assert torch.equal(dst[:4], exp)
+    assert torch.equal(dst[4], torch.zeros_like(dst[4]))
+
+
+def _bf(t):
+    return t.to(torch.bfloat16)
+
+
+def _close(got, ref, tol=2e-2):
+    err = (got.float() - ref.float()).abs().max().item()
+    scale = ref.float().abs().max().item() + 1e-6
+    return err <= tol * scale, err, scale
+
+
+@pytest.mark.parametrize("M,K,N,BN,relu", [
+    (128, 64, 64, 64, False), (1, 64, 32, 32, False), (300, 192, 96, 96, True),
+    (1000, 1024, 256, 256, True), (517, 576, 352, 192, True), (64, 3072, 512, 128, True),
+])
+def test_gemm_dense_vs_torch(dev, M, K, N, BN, relu):
+    g = torch.Generator(device="cpu").manual_seed(M + K + N)
+    A = _bf(torch.randn(M, K, generator=g)).cuda()
+    Kp = (K + 63) // 64 * 64
+    W = torch.zeros(N, Kp, dtype=torch.bfloat16)
+    W[:, :K] = _bf(torch.randn(N, K, generator=g) * 0.05)
+    W = W.cuda()
+    b = (torch.randn(N, generator=g) * 0.1).cuda()
+    D = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_dense(A, W, b, D, BN=BN, relu=relu)
+    p.run()
+    torch.cuda.synchronize()
+    ref = A.float().cpu() @ W[:, :K].float().cpu().T + b.cpu()
+    if relu:
+        ref = ref.clamp_min(0)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
+def test_gemm_dense_fp32_out_and_segments(dev):
+    g = torch.Generator().manual_seed(7)
+    M, K = 200, 256
+    A = _bf(torch.randn(M, K, generator=g)).cuda()
+    W = _bf(torch.randn(160, K, generator=g) * 0.05).cuda()
+    D1 = torch.zeros(M, 96, dtype=torch.bfloat16, device="cuda")
+    D2 = torch.zeros(M, 200, dtype=torch.bfloat16, device="cuda")
+    segs = [(0, 64, D1, 96, 32), (64, 160, D2, 200, 104)]
+    p = dev.plan_dense(A, W, None, D1, BN=160, segs=segs)
+    p.run()
+    L = torch.zeros(M, 397, dtype=torch.float32, device="cuda")
+    W2 = _bf(torch.randn(397, K, generator=g) * 0.05).cuda()
+    dev.plan_dense(A, W2, None, L, BN=128, out_fp32=True).run()
+    torch.cuda.synchronize()
+    ref = A.float().cpu() @ W.float().cpu().T
+    assert _close(D1[:, 32:96].cpu(), ref[:, :64])[0]
+    assert _close(D2[:, 104:200].cpu(), ref[:, 64:160])[0]
+    assert torch.count_nonzero(D1[:, :32]) == 0
+    ref2 = A.float().cpu() @ W2.float().cpu().T
+    assert _close(L.cpu(), ref2, tol=1e-3)[0]
+
+
+def _conv_weights(Cout, Cin, k, g):
+    w = _bf(torch.randn(Cout, Cin, k, k, generator=g) * (2.0 / (Cin * k * k)) ** 0.5)
+    cc = (Cin + 63) // 64
+    packed = torch.zeros(Cout, k * k, cc * 64, dtype=torch.bfloat16)
+    packed[:, :, :Cin] = w.permute(0, 2, 3, 1).reshape(Cout, k * k, Cin)
+    return w, packed.reshape(Cout, -1).contiguous()
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout,k,s,pad,tile,BN", [
+    (2, 14, 64, 96, 3, 1, 1, (1, 7, 14), 96),
+    (3, 28, 96, 96, 3, 2, 1, (1, 7, 14), 96),
+    (5, 7, 160, 224, 3, 1, 1, (2, 7, 7), 224),
+    (4, 56, 64, 192, 3, 1, 1, (1, 8, 16), 192),
+    (2, 8, 192, 320, 3, 1, 1, (2, 8, 8), 160),
+    (2, 28, 320, 160, 3, 2, 1, (1, 7, 14), 160),
+])
+def test_conv_implicit_gemm_vs_torch(dev, n, H, Cin, Cout, k, s, pad, tile, BN):
+    g = torch.Generator().manual_seed(n * H + Cin)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, k, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    OH = (H + 2 * pad - k) // s + 1
+    D = torch.zeros(n * OH * OH, Cout, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, k, k, s, pad, packed.cuda(), Cout, b.cuda(), D, ldd=Cout,
+                      BN=BN, relu=True, tile=tile)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=s, padding=pad).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
+def test_gather_concat_gemm_vs_torch(dev):
+    g = torch.Generator().manual_seed(11)
+    N, F, K = 300, 1024, 3
+    masks = torch.randint(1, 8, (N,), generator=g)
+    feats, invs = [], []
+    full = torch.zeros(N, K * F)
+    for k in range(K):
+        have = ((masks >> k) & 1).bool()
+        nk = int(have.sum())
+        f = _bf(torch.randn(nk, F, generator=g))
+        inv = torch.full((N,), -1, dtype=torch.int32)
+        inv[have] = torch.arange(nk, dtype=torch.int32)
+        full[have, k * F:(k + 1) * F] = f.float()
+        feats.append(f.cuda())
+        invs.append(inv)
+    inv = torch.stack(invs).cuda()
+    W = _bf(torch.randn(512, K * F, generator=g) * 0.02)
+    b = torch.randn(512, generator=g) * 0.1
+    H = torch.zeros(N, 512, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_gather(feats, inv, W.cuda(), b.cuda(), H, M=N, feat_dim=F, BN=256, relu=True)
+    p.run()
+    torch.cuda.synchronize()
+    ref = (full @ W.float().T + b).clamp_min(0)
+    ok, err, scale = _close(H.cpu(), ref)
+    assert ok, (err, scale)
+
+
+def test_pool_im2col_segment_mean(dev):
+    L = dev.lib()
+    g = torch.Generator().manual_seed(5)
+    x = _bf(torch.randn(3, 64, 28, 28, generator=g))
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    # max 3x3 s2 ceil -> 14x14 written into a 96-wide concat slice at col 32
+    Y = torch.zeros(3 * 14 * 14, 96, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_pool2d(dev.ptr(X), 3, 28, 28, 64, 64, 3, 2, 0, 1, 1, dev.ptr(Y), 96, 32, dev.stream_ptr()), "pool")
+    ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 0, ceil_mode=True).permute(0, 2, 3, 1).reshape(-1, 64)
+    torch.cuda.synchronize()
+    assert torch.equal(Y[:, 32:].cpu().float(), ref)
+    # avg 3x3 s1 p1 (count_include_pad)
+    Z = torch.zeros(3 * 28 * 28, 64, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_pool2d(dev.ptr(X), 3, 28, 28, 64, 64, 3, 1, 1, 0, 0, dev.ptr(Z), 64, 0, dev.stream_ptr()), "pool")
+    ref = torch.nn.functional.avg_pool2d(x.float(), 3, 1, 1).permute(0, 2, 3, 1).reshape(-1, 64)
+    torch.cuda.synchronize()
+    assert _close(Z.cpu(), ref, tol=1e-2)[0]
+    # im2col of a 3-channel 7x7/2 conv
+    xi = _bf(torch.randn(2, 3, 32, 32, generator=g))
+    Xi = xi.permute(0, 2, 3, 1).contiguous().cuda()
+    out = torch.zeros(2 * 16 * 16, 192, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_im2col(dev.ptr(Xi), 2, 32, 32, 3, 7, 7, 2, 3, dev.ptr(out), 192, dev.stream_ptr()), "im2col")
+    cols = torch.nn.functional.unfold(xi.float(), 7, padding=3, stride=2)  # [n, C*49, L] (c, kh, kw)
+    cols = cols.reshape(2, 3, 49, 256).permute(0, 3, 2, 1).reshape(2 * 256, 147)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :147].cpu().float(), cols)
+    assert torch.count_nonzero(out[:, 147:]) == 0
+    # segment mean
+    f = _bf(torch.randn(4 * 3 * 49, 64, generator=g)).cuda()
+    y = torch.zeros(4, 64, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_segment_mean(dev.ptr(f), 4, 3, 49, 64, dev.ptr(y), 64, dev.stream_ptr()), "segmean")
+    torch.cuda.synchronize()
+    ref = f.float().cpu().reshape(4, 147, 64).mean(1)
+    assert _close(y.cpu(), ref, tol=1e-2)[0]
