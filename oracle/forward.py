@@ -1,0 +1,142 @@
+"""ORACLE — CPU restatement of the forward half of the hot path.
+
+TEST INFRASTRUCTURE ONLY (see oracle/selection.py for the rule).
+
+The reference runs no model: a part's cost is ``profile.part_latency_us``
+(sim.py:372-377) and its accuracy a per-combo constant (profile.py:170-174);
+the only thing it pins is WHICH modalities a request uses (its assigned
+part's mask; dropped set = all_mask & ~mask, profile.py:157-159).  Logits
+are therefore "parity unpinned" by the reference.  This module
+is the frozen restatement they are checked against:
+
+* plain ``torch.nn.functional`` in fp32 on the CPU, NCHW layout — an
+  independent formulation of the same network, not the device's
+  implicit-GEMM/NHWC code path;
+* the device stores every activation in bf16, so the oracle rounds to bf16
+  at exactly those points (conv+ReLU outputs, pool outputs, the segment
+  consensus features, the fusion hidden layer) and nowhere else;
+* weights come from the model definition's seeded generators
+  (``encoders.*_weights``), i.e. the same numbers, not the same code path.
+
+Missing-modality rule (builder contract): a request's absent
+modality contributes a zero block to the concat, i.e. its FC1 columns are
+skipped.  Tolerance (north_star): rtol 2e-2 and >= 99.9 % top-1 agreement.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from paper_2310_18481_b200.encoders import (FEAT_DIM, bninception_layers, bninception_weights,
+                                            fusion_weights, mlp_weights)
+
+
+def _bf(x):
+    return x.to(torch.bfloat16).float()
+
+
+def _conv(x, wb, s, p):
+    w, b = wb
+    return _bf(F.relu(F.conv2d(x, w.float(), b, stride=s, padding=p)))
+
+
+def bninception_forward(frames, weights, cin: int, size: int):
+    """frames: float tensor [n, cin, H, W] (bf16-representable values).
+    Returns per-frame features after global average pooling, fp32 [n, 1024]
+    (not yet rounded)."""
+    x = frames.float()
+    for L in bninception_layers(cin, size):
+        k = L["kind"]
+        if k == "conv":
+            x = _conv(x, weights[L["name"]], L["s"], L["p"])
+        elif k == "pool":
+            x = F.max_pool2d(x, L["k"], L["s"], L["p"], ceil_mode=L["ceil"])
+        elif k == "block":
+            n, s = L["name"], L["s"]
+            outs = []
+            if L["c1"]:
+                outs.append(_conv(x, weights[n + "/1x1"], 1, 0))
+            t = _conv(x, weights[n + "/3x3_reduce"], 1, 0)
+            outs.append(_conv(t, weights[n + "/3x3"], s, 1))
+            t = _conv(x, weights[n + "/d3x3_reduce"], 1, 0)
+            t = _conv(t, weights[n + "/d3x3_a"], 1, 1)
+            outs.append(_conv(t, weights[n + "/d3x3_b"], s, 1))
+            if L["pool"] == "avg":
+                pooled = _bf(F.avg_pool2d(x, 3, 1, 1, count_include_pad=True))
+                outs.append(_conv(pooled, weights[n + "/pool_proj"], 1, 0))
+            elif L["pool"] == "maxproj":
+                pooled = F.max_pool2d(x, 3, 1, 1)
+                outs.append(_conv(pooled, weights[n + "/pool_proj"], 1, 0))
+            else:
+                outs.append(F.max_pool2d(x, 3, 2, 0, ceil_mode=True))
+            x = torch.cat(outs, 1)
+    return x
+
+
+def encode_requests(clips, weights, cin: int, size: int, segments: int):
+    """clips: [n_req, S, H, W, C] NHWC (as stored on the device) ->
+    bf16-rounded TSN consensus features [n_req, 1024]."""
+    n = clips.shape[0]
+    frames = clips.reshape(n * segments, size, size, cin).permute(0, 3, 1, 2)
+    f = bninception_forward(frames, weights, cin, size)  # [n*S, 1024, h, w]
+    f = f.reshape(n, segments, f.shape[1], -1).mean(dim=(1, 3))
+    return _bf(f)
+
+
+def mlp_forward(x, layers):
+    h = x.float()
+    for w, b in layers:
+        h = _bf(F.relu(h @ w.float().T + b))
+    return h
+
+
+def fusion_forward(feats, masks, weights):
+    """feats: list over modalities of [n_req, F] features for EVERY request
+    (rows of absent modalities ignored); masks: int [n_req]."""
+    w1, b1, w2, b2 = weights
+    n = masks.shape[0]
+    cols = []
+    for k, f in enumerate(feats):
+        present = ((masks >> k) & 1).bool().reshape(n, 1)
+        cols.append(torch.where(present, f.float(), torch.zeros_like(f.float())))
+    z = torch.cat(cols, 1)
+    h = _bf(F.relu(z @ w1.float().T + b1))
+    return h @ w2.float().T + b2
+
+
+class OracleTBN:
+    """Whole TBN-shaped model on the CPU: per-modality BN-Inception +
+    segment consensus + masked fusion head."""
+
+    def __init__(self, modalities, seeds, fusion_seed: int, segments: int):
+        self.mods = modalities
+        self.S = segments
+        self.enc_w = [bninception_weights(m.channels, m.size, s) for m, s in zip(modalities, seeds)]
+        self.fus_w = fusion_weights(len(modalities), FEAT_DIM, fusion_seed)
+
+    def logits(self, clips_per_mod, masks):
+        """clips_per_mod[k]: [n_req, S, H, W, C] for every request (absent
+        modalities are not encoded)."""
+        n = masks.shape[0]
+        feats = []
+        for k, m in enumerate(self.mods):
+            f = torch.zeros(n, FEAT_DIM)
+            sel = torch.nonzero((masks >> k) & 1).flatten()
+            if sel.numel():
+                f[sel] = encode_requests(clips_per_mod[k][sel], self.enc_w[k], m.channels, m.size,
+                                         self.S)
+            feats.append(f)
+        return fusion_forward(feats, masks, self.fus_w)
+
+
+class OracleMLP:
+    """configs[0]: per-modality MLP towers + masked fusion head."""
+
+    def __init__(self, in_dims, seeds, fusion_seed: int, hidden=(1024, 1024)):
+        self.towers = [mlp_weights((d,) + tuple(hidden), s) for d, s in zip(in_dims, seeds)]
+        self.fus_w = fusion_weights(len(in_dims), hidden[-1], fusion_seed)
+
+    def logits(self, inputs, masks):
+        feats = [mlp_forward(x, t) for x, t in zip(inputs, self.towers)]
+        return fusion_forward(feats, masks, self.fus_w)

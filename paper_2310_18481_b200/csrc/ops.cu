@@ -171,7 +171,7 @@ struct alignas(64) Op {
     SegArgs seg;
   } u;
 };
-static_assert(sizeof(Op) <= MS_OP_BYTES, "MS_OP_BYTES too small");
+static_assert(sizeof(Op) <= MS_OP_BYTES && MS_OP_BYTES % 64 == 0, "MS_OP_BYTES too small / misaligned");
 
 static int run_pool(const PoolArgs& a, cudaStream_t st) {
   if (a.C % 8 != 0 || a.xcs % 8 != 0 || a.ycs % 8 != 0 || a.ycol0 % 8 != 0)
@@ -274,15 +274,17 @@ int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C,
 }
 
 int ms_program_run(const void* ops, int n_ops, void* stream) {
-  const Op* o = reinterpret_cast<const Op*>(ops);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(ops);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_ops; ++i) {
+    // ops are laid out MS_OP_BYTES apart (the ABI stride), not sizeof(Op)
+    const Op& o = *reinterpret_cast<const Op*>(base + (size_t)i * MS_OP_BYTES);
     int rc = MS_OK;
-    switch (o[i].kind) {
-      case OP_GEMM: rc = ms_gemm_run(o[i].u.plan, stream); break;
-      case OP_POOL: rc = run_pool(o[i].u.pool, st); break;
-      case OP_IM2COL: rc = run_im2col(o[i].u.im2col, st); break;
-      case OP_SEGMEAN: rc = run_segmean(o[i].u.seg, st); break;
+    switch (o.kind) {
+      case OP_GEMM: rc = ms_gemm_run(o.u.plan, stream); break;
+      case OP_POOL: rc = run_pool(o.u.pool, st); break;
+      case OP_IM2COL: rc = run_im2col(o.u.im2col, st); break;
+      case OP_SEGMEAN: rc = run_segmean(o.u.seg, st); break;
       default: rc = set_error(MS_ERR_INVALID, "unknown op kind");
     }
     if (rc != MS_OK) return rc;

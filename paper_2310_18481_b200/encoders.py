@@ -1,0 +1,495 @@
+"""Per-modality encoders and the late-fusion head, as native op programs.
+
+The reference has no model at all: a part's cost is a table lookup
+(sim.py:372-377, profile.py:164-168) and its accuracy a per-combo constant
+(profile.py:170-174).  These are the random-init encoders the north_star
+names; their numerics are pinned by the frozen
+CPU restatement in ``oracle/forward.py`` ("parity unpinned" by the
+reference).
+
+* ``TBN_BNINCEPTION``: TSN/TBN-style BN-Inception (69 convolutions, 1024-d
+  output; BatchNorm folded into conv bias as at inference) applied to S=3
+  segments per request, global-average pooled and averaged over segments
+  (TSN consensus).  Inputs per modality: rgb 3x224x224, flow 10x224x224
+  (5 stacked x/y frames), audio 1x256x256 spectrogram.
+* ``MLP``: configs[0]'s small per-modality MLP towers (D -> 1024 -> 1024).
+* ``FusionHead``: masked concat over the present modalities (absent slots
+  are zero, i.e. their K columns are skipped) -> FC 3072->512 -> ReLU ->
+  verb/noun heads 97+300 = 397 logits.
+
+Every layer maps to one tcgen05 GEMM plan (``csrc/gemm.cu``), a pooling,
+im2col or segment-mean op (``csrc/ops.cu``); the list for one (modality,
+batch) is sealed into a ``device.Program`` and executed by one native call
+(``ms_program_run``), optionally captured in a CUDA graph.
+
+Weights are generated on the CPU from ``torch.manual_seed``-style
+generators so the oracle rebuilds them bit-identically.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+FEAT_DIM = 1024
+N_VERBS, N_NOUNS = 97, 300
+N_CLASSES = N_VERBS + N_NOUNS
+FUSION_HIDDEN = 512
+SEGMENTS = 3
+
+# name, 1x1, 3x3 reduce, 3x3, double-3x3 reduce, double-3x3, pool kind, pool proj, stride
+# (TSN's Caffe BN-Inception: 4c 1x1=128, 4d 1x1=64 so every 4x block emits 576)
+INCEPTION_BLOCKS = (
+    ("3a", 64, 64, 64, 64, 96, "avg", 32, 1),
+    ("3b", 64, 64, 96, 64, 96, "avg", 64, 1),
+    ("3c", 0, 128, 160, 64, 96, "max", 0, 2),
+    ("4a", 224, 64, 96, 96, 128, "avg", 128, 1),
+    ("4b", 192, 96, 128, 96, 128, "avg", 128, 1),
+    ("4c", 128, 128, 160, 128, 160, "avg", 128, 1),
+    ("4d", 64, 128, 192, 160, 192, "avg", 128, 1),
+    ("4e", 0, 128, 192, 192, 256, "max", 0, 2),
+    ("5a", 352, 192, 320, 160, 224, "avg", 128, 1),
+    ("5b", 352, 192, 320, 192, 224, "maxproj", 128, 1),
+)
+
+
+@dataclass(frozen=True)
+class ModalitySpec:
+    name: str
+    channels: int
+    size: int  # square input H = W
+
+    def frame_elems(self) -> int:
+        return self.size * self.size * self.channels
+
+
+TBN_MODALITIES = (ModalitySpec("rgb", 3, 224), ModalitySpec("flow", 10, 224),
+                  ModalitySpec("audio", 1, 256))
+
+
+def conv_out(h: int, k: int, s: int, p: int) -> int:
+    return (h + 2 * p - k) // s + 1
+
+
+def pool_out(h: int, k: int, s: int, p: int, ceil_mode: bool) -> int:
+    span = h + 2 * p - k
+    o = (-(-span // s) if ceil_mode else span // s) + 1
+    if ceil_mode and (o - 1) * s >= h + p:
+        o -= 1
+    return o
+
+
+def bninception_layers(cin: int, size: int):
+    """Static layer list: dicts with kind/name/geometry, in execution order.
+
+    Each conv dict has cin, cout, k, s, p, h (input side) and its MACs per
+    frame; pools carry k, s, p, ceil, is_max.  Used by the device builder,
+    the oracle and the FLOP count.
+    """
+    L = []
+    h = size
+    L.append(dict(kind="conv", name="conv1", cin=cin, cout=64, k=7, s=2, p=3, h=h))
+    h = conv_out(h, 7, 2, 3)
+    L.append(dict(kind="pool", name="pool1", c=64, k=3, s=2, p=0, ceil=True, is_max=True, h=h))
+    h = pool_out(h, 3, 2, 0, True)
+    L.append(dict(kind="conv", name="conv2_red", cin=64, cout=64, k=1, s=1, p=0, h=h))
+    L.append(dict(kind="conv", name="conv2", cin=64, cout=192, k=3, s=1, p=1, h=h))
+    L.append(dict(kind="pool", name="pool2", c=192, k=3, s=2, p=0, ceil=True, is_max=True, h=h))
+    h = pool_out(h, 3, 2, 0, True)
+    c = 192
+    for name, c1, c3r, c3, cdr, cd, pk, proj, s in INCEPTION_BLOCKS:
+        out_c = c1 + c3 + cd + (proj if proj else c)
+        L.append(dict(kind="block", name=name, cin=c, c1=c1, c3r=c3r, c3=c3, cdr=cdr, cd=cd,
+                      pool=pk, proj=proj, s=s, h=h, cout=out_c))
+        h = conv_out(h, 3, s, 1) if s == 2 else h
+        c = out_c
+    L.append(dict(kind="final", c=c, h=h))
+    return L
+
+
+def bninception_macs(cin: int, size: int) -> int:
+    """Multiply-accumulates of one frame (real channels, no padding)."""
+    total = 0
+    for L in bninception_layers(cin, size):
+        if L["kind"] == "conv":
+            o = conv_out(L["h"], L["k"], L["s"], L["p"])
+            total += o * o * L["cout"] * L["cin"] * L["k"] * L["k"]
+        elif L["kind"] == "block":
+            h, c, s = L["h"], L["cin"], L["s"]
+            o = conv_out(h, 3, s, 1) if s == 2 else h
+            total += h * h * c * (L["c1"] + L["c3r"] + L["cdr"])  # 1x1s at input size
+            total += o * o * L["c3r"] * 9 * L["c3"]
+            total += h * h * L["cdr"] * 9 * L["cd"]
+            total += o * o * L["cd"] * 9 * L["cd"]
+            if L["proj"]:
+                total += h * h * c * L["proj"]
+    return total
+
+
+def request_flops(modality: ModalitySpec, segments: int = SEGMENTS) -> int:
+    return 2 * segments * bninception_macs(modality.channels, modality.size)
+
+
+# ------------------------------------------------------------------ weights
+
+
+def _gen(seed: int):
+    import torch
+    g = torch.Generator(device="cpu")
+    g.manual_seed(seed)
+    return g
+
+
+def make_conv(g, cout: int, cin: int, k: int):
+    """He-normal conv weight (bf16-rounded) + small bias, CPU tensors.
+    Weight layout [cout, cin, k, k] (PyTorch), bias fp32."""
+    import torch
+    w = (torch.randn(cout, cin, k, k, generator=g) * (2.0 / (cin * k * k)) ** 0.5).to(torch.bfloat16)
+    b = (torch.randn(cout, generator=g) * 0.02).float()
+    return w, b
+
+
+def bninception_weights(cin: int, size: int, seed: int):
+    """Deterministic weights for one modality's encoder: dict name -> (w, b)."""
+    g = _gen(seed)
+    W = {}
+    for L in bninception_layers(cin, size):
+        if L["kind"] == "conv":
+            W[L["name"]] = make_conv(g, L["cout"], L["cin"], L["k"])
+        elif L["kind"] == "block":
+            n, c = L["name"], L["cin"]
+            if L["c1"]:
+                W[n + "/1x1"] = make_conv(g, L["c1"], c, 1)
+            W[n + "/3x3_reduce"] = make_conv(g, L["c3r"], c, 1)
+            W[n + "/3x3"] = make_conv(g, L["c3"], L["c3r"], 3)
+            W[n + "/d3x3_reduce"] = make_conv(g, L["cdr"], c, 1)
+            W[n + "/d3x3_a"] = make_conv(g, L["cd"], L["cdr"], 3)
+            W[n + "/d3x3_b"] = make_conv(g, L["cd"], L["cd"], 3)
+            if L["proj"]:
+                W[n + "/pool_proj"] = make_conv(g, L["proj"], c, 1)
+    return W
+
+
+def fusion_weights(n_mod: int, feat_dim: int, seed: int):
+    import torch
+    g = _gen(seed)
+    k = n_mod * feat_dim
+    w1 = (torch.randn(FUSION_HIDDEN, k, generator=g) * (2.0 / k) ** 0.5).to(torch.bfloat16)
+    b1 = (torch.randn(FUSION_HIDDEN, generator=g) * 0.02).float()
+    w2 = (torch.randn(N_CLASSES, FUSION_HIDDEN, generator=g) * (1.0 / FUSION_HIDDEN) ** 0.5).to(torch.bfloat16)
+    b2 = (torch.randn(N_CLASSES, generator=g) * 0.02).float()
+    return w1, b1, w2, b2
+
+
+def mlp_weights(dims, seed: int):
+    import torch
+    g = _gen(seed)
+    out = []
+    for din, dout in zip(dims, dims[1:]):
+        w = (torch.randn(dout, din, generator=g) * (2.0 / din) ** 0.5).to(torch.bfloat16)
+        b = (torch.randn(dout, generator=g) * 0.02).float()
+        out.append((w, b))
+    return out
+
+
+def pack_conv_weight(w):
+    """[cout, cin, k, k] -> [cout, k*k*ceil64(cin)] tap-major, channel-padded
+    (the implicit-GEMM K order of ``ms_gemm_plan_conv``)."""
+    import torch
+    cout, cin, k, _ = w.shape
+    cc = -(-cin // 64) * 64
+    out = torch.zeros(cout, k * k, cc, dtype=torch.bfloat16)
+    out[:, :, :cin] = w.permute(0, 2, 3, 1).reshape(cout, k * k, cin)
+    return out.reshape(cout, k * k * cc).contiguous()
+
+
+def pack_im2col_weight(w, k_pad: int):
+    """[cout, cin, k, k] -> [cout, k_pad] in im2col order (kh, kw, c)."""
+    import torch
+    cout, cin, k, _ = w.shape
+    out = torch.zeros(cout, k_pad, dtype=torch.bfloat16)
+    out[:, : k * k * cin] = w.permute(0, 2, 3, 1).reshape(cout, k * k * cin)
+    return out.contiguous()
+
+
+def pack_dense_weight(w):
+    """[n, k] -> [n, ceil64(k)] zero padded."""
+    import torch
+    n, k = w.shape
+    kp = -(-k // 64) * 64
+    out = torch.zeros(n, kp, dtype=torch.bfloat16)
+    out[:, :k] = w
+    return out.contiguous()
+
+
+def pick_bn(n: int) -> int:
+    """Tile width for N output columns: one tile when N <= 256, else the
+    fewest equal-ish tiles (multiples of 32)."""
+    tiles = -(-n // 256)
+    bn = -(-n // tiles)
+    return -(-bn // 32) * 32
+
+
+def pick_conv_tile(n_img: int, oh: int, ow: int):
+    """(bn, bh, bw) with bn*bh*bw <= 128 minimising the number of 128-row
+    tiles (ties: larger bw for contiguous TMA rows)."""
+    best = None
+    for bw in range(1, min(ow, 128) + 1):
+        for bh in range(1, min(oh, 128 // bw) + 1):
+            per = bh * bw
+            for bn in sorted({1, max(1, min(n_img, 128 // per))}):
+                if bn * per > 128:
+                    continue
+                tiles = -(-n_img // bn) * -(-oh // bh) * -(-ow // bw)
+                key = (tiles, -bw, -bh)
+                if best is None or key < best[0]:
+                    best = (key, (bn, bh, bw))
+    return best[1]
+
+
+# ------------------------------------------------------------ device build
+
+
+class BNInceptionEncoder:
+    """One modality's BN-Inception on the device for up to ``max_req``
+    requests of ``segments`` frames each.
+
+    ``program(n_req)`` returns a sealed native op program that maps the
+    gathered input ``X [n_req*S, H, W, C]`` (NHWC bf16) to features
+    ``out [n_req, 1024]`` (bf16).  Buffers are allocated once at capacity;
+    programs are cached per request count.
+    """
+
+    def __init__(self, modality: ModalitySpec, max_req: int, seed: int, segments: int = SEGMENTS,
+                 device="cuda"):
+        import torch
+        self.mod = modality
+        self.max_req = max_req
+        self.S = segments
+        self.dev = torch.device(device)
+        self.layers = bninception_layers(modality.channels, modality.size)
+        self.weights_cpu = bninception_weights(modality.channels, modality.size, seed)
+        self.k_pad1 = -(-(49 * modality.channels) // 64) * 64
+        self._pack()
+        self._alloc()
+        self._programs = {}
+
+    # -- weights on device
+    def _pack(self):
+        import torch
+        d = self.dev
+        W = self.weights_cpu
+        self.w = {}
+        self.b = {}
+        for name, (w, b) in W.items():
+            if name == "conv1":
+                self.w[name] = pack_im2col_weight(w, self.k_pad1).to(d)
+            elif w.shape[-1] == 1:
+                self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
+            else:
+                self.w[name] = pack_conv_weight(w).to(d)
+            self.b[name] = b.to(d)
+        # merged 1x1 weights/biases per block (1x1 | 3x3_reduce | d3x3_reduce)
+        for L in self.layers:
+            if L["kind"] != "block":
+                continue
+            n = L["name"]
+            parts = ([n + "/1x1"] if L["c1"] else []) + [n + "/3x3_reduce", n + "/d3x3_reduce"]
+            self.w[n + "/merged"] = torch.cat([self.w[p] for p in parts], 0).contiguous()
+            self.b[n + "/merged"] = torch.cat([self.b[p] for p in parts], 0).contiguous()
+
+    # -- activation buffers at capacity
+    def _alloc(self):
+        import torch
+        d = self.dev
+        n_img = self.max_req * self.S
+        bf = torch.bfloat16
+
+        def buf(pixels, ch):
+            return torch.empty(max(1, pixels), ch, dtype=bf, device=d)
+
+        size = self.mod.size
+        h1 = conv_out(size, 7, 2, 3)
+        self.cols1 = buf(n_img * h1 * h1, self.k_pad1)
+        self.a_c1 = buf(n_img * h1 * h1, 64)
+        h2 = pool_out(h1, 3, 2, 0, True)
+        self.a_p1 = buf(n_img * h2 * h2, 64)
+        self.a_c2r = buf(n_img * h2 * h2, 64)
+        self.a_c2 = buf(n_img * h2 * h2, 192)
+        self.blocks = {}
+        # ping-pong block outputs + scratch sized for the largest block
+        max_pix_c = 0
+        max_tmp = 0
+        for L in self.layers:
+            if L["kind"] == "block":
+                h, s = L["h"], L["s"]
+                o = conv_out(h, 3, s, 1) if s == 2 else h
+                max_pix_c = max(max_pix_c, o * o * L["cout"], h * h * L["cin"])
+                max_tmp = max(max_tmp, h * h * max(L["c3r"], L["cdr"], L["cd"], L["cin"]))
+        self.ping = torch.empty(n_img * max_pix_c, dtype=bf, device=d)
+        self.pong = torch.empty(n_img * max_pix_c, dtype=bf, device=d)
+        self.t3 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
+        self.td = torch.empty(n_img * max_tmp, dtype=bf, device=d)
+        self.td2 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
+        self.tp = torch.empty(n_img * max_tmp, dtype=bf, device=d)
+        self.out = torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d)
+        self.x = torch.empty(n_img, size, size, self.mod.channels, dtype=bf, device=d)
+
+    def program(self, n_req: int):
+        if n_req in self._programs:
+            return self._programs[n_req]
+        if not 1 <= n_req <= self.max_req:
+            raise ValueError(f"n_req {n_req} outside 1..{self.max_req}")
+        prog = self._build(n_req)
+        self._programs[n_req] = prog
+        return prog
+
+    def _build(self, n_req: int):
+        from . import device as dv
+        P = dv.Program()
+        n = n_req * self.S
+        size, cin = self.mod.size, self.mod.channels
+        h1 = conv_out(size, 7, 2, 3)
+        # stem: im2col + GEMM for the few-channel 7x7/2 conv
+        P.im2col(self.x, n, size, size, cin, 7, 7, 2, 3, self.cols1, self.k_pad1)
+        P.gemm(dv.plan_dense(self.cols1, self.w["conv1"], self.b["conv1"], self.a_c1,
+                             M=n * h1 * h1, K=self.k_pad1, BN=64, relu=True))
+        h2 = pool_out(h1, 3, 2, 0, True)
+        P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
+        P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
+                             M=n * h2 * h2, K=64, BN=64, relu=True))
+        P.gemm(dv.plan_conv(self.a_c2r, n, h2, h2, 64, 64, 3, 3, 1, 1, self.w["conv2"], 192,
+                            self.b["conv2"], self.a_c2, ldd=192, BN=192, relu=True,
+                            tile=pick_conv_tile(n, h2, h2)))
+        h = pool_out(h2, 3, 2, 0, True)
+        cur = self.ping
+        P.pool(self.a_c2, n, h2, h2, 192, 192, 3, 2, 0, True, True, cur, 192, 0)
+        c = 192
+        nxt = self.pong
+        for L in self.layers:
+            if L["kind"] != "block":
+                continue
+            self._block(P, L, n, h, c, cur, nxt)
+            h = conv_out(h, 3, L["s"], 1) if L["s"] == 2 else h
+            c = L["cout"]
+            cur, nxt = nxt, cur
+        P.segment_mean(cur, n_req, self.S, h * h, c, self.out, FEAT_DIM)
+        return P.seal()
+
+    def _block(self, P, L, n, h, cin, X, Y):
+        from . import device as dv
+        name, s = L["name"], L["s"]
+        c1, c3r, c3, cdr, cd, proj = L["c1"], L["c3r"], L["c3"], L["cdr"], L["cd"], L["proj"]
+        o = conv_out(h, 3, s, 1) if s == 2 else h
+        cout = L["cout"]
+        pix_in, pix_out = n * h * h, n * o * o
+        Xv = X[: pix_in * cin].view(pix_in, cin)
+        Yv = Y[: pix_out * cout].view(pix_out, cout)
+        T3 = self.t3[: pix_in * c3r].view(pix_in, c3r)
+        Td = self.td[: pix_in * cdr].view(pix_in, cdr)
+        Td2 = self.td2[: pix_in * cd].view(pix_in, cd)
+        # merged 1x1s: [1x1 -> Y slice 0 | 3x3_reduce -> T3 | d3x3_reduce -> Td]
+        segs = []
+        col = 0
+        if c1:
+            segs.append((0, c1, Yv, cout, 0))
+            col = c1
+        segs.append((col, col + c3r, T3, c3r, 0))
+        segs.append((col + c3r, col + c3r + cdr, Td, cdr, 0))
+        nm = col + c3r + cdr
+        P.gemm(dv.plan_dense(Xv, self.w[name + "/merged"], self.b[name + "/merged"], Yv, M=pix_in,
+                             K=cin, BN=pick_bn(nm), relu=True, segs=segs))
+        tile_in = pick_conv_tile(n, h, h)
+        tile_out = pick_conv_tile(n, o, o)
+        # 3x3 branch (stride s) -> Y[:, c1 : c1+c3]
+        P.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
+                            self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
+                            tile=tile_out))
+        # double 3x3: stride 1 then stride s -> Y[:, c1+c3 : c1+c3+cd]
+        P.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
+                            self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
+                            tile=tile_in))
+        P.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
+                            self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
+                            relu=True, tile=tile_out))
+        pc = c1 + c3 + cd
+        if proj:
+            Tp = self.tp[: pix_in * cin].view(pix_in, cin)
+            is_max = L["pool"] == "maxproj"
+            P.pool(Xv, n, h, h, cin, cin, 3, 1, 1, False, is_max, Tp, cin, 0)
+            P.gemm(dv.plan_dense(Tp, self.w[name + "/pool_proj"], self.b[name + "/pool_proj"], Yv,
+                                 M=pix_in, K=cin, BN=pick_bn(proj), relu=True, col0=pc, ldd=cout))
+        else:  # stride-2 max-pool pass-through into the concat
+            P.pool(Xv, n, h, h, cin, cin, 3, 2, 0, True, True, Yv, cout, pc)
+
+    def flops(self, n_req: int) -> int:
+        return n_req * request_flops(self.mod, self.S)
+
+
+class MLPEncoder:
+    """configs[0]'s per-modality MLP tower D -> 1024 -> 1024 (ReLU)."""
+
+    def __init__(self, in_dim: int, max_req: int, seed: int, hidden=(1024, 1024), device="cuda"):
+        import torch
+        self.dims = (in_dim,) + tuple(hidden)
+        self.max_req = max_req
+        self.dev = torch.device(device)
+        self.weights_cpu = mlp_weights(self.dims, seed)
+        self.w = [pack_dense_weight(w).to(self.dev) for w, _ in self.weights_cpu]
+        self.b = [b.to(self.dev) for _, b in self.weights_cpu]
+        self.x = torch.empty(max_req, -(-in_dim // 64) * 64, dtype=torch.bfloat16, device=self.dev)
+        self.x.zero_()
+        self.acts = [torch.empty(max_req, d, dtype=torch.bfloat16, device=self.dev) for d in hidden]
+        self.out = self.acts[-1]
+        self._programs = {}
+
+    def program(self, n_req: int):
+        from . import device as dv
+        if n_req in self._programs:
+            return self._programs[n_req]
+        P = dv.Program()
+        src, k = self.x, self.dims[0]
+        for (w, b, dst) in zip(self.w, self.b, self.acts):
+            P.gemm(dv.plan_dense(src, w, b, dst, M=n_req, K=k, BN=pick_bn(dst.shape[1]), relu=True))
+            src, k = dst, dst.shape[1]
+        self._programs[n_req] = P.seal()
+        return self._programs[n_req]
+
+    def flops(self, n_req: int) -> int:
+        return n_req * sum(2 * a * b for a, b in zip(self.dims, self.dims[1:]))
+
+
+class FusionHead:
+    """Masked concat -> FC(K*F -> 512) -> ReLU -> FC(512 -> 397) logits."""
+
+    def __init__(self, n_mod: int, max_req: int, seed: int, feat_dim: int = FEAT_DIM, device="cuda"):
+        import torch
+        self.n_mod = n_mod
+        self.feat_dim = feat_dim
+        self.max_req = max_req
+        self.dev = torch.device(device)
+        self.weights_cpu = fusion_weights(n_mod, feat_dim, seed)
+        w1, b1, w2, b2 = self.weights_cpu
+        self.w1, self.b1 = w1.to(self.dev).contiguous(), b1.to(self.dev)
+        self.w2, self.b2 = pack_dense_weight(w2).to(self.dev), b2.to(self.dev)
+        self.h = torch.empty(max_req, FUSION_HIDDEN, dtype=torch.bfloat16, device=self.dev)
+        self.logits = torch.empty(max_req, N_CLASSES, dtype=torch.float32, device=self.dev)
+        self._programs = {}
+
+    def program(self, n_req: int, feats, inv):
+        """feats: per-modality compacted feature buffers; inv [n_mod, >=n_req]."""
+        from . import device as dv
+        key = (n_req, tuple(f.data_ptr() for f in feats), inv.data_ptr())
+        if key in self._programs:
+            return self._programs[key]
+        P = dv.Program()
+        P.gemm(dv.plan_gather(list(feats), inv, self.w1, self.b1, self.h, M=n_req,
+                              feat_dim=self.feat_dim, BN=256, relu=True))
+        P.gemm(dv.plan_dense(self.h, self.w2, self.b2, self.logits, M=n_req, K=FUSION_HIDDEN,
+                             BN=pick_bn(N_CLASSES), out_fp32=True))
+        self._programs[key] = P.seal()
+        return self._programs[key]
+
+    def flops(self, n_req: int) -> int:
+        return n_req * (2 * self.n_mod * self.feat_dim * FUSION_HIDDEN + 2 * FUSION_HIDDEN * N_CLASSES)

@@ -1,0 +1,246 @@
+"""The modality-masked batched forward on the device, and the serving-loop
+worker that runs it.
+
+``MaskedModel.forward(slots, masks)`` is one device pass over a batch of
+requests with per-request modality masks:
+
+  1. request compaction (``ms_compact``): per-modality stable index lists,
+     inverse maps, counting sort by combo, and a gather of each present
+     modality's clip rows from the resident clip pool into contiguous
+     modality-grouped sub-batches;
+  2. each modality's encoder program over its compacted rows only (absent
+     modalities cost nothing);
+  3. the fusion head reads the compacted features through the inverse maps
+     (absent modalities contribute zeros) and writes logits in the original
+     request order — the scatter is fused into the gather GEMM.
+
+Whole passes are captured as CUDA graphs keyed by (N, N_1..N_K) so a part's
+~200 launches replay as one graph launch.
+
+``DeviceExecutor`` plugs this into the serving loop's worker seam
+(reference sim.py:365-397): each dispatched job's canonical parts
+(strategy.py:54-60) become one masked batch (G2(i): requests fill parts in
+index order), timed with CUDA events.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import device as dv
+from .encoders import (FEAT_DIM, SEGMENTS, TBN_MODALITIES, BNInceptionEncoder, FusionHead,
+                       MLPEncoder)
+
+
+def request_masks(parts, size: int) -> np.ndarray:
+    """G2(i): requests 0..size-1 in index order fill the job's canonical
+    parts in order; parts past the true size (rounded-up strategies,
+    scheduler.py:138-167) are truncated."""
+    out = np.zeros(size, dtype=np.int16)
+    lo = 0
+    for mask, batch in parts:
+        hi = min(size, lo + batch)
+        out[lo:hi] = mask
+        lo = hi
+        if lo >= size:
+            break
+    return out
+
+
+class MaskedModel:
+    """Encoders + fusion head + resident input pool + compaction buffers."""
+
+    def __init__(self, encoders, head, pools, row_elems, max_req: int, device="cuda"):
+        import torch
+        self.torch = torch
+        self.dev = torch.device(device)
+        self.encoders = encoders
+        self.head = head
+        self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
+        self.row_bytes = [int(r) * 2 for r in row_elems]
+        self.K = len(encoders)
+        self.max_req = max_req
+        K, n = self.K, max_req
+        self.mask_d = torch.zeros(n, dtype=torch.int16, device=self.dev)
+        self.slot_d = torch.zeros(n, dtype=torch.int32, device=self.dev)
+        self.idx = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
+        self.inv = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
+        self.counts = torch.zeros(K, dtype=torch.int32, device=self.dev)
+        self.offs = torch.zeros((1 << K) + 1, dtype=torch.int32, device=self.dev)
+        self.perm = torch.zeros(n, dtype=torch.int32, device=self.dev)
+        self.mask_h = torch.zeros(n, dtype=torch.int16).pin_memory()
+        self.slot_h = torch.zeros(n, dtype=torch.int32).pin_memory()
+        import ctypes
+        self._X = (ctypes.c_void_p * K)(*[p.data_ptr() for p in pools])
+        self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
+        self._RB = (ctypes.c_longlong * K)(*self.row_bytes)
+        self._graphs = {}
+        self.use_graphs = True
+
+    @property
+    def n_slots(self) -> int:
+        return self.pools[0].shape[0]
+
+    # -- host-side bookkeeping ------------------------------------------
+    def counts_for(self, masks: np.ndarray):
+        m = masks.astype(np.int64)
+        return tuple(int(((m >> k) & 1).sum()) for k in range(self.K))
+
+    def stage_inputs(self, slots, masks, stream=None):
+        """Copy one batch's slots/masks into the fixed device buffers (H2D
+        from pinned memory; stream-ordered)."""
+        n = len(masks)
+        if n > self.max_req:
+            raise ValueError(f"batch of {n} exceeds capacity {self.max_req}")
+        self.mask_h[:n] = self.torch.as_tensor(np.asarray(masks, dtype=np.int16))
+        self.slot_h[:n] = self.torch.as_tensor(np.asarray(slots, dtype=np.int32))
+        s = stream or self.torch.cuda.current_stream()
+        with self.torch.cuda.stream(s):
+            self.mask_d[:n].copy_(self.mask_h[:n], non_blocking=True)
+            self.slot_d[:n].copy_(self.slot_h[:n], non_blocking=True)
+
+    # -- device pass ------------------------------------------------------
+    def _launch(self, n: int, counts):
+        """All kernels of one pass for a staged batch of n requests."""
+        L = dv.lib()
+        sp = dv.stream_ptr()
+        dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._RB,
+                              self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
+                              self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
+                              self.perm.data_ptr(), sp), "ms_compact")
+        for enc, nk in zip(self.encoders, counts):
+            if nk:
+                enc.program(nk).run()
+        inv = self.inv[: self.K * n].view(self.K, n)
+        self.head.program(n, [e.out for e in self.encoders], inv).run()
+
+    def launches_per_pass(self, counts) -> int:
+        n = 1 + sum(1 for c in counts if c)  # index kernel + one gather per present modality
+        n += sum(e.program(c).n_launches for e, c in zip(self.encoders, counts) if c)
+        return n + 2
+
+    def run_staged(self, n: int, counts):
+        """Replay (capturing on first use) the pass for this shape."""
+        if not self.use_graphs:
+            self._launch(n, counts)
+            return
+        key = (n,) + tuple(counts)
+        g = self._graphs.get(key)
+        if g is None:
+            torch = self.torch
+            self._launch(n, counts)  # warm: builds plans/programs outside capture
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch(n, counts)
+            torch.cuda.current_stream().wait_stream(s)
+            self._graphs[key] = g
+        g.replay()
+
+    def forward(self, slots, masks):
+        """One masked pass; returns the logits view [N, 397] (async)."""
+        masks = np.asarray(masks)
+        n = len(masks)
+        counts = self.counts_for(masks)
+        self.stage_inputs(slots, masks)
+        self.run_staged(n, counts)
+        return self.head.logits[:n]
+
+    def flops(self, masks) -> int:
+        counts = self.counts_for(np.asarray(masks))
+        return sum(e.flops(c) for e, c in zip(self.encoders, counts)) + self.head.flops(len(masks))
+
+    def compaction_bytes(self, masks) -> int:
+        """sum over present (request, modality) of 2*row_bytes,
+        + 2N mask bytes + 4*sum N_k index bytes."""
+        counts = self.counts_for(np.asarray(masks))
+        return (sum(2 * rb * c for rb, c in zip(self.row_bytes, counts)) + 2 * len(masks)
+                + 4 * sum(counts))
+
+
+def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_seed: int = 199,
+                    segments: int = SEGMENTS, device="cuda", data_seed: int = 0) -> MaskedModel:
+    """configs[1]: TBN-shaped rgb/flow/audio BN-Inception encoders over
+    EPIC-shaped synthetic clips resident in HBM (N(0,1), bf16)."""
+    import torch
+    encs = [BNInceptionEncoder(m, max_req, s, segments, device) for m, s in zip(TBN_MODALITIES, seeds)]
+    head = FusionHead(len(encs), max_req, fusion_seed, FEAT_DIM, device)
+    g = torch.Generator(device=device)
+    g.manual_seed(data_seed)
+    pools, rows = [], []
+    for m in TBN_MODALITIES:
+        shape = (n_slots, segments, m.size, m.size, m.channels)
+        pools.append(torch.randn(shape, generator=g, device=device, dtype=torch.float32)
+                     .to(torch.bfloat16))
+        rows.append(segments * m.frame_elems())
+    return MaskedModel(encs, head, pools, rows, max_req, device)
+
+
+def build_mlp_model(in_dims, max_req: int, n_slots: int, seeds=(201, 202, 203),
+                    fusion_seed: int = 299, device="cuda", data_seed: int = 0) -> MaskedModel:
+    """configs[0]: small per-modality MLP towers with the same fusion head."""
+    import torch
+    encs = [MLPEncoder(d, max_req, s, device=device) for d, s in zip(in_dims, seeds)]
+    head = FusionHead(len(encs), max_req, fusion_seed, FEAT_DIM, device)
+    g = torch.Generator(device=device)
+    g.manual_seed(data_seed)
+    pools, rows = [], []
+    for e, d in zip(encs, in_dims):
+        width = e.x.shape[1]
+        p = torch.zeros(n_slots, width, dtype=torch.bfloat16, device=device)
+        p[:, :d] = torch.randn(n_slots, d, generator=g, device=device).to(torch.bfloat16)
+        pools.append(p)
+        rows.append(width)
+    return MaskedModel(encs, head, pools, rows, max_req, device)
+
+
+class DeviceExecutor:
+    """Serving-loop worker seam backed by the GPU.
+
+    ``timing="virtual"``: the device pass runs but each part still takes
+    ``max(1, round(predicted * d))`` (reference sim.py:375) so run() logs are
+    bit-identical to the reference.  ``timing="measured"``: the job's pass is
+    timed with CUDA events and that time is attributed to its parts in
+    proportion to their predicted latency; those observations feed the
+    latency-feedback EWMA (scheduler.py:86-91).
+    """
+
+    def __init__(self, model: MaskedModel, timing: str = "measured", slot_seed: int = 0):
+        if timing not in ("virtual", "measured"):
+            raise ValueError("timing must be 'virtual' or 'measured'")
+        self.model = model
+        self.timing = timing
+        self.rng = np.random.default_rng(slot_seed)
+        self.ev0, self.ev1 = dv.Event(), dv.Event()
+        self.passes = 0
+        self.requests = 0
+        self.device_us = 0.0
+        self.last_logits = None
+
+    def execute(self, job, profile, discrepancy: float, now_us: int):
+        parts = job.assigned.strategy.parts
+        masks = request_masks(parts, job.size)
+        slots = self.rng.integers(0, self.model.n_slots, size=job.size)
+        self.ev0.record()
+        logits = self.model.forward(slots, masks)
+        self.ev1.record()
+        us = self.ev0.elapsed_us(self.ev1)  # synchronises on the pass
+        self.passes += 1
+        self.requests += job.size
+        self.device_us += us
+        self.last_logits = logits
+        preds = [profile.part_latency_us(m, b) for m, b in parts]
+        if self.timing == "virtual":
+            return [(p, max(1, round(p * discrepancy))) for p in preds]
+        total = max(1, int(round(us)))
+        tot_pred = sum(preds)
+        out, used = [], 0
+        for i, p in enumerate(preds):
+            a = total - used if i == len(preds) - 1 else max(1, int(round(total * p / tot_pred)))
+            a = max(1, a)
+            used += a
+            out.append((p, a))
+        return out
