@@ -1,0 +1,446 @@
+"""Benchmark: requests/s at >= 99 % latency-SLO attainment (p50/p99 JCT) on
+the TBN-shaped workload (BASELINE.json configs[1]: rgb/flow/audio
+BN-Inception encoders, EPIC-shaped synthetic clips, bf16, 1x B200, fixed
+per-request latency budgets), one independent replica per GPU.
+
+    python bench.py [--gpus N --steps K --warmup W]           # our arm
+    python bench.py --impl reference [--steps K --warmup W]   # CPU reference arm
+
+Our arm, per rank (replicas only; no data-path collective):
+  1. build the model, clip pool resident in HBM, capture the CUDA graphs;
+  2. device profiler: every (combo, batch) cell timed with CUDA events ->
+     ModelProfile (reference YAML format) -> strategy matrix (host DP);
+  3. QPS search: short real-time serving runs (Poisson arrivals, fixed
+     deadline budget) bisected to the highest offered rate with request-
+     weighted violation ratio <= 1 %;
+  4. timed region: W warm-up + K measured serving windows at that rate,
+     real time, inputs resident in HBM; barrier + synchronize on both
+     sides; CUDA events bracket the region; max over ranks.
+     value = requests completed within their deadline / region time (all
+     ranks); latency = request-weighted JCT p50/p99;
+  5. e2e: the same serving at the same rate through the public API with
+     host buffers: each job's clips (present modalities only) H2D from
+     pinned memory and logits D2H inside the timed region;
+  6. roofline: the dominant encoder GEMM launch timed alone with CUDA
+     events (FLOP / time vs measured bf16 peak); compaction gather vs HBM;
+  7. cpu_baseline (rank 0): the CPU oracle (reference path restated) on a
+     bounded sample, all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "requests/sec at >=99% SLO attainment; p50/p99 latency at 1/2/4/8 B200"
+UNIT = "requests/s"
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/mosel_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _init_pg(world):
+    import torch.distributed as tdist
+    if world > 1 and not tdist.is_initialized():
+        tdist.init_process_group("nccl")
+    return tdist if world > 1 else None
+
+
+def _allreduce(pg, vals, op="max"):
+    if pg is None:
+        return vals
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX if op == "max" else pg.ReduceOp.SUM)
+    return t.tolist()
+
+
+# ------------------------------------------------------------- reference arm
+
+
+def cpu_reference_step(orc, rng, n_req, pools_cpu, matrix, profile):
+    """One bounded CPU step of the reference path: selection (oracle P5 on
+    each job's frontier) + the CPU forward for the chosen masks."""
+    import torch
+    from oracle import selection
+    from paper_2310_18481_b200.executor import request_masks
+    from paper_2310_18481_b200.policy import candidates_with_rounding
+    slo = round(float(rng.uniform(profile.min_accuracy, profile.max_accuracy)), 4)
+    cands = candidates_with_rounding(matrix, n_req, slo)
+    lat = [c.latency_us for c in cands]
+    budget = int(rng.integers(lat[0], 2 * lat[-1] + 1))
+    choice = selection.policy_select_one(lat, budget, 0, 1.0)
+    if choice < 0:
+        choice = 0
+    masks = request_masks(cands[choice].strategy.parts, n_req)
+    slots = rng.integers(0, pools_cpu[0].shape[0], size=n_req)
+    clips = [p[torch.as_tensor(slots)].float() for p in pools_cpu]
+    return orc.logits(clips, torch.as_tensor(masks.astype(np.int64))), masks
+
+
+def cpu_baseline_arm(steps, warmup, n_req=2, seconds_cap=30.0):
+    """The oracle (reference path restated) on the host cores."""
+    import torch
+    from oracle.forward import OracleTBN
+    from paper_2310_18481_b200.encoders import SEGMENTS, TBN_MODALITIES
+    from paper_2310_18481_b200.planner import build_matrix, recommended_alphas
+    from paper_2310_18481_b200.profiler import TBN_ACCURACY
+    from paper_2310_18481_b200.registry import ModelProfile
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    g = torch.Generator().manual_seed(0)
+    pools = [torch.randn(4, SEGMENTS, m.size, m.size, m.channels, generator=g).to(torch.bfloat16)
+             for m in TBN_MODALITIES]
+    orc = OracleTBN(TBN_MODALITIES, (101, 102, 103), 199, SEGMENTS)
+    # a synthetic table with the device profile's shape (accuracies fixed)
+    lat = tuple(tuple(1000 * (m.bit_count()) * b for b in range(1, 9)) for m in range(1, 8))
+    prof = ModelProfile("tbn-cpu", ("rgb", "flow", "audio"), 8, lat, TBN_ACCURACY)
+    matrix = build_matrix(prof, range(1, 9), recommended_alphas(prof))
+    rng = np.random.default_rng(0)
+    for _ in range(warmup):
+        cpu_reference_step(orc, rng, n_req, pools, matrix, prof)
+    t0 = time.perf_counter()
+    done = 0
+    n_steps = 0
+    for _ in range(steps):
+        cpu_reference_step(orc, rng, n_req, pools, matrix, prof)
+        done += n_req
+        n_steps += 1
+        if time.perf_counter() - t0 > seconds_cap:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n_steps} steps x {n_req} TBN requests (selection + 3-segment BN-Inception "
+                      f"forward for the chosen masks + fusion), torch fp32 on {cores} threads",
+            "seconds": dt, "steps": n_steps}
+
+
+def reference_arm(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    cb = cpu_baseline_arm(args.steps, args.warmup, n_req=2, seconds_cap=240.0)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": cb["steps"], "warmup": args.warmup,
+            "ms_per_step": 1000.0 * cb["seconds"] / max(1, cb["steps"]), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": "configs[1] TBN BN-Inception rgb/flow/audio, EPIC-shaped clips",
+                       "path": "oracle port of the reference hot path on host cores"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
+    from paper_2310_18481_b200.serving import WorkloadSpec, generate_jobs
+    spec = WorkloadSpec(kind="poisson", qps=qps * world, duration_s=max(1, int(np.ceil(seconds))),
+                        deadline_ms=deadline_ms, seed=seed)
+    jobs = [j for j in generate_jobs(spec, profile) if j.arrival_us < seconds * 1e6]
+    return jobs[rank::world]
+
+
+def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
+          host_clips=None, max_size=None):
+    from paper_2310_18481_b200.realtime import serve_realtime
+    jobs = make_jobs(profile, qps, seconds, deadline_ms, seed, rank, world)
+    if max_size:
+        from paper_2310_18481_b200.serving import JobTemplate
+        jobs = [JobTemplate(j.arrival_us, min(j.size, max_size), j.accuracy_slo, j.deadline_us)
+                for j in jobs]
+    return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed)
+
+
+def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print):
+    """Highest offered rate (req/s) with violation ratio <= 1 %."""
+    lo, hi = 0.0, None
+    q = hi_guess
+    trials = []
+    for it in range(14):
+        lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 1000 + it, max_size=max_size)
+        v = lg.violation_ratio()
+        trials.append((q, v))
+        log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f}")
+        if v <= 0.01:
+            lo = q
+            q = q * 2 if hi is None else (lo + hi) / 2
+        else:
+            hi = q
+            q = (lo + hi) / 2
+        if hi is not None and hi - lo <= 0.04 * hi:
+            break
+    return lo, trials
+
+
+def dominant_gemm_roofline(model, peak_tflops):
+    """Time the largest-FLOP GEMM launch of the rgb encoder at full batch
+    alone with CUDA events on its launching stream."""
+    from paper_2310_18481_b200 import device as dv
+    enc = model.encoders[0]
+    prog = enc.program(model.max_req)
+    best = None
+    for kind, plan in prog.ops:
+        if kind != "gemm":
+            continue
+        fl = plan.flops if hasattr(plan, "flops") else None
+        if fl and (best is None or fl > best[0]):
+            best = (fl, plan)
+    if best is None:
+        return None
+    fl, plan = best
+    e0, e1 = dv.Event(), dv.Event()
+    for _ in range(3):
+        plan.run()
+    n = 20
+    e0.record()
+    for _ in range(n):
+        plan.run()
+    e1.record()
+    us = e0.elapsed_us(e1) / n
+    ach = fl / (us * 1e-6) / 1e12
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": round(ach / peak_tflops, 4), "traffic": None,
+            "kernel": f"gemm_tc_kernel {plan.label}", "flop_per_launch": fl,
+            "avg_launch_us": round(us, 2)}
+
+
+def compaction_roofline(model, peak_gbs, n):
+    from paper_2310_18481_b200 import device as dv
+    rng = np.random.default_rng(5)
+    masks = rng.integers(1, 8, size=n).astype(np.int16)
+    slots = rng.integers(0, model.n_slots, size=n)
+    model.stage_inputs(slots, masks)
+    e0, e1 = dv.Event(), dv.Event()
+    for _ in range(3):
+        model._compact(n)
+    reps = 10
+    e0.record()
+    for _ in range(reps):
+        model._compact(n)
+    e1.record()
+    us = e0.elapsed_us(e1) / reps
+    b = model.compaction_bytes(masks)
+    ach = b / (us * 1e-6) / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(ach / peak_gbs, 4), "bytes_per_launch": b, "avg_us": round(us, 2),
+            "kernel": "compact_index_kernel + gather_rows_kernel (x3)"}
+
+
+def our_arm(args):
+    import torch
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    pg = _init_pg(world)
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
+    from paper_2310_18481_b200 import build
+    build.build()
+    from paper_2310_18481_b200.executor import build_tbn_model
+    from paper_2310_18481_b200.planner import build_matrix, recommended_alphas
+    from paper_2310_18481_b200.profiler import TBN_ACCURACY, profile_model
+    from paper_2310_18481_b200.realtime import HostClips
+    from paper_2310_18481_b200.registry import save_profile
+    peaks, peak_kind = _peaks()
+
+    max_req = args.max_req
+    t_setup = time.perf_counter()
+    model = build_tbn_model(max_req=max_req, n_slots=args.slots, data_seed=rank)
+    model.warm_graphs()
+    log(f"[bench] model + {len(model._graphs)} graphs in {time.perf_counter() - t_setup:.1f}s")
+    prof = profile_model(model, ("rgb", "flow", "audio"), TBN_ACCURACY, max_batch=args.profile_batch,
+                         reps=3)
+    out_dir = ROOT / "gpurun_out"
+    out_dir.mkdir(exist_ok=True)
+    if rank == 0:
+        save_profile(prof, out_dir / "tbn_b200_profile.yaml")
+    matrix = build_matrix(prof, range(1, max_req + 1), recommended_alphas(prof))
+    full1 = prof.part_latency_us(7, 1)
+    log(f"[bench] profile: all-modality batch1 {full1} us, batch{args.profile_batch} "
+        f"{prof.part_latency_us(7, args.profile_batch)} us; audio b1 {prof.part_latency_us(4, 1)} us")
+    deadline_ms = args.deadline_ms or round(10 * full1 / 1000.0, 1)
+    # capacity guess: all-modality requests at the profiled batch
+    cap = args.profile_batch / (prof.part_latency_us(7, args.profile_batch) * 1e-6)
+    rate, trials = find_rate(model, prof, matrix, deadline_ms, args.search_seconds, cap, max_req, log)
+    if pg is not None:  # every replica runs at the slowest replica's rate
+        import torch.distributed as tdist
+        t = torch.tensor([rate], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+        rate = float(t.item())
+    log(f"[bench] operating rate {rate:.1f} req/s per GPU, deadline {deadline_ms} ms")
+
+    # ---- timed region: W warm-up windows then K windows, real time
+    win = args.window_s
+    seconds = (args.warmup + args.steps) * win
+    from paper_2310_18481_b200 import device as dv
+    clocks = ClockSampler(local)
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e_start, e_end = dv.Event(), dv.Event()
+    e_start.record()
+    lg, st = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world, max_size=max_req)
+    e_end.record()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    clk = clocks.stop()
+    region_us = e_start.elapsed_us(e_end)
+    t_lo = args.warmup * win * 1e6
+    timed = [r for r in lg.records if r.arrival_us >= t_lo]
+    ok_req = sum(r.size for r in timed if not r.violated)
+    tot_req = sum(r.size for r in timed)
+    timed_s = args.steps * win
+    from paper_2310_18481_b200.records import MetricsLog
+    tlog = MetricsLog(lg.window_us, tuple(timed))
+    pct = tlog.jct_percentiles_us((50, 99))
+    agg = _allreduce(pg, [ok_req, tot_req], op="sum")
+    agg_t = _allreduce(pg, [timed_s, region_us], op="max")
+    value = agg[0] / agg_t[0]
+    attainment = agg[0] / max(1, agg[1])
+    steps_passes = sum(1 for r in timed if not r.dropped)
+
+    # ---- e2e through the public API with host buffers (same rate)
+    hc = HostClips(model)
+    lg2, st2 = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
+                     max_size=max_req)
+    timed2 = [r for r in lg2.records if r.arrival_us >= t_lo]
+    ok2 = sum(r.size for r in timed2 if not r.violated)
+    tot2 = sum(r.size for r in timed2)
+    agg2 = _allreduce(pg, [ok2, tot2], op="sum")
+    e2e_value = agg2[0] / agg_t[0]
+    n_steps_total = args.warmup + args.steps
+
+    # ---- roofline of the dominant kernel + compaction
+    roof = dominant_gemm_roofline(model, peaks.get("bf16_tflops"))
+    comp = compaction_roofline(model, peaks.get("hbm_gbs"), max_req)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline_arm(steps=args.cpu_steps, warmup=1, n_req=2, seconds_cap=25.0)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000.0 * win, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "configs[1]: TBN BN-Inception rgb/flow/audio encoders (3 segments), "
+                               "EPIC-shaped clips resident in HBM, fixed per-request deadline",
+                   "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
+                   "arrivals": "Poisson, job sizes round(max(1,N(1,6))) capped at max_req",
+                   "policy": "optimized (EDF + MCKP + upgrade), per-job device pass",
+                   "step": f"one {win}s real-time serving window", "max_req": max_req,
+                   "parallelism": f"replicas x{world} (no collective)",
+                   "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
+        "slo_attainment": round(attainment, 5),
+        "latency_ms": {"p50": None if pct[50] is None else round(pct[50] / 1000, 3),
+                       "p99": None if pct[99] is None else round(pct[99] / 1000, 3)},
+        "gpu_launches": st.gpu_launches,
+        "gpu_util": round(st.busy_us / max(1.0, region_us), 4),
+        "passes": st.passes, "region_ms": round(region_us / 1000, 1),
+        "roofline": roof, "roofline_compaction": comp, "peak_kind": peak_kind,
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(st2.h2d_bytes / n_steps_total),
+                "d2h_bytes_per_step": int(st2.d2h_bytes / n_steps_total),
+                "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5)},
+        "clocks": clk, "cpu_baseline": cpu,
+        "search": [(round(q, 1), round(v, 4)) for q, v in trials],
+        "profile_us": {"all_b1": prof.part_latency_us(7, 1),
+                       f"all_b{args.profile_batch}": prof.part_latency_us(7, args.profile_batch),
+                       "audio_b1": prof.part_latency_us(4, 1)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--window-s", type=float, default=1.0)
+    ap.add_argument("--search-seconds", type=float, default=2.0)
+    ap.add_argument("--deadline-ms", type=float, default=0.0)
+    ap.add_argument("--max-req", type=int, default=24)
+    ap.add_argument("--slots", type=int, default=64)
+    ap.add_argument("--profile-batch", type=int, default=8)
+    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -134,6 +134,8 @@ int ms_event_create(void** ev);
 int ms_event_destroy(void* ev);
 int ms_event_record(void* ev, void* stream);
 int ms_event_elapsed_us(void* start, void* stop, double* us);
+/* 0 = completed, 1 = not yet, -1 = error (see ms_last_error) */
+int ms_event_query(void* ev);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

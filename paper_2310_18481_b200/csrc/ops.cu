@@ -307,6 +307,14 @@ int ms_event_record(void* ev, void* stream) {
     return set_error(MS_ERR_CUDA, "cudaEventRecord failed");
   return MS_OK;
 }
+int ms_event_query(void* ev) {
+  cudaError_t e = cudaEventQuery(reinterpret_cast<cudaEvent_t>(ev));
+  if (e == cudaSuccess) return 0;
+  if (e == cudaErrorNotReady) return 1;
+  set_error(MS_ERR_CUDA, cudaGetErrorString(e));
+  return -1;
+}
+
 int ms_event_elapsed_us(void* start, void* stop, double* us) {
   float ms = 0.0f;
   if (cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)) != cudaSuccess ||

@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libmosel_b200.so"
 GEMM_PLAN_BYTES = 1024
 OP_BYTES = 1152
 DROP = -1
+MS_ERR_CUDA_STATUS = 2
 
 _lib = None
 
@@ -60,6 +61,7 @@ _SIGS = {
     "ms_event_destroy": ([_P], C.c_int),
     "ms_event_record": ([_P, _P], C.c_int),
     "ms_event_elapsed_us": ([_P, _P, _P], C.c_int),
+    "ms_event_query": ([_P], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -179,6 +181,8 @@ class GemmPlan:
         addr = C.addressof(self._raw)
         self.addr = (addr + 63) & ~63
         self.keep = []
+        self.flops = 0
+        self.label = ""
 
     def run(self, stream=None):
         check(lib().ms_gemm_run(self.addr, stream_ptr(stream)), "ms_gemm_run")
@@ -210,6 +214,8 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
                                    D.stride(0) if ldd is None else ldd, col0, nseg, sarr),
           "ms_gemm_plan_dense")
     p.keep = [A, W, bias, D, segs]
+    p.flops = 2 * m * W.shape[0] * k
+    p.label = f"dense M={m} N={W.shape[0]} K={k}"
     return p
 
 
@@ -222,6 +228,10 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
                                   ptr(Wt), Cout, BN, ptr(bias), int(relu), ptr(D), ldd, col0, nseg,
                                   sarr, bn, bh, bw), "ms_gemm_plan_conv")
     p.keep = [X, Wt, bias, D, segs]
+    oh = (H + 2 * pad - KH) // stride + 1
+    ow = (W_in + 2 * pad - KW) // stride + 1
+    p.flops = 2 * n_img * oh * ow * Cout * KH * KW * C_in
+    p.label = f"conv {KH}x{KW}/{stride} {C_in}->{Cout} {n_img}x{oh}x{ow}"
     return p
 
 
@@ -232,6 +242,8 @@ def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_f
                                     ptr(W), W.shape[0], BN, ptr(bias), int(relu), int(out_fp32),
                                     ptr(D), D.stride(0), 0), "ms_gemm_plan_gather")
     p.keep = [feats, inv, W, bias, D, arr]
+    p.flops = 2 * M * W.shape[0] * len(feats) * feat_dim
+    p.label = f"gather-concat M={M} N={W.shape[0]} K={len(feats) * feat_dim}"
     return p
 
 
@@ -302,6 +314,13 @@ class Event:
 
     def record(self, stream=None):
         check(lib().ms_event_record(self.h, stream_ptr(stream)), "ms_event_record")
+
+    def done(self) -> bool:
+        """True once the device has passed this event (non-blocking)."""
+        rc = lib().ms_event_query(self.h)
+        if rc < 0:
+            check(MS_ERR_CUDA_STATUS, "ms_event_query")
+        return rc == 0
 
     def elapsed_us(self, end: "Event") -> float:
         out = C.c_double()

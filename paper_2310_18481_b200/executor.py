@@ -100,45 +100,69 @@ class MaskedModel:
             self.slot_d[:n].copy_(self.slot_h[:n], non_blocking=True)
 
     # -- device pass ------------------------------------------------------
-    def _launch(self, n: int, counts):
-        """All kernels of one pass for a staged batch of n requests."""
+    def _compact(self, n: int):
         L = dv.lib()
-        sp = dv.stream_ptr()
         dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._RB,
                               self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
-                              self.perm.data_ptr(), sp), "ms_compact")
+                              self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
+
+    def _head(self, n: int):
+        inv = self.inv[: self.K * n].view(self.K, n)
+        return self.head.program(n, [e.out for e in self.encoders], inv)
+
+    def _launch(self, n: int, counts):
+        """All kernels of one pass for a staged batch of n requests, eagerly."""
+        self._compact(n)
         for enc, nk in zip(self.encoders, counts):
             if nk:
                 enc.program(nk).run()
-        inv = self.inv[: self.K * n].view(self.K, n)
-        self.head.program(n, [e.out for e in self.encoders], inv).run()
+        self._head(n).run()
 
     def launches_per_pass(self, counts) -> int:
         n = 1 + sum(1 for c in counts if c)  # index kernel + one gather per present modality
         n += sum(e.program(c).n_launches for e, c in zip(self.encoders, counts) if c)
         return n + 2
 
-    def run_staged(self, n: int, counts):
-        """Replay (capturing on first use) the pass for this shape."""
-        if not self.use_graphs:
-            self._launch(n, counts)
-            return
-        key = (n,) + tuple(counts)
+    def _graph(self, key, fn):
+        """CUDA graph of ``fn``'s launches, captured on first use."""
         g = self._graphs.get(key)
         if g is None:
             torch = self.torch
-            self._launch(n, counts)  # warm: builds plans/programs outside capture
+            fn()  # warm: builds plans and tensor maps outside capture
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
-                    self._launch(n, counts)
+                    fn()
             torch.cuda.current_stream().wait_stream(s)
             self._graphs[key] = g
-        g.replay()
+        return g
+
+    def run_staged(self, n: int, counts):
+        """Compaction (direct launches), then one graph per present
+        modality's encoder (keyed by its compacted count) and one for the
+        fusion head (keyed by n): O(K * max_req) captures in total."""
+        if not self.use_graphs:
+            self._launch(n, counts)
+            return
+        self._compact(n)
+        for k, (enc, nk) in enumerate(zip(self.encoders, counts)):
+            if nk:
+                self._graph(("enc", k, nk), enc.program(nk).run).replay()
+        self._graph(("head", n), self._head(n).run).replay()
+
+    def warm_graphs(self, max_n: int | None = None):
+        """Capture every encoder/head graph up to ``max_n`` requests."""
+        top = min(max_n or self.max_req, self.max_req)
+        for k, enc in enumerate(self.encoders):
+            for nk in range(1, top + 1):
+                self._graph(("enc", k, nk), enc.program(nk).run)
+        for n in range(1, top + 1):
+            self._graph(("head", n), self._head(n).run)
+        self.torch.cuda.synchronize()
 
     def forward(self, slots, masks):
         """One masked pass; returns the logits view [N, 397] (async)."""

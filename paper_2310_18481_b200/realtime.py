@@ -1,0 +1,183 @@
+"""Real-time serving on one GPU replica.
+
+Same monitor/worker semantics as ``serving.run`` (reference sim.py:241-397:
+EDF admission at the highest-accuracy candidate, policy passes after
+``watermark`` arrivals or when the worker idles, dispatch-time drop rule,
+per-part latency feedback) but driven by the wall clock: arrivals are
+released at their real arrival times, the policy's host time is real, and
+each dispatched job's modality-masked pass runs on the GPU with its
+completion time read from CUDA events on the device clock.  This is how the
+QPS-at-SLO benchmark is measured.
+
+With ``host_io=True`` every job also copies its requests' clips for the
+modalities it actually uses from pinned host memory into the resident pool
+(H2D) and its logits back (D2H) inside the pass — the end-to-end path.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import device as dv
+from .executor import request_masks
+from .planner import StrategyMatrix
+from .policy import (FeedbackState, Job, JobQueue, JobState, Policy, apply_policy,
+                     candidates_with_rounding, next_dispatch, update_latency_feedback)
+from .records import JobRecord, MetricsLog
+from .registry import ModelProfile
+
+
+@dataclass
+class ServeStats:
+    passes: int = 0
+    requests: int = 0
+    gpu_launches: int = 0
+    busy_us: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    policy_host_us: float = 0.0
+    wall_s: float = 0.0
+
+
+class HostClips:
+    """Pinned host copies of the clip pool (for the end-to-end path)."""
+
+    def __init__(self, model):
+        self.host = [p.cpu().pin_memory() for p in model.pools]
+        self.row_bytes = list(model.row_bytes)
+
+
+def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templates,
+                   policy: Policy = Policy.OPTIMIZED, watermark: int = 2,
+                   host_clips: HostClips | None = None, slot_seed: int = 0,
+                   window_us: int = 4_000_000):
+    """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
+
+    Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
+    """
+    import torch
+    rng = np.random.default_rng(slot_seed)
+    queue = JobQueue()
+    fb = FeedbackState()
+    records: list[JobRecord] = []
+    stats = ServeStats()
+    stream = torch.cuda.current_stream()
+    ev_zero = dv.Event()
+    pending = list(enumerate(templates, start=1))
+    pos = 0
+    running = None  # (job, end_event, predicted_parts)
+    since_opt = 0
+    logits_host = torch.empty(model.max_req, model.head.logits.shape[1], dtype=torch.float32).pin_memory()
+    pol_rng = np.random.default_rng([0, list(Policy).index(policy)])
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev_zero.record()
+
+    def now_us() -> int:
+        return int((time.perf_counter() - t0) * 1e6)
+
+    def drop(job):
+        records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo, None, None,
+                                 True, True))
+
+    def run_policy(now):
+        nonlocal since_opt
+        t = time.perf_counter()
+        for j in apply_policy(policy, queue, now, fb, pol_rng):
+            drop(j)
+        stats.policy_host_us += (time.perf_counter() - t) * 1e6
+        since_opt = 0
+
+    def dispatch(now):
+        nonlocal running
+        job, drops = next_dispatch(queue, now, fb)
+        for j in drops:
+            drop(j)
+        if job is None:
+            return
+        parts = job.assigned.strategy.parts
+        masks = request_masks(parts, job.size)
+        slots = rng.integers(0, model.n_slots, size=job.size)
+        ev_s, ev_e = dv.Event(), dv.Event()
+        ev_s.record()
+        if host_clips is not None:
+            for k in range(model.K):
+                use = np.flatnonzero((masks.astype(np.int64) >> k) & 1)
+                for i in use:
+                    model.pools[k][int(slots[i])].copy_(host_clips.host[k][int(slots[i])],
+                                                        non_blocking=True)
+                    stats.h2d_bytes += host_clips.row_bytes[k]
+            stats.h2d_bytes += job.size * 6  # masks + slots
+        logits = model.forward(slots, masks)
+        if host_clips is not None:
+            logits_host[: job.size].copy_(logits, non_blocking=True)
+            stats.d2h_bytes += logits.numel() * 4
+        ev_e.record()
+        counts = model.counts_for(masks)
+        stats.gpu_launches += model.launches_per_pass(counts)
+        stats.passes += 1
+        stats.requests += job.size
+        preds = [profile.part_latency_us(m, b) for m, b in parts]
+        running = (job, ev_s, ev_e, preds)
+
+    def finish(now):
+        """Running job's pass has completed on the device."""
+        nonlocal running
+        job, ev_s, ev_e, preds = running
+        end_us = int(round(ev_zero.elapsed_us(ev_e)))
+        dur = max(1.0, ev_s.elapsed_us(ev_e))
+        stats.busy_us += dur
+        tot = sum(preds)
+        used = 0
+        for i, p in enumerate(preds):
+            a = int(round(dur)) - used if i == len(preds) - 1 else max(1, int(round(dur * p / tot)))
+            a = max(1, a)
+            used += a
+            update_latency_feedback(fb, p, a)
+        job.state = JobState.COMPLETED
+        job.completion_us = end_us
+        queue.running = None
+        records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
+                                 job.assigned.effective_accuracy, end_us, False,
+                                 end_us > job.deadline_us))
+        running = None
+
+    while pos < len(pending) or len(queue) or running is not None:
+        now = now_us()
+        # arrivals due
+        arrived = False
+        while pos < len(pending) and pending[pos][1].arrival_us <= now:
+            jid, tpl = pending[pos]
+            pos += 1
+            cands = candidates_with_rounding(matrix, tpl.size, tpl.accuracy_slo)
+            job = Job(jid, tpl.arrival_us, tpl.size, tpl.accuracy_slo, tpl.deadline_us, cands)
+            if not cands:
+                job.state = JobState.DROPPED
+                drop(job)
+                continue
+            job.assigned_idx = len(cands) - 1
+            queue.admit(job)
+            since_opt += 1
+            arrived = True
+        if running is not None and running[2].done():  # non-blocking completion check
+            finish(now_us())
+        if running is None:
+            if len(queue):
+                if policy is not Policy.NONE and (since_opt > 0 or arrived):
+                    run_policy(now_us())
+                dispatch(now_us())
+        elif arrived and since_opt >= watermark and policy is not Policy.NONE:
+            run_policy(now_us())
+        if running is None and not len(queue) and pos < len(pending):
+            # idle until the next arrival
+            wait = pending[pos][1].arrival_us - now_us()
+            if wait > 200:
+                time.sleep((wait - 100) / 1e6)
+    torch.cuda.synchronize()
+    stats.wall_s = time.perf_counter() - t0
+    log = MetricsLog(window_us, tuple(sorted(records, key=lambda r: r.id)))
+    return log, stats
