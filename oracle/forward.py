@@ -78,7 +78,8 @@ def encode_requests(clips, weights, cin: int, size: int, segments: int):
     """clips: [n_req, S, H, W, C] NHWC (as stored on the device) ->
     bf16-rounded TSN consensus features [n_req, 1024]."""
     n = clips.shape[0]
-    frames = clips.reshape(n * segments, size, size, cin).permute(0, 3, 1, 2)
+    # the device stores channels zero-padded to a multiple of 8: use the real ones
+    frames = clips[..., :cin].reshape(n * segments, size, size, cin).permute(0, 3, 1, 2)
     f = bninception_forward(frames, weights, cin, size)  # [n*S, 1024, h, w]
     f = f.reshape(n, segments, f.shape[1], -1).mean(dim=(1, 3))
     return _bf(f)

@@ -32,12 +32,21 @@
 
 namespace mosel {
 
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                  // 2 per TMEM lane quarter
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // TMA + MMA + epilogue warps
+constexpr int kMaxBias = 1024;
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
-enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2 };
+enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3 };
+// MODE_CONV_SMALLC: first-layer convolutions with few channels (C padded to a
+// multiple of 8 in memory, C < 64).  K is ordered (tap, 8-channel chunk); a
+// 64-wide K block is 8 chunks, each ONE 4-D TMA box {8, bw*s, bh*s, bn}
+// (16-B rows, no swizzle) placed 2 KB apart, which is exactly the UMMA
+// K-major no-swizzle canonical layout (SBO = 128 B, LBO = 2 KB).  This
+// replaces an explicit im2col round trip through HBM.
+constexpr int kSmallcBox = 2048;
 
 struct Seg {
   int n_begin, n_end;
@@ -50,6 +59,7 @@ struct Seg {
 struct GemmParams {
   int mode;
   int M;       // DENSE/GATHER rows
+  int m_tiles; // 128-row tiles (CONV: pixel blocks)
   int N;       // valid output columns
   int BN;      // tile width (multiple of 32, <= 256)
   int num_kb;  // K blocks
@@ -58,6 +68,7 @@ struct GemmParams {
   int b_bytes;
   // CONV geometry
   int n_img, OH, OW, stride, pad, KW, cchunks, bn, bh, bw, tiles_w, tiles_h;
+  int smallc_chunks, smallc_cpt, smallc_cdim;  // total 8-ch chunks, chunks per tap, channel dim
   // GATHER
   const __nv_bfloat16* feat[4];
   const int32_t* inv;  // [n_mod, inv_ld]
@@ -78,6 +89,10 @@ struct alignas(64) GemmPlan {
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ GemmParams p) {
+  // Persistent: CTA b processes tiles b, b + grid, ...; tile t -> (m = t / n_tiles,
+  // n = t % n_tiles).  The smem ring (full/empty) and the two TMEM accumulator
+  // buffers (tfull/tempty) carry their phases across tiles, so the TMA
+  // producer prefetches the next tile while the epilogue drains this one.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = p.stages;
@@ -85,13 +100,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smB = smem + stages * kABytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smB + stages * p.b_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* acc_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* tfull = empty + stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [kMaxBias]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x;
-  const int n_tile = blockIdx.y;
+  const int n_tiles = (p.N + p.BN - 1) / p.BN;
+  const int num_tiles = p.m_tiles * n_tiles;
 
   if (threadIdx.x == 0) {
     const uint32_t full_count = (p.mode == MODE_GATHER) ? 1 + 128 : 1;
@@ -99,31 +116,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], full_count);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     if (p.mode != MODE_GATHER) tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)p.BN) tmem_cols <<= 1;
+  uint32_t acc_stride = 32;
+  while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
+  const uint32_t tmem_cols = 2 * acc_stride;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  for (int i = threadIdx.x; i < p.N && i < kMaxBias; i += blockDim.x)
+    sbias[i] = p.bias != nullptr ? p.bias[i] : 0.0f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  // CONV tile origin
-  int n0 = 0, oh0 = 0, ow0 = 0;
-  if (p.mode == MODE_CONV) {
-    const int tw = m_tile % p.tiles_w;
-    const int th = (m_tile / p.tiles_w) % p.tiles_h;
-    const int tn = m_tile / (p.tiles_w * p.tiles_h);
-    n0 = tn * p.bn;
-    oh0 = th * p.bh;
-    ow0 = tw * p.bw;
-  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -131,25 +143,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t phase = 0;
       const uint32_t tx = (p.mode == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        mbar_wait(&empty[s], phase ^ 1);
-        const uint32_t a_dst = smem_addr(smA + s * kABytes);
-        const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
-        mbar_arrive_expect_tx(&full[s], tx);
-        if (p.mode == MODE_DENSE) {
-          tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
-        } else if (p.mode == MODE_CONV) {
-          const int tap = kb / p.cchunks;
-          const int cc = kb - tap * p.cchunks;
-          const int kh = tap / p.KW;
-          const int kw = tap - kh * p.KW;
-          tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 * p.stride - p.pad + kw,
-                      oh0 * p.stride - p.pad + kh, n0);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m_tile = t / n_tiles, n_tile = t - (t / n_tiles) * n_tiles;
+        int n0 = 0, oh0 = 0, ow0 = 0;
+        if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC) {
+          const int tw = m_tile % p.tiles_w;
+          const int th = (m_tile / p.tiles_w) % p.tiles_h;
+          const int tn = m_tile / (p.tiles_w * p.tiles_h);
+          n0 = tn * p.bn;
+          oh0 = th * p.bh * p.stride - p.pad;
+          ow0 = tw * p.bw * p.stride - p.pad;
         }
-        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
-        if (++s == stages) {
-          s = 0;
-          phase ^= 1;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[s], phase ^ 1);
+          const uint32_t a_dst = smem_addr(smA + s * kABytes);
+          const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
+          mbar_arrive_expect_tx(&full[s], tx);
+          if (p.mode == MODE_DENSE) {
+            tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
+          } else if (p.mode == MODE_CONV) {
+            const int tap = kb / p.cchunks;
+            const int cc = kb - tap * p.cchunks;
+            const int kh = tap / p.KW;
+            const int kw = tap - kh * p.KW;
+            tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
+          } else if (p.mode == MODE_CONV_SMALLC) {
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {
+              const int qc = kb * 8 + j;
+              int c = p.smallc_cdim, w = 0, h = 0;  // past-the-end channel -> zero fill
+              if (qc < p.smallc_chunks) {
+                const int tap = qc / p.smallc_cpt;
+                c = (qc - tap * p.smallc_cpt) * 8;
+                const int kh = tap / p.KW;
+                w = ow0 + (tap - kh * p.KW);
+                h = oh0 + kh;
+              }
+              tma_load_4d(a_dst + j * kSmallcBox, &tmA, &full[s], c, w, h, n0);
+            }
+          }
+          tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -158,123 +195,163 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)p.BN);
     int s = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < p.num_kb; ++kb) {
-      mbar_wait(&full[s], phase);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
       tc_fence_after();
-      if (p.mode == MODE_GATHER) fence_proxy_async_smem();
-      if (lane == 0) {
-        const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
-        const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
-          umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-        }
-        umma_commit(&empty[s]);
-      }
-      __syncwarp();
-      if (++s == stages) {
-        s = 0;
-        phase ^= 1;
-      }
-    }
-    if (lane == 0) umma_commit(acc_full);
-    __syncwarp();
-  } else {
-    // ------------------------------------- warps 2..5: gather + epilogue
-    const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int r = q * 32 + lane;         // tile row owned by this thread
-    if (p.mode == MODE_GATHER) {
-      const int row = m_tile * kBM + r;
-      const __nv_bfloat16* src_row[4];
-      for (int k = 0; k < 4; ++k) {
-        src_row[k] = nullptr;
-        if (k < p.n_mod && row < p.M) {
-          const int j = p.inv[(long long)k * p.inv_ld + row];
-          if (j >= 0) src_row[k] = p.feat[k] + (long long)j * p.feat_dim;
-        }
-      }
-      const int kb_per_mod = p.feat_dim / kBK;
-      int s = 0;
-      uint32_t phase = 0;
+      const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
       for (int kb = 0; kb < p.num_kb; ++kb) {
-        mbar_wait(&empty[s], phase ^ 1);
-        const int k = kb / kb_per_mod;
-        const int off = (kb - k * kb_per_mod) * kBK;
-        const __nv_bfloat16* src = (k < 4) ? src_row[k] : nullptr;
-        const uint32_t dst = smem_addr(smA + s * kABytes) + r * 128;
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        if (p.mode == MODE_GATHER) fence_proxy_async_smem();
+        if (lane == 0) {
+          const bool smallc = p.mode == MODE_CONV_SMALLC;
+          const uint64_t adesc = smallc ? umma_desc_interleave(smem_addr(smA + s * kABytes), kSmallcBox, 128)
+                                        : umma_desc_sw128(smem_addr(smA + s * kABytes));
+          const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
+          // K step of 16: +32 B inside a swizzled 128-B row, or +2 core-matrix
+          // columns (2 x 2 KB) in the no-swizzle small-channel layout
+          const uint64_t a_step = smallc ? (2 * kSmallcBox) >> 4 : 2;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t phys = (uint32_t)(c ^ (r & 7));
-          cp_async_16(dst + phys * 16, src ? (const void*)(src + off + c * 8) : (const void*)p.feat[0],
-                      src ? 16u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_bf16(d_tmem, adesc + a_step * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+          if (kb == p.num_kb - 1) umma_commit(&tfull[acc]);
         }
-        cp_async_mbar_arrive_noinc(&full[s]);
+        __syncwarp();
         if (++s == stages) {
           s = 0;
           phase ^= 1;
         }
       }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
-
-    // output row for this thread (or -1)
-    long long out_row = -1;
-    if (p.mode == MODE_CONV) {
-      const int per_img = p.bh * p.bw;
-      if (r < p.bn * per_img) {
-        const int i = r / per_img;
-        const int y = (r - i * per_img) / p.bw;
-        const int x = r - i * per_img - y * p.bw;
-        const int n = n0 + i, oh = oh0 + y, ow = ow0 + x;
-        if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
-      }
-    } else {
-      const int row = m_tile * kBM + r;
-      if (row < p.M) out_row = row;
-    }
-
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const int n_first = n_tile * p.BN;
-    for (int c = 0; c < p.BN / 32; ++c) {
-      const int nb = n_first + c * 32;
-      if (nb >= p.N) break;  // warp-uniform
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
-      tmem_wait_ld();
-      if (out_row < 0) continue;
-      int sg = 0;
-      while (sg + 1 < p.nseg && nb >= p.seg[sg].n_end) ++sg;
-      const Seg& S = p.seg[sg];
-      const long long base = out_row * S.ldd + S.col0 + (nb - S.n_begin);
-      float f[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float x = __uint_as_float(v[j]);
-        const int n = nb + j;
-        if (p.bias != nullptr && n < p.N) x += p.bias[n];
-        if (p.relu) x = fmaxf(x, 0.0f);
-        f[j] = x;
-      }
-      if (p.out_fp32) {
-        float* dst = reinterpret_cast<float*>(S.ptr) + base;
-        const int lim = min(32, p.N - nb);
-        for (int j = 0; j < lim; ++j) dst[j] = f[j];
-      } else {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(S.ptr) + base;
-        if (nb + 32 <= p.N) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            d4[j] = make_uint4(pack_bf16x2(f[8 * j + 0], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+  } else {
+    // ---------------------- warps 2..9: gather (2..5) + epilogue (all 8)
+    const int q = warp & 3;               // TMEM lane quarter of this warp
+    const int grp = (warp - 2) >> 2;      // column-chunk group: chunks c with c % 2 == grp
+    const int r = q * 32 + lane;          // tile row owned by this thread
+    const bool gatherer = (p.mode == MODE_GATHER) && grp == 0;
+    int s = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m_tile = t / n_tiles, n_tile = t - (t / n_tiles) * n_tiles;
+      if (gatherer) {
+        const int row = m_tile * kBM + r;
+        const int kb_per_mod = p.feat_dim / kBK;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[s], phase ^ 1);
+          const int k = kb / kb_per_mod;
+          const int off = (kb - k * kb_per_mod) * kBK;
+          const __nv_bfloat16* src = nullptr;
+          if (row < p.M) {
+            const int j = p.inv[(long long)k * p.inv_ld + row];
+            if (j >= 0) src = p.feat[k] + (long long)j * p.feat_dim + off;
           }
-        } else {
-          for (int j = 0; j < p.N - nb; ++j) dst[j] = __float2bfloat16_rn(f[j]);
+          const uint32_t dst = smem_addr(smA + s * kABytes) + r * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t phys = (uint32_t)(c ^ (r & 7));
+            cp_async_16(dst + phys * 16, src ? (const void*)(src + c * 8) : (const void*)p.feat[0],
+                        src ? 16u : 0u);
+          }
+          cp_async_mbar_arrive_noinc(&full[s]);
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
         }
       }
+
+      // output row for this thread (or -1)
+      long long out_row = -1;
+      if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC) {
+        const int tw = m_tile % p.tiles_w;
+        const int th = (m_tile / p.tiles_w) % p.tiles_h;
+        const int tn = m_tile / (p.tiles_w * p.tiles_h);
+        const int per_img = p.bh * p.bw;
+        if (r < p.bn * per_img) {
+          const int i = r / per_img;
+          const int y = (r - i * per_img) / p.bw;
+          const int x = r - i * per_img - y * p.bw;
+          const int n = tn * p.bn + i, oh = th * p.bh + y, ow = tw * p.bw + x;
+          if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
+        }
+      } else {
+        const int row = m_tile * kBM + r;
+        if (row < p.M) out_row = row;
+      }
+
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
+      const int n_first = n_tile * p.BN;
+      for (int c = grp; c < p.BN / 32; c += 2) {
+        const int nb = n_first + c * 32;
+        if (nb >= p.N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
+        tmem_wait_ld();
+        if (out_row < 0) continue;
+        // destination segment of this 32-column chunk (segments are 32-aligned)
+        void* seg_ptr = p.seg[0].ptr;
+        long long seg_ld = p.seg[0].ldd;
+        int seg_off = p.seg[0].col0 - p.seg[0].n_begin;
+#pragma unroll
+        for (int g = 1; g < 4; ++g) {
+          if (g < p.nseg && nb >= p.seg[g].n_begin) {
+            seg_ptr = p.seg[g].ptr;
+            seg_ld = p.seg[g].ldd;
+            seg_off = p.seg[g].col0 - p.seg[g].n_begin;
+          }
+        }
+        const long long base = out_row * seg_ld + seg_off + nb;
+        const bool full_chunk = nb + 32 <= p.N;
+        const float* bch = sbias + nb;
+        if (p.out_fp32) {
+          float* dst = reinterpret_cast<float*>(seg_ptr) + base;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __uint_as_float(v[j]) + (nb + j < p.N ? bch[j] : 0.0f);
+            if (p.relu) x = fmaxf(x, 0.0f);
+            if (nb + j < p.N) dst[j] = x;
+          }
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(seg_ptr) + base;
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float a = __uint_as_float(v[2 * j]) + bch[2 * j];
+            float b = __uint_as_float(v[2 * j + 1]) + bch[2 * j + 1];
+            if (p.relu) {
+              a = fmaxf(a, 0.0f);
+              b = fmaxf(b, 0.0f);
+            }
+            pk[j] = pack_bf16x2(a, b);
+          }
+          if (full_chunk) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          } else {
+            unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < p.N) d2[j] = (unsigned short)((pk[j >> 1] >> (16 * (j & 1))) & 0xffff);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 1) {
@@ -302,11 +379,12 @@ static EncodeTiledFn encode_fn() {
 }
 
 static int encode_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims,
-                      const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estride) {
+                      const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estride,
+                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return set_error(MS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box,
-                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char msg[160];
@@ -316,9 +394,20 @@ static int encode_map(CUtensorMap* m, int rank, const void* base, const cuuint64
   return MS_OK;
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int BN, int num_kb, int grid_x) {
   GemmParams& p = P->p;
   if (BN % 32 != 0 || BN < 32 || BN > 256) return set_error(MS_ERR_INVALID, "BN must be a multiple of 32 in [32, 256]");
+  if (p.N > kMaxBias) return set_error(MS_ERR_INVALID, "N exceeds the staged-bias capacity (1024)");
   if (K_pad % kBK != 0) return set_error(MS_ERR_INVALID, "weight K must be padded to a multiple of 64");
   cuuint64_t dims[2] = {(cuuint64_t)K_pad, (cuuint64_t)N_rows_w};
   cuuint64_t strides[1] = {(cuuint64_t)K_pad * 2};
@@ -330,16 +419,18 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   p.num_kb = num_kb;
   p.b_bytes = BN * kBK * 2;
   const int per_stage = kABytes + p.b_bytes;
-  int stages = (200 * 1024) / per_stage;
+  int stages = (196 * 1024) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 1) * 8 + 16;
-  P->grid_x = grid_x;
-  P->grid_y = (p.N + BN - 1) / BN;
+  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + kMaxBias * 4;
+  p.m_tiles = grid_x;
+  const int tiles = grid_x * ((p.N + BN - 1) / BN);
+  P->grid_x = tiles < sm_count() ? tiles : sm_count();
+  P->grid_y = 1;
   int tc = 32;
   while (tc < BN) tc <<= 1;
-  P->tmem_cols = tc;
+  P->tmem_cols = 2 * tc;
   return MS_OK;
 }
 
@@ -433,11 +524,25 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W_in, (cuuint64_t)H, (cuuint64_t)n_img};
   cuuint64_t strides[3] = {(cuuint64_t)c_stride * 2, (cuuint64_t)c_stride * 2 * W_in,
                            (cuuint64_t)c_stride * 2 * W_in * H};
-  cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
-  int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es);
-  if (rc) return rc;
-  const int num_kb = KH * KW * p.cchunks;
+  int num_kb;
+  if (C < kBK) {
+    if (C % 8 != 0) return set_error(MS_ERR_INVALID, "small-channel conv needs C padded to a multiple of 8");
+    p.mode = MODE_CONV_SMALLC;
+    p.smallc_cpt = C / 8;
+    p.smallc_chunks = KH * KW * p.smallc_cpt;
+    p.smallc_cdim = C;
+    p.a_bytes = 8 * bn * bh * bw * 16;
+    num_kb = (p.smallc_chunks + 7) / 8;
+    cuuint32_t box[4] = {8, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+    int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+  } else {
+    cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+    int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es);
+    if (rc) return rc;
+    num_kb = KH * KW * p.cchunks;
+  }
   const int tiles_n = (n_img + bn - 1) / bn;
   return finish_plan(P, Wt, num_kb * kBK, Cout, BN, num_kb, tiles_n * p.tiles_h * p.tiles_w);
 }

@@ -80,27 +80,52 @@ static int pool_out(int in, int k, int stride, int pad, int ceil_mode) {
 }
 
 // -------------------------------------------------------------- im2col
+// One thread = one output pixel x 8 consecutive K columns (one 16-B store,
+// coalesced across threads).  K index = (kh*KW + kw)*C + c; the 8 source
+// elements are scalar loads that hit L1/L2 (each input element is reused by
+// ~KH*KW/stride^2 overlapping windows).
 __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H, int W, int C, int KH,
                               int KW, int stride, int pad, int OH, int OW, __nv_bfloat16* __restrict__ out,
                               int K_pad) {
-  const long long total = (long long)n_img * OH * OW * K_pad;
+  const int k8n = K_pad / 8;
+  const long long total = (long long)n_img * OH * OW * k8n;
   const int kreal = KH * KW * C;
+  const unsigned short* Xs = reinterpret_cast<const unsigned short*>(X);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const int kk = (int)(t % K_pad);
-    const long long pix = t / K_pad;
-    __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
-    if (kk < kreal) {
-      const int c = kk % C;
-      const int tap = kk / C;
-      const int kw = tap % KW, kh = tap / KW;
-      const int ow = (int)(pix % OW);
-      const int oh = (int)((pix / OW) % OH);
-      const int n = (int)(pix / ((long long)OW * OH));
-      const int h = oh * stride - pad + kh, w = ow * stride - pad + kw;
-      if (h >= 0 && h < H && w >= 0 && w < W) v = X[(((long long)n * H + h) * W + w) * C + c];
+    const int k8 = (int)(t % k8n);
+    const long long pix = t / k8n;
+    const int ow = (int)(pix % OW);
+    const int oh = (int)((pix / OW) % OH);
+    const int n = (int)(pix / ((long long)OW * OH));
+    const long long img = (long long)n * H * W;
+    int k = k8 * 8;
+    int c = k % C;
+    int tap = k / C;
+    int kw = tap % KW, kh = tap / KW;
+    unsigned short v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      unsigned short e = 0;
+      if (k + j < kreal) {
+        const int h = oh * stride - pad + kh, w = ow * stride - pad + kw;
+        if (h >= 0 && h < H && w >= 0 && w < W) e = __ldg(Xs + (img + (long long)h * W + w) * C + c);
+      }
+      v[j] = e;
+      if (++c == C) {
+        c = 0;
+        if (++kw == KW) {
+          kw = 0;
+          ++kh;
+        }
+      }
     }
-    out[t] = v;
+    uint4 o;
+    o.x = v[0] | ((unsigned)v[1] << 16);
+    o.y = v[2] | ((unsigned)v[3] << 16);
+    o.z = v[4] | ((unsigned)v[5] << 16);
+    o.w = v[6] | ((unsigned)v[7] << 16);
+    reinterpret_cast<uint4*>(out)[t] = o;
   }
 }
 
@@ -134,7 +159,7 @@ __global__ void segment_mean_kernel(const __nv_bfloat16* __restrict__ X, int n_r
 
 static int grid_for(long long work, int threads) {
   long long b = (work + threads - 1) / threads;
-  const long long cap = 148LL * 16;  // 16 resident 256-thread CTAs per SM
+  const long long cap = 148LL * 32;  // grid-stride beyond 32 CTAs per SM
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;
@@ -188,7 +213,8 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
 static int run_im2col(const Im2colArgs& a, cudaStream_t st) {
   const int OH = (a.H + 2 * a.pad - a.KH) / a.stride + 1;
   const int OW = (a.W + 2 * a.pad - a.KW) / a.stride + 1;
-  const long long work = (long long)a.n_img * OH * OW * a.K_pad;
+  if (a.K_pad % 8 != 0) return set_error(MS_ERR_INVALID, "im2col K_pad must be a multiple of 8");
+  const long long work = (long long)a.n_img * OH * OW * (a.K_pad / 8);
   im2col_kernel<<<grid_for(work, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H,
                                                       a.W, a.C, a.KH, a.KW, a.stride, a.pad, OH, OW,
                                                       reinterpret_cast<__nv_bfloat16*>(a.out), a.K_pad);

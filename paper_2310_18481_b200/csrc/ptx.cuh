@@ -145,6 +145,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;                  // SWIZZLE_128B
   return d;
 }
+// UMMA descriptor, K-major, no swizzle (INTERLEAVE): core matrices of 8 rows
+// x 16 B stored contiguously; SBO = byte stride between 8-row groups (M),
+// LBO = byte stride between core matrices along K.
+__device__ __forceinline__ uint64_t umma_desc_interleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;  // layout type 0 = SWIZZLE_NONE
+}
+
 // instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, M=128
 __host__ __device__ constexpr uint32_t umma_idesc_bf16_m128(uint32_t n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);

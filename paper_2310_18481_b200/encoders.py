@@ -60,8 +60,14 @@ class ModalitySpec:
     channels: int
     size: int  # square input H = W
 
+    @property
+    def cpad(self) -> int:
+        """Stored channels: padded to a multiple of 8 (16-B pixels) so the
+        first conv can read frames with TMA directly (MODE_CONV_SMALLC)."""
+        return -(-self.channels // 8) * 8
+
     def frame_elems(self) -> int:
-        return self.size * self.size * self.channels
+        return self.size * self.size * self.cpad
 
 
 TBN_MODALITIES = (ModalitySpec("rgb", 3, 224), ModalitySpec("flow", 10, 224),
@@ -204,6 +210,19 @@ def pack_conv_weight(w):
     return out.reshape(cout, k * k * cc).contiguous()
 
 
+def pack_smallc_weight(w, cpad: int):
+    """[cout, cin, k, k] -> [cout, ceil64(k*k*cpad)]: K ordered (tap, channel)
+    with channels zero-padded to ``cpad`` (MODE_CONV_SMALLC's K order)."""
+    import torch
+    cout, cin, k, _ = w.shape
+    kk = k * k * cpad
+    out = torch.zeros(cout, -(-kk // 64) * 64, dtype=torch.bfloat16)
+    wp = torch.zeros(cout, cpad, k, k, dtype=torch.bfloat16)
+    wp[:, :cin] = w
+    out[:, :kk] = wp.permute(0, 2, 3, 1).reshape(cout, kk)
+    return out.contiguous()
+
+
 def pack_im2col_weight(w, k_pad: int):
     """[cout, cin, k, k] -> [cout, k_pad] in im2col order (kh, kw, c)."""
     import torch
@@ -270,7 +289,6 @@ class BNInceptionEncoder:
         self.dev = torch.device(device)
         self.layers = bninception_layers(modality.channels, modality.size)
         self.weights_cpu = bninception_weights(modality.channels, modality.size, seed)
-        self.k_pad1 = -(-(49 * modality.channels) // 64) * 64
         self._pack()
         self._alloc()
         self._programs = {}
@@ -284,7 +302,7 @@ class BNInceptionEncoder:
         self.b = {}
         for name, (w, b) in W.items():
             if name == "conv1":
-                self.w[name] = pack_im2col_weight(w, self.k_pad1).to(d)
+                self.w[name] = pack_smallc_weight(w, self.mod.cpad).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
             else:
@@ -311,7 +329,6 @@ class BNInceptionEncoder:
 
         size = self.mod.size
         h1 = conv_out(size, 7, 2, 3)
-        self.cols1 = buf(n_img * h1 * h1, self.k_pad1)
         self.a_c1 = buf(n_img * h1 * h1, 64)
         h2 = pool_out(h1, 3, 2, 0, True)
         self.a_p1 = buf(n_img * h2 * h2, 64)
@@ -334,7 +351,7 @@ class BNInceptionEncoder:
         self.td2 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.tp = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.out = torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d)
-        self.x = torch.empty(n_img, size, size, self.mod.channels, dtype=bf, device=d)
+        self.x = torch.zeros(n_img, size, size, self.mod.cpad, dtype=bf, device=d)
 
     def program(self, n_req: int):
         if n_req in self._programs:
@@ -349,12 +366,14 @@ class BNInceptionEncoder:
         from . import device as dv
         P = dv.Program()
         n = n_req * self.S
-        size, cin = self.mod.size, self.mod.channels
+        size = self.mod.size
         h1 = conv_out(size, 7, 2, 3)
-        # stem: im2col + GEMM for the few-channel 7x7/2 conv
-        P.im2col(self.x, n, size, size, cin, 7, 7, 2, 3, self.cols1, self.k_pad1)
-        P.gemm(dv.plan_dense(self.cols1, self.w["conv1"], self.b["conv1"], self.a_c1,
-                             M=n * h1 * h1, K=self.k_pad1, BN=64, relu=True))
+        # stem: the few-channel 7x7/2 conv reads the frames directly with TMA
+        # (channels padded to 8 in memory; no im2col round trip)
+        cp = self.mod.cpad
+        P.gemm(dv.plan_conv(self.x, n, size, size, cp, cp, 7, 7, 2, 3, self.w["conv1"], 64,
+                            self.b["conv1"], self.a_c1, ldd=64, BN=64, relu=True,
+                            tile=pick_conv_tile(n, h1, h1)))
         h2 = pool_out(h1, 3, 2, 0, True)
         P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
         P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,

@@ -14,8 +14,9 @@ requests with per-request modality masks:
      (absent modalities contribute zeros) and writes logits in the original
      request order — the scatter is fused into the gather GEMM.
 
-Whole passes are captured as CUDA graphs keyed by (N, N_1..N_K) so a part's
-~200 launches replay as one graph launch.
+Each modality's encoder is a CUDA graph keyed by its compacted count and the
+head a graph keyed by N; the present modalities' graphs replay concurrently
+on side streams (fork after compaction, join before the head).
 
 ``DeviceExecutor`` plugs this into the serving loop's worker seam
 (reference sim.py:365-397): each dispatched job's canonical parts
@@ -76,6 +77,10 @@ class MaskedModel:
         self._RB = (ctypes.c_longlong * K)(*self.row_bytes)
         self._graphs = {}
         self.use_graphs = True
+        self.parallel_modalities = True
+        self._side = [torch.cuda.Stream() for _ in range(K)]
+        self._ev_c = torch.cuda.Event()
+        self._ev_k = [torch.cuda.Event() for _ in range(K)]
 
     @property
     def n_slots(self) -> int:
@@ -149,10 +154,28 @@ class MaskedModel:
             self._launch(n, counts)
             return
         self._compact(n)
-        for k, (enc, nk) in enumerate(zip(self.encoders, counts)):
-            if nk:
-                self._graph(("enc", k, nk), enc.program(nk).run).replay()
-        self._graph(("head", n), self._head(n).run).replay()
+        torch = self.torch
+        main = torch.cuda.current_stream()
+        present = [k for k, nk in enumerate(counts) if nk]
+        graphs = [self._graph(("enc", k, counts[k]), self.encoders[k].program(counts[k]).run)
+                  for k in present]
+        head = self._graph(("head", n), self._head(n).run)
+        if not self.parallel_modalities or len(present) < 2:
+            for g in graphs:
+                g.replay()
+        else:
+            # independent encoders run concurrently: fork after compaction,
+            # join before the fusion head
+            self._ev_c.record(main)
+            for k, g in zip(present, graphs):
+                side = self._side[k]
+                side.wait_event(self._ev_c)
+                with torch.cuda.stream(side):
+                    g.replay()
+                self._ev_k[k].record(side)
+            for k in present:
+                main.wait_event(self._ev_k[k])
+        head.replay()
 
     def warm_graphs(self, max_n: int | None = None):
         """Capture every encoder/head graph up to ``max_n`` requests."""
@@ -196,9 +219,12 @@ def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_se
     g.manual_seed(data_seed)
     pools, rows = [], []
     for m in TBN_MODALITIES:
-        shape = (n_slots, segments, m.size, m.size, m.channels)
-        pools.append(torch.randn(shape, generator=g, device=device, dtype=torch.float32)
-                     .to(torch.bfloat16))
+        # NHWC with channels zero-padded to m.cpad (16-B pixels for TMA)
+        pool = torch.zeros((n_slots, segments, m.size, m.size, m.cpad), dtype=torch.bfloat16,
+                           device=device)
+        pool[..., : m.channels] = torch.randn((n_slots, segments, m.size, m.size, m.channels),
+                                              generator=g, device=device).to(torch.bfloat16)
+        pools.append(pool)
         rows.append(segments * m.frame_elems())
     return MaskedModel(encs, head, pools, rows, max_req, device)
 

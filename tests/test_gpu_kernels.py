@@ -247,3 +247,29 @@ def test_pool_im2col_segment_mean(dev):
     torch.cuda.synchronize()
     ref = f.float().cpu().reshape(4, 147, 64).mean(1)
     assert _close(y.cpu(), ref, tol=1e-2)[0]
+
+
+@pytest.mark.parametrize("n,H,Cin,Cpad,tile", [
+    (2, 32, 3, 8, (1, 8, 16)), (3, 64, 10, 16, (1, 8, 16)), (2, 64, 1, 8, (1, 4, 32)),
+    (5, 224, 3, 8, (1, 8, 16)),
+])
+def test_conv_small_channel_direct_vs_torch(dev, n, H, Cin, Cpad, tile):
+    """7x7/2 first-layer conv read straight from 8-channel-padded NHWC frames
+    (MODE_CONV_SMALLC: 8 no-swizzle TMA boxes per K block)."""
+    from paper_2310_18481_b200.encoders import pack_smallc_weight
+    g = torch.Generator().manual_seed(H + Cin)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    X = torch.zeros(n, H, H, Cpad, dtype=torch.bfloat16)
+    X[..., :Cin] = x.permute(0, 2, 3, 1)
+    OH = (H + 6 - 7) // 2 + 1
+    D = torch.zeros(n * OH * OH, 64, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X.cuda(), n, H, H, Cpad, Cpad, 7, 7, 2, 3, pack_smallc_weight(w, Cpad).cuda(), 64,
+                      b.cuda(), D, ldd=64, BN=64, relu=True, tile=tile)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=2, padding=3).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, 64)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
