@@ -53,11 +53,18 @@ class HostClips:
 def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templates,
                    policy: Policy = Policy.OPTIMIZED, watermark: int = 2,
                    host_clips: HostClips | None = None, slot_seed: int = 0,
-                   window_us: int = 4_000_000):
+                   window_us: int = 4_000_000, depth: int = 2):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
+
+    ``depth`` jobs may be in flight on the GPU stream at once: the next job
+    is dispatched (with dispatch time = the last in-flight job's estimated
+    finish, exactly the reference's ``dispatch_time_us``) while the previous
+    one still runs, so host scheduling overlaps device execution.  Jobs still
+    execute one after another on the device, in EDF order.
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
+    from collections import deque
     import torch
     rng = np.random.default_rng(slot_seed)
     queue = JobQueue()
@@ -68,7 +75,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     ev_zero = dv.Event()
     pending = list(enumerate(templates, start=1))
     pos = 0
-    running = None  # (job, end_event, predicted_parts)
+    inflight = deque()  # (job, start_event, end_event, predicted part latencies)
     since_opt = 0
     logits_host = torch.empty(model.max_req, model.head.logits.shape[1], dtype=torch.float32).pin_memory()
     pol_rng = np.random.default_rng([0, list(Policy).index(policy)])
@@ -93,12 +100,13 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         since_opt = 0
 
     def dispatch(now):
-        nonlocal running
+        queue.running = None  # next_dispatch plans one job at a time
         job, drops = next_dispatch(queue, now, fb)
         for j in drops:
             drop(j)
         if job is None:
-            return
+            queue.running = inflight[-1][0] if inflight else None
+            return False
         parts = job.assigned.strategy.parts
         masks = request_masks(parts, job.size)
         slots = rng.integers(0, model.n_slots, size=job.size)
@@ -122,12 +130,13 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         stats.passes += 1
         stats.requests += job.size
         preds = [profile.part_latency_us(m, b) for m, b in parts]
-        running = (job, ev_s, ev_e, preds)
+        inflight.append((job, ev_s, ev_e, preds))
+        queue.running = job  # the latest in-flight job sets the next dispatch time
+        return True
 
-    def finish(now):
-        """Running job's pass has completed on the device."""
-        nonlocal running
-        job, ev_s, ev_e, preds = running
+    def finish():
+        """The oldest in-flight job's pass has completed on the device."""
+        job, ev_s, ev_e, preds = inflight.popleft()
         end_us = int(round(ev_zero.elapsed_us(ev_e)))
         dur = max(1.0, ev_s.elapsed_us(ev_e))
         stats.busy_us += dur
@@ -140,13 +149,13 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             update_latency_feedback(fb, p, a)
         job.state = JobState.COMPLETED
         job.completion_us = end_us
-        queue.running = None
+        if queue.running is job:
+            queue.running = None
         records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
                                  job.assigned.effective_accuracy, end_us, False,
                                  end_us > job.deadline_us))
-        running = None
 
-    while pos < len(pending) or len(queue) or running is not None:
+    while pos < len(pending) or len(queue) or inflight:
         now = now_us()
         # arrivals due
         arrived = False
@@ -163,16 +172,18 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             queue.admit(job)
             since_opt += 1
             arrived = True
-        if running is not None and running[2].done():  # non-blocking completion check
-            finish(now_us())
-        if running is None:
-            if len(queue):
-                if policy is not Policy.NONE and (since_opt > 0 or arrived):
-                    run_policy(now_us())
-                dispatch(now_us())
-        elif arrived and since_opt >= watermark and policy is not Policy.NONE:
+        while inflight and inflight[0][2].done():  # non-blocking completion checks
+            finish()
+        if policy is not Policy.NONE and since_opt > 0 and len(queue) and \
+                (since_opt >= watermark or not inflight):
             run_policy(now_us())
-        if running is None and not len(queue) and pos < len(pending):
+        while len(inflight) < depth and len(queue):
+            t = now_us()
+            if inflight and inflight[-1][0].est_finish_us is not None:
+                t = max(t, inflight[-1][0].est_finish_us)
+            if not dispatch(t):
+                break
+        if not inflight and not len(queue) and pos < len(pending):
             # idle until the next arrival
             wait = pending[pos][1].arrival_us - now_us()
             if wait > 200:
