@@ -208,23 +208,28 @@ def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
 
 
 def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
-          host_clips=None, max_size=None):
+          host_clips=None, max_size=None, cost=None):
     from paper_2310_18481_b200.realtime import serve_realtime
     jobs = make_jobs(profile, qps, seconds, deadline_ms, seed, rank, world)
     if max_size:
         from paper_2310_18481_b200.serving import JobTemplate
         jobs = [JobTemplate(j.arrival_us, min(j.size, max_size), j.accuracy_slo, j.deadline_us)
                 for j in jobs]
-    return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed)
+    if cost is not None:
+        cost.factor = 1.0
+    return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed,
+                          cost=cost)
 
 
-def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print):
+def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print,
+              cost=None):
     """Highest offered rate (req/s) with violation ratio <= 1 %."""
     lo, hi = 0.0, None
     q = hi_guess
     trials = []
     for it in range(14):
-        lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 1000 + it, max_size=max_size)
+        lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 1000 + it, max_size=max_size,
+                       cost=cost)
         v = lg.violation_ratio()
         trials.append((q, v))
         log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f}")
@@ -319,14 +324,21 @@ def our_arm(args):
     out_dir.mkdir(exist_ok=True)
     if rank == 0:
         save_profile(prof, out_dir / "tbn_b200_profile.yaml")
-    matrix = build_matrix(prof, range(1, max_req + 1), recommended_alphas(prof))
+    matrix = build_matrix(prof, range(1, args.max_job + 1), recommended_alphas(prof))
     full1 = prof.part_latency_us(7, 1)
     log(f"[bench] profile: all-modality batch1 {full1} us, batch{args.profile_batch} "
         f"{prof.part_latency_us(7, args.profile_batch)} us; audio b1 {prof.part_latency_us(4, 1)} us")
     deadline_ms = args.deadline_ms
     # capacity guess: all-modality requests at the profiled batch
     cap = args.profile_batch / (prof.part_latency_us(7, args.profile_batch) * 1e-6)
-    rate, trials = find_rate(model, prof, matrix, deadline_ms, args.search_seconds, cap, max_req, log)
+    cost = None
+    if not args.no_batching:
+        from paper_2310_18481_b200.profiler import profile_pass_costs
+        cost = profile_pass_costs(model, reps=3)
+        log(f"[bench] pass cost model: enc b1 {[round(r[0]) for r in cost.enc_us]} us, "
+            f"b{max_req} {[round(r[-1]) for r in cost.enc_us]} us, head b{max_req} {cost.head_us[-1]:.0f} us")
+    rate, trials = find_rate(model, prof, matrix, deadline_ms, args.search_seconds, cap, args.max_job,
+                             log, cost=cost)
     if pg is not None:  # every replica runs at the slowest replica's rate
         import torch.distributed as tdist
         t = torch.tensor([rate], dtype=torch.float64, device="cuda")
@@ -347,7 +359,7 @@ def our_arm(args):
         e_start, e_end = dv.Event(), dv.Event()
         e_start.record()
         lg, st = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world,
-                       max_size=max_req)
+                       max_size=args.max_job, cost=cost)
         e_end.record()
         torch.cuda.synchronize()
         if pg is not None:
@@ -374,7 +386,7 @@ def our_arm(args):
     # ---- e2e through the public API with host buffers (same rate)
     hc = HostClips(model)
     lg2, st2 = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
-                     max_size=max_req)
+                     max_size=args.max_job, cost=cost)
     timed2 = [r for r in lg2.records if r.arrival_us >= t_lo]
     ok2 = sum(r.size for r in timed2 if not r.violated)
     tot2 = sum(r.size for r in timed2)
@@ -401,8 +413,9 @@ def our_arm(args):
         "config": {"workload": "configs[1]: TBN BN-Inception rgb/flow/audio encoders (3 segments), "
                                "EPIC-shaped clips resident in HBM, fixed per-request deadline",
                    "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
-                   "arrivals": "Poisson, job sizes round(max(1,N(1,6))) capped at max_req",
-                   "policy": "optimized (EDF + MCKP + upgrade), per-job device pass",
+                   "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
+                   "policy": "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
+                             " + cross-job batched device passes"),
                    "step": f"one {win}s real-time serving window", "max_req": max_req,
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
@@ -436,8 +449,10 @@ def main():
     ap.add_argument("--search-seconds", type=float, default=2.0)
     ap.add_argument("--deadline-ms", type=float, default=15.0,
                     help="fixed per-request latency budget (deadline - arrival)")
-    ap.add_argument("--max-req", type=int, default=24)
-    ap.add_argument("--slots", type=int, default=64)
+    ap.add_argument("--max-req", type=int, default=48, help="device pass capacity (requests)")
+    ap.add_argument("--max-job", type=int, default=24, help="job size cap (matrix sizes 1..max_job)")
+    ap.add_argument("--no-batching", action="store_true", help="one job per device pass")
+    ap.add_argument("--slots", type=int, default=128)
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")

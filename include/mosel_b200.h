@@ -82,10 +82,18 @@ int ms_compact_index(const uint16_t* mask, int N, int K, int32_t* idx, int32_t* 
  * device); rows of row_bytes (multiple of 16), vectorised 16-B copies. */
 int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
                    const int32_t* count, int max_rows, void* dst, void* stream);
-/* index + one gather per modality (X[k]/G[k]/row_bytes[k], K <= 8) */
-int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_bytes,
-               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
-               int32_t* combo_offsets, int32_t* perm, void* stream);
+/* channel-padding gather: rows of `pixels` bf16 pixels with c_src channels in
+ * src become rows with c_dst (>= c_src, multiple of 8) channels in dst, pad
+ * channels zero (inputs stay compact in host/HBM pools; the encoders' TMA
+ * needs 16-byte pixels) */
+int ms_gather_rows_pad(const void* src, long long pixels, int c_src, int c_dst, const int32_t* slot,
+                       const int32_t* idx, const int32_t* count, int max_rows, void* dst, void* stream);
+/* index + one gather per modality, K <= 8: row k = row_pixels[k] pixels of
+ * c_src[k] channels in X[k] -> c_dst[k] channels in G[k] */
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_pixels,
+               const int32_t* c_src, const int32_t* c_dst, const int32_t* slot, void* const* G,
+               int32_t* idx, int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm,
+               void* stream);
 
 /* ---- tcgen05 GEMM plans (encoders, fusion head) -----------------------
  * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL. */

@@ -40,7 +40,8 @@ _SIGS = {
     "ms_policy_select": ([_P, _P, _P, _I, _P, C.c_int64, _D, _I, _P, _P], C.c_int),
     "ms_compact_index": ([_P, _I, _I, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_gather_rows": ([_P, _LL, _P, _P, _P, _I, _P, _P], C.c_int),
-    "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_gather_rows_pad": ([_P, _LL, _I, _I, _P, _P, _P, _I, _P, _P], C.c_int),
+    "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_gemm_plan_dense": ([_P, _P, _I, _I, _LL, _P, _I, _I, _I, _P, _I, _I, _P, _LL, _I, _I, _P],
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,

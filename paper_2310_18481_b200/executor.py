@@ -51,14 +51,18 @@ def request_masks(parts, size: int) -> np.ndarray:
 class MaskedModel:
     """Encoders + fusion head + resident input pool + compaction buffers."""
 
-    def __init__(self, encoders, head, pools, row_elems, max_req: int, device="cuda"):
+    def __init__(self, encoders, head, pools, rows, max_req: int, device="cuda"):
+        """``rows[k] = (pixels, c_src, c_dst)``: one request of modality k is
+        ``pixels`` pixels of ``c_src`` channels in the pool and ``c_dst``
+        channels in the encoder's input (the gather zero-pads)."""
         import torch
         self.torch = torch
         self.dev = torch.device(device)
         self.encoders = encoders
         self.head = head
         self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
-        self.row_bytes = [int(r) * 2 for r in row_elems]
+        self.rows = [tuple(int(v) for v in r) for r in rows]
+        self.row_bytes = [px * cs * 2 for px, cs, _ in self.rows]  # pool (source) bytes
         self.K = len(encoders)
         self.max_req = max_req
         K, n = self.K, max_req
@@ -74,7 +78,9 @@ class MaskedModel:
         import ctypes
         self._X = (ctypes.c_void_p * K)(*[p.data_ptr() for p in pools])
         self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
-        self._RB = (ctypes.c_longlong * K)(*self.row_bytes)
+        self._PX = (ctypes.c_longlong * K)(*[r[0] for r in self.rows])
+        self._CS = (ctypes.c_int32 * K)(*[r[1] for r in self.rows])
+        self._CD = (ctypes.c_int32 * K)(*[r[2] for r in self.rows])
         self._graphs = {}
         self.use_graphs = True
         self.parallel_modalities = True
@@ -107,8 +113,8 @@ class MaskedModel:
     # -- device pass ------------------------------------------------------
     def _compact(self, n: int):
         L = dv.lib()
-        dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._RB,
-                              self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
+        dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._PX, self._CS,
+                              self._CD, self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
                               self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
 
@@ -201,11 +207,12 @@ class MaskedModel:
         return sum(e.flops(c) for e, c in zip(self.encoders, counts)) + self.head.flops(len(masks))
 
     def compaction_bytes(self, masks) -> int:
-        """sum over present (request, modality) of 2*row_bytes,
-        + 2N mask bytes + 4*sum N_k index bytes."""
+        """per present (request, modality) the row read (real
+        channels) + written (padded channels), + 2N mask bytes + 4*sum N_k
+        index bytes."""
         counts = self.counts_for(np.asarray(masks))
-        return (sum(2 * rb * c for rb, c in zip(self.row_bytes, counts)) + 2 * len(masks)
-                + 4 * sum(counts))
+        rows = sum(2 * px * (cs + cd) * c for (px, cs, cd), c in zip(self.rows, counts))
+        return rows + 2 * len(masks) + 4 * sum(counts)
 
 
 def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_seed: int = 199,
@@ -219,13 +226,10 @@ def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_se
     g.manual_seed(data_seed)
     pools, rows = [], []
     for m in TBN_MODALITIES:
-        # NHWC with channels zero-padded to m.cpad (16-B pixels for TMA)
-        pool = torch.zeros((n_slots, segments, m.size, m.size, m.cpad), dtype=torch.bfloat16,
-                           device=device)
-        pool[..., : m.channels] = torch.randn((n_slots, segments, m.size, m.size, m.channels),
-                                              generator=g, device=device).to(torch.bfloat16)
-        pools.append(pool)
-        rows.append(segments * m.frame_elems())
+        # compact NHWC (real channels); the compaction gather pads to m.cpad
+        pools.append(torch.randn((n_slots, segments, m.size, m.size, m.channels), generator=g,
+                                 device=device).to(torch.bfloat16))
+        rows.append((segments * m.size * m.size, m.channels, m.cpad))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 
@@ -243,7 +247,7 @@ def build_mlp_model(in_dims, max_req: int, n_slots: int, seeds=(201, 202, 203),
         p = torch.zeros(n_slots, width, dtype=torch.bfloat16, device=device)
         p[:, :d] = torch.randn(n_slots, d, generator=g, device=device).to(torch.bfloat16)
         pools.append(p)
-        rows.append(width)
+        rows.append((1, width, width))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 

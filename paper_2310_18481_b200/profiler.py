@@ -65,3 +65,79 @@ def refresh_profile(profile: ModelProfile, model, masks_batches, reps: int = 3) 
     table = [tuple(int(v) for v in np.maximum.accumulate(r)) for r in table]
     return ModelProfile(profile.name, profile.modalities, profile.max_batch, tuple(table),
                         profile.accuracy)
+
+
+class PassCostModel:
+    """Device cost of ONE masked pass for cross-job batching.
+
+    The reference's cost model is additive per part (strategy.py:99-102),
+    which overestimates a merged pass.  Here each modality encoder's graph
+    and the fusion head are timed alone with CUDA events for every batch
+    size, and a pass over compacted counts (N_1..N_K) is estimated as
+    ``compact + sum_k enc_k(N_k) + head(N)`` scaled by an EWMA of
+    observed/estimated pass time (the modality encoders overlap on side
+    streams, which the EWMA learns).
+    """
+
+    def __init__(self, enc_us, head_us, compact_us: float, weight: float = 0.2):
+        self.enc_us = [list(map(float, r)) for r in enc_us]  # [K][n-1]
+        self.head_us = list(map(float, head_us))
+        self.compact_us = float(compact_us)
+        self.factor = 1.0
+        self.weight = weight
+
+    @property
+    def max_n(self) -> int:
+        return len(self.head_us)
+
+    def raw_us(self, counts, n: int) -> float:
+        t = self.compact_us + self.head_us[n - 1]
+        for k, c in enumerate(counts):
+            if c:
+                t += self.enc_us[k][c - 1]
+        return t
+
+    def estimate_us(self, counts, n: int) -> float:
+        return self.raw_us(counts, n) * self.factor
+
+    def observe(self, counts, n: int, observed_us: float) -> None:
+        r = observed_us / max(1.0, self.raw_us(counts, n))
+        self.factor = (1.0 - self.weight) * self.factor + self.weight * r
+
+    def to_json(self):
+        return {"enc_us": self.enc_us, "head_us": self.head_us, "compact_us": self.compact_us}
+
+
+def profile_pass_costs(model, max_n: int | None = None, reps: int = 5) -> PassCostModel:
+    """Time every encoder graph (per modality, per count) and the head."""
+    import torch
+    top = min(max_n or model.max_req, model.max_req)
+    e0, e1 = dv.Event(), dv.Event()
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0.record()
+            fn()
+            e1.record()
+            ts.append(e0.elapsed_us(e1))
+        return float(np.median(ts))
+
+    enc = []
+    for k, e in enumerate(model.encoders):
+        row = []
+        for n in range(1, top + 1):
+            g = model._graph(("enc", k, n), e.program(n).run)
+            row.append(timed(g.replay))
+        enc.append(list(np.maximum.accumulate(row)))
+    # head + compaction on a staged all-modality batch
+    head = []
+    masks = np.full(top, (1 << model.K) - 1, dtype=np.int16)
+    model.stage_inputs(np.arange(top) % model.n_slots, masks)
+    torch.cuda.synchronize()
+    for n in range(1, top + 1):
+        g = model._graph(("head", n), model._head(n).run)
+        head.append(timed(g.replay))
+    comp = timed(lambda: model._compact(top))
+    return PassCostModel(enc, list(np.maximum.accumulate(head)), comp)

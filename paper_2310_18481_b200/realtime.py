@@ -53,7 +53,8 @@ class HostClips:
 def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templates,
                    policy: Policy = Policy.OPTIMIZED, watermark: int = 2,
                    host_clips: HostClips | None = None, slot_seed: int = 0,
-                   window_us: int = 4_000_000, depth: int = 2):
+                   window_us: int = 4_000_000, depth: int = 2, cost=None,
+                   max_batch_requests: int | None = None):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -61,6 +62,15 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     finish, exactly the reference's ``dispatch_time_us``) while the previous
     one still runs, so host scheduling overlaps device execution.  Jobs still
     execute one after another on the device, in EDF order.
+
+    ``cost`` (a ``profiler.PassCostModel``) enables cross-job batching
+    (the reference never batches across jobs):
+    after the EDF head is popped, the following queued jobs (in EDF order,
+    never skipping one) join the same masked device pass while the pass
+    estimate keeps every member within its deadline and the batch within
+    ``max_batch_requests``.  Each job keeps its own assigned strategy; the
+    pass's observed time feeds both the scheduler EWMA (attributed to jobs
+    in proportion to their predicted latency) and the cost model's EWMA.
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
@@ -78,6 +88,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     inflight = deque()  # (job, start_event, end_event, predicted part latencies)
     since_opt = 0
     logits_host = torch.empty(model.max_req, model.head.logits.shape[1], dtype=torch.float32).pin_memory()
+    copy_stream = torch.cuda.Stream() if host_clips is not None else None
+    ring = 0  # host-IO path: each pass uses fresh pool slots (no overlap with in-flight passes)
     pol_rng = np.random.default_rng([0, list(Policy).index(policy)])
 
     torch.cuda.synchronize()
@@ -99,61 +111,100 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         stats.policy_host_us += (time.perf_counter() - t) * 1e6
         since_opt = 0
 
+    cap = min(max_batch_requests or model.max_req, model.max_req)
+
+    def counts_of(masks):
+        m = masks.astype(np.int64)
+        return [int(((m >> k) & 1).sum()) for k in range(model.K)]
+
     def dispatch(now):
         queue.running = None  # next_dispatch plans one job at a time
         job, drops = next_dispatch(queue, now, fb)
         for j in drops:
             drop(j)
         if job is None:
-            queue.running = inflight[-1][0] if inflight else None
+            queue.running = inflight[-1][0][-1] if inflight else None
             return False
-        parts = job.assigned.strategy.parts
-        masks = request_masks(parts, job.size)
-        slots = rng.integers(0, model.n_slots, size=job.size)
+        batch = [job]
+        mlist = [request_masks(job.assigned.strategy.parts, job.size)]
+        counts = counts_of(mlist[0])
+        n = job.size
+        est_us = None
+        if cost is not None:
+            est_us = cost.estimate_us(counts, n)
+            tight = job.deadline_us
+            for cand in list(queue._jobs):  # EDF order; stop at the first misfit
+                if n + cand.size > cap:
+                    break
+                cm = request_masks(cand.assigned.strategy.parts, cand.size)
+                c2 = [a + b for a, b in zip(counts, counts_of(cm))]
+                e2 = cost.estimate_us(c2, n + cand.size)
+                if now + e2 > min(tight, cand.deadline_us):
+                    break
+                queue.remove(cand)
+                cand.state = JobState.RUNNING
+                batch.append(cand)
+                mlist.append(cm)
+                counts, n, est_us = c2, n + cand.size, e2
+                tight = min(tight, cand.deadline_us)
+            for j in batch:
+                j.est_finish_us = now + int(round(est_us))
+        nonlocal ring
+        masks = np.concatenate(mlist)
         ev_s, ev_e = dv.Event(), dv.Event()
-        ev_s.record()
         if host_clips is not None:
-            for k in range(model.K):
-                use = np.flatnonzero((masks.astype(np.int64) >> k) & 1)
-                for i in use:
-                    model.pools[k][int(slots[i])].copy_(host_clips.host[k][int(slots[i])],
-                                                        non_blocking=True)
-                    stats.h2d_bytes += host_clips.row_bytes[k]
-            stats.h2d_bytes += job.size * 6  # masks + slots
+            # H2D of the present modalities' clips on a copy stream (overlaps the
+            # previous pass); the pass waits for it
+            slots = (ring + np.arange(n)) % model.n_slots
+            ring = (ring + n) % model.n_slots
+            with torch.cuda.stream(copy_stream):
+                for k in range(model.K):
+                    for i in np.flatnonzero((masks.astype(np.int64) >> k) & 1):
+                        sl = int(slots[i])
+                        model.pools[k][sl].copy_(host_clips.host[k][sl], non_blocking=True)
+                        stats.h2d_bytes += host_clips.row_bytes[k]
+            stream.wait_stream(copy_stream)
+            stats.h2d_bytes += n * 6  # masks + slots
+        else:
+            slots = rng.integers(0, model.n_slots, size=n)
+        ev_s.record()
         logits = model.forward(slots, masks)
         if host_clips is not None:
-            logits_host[: job.size].copy_(logits, non_blocking=True)
+            logits_host[:n].copy_(logits, non_blocking=True)
             stats.d2h_bytes += logits.numel() * 4
         ev_e.record()
-        counts = model.counts_for(masks)
-        stats.gpu_launches += model.launches_per_pass(counts)
+        stats.gpu_launches += model.launches_per_pass(tuple(counts))
         stats.passes += 1
-        stats.requests += job.size
-        preds = [profile.part_latency_us(m, b) for m, b in parts]
-        inflight.append((job, ev_s, ev_e, preds))
-        queue.running = job  # the latest in-flight job sets the next dispatch time
+        stats.requests += n
+        preds = [[profile.part_latency_us(m, b) for m, b in j.assigned.strategy.parts] for j in batch]
+        inflight.append((batch, ev_s, ev_e, preds, tuple(counts), n))
+        queue.running = batch[-1]  # the latest in-flight job sets the next dispatch time
         return True
 
     def finish():
-        """The oldest in-flight job's pass has completed on the device."""
-        job, ev_s, ev_e, preds = inflight.popleft()
+        """The oldest in-flight pass has completed on the device."""
+        batch, ev_s, ev_e, preds, counts, n = inflight.popleft()
         end_us = int(round(ev_zero.elapsed_us(ev_e)))
         dur = max(1.0, ev_s.elapsed_us(ev_e))
         stats.busy_us += dur
-        tot = sum(preds)
+        if cost is not None:
+            cost.observe(counts, n, dur)
+        flat = [p for ps in preds for p in ps]
+        tot = sum(flat)
         used = 0
-        for i, p in enumerate(preds):
-            a = int(round(dur)) - used if i == len(preds) - 1 else max(1, int(round(dur * p / tot)))
+        for i, p in enumerate(flat):  # per part, in execution order (sim.py:381)
+            a = int(round(dur)) - used if i == len(flat) - 1 else max(1, int(round(dur * p / tot)))
             a = max(1, a)
             used += a
             update_latency_feedback(fb, p, a)
-        job.state = JobState.COMPLETED
-        job.completion_us = end_us
-        if queue.running is job:
-            queue.running = None
-        records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
-                                 job.assigned.effective_accuracy, end_us, False,
-                                 end_us > job.deadline_us))
+        for job in batch:
+            job.state = JobState.COMPLETED
+            job.completion_us = end_us
+            if queue.running is job:
+                queue.running = None
+            records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
+                                     job.assigned.effective_accuracy, end_us, False,
+                                     end_us > job.deadline_us))
 
     while pos < len(pending) or len(queue) or inflight:
         now = now_us()
@@ -179,8 +230,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             run_policy(now_us())
         while len(inflight) < depth and len(queue):
             t = now_us()
-            if inflight and inflight[-1][0].est_finish_us is not None:
-                t = max(t, inflight[-1][0].est_finish_us)
+            if inflight and inflight[-1][0][-1].est_finish_us is not None:
+                t = max(t, inflight[-1][0][-1].est_finish_us)
             if not dispatch(t):
                 break
         if not inflight and not len(queue) and pos < len(pending):

@@ -273,3 +273,20 @@ def test_conv_small_channel_direct_vs_torch(dev, n, H, Cin, Cpad, tile):
     ref = ref.permute(0, 2, 3, 1).reshape(-1, 64)
     ok, err, scale = _close(D.cpu(), ref)
     assert ok, (err, scale)
+
+
+@pytest.mark.parametrize("c_src,c_dst", [(3, 8), (10, 16), (1, 8), (16, 16)])
+def test_gather_rows_channel_pad(dev, c_src, c_dst):
+    L = dev.lib()
+    pix = 3 * 17 * 19
+    pool = _bf(torch.randn(9, pix, c_src)).cuda()
+    idx = torch.tensor([4, 0, 7], dtype=torch.int32, device="cuda")
+    slot = torch.tensor([8, 7, 6, 5, 4, 3, 2, 1, 0], dtype=torch.int32, device="cuda")
+    count = torch.tensor([3], dtype=torch.int32, device="cuda")
+    dst = torch.full((3, pix, c_dst), 7.0, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_gather_rows_pad(dev.ptr(pool), pix, c_src, c_dst, dev.ptr(slot), dev.ptr(idx),
+                                   dev.ptr(count), 3, dev.ptr(dst), dev.stream_ptr()), "gather_pad")
+    torch.cuda.synchronize()
+    src = pool[slot[idx.long()].long()]
+    assert torch.equal(dst[..., :c_src], src)
+    assert torch.count_nonzero(dst[..., c_src:]) == 0

@@ -88,3 +88,31 @@ def test_tbn_graph_replay_matches_eager(built):
     c = model.forward(slots, masks).clone()
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(b, c)
+
+
+def test_realtime_serving_batched_and_host_io(built):
+    """Wall-clock serving on the device: every request accounted for, each
+    completed job met its accuracy floor, batching merged jobs, and the
+    host-IO path copied only the present modalities' clips."""
+    import paper_2310_18481_b200 as ms
+    from paper_2310_18481_b200.executor import build_tbn_model
+    from paper_2310_18481_b200.profiler import TBN_ACCURACY, profile_model, profile_pass_costs
+    from paper_2310_18481_b200.realtime import HostClips, serve_realtime
+    model = build_tbn_model(max_req=16, n_slots=32)
+    prof = profile_model(model, ("rgb", "flow", "audio"), TBN_ACCURACY, max_batch=4, reps=2)
+    matrix = ms.build_matrix(prof, range(1, 9), ms.recommended_alphas(prof))
+    cost = profile_pass_costs(model, reps=2)
+    spec = ms.WorkloadSpec(kind="poisson", qps=1500, duration_s=1, deadline_ms=20, seed=5)
+    jobs = [ms.JobTemplate(j.arrival_us, min(j.size, 8), j.accuracy_slo, j.deadline_us)
+            for j in ms.generate_jobs(spec, prof)]
+    log, st = serve_realtime(model, prof, matrix, jobs, cost=cost)
+    assert len(log.records) == len(jobs)
+    assert sum(r.size for r in log.records) == sum(j.size for j in jobs)
+    assert all(r.achieved_accuracy >= r.accuracy_slo for r in log.records if not r.dropped)
+    assert st.passes < len([r for r in log.records if not r.dropped])  # jobs were merged
+    log2, st2 = serve_realtime(model, prof, matrix, jobs, cost=cost, host_clips=HostClips(model))
+    assert len(log2.records) == len(jobs)
+    n_req = sum(j.size for j in jobs)
+    full = sum(model.row_bytes) * n_req
+    assert 0 < st2.h2d_bytes <= full + 6 * n_req  # only present modalities are transferred
+    assert st2.h2d_bytes % 2 == 0 and st2.d2h_bytes > 0
