@@ -82,18 +82,22 @@ int ms_compact_index(const uint16_t* mask, int N, int K, int32_t* idx, int32_t* 
  * device); rows of row_bytes (multiple of 16), vectorised 16-B copies. */
 int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
                    const int32_t* count, int max_rows, void* dst, void* stream);
-/* channel-padding gather: rows of `pixels` bf16 pixels with c_src channels in
- * src become rows with c_dst (>= c_src, multiple of 8) channels in dst, pad
- * channels zero (inputs stay compact in host/HBM pools; the encoders' TMA
- * needs 16-byte pixels) */
-int ms_gather_rows_pad(const void* src, long long pixels, int c_src, int c_dst, const int32_t* slot,
-                       const int32_t* idx, const int32_t* count, int max_rows, void* dst, void* stream);
-/* index + one gather per modality, K <= 8: row k = row_pixels[k] pixels of
- * c_src[k] channels in X[k] -> c_dst[k] channels in G[k] */
-int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_pixels,
-               const int32_t* c_src, const int32_t* c_dst, const int32_t* slot, void* const* G,
-               int32_t* idx, int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm,
-               void* stream);
+/* One request row of a modality: `lines` lines of `width` pixels with c_src
+ * channels in the pool; in the encoder input each pixel has c_dst (>= c_src,
+ * multiple of 8) channels and every line gets pad_w zero pixels on both
+ * ends (the first conv's window padding).  Plain rows: lines=1, width=1,
+ * c_src=c_dst=elements, pad_w=0. */
+typedef struct MsRowDesc {
+  long long lines;
+  int width, c_src, c_dst, pad_w;
+} MsRowDesc;
+int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
+                       const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows,
+                       void* dst, void* stream);
+/* index + one gather per modality (K <= 8), rows described by rows[k] */
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
+               int32_t* combo_offsets, int32_t* perm, void* stream);
 
 /* ---- tcgen05 GEMM plans (encoders, fusion head) -----------------------
  * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL. */
@@ -103,7 +107,10 @@ int ms_gemm_plan_dense(void* plan, const void* A, int M, int K, long long lda, c
 /* implicit-GEMM conv over NHWC bf16 input [n_img, H, W, C] (channel stride
  * c_stride); weights [Cout, KH*KW*ceil64(C)] tap-major, each tap's channels
  * zero-padded to a multiple of 64; output pixel-major [n_img*OH*OW, ...].
- * (bn, bh, bw) is the output-pixel block one 128-row tile covers. */
+ * (bn, bh, bw) is the output-pixel block one 128-row tile covers.
+ * C = 8 or 16: first-layer mode; X is [n_img, H, W_in + 2*pad, C] (W
+ * pre-padded, e.g. by ms_compact's pad_w) and the weights are
+ * [Cout, KH * 8 * C] in (kh, window pixel j < 8, c) order, taps j >= KW zero. */
 int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
                       int KH, int KW, int stride, int pad, const void* Wt, int Cout, int BN,
                       const float* bias, int relu, void* D, long long ldd, int col0, int nseg,

@@ -40,13 +40,15 @@ constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3 };
-// MODE_CONV_SMALLC: first-layer convolutions with few channels (C padded to a
-// multiple of 8 in memory, C < 64).  K is ordered (tap, 8-channel chunk); a
-// 64-wide K block is 8 chunks, each ONE 4-D TMA box {8, bw*s, bh*s, bn}
-// (16-B rows, no swizzle) placed 2 KB apart, which is exactly the UMMA
-// K-major no-swizzle canonical layout (SBO = 128 B, LBO = 2 KB).  This
-// replaces an explicit im2col round trip through HBM.
-constexpr int kSmallcBox = 2048;
+// MODE_CONV_SMALLC: first-layer convolutions with few channels (C8 = 8 or
+// 16 stored channels).  The input is stored W-padded by `pad` zero pixels on
+// each side, so for output pixel (oh, ow) and filter row kh the KW-tap
+// window is one contiguous run of 8 pixels (8*C8 elements).  A 4-D tensor
+// map whose innermost dimension IS that window and whose next dimension
+// steps one output column (s pixels — the windows overlap) turns each
+// 128-byte slice of a window into one smem row, so a K block = (kh, window
+// half) is ONE TMA box in the standard SW128 K-major layout.  K order: (kh, j, c) with j < 8 (taps j >= KW are
+// zero-weight).  Replaces an im2col round trip through HBM.
 
 struct Seg {
   int n_begin, n_end;
@@ -68,7 +70,7 @@ struct GemmParams {
   int b_bytes;
   // CONV geometry
   int n_img, OH, OW, stride, pad, KW, cchunks, bn, bh, bw, tiles_w, tiles_h;
-  int smallc_chunks, smallc_cpt, smallc_cdim;  // total 8-ch chunks, chunks per tap, channel dim
+  int smallc_halves, smallc_jpb;  // K blocks per filter row, window pixels per K block
   // GATHER
   const __nv_bfloat16* feat[4];
   const int32_t* inv;  // [n_mod, inv_ld]
@@ -168,19 +170,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kw = tap - kh * p.KW;
             tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
           } else if (p.mode == MODE_CONV_SMALLC) {
-#pragma unroll 1
-            for (int j = 0; j < 8; ++j) {
-              const int qc = kb * 8 + j;
-              int c = p.smallc_cdim, w = 0, h = 0;  // past-the-end channel -> zero fill
-              if (qc < p.smallc_chunks) {
-                const int tap = qc / p.smallc_cpt;
-                c = (qc - tap * p.smallc_cpt) * 8;
-                const int kh = tap / p.KW;
-                w = ow0 + (tap - kh * p.KW);
-                h = oh0 + kh;
-              }
-              tma_load_4d(a_dst + j * kSmallcBox, &tmA, &full[s], c, w, h, n0);
-            }
+            const int kh = kb / p.smallc_halves;
+            const int half = kb - kh * p.smallc_halves;
+            // ow0/oh0 already include -pad; W is pre-padded in memory so the
+            // column coordinate is the raw output column
+            tma_load_4d(a_dst, &tmA, &full[s], half * kBK, (ow0 + p.pad) / p.stride, oh0 + kh, n0);
           }
           tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
           if (++s == stages) {
@@ -206,16 +200,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (p.mode == MODE_GATHER) fence_proxy_async_smem();
         if (lane == 0) {
-          const bool smallc = p.mode == MODE_CONV_SMALLC;
-          const uint64_t adesc = smallc ? umma_desc_interleave(smem_addr(smA + s * kABytes), kSmallcBox, 128)
-                                        : umma_desc_sw128(smem_addr(smA + s * kABytes));
+          const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
-          // K step of 16: +32 B inside a swizzled 128-B row, or +2 core-matrix
-          // columns (2 x 2 KB) in the no-swizzle small-channel layout
-          const uint64_t a_step = smallc ? (2 * kSmallcBox) >> 4 : 2;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            umma_bf16(d_tmem, adesc + a_step * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
           umma_commit(&empty[s]);
           if (kb == p.num_kb - 1) umma_commit(&tfull[acc]);
@@ -527,15 +517,23 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   int num_kb;
   if (C < kBK) {
-    if (C % 8 != 0) return set_error(MS_ERR_INVALID, "small-channel conv needs C padded to a multiple of 8");
+    // X is [n_img, H, W_in + 2*pad, C] (W pre-padded with zeros)
+    if (C != 8 && C != 16) return set_error(MS_ERR_INVALID, "small-channel conv needs C == 8 or 16 (padded)");
+    if (KW > 8) return set_error(MS_ERR_INVALID, "small-channel conv supports KW <= 8");
     p.mode = MODE_CONV_SMALLC;
-    p.smallc_cpt = C / 8;
-    p.smallc_chunks = KH * KW * p.smallc_cpt;
-    p.smallc_cdim = C;
-    p.a_bytes = 8 * bn * bh * bw * 16;
-    num_kb = (p.smallc_chunks + 7) / 8;
-    cuuint32_t box[4] = {8, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
-    int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es, CU_TENSOR_MAP_SWIZZLE_NONE);
+    p.smallc_jpb = 64 / C;          // window pixels per 128-B row
+    p.smallc_halves = 8 / p.smallc_jpb;
+    p.a_bytes = bn * bh * bw * 128;
+    num_kb = KH * p.smallc_halves;
+    const long long wp = W_in + 2LL * pad;
+    // dim0 = the contiguous 8-pixel window (8*C elements) starting at padded
+    // column ow*stride; dim1 = output column, stride `stride` pixels (the
+    // windows overlap); dim2 = input row (element stride = conv stride)
+    cuuint64_t d5[4] = {(cuuint64_t)(8 * C), (cuuint64_t)OW, (cuuint64_t)H, (cuuint64_t)n_img};
+    cuuint64_t s5[3] = {(cuuint64_t)C * 2 * stride, (cuuint64_t)(wp * C * 2), (cuuint64_t)(wp * C * 2 * H)};
+    cuuint32_t b5[4] = {(cuuint32_t)kBK, (cuuint32_t)bw, (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+    cuuint32_t e5[4] = {1, 1, (cuuint32_t)stride, 1};
+    int rc = encode_map(&P->tmA, 4, X, d5, s5, b5, e5);
     if (rc) return rc;
   } else {
     cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};

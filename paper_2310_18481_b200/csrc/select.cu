@@ -176,47 +176,57 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_
   }
 }
 
-// Channel-padding gather: rows are `pixels` pixels of c_src channels in the
-// pool and c_dst (multiple of 8, >= c_src) channels in the sub-batch; the
-// pad channels are zero.  One thread = one pixel x 8 destination channels
-// (16-B store); source reads are contiguous across consecutive pixels.
-__global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, long long pixels, int c_src,
-                                       int c_dst, const int32_t* __restrict__ slot,
+// Padding gather: a source row is `lines` lines of `width` pixels with c_src
+// channels; the destination row has c_dst (multiple of 8, >= c_src) channels
+// and `pad_w` zero pixels on both ends of every line (the first conv's
+// window padding, so its TMA windows never leave the line).  One thread =
+// one destination pixel x 8 channels (one 16-B store).
+__global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, long long lines, int width,
+                                       int c_src, int c_dst, int pad_w, const int32_t* __restrict__ slot,
                                        const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
                                        uint4* __restrict__ dst) {
   const int n = *count;
   const int g8 = c_dst / 8;
-  const long long work = pixels * g8;
+  const int wd = width + 2 * pad_w;
+  const long long work = lines * wd * g8;
+  const long long src_row = lines * width * c_src;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
     int r = idx[j];
     if (slot) r = slot[r];
-    const unsigned short* s = src + (long long)r * pixels * c_src;
+    const unsigned short* s = src + (long long)r * src_row;
     uint4* d = dst + (long long)j * work;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < work;
          t += (long long)gridDim.x * blockDim.x) {
       const long long px = t / g8;
       const int c0 = (int)(t - px * g8) * 8;
-      const unsigned short* sp = s + px * c_src;
-      unsigned short v[8];
+      const long long line = px / wd;
+      const int x = (int)(px - line * wd) - pad_w;
+      unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (x >= 0 && x < width) {
+        const unsigned short* sp = s + (line * width + x) * c_src;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = (c0 + i < c_src) ? __ldcs(sp + c0 + i) : (unsigned short)0;
+        for (int i = 0; i < 8; ++i)
+          if (c0 + i < c_src) v[i] = __ldcs(sp + c0 + i);
+      }
       d[t] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
                         v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
     }
   }
 }
 
-static int gather_pad_launch(const void* src, long long pixels, int c_src, int c_dst, const int32_t* slot,
-                             const int32_t* idx, const int32_t* count, int max_rows, void* dst, cudaStream_t st) {
-  if (c_dst % 8 != 0 || c_src > c_dst || c_src < 1) return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0");
+static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
+                             const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
+                             cudaStream_t st) {
+  if (c_dst % 8 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
+    return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0, pad_w >= 0");
   if (max_rows <= 0) return MS_OK;
-  const long long work = pixels * (c_dst / 8);
+  const long long work = lines * (width + 2LL * pad_w) * (c_dst / 8);
   long long bx = (work + 255) / 256;
   if (bx > 1024) bx = 1024;
   if (bx < 1) bx = 1;
   const int gy = max_rows < 65535 ? max_rows : 65535;
   gather_rows_pad_kernel<<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-      reinterpret_cast<const unsigned short*>(src), pixels, c_src, c_dst, slot, idx, count,
+      reinterpret_cast<const unsigned short*>(src), lines, width, c_src, c_dst, pad_w, slot, idx, count,
       reinterpret_cast<uint4*>(dst));
   return check_launch("gather_rows_pad_kernel");
 }
@@ -274,26 +284,29 @@ int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, co
   return gather_launch(src, row_bytes, slot, idx, count, max_rows, dst, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ms_gather_rows_pad(const void* src, long long pixels, int c_src, int c_dst, const int32_t* slot,
-                       const int32_t* idx, const int32_t* count, int max_rows, void* dst, void* stream) {
+int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
+                       const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
+                       void* stream) {
   if (!src || !idx || !count || !dst) return set_error(MS_ERR_INVALID, "gather_rows_pad: null pointer");
-  return gather_pad_launch(src, pixels, c_src, c_dst, slot, idx, count, max_rows, dst,
+  return gather_pad_launch(src, lines, width, c_src, c_dst, pad_w, slot, idx, count, max_rows, dst,
                            reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const long long* row_pixels,
-               const int32_t* c_src, const int32_t* c_dst, const int32_t* slot, void* const* G, int32_t* idx,
-               int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm, void* stream) {
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
+               int32_t* combo_offsets, int32_t* perm, void* stream) {
   int rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   for (int k = 0; k < K; ++k) {
-    if (X == nullptr || G == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
-    if (c_src[k] == c_dst[k] && (row_pixels[k] * c_src[k] * 2) % 16 == 0)
-      rc = gather_launch(X[k], row_pixels[k] * c_src[k] * 2, slot, idx + (long long)k * N, counts + k, N, G[k], st);
+    if (X == nullptr || G == nullptr || rows == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
+    const MsRowDesc& r = rows[k];
+    const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
+    if (r.c_src == r.c_dst && r.pad_w == 0 && bytes % 16 == 0)
+      rc = gather_launch(X[k], bytes, slot, idx + (long long)k * N, counts + k, N, G[k], st);
     else
-      rc = gather_pad_launch(X[k], row_pixels[k], c_src[k], c_dst[k], slot, idx + (long long)k * N, counts + k, N,
-                             G[k], st);
+      rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, slot, idx + (long long)k * N,
+                             counts + k, N, G[k], st);
     if (rc) return rc;
   }
   return MS_OK;

@@ -32,6 +32,11 @@ class Segment(C.Structure):
                 ("ldd", C.c_longlong), ("col0", C.c_int), ("pad_", C.c_int)]
 
 
+class RowDesc(C.Structure):
+    _fields_ = [("lines", C.c_longlong), ("width", C.c_int), ("c_src", C.c_int), ("c_dst", C.c_int),
+                ("pad_w", C.c_int)]
+
+
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
 _SIGS = {
     "ms_abi_version": ([], C.c_int),
@@ -40,8 +45,8 @@ _SIGS = {
     "ms_policy_select": ([_P, _P, _P, _I, _P, C.c_int64, _D, _I, _P, _P], C.c_int),
     "ms_compact_index": ([_P, _I, _I, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_gather_rows": ([_P, _LL, _P, _P, _P, _I, _P, _P], C.c_int),
-    "ms_gather_rows_pad": ([_P, _LL, _I, _I, _P, _P, _P, _I, _P, _P], C.c_int),
-    "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_gather_rows_pad": ([_P, _LL, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P], C.c_int),
+    "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_gemm_plan_dense": ([_P, _P, _I, _I, _LL, _P, _I, _I, _I, _P, _I, _I, _P, _LL, _I, _I, _P],
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,

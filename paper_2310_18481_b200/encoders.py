@@ -37,6 +37,7 @@ N_VERBS, N_NOUNS = 97, 300
 N_CLASSES = N_VERBS + N_NOUNS
 FUSION_HIDDEN = 512
 SEGMENTS = 3
+CONV1_PAD = 3  # conv1 is 7x7/2 pad 3; its input is stored W-padded by this much
 
 # name, 1x1, 3x3 reduce, 3x3, double-3x3 reduce, double-3x3, pool kind, pool proj, stride
 # (TSN's Caffe BN-Inception: 4c 1x1=128, 4d 1x1=64 so every 4x block emits 576)
@@ -211,16 +212,14 @@ def pack_conv_weight(w):
 
 
 def pack_smallc_weight(w, cpad: int):
-    """[cout, cin, k, k] -> [cout, ceil64(k*k*cpad)]: K ordered (tap, channel)
-    with channels zero-padded to ``cpad`` (MODE_CONV_SMALLC's K order)."""
+    """[cout, cin, kh, kw] -> [cout, kh * 8 * cpad]: K ordered (kh, window
+    pixel j < 8, channel) with channels zero-padded to ``cpad`` and taps
+    j >= kw zero (MODE_CONV_SMALLC's K order)."""
     import torch
-    cout, cin, k, _ = w.shape
-    kk = k * k * cpad
-    out = torch.zeros(cout, -(-kk // 64) * 64, dtype=torch.bfloat16)
-    wp = torch.zeros(cout, cpad, k, k, dtype=torch.bfloat16)
-    wp[:, :cin] = w
-    out[:, :kk] = wp.permute(0, 2, 3, 1).reshape(cout, kk)
-    return out.contiguous()
+    cout, cin, kh, kw = w.shape
+    wp = torch.zeros(cout, kh, 8, cpad, dtype=torch.bfloat16)
+    wp[:, :, :kw, :cin] = w.permute(0, 2, 3, 1)
+    return wp.reshape(cout, kh * 8 * cpad).contiguous()
 
 
 def pack_im2col_weight(w, k_pad: int):
@@ -351,7 +350,8 @@ class BNInceptionEncoder:
         self.td2 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.tp = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.out = torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d)
-        self.x = torch.zeros(n_img, size, size, self.mod.cpad, dtype=bf, device=d)
+        # conv1 input: W-padded by CONV1_PAD zero pixels per side (the gather pads)
+        self.x = torch.zeros(n_img, size, size + 2 * CONV1_PAD, self.mod.cpad, dtype=bf, device=d)
 
     def program(self, n_req: int):
         if n_req in self._programs:

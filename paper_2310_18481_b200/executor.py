@@ -29,8 +29,8 @@ from __future__ import annotations
 import numpy as np
 
 from . import device as dv
-from .encoders import (FEAT_DIM, SEGMENTS, TBN_MODALITIES, BNInceptionEncoder, FusionHead,
-                       MLPEncoder)
+from .encoders import (CONV1_PAD, FEAT_DIM, SEGMENTS, TBN_MODALITIES, BNInceptionEncoder,
+                       FusionHead, MLPEncoder)
 
 
 def request_masks(parts, size: int) -> np.ndarray:
@@ -52,9 +52,10 @@ class MaskedModel:
     """Encoders + fusion head + resident input pool + compaction buffers."""
 
     def __init__(self, encoders, head, pools, rows, max_req: int, device="cuda"):
-        """``rows[k] = (pixels, c_src, c_dst)``: one request of modality k is
-        ``pixels`` pixels of ``c_src`` channels in the pool and ``c_dst``
-        channels in the encoder's input (the gather zero-pads)."""
+        """``rows[k] = (lines, width, c_src, c_dst, pad_w)``: one request of
+        modality k is ``lines`` x ``width`` pixels of ``c_src`` channels in the
+        pool; in the encoder's input each pixel has ``c_dst`` channels and each
+        line ``pad_w`` zero pixels on both ends (the gather pads)."""
         import torch
         self.torch = torch
         self.dev = torch.device(device)
@@ -62,7 +63,7 @@ class MaskedModel:
         self.head = head
         self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
         self.rows = [tuple(int(v) for v in r) for r in rows]
-        self.row_bytes = [px * cs * 2 for px, cs, _ in self.rows]  # pool (source) bytes
+        self.row_bytes = [ln * w * cs * 2 for ln, w, cs, _, _ in self.rows]  # pool (source) bytes
         self.K = len(encoders)
         self.max_req = max_req
         K, n = self.K, max_req
@@ -78,9 +79,7 @@ class MaskedModel:
         import ctypes
         self._X = (ctypes.c_void_p * K)(*[p.data_ptr() for p in pools])
         self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
-        self._PX = (ctypes.c_longlong * K)(*[r[0] for r in self.rows])
-        self._CS = (ctypes.c_int32 * K)(*[r[1] for r in self.rows])
-        self._CD = (ctypes.c_int32 * K)(*[r[2] for r in self.rows])
+        self._ROWS = (dv.RowDesc * K)(*[dv.RowDesc(*r) for r in self.rows])
         self._graphs = {}
         self.use_graphs = True
         self.parallel_modalities = True
@@ -113,8 +112,8 @@ class MaskedModel:
     # -- device pass ------------------------------------------------------
     def _compact(self, n: int):
         L = dv.lib()
-        dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._PX, self._CS,
-                              self._CD, self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
+        dv.check(L.ms_compact(self.mask_d.data_ptr(), n, self.K, self._X, self._ROWS,
+                              self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
                               self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
 
@@ -211,7 +210,8 @@ class MaskedModel:
         channels) + written (padded channels), + 2N mask bytes + 4*sum N_k
         index bytes."""
         counts = self.counts_for(np.asarray(masks))
-        rows = sum(2 * px * (cs + cd) * c for (px, cs, cd), c in zip(self.rows, counts))
+        rows = sum(2 * ln * (w * cs + (w + 2 * pw) * cd) * c
+                   for (ln, w, cs, cd, pw), c in zip(self.rows, counts))
         return rows + 2 * len(masks) + 4 * sum(counts)
 
 
@@ -229,7 +229,7 @@ def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_se
         # compact NHWC (real channels); the compaction gather pads to m.cpad
         pools.append(torch.randn((n_slots, segments, m.size, m.size, m.channels), generator=g,
                                  device=device).to(torch.bfloat16))
-        rows.append((segments * m.size * m.size, m.channels, m.cpad))
+        rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 
@@ -247,7 +247,7 @@ def build_mlp_model(in_dims, max_req: int, n_slots: int, seeds=(201, 202, 203),
         p = torch.zeros(n_slots, width, dtype=torch.bfloat16, device=device)
         p[:, :d] = torch.randn(n_slots, d, generator=g, device=device).to(torch.bfloat16)
         pools.append(p)
-        rows.append((1, width, width))
+        rows.append((1, 1, width, width, 0))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 

@@ -254,15 +254,15 @@ def test_pool_im2col_segment_mean(dev):
     (5, 224, 3, 8, (1, 8, 16)),
 ])
 def test_conv_small_channel_direct_vs_torch(dev, n, H, Cin, Cpad, tile):
-    """7x7/2 first-layer conv read straight from 8-channel-padded NHWC frames
-    (MODE_CONV_SMALLC: 8 no-swizzle TMA boxes per K block)."""
+    """7x7/2 first-layer conv read straight from channel-padded, W-padded NHWC
+    frames (MODE_CONV_SMALLC: one overlapping-stride 5-D TMA box per K block)."""
     from paper_2310_18481_b200.encoders import pack_smallc_weight
     g = torch.Generator().manual_seed(H + Cin)
     x = _bf(torch.randn(n, Cin, H, H, generator=g))
     w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
     b = torch.randn(64, generator=g) * 0.1
-    X = torch.zeros(n, H, H, Cpad, dtype=torch.bfloat16)
-    X[..., :Cin] = x.permute(0, 2, 3, 1)
+    X = torch.zeros(n, H, H + 6, Cpad, dtype=torch.bfloat16)  # W pre-padded by 3 per side
+    X[:, :, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
     OH = (H + 6 - 7) // 2 + 1
     D = torch.zeros(n * OH * OH, 64, dtype=torch.bfloat16, device="cuda")
     p = dev.plan_conv(X.cuda(), n, H, H, Cpad, Cpad, 7, 7, 2, 3, pack_smallc_weight(w, Cpad).cuda(), 64,
@@ -275,18 +275,19 @@ def test_conv_small_channel_direct_vs_torch(dev, n, H, Cin, Cpad, tile):
     assert ok, (err, scale)
 
 
-@pytest.mark.parametrize("c_src,c_dst", [(3, 8), (10, 16), (1, 8), (16, 16)])
-def test_gather_rows_channel_pad(dev, c_src, c_dst):
+@pytest.mark.parametrize("c_src,c_dst,pad_w", [(3, 8, 3), (10, 16, 3), (1, 8, 0), (16, 16, 2)])
+def test_gather_rows_channel_and_line_pad(dev, c_src, c_dst, pad_w):
     L = dev.lib()
-    pix = 3 * 17 * 19
-    pool = _bf(torch.randn(9, pix, c_src)).cuda()
+    lines, width = 3 * 17, 19
+    pool = _bf(torch.randn(9, lines, width, c_src)).cuda()
     idx = torch.tensor([4, 0, 7], dtype=torch.int32, device="cuda")
     slot = torch.tensor([8, 7, 6, 5, 4, 3, 2, 1, 0], dtype=torch.int32, device="cuda")
     count = torch.tensor([3], dtype=torch.int32, device="cuda")
-    dst = torch.full((3, pix, c_dst), 7.0, dtype=torch.bfloat16, device="cuda")
-    dev.check(L.ms_gather_rows_pad(dev.ptr(pool), pix, c_src, c_dst, dev.ptr(slot), dev.ptr(idx),
-                                   dev.ptr(count), 3, dev.ptr(dst), dev.stream_ptr()), "gather_pad")
+    dst = torch.full((3, lines, width + 2 * pad_w, c_dst), 7.0, dtype=torch.bfloat16, device="cuda")
+    dev.check(L.ms_gather_rows_pad(dev.ptr(pool), lines, width, c_src, c_dst, pad_w, dev.ptr(slot),
+                                   dev.ptr(idx), dev.ptr(count), 3, dev.ptr(dst), dev.stream_ptr()), "gather_pad")
     torch.cuda.synchronize()
     src = pool[slot[idx.long()].long()]
-    assert torch.equal(dst[..., :c_src], src)
-    assert torch.count_nonzero(dst[..., c_src:]) == 0
+    assert torch.equal(dst[:, :, pad_w:pad_w + width, :c_src], src)
+    dst[:, :, pad_w:pad_w + width, :c_src] = 0
+    assert torch.count_nonzero(dst) == 0
