@@ -54,8 +54,9 @@ typedef struct MsSegment {
   void* ptr;     /* destination base */
   long long ldd; /* destination row stride (elements) */
   int col0;      /* destination column of n_begin */
-  int pad_;
+  int flags;     /* MS_SEG_NO_RELU: store this segment pre-activation */
 } MsSegment;
+#define MS_SEG_NO_RELU 1
 
 int ms_abi_version(void);
 const char* ms_last_error(void);
@@ -127,6 +128,12 @@ int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, i
 /* max (is_max=1) or average (count includes padding) pooling, k x k */
 int ms_pool2d(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride,
               int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, void* stream);
+/* as ms_pool2d, then y = act(pool + bias[c]) (bias fp32 or NULL, relu 0/1):
+ * used for avgpool(proj(x)) + bias == proj(avgpool(x)) + bias, exact for
+ * count-include-pad averaging, so the projection runs at the narrow width */
+int ms_pool2d_ex(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride,
+                 int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0,
+                 const float* bias, int relu, void* stream);
 /* conv im2col for small-channel first layers: out[pixel, (kh*KW+kw)*C + c],
  * zero for columns >= KH*KW*C up to K_pad */
 int ms_im2col(const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride, int pad,
@@ -139,6 +146,9 @@ int ms_segment_mean(const void* X, int n_req, int S, int HW, int C, void* Y, lon
 int ms_op_gemm(void* op, const void* plan);
 int ms_op_pool2d(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k,
                  int stride, int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0);
+int ms_op_pool2d_ex(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k,
+                    int stride, int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0,
+                    const float* bias, int relu);
 int ms_op_im2col(void* op, const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride,
                  int pad, void* out, int K_pad);
 int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld);

@@ -55,7 +55,7 @@ struct Seg {
   void* ptr;
   long long ldd;
   int col0;
-  int pad_;
+  int flags;  // MS_SEG_NO_RELU
 };
 
 struct GemmParams {
@@ -292,14 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         void* seg_ptr = p.seg[0].ptr;
         long long seg_ld = p.seg[0].ldd;
         int seg_off = p.seg[0].col0 - p.seg[0].n_begin;
+        int seg_flags = p.seg[0].flags;
 #pragma unroll
         for (int g = 1; g < 4; ++g) {
           if (g < p.nseg && nb >= p.seg[g].n_begin) {
             seg_ptr = p.seg[g].ptr;
             seg_ld = p.seg[g].ldd;
             seg_off = p.seg[g].col0 - p.seg[g].n_begin;
+            seg_flags = p.seg[g].flags;
           }
         }
+        const bool relu = p.relu && !(seg_flags & MS_SEG_NO_RELU);
         const long long base = out_row * seg_ld + seg_off + nb;
         const bool full_chunk = nb + 32 <= p.N;
         const float* bch = sbias + nb;
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             float x = __uint_as_float(v[j]) + (nb + j < p.N ? bch[j] : 0.0f);
-            if (p.relu) x = fmaxf(x, 0.0f);
+            if (relu) x = fmaxf(x, 0.0f);
             if (nb + j < p.N) dst[j] = x;
           }
         } else {
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) {
             float a = __uint_as_float(v[2 * j]) + bch[2 * j];
             float b = __uint_as_float(v[2 * j + 1]) + bch[2 * j + 1];
-            if (p.relu) {
+            if (relu) {
               a = fmaxf(a, 0.0f);
               b = fmaxf(b, 0.0f);
             }
@@ -432,7 +435,7 @@ static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D
   }
   p.nseg = nseg;
   for (int i = 0; i < nseg && i < 4; ++i)
-    p.seg[i] = Seg{segs[i].n_begin, segs[i].n_end, segs[i].ptr, segs[i].ldd, segs[i].col0, 0};
+    p.seg[i] = Seg{segs[i].n_begin, segs[i].n_end, segs[i].ptr, segs[i].ldd, segs[i].col0, segs[i].flags};
 }
 
 static int launch_plan(const GemmPlan* P, cudaStream_t stream) {

@@ -32,7 +32,8 @@ int check_launch(const char* what) {
 // one thread = one output pixel x 8 channels (16-B vectors)
 __global__ void pool2d_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H, int W, int C,
                               long long xcs, int k, int stride, int pad, int OH, int OW, int is_max,
-                              __nv_bfloat16* __restrict__ Y, long long ycs, int ycol0) {
+                              __nv_bfloat16* __restrict__ Y, long long ycs, int ycol0,
+                              const float* __restrict__ bias, int relu) {
   const int cg = C / 8;
   const long long total = (long long)n_img * OH * OW * cg;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -62,11 +63,18 @@ __global__ void pool2d_kernel(const __nv_bfloat16* __restrict__ X, int n_img, in
       }
     }
     const float scale = is_max ? 1.0f : 1.0f / (float)(k * k);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = acc[j] * scale;
+      if (bias != nullptr) v += __ldg(bias + g * 8 + j);
+      if (relu) v = fmaxf(v, 0.0f);
+      acc[j] = v;
+    }
     uint4 o;
-    o.x = pack_bf16x2(acc[0] * scale, acc[1] * scale);
-    o.y = pack_bf16x2(acc[2] * scale, acc[3] * scale);
-    o.z = pack_bf16x2(acc[4] * scale, acc[5] * scale);
-    o.w = pack_bf16x2(acc[6] * scale, acc[7] * scale);
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
     *reinterpret_cast<uint4*>(Y + pix * ycs + ycol0 + g * 8) = o;
   }
 }
@@ -173,6 +181,8 @@ struct PoolArgs {
   void* Y;
   long long xcs, ycs;
   int n_img, H, W, C, k, stride, pad, ceil_mode, is_max, ycol0;
+  const float* bias;
+  int relu;
 };
 struct Im2colArgs {
   const void* X;
@@ -206,7 +216,7 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const long long work = (long long)a.n_img * OH * OW * (a.C / 8);
   pool2d_kernel<<<grid_for(work, 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H, a.W, a.C, a.xcs, a.k, a.stride, a.pad, OH, OW,
-      a.is_max, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0);
+      a.is_max, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0, a.bias, a.relu);
   return check_launch("pool2d_kernel");
 }
 
@@ -246,7 +256,14 @@ int ms_device_sync(void) {
 
 int ms_pool2d(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride, int pad,
               int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, void* stream) {
-  PoolArgs a{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0};
+  PoolArgs a{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0, nullptr, 0};
+  return run_pool(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ms_pool2d_ex(const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride, int pad,
+                 int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, const float* bias, int relu,
+                 void* stream) {
+  PoolArgs a{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0, bias, relu};
   return run_pool(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -276,7 +293,19 @@ int ms_op_pool2d(void* op, const void* X, int n_img, int H, int W, int C, long l
   Op* o = reinterpret_cast<Op*>(op);
   memset(o, 0, sizeof(Op));
   o->kind = OP_POOL;
-  o->u.pool = PoolArgs{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0};
+  o->u.pool = PoolArgs{X, Y, x_cstride, y_cstride, n_img, H, W, C, k, stride, pad, ceil_mode, is_max, y_col0,
+                       nullptr, 0};
+  return MS_OK;
+}
+
+int ms_op_pool2d_ex(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k, int stride,
+                    int pad, int ceil_mode, int is_max, void* Y, long long y_cstride, int y_col0, const float* bias,
+                    int relu) {
+  int rc = ms_op_pool2d(op, X, n_img, H, W, C, x_cstride, k, stride, pad, ceil_mode, is_max, Y, y_cstride, y_col0);
+  if (rc) return rc;
+  Op* o = reinterpret_cast<Op*>(op);
+  o->u.pool.bias = bias;
+  o->u.pool.relu = relu;
   return MS_OK;
 }
 

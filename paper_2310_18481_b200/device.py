@@ -27,9 +27,12 @@ class DeviceError(ValueError):
     """A C-ABI call returned a nonzero status."""
 
 
+SEG_NO_RELU = 1
+
+
 class Segment(C.Structure):
     _fields_ = [("n_begin", C.c_int), ("n_end", C.c_int), ("ptr", C.c_void_p),
-                ("ldd", C.c_longlong), ("col0", C.c_int), ("pad_", C.c_int)]
+                ("ldd", C.c_longlong), ("col0", C.c_int), ("flags", C.c_int)]
 
 
 class RowDesc(C.Structure):
@@ -56,6 +59,9 @@ _SIGS = {
     "ms_gemm_run": ([_P, _P], C.c_int),
     "ms_gemm_plan_info": ([_P, _P, _P, _P, _P], C.c_int),
     "ms_pool2d": ([_P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P], C.c_int),
+    "ms_pool2d_ex": ([_P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P, _I, _P], C.c_int),
+    "ms_op_pool2d_ex": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P, _I],
+                        C.c_int),
     "ms_im2col": ([_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P], C.c_int),
     "ms_segment_mean": ([_P, _I, _I, _I, _I, _P, _LL, _P], C.c_int),
     "ms_op_gemm": ([_P, _P], C.c_int),
@@ -203,8 +209,9 @@ def _segments(segs):
     if not segs:
         return 0, None
     arr = (Segment * len(segs))()
-    for i, (nb, ne, t, ldd, col0) in enumerate(segs):
-        arr[i] = Segment(nb, ne, ptr(t), ldd, col0, 0)
+    for i, sg in enumerate(segs):
+        nb, ne, t, ldd, col0 = sg[:5]
+        arr[i] = Segment(nb, ne, ptr(t), ldd, col0, sg[5] if len(sg) > 5 else 0)
     return len(segs), arr
 
 
@@ -269,10 +276,11 @@ class Program:
         self.ops.append(("gemm", plan))
         self.keep.append(plan)
 
-    def pool(self, X, n_img, H, W, C_, x_cs, k, stride, pad, ceil_mode, is_max, Y, y_cs, y_col0):
+    def pool(self, X, n_img, H, W, C_, x_cs, k, stride, pad, ceil_mode, is_max, Y, y_cs, y_col0,
+             bias=None, relu=False):
         self.ops.append(("pool", (ptr(X), n_img, H, W, C_, x_cs, k, stride, pad, int(ceil_mode),
-                                  int(is_max), ptr(Y), y_cs, y_col0)))
-        self.keep += [X, Y]
+                                  int(is_max), ptr(Y), y_cs, y_col0, ptr(bias), int(relu))))
+        self.keep += [X, Y, bias]
 
     def im2col(self, X, n_img, H, W, C_, KH, KW, stride, pad, out, K_pad):
         self.ops.append(("im2col", (ptr(X), n_img, H, W, C_, KH, KW, stride, pad, ptr(out), K_pad)))
@@ -292,7 +300,7 @@ class Program:
             if kind == "gemm":
                 check(L.ms_op_gemm(at, a.addr), "ms_op_gemm")
             elif kind == "pool":
-                check(L.ms_op_pool2d(at, *a), "ms_op_pool2d")
+                check(L.ms_op_pool2d_ex(at, *a), "ms_op_pool2d_ex")
             elif kind == "im2col":
                 check(L.ms_op_im2col(at, *a), "ms_op_im2col")
             else:

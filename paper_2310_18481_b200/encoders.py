@@ -313,8 +313,15 @@ class BNInceptionEncoder:
                 continue
             n = L["name"]
             parts = ([n + "/1x1"] if L["c1"] else []) + [n + "/3x3_reduce", n + "/d3x3_reduce"]
+            biases = [self.b[p] for p in parts]
+            if L["pool"] == "avg":
+                # proj(avgpool(x)) == avgpool(proj(x)) for count-include-pad
+                # averaging: project at the narrow width inside the merged GEMM
+                # (bias and ReLU are applied after the pool)
+                parts.append(n + "/pool_proj")
+                biases.append(torch.zeros_like(self.b[n + "/pool_proj"]))
             self.w[n + "/merged"] = torch.cat([self.w[p] for p in parts], 0).contiguous()
-            self.b[n + "/merged"] = torch.cat([self.b[p] for p in parts], 0).contiguous()
+            self.b[n + "/merged"] = torch.cat(biases, 0).contiguous()
 
     # -- activation buffers at capacity
     def _alloc(self):
@@ -417,6 +424,11 @@ class BNInceptionEncoder:
         segs.append((col, col + c3r, T3, c3r, 0))
         segs.append((col + c3r, col + c3r + cdr, Td, cdr, 0))
         nm = col + c3r + cdr
+        fold_pool = L["pool"] == "avg"
+        if fold_pool:
+            Tq = self.tp[: pix_in * proj].view(pix_in, proj)
+            segs.append((nm, nm + proj, Tq, proj, 0, dv.SEG_NO_RELU))
+            nm += proj
         P.gemm(dv.plan_dense(Xv, self.w[name + "/merged"], self.b[name + "/merged"], Yv, M=pix_in,
                              K=cin, BN=pick_bn(nm), relu=True, segs=segs))
         tile_in = pick_conv_tile(n, h, h)
@@ -433,10 +445,12 @@ class BNInceptionEncoder:
                             self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
                             relu=True, tile=tile_out))
         pc = c1 + c3 + cd
-        if proj:
+        if fold_pool:  # avgpool of the projected (pre-bias) branch + bias + ReLU
+            P.pool(Tq, n, h, h, proj, proj, 3, 1, 1, False, False, Yv, cout, pc,
+                   bias=self.b[name + "/pool_proj"], relu=True)
+        elif proj:  # max pool does not commute with the projection
             Tp = self.tp[: pix_in * cin].view(pix_in, cin)
-            is_max = L["pool"] == "maxproj"
-            P.pool(Xv, n, h, h, cin, cin, 3, 1, 1, False, is_max, Tp, cin, 0)
+            P.pool(Xv, n, h, h, cin, cin, 3, 1, 1, False, True, Tp, cin, 0)
             P.gemm(dv.plan_dense(Tp, self.w[name + "/pool_proj"], self.b[name + "/pool_proj"], Yv,
                                  M=pix_in, K=cin, BN=pick_bn(proj), relu=True, col0=pc, ldd=cout))
         else:  # stride-2 max-pool pass-through into the concat
