@@ -101,7 +101,12 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
                int32_t* combo_offsets, int32_t* perm, void* stream);
 
 /* ---- tcgen05 GEMM plans (encoders, fusion head) -----------------------
- * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL. */
+ * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL,
+ * N <= 4096.  The `relu` argument is the epilogue activation MS_ACT_*. */
+#define MS_ACT_NONE 0
+#define MS_ACT_RELU 1
+#define MS_ACT_GELU 2
+#define MS_ACT_TANH 3
 int ms_gemm_plan_dense(void* plan, const void* A, int M, int K, long long lda, const void* W, int N,
                        int K_pad, int BN, const float* bias, int relu, int out_fp32, void* D,
                        long long ldd, int col0, int nseg, const MsSegment* segs);
@@ -121,6 +126,9 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                         int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
                         int out_fp32, void* D, long long ldd, int col0);
+/* add a bf16 residual (same row mapping as the output, row stride res_ld)
+ * after the activation: D = act(A W^T + b) + R */
+int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld);
 int ms_gemm_run(const void* plan, void* stream);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
 
@@ -142,6 +150,23 @@ int ms_im2col(const void* X, int n_img, int H, int W, int C, int KH, int KW, int
  * Y[r, C] = mean over s, p */
 int ms_segment_mean(const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld, void* stream);
 
+/* ---- transformer towers (configs[2]: ViT-B/16 image + BERT-base text) --
+ * ms_layernorm: Y[r] = LN(X[r]) * gamma + beta over C (C % 256 == 0), fp32
+ *   statistics, arbitrary row strides (e.g. only the CLS rows).
+ * ms_attention: per sequence s and head h, O = softmax(Q K^T * scale) V with
+ *   qkv rows [Q | K | V] (H*64 each), row stride ld; O rows H*64, stride ldo.
+ * ms_patchify: NHWC [n, S, S, C] -> [n*(S/P)^2, P*P*C] rows, K order (kh,kw,c).
+ * ms_vit_embed: tok[s*L] = cls + pos[0]; tok[s*L+1+p] = pe[s*(L-1)+p] + pos[1+p].
+ * ms_bert_embed: Y[t] = LN(word[ids[t]] + pos[t % L] + type0). */
+int ms_layernorm(const void* X, long long ldx, long long rows, const float* gamma, const float* beta, void* Y,
+                 long long ldy, int C, float eps, void* stream);
+int ms_attention(const void* qkv, long long ld, int L, int H, int n_seq, void* out, long long ldo, float scale,
+                 void* stream);
+int ms_patchify(const void* X, int n, int S, int C, int P, void* Y, void* stream);
+int ms_vit_embed(const void* pe, const void* cls, const void* pos, int n, int L, int D, void* tok, void* stream);
+int ms_bert_embed(const int32_t* ids, long long n_tok, int L, const void* word, const void* pos, const void* type0,
+                  const float* gamma, const float* beta, void* Y, int D, float eps, void* stream);
+
 /* ---- op programs: a whole encoder forward as one native call ---------- */
 int ms_op_gemm(void* op, const void* plan);
 int ms_op_pool2d(void* op, const void* X, int n_img, int H, int W, int C, long long x_cstride, int k,
@@ -152,6 +177,14 @@ int ms_op_pool2d_ex(void* op, const void* X, int n_img, int H, int W, int C, lon
 int ms_op_im2col(void* op, const void* X, int n_img, int H, int W, int C, int KH, int KW, int stride,
                  int pad, void* out, int K_pad);
 int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C, void* Y, long long y_ld);
+int ms_op_layernorm(void* op, const void* X, long long ldx, long long rows, const float* gamma, const float* beta,
+                    void* Y, long long ldy, int C, float eps);
+int ms_op_attention(void* op, const void* qkv, long long ld, int L, int H, int n_seq, void* out, long long ldo,
+                    float scale);
+int ms_op_patchify(void* op, const void* X, int n, int S, int C, int P, void* Y);
+int ms_op_vit_embed(void* op, const void* pe, const void* cls, const void* pos, int n, int L, int D, void* tok);
+int ms_op_bert_embed(void* op, const int32_t* ids, long long n_tok, int L, const void* word, const void* pos,
+                     const void* type0, const float* gamma, const float* beta, void* Y, int D, float eps);
 int ms_program_run(const void* ops, int n_ops, void* stream);
 
 /* ---- profiler timing (CUDA events) ------------------------------------ */

@@ -141,3 +141,91 @@ class OracleMLP:
     def logits(self, inputs, masks):
         feats = [mlp_forward(x, t) for x, t in zip(inputs, self.towers)]
         return fusion_forward(feats, masks, self.fus_w)
+
+
+# ---------------------------------------------------------------- configs[2]
+# ViT-B/16 + BERT-base two-tower.  Same rules: fp32 math,
+# bf16 rounding where the device stores (LN outputs, QKV, attention output,
+# the residual stream, MLP hidden, features).
+
+
+def _lin(x, wb, act=None):
+    w, b = wb
+    y = x @ w.float().T + b
+    if act == "gelu":
+        y = F.gelu(y)
+    elif act == "tanh":
+        y = torch.tanh(y)
+    return y
+
+
+def _ln(x, gb, eps):
+    g, b = gb
+    return F.layer_norm(x, (x.shape[-1],), g, b, eps)
+
+
+def _attn(qkv, L, H):
+    n = qkv.shape[0] // L
+    q, k, v = qkv.reshape(n, L, 3, H, 64).permute(2, 0, 3, 1, 4)
+    p = torch.softmax(q @ k.transpose(-1, -2) * 0.125, dim=-1)
+    return (p @ v).permute(0, 2, 1, 3).reshape(n * L, H * 64)
+
+
+def vit_forward(images, W):
+    """images [n, 224, 224, 3] NHWC -> CLS features [n, 768] (bf16-rounded)."""
+    from paper_2310_18481_b200.towers import N_LAYERS, N_PATCHES, PATCH, VIT_TOKENS
+    n = images.shape[0]
+    G = images.shape[1] // PATCH
+    p = images.float().reshape(n, G, PATCH, G, PATCH, 3).permute(0, 1, 3, 2, 4, 5)
+    p = p.reshape(n * N_PATCHES, PATCH * PATCH * 3)
+    pe = _bf(_lin(p, W["patch"])).reshape(n, N_PATCHES, -1)
+    x = torch.cat([W["cls"].float().expand(n, 1, -1), pe], 1) + W["pos"].float()
+    x = _bf(x).reshape(n * VIT_TOKENS, -1)
+    for i in range(N_LAYERS):
+        h = _bf(_ln(x, W[f"{i}.ln1"], 1e-6))
+        a = _bf(_attn(_bf(_lin(h, W[f"{i}.qkv"])), VIT_TOKENS, 12))
+        x = _bf(x + _lin(a, W[f"{i}.proj"]))
+        h = _bf(_ln(x, W[f"{i}.ln2"], 1e-6))
+        m = _bf(_lin(h, W[f"{i}.fc1"], "gelu"))
+        x = _bf(x + _lin(m, W[f"{i}.fc2"]))
+    cls = x.reshape(n, VIT_TOKENS, -1)[:, 0]
+    return _bf(_ln(cls, W["ln_f"], 1e-6))
+
+
+def bert_forward(ids, W):
+    """ids [n, 40] int -> pooled [CLS] features [n, 768] (bf16-rounded)."""
+    from paper_2310_18481_b200.towers import N_LAYERS, TEXT_TOKENS
+    n = ids.shape[0]
+    e = W["word"].float()[ids.long()] + W["pos"].float()[:TEXT_TOKENS] + W["type"].float()[0]
+    x = _bf(_ln(e, W["ln_e"], 1e-12)).reshape(n * TEXT_TOKENS, -1)
+    for i in range(N_LAYERS):
+        a = _bf(_attn(_bf(_lin(x, W[f"{i}.qkv"])), TEXT_TOKENS, 12))
+        t = _bf(x + _lin(a, W[f"{i}.proj"]))
+        x = _bf(_ln(t, W[f"{i}.ln1"], 1e-12))
+        m = _bf(_lin(x, W[f"{i}.fc1"], "gelu"))
+        t = _bf(x + _lin(m, W[f"{i}.fc2"]))
+        x = _bf(_ln(t, W[f"{i}.ln2"], 1e-12))
+    cls = x.reshape(n, TEXT_TOKENS, -1)[:, 0]
+    return _bf(_lin(cls, W["pooler"], "tanh"))
+
+
+class OracleVQA:
+    """configs[2] on the CPU: ViT + BERT towers, masked fusion (bit 0 image,
+    bit 1 text)."""
+
+    def __init__(self, seeds=(301, 302), fusion_seed: int = 399):
+        from paper_2310_18481_b200.towers import VQA_CLASSES, bert_weights, vit_weights
+        self.vit_w = vit_weights(seeds[0])
+        self.bert_w = bert_weights(seeds[1])
+        self.fus_w = fusion_weights(2, 768, fusion_seed, VQA_CLASSES)
+
+    def logits(self, images, ids, masks):
+        n = masks.shape[0]
+        feats = [torch.zeros(n, 768), torch.zeros(n, 768)]
+        sel = torch.nonzero(masks & 1).flatten()
+        if sel.numel():
+            feats[0][sel] = vit_forward(images[sel], self.vit_w)
+        sel = torch.nonzero((masks >> 1) & 1).flatten()
+        if sel.numel():
+            feats[1][sel] = bert_forward(ids[sel], self.bert_w)
+        return fusion_forward(feats, masks, self.fus_w)

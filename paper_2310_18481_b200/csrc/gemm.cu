@@ -34,7 +34,7 @@ namespace mosel {
 
 constexpr int kEpiWarps = 8;                  // 2 per TMEM lane quarter
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // TMA + MMA + epilogue warps
-constexpr int kMaxBias = 1024;
+constexpr int kMaxBias = 4096;  // staged bias floats (N <= 4096)
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
@@ -75,9 +75,11 @@ struct GemmParams {
   const __nv_bfloat16* feat[4];
   const int32_t* inv;  // [n_mod, inv_ld]
   int inv_ld, feat_dim, n_mod;
-  // epilogue
+  // epilogue: v = act(acc + bias[n]) (+ residual[row, n])
   const float* bias;
-  int relu, out_fp32, nseg, pad_;
+  int relu, out_fp32, nseg, pad_;  // relu: activation MS_ACT_* (1 = ReLU for compatibility)
+  const __nv_bfloat16* residual;   // same row mapping as the output, row stride res_ld
+  long long res_ld;
   Seg seg[4];
 };
 
@@ -87,6 +89,15 @@ struct alignas(64) GemmPlan {
   GemmParams p;
   int grid_x, grid_y, smem_bytes, tmem_cols;
 };
+
+__device__ __forceinline__ float activate(float x, int act) {
+  switch (act) {
+    case MS_ACT_RELU: return fmaxf(x, 0.0f);
+    case MS_ACT_GELU: return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+    case MS_ACT_TANH: return tanhf(x);
+    default: return x;
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             seg_flags = p.seg[g].flags;
           }
         }
-        const bool relu = p.relu && !(seg_flags & MS_SEG_NO_RELU);
+        const int act = (seg_flags & MS_SEG_NO_RELU) ? 0 : p.relu;
         const long long base = out_row * seg_ld + seg_off + nb;
         const bool full_chunk = nb + 32 <= p.N;
         const float* bch = sbias + nb;
@@ -310,20 +321,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           float* dst = reinterpret_cast<float*>(seg_ptr) + base;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            float x = __uint_as_float(v[j]) + (nb + j < p.N ? bch[j] : 0.0f);
-            if (relu) x = fmaxf(x, 0.0f);
+            float x = activate(__uint_as_float(v[j]) + (nb + j < p.N ? bch[j] : 0.0f), act);
             if (nb + j < p.N) dst[j] = x;
           }
         } else {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(seg_ptr) + base;
+          uint32_t res[16];
+          if (p.residual != nullptr && full_chunk) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(p.residual + out_row * p.res_ld + nb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 q4 = r4[j];
+              res[4 * j] = q4.x;
+              res[4 * j + 1] = q4.y;
+              res[4 * j + 2] = q4.z;
+              res[4 * j + 3] = q4.w;
+            }
+          }
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            float a = __uint_as_float(v[2 * j]) + bch[2 * j];
-            float b = __uint_as_float(v[2 * j + 1]) + bch[2 * j + 1];
-            if (relu) {
-              a = fmaxf(a, 0.0f);
-              b = fmaxf(b, 0.0f);
+            float a = activate(__uint_as_float(v[2 * j]) + bch[2 * j], act);
+            float b = activate(__uint_as_float(v[2 * j + 1]) + bch[2 * j + 1], act);
+            if (p.residual != nullptr && full_chunk) {
+              const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&res[j]);
+              a += __bfloat162float(r2.x);
+              b += __bfloat162float(r2.y);
             }
             pk[j] = pack_bf16x2(a, b);
           }
@@ -400,7 +423,7 @@ static int sm_count() {
 static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int BN, int num_kb, int grid_x) {
   GemmParams& p = P->p;
   if (BN % 32 != 0 || BN < 32 || BN > 256) return set_error(MS_ERR_INVALID, "BN must be a multiple of 32 in [32, 256]");
-  if (p.N > kMaxBias) return set_error(MS_ERR_INVALID, "N exceeds the staged-bias capacity (1024)");
+  if (p.N > kMaxBias) return set_error(MS_ERR_INVALID, "N exceeds the staged-bias capacity (4096)");
   if (K_pad % kBK != 0) return set_error(MS_ERR_INVALID, "weight K must be padded to a multiple of 64");
   cuuint64_t dims[2] = {(cuuint64_t)K_pad, (cuuint64_t)N_rows_w};
   cuuint64_t strides[1] = {(cuuint64_t)K_pad * 2};
@@ -412,11 +435,12 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   p.num_kb = num_kb;
   p.b_bytes = BN * kBK * 2;
   const int per_stage = kABytes + p.b_bytes;
-  int stages = (196 * 1024) / per_stage;
+  int stages = (200 * 1024 - kMaxBias * 4) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
   P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + kMaxBias * 4;
+  if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
   P->grid_x = tiles < sm_count() ? tiles : sm_count();
@@ -573,6 +597,16 @@ int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv,
   set_segments(p, 0, nullptr, D, ldd, col0);
   const int K = n_mod * feat_dim;
   return finish_plan(P, W, K, N, BN, K / kBK, (M + kBM - 1) / kBM);
+}
+
+int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  if (P->p.out_fp32 || P->p.nseg > 1 || (res_ld * 2) % 16 != 0)
+    return set_error(MS_ERR_INVALID, "residual needs a bf16 single-segment output and res_ld*2 % 16 == 0");
+  P->p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  P->p.res_ld = res_ld;
+  return MS_OK;
 }
 
 int ms_gemm_run(const void* plan, void* stream) {

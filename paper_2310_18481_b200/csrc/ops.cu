@@ -174,7 +174,10 @@ static int grid_for(long long work, int threads) {
 }
 
 // ---------------------------------------------------------- op programs
-enum OpKind : int { OP_GEMM = 1, OP_POOL = 2, OP_IM2COL = 3, OP_SEGMEAN = 4 };
+enum OpKind : int {
+  OP_GEMM = 1, OP_POOL = 2, OP_IM2COL = 3, OP_SEGMEAN = 4,
+  OP_LAYERNORM = 5, OP_ATTENTION = 6, OP_PATCHIFY = 7, OP_VIT_EMBED = 8, OP_BERT_EMBED = 9
+};
 
 struct PoolArgs {
   const void* X;
@@ -196,6 +199,41 @@ struct SegArgs {
   int n_req, S, HW, C;
 };
 
+struct LnArgs {
+  const void* X;
+  void* Y;
+  const float *gamma, *beta;
+  long long ldx, rows, ldy;
+  int C;
+  float eps;
+};
+struct AttnArgs {
+  const void* qkv;
+  void* out;
+  long long ld, ldo;
+  int L, H, n_seq;
+  float scale;
+};
+struct PatchArgs {
+  const void* X;
+  void* Y;
+  int n, S, C, P;
+};
+struct VitEmbedArgs {
+  const void *pe, *cls, *pos;
+  void* tok;
+  int n, L, D;
+};
+struct BertEmbedArgs {
+  const int32_t* ids;
+  const void *word, *pos, *type0;
+  const float *gamma, *beta;
+  void* Y;
+  long long n_tok;
+  int L, D;
+  float eps;
+};
+
 struct alignas(64) Op {
   int kind;
   int pad_[15];
@@ -204,6 +242,11 @@ struct alignas(64) Op {
     PoolArgs pool;
     Im2colArgs im2col;
     SegArgs seg;
+    LnArgs ln;
+    AttnArgs attn;
+    PatchArgs patch;
+    VitEmbedArgs vit;
+    BertEmbedArgs bert;
   } u;
 };
 static_assert(sizeof(Op) <= MS_OP_BYTES && MS_OP_BYTES % 64 == 0, "MS_OP_BYTES too small / misaligned");
@@ -328,6 +371,46 @@ int ms_op_segment_mean(void* op, const void* X, int n_req, int S, int HW, int C,
   return MS_OK;
 }
 
+static Op* op_reset(void* op, int kind) {
+  Op* o = reinterpret_cast<Op*>(op);
+  memset(o, 0, sizeof(Op));
+  o->kind = kind;
+  return o;
+}
+
+int ms_op_layernorm(void* op, const void* X, long long ldx, long long rows, const float* gamma, const float* beta,
+                    void* Y, long long ldy, int C, float eps) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  op_reset(op, OP_LAYERNORM)->u.ln = LnArgs{X, Y, gamma, beta, ldx, rows, ldy, C, eps};
+  return MS_OK;
+}
+
+int ms_op_attention(void* op, const void* qkv, long long ld, int L, int H, int n_seq, void* out, long long ldo,
+                    float scale) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  op_reset(op, OP_ATTENTION)->u.attn = AttnArgs{qkv, out, ld, ldo, L, H, n_seq, scale};
+  return MS_OK;
+}
+
+int ms_op_patchify(void* op, const void* X, int n, int S, int C, int P, void* Y) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  op_reset(op, OP_PATCHIFY)->u.patch = PatchArgs{X, Y, n, S, C, P};
+  return MS_OK;
+}
+
+int ms_op_vit_embed(void* op, const void* pe, const void* cls, const void* pos, int n, int L, int D, void* tok) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  op_reset(op, OP_VIT_EMBED)->u.vit = VitEmbedArgs{pe, cls, pos, tok, n, L, D};
+  return MS_OK;
+}
+
+int ms_op_bert_embed(void* op, const int32_t* ids, long long n_tok, int L, const void* word, const void* pos,
+                     const void* type0, const float* gamma, const float* beta, void* Y, int D, float eps) {
+  if (!op) return set_error(MS_ERR_INVALID, "null op");
+  op_reset(op, OP_BERT_EMBED)->u.bert = BertEmbedArgs{ids, word, pos, type0, gamma, beta, Y, n_tok, L, D, eps};
+  return MS_OK;
+}
+
 int ms_program_run(const void* ops, int n_ops, void* stream) {
   const unsigned char* base = reinterpret_cast<const unsigned char*>(ops);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -340,6 +423,27 @@ int ms_program_run(const void* ops, int n_ops, void* stream) {
       case OP_POOL: rc = run_pool(o.u.pool, st); break;
       case OP_IM2COL: rc = run_im2col(o.u.im2col, st); break;
       case OP_SEGMEAN: rc = run_segmean(o.u.seg, st); break;
+      case OP_LAYERNORM: {
+        const LnArgs& a = o.u.ln;
+        rc = run_layernorm(a.X, a.ldx, a.rows, a.gamma, a.beta, a.Y, a.ldy, a.C, a.eps, st);
+        break;
+      }
+      case OP_ATTENTION: {
+        const AttnArgs& a = o.u.attn;
+        rc = run_attention(a.qkv, a.ld, a.L, a.H, a.n_seq, a.out, a.ldo, a.scale, st);
+        break;
+      }
+      case OP_PATCHIFY: rc = run_patchify(o.u.patch.X, o.u.patch.n, o.u.patch.S, o.u.patch.C, o.u.patch.P, o.u.patch.Y, st); break;
+      case OP_VIT_EMBED: {
+        const VitEmbedArgs& a = o.u.vit;
+        rc = run_vit_embed(a.pe, a.cls, a.pos, a.n, a.L, a.D, a.tok, st);
+        break;
+      }
+      case OP_BERT_EMBED: {
+        const BertEmbedArgs& a = o.u.bert;
+        rc = run_bert_embed(a.ids, a.n_tok, a.L, a.word, a.pos, a.type0, a.gamma, a.beta, a.Y, a.D, a.eps, st);
+        break;
+      }
       default: rc = set_error(MS_ERR_INVALID, "unknown op kind");
     }
     if (rc != MS_OK) return rc;

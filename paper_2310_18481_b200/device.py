@@ -74,6 +74,17 @@ _SIGS = {
     "ms_event_record": ([_P, _P], C.c_int),
     "ms_event_elapsed_us": ([_P, _P, _P], C.c_int),
     "ms_event_query": ([_P], C.c_int),
+    "ms_gemm_plan_set_residual": ([_P, _P, _LL], C.c_int),
+    "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
+    "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),
+    "ms_patchify": ([_P, _I, _I, _I, _I, _P, _P], C.c_int),
+    "ms_vit_embed": ([_P, _P, _P, _I, _I, _I, _P, _P], C.c_int),
+    "ms_bert_embed": ([_P, _LL, _I, _P, _P, _P, _P, _P, _P, _I, C.c_float, _P], C.c_int),
+    "ms_op_layernorm": ([_P, _P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float], C.c_int),
+    "ms_op_attention": ([_P, _P, _LL, _I, _I, _I, _P, _LL, C.c_float], C.c_int),
+    "ms_op_patchify": ([_P, _P, _I, _I, _I, _I, _P], C.c_int),
+    "ms_op_vit_embed": ([_P, _P, _P, _P, _I, _I, _I, _P], C.c_int),
+    "ms_op_bert_embed": ([_P, _P, _LL, _I, _P, _P, _P, _P, _P, _P, _I, C.c_float], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -215,18 +226,26 @@ def _segments(segs):
     return len(segs), arr
 
 
+ACT_NONE, ACT_RELU, ACT_GELU, ACT_TANH = 0, 1, 2, 3
+
+
 def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col0=0, ldd=None,
-               segs=None, M=None):
-    """D = act(A[M,K] @ W[N,K_pad]^T + bias); A row stride = A.stride(0)."""
+               segs=None, M=None, act=None, residual=None, lda=None):
+    """D = act(A[M,K] @ W[N,K_pad]^T + bias) (+ residual); A row stride =
+    ``lda`` or A.stride(0).  ``act`` is ACT_* (``relu=True`` == ACT_RELU)."""
     p = GemmPlan()
     m = A.shape[0] if M is None else M
     k = A.shape[1] if K is None else K
     nseg, sarr = _segments(segs)
-    check(lib().ms_gemm_plan_dense(p.addr, ptr(A), m, k, A.stride(0), ptr(W), W.shape[0], W.shape[1],
-                                   BN, ptr(bias), int(relu), int(out_fp32), ptr(D),
+    a = int(relu) if act is None else int(act)
+    check(lib().ms_gemm_plan_dense(p.addr, ptr(A), m, k, A.stride(0) if lda is None else lda, ptr(W),
+                                   W.shape[0], W.shape[1], BN, ptr(bias), a, int(out_fp32), ptr(D),
                                    D.stride(0) if ldd is None else ldd, col0, nseg, sarr),
           "ms_gemm_plan_dense")
-    p.keep = [A, W, bias, D, segs]
+    if residual is not None:
+        check(lib().ms_gemm_plan_set_residual(p.addr, ptr(residual), residual.stride(0)),
+              "ms_gemm_plan_set_residual")
+    p.keep = [A, W, bias, D, segs, residual]
     p.flops = 2 * m * W.shape[0] * k
     p.label = f"dense M={m} N={W.shape[0]} K={k}"
     return p
@@ -290,6 +309,28 @@ class Program:
         self.ops.append(("segmean", (ptr(X), n_req, S, HW, C_, ptr(Y), y_ld)))
         self.keep += [X, Y]
 
+    def layernorm(self, X, ldx, rows, gamma, beta, Y, ldy, C_, eps=1e-6):
+        self.ops.append(("ms_op_layernorm", (ptr(X), ldx, rows, ptr(gamma), ptr(beta), ptr(Y), ldy, C_,
+                                             float(eps))))
+        self.keep += [X, gamma, beta, Y]
+
+    def attention(self, qkv, ld, L, H, n_seq, out, ldo, scale):
+        self.ops.append(("ms_op_attention", (ptr(qkv), ld, L, H, n_seq, ptr(out), ldo, float(scale))))
+        self.keep += [qkv, out]
+
+    def patchify(self, X, n, S, C_, P_, Y):
+        self.ops.append(("ms_op_patchify", (ptr(X), n, S, C_, P_, ptr(Y))))
+        self.keep += [X, Y]
+
+    def vit_embed(self, pe, cls, pos, n, L, D, tok):
+        self.ops.append(("ms_op_vit_embed", (ptr(pe), ptr(cls), ptr(pos), n, L, D, ptr(tok))))
+        self.keep += [pe, cls, pos, tok]
+
+    def bert_embed(self, ids, n_tok, L, word, pos, type0, gamma, beta, Y, D, eps=1e-12):
+        self.ops.append(("ms_op_bert_embed", (ptr(ids), n_tok, L, ptr(word), ptr(pos), ptr(type0),
+                                              ptr(gamma), ptr(beta), ptr(Y), D, float(eps))))
+        self.keep += [ids, word, pos, type0, gamma, beta, Y]
+
     def seal(self):
         n = len(self.ops)
         self._buf = C.create_string_buffer(OP_BYTES * max(n, 1) + 64)
@@ -303,8 +344,10 @@ class Program:
                 check(L.ms_op_pool2d_ex(at, *a), "ms_op_pool2d_ex")
             elif kind == "im2col":
                 check(L.ms_op_im2col(at, *a), "ms_op_im2col")
-            else:
+            elif kind == "segmean":
                 check(L.ms_op_segment_mean(at, *a), "ms_op_segment_mean")
+            else:
+                check(getattr(L, kind)(at, *a), kind)
         return self
 
     def run(self, stream=None):

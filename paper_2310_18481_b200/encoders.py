@@ -178,14 +178,14 @@ def bninception_weights(cin: int, size: int, seed: int):
     return W
 
 
-def fusion_weights(n_mod: int, feat_dim: int, seed: int):
+def fusion_weights(n_mod: int, feat_dim: int, seed: int, n_classes: int = N_CLASSES):
     import torch
     g = _gen(seed)
     k = n_mod * feat_dim
     w1 = (torch.randn(FUSION_HIDDEN, k, generator=g) * (2.0 / k) ** 0.5).to(torch.bfloat16)
     b1 = (torch.randn(FUSION_HIDDEN, generator=g) * 0.02).float()
-    w2 = (torch.randn(N_CLASSES, FUSION_HIDDEN, generator=g) * (1.0 / FUSION_HIDDEN) ** 0.5).to(torch.bfloat16)
-    b2 = (torch.randn(N_CLASSES, generator=g) * 0.02).float()
+    w2 = (torch.randn(n_classes, FUSION_HIDDEN, generator=g) * (1.0 / FUSION_HIDDEN) ** 0.5).to(torch.bfloat16)
+    b2 = (torch.randn(n_classes, generator=g) * 0.02).float()
     return w1, b1, w2, b2
 
 
@@ -496,18 +496,20 @@ class MLPEncoder:
 class FusionHead:
     """Masked concat -> FC(K*F -> 512) -> ReLU -> FC(512 -> 397) logits."""
 
-    def __init__(self, n_mod: int, max_req: int, seed: int, feat_dim: int = FEAT_DIM, device="cuda"):
+    def __init__(self, n_mod: int, max_req: int, seed: int, feat_dim: int = FEAT_DIM, device="cuda",
+                 n_classes: int = N_CLASSES):
         import torch
         self.n_mod = n_mod
         self.feat_dim = feat_dim
         self.max_req = max_req
+        self.n_classes = n_classes
         self.dev = torch.device(device)
-        self.weights_cpu = fusion_weights(n_mod, feat_dim, seed)
+        self.weights_cpu = fusion_weights(n_mod, feat_dim, seed, n_classes)
         w1, b1, w2, b2 = self.weights_cpu
         self.w1, self.b1 = w1.to(self.dev).contiguous(), b1.to(self.dev)
         self.w2, self.b2 = pack_dense_weight(w2).to(self.dev), b2.to(self.dev)
         self.h = torch.empty(max_req, FUSION_HIDDEN, dtype=torch.bfloat16, device=self.dev)
-        self.logits = torch.empty(max_req, N_CLASSES, dtype=torch.float32, device=self.dev)
+        self.logits = torch.empty(max_req, n_classes, dtype=torch.float32, device=self.dev)
         self._programs = {}
 
     def program(self, n_req: int, feats, inv):
@@ -520,9 +522,9 @@ class FusionHead:
         P.gemm(dv.plan_gather(list(feats), inv, self.w1, self.b1, self.h, M=n_req,
                               feat_dim=self.feat_dim, BN=256, relu=True))
         P.gemm(dv.plan_dense(self.h, self.w2, self.b2, self.logits, M=n_req, K=FUSION_HIDDEN,
-                             BN=pick_bn(N_CLASSES), out_fp32=True))
+                             BN=pick_bn(self.n_classes), out_fp32=True))
         self._programs[key] = P.seal()
         return self._programs[key]
 
     def flops(self, n_req: int) -> int:
-        return n_req * (2 * self.n_mod * self.feat_dim * FUSION_HIDDEN + 2 * FUSION_HIDDEN * N_CLASSES)
+        return n_req * (2 * self.n_mod * self.feat_dim * FUSION_HIDDEN + 2 * FUSION_HIDDEN * self.n_classes)
