@@ -45,6 +45,31 @@ sys.path.insert(0, str(ROOT))
 METRIC = "requests/sec at >=99% SLO attainment; p50/p99 latency at 1/2/4/8 B200"
 UNIT = "requests/s"
 
+# accuracy tables for the random-init models (masks bit order = modality order)
+VQA_ACCURACY = (0.25, 0.44, 0.70)     # image only, text only (image tower dropped), both
+MLP_ACCURACY = (0.55, 0.50, 0.62, 0.38, 0.60, 0.56, 0.66)
+
+
+def workload_spec(name):
+    """(description, modality names, accuracy table, model builder)."""
+    if name == "tbn":
+        from paper_2310_18481_b200.executor import build_tbn_model
+        from paper_2310_18481_b200.profiler import TBN_ACCURACY
+        return ("configs[1]: TBN BN-Inception rgb/flow/audio encoders (3 segments), EPIC-shaped clips "
+                "resident in HBM, fixed per-request deadline", ("rgb", "flow", "audio"), TBN_ACCURACY,
+                lambda mr, ns, seed: build_tbn_model(max_req=mr, n_slots=ns, data_seed=seed))
+    if name == "vqa":
+        from paper_2310_18481_b200.towers import build_vqa_model
+        return ("configs[2]: VQA two-tower ViT-B/16 (224^2) + BERT-base (40 tokens), random init, "
+                "image tower dropped under tight SLO", ("image", "text"), VQA_ACCURACY,
+                lambda mr, ns, seed: build_vqa_model(max_req=mr, n_slots=ns, data_seed=seed))
+    if name == "mlp":
+        from paper_2310_18481_b200.executor import build_mlp_model
+        return ("configs[0]: 3-modality rgb/flow/audio MLP encoders 1024->1024->1024", ("rgb", "flow", "audio"),
+                MLP_ACCURACY, lambda mr, ns, seed: build_mlp_model((1024, 1024, 1024), max_req=mr, n_slots=ns,
+                                                                   data_seed=seed))
+    raise ValueError(name)
+
 
 def _peaks():
     try:
@@ -306,31 +331,32 @@ def our_arm(args):
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
     from paper_2310_18481_b200 import build
     build.build()
-    from paper_2310_18481_b200.executor import build_tbn_model
     from paper_2310_18481_b200.planner import build_matrix, recommended_alphas
-    from paper_2310_18481_b200.profiler import TBN_ACCURACY, profile_model
+    from paper_2310_18481_b200.profiler import profile_model
     from paper_2310_18481_b200.realtime import HostClips
     from paper_2310_18481_b200.registry import save_profile
     peaks, peak_kind = _peaks()
+    desc, mod_names, accuracy, builder = workload_spec(args.workload)
 
     max_req = args.max_req
     t_setup = time.perf_counter()
-    model = build_tbn_model(max_req=max_req, n_slots=args.slots, data_seed=rank)
+    model = builder(max_req, args.slots, rank)
     model.warm_graphs()
     log(f"[bench] model + {len(model._graphs)} graphs in {time.perf_counter() - t_setup:.1f}s")
-    prof = profile_model(model, ("rgb", "flow", "audio"), TBN_ACCURACY, max_batch=args.profile_batch,
-                         reps=3)
+    prof = profile_model(model, mod_names, accuracy, max_batch=args.profile_batch, reps=3,
+                         name=f"{args.workload}-b200")
     out_dir = ROOT / "gpurun_out"
     out_dir.mkdir(exist_ok=True)
     if rank == 0:
-        save_profile(prof, out_dir / "tbn_b200_profile.yaml")
+        save_profile(prof, out_dir / f"{args.workload}_b200_profile.yaml")
     matrix = build_matrix(prof, range(1, args.max_job + 1), recommended_alphas(prof))
-    full1 = prof.part_latency_us(7, 1)
+    full = prof.all_modalities_mask
+    full1 = prof.part_latency_us(full, 1)
     log(f"[bench] profile: all-modality batch1 {full1} us, batch{args.profile_batch} "
-        f"{prof.part_latency_us(7, args.profile_batch)} us; audio b1 {prof.part_latency_us(4, 1)} us")
+        f"{prof.part_latency_us(full, args.profile_batch)} us; mask1 b1 {prof.part_latency_us(1, 1)} us")
     deadline_ms = args.deadline_ms
     # capacity guess: all-modality requests at the profiled batch
-    cap = args.profile_batch / (prof.part_latency_us(7, args.profile_batch) * 1e-6)
+    cap = args.profile_batch / (prof.part_latency_us(full, args.profile_batch) * 1e-6)
     cost = None
     if not args.no_batching:
         from paper_2310_18481_b200.profiler import profile_pass_costs
@@ -398,8 +424,15 @@ def our_arm(args):
     roof = dominant_gemm_roofline(model, peaks.get("bf16_tflops"))
     comp = compaction_roofline(model, peaks.get("hbm_gbs"), max_req)
 
+    # modality-dropping share: requests served without some modality
+    drop_share = None
+    served = [r for r in timed if not r.dropped]
+    if served:
+        full_acc = prof.combo_accuracy(full)
+        drop_share = round(sum(r.size for r in served if r.achieved_accuracy < full_acc) /
+                           sum(r.size for r in served), 4)
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and args.workload == "tbn":
         cpu = cpu_baseline_arm(steps=args.cpu_steps, warmup=1, n_req=2, seconds_cap=25.0)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
@@ -410,8 +443,7 @@ def our_arm(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000.0 * win, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "configs[1]: TBN BN-Inception rgb/flow/audio encoders (3 segments), "
-                               "EPIC-shaped clips resident in HBM, fixed per-request deadline",
+        "config": {"workload": desc,
                    "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
                    "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
                    "policy": "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
@@ -420,6 +452,7 @@ def our_arm(args):
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
         "slo_attainment": round(attainment, 5),
+        "requests_with_modalities_dropped": drop_share,
         "latency_ms": {"p50": None if pct[50] is None else round(pct[50] / 1000, 3),
                        "p99": None if pct[99] is None else round(pct[99] / 1000, 3)},
         "gpu_launches": st.gpu_launches,
@@ -432,9 +465,9 @@ def our_arm(args):
                 "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5)},
         "clocks": clk, "cpu_baseline": cpu,
         "search": [(round(q, 1), round(v, 4)) for q, v in trials],
-        "profile_us": {"all_b1": prof.part_latency_us(7, 1),
-                       f"all_b{args.profile_batch}": prof.part_latency_us(7, args.profile_batch),
-                       "audio_b1": prof.part_latency_us(4, 1)},
+        "profile_us": {prof.combo_label(m): [prof.part_latency_us(m, 1),
+                                             prof.part_latency_us(m, args.profile_batch)]
+                       for m in range(1, full + 1)},
     }
     print(json.dumps(line), flush=True)
 
@@ -445,6 +478,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="tbn", choices=["tbn", "vqa", "mlp"],
+                    help="tbn = configs[1] (the headline); vqa = configs[2]; mlp = configs[0]")
     ap.add_argument("--window-s", type=float, default=1.0)
     ap.add_argument("--search-seconds", type=float, default=2.0)
     ap.add_argument("--deadline-ms", type=float, default=15.0,

@@ -135,6 +135,8 @@ def profile_pass_costs(model, max_n: int | None = None, reps: int = 5) -> PassCo
     head = []
     masks = np.full(top, (1 << model.K) - 1, dtype=np.int16)
     model.stage_inputs(np.arange(top) % model.n_slots, masks)
+    model._compact(top)
+    model.stage_inputs(np.arange(top) % model.n_slots, masks)
     torch.cuda.synchronize()
     for n in range(1, top + 1):
         g = model._graph(("head", n), model._head(n).run)

@@ -32,3 +32,24 @@ for _ in range(a.reps):
     m.forward(slots, masks)
 torch.cuda.synchronize()
 print("launches per pass", m.launches_per_pass(m.counts_for(masks)), "flops", m.flops(masks))
+
+if a.graphs == 0:
+    import json
+    order = []
+    counts = m.counts_for(masks)
+    order.append(("compact_index", "", 0))
+    for k, c in enumerate(counts):
+        if c:
+            order.append(("gather", f"mod{k}", 0))
+    for k, (e, c) in enumerate(zip(m.encoders, counts)):
+        if not c:
+            continue
+        for kind, op in e.program(c).ops:
+            if kind == "gemm":
+                order.append(("gemm", f"mod{k} " + op.label, op.flops))
+            else:
+                order.append((kind, f"mod{k}", 0))
+    for kind, op in m.head.program(a.n, [e.out for e in m.encoders], m.inv[: m.K * a.n].view(m.K, a.n)).ops:
+        order.append(("gemm", "head " + op.label, op.flops))
+    Path("gpurun_out").mkdir(exist_ok=True)
+    Path("gpurun_out/pass_ops.json").write_text(json.dumps(order))
