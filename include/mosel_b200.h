@@ -129,6 +129,11 @@ int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv,
 /* add a bf16 residual (same row mapping as the output, row stride res_ld)
  * after the activation: D = act(A W^T + b) + R */
 int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld);
+/* split K over `ksplit` CTAs per output tile (small-M GEMMs): partial sums
+ * go to the caller's fp32 workspace ws[M, ws_ld] (ws_ld >= N, % 4 == 0),
+ * then a finalize kernel applies bias/activation/residual; ms_gemm_run then
+ * issues memset + GEMM + finalize.  Dense/gather single-segment plans only. */
+int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld);
 int ms_gemm_run(const void* plan, void* stream);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
 

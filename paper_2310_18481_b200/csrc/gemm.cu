@@ -81,6 +81,11 @@ struct GemmParams {
   const __nv_bfloat16* residual;   // same row mapping as the output, row stride res_ld
   long long res_ld;
   Seg seg[4];
+  // split-K: tile = (m, n, k-part); partial sums -> fp32 workspace (atomics),
+  // bias/act/convert applied by splitk_finalize_kernel
+  int ksplit, kb_per;
+  float* ws;
+  long long ws_ld;
 };
 
 struct alignas(64) GemmPlan {
@@ -97,6 +102,28 @@ __device__ __forceinline__ float activate(float x, int act) {
     case MS_ACT_TANH: return tanhf(x);
     default: return x;
   }
+}
+
+template <int ACT>
+__device__ __forceinline__ void convert_chunk(const uint32_t (&v)[32], const float* bch, uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    pk[j] = pack_bf16x2(activate(__uint_as_float(v[2 * j]) + bch[2 * j], ACT),
+                        activate(__uint_as_float(v[2 * j + 1]) + bch[2 * j + 1], ACT));
+}
+
+struct TileIdx {
+  int m, n, kb0, kb1;
+};
+__device__ __forceinline__ TileIdx decode_tile(const GemmParams& p, int t, int n_tiles) {
+  TileIdx r;
+  const int kp = t % p.ksplit;
+  const int mn = t / p.ksplit;
+  r.m = mn / n_tiles;
+  r.n = mn - r.m * n_tiles;
+  r.kb0 = kp * p.kb_per;
+  r.kb1 = min(p.num_kb, r.kb0 + p.kb_per);
+  return r;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -121,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (p.N + p.BN - 1) / p.BN;
-  const int num_tiles = p.m_tiles * n_tiles;
+  const int num_tiles = p.m_tiles * n_tiles * p.ksplit;
 
   if (threadIdx.x == 0) {
     const uint32_t full_count = (p.mode == MODE_GATHER) ? 1 + 128 : 1;
@@ -157,7 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       const uint32_t tx = (p.mode == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m_tile = t / n_tiles, n_tile = t - (t / n_tiles) * n_tiles;
+        const TileIdx ti = decode_tile(p, t, n_tiles);
+        const int m_tile = ti.m, n_tile = ti.n;
         int n0 = 0, oh0 = 0, ow0 = 0;
         if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC) {
           const int tw = m_tile % p.tiles_w;
@@ -167,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           oh0 = th * p.bh * p.stride - p.pad;
           ow0 = tw * p.bw * p.stride - p.pad;
         }
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
           mbar_wait(&empty[s], phase ^ 1);
           const uint32_t a_dst = smem_addr(smA + s * kABytes);
           const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
@@ -203,10 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const TileIdx ti = decode_tile(p, t, n_tiles);
       mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
+      for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
         mbar_wait(&full[s], phase);
         tc_fence_after();
         if (p.mode == MODE_GATHER) fence_proxy_async_smem();
@@ -216,10 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
-            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
           }
           umma_commit(&empty[s]);
-          if (kb == p.num_kb - 1) umma_commit(&tfull[acc]);
+          if (kb == ti.kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++s == stages) {
@@ -241,11 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m_tile = t / n_tiles, n_tile = t - (t / n_tiles) * n_tiles;
+      const TileIdx ti = decode_tile(p, t, n_tiles);
+      const int m_tile = ti.m, n_tile = ti.n;
       if (gatherer) {
         const int row = m_tile * kBM + r;
         const int kb_per_mod = p.feat_dim / kBK;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
           mbar_wait(&empty[s], phase ^ 1);
           const int k = kb / kb_per_mod;
           const int off = (kb - k * kb_per_mod) * kBK;
@@ -299,6 +329,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
         tmem_wait_ld();
         if (out_row < 0) continue;
+        if (p.ksplit > 1) {  // partial sums: vector fp32 atomics into the workspace
+          float* w = p.ws + out_row * p.ws_ld + nb;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (nb + j < p.N)
+              atomicAdd(reinterpret_cast<float4*>(w + j),
+                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                    __uint_as_float(v[j + 3])));
+          }
+          continue;
+        }
         // destination segment of this 32-column chunk (segments are 32-aligned)
         void* seg_ptr = p.seg[0].ptr;
         long long seg_ld = p.seg[0].ldd;
@@ -339,16 +380,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           uint32_t pk[16];
+          switch (act) {
+            case MS_ACT_RELU: convert_chunk<MS_ACT_RELU>(v, bch, pk); break;
+            case MS_ACT_GELU: convert_chunk<MS_ACT_GELU>(v, bch, pk); break;
+            case MS_ACT_TANH: convert_chunk<MS_ACT_TANH>(v, bch, pk); break;
+            default: convert_chunk<MS_ACT_NONE>(v, bch, pk);
+          }
+          if (p.residual != nullptr && full_chunk) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float a = activate(__uint_as_float(v[2 * j]) + bch[2 * j], act);
-            float b = activate(__uint_as_float(v[2 * j + 1]) + bch[2 * j + 1], act);
-            if (p.residual != nullptr && full_chunk) {
+            for (int j = 0; j < 16; ++j) {
+              const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
               const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&res[j]);
-              a += __bfloat162float(r2.x);
-              b += __bfloat162float(r2.y);
+              // residual added in fp32 from the bf16-rounded branch output
+              pk[j] = pack_bf16x2(__bfloat162float(a2.x) + __bfloat162float(r2.x),
+                                  __bfloat162float(a2.y) + __bfloat162float(r2.y));
             }
-            pk[j] = pack_bf16x2(a, b);
           }
           if (full_chunk) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -373,6 +419,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+// split-K finalize: D = act(ws + bias) (+ residual), bf16 or fp32, one thread
+// per 4 columns
+__global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
+  const int n4 = (p.N + 3) / 4;
+  const long long total = (long long)p.M * n4;
+  const Seg& S = p.seg[0];
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long row = t / n4;
+    const int n = (int)(t - row * n4) * 4;
+    const float4 a = *reinterpret_cast<const float4*>(p.ws + row * p.ws_ld + n);
+    const float av[4] = {a.x, a.y, a.z, a.w};
+    for (int j = 0; j < 4 && n + j < p.N; ++j) {
+      float x = activate(av[j] + (p.bias ? p.bias[n + j] : 0.0f), p.relu);
+      if (p.residual) x += __bfloat162float(p.residual[row * p.res_ld + n + j]);
+      const long long o = row * S.ldd + S.col0 + n + j - S.n_begin;
+      if (p.out_fp32)
+        reinterpret_cast<float*>(S.ptr)[o] = x;
+      else
+        reinterpret_cast<__nv_bfloat16*>(S.ptr)[o] = __float2bfloat16_rn(x);
+    }
   }
 }
 
@@ -433,13 +503,16 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   if (rc) return rc;
   p.BN = BN;
   p.num_kb = num_kb;
+  p.ksplit = 1;
+  p.kb_per = num_kb;
   p.b_bytes = BN * kBK * 2;
   const int per_stage = kABytes + p.b_bytes;
-  int stages = (200 * 1024 - kMaxBias * 4) / per_stage;
+  const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
+  int stages = (200 * 1024 - bias_bytes) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + kMaxBias * 4;
+  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + bias_bytes;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
@@ -468,9 +541,19 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = 1;
   }
+  const GemmParams& p = P->p;
+  if (p.ksplit > 1 &&
+      cudaMemsetAsync(p.ws, 0, sizeof(float) * (size_t)p.M * (size_t)p.ws_ld, stream) != cudaSuccess)
+    return set_error(MS_ERR_CUDA, "split-K workspace memset failed");
   dim3 grid(P->grid_x, P->grid_y);
-  gemm_tc_kernel<<<grid, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, P->p);
-  return check_launch("gemm_tc_kernel");
+  gemm_tc_kernel<<<grid, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, p);
+  int rc = check_launch("gemm_tc_kernel");
+  if (rc || p.ksplit <= 1) return rc;
+  const long long work = (long long)p.M * ((p.N + 3) / 4);
+  long long blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  splitk_finalize_kernel<<<(int)blocks, 256, 0, stream>>>(p);
+  return check_launch("splitk_finalize_kernel");
 }
 
 }  // namespace mosel
@@ -606,6 +689,26 @@ int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld
     return set_error(MS_ERR_INVALID, "residual needs a bf16 single-segment output and res_ld*2 % 16 == 0");
   P->p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
   P->p.res_ld = res_ld;
+  return MS_OK;
+}
+
+int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  GemmParams& p = P->p;
+  if (ksplit < 1) return set_error(MS_ERR_INVALID, "ksplit must be >= 1");
+  if (ksplit > 1) {
+    if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.nseg > 1 || ws == nullptr || ws_ld % 4 != 0 ||
+        ws_ld < p.N)
+      return set_error(MS_ERR_INVALID, "split-K needs a dense/gather single-segment plan and ws[M, ws_ld>=N, %4]");
+  }
+  const int kb_per = (p.num_kb + ksplit - 1) / ksplit;
+  p.ksplit = (p.num_kb + kb_per - 1) / kb_per;  // no empty K parts
+  p.kb_per = kb_per;
+  p.ws = ws;
+  p.ws_ld = ws_ld;
+  const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN) * p.ksplit;
+  P->grid_x = tiles < sm_count() ? tiles : sm_count();
   return MS_OK;
 }
 

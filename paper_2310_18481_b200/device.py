@@ -75,6 +75,7 @@ _SIGS = {
     "ms_event_elapsed_us": ([_P, _P, _P], C.c_int),
     "ms_event_query": ([_P], C.c_int),
     "ms_gemm_plan_set_residual": ([_P, _P, _LL], C.c_int),
+    "ms_gemm_plan_set_splitk": ([_P, _I, _P, _LL], C.c_int),
     "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
     "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),
     "ms_patchify": ([_P, _I, _I, _I, _I, _P, _P], C.c_int),
@@ -206,6 +207,7 @@ class GemmPlan:
         self.keep = []
         self.flops = 0
         self.label = ""
+        self.split_k = 1
 
     def run(self, stream=None):
         check(lib().ms_gemm_run(self.addr, stream_ptr(stream)), "ms_gemm_run")
@@ -229,8 +231,31 @@ def _segments(segs):
 ACT_NONE, ACT_RELU, ACT_GELU, ACT_TANH = 0, 1, 2, 3
 
 
+SM_COUNT = 148
+
+
+def _auto_splitk(p, M, N, BN, num_kb, split_k, dev):
+    """Split K when the output tiles cannot fill the GPU and K is deep:
+    ksplit ~ SMs / tiles, each part >= 4 K blocks."""
+    import torch
+    tiles = -(-M // 128) * -(-N // BN)
+    if split_k is None:
+        # memset + finalize cost ~2 launches: only worth it for deep K on
+        # a grid that leaves most SMs idle
+        split_k = 1
+        if tiles * 4 <= SM_COUNT and num_kb >= 16:
+            split_k = max(1, min(num_kb // 4, SM_COUNT // tiles))
+    if split_k > 1:
+        ws_ld = -(-N // 4) * 4
+        ws = torch.empty(M, ws_ld, dtype=torch.float32, device=dev)
+        check(lib().ms_gemm_plan_set_splitk(p.addr, split_k, ws.data_ptr(), ws_ld), "ms_gemm_plan_set_splitk")
+        p.keep.append(ws)
+        p.split_k = split_k
+    return p
+
+
 def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col0=0, ldd=None,
-               segs=None, M=None, act=None, residual=None, lda=None):
+               segs=None, M=None, act=None, residual=None, lda=None, split_k=None):
     """D = act(A[M,K] @ W[N,K_pad]^T + bias) (+ residual); A row stride =
     ``lda`` or A.stride(0).  ``act`` is ACT_* (``relu=True`` == ACT_RELU)."""
     p = GemmPlan()
@@ -248,6 +273,8 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
     p.keep = [A, W, bias, D, segs, residual]
     p.flops = 2 * m * W.shape[0] * k
     p.label = f"dense M={m} N={W.shape[0]} K={k}"
+    if not segs or len(segs) == 1:
+        _auto_splitk(p, m, W.shape[0], BN, W.shape[1] // 64, split_k, A.device)
     return p
 
 
@@ -267,7 +294,8 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
     return p
 
 
-def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_fp32=False):
+def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_fp32=False,
+                split_k=None):
     p = GemmPlan()
     arr = (C.c_void_p * len(feats))(*[ptr(f) for f in feats])
     check(lib().ms_gemm_plan_gather(p.addr, arr, ptr(inv), inv.stride(0), len(feats), feat_dim, M,
@@ -276,6 +304,7 @@ def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_f
     p.keep = [feats, inv, W, bias, D, arr]
     p.flops = 2 * M * W.shape[0] * len(feats) * feat_dim
     p.label = f"gather-concat M={M} N={W.shape[0]} K={len(feats) * feat_dim}"
+    _auto_splitk(p, M, W.shape[0], BN, len(feats) * feat_dim // 64, split_k, W.device)
     return p
 
 

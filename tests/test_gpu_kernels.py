@@ -291,3 +291,58 @@ def test_gather_rows_channel_and_line_pad(dev, c_src, c_dst, pad_w):
     assert torch.equal(dst[:, :, pad_w:pad_w + width, :c_src], src)
     dst[:, :, pad_w:pad_w + width, :c_src] = 0
     assert torch.count_nonzero(dst) == 0
+
+
+@pytest.mark.parametrize("M,K,N,BN,split,act", [
+    (48, 3072, 512, 256, 12, 1), (1, 768, 2304, 256, 3, 0), (197, 3072, 768, 256, 8, 0), (40, 768, 3129, 224, 4, 0),
+])
+def test_gemm_split_k_vs_torch(dev, M, K, N, BN, split, act):
+    g = torch.Generator().manual_seed(M * 7 + N)
+    A = _bf(torch.randn(M, K, generator=g)).cuda()
+    W = _bf(torch.randn(N, K, generator=g) * 0.03).cuda()
+    b = (torch.randn(N, generator=g) * 0.1).cuda()
+    out_fp32 = N == 3129
+    D = torch.zeros(M, N, dtype=torch.float32 if out_fp32 else torch.bfloat16, device="cuda")
+    R = _bf(torch.randn(M, N, generator=g)).cuda() if (N == 768 and not out_fp32) else None
+    if R is not None:
+        D.copy_(R)
+    p = dev.plan_dense(A, W, b, D, BN=BN, act=act, out_fp32=out_fp32, split_k=split,
+                       residual=D if R is not None else None)
+    assert p.split_k == split
+    p.run()
+    p.run()  # the workspace is re-zeroed every run
+    torch.cuda.synchronize()
+    ref = A.float().cpu() @ W.float().cpu().T + b.cpu()
+    if act == 1:
+        ref = ref.clamp_min(0)
+    if R is not None:  # residual applied twice (in-place D += ...)
+        ref = R.float().cpu() + 2 * ref
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
+def test_gather_gemm_split_k(dev):
+    g = torch.Generator().manual_seed(5)
+    N_req, F, K = 37, 1024, 3
+    masks = torch.randint(1, 8, (N_req,), generator=g)
+    feats, invs = [], []
+    full = torch.zeros(N_req, K * F)
+    for k in range(K):
+        have = ((masks >> k) & 1).bool()
+        f = _bf(torch.randn(int(have.sum()), F, generator=g))
+        inv = torch.full((N_req,), -1, dtype=torch.int32)
+        inv[have] = torch.arange(int(have.sum()), dtype=torch.int32)
+        full[have, k * F:(k + 1) * F] = f.float()
+        feats.append(f.cuda())
+        invs.append(inv)
+    W = _bf(torch.randn(512, K * F, generator=g) * 0.02)
+    b = torch.randn(512, generator=g) * 0.1
+    H = torch.zeros(N_req, 512, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_gather(feats, torch.stack(invs).cuda(), W.cuda(), b.cuda(), H, M=N_req, feat_dim=F, BN=256,
+                        relu=True, split_k=6)
+    assert p.split_k == 6
+    p.run()
+    torch.cuda.synchronize()
+    ref = (full @ W.float().T + b).clamp_min(0)
+    ok, err, scale = _close(H.cpu(), ref)
+    assert ok, (err, scale)
