@@ -409,14 +409,22 @@ def our_arm(args):
     value = agg[0] / agg_t[0]
     attainment = agg[0] / max(1, agg[1])
 
-    # ---- e2e through the public API with host buffers (same rate)
+    # ---- e2e through the public API with host buffers: same serving, clips
+    # H2D (present modalities only) + logits D2H inside each pass; PCIe can
+    # bind before the GPU does, so back off (10 %/step) to its own >=99 % rate
     hc = HostClips(model)
-    lg2, st2 = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
-                     max_size=args.max_job, cost=cost)
-    timed2 = [r for r in lg2.records if r.arrival_us >= t_lo]
-    ok2 = sum(r.size for r in timed2 if not r.violated)
-    tot2 = sum(r.size for r in timed2)
-    agg2 = _allreduce(pg, [ok2, tot2], op="sum")
+    e2e_rate = rate
+    for attempt in range(8):
+        lg2, st2 = serve(model, prof, matrix, e2e_rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
+                         max_size=args.max_job, cost=cost)
+        timed2 = [r for r in lg2.records if r.arrival_us >= t_lo]
+        ok2 = sum(r.size for r in timed2 if not r.violated)
+        tot2 = sum(r.size for r in timed2)
+        agg2 = _allreduce(pg, [ok2, tot2], op="sum")
+        if agg2[0] >= 0.99 * agg2[1]:
+            break
+        log(f"[bench] e2e attainment {agg2[0] / max(1, agg2[1]):.4f} at {e2e_rate:.1f} req/s: backing off 10%")
+        e2e_rate *= 0.9
     e2e_value = agg2[0] / agg_t[0]
     n_steps_total = args.warmup + args.steps
 
@@ -459,7 +467,7 @@ def our_arm(args):
         "gpu_util": round(st.busy_us / max(1.0, region_us), 4),
         "passes": st.passes, "region_ms": round(region_us / 1000, 1),
         "roofline": roof, "roofline_compaction": comp, "peak_kind": peak_kind,
-        "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "offered_rate_per_gpu": round(e2e_rate, 1),
                 "h2d_bytes_per_step": int(st2.h2d_bytes / n_steps_total),
                 "d2h_bytes_per_step": int(st2.d2h_bytes / n_steps_total),
                 "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5)},
@@ -484,10 +492,10 @@ def main():
     ap.add_argument("--search-seconds", type=float, default=2.0)
     ap.add_argument("--deadline-ms", type=float, default=15.0,
                     help="fixed per-request latency budget (deadline - arrival)")
-    ap.add_argument("--max-req", type=int, default=48, help="device pass capacity (requests)")
+    ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")
     ap.add_argument("--max-job", type=int, default=24, help="job size cap (matrix sizes 1..max_job)")
     ap.add_argument("--no-batching", action="store_true", help="one job per device pass")
-    ap.add_argument("--slots", type=int, default=128)
+    ap.add_argument("--slots", type=int, default=192)
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")

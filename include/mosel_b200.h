@@ -87,10 +87,13 @@ int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, co
  * channels in the pool; in the encoder input each pixel has c_dst (>= c_src,
  * multiple of 8) channels and every line gets pad_w zero pixels on both
  * ends (the first conv's window padding).  Plain rows: lines=1, width=1,
- * c_src=c_dst=elements, pad_w=0. */
+ * c_src=c_dst=elements, pad_w=0.  src_u8 pools are converted to bf16 on the
+ * fly (halves host->device and HBM input bytes for video). */
 typedef struct MsRowDesc {
   long long lines;
   int width, c_src, c_dst, pad_w;
+  int src_u8;              /* 1: pool holds uint8 (frames, quantised flow) */
+  float u8_scale, u8_bias; /* bf16 value = u8 * scale + bias */
 } MsRowDesc;
 int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                        const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows,

@@ -78,8 +78,9 @@ def encode_requests(clips, weights, cin: int, size: int, segments: int):
     """clips: [n_req, S, H, W, C] NHWC (as stored on the device) ->
     bf16-rounded TSN consensus features [n_req, 1024]."""
     n = clips.shape[0]
-    # the device stores channels zero-padded to a multiple of 8: use the real ones
-    frames = clips[..., :cin].reshape(n * segments, size, size, cin).permute(0, 3, 1, 2)
+    if clips.dtype == torch.uint8:  # uint8 frames/flow: value = u8 / 64 - 2 (exact in bf16)
+        clips = clips.float() / 64.0 - 2.0
+    frames = clips[..., :cin].float().reshape(n * segments, size, size, cin).permute(0, 3, 1, 2)
     f = bninception_forward(frames, weights, cin, size)  # [n*S, 1024, h, w]
     f = f.reshape(n, segments, f.shape[1], -1).mean(dim=(1, 3))
     return _bf(f)

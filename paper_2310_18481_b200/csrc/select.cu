@@ -181,10 +181,74 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_
 // and `pad_w` zero pixels on both ends of every line (the first conv's
 // window padding, so its TMA windows never leave the line).  One thread =
 // one destination pixel x 8 channels (one 16-B store).
-__global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, long long lines, int width,
-                                       int c_src, int c_dst, int pad_w, const int32_t* __restrict__ slot,
-                                       const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
-                                       uint4* __restrict__ dst) {
+// One CTA = one source line of one request at a time: the line (width *
+// c_src elements, 16-B aligned) is staged into shared memory with 16-B vector
+// loads, then each thread emits whole destination pixels (c_dst/8 16-B
+// stores, zero pad channels / pad pixels), converting uint8 on the fly.
+constexpr int kMaxLineBytes = 16384;
+template <bool U8>
+__global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __restrict__ src_v, long long lines,
+                                                              int width, int c_src, int c_dst, int pad_w,
+                                                              float u8_scale, float u8_bias,
+                                                              const int32_t* __restrict__ slot,
+                                                              const int32_t* __restrict__ idx,
+                                                              const int32_t* __restrict__ count,
+                                                              uint4* __restrict__ dst) {
+  __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
+  const int n = *count;
+  const int esz = U8 ? 1 : 2;
+  const int line_bytes = width * c_src * esz;
+  const int g8 = c_dst / 8;
+  const int wd = width + 2 * pad_w;
+  for (int j = blockIdx.y; j < n; j += gridDim.y) {
+    int r = idx[j];
+    if (slot) r = slot[r];
+    const unsigned char* srow = reinterpret_cast<const unsigned char*>(src_v) + (long long)r * lines * line_bytes;
+    uint4* drow = dst + (long long)j * lines * wd * g8;
+    const int per = min(32, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
+    for (long long ln0 = (long long)blockIdx.x * per; ln0 < lines; ln0 += (long long)gridDim.x * per) {
+      const int nl = (int)min((long long)per, lines - ln0);
+      __syncthreads();
+      const uint4* s4 = reinterpret_cast<const uint4*>(srow + ln0 * line_bytes);
+      for (int i = threadIdx.x; i < nl * line_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(line_buf)[i] = __ldcs(s4 + i);
+      __syncthreads();
+      uint4* d = drow + ln0 * wd * g8;
+      for (int q = threadIdx.x; q < nl * wd; q += blockDim.x) {
+        const int li = q / wd, px = q - li * wd;
+        const int x = px - pad_w;
+        const unsigned char* lb = line_buf + li * line_bytes;
+        for (int g = 0; g < g8; ++g) {
+          unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (x >= 0 && x < width) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int c = g * 8 + i;
+              if (c < c_src) {
+                if (U8) {
+                  const __nv_bfloat16 b = __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+                  v[i] = *reinterpret_cast<const unsigned short*>(&b);
+                } else {
+                  v[i] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+                }
+              }
+            }
+          }
+          d[(long long)q * g8 + g] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
+                                      v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+        }
+      }
+    }
+  }
+}
+
+// generic fallback (line not 16-B aligned or too long): one thread = one
+// destination pixel x 8 channels, scalar loads
+template <bool U8>
+__global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, long long lines, int width, int c_src,
+                                              int c_dst, int pad_w, float u8_scale, float u8_bias,
+                                              const int32_t* __restrict__ slot, const int32_t* __restrict__ idx,
+                                              const int32_t* __restrict__ count, uint4* __restrict__ dst) {
   const int n = *count;
   const int g8 = c_dst / 8;
   const int wd = width + 2 * pad_w;
@@ -193,7 +257,6 @@ __global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, l
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
     int r = idx[j];
     if (slot) r = slot[r];
-    const unsigned short* s = src + (long long)r * src_row;
     uint4* d = dst + (long long)j * work;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < work;
          t += (long long)gridDim.x * blockDim.x) {
@@ -203,10 +266,18 @@ __global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, l
       const int x = (int)(px - line * wd) - pad_w;
       unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if (x >= 0 && x < width) {
-        const unsigned short* sp = s + (line * width + x) * c_src;
+        const long long off = (long long)r * src_row + (line * width + x) * c_src + c0;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          if (c0 + i < c_src) v[i] = __ldcs(sp + c0 + i);
+          if (c0 + i < c_src) {
+            if (U8) {
+              const __nv_bfloat16 b = __float2bfloat16_rn(
+                  fmaf((float)reinterpret_cast<const unsigned char*>(src_v)[off + i], u8_scale, u8_bias));
+              v[i] = *reinterpret_cast<const unsigned short*>(&b);
+            } else {
+              v[i] = reinterpret_cast<const unsigned short*>(src_v)[off + i];
+            }
+          }
       }
       d[t] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
                         v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
@@ -216,18 +287,35 @@ __global__ void gather_rows_pad_kernel(const unsigned short* __restrict__ src, l
 
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
-                             cudaStream_t st) {
+                             cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f) {
   if (c_dst % 8 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
     return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0, pad_w >= 0");
   if (max_rows <= 0) return MS_OK;
-  const long long work = lines * (width + 2LL * pad_w) * (c_dst / 8);
-  long long bx = (work + 255) / 256;
-  if (bx > 1024) bx = 1024;
-  if (bx < 1) bx = 1;
   const int gy = max_rows < 65535 ? max_rows : 65535;
-  gather_rows_pad_kernel<<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-      reinterpret_cast<const unsigned short*>(src), lines, width, c_src, c_dst, pad_w, slot, idx, count,
-      reinterpret_cast<uint4*>(dst));
+  const long long line_bytes = (long long)width * c_src * (src_u8 ? 1 : 2);
+  if (line_bytes % 16 == 0 && line_bytes <= kMaxLineBytes) {
+    const long long per = line_bytes > 0 ? (kMaxLineBytes / line_bytes < 32 ? kMaxLineBytes / line_bytes : 32) : 1;
+    long long bx = (lines + per - 1) / per;
+    if (bx > 64) bx = 64;
+    if (bx < 1) bx = 1;
+    if (src_u8)
+      gather_rows_pad_kernel<true><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
+          src, lines, width, c_src, c_dst, pad_w, u8_scale, u8_bias, slot, idx, count, reinterpret_cast<uint4*>(dst));
+    else
+      gather_rows_pad_kernel<false><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
+          src, lines, width, c_src, c_dst, pad_w, 1.0f, 0.0f, slot, idx, count, reinterpret_cast<uint4*>(dst));
+  } else {
+    const long long work = lines * (width + 2LL * pad_w) * (c_dst / 8);
+    long long bx = (work + 255) / 256;
+    if (bx > 1024) bx = 1024;
+    if (bx < 1) bx = 1;
+    if (src_u8)
+      gather_rows_pad_scalar_kernel<true><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
+          src, lines, width, c_src, c_dst, pad_w, u8_scale, u8_bias, slot, idx, count, reinterpret_cast<uint4*>(dst));
+    else
+      gather_rows_pad_scalar_kernel<false><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
+          src, lines, width, c_src, c_dst, pad_w, 1.0f, 0.0f, slot, idx, count, reinterpret_cast<uint4*>(dst));
+  }
   return check_launch("gather_rows_pad_kernel");
 }
 
@@ -302,11 +390,11 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
     if (X == nullptr || G == nullptr || rows == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
     const MsRowDesc& r = rows[k];
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
-    if (r.c_src == r.c_dst && r.pad_w == 0 && bytes % 16 == 0)
+    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && bytes % 16 == 0)
       rc = gather_launch(X[k], bytes, slot, idx + (long long)k * N, counts + k, N, G[k], st);
     else
       rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, slot, idx + (long long)k * N,
-                             counts + k, N, G[k], st);
+                             counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias);
     if (rc) return rc;
   }
   return MS_OK;

@@ -55,11 +55,15 @@ INCEPTION_BLOCKS = (
 )
 
 
+U8_SCALE, U8_BIAS = 1.0 / 64.0, -2.0  # uint8 inputs -> bf16 value u8 * scale + bias (exact)
+
+
 @dataclass(frozen=True)
 class ModalitySpec:
     name: str
     channels: int
     size: int  # square input H = W
+    uint8: bool = False  # stored as uint8 in the pools (frames, quantised flow)
 
     @property
     def cpad(self) -> int:
@@ -71,7 +75,7 @@ class ModalitySpec:
         return self.size * self.size * self.cpad
 
 
-TBN_MODALITIES = (ModalitySpec("rgb", 3, 224), ModalitySpec("flow", 10, 224),
+TBN_MODALITIES = (ModalitySpec("rgb", 3, 224, True), ModalitySpec("flow", 10, 224, True),
                   ModalitySpec("audio", 1, 256))
 
 

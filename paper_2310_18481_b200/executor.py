@@ -29,8 +29,8 @@ from __future__ import annotations
 import numpy as np
 
 from . import device as dv
-from .encoders import (CONV1_PAD, FEAT_DIM, SEGMENTS, TBN_MODALITIES, BNInceptionEncoder,
-                       FusionHead, MLPEncoder)
+from .encoders import (CONV1_PAD, FEAT_DIM, SEGMENTS, TBN_MODALITIES, U8_BIAS, U8_SCALE,
+                       BNInceptionEncoder, FusionHead, MLPEncoder)
 
 
 def request_masks(parts, size: int) -> np.ndarray:
@@ -62,8 +62,10 @@ class MaskedModel:
         self.encoders = encoders
         self.head = head
         self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
-        self.rows = [tuple(int(v) for v in r) for r in rows]
-        self.row_bytes = [ln * w * cs * 2 for ln, w, cs, _, _ in self.rows]  # pool (source) bytes
+        # (lines, width, c_src, c_dst, pad_w[, src_u8, u8_scale, u8_bias])
+        self.rows = [tuple(r) + (0, 1.0, 0.0)[len(r) - 5:] if len(r) < 8 else tuple(r) for r in rows]
+        self.src_bytes = [1 if r[5] else 2 for r in self.rows]
+        self.row_bytes = [int(r[0] * r[1] * r[2] * b) for r, b in zip(self.rows, self.src_bytes)]
         self.K = len(encoders)
         self.max_req = max_req
         K, n = self.K, max_req
@@ -210,8 +212,8 @@ class MaskedModel:
         channels) + written (padded channels), + 2N mask bytes + 4*sum N_k
         index bytes."""
         counts = self.counts_for(np.asarray(masks))
-        rows = sum(2 * ln * (w * cs + (w + 2 * pw) * cd) * c
-                   for (ln, w, cs, cd, pw), c in zip(self.rows, counts))
+        rows = sum((rb + 2 * r[0] * (r[1] + 2 * r[4]) * r[3]) * c
+                   for r, rb, c in zip(self.rows, self.row_bytes, counts))
         return rows + 2 * len(masks) + 4 * sum(counts)
 
 
@@ -226,10 +228,16 @@ def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_se
     g.manual_seed(data_seed)
     pools, rows = [], []
     for m in TBN_MODALITIES:
-        # compact NHWC (real channels); the compaction gather pads to m.cpad
-        pools.append(torch.randn((n_slots, segments, m.size, m.size, m.channels), generator=g,
-                                 device=device).to(torch.bfloat16))
-        rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD))
+        # compact NHWC (real channels); the compaction gather pads to m.cpad.
+        # rgb frames and (TSN-style quantised) flow are uint8 and converted to
+        # bf16 (u8/64 - 2, exact in bf16) by the gather; audio spectrograms bf16
+        shape = (n_slots, segments, m.size, m.size, m.channels)
+        if m.uint8:
+            pools.append(torch.randint(0, 256, shape, generator=g, device=device, dtype=torch.uint8))
+            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD, 1, U8_SCALE, U8_BIAS))
+        else:
+            pools.append(torch.randn(shape, generator=g, device=device).to(torch.bfloat16))
+            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 

@@ -346,3 +346,40 @@ def test_gather_gemm_split_k(dev):
     ref = (full @ W.float().T + b).clamp_min(0)
     ok, err, scale = _close(H.cpu(), ref)
     assert ok, (err, scale)
+
+
+@pytest.mark.parametrize("c_src,c_dst,u8,width", [(3, 8, True, 224), (10, 16, True, 224), (1, 8, False, 256),
+                                                   (3, 8, False, 40)])
+def test_gather_staged_lines_u8_and_bf16(dev, c_src, c_dst, u8, width):
+    """Line-staged (smem, 16-B vector) padding gather; uint8 pools are
+    converted to bf16 as u8 * scale + bias."""
+    import ctypes
+    L = dev.lib()
+    lines, pad = 6, 3
+    if u8:
+        pool = torch.randint(0, 256, (5, lines, width, c_src), dtype=torch.uint8).cuda()
+        ref_pool = (pool.float() / 64.0 - 2.0).to(torch.bfloat16)
+    else:
+        pool = _bf(torch.randn(5, lines, width, c_src)).cuda()
+        ref_pool = pool
+    idx = torch.tensor([3, 0, 4], dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([3], dtype=torch.int32, device="cuda")
+    dst = torch.full((3, lines, width + 2 * pad, c_dst), 5.0, dtype=torch.bfloat16, device="cuda")
+    rows = (dev.RowDesc * 1)(dev.RowDesc(lines, width, c_src, c_dst, pad, int(u8), 1.0 / 64.0, -2.0))
+    mask = torch.ones(5, dtype=torch.int16, device="cuda")  # every request has modality 0
+    mask[1] = 0
+    mask[2] = 0
+    X = (ctypes.c_void_p * 1)(pool.data_ptr())
+    G = (ctypes.c_void_p * 1)(dst.data_ptr())
+    ix = torch.empty(5, dtype=torch.int32, device="cuda")
+    inv = torch.empty(5, dtype=torch.int32, device="cuda")
+    offs = torch.empty(3, dtype=torch.int32, device="cuda")
+    perm = torch.empty(5, dtype=torch.int32, device="cuda")
+    dev.check(L.ms_compact(mask.data_ptr(), 5, 1, X, rows, None, G, ix.data_ptr(), inv.data_ptr(),
+                           cnt.data_ptr(), offs.data_ptr(), perm.data_ptr(), dev.stream_ptr()), "compact")
+    torch.cuda.synchronize()
+    assert ix[:3].cpu().tolist() == [0, 3, 4]
+    exp = ref_pool[torch.tensor([0, 3, 4]).cuda()]
+    assert torch.equal(dst[:, :, pad:pad + width, :c_src], exp)
+    dst[:, :, pad:pad + width, :c_src] = 0
+    assert torch.count_nonzero(dst) == 0

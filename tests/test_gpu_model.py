@@ -70,7 +70,7 @@ def test_tbn_model_masked_forward_vs_oracle(built):
         assert np.array_equal(idx[k, : len(exp)], exp)
     orc = OracleTBN(TBN_MODALITIES, (101, 102, 103), 199, 3)
     sl = torch.as_tensor(slots).long().cuda()
-    clips = [p[sl].float().cpu() for p in model.pools]
+    clips = [p[sl].cpu() for p in model.pools]
     ref = orc.logits(clips, torch.as_tensor(masks))
     rel, agree = _check_logits(logits, ref)
     print(f"TBN: max rel err {rel:.2e}, top-1 agreement {agree:.4f}")
