@@ -79,6 +79,90 @@ __global__ void pool2d_kernel(const __nv_bfloat16* __restrict__ X, int n_img, in
   }
 }
 
+// 3x3 pooling, row-streaming: a CTA covers TH output rows of one image; a
+// thread owns one output column x 8 channels and walks down the strip,
+// caching the horizontal 3-tap reduction of each input row in registers, so
+// every input row is read once per column (vs 3x for a window-per-thread
+// kernel).  max ignores padding; avg counts it (divide by 9).
+template <bool MAX>
+__device__ __forceinline__ void pool_hrow(const __nv_bfloat16* __restrict__ X, long long img, int H, int W,
+                                          long long xcs, int g, int ih, int w0, float (&h)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = MAX ? -INFINITY : 0.0f;
+  if (ih < 0 || ih >= H) return;
+#pragma unroll
+  for (int dx = 0; dx < 3; ++dx) {
+    const int iw = w0 + dx;
+    if (iw < 0 || iw >= W) continue;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(X + ((img * H + ih) * W + iw) * xcs + g * 8));
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = MAX ? fmaxf(h[j], __bfloat162float(e[j])) : h[j] + __bfloat162float(e[j]);
+  }
+}
+
+template <bool MAX, int STRIDE>
+__global__ void __launch_bounds__(512) pool3_rows_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C, long long xcs,
+                                  int pad, int OH, int OW, int TH, __nv_bfloat16* __restrict__ Y,
+                                  long long ycs, int ycol0, const float* __restrict__ bias, int relu) {
+  const int cg = C / 8;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;  // (column, channel group)
+  if (t >= cg * OW) return;
+  const int g = t % cg, ow = t / cg;
+  const long long img = blockIdx.y;
+  const int oh0 = blockIdx.x * TH;
+  const int oh1 = min(OH, oh0 + TH);
+  const int w0 = ow * STRIDE - pad;
+  float bsum[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bsum[j] = (bias != nullptr) ? bias[g * 8 + j] : 0.0f;
+  // rows r0, r0+1, r0+2 of the current output row, reduced horizontally
+  float h0[8], h1[8], h2[8];
+  int r0 = oh0 * STRIDE - pad;
+  pool_hrow<MAX>(X, img, H, W, xcs, g, r0, w0, h0);
+  pool_hrow<MAX>(X, img, H, W, xcs, g, r0 + 1, w0, h1);
+  pool_hrow<MAX>(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+  for (int oh = oh0; oh < oh1; ++oh) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float a, b;
+      if (MAX) {
+        a = fmaxf(fmaxf(h0[2 * j], h1[2 * j]), h2[2 * j]);
+        b = fmaxf(fmaxf(h0[2 * j + 1], h1[2 * j + 1]), h2[2 * j + 1]);
+      } else {
+        a = (h0[2 * j] + h1[2 * j] + h2[2 * j]) * (1.0f / 9.0f);
+        b = (h0[2 * j + 1] + h1[2 * j + 1] + h2[2 * j + 1]) * (1.0f / 9.0f);
+      }
+      a += bsum[2 * j];
+      b += bsum[2 * j + 1];
+      if (relu) {
+        a = fmaxf(a, 0.0f);
+        b = fmaxf(b, 0.0f);
+      }
+      pk[j] = pack_bf16x2(a, b);
+    }
+    *reinterpret_cast<uint4*>(Y + ((img * OH + oh) * OW + ow) * ycs + ycol0 + g * 8) =
+        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    if (oh + 1 < oh1) {
+      r0 += STRIDE;
+      if (STRIDE == 1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          h0[j] = h1[j];
+          h1[j] = h2[j];
+        }
+        pool_hrow<MAX>(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h0[j] = h2[j];
+        pool_hrow<MAX>(X, img, H, W, xcs, g, r0 + 1, w0, h1);
+        pool_hrow<MAX>(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+      }
+    }
+  }
+}
+
 static int pool_out(int in, int k, int stride, int pad, int ceil_mode) {
   const int span = in + 2 * pad - k;
   int o = (ceil_mode ? (span + stride - 1) / stride : span / stride) + 1;
@@ -256,6 +340,27 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
     return set_error(MS_ERR_INVALID, "pool2d needs channel counts/strides multiple of 8");
   const int OH = pool_out(a.H, a.k, a.stride, a.pad, a.ceil_mode);
   const int OW = pool_out(a.W, a.k, a.stride, a.pad, a.ceil_mode);
+  const int threads = (a.C / 8) * OW;
+  if (a.k == 3 && (a.stride == 1 || a.stride == 2) && a.n_img <= 65535) {
+    const int block = threads < 512 ? (threads + 31) / 32 * 32 : 512;
+    const int TH = 8;
+    dim3 grid((OH + TH - 1) / TH, a.n_img, (threads + block - 1) / block);
+    auto X = reinterpret_cast<const __nv_bfloat16*>(a.X);
+    auto Y = reinterpret_cast<__nv_bfloat16*>(a.Y);
+    if (a.is_max && a.stride == 2)
+      pool3_rows_kernel<true, 2><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+                                                        a.ycol0, a.bias, a.relu);
+    else if (a.is_max)
+      pool3_rows_kernel<true, 1><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+                                                        a.ycol0, a.bias, a.relu);
+    else if (a.stride == 2)
+      pool3_rows_kernel<false, 2><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+                                                         a.ycol0, a.bias, a.relu);
+    else
+      pool3_rows_kernel<false, 1><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+                                                         a.ycol0, a.bias, a.relu);
+    return check_launch("pool3_rows_kernel");
+  }
   const long long work = (long long)a.n_img * OH * OW * (a.C / 8);
   pool2d_kernel<<<grid_for(work, 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H, a.W, a.C, a.xcs, a.k, a.stride, a.pad, OH, OW,

@@ -1,0 +1,70 @@
+"""Warm per-op device times of one masked TBN pass: every op of every
+encoder program (and the head) run alone between CUDA events, in program
+order, after a full warm-up pass.  Prints ops sorted by time with achieved
+TFLOP/s for GEMMs.
+
+    python tools/op_times.py --n 96 [--mixed]
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=96)
+ap.add_argument("--mixed", action="store_true")
+ap.add_argument("--top", type=int, default=45)
+a = ap.parse_args()
+
+import torch  # noqa: E402
+
+from paper_2310_18481_b200 import build  # noqa: E402
+
+build.build()
+from paper_2310_18481_b200 import device as dv  # noqa: E402
+from paper_2310_18481_b200.executor import build_tbn_model  # noqa: E402
+
+m = build_tbn_model(max_req=a.n, n_slots=max(8, a.n))
+rng = np.random.default_rng(0)
+masks = rng.integers(1, 8, size=a.n).astype(np.int16) if a.mixed else np.full(a.n, 7, dtype=np.int16)
+slots = np.arange(a.n) % m.n_slots
+m.use_graphs = False
+for _ in range(2):
+    m.forward(slots, masks)
+torch.cuda.synchronize()
+counts = m.counts_for(masks)
+e0, e1 = dv.Event(), dv.Event()
+rows = []
+for k, (enc, c) in enumerate(zip(m.encoders, counts)):
+    if not c:
+        continue
+    prog = enc.program(c)
+    for i, (kind, op) in enumerate(prog.ops):
+        single = dv.Program()
+        single.ops = [(kind, op)]
+        single.keep = prog.keep
+        single.seal()
+        single.run()
+        ts = []
+        for _ in range(5):
+            e0.record()
+            single.run()
+            e1.record()
+            ts.append(e0.elapsed_us(e1))
+        us = float(np.median(ts))
+        fl = op.flops if kind == "gemm" else 0
+        rows.append((us, k, i, kind, op.label if kind == "gemm" else "", fl))
+tot = sum(r[0] for r in rows)
+gem = [r for r in rows if r[3] == "gemm"]
+gt = sum(r[0] for r in gem)
+print(f"encoders: {tot:.0f} us ({len(rows)} ops); GEMM {gt:.0f} us = {sum(r[5] for r in gem) / gt / 1e6:.0f} TFLOP/s; "
+      f"other {tot - gt:.0f} us")
+by_kind = {}
+for r in rows:
+    by_kind[r[3]] = by_kind.get(r[3], 0.0) + r[0]
+print("by kind:", {k: round(v) for k, v in sorted(by_kind.items(), key=lambda x: -x[1])})
+for r in sorted(rows, key=lambda r: -r[0])[: a.top]:
+    tf = f"{r[5] / r[0] / 1e6:7.1f} TF/s" if r[5] else " " * 12
+    print(f"{r[0]:8.1f} us {tf} mod{r[1]} #{r[2]:<3d} {r[3]:8s} {r[4]}")
