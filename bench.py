@@ -257,7 +257,9 @@ def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, 
                        cost=cost)
         v = lg.violation_ratio()
         trials.append((q, v))
-        log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f}")
+        log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f} "
+            f"req/pass {st.requests / max(1, st.passes):.1f} late {st.late} drop(policy/dispatch/admit) "
+            f"{st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} policy {st.policy_host_us / max(1, st.policy_runs):.0f}us x{st.policy_runs}")
         if v <= 0.01:
             lo = q
             q = q * 2 if hi is None else (lo + hi) / 2

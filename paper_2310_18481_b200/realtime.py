@@ -39,6 +39,11 @@ class ServeStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     policy_host_us: float = 0.0
+    policy_runs: int = 0
+    dropped_policy: int = 0    # requests dropped by apply_policy (unsavable violators)
+    dropped_dispatch: int = 0  # requests dropped by the dispatch-time rule
+    dropped_admit: int = 0     # requests with an empty frontier at admission
+    late: int = 0              # requests completed after their deadline
     wall_s: float = 0.0
 
 
@@ -54,7 +59,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
                    policy: Policy = Policy.OPTIMIZED, watermark: int = 2,
                    host_clips: HostClips | None = None, slot_seed: int = 0,
                    window_us: int = 4_000_000, depth: int = 2, cost=None,
-                   max_batch_requests: int | None = None):
+                   max_batch_requests: int | None = None, lead_us: int = 600):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -68,7 +73,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     after the EDF head is popped, the following queued jobs (in EDF order,
     never skipping one) join the same masked device pass while the pass
     estimate keeps every member within its deadline and the batch within
-    ``max_batch_requests``.  Each job keeps its own assigned strategy; the
+    ``max_batch_requests``.  With batching, the next pass is formed just in
+    time — once the in-flight pass is within ``lead_us`` of its estimated
+    finish (or a full batch is already queued) — so batches grow with load
+    instead of being cut at whatever was queued when the previous pass was
+    launched.  Each job keeps its own assigned strategy; the
     pass's observed time feeds both the scheduler EWMA (attributed to jobs
     in proportion to their predicted latency) and the cost model's EWMA.
 
@@ -108,7 +117,9 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         t = time.perf_counter()
         for j in apply_policy(policy, queue, now, fb, pol_rng):
             drop(j)
+            stats.dropped_policy += j.size
         stats.policy_host_us += (time.perf_counter() - t) * 1e6
+        stats.policy_runs += 1
         since_opt = 0
 
     cap = min(max_batch_requests or model.max_req, model.max_req)
@@ -122,6 +133,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         job, drops = next_dispatch(queue, now, fb)
         for j in drops:
             drop(j)
+            stats.dropped_dispatch += j.size
         if job is None:
             queue.running = inflight[-1][0][-1] if inflight else None
             return False
@@ -205,6 +217,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
                                      job.assigned.effective_accuracy, end_us, False,
                                      end_us > job.deadline_us))
+            if end_us > job.deadline_us:
+                stats.late += job.size
 
     while pos < len(pending) or len(queue) or inflight:
         now = now_us()
@@ -218,6 +232,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             if not cands:
                 job.state = JobState.DROPPED
                 drop(job)
+                stats.dropped_admit += job.size
                 continue
             job.assigned_idx = len(cands) - 1
             queue.admit(job)
@@ -231,7 +246,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         while len(inflight) < depth and len(queue):
             t = now_us()
             if inflight and inflight[-1][0][-1].est_finish_us is not None:
-                t = max(t, inflight[-1][0][-1].est_finish_us)
+                fin = inflight[-1][0][-1].est_finish_us
+                if cost is not None and fin - t > lead_us and \
+                        sum(j.size for j in queue._jobs) < cap:
+                    break  # let the batch grow; dispatch closer to the GPU freeing up
+                t = max(t, fin)
             if not dispatch(t):
                 break
         if not inflight and not len(queue) and pos < len(pending):
