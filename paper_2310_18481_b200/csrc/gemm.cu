@@ -35,6 +35,9 @@ namespace mosel {
 constexpr int kEpiWarps = 8;                  // 2 per TMEM lane quarter
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // TMA + MMA + epilogue warps
 constexpr int kMaxBias = 4096;  // staged bias floats (N <= 4096)
+constexpr int kStageRowBytes = 80;                         // 64 B of bf16 + 16 B pad (conflict-free)
+constexpr int kStageWarpBytes = 32 * kStageRowBytes;       // one warp's 32 x 32 bf16 chunk
+constexpr int kStageBytes = kEpiWarps * kStageWarpBytes;   // epilogue staging buffers
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
@@ -77,7 +80,7 @@ struct GemmParams {
   int inv_ld, feat_dim, n_mod;
   // epilogue: v = act(acc + bias[n]) (+ residual[row, n])
   const float* bias;
-  int relu, out_fp32, nseg, pad_;  // relu: activation MS_ACT_* (1 = ReLU for compatibility)
+  int relu, out_fp32, nseg, debug_flags;  // relu: activation MS_ACT_*; debug_flags bit0: skip stores
   const __nv_bfloat16* residual;   // same row mapping as the output, row stride res_ld
   long long res_ld;
   Seg seg[4];
@@ -134,7 +137,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align inside the shared window without leaving the shared address space
+  // (a uintptr_t round trip would turn every smem access into a generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + stages * kABytes;
@@ -143,7 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [kMaxBias]
+  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);  // [kStageBytes], 16-B aligned
+  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);  // [N]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -328,8 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
         tmem_wait_ld();
-        if (out_row < 0) continue;
-        if (p.ksplit > 1) {  // partial sums: vector fp32 atomics into the workspace
+        if (p.debug_flags & 1) continue;
+        // rows outside the output still take part in the (warp-collective)
+        // staged store below; they are masked at the global write
+        const bool row_ok = out_row >= 0;
+        if (p.ksplit > 1) {
+          if (!row_ok) continue;  // partial sums: vector fp32 atomics into the workspace
           float* w = p.ws + out_row * p.ws_ld + nb;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
@@ -359,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full_chunk = nb + 32 <= p.N;
         const float* bch = sbias + nb;
         if (p.out_fp32) {
+          if (!row_ok) continue;
           float* dst = reinterpret_cast<float*>(seg_ptr) + base;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(seg_ptr) + base;
           uint32_t res[16];
-          if (p.residual != nullptr && full_chunk) {
+          if (p.residual != nullptr && full_chunk && row_ok) {
             const uint4* r4 = reinterpret_cast<const uint4*>(p.residual + out_row * p.res_ld + nb);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -397,10 +408,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (full_chunk) {
+            // coalesced write-back: stage the warp's 32 rows x 64 B in smem,
+            // then each store instruction covers 8 rows x 64 contiguous bytes
+            uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
+            uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            __syncwarp();
+            const long long col = seg_off + nb;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = i * 8 + (lane >> 2), piece = lane & 3;
+              const long long orow = __shfl_sync(0xffffffffu, out_row, rr);
+              const uint4 val = *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
+              if (orow >= 0)
+                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(seg_ptr) + orow * seg_ld + col +
+                                          piece * 8) = val;
+            }
+            __syncwarp();
+            continue;
+          }
+          if (full_chunk) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
             for (int j = 0; j < 4; ++j) d4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          } else {
+          } else if (row_ok) {
             unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -508,11 +540,12 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   p.b_bytes = BN * kBK * 2;
   const int per_stage = kABytes + p.b_bytes;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
-  int stages = (200 * 1024 - bias_bytes) / per_stage;
+  // 227 KB usable: 1 KB alignment slack, barriers, epilogue staging, bias
+  int stages = (226 * 1024 - 1024 - 256 - kStageBytes - bias_bytes) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + bias_bytes;
+  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + kStageBytes + bias_bytes;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
@@ -709,6 +742,13 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
   p.ws_ld = ws_ld;
   const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN) * p.ksplit;
   P->grid_x = tiles < sm_count() ? tiles : sm_count();
+  return MS_OK;
+}
+
+int ms_gemm_plan_debug(void* plan, int flags) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  P->p.debug_flags = flags;
   return MS_OK;
 }
 
