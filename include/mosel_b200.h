@@ -138,6 +138,10 @@ int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld
  * issues memset + GEMM + finalize.  Dense/gather single-segment plans only. */
 int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld);
 int ms_gemm_run(const void* plan, void* stream);
+/* run the plan as 2-CTA clusters on SM pairs (tcgen05.mma.cta_group::2,
+ * 256-row tiles, half the weight rows per CTA); dense/conv bf16 plans
+ * without split-K or residual */
+int ms_gemm_plan_set_pair(void* plan, int enable);
 /* profiling aid: bit0 = skip the epilogue stores (mainloop-only timing) */
 int ms_gemm_plan_debug(void* plan, int flags);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);

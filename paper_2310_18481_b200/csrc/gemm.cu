@@ -42,7 +42,7 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
-enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3 };
+enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4 };
 // MODE_CONV_SMALLC: first-layer convolutions with few channels (C8 = 8 or
 // 16 stored channels).  The input is stored W-padded by `pad` zero pixels on
 // each side, so for output pixel (oh, ow) and filter row kh the KW-tap
@@ -74,6 +74,8 @@ struct GemmParams {
   // CONV geometry
   int n_img, OH, OW, stride, pad, KW, cchunks, bn, bh, bw, tiles_w, tiles_h;
   int smallc_halves, smallc_jpb;  // K blocks per filter row, window pixels per K block
+  int H_in;                       // input height (MODE_CONV1_ROWS)
+  int pair;                       // 1: CTA-pair (cta_group::2) kernel
   // GATHER
   const __nv_bfloat16* feat[4];
   const int32_t* inv;  // [n_mod, inv_ld]
@@ -96,6 +98,8 @@ struct alignas(64) GemmPlan {
   CUtensorMap tmB;
   GemmParams p;
   int grid_x, grid_y, smem_bytes, tmem_cols;
+  const void* w_ptr;  // weight tensor (re-encoded for CTA-pair half boxes)
+  long long w_kpad, w_rows;
 };
 
 __device__ __forceinline__ float activate(float x, int act) {
@@ -454,6 +458,413 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ------------------------------------------------------------------------
+// CTA-pair (2-SM) variant for DENSE / CONV plans: clusters of 2 CTAs on an
+// SM pair compute 256 x BN tiles with tcgen05.mma.cta_group::2 (M = 256),
+// issued by the leader CTA only.  Each CTA loads its own 128-row A block and
+// HALF of the BN weight rows, so each tensor instruction does twice the work
+// of the single-SM kernel and weight traffic per CTA halves.  Protocol:
+//   full[s]   (leader)  : count 2 = one arrive.expect_tx per CTA; both CTAs'
+//                         TMA bytes complete on it (.cta_group::2 loads)
+//   empty[s]  (each CTA): multicast tcgen05.commit from the leader
+//   tfull[a]  (each CTA): multicast commit after a tile's last K block
+//   tempty[a] (leader)  : count 2*kEpiWarps, peer epilogue arrives remotely
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  const int stages = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + stages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smB + stages * p.b_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);
+  sstage += (16u - (smem_addr(sstage) & 15u)) & 15u;
+  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int n_tiles = (p.N + p.BN - 1) / p.BN;
+  const int m_pairs = (p.m_tiles + 1) / 2;
+  const int num_tiles = m_pairs * n_tiles;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int half_bn = p.BN / 2;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);  // leader's arrive.expect_tx of BOTH CTAs' bytes
+      mbar_init(&empty[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  uint32_t acc_stride = 32;
+  while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
+  const uint32_t tmem_cols = 2 * acc_stride;
+  if (warp == 1) tmem_alloc_pair(tmem_slot, tmem_cols);
+  for (int i = threadIdx.x; i < p.N; i += blockDim.x) sbias[i] = p.bias != nullptr ? p.bias[i] : 0.0f;
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits + TMEM allocation visible to the pair
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------- TMA producer (both CTAs)
+      int s = 0;
+      uint32_t phase = 0;
+      const uint32_t tx = p.a_bytes + p.b_bytes;  // this CTA's bytes
+      for (int t = cluster; t < num_tiles; t += n_clusters) {
+        const int m_tile = (t / n_tiles) * 2 + (int)rank, n_tile = t % n_tiles;
+        int n0 = 0, oh0 = 0, ow0 = 0;
+        if (p.mode == MODE_CONV) {
+          const int tw = m_tile % p.tiles_w;
+          const int th = (m_tile / p.tiles_w) % p.tiles_h;
+          const int tn = m_tile / (p.tiles_w * p.tiles_h);
+          n0 = tn * p.bn;
+          oh0 = th * p.bh * p.stride - p.pad;
+          ow0 = tw * p.bw * p.stride - p.pad;
+        }
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[s], phase ^ 1);
+          const uint32_t a_dst = smem_addr(smA + s * kABytes);
+          const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
+          // only the leader arrives, expecting both CTAs' bytes; the peer's TMA
+          // completes on the leader's barrier (tx may transiently go negative)
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * tx);
+          if (p.mode == MODE_DENSE) {
+            tma_load_2d_pair(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
+          } else {
+            const int tap = kb / p.cchunks;
+            const int cc = kb - tap * p.cchunks;
+            const int kh = tap / p.KW;
+            const int kw = tap - kh * p.KW;
+            tma_load_4d_pair(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
+          }
+          tma_load_2d_pair(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN + (int)rank * half_bn);
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // ---------------------------------------- MMA issuer (leader only)
+      const uint32_t idesc = umma_idesc_bf16_m256((uint32_t)p.BN);
+      int s = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += n_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);  // both CTAs drained this buffer
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[s], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
+            const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_commit_pair(&empty[s], 0x3);
+            if (kb == p.num_kb - 1) umma_commit_pair(&tfull[acc], 0x3);
+          }
+          __syncwarp();
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {  // -------------------------------------------- epilogue warps 2..9 (both CTAs)
+    const int q = warp & 3, grp = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_addr(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_addr(&tempty[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
+    for (int t = cluster; t < num_tiles; t += n_clusters) {
+      const int m_tile = (t / n_tiles) * 2 + (int)rank, n_tile = t % n_tiles;
+      long long out_row = -1;
+      if (p.mode == MODE_CONV) {
+        const int tw = m_tile % p.tiles_w;
+        const int th = (m_tile / p.tiles_w) % p.tiles_h;
+        const int tn = m_tile / (p.tiles_w * p.tiles_h);
+        const int per_img = p.bh * p.bw;
+        if (r < p.bn * per_img) {
+          const int i = r / per_img;
+          const int y = (r - i * per_img) / p.bw;
+          const int x = r - i * per_img - y * p.bw;
+          const int n = tn * p.bn + i, oh = th * p.bh + y, ow = tw * p.bw + x;
+          if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
+        }
+      } else {
+        const int row = m_tile * kBM + r;
+        if (m_tile < p.m_tiles && row < p.M) out_row = row;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
+      const int n_first = n_tile * p.BN;
+      for (int c = grp; c < p.BN / 32; c += 2) {
+        const int nb = n_first + c * 32;
+        if (nb >= p.N) break;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
+        tmem_wait_ld();
+        if (p.debug_flags & 1) continue;
+        void* seg_ptr = p.seg[0].ptr;
+        long long seg_ld = p.seg[0].ldd;
+        int seg_off = p.seg[0].col0 - p.seg[0].n_begin;
+        int seg_flags = p.seg[0].flags;
+#pragma unroll
+        for (int g = 1; g < 4; ++g) {
+          if (g < p.nseg && nb >= p.seg[g].n_begin) {
+            seg_ptr = p.seg[g].ptr;
+            seg_ld = p.seg[g].ldd;
+            seg_off = p.seg[g].col0 - p.seg[g].n_begin;
+            seg_flags = p.seg[g].flags;
+          }
+        }
+        const int act = (seg_flags & MS_SEG_NO_RELU) ? 0 : p.relu;
+        const float* bch = sbias + nb;
+        uint32_t pk[16];
+        switch (act) {
+          case MS_ACT_RELU: convert_chunk<MS_ACT_RELU>(v, bch, pk); break;
+          case MS_ACT_GELU: convert_chunk<MS_ACT_GELU>(v, bch, pk); break;
+          case MS_ACT_TANH: convert_chunk<MS_ACT_TANH>(v, bch, pk); break;
+          default: convert_chunk<MS_ACT_NONE>(v, bch, pk);
+        }
+        if (nb + 32 <= p.N) {  // staged, coalesced write-back
+          uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          __syncwarp();
+          const long long col = seg_off + nb;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2), piece = lane & 3;
+            const long long orow = __shfl_sync(0xffffffffu, out_row, rr);
+            const uint4 val = *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
+            if (orow >= 0)
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(seg_ptr) + orow * seg_ld + col + piece * 8) =
+                  val;
+          }
+          __syncwarp();
+        } else if (out_row >= 0) {
+          unsigned short* d2 = reinterpret_cast<unsigned short*>(
+              reinterpret_cast<__nv_bfloat16*>(seg_ptr) + out_row * seg_ld + seg_off + nb);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < p.N) d2[j] = (unsigned short)((pk[j >> 1] >> (16 * (j & 1))) & 0xffff);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------------
+// MODE_CONV1_ROWS: the few-channel first convolution (7x7/2 over 8/16 padded
+// channels) streamed input row by input row.  One CTA owns whole images; a
+// K block is (input row hi, window half) = ONE overlapping-stride TMA box of
+// all OW output windows (128 B each).  Every input row is loaded ONCE and
+// feeds each output row whose 7-row window contains it (up to 4), each into
+// its own TMEM accumulator: 8 accumulators of 64 columns form a ring over
+// output rows, retired to the epilogue as soon as their last input row has
+// been consumed.  Versus one box per (output row, kh) this cuts the A-operand
+// (L2->SMEM) traffic ~3.4x, which is what bounds this layer (N = Cout = 64).
+constexpr int kC1Slots = 8;
+constexpr int kC1WBytes = 64 * 128;  // one (kh, half) weight block: 64 co x 64 k
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv1_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  const int KH = p.num_kb / p.smallc_halves;  // num_kb = KH * halves weight blocks
+  const int halves = p.smallc_halves;
+  const int stages = p.stages;
+  uint8_t* smW = smem;                                    // [KH*halves][8 KB], resident
+  uint8_t* smA = smW + p.num_kb * kC1WBytes;              // [stages][16 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smA + stages * kABytes);
+  uint64_t* empty = full + stages;
+  uint64_t* wbar = empty + stages;
+  uint64_t* tfull = wbar + 1;
+  uint64_t* tempty = tfull + kC1Slots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kC1Slots);
+  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);
+  sstage += (16u - (smem_addr(sstage) & 15u)) & 15u;  // 16-B aligned staging rows
+  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.H_in, OH = p.OH, OW = p.OW, S = p.stride, PAD = p.pad;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(wbar, 1);
+    for (int i = 0; i < kC1Slots; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  for (int i = threadIdx.x; i < p.N; i += blockDim.x) sbias[i] = p.bias ? p.bias[i] : 0.0f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------- TMA producer
+      mbar_arrive_expect_tx(wbar, p.num_kb * kC1WBytes);
+      for (int wb = 0; wb < p.num_kb; ++wb) tma_load_2d(smem_addr(smW + wb * kC1WBytes), &tmB, wbar, wb * kBK, 0);
+      int s = 0;
+      uint32_t phase = 0;
+      for (int img = blockIdx.x; img < p.n_img; img += gridDim.x)
+        for (int hi = 0; hi < H; ++hi)
+          for (int hf = 0; hf < halves; ++hf) {
+            mbar_wait(&empty[s], phase ^ 1);
+            mbar_arrive_expect_tx(&full[s], p.a_bytes);
+            tma_load_4d(smem_addr(smA + s * kABytes), &tmA, &full[s], hf * kBK, 0, hi, img);
+            if (++s == stages) {
+              s = 0;
+              phase ^= 1;
+            }
+          }
+    }
+  } else if (warp == 1) {  // ------------------------------------ MMA issuer
+    const uint32_t idesc = umma_idesc_bf16_m128(64);
+    mbar_wait(wbar, 0);
+    tc_fence_after();
+    int s = 0;
+    uint32_t phase = 0;
+    int rbase = 0;  // this CTA's output-row counter (ring slot = r & 7, use = r >> 3)
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, rbase += OH) {
+      for (int hi = 0; hi < H; ++hi) {
+        for (int hf = 0; hf < halves; ++hf) {
+          mbar_wait(&full[s], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
+            // kh = hi + PAD - S*oh: walk the contributing output rows directly
+            const int t0 = hi + PAD;
+            int oh_hi = S == 2 ? (t0 >> 1) : t0;             // kh = t0 - S*oh >= 0
+            int oh_lo = S == 2 ? ((t0 - KH + 2) >> 1) : t0 - KH + 1;  // kh <= KH-1
+            if (oh_lo < 0) oh_lo = 0;
+            if (oh_hi > OH - 1) oh_hi = OH - 1;
+            for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+              const int kh = t0 - S * oh;
+              const int r = rbase + oh;
+              const int slot = r & (kC1Slots - 1);
+              const int first_in = max(0, oh * S - PAD);
+              const int last_in = min(H - 1, oh * S - PAD + KH - 1);
+              const bool first = (hi == first_in) && hf == 0;
+              if (first) {  // accumulator slot must have been drained by the epilogue
+                mbar_wait(&tempty[slot], (uint32_t)(((r >> 3) & 1) ^ 1));
+                tc_fence_after();
+              }
+              const uint64_t bdesc = umma_desc_sw128(smem_addr(smW + (kh * halves + hf) * kC1WBytes));
+              const uint32_t d = tmem_base + (uint32_t)slot * 64;
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k) umma_bf16(d, adesc + 2 * k, bdesc + 2 * k, idesc, !(first && k == 0));
+              if (hi == last_in && hf == halves - 1) umma_commit(&tfull[slot]);
+            }
+            umma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {  // -------------------------------------------- epilogue warps 2..9
+    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-column chunk
+    const int ow = q * 32 + lane;
+    int rbase = 0;
+    uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
+    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, rbase += OH) {
+      for (int oh = 0; oh < OH; ++oh) {
+        const int r = rbase + oh;
+        const int slot = r & (kC1Slots - 1);
+        mbar_wait(&tfull[slot], (uint32_t)((r >> 3) & 1));
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t)(slot * 64 + c * 32) + ((uint32_t)(q * 32) << 16), v);
+        tmem_wait_ld();
+        uint32_t pk[16];
+        const float* bch = sbias + c * 32;
+        if (p.relu)
+          convert_chunk<MS_ACT_RELU>(v, bch, pk);
+        else
+          convert_chunk<MS_ACT_NONE>(v, bch, pk);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[slot]);  // TMEM slot free; data is in registers
+        uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        __syncwarp();
+        const Seg& D = p.seg[0];
+        const long long row0 = ((long long)img * OH + oh) * OW;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + (lane >> 2), piece = lane & 3;
+          const int oc = q * 32 + rr;
+          if (oc < OW)
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.ptr) + (row0 + oc) * D.ldd + D.col0 +
+                                      c * 32 + piece * 8) =
+                *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
+        }
+        __syncwarp();
+      }
+    }
+    (void)ow;
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
 // split-K finalize: D = act(ws + bias) (+ residual), bf16 or fp32, one thread
 // per 4 columns
 __global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
@@ -531,6 +942,9 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   cuuint64_t strides[1] = {(cuuint64_t)K_pad * 2};
   cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)BN};
   cuuint32_t es[2] = {1, 1};
+  P->w_ptr = W;
+  P->w_kpad = K_pad;
+  P->w_rows = N_rows_w;
   int rc = encode_map(&P->tmB, 2, W, dims, strides, box, es);
   if (rc) return rc;
   p.BN = BN;
@@ -557,6 +971,30 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   return MS_OK;
 }
 
+static int finish_conv1_rows(GemmPlan* P, const void* Wt, int num_wb) {
+  GemmParams& p = P->p;
+  cuuint64_t dims[2] = {(cuuint64_t)(num_wb * kBK), 64};
+  cuuint64_t strides[1] = {(cuuint64_t)num_wb * kBK * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, 64};
+  cuuint32_t es[2] = {1, 1};
+  int rc = encode_map(&P->tmB, 2, Wt, dims, strides, box, es);
+  if (rc) return rc;
+  p.BN = 64;
+  p.num_kb = num_wb;
+  p.ksplit = 1;
+  p.kb_per = num_wb;
+  const int fixed = 1024 + num_wb * kC1WBytes + 256 + kStageBytes + 64 * 4 + (4 + 2 * kC1Slots) * 8 + 32;
+  int stages = (226 * 1024 - fixed) / kABytes;
+  if (stages > 8) stages = 8;
+  if (stages < 2) return set_error(MS_ERR_INVALID, "conv1 rows: weights do not fit in shared memory");
+  p.stages = stages;
+  P->smem_bytes = fixed + stages * kABytes;
+  P->grid_x = p.n_img < sm_count() ? p.n_img : sm_count();
+  P->grid_y = 1;
+  P->tmem_cols = 512;
+  return MS_OK;
+}
+
 static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D, long long ldd, int col0) {
   if (nseg <= 0 || segs == nullptr) {
     p.nseg = 1;
@@ -578,6 +1016,36 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
   if (p.ksplit > 1 &&
       cudaMemsetAsync(p.ws, 0, sizeof(float) * (size_t)p.M * (size_t)p.ws_ld, stream) != cudaSuccess)
     return set_error(MS_ERR_CUDA, "split-K workspace memset failed");
+  if (p.mode == MODE_CONV1_ROWS) {
+    static int c1_attr = 0;
+    if (!c1_attr) {
+      cudaFuncSetAttribute(conv1_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      c1_attr = 1;
+    }
+    conv1_rows_kernel<<<P->grid_x, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, p);
+    return check_launch("conv1_rows_kernel");
+  }
+  if (p.pair) {
+    static int pair_attr = 0;
+    if (!pair_attr) {
+      cudaFuncSetAttribute(gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      pair_attr = 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P->grid_x, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = P->smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, gemm_tc_pair_kernel, P->tmA, P->tmB, p);
+    return check_launch("gemm_tc_pair_kernel");
+  }
   dim3 grid(P->grid_x, P->grid_y);
   gemm_tc_kernel<<<grid, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, p);
   int rc = check_launch("gemm_tc_kernel");
@@ -676,8 +1144,26 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
     cuuint64_t s5[3] = {(cuuint64_t)C * 2 * stride, (cuuint64_t)(wp * C * 2), (cuuint64_t)(wp * C * 2 * H)};
     cuuint32_t b5[4] = {(cuuint32_t)kBK, (cuuint32_t)bw, (cuuint32_t)(bh * stride), (cuuint32_t)bn};
     cuuint32_t e5[4] = {1, 1, (cuuint32_t)stride, 1};
+    // row-streaming kernel: selected with BN == 64 + bit 30 of `relu` (opt-in; measured
+    // on par with the window kernel at large batch, worse at small batch)
+    const bool rows_mode = OW <= kBM && Cout == 64 && BN == 64 && nseg <= 1 && (relu & (1 << 30));
+    relu &= ~(1 << 30);
+    p.relu = relu;
+    if (rows_mode) {  // row-streaming kernel: one box = all OW windows of one input row
+      b5[1] = (cuuint32_t)OW;
+      b5[2] = 1;
+      b5[3] = 1;
+      e5[2] = 1;
+      p.a_bytes = OW * 128;
+    }
     int rc = encode_map(&P->tmA, 4, X, d5, s5, b5, e5);
     if (rc) return rc;
+    if (rows_mode) {
+      p.mode = MODE_CONV1_ROWS;
+      p.H_in = H;
+      set_segments(p, 0, nullptr, D, ldd, col0);
+      return finish_conv1_rows(P, Wt, KH * p.smallc_halves);
+    }
   } else {
     cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
     int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es);
@@ -742,6 +1228,36 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
   p.ws_ld = ws_ld;
   const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN) * p.ksplit;
   P->grid_x = tiles < sm_count() ? tiles : sm_count();
+  return MS_OK;
+}
+
+int ms_gemm_plan_set_pair(void* plan, int enable) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  GemmParams& p = P->p;
+  if (!enable) return MS_OK;
+  if ((p.mode != MODE_DENSE && p.mode != MODE_CONV) || p.ksplit > 1 || p.residual != nullptr || p.out_fp32 ||
+      p.BN % 32 != 0)
+    return set_error(MS_ERR_INVALID, "CTA-pair mode needs a dense/conv bf16 plan without split-K/residual");
+  // the weight box becomes BN/2 rows per CTA
+  cuuint64_t dims[2] = {(cuuint64_t)P->w_kpad, (cuuint64_t)P->w_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)P->w_kpad * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)(p.BN / 2)};
+  cuuint32_t es[2] = {1, 1};
+  int rc = encode_map(&P->tmB, 2, P->w_ptr, dims, strides, box, es);
+  if (rc) return rc;
+  p.pair = 1;
+  p.b_bytes = (p.BN / 2) * kBK * 2;
+  const int per_stage = kABytes + p.b_bytes;
+  const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
+  int stages = (226 * 1024 - 1024 - 256 - 32 - kStageBytes - bias_bytes) / per_stage;
+  if (stages > 8) stages = 8;
+  p.stages = stages;
+  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + 32 + kStageBytes + bias_bytes;
+  const int m_pairs = (p.m_tiles + 1) / 2;
+  const int tiles = m_pairs * ((p.N + p.BN - 1) / p.BN);
+  const int clusters = tiles < sm_count() / 2 ? tiles : sm_count() / 2;
+  P->grid_x = 2 * clusters;
   return MS_OK;
 }
 

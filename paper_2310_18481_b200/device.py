@@ -77,6 +77,7 @@ _SIGS = {
     "ms_gemm_plan_set_residual": ([_P, _P, _LL], C.c_int),
     "ms_gemm_plan_set_splitk": ([_P, _I, _P, _LL], C.c_int),
     "ms_gemm_plan_debug": ([_P, _I], C.c_int),
+    "ms_gemm_plan_set_pair": ([_P, _I], C.c_int),
     "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
     "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),
     "ms_patchify": ([_P, _I, _I, _I, _I, _P, _P], C.c_int),
@@ -213,6 +214,12 @@ class GemmPlan:
     def run(self, stream=None):
         check(lib().ms_gemm_run(self.addr, stream_ptr(stream)), "ms_gemm_run")
 
+    def set_pair(self, enable: bool = True):
+        """Run as 2-CTA clusters (tcgen05.mma.cta_group::2, M=256 tiles)."""
+        check(lib().ms_gemm_plan_set_pair(self.addr, int(enable)), "ms_gemm_plan_set_pair")
+        self.pair = bool(enable)
+        return self
+
     def info(self):
         vals = [C.c_int() for _ in range(4)]
         check(lib().ms_gemm_plan_info(self.addr, *[C.byref(v) for v in vals]), "ms_gemm_plan_info")
@@ -255,8 +262,16 @@ def _auto_splitk(p, M, N, BN, num_kb, split_k, dev):
     return p
 
 
+def _auto_pair(p, n_m_tiles, BN, allowed):
+    """Use 2-SM CTA pairs where they measured faster (tools/gemm_bench.py):
+    wide tiles (BN >= 128) with at least two waves of 256-row tiles."""
+    if allowed and BN >= 128 and n_m_tiles >= 4 * SM_COUNT and getattr(p, "split_k", 1) == 1:
+        p.set_pair()
+    return p
+
+
 def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col0=0, ldd=None,
-               segs=None, M=None, act=None, residual=None, lda=None, split_k=None):
+               segs=None, M=None, act=None, residual=None, lda=None, split_k=None, pair=None):
     """D = act(A[M,K] @ W[N,K_pad]^T + bias) (+ residual); A row stride =
     ``lda`` or A.stride(0).  ``act`` is ACT_* (``relu=True`` == ACT_RELU)."""
     p = GemmPlan()
@@ -276,11 +291,16 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
     p.label = f"dense M={m} N={W.shape[0]} K={k}"
     if not segs or len(segs) == 1:
         _auto_splitk(p, m, W.shape[0], BN, W.shape[1] // 64, split_k, A.device)
+    if pair is not False and not out_fp32 and residual is None:
+        if pair:
+            p.set_pair()
+        else:
+            _auto_pair(p, -(-m // 128), BN, True)
     return p
 
 
 def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, bias, D, *, ldd,
-              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16)):
+              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None):
     p = GemmPlan()
     nseg, sarr = _segments(segs)
     bn, bh, bw = tile
@@ -292,6 +312,13 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
     ow = (W_in + 2 * pad - KW) // stride + 1
     p.flops = 2 * n_img * oh * ow * Cout * KH * KW * C_in
     p.label = f"conv {KH}x{KW}/{stride} {C_in}->{Cout} {n_img}x{oh}x{ow}"
+    if C_in >= 64 and pair is not False:  # not the small-channel first layer
+        if pair:
+            p.set_pair()
+        else:
+            bn_, bh_, bw_ = tile
+            tiles = -(-n_img // bn_) * -(-oh // bh_) * -(-ow // bw_)
+            _auto_pair(p, tiles, BN, True)
     return p
 
 

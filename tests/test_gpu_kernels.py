@@ -383,3 +383,41 @@ def test_gather_staged_lines_u8_and_bf16(dev, c_src, c_dst, u8, width):
     assert torch.equal(dst[:, :, pad:pad + width, :c_src], exp)
     dst[:, :, pad:pad + width, :c_src] = 0
     assert torch.count_nonzero(dst) == 0
+
+
+@pytest.mark.parametrize("M,K,N,BN", [(1000, 1024, 256, 256), (300, 192, 96, 96), (128, 64, 64, 64), (517, 576, 352, 192)])
+def test_gemm_cta_pair_dense_vs_torch(dev, M, K, N, BN):
+    """2-CTA clusters (tcgen05.mma.cta_group::2, M=256 tiles)."""
+    g = torch.Generator().manual_seed(M + 3 * N)
+    A = _bf(torch.randn(M, K, generator=g)).cuda()
+    W = _bf(torch.randn(N, K, generator=g) * 0.05).cuda()
+    b = (torch.randn(N, generator=g) * 0.1).cuda()
+    D = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_dense(A, W, b, D, BN=BN, relu=True, split_k=1).set_pair()
+    p.run()
+    torch.cuda.synchronize()
+    ref = (A.float().cpu() @ W.float().cpu().T + b.cpu()).clamp_min(0)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout,k,s,pad,tile,BN", [
+    (4, 56, 64, 192, 3, 1, 1, (1, 8, 16), 192), (3, 28, 96, 96, 3, 2, 1, (1, 7, 14), 96),
+    (5, 7, 160, 224, 3, 1, 1, (2, 7, 7), 224),
+])
+def test_conv_cta_pair_vs_torch(dev, n, H, Cin, Cout, k, s, pad, tile, BN):
+    g = torch.Generator().manual_seed(n * H + Cin + 1)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, k, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    OH = (H + 2 * pad - k) // s + 1
+    D = torch.zeros(n * OH * OH, Cout, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, k, k, s, pad, packed.cuda(), Cout, b.cuda(), D, ldd=Cout,
+                      BN=BN, relu=True, tile=tile).set_pair()
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=s, padding=pad).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)

@@ -50,8 +50,17 @@ cases = [conv(288, 56, 64, 192, 3, 1, 192), conv(288, 56, 64, 192, 3, 1, 96),
          conv(288, 14, 160, 224, 3, 1, 224), conv(288, 7, 192, 320, 3, 1, 160),
          dense(903168, 64, 64, 64), dense(225792, 256, 256, 256), dense(73728, 576, 512, 256),
          dense(8192, 4096, 4096, 256)]
+rows = []
 for p, label in cases:
     us = t_plan(p)
+    try:
+        p.set_pair()
+        us_pair = t_plan(p)
+    except Exception as exc:  # plans the pair kernel does not support
+        us_pair = float("nan")
+        print("  pair n/a:", exc)
+    print(f"{us:8.1f} us {p.flops / us / 1e6:7.1f} TF/s | pair {us_pair:8.1f} us {p.flops / us_pair / 1e6:7.1f} TF/s  {label}")
+    continue
     dv.check(dv.lib().ms_gemm_plan_debug(p.addr, 1), "debug")
     us_ns = t_plan(p)
     dv.check(dv.lib().ms_gemm_plan_debug(p.addr, 0), "debug")
