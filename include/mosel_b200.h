@@ -59,6 +59,10 @@ typedef struct MsSegment {
 #define MS_SEG_NO_RELU 1
 
 int ms_abi_version(void);
+/* Programmatic dependent launch for op-program kernels (default on): the
+ * next kernel's prologue overlaps the previous kernel's tail.  Returns the
+ * previous setting. */
+int ms_set_pdl(int enable);
 const char* ms_last_error(void);
 int ms_device_sync(void);
 

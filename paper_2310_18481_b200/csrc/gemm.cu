@@ -186,6 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: this prologue overlapped the previous kernel's tail.  Trigger only
+  // once TMEM is held: a dependent CTA that allocated first on this SM while
+  // waiting for us would otherwise deadlock our tcgen05.alloc.
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -519,6 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync_all();  // barrier inits + TMEM allocation visible to the pair
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------- TMA producer (both CTAs)
@@ -749,6 +756,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------------------------------- TMA producer
@@ -866,8 +875,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // split-K finalize: D = act(ws + bias) (+ residual), bf16 or fp32, one thread
-// per 4 columns
+// per 4 columns.  It re-zeroes the workspace as it reads it, so the next
+// launch needs no memset (the plan's workspace starts zeroed).
 __global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int n4 = (p.N + 3) / 4;
   const long long total = (long long)p.M * n4;
   const Seg& S = p.seg[0];
@@ -875,7 +887,9 @@ __global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
        t += (long long)gridDim.x * blockDim.x) {
     const long long row = t / n4;
     const int n = (int)(t - row * n4) * 4;
-    const float4 a = *reinterpret_cast<const float4*>(p.ws + row * p.ws_ld + n);
+    float4* wsp = reinterpret_cast<float4*>(p.ws + row * p.ws_ld + n);
+    const float4 a = *wsp;
+    *wsp = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // leave the workspace zeroed for the next launch
     const float av[4] = {a.x, a.y, a.z, a.w};
     for (int j = 0; j < 4 && n + j < p.N; ++j) {
       float x = activate(av[j] + (p.bias ? p.bias[n + j] : 0.0f), p.relu);
@@ -1013,16 +1027,13 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
     attr_set = 1;
   }
   const GemmParams& p = P->p;
-  if (p.ksplit > 1 &&
-      cudaMemsetAsync(p.ws, 0, sizeof(float) * (size_t)p.M * (size_t)p.ws_ld, stream) != cudaSuccess)
-    return set_error(MS_ERR_CUDA, "split-K workspace memset failed");
   if (p.mode == MODE_CONV1_ROWS) {
     static int c1_attr = 0;
     if (!c1_attr) {
       cudaFuncSetAttribute(conv1_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       c1_attr = 1;
     }
-    conv1_rows_kernel<<<P->grid_x, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, p);
+    launch_k(conv1_rows_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p);
     return check_launch("conv1_rows_kernel");
   }
   if (p.pair) {
@@ -1031,29 +1042,16 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
       cudaFuncSetAttribute(gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       pair_attr = 1;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P->grid_x, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = P->smem_bytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, gemm_tc_pair_kernel, P->tmA, P->tmB, p);
+    launch_k(gemm_tc_pair_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 2, P->tmA, P->tmB, p);
     return check_launch("gemm_tc_pair_kernel");
   }
-  dim3 grid(P->grid_x, P->grid_y);
-  gemm_tc_kernel<<<grid, kThreads, P->smem_bytes, stream>>>(P->tmA, P->tmB, p);
+  launch_k(gemm_tc_kernel, dim3(P->grid_x, P->grid_y), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p);
   int rc = check_launch("gemm_tc_kernel");
   if (rc || p.ksplit <= 1) return rc;
   const long long work = (long long)p.M * ((p.N + 3) / 4);
   long long blocks = (work + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  splitk_finalize_kernel<<<(int)blocks, 256, 0, stream>>>(p);
+  launch_k(splitk_finalize_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, 1, p);
   return check_launch("splitk_finalize_kernel");
 }
 

@@ -12,6 +12,7 @@
 namespace mosel {
 
 static thread_local char g_err[512] = "";
+int g_pdl = 1;
 
 int set_error(int code, const char* msg) {
   snprintf(g_err, sizeof g_err, "%s", msg);
@@ -34,6 +35,8 @@ __global__ void pool2d_kernel(const __nv_bfloat16* __restrict__ X, int n_img, in
                               long long xcs, int k, int stride, int pad, int OH, int OW, int is_max,
                               __nv_bfloat16* __restrict__ Y, long long ycs, int ycol0,
                               const float* __restrict__ bias, int relu) {
+  pdl_trigger();
+  pdl_wait();
   const int cg = C / 8;
   const long long total = (long long)n_img * OH * OW * cg;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -105,6 +108,8 @@ template <bool MAX, int STRIDE>
 __global__ void __launch_bounds__(512) pool3_rows_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C, long long xcs,
                                   int pad, int OH, int OW, int TH, __nv_bfloat16* __restrict__ Y,
                                   long long ycs, int ycol0, const float* __restrict__ bias, int relu) {
+  pdl_trigger();
+  pdl_wait();
   const int cg = C / 8;
   const int t = blockIdx.z * blockDim.x + threadIdx.x;  // (column, channel group)
   if (t >= cg * OW) return;
@@ -179,6 +184,8 @@ static int pool_out(int in, int k, int stride, int pad, int ceil_mode) {
 __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H, int W, int C, int KH,
                               int KW, int stride, int pad, int OH, int OW, __nv_bfloat16* __restrict__ out,
                               int K_pad) {
+  pdl_trigger();
+  pdl_wait();
   const int k8n = K_pad / 8;
   const long long total = (long long)n_img * OH * OW * k8n;
   const int kreal = KH * KW * C;
@@ -222,29 +229,49 @@ __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ X, int n_img, in
 }
 
 // ----------------------------------------- global pool + segment consensus
-__global__ void segment_mean_kernel(const __nv_bfloat16* __restrict__ X, int n_req, int S, int HW, int C,
-                                    __nv_bfloat16* __restrict__ Y, long long y_ld) {
+// Y[r, c] = mean over the S*HW pixels of request r's S frames.  One CTA per
+// (request, 32 channel groups = 256 channels); its 256 threads are 32 channel
+// groups x 8 pixel slices (each warp reads 512 contiguous bytes per row),
+// reduced through shared memory.
+constexpr int kSegSlices = 8;
+__global__ void __launch_bounds__(256) segment_mean_kernel(const __nv_bfloat16* __restrict__ X, int n_req, int S,
+                                                           int HW, int C, __nv_bfloat16* __restrict__ Y,
+                                                           long long y_ld) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float part[kSegSlices][32][9];
   const int cg = C / 8;
-  const long long total = (long long)n_req * cg;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(t % cg);
-    const long long r = t / cg;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long rows = (long long)S * HW;
+  const int lane = threadIdx.x & 31, slice = threadIdx.x >> 5;
+  const int g = blockIdx.y * 32 + lane;
+  const long long r = blockIdx.x;
+  const long long rows = (long long)S * HW;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (g < cg) {
     const __nv_bfloat16* base = X + r * rows * C + g * 8;
-    for (long long p = 0; p < rows; ++p) {
+    for (long long p = slice; p < rows; p += kSegSlices) {
       const uint4 v = *reinterpret_cast<const uint4*>(base + p * C);
       const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(e[j]);
     }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[slice][lane][j] = acc[j];
+  __syncthreads();
+  if (slice == 0 && g < cg) {
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = 0.0f;
+    // fixed summation order (slice 0..7) keeps the result deterministic
+    for (int q = 0; q < kSegSlices; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] += part[q][lane][j];
     const float s = 1.0f / (float)rows;
     uint4 o;
-    o.x = pack_bf16x2(acc[0] * s, acc[1] * s);
-    o.y = pack_bf16x2(acc[2] * s, acc[3] * s);
-    o.z = pack_bf16x2(acc[4] * s, acc[5] * s);
-    o.w = pack_bf16x2(acc[6] * s, acc[7] * s);
+    o.x = pack_bf16x2(t[0] * s, t[1] * s);
+    o.y = pack_bf16x2(t[2] * s, t[3] * s);
+    o.z = pack_bf16x2(t[4] * s, t[5] * s);
+    o.w = pack_bf16x2(t[6] * s, t[7] * s);
     *reinterpret_cast<uint4*>(Y + r * y_ld + g * 8) = o;
   }
 }
@@ -348,21 +375,21 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
     auto X = reinterpret_cast<const __nv_bfloat16*>(a.X);
     auto Y = reinterpret_cast<__nv_bfloat16*>(a.Y);
     if (a.is_max && a.stride == 2)
-      pool3_rows_kernel<true, 2><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+      launch_k(pool3_rows_kernel<true, 2>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
                                                         a.ycol0, a.bias, a.relu);
     else if (a.is_max)
-      pool3_rows_kernel<true, 1><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+      launch_k(pool3_rows_kernel<true, 1>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
                                                         a.ycol0, a.bias, a.relu);
     else if (a.stride == 2)
-      pool3_rows_kernel<false, 2><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+      launch_k(pool3_rows_kernel<false, 2>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
                                                          a.ycol0, a.bias, a.relu);
     else
-      pool3_rows_kernel<false, 1><<<grid, block, 0, st>>>(X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
+      launch_k(pool3_rows_kernel<false, 1>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
                                                          a.ycol0, a.bias, a.relu);
     return check_launch("pool3_rows_kernel");
   }
   const long long work = (long long)a.n_img * OH * OW * (a.C / 8);
-  pool2d_kernel<<<grid_for(work, 256), 256, 0, st>>>(
+  launch_k(pool2d_kernel, dim3(grid_for(work, 256)), dim3(256), 0, st, 1,
       reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H, a.W, a.C, a.xcs, a.k, a.stride, a.pad, OH, OW,
       a.is_max, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0, a.bias, a.relu);
   return check_launch("pool2d_kernel");
@@ -373,7 +400,7 @@ static int run_im2col(const Im2colArgs& a, cudaStream_t st) {
   const int OW = (a.W + 2 * a.pad - a.KW) / a.stride + 1;
   if (a.K_pad % 8 != 0) return set_error(MS_ERR_INVALID, "im2col K_pad must be a multiple of 8");
   const long long work = (long long)a.n_img * OH * OW * (a.K_pad / 8);
-  im2col_kernel<<<grid_for(work, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H,
+  launch_k(im2col_kernel, dim3(grid_for(work, 256)), dim3(256), 0, st, 1, reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H,
                                                       a.W, a.C, a.KH, a.KW, a.stride, a.pad, OH, OW,
                                                       reinterpret_cast<__nv_bfloat16*>(a.out), a.K_pad);
   return check_launch("im2col_kernel");
@@ -381,8 +408,9 @@ static int run_im2col(const Im2colArgs& a, cudaStream_t st) {
 
 static int run_segmean(const SegArgs& a, cudaStream_t st) {
   if (a.C % 8 != 0 || a.y_ld % 8 != 0) return set_error(MS_ERR_INVALID, "segment_mean needs C % 8 == 0");
-  const long long work = (long long)a.n_req * (a.C / 8);
-  segment_mean_kernel<<<grid_for(work, 128), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_req,
+  if (a.n_req <= 0) return MS_OK;
+  const dim3 grid((unsigned)a.n_req, (unsigned)((a.C / 8 + 31) / 32));
+  launch_k(segment_mean_kernel, grid, dim3(256), 0, st, 1, reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_req,
                                                             a.S, a.HW, a.C, reinterpret_cast<__nv_bfloat16*>(a.Y),
                                                             a.y_ld);
   return check_launch("segment_mean_kernel");
@@ -395,6 +423,11 @@ using namespace mosel;
 extern "C" {
 
 int ms_abi_version(void) { return 1; }
+int ms_set_pdl(int enable) {
+  const int prev = g_pdl;
+  g_pdl = enable ? 1 : 0;
+  return prev;
+}
 const char* ms_last_error(void) { return g_err; }
 int ms_device_sync(void) {
   cudaError_t e = cudaDeviceSynchronize();

@@ -69,6 +69,8 @@ template <int CH>
 __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ X, long long ldx, long long rows,
                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                  __nv_bfloat16* __restrict__ Y, long long ldy, int C, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (row >= rows) return;
   ln_row<CH>(X + row * ldx, Y + row * ldy, gamma, beta, C, eps, threadIdx.x & 31);
@@ -103,6 +105,8 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], 
 __global__ void __launch_bounds__(128) attention_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int L,
                                                         int H, __nv_bfloat16* __restrict__ out, long long ldo,
                                                         float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ __align__(16) __nv_bfloat16 sQ[kBq][kHd + kPad];
   __shared__ __align__(16) __nv_bfloat16 sK[kBk][kHd + kPad];
   __shared__ __align__(16) __nv_bfloat16 sV[kBk][kHd + kPad];
@@ -235,6 +239,8 @@ __global__ void __launch_bounds__(128) attention_kernel(const __nv_bfloat16* __r
 // requires P*C % 8 == 0 (16-B vectors along each patch row).
 __global__ void patchify_kernel(const __nv_bfloat16* __restrict__ X, int n, int S, int C, int P,
                                 __nv_bfloat16* __restrict__ Y) {
+  pdl_trigger();
+  pdl_wait();
   const int G = S / P, row_elems = P * P * C, c8 = row_elems / 8;
   const long long total = (long long)n * G * G * c8;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -253,6 +259,8 @@ __global__ void patchify_kernel(const __nv_bfloat16* __restrict__ X, int n, int 
 __global__ void vit_embed_kernel(const __nv_bfloat16* __restrict__ pe, const __nv_bfloat16* __restrict__ cls,
                                  const __nv_bfloat16* __restrict__ pos, int n, int L, int D,
                                  __nv_bfloat16* __restrict__ tok) {
+  pdl_trigger();
+  pdl_wait();
   const int d8 = D / 8;
   const long long total = (long long)n * L * d8;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -281,6 +289,8 @@ __global__ void bert_embed_kernel(const int32_t* __restrict__ ids, long long n_t
                                   const __nv_bfloat16* __restrict__ word, const __nv_bfloat16* __restrict__ pos,
                                   const __nv_bfloat16* __restrict__ type0, const float* __restrict__ gamma,
                                   const float* __restrict__ beta, __nv_bfloat16* __restrict__ Y, int D, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (tok >= n_tok) return;
   const int lane = threadIdx.x & 31;
@@ -341,10 +351,10 @@ int run_layernorm(const void* X, long long ldx, long long rows, const float* gam
   auto Xp = reinterpret_cast<const __nv_bfloat16*>(X);
   auto Yp = reinterpret_cast<__nv_bfloat16*>(Y);
   switch (C / 256) {
-    case 1: layernorm_kernel<1><<<blocks, 256, 0, st>>>(Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
-    case 2: layernorm_kernel<2><<<blocks, 256, 0, st>>>(Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
-    case 3: layernorm_kernel<3><<<blocks, 256, 0, st>>>(Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
-    case 4: layernorm_kernel<4><<<blocks, 256, 0, st>>>(Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
+    case 1: launch_k(layernorm_kernel<1>, dim3((unsigned)blocks), dim3(256), 0, st, 1, Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
+    case 2: launch_k(layernorm_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, st, 1, Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
+    case 3: launch_k(layernorm_kernel<3>, dim3((unsigned)blocks), dim3(256), 0, st, 1, Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
+    case 4: launch_k(layernorm_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, st, 1, Xp, ldx, rows, gamma, beta, Yp, ldy, C, eps); break;
     default: return set_error(MS_ERR_INVALID, "layernorm: unsupported C");
   }
   return check_launch("layernorm_kernel");
@@ -356,7 +366,7 @@ int run_attention(const void* qkv, long long ld, int L, int H, int n_seq, void* 
     return set_error(MS_ERR_INVALID, "attention: bad shape/stride");
   if (n_seq == 0) return MS_OK;
   dim3 grid((L + kBq - 1) / kBq, H, n_seq);
-  attention_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), ld, L, H,
+  launch_k(attention_kernel, grid, dim3(128), 0, st, 1, reinterpret_cast<const __nv_bfloat16*>(qkv), ld, L, H,
                                          reinterpret_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
   return check_launch("attention_kernel");
 }
@@ -364,7 +374,7 @@ int run_attention(const void* qkv, long long ld, int L, int H, int n_seq, void* 
 int run_patchify(const void* X, int n, int S, int C, int P, void* Y, cudaStream_t st) {
   if ((P * C) % 8 != 0 || S % P != 0) return set_error(MS_ERR_INVALID, "patchify: P*C % 8 == 0, S % P == 0");
   const long long work = (long long)n * (S / P) * (S / P) * P * P * C / 8;
-  patchify_kernel<<<grid_cap(work, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(X), n, S, C, P,
+  launch_k(patchify_kernel, dim3(grid_cap(work, 256)), dim3(256), 0, st, 1, reinterpret_cast<const __nv_bfloat16*>(X), n, S, C, P,
                                                        reinterpret_cast<__nv_bfloat16*>(Y));
   return check_launch("patchify_kernel");
 }
@@ -372,7 +382,7 @@ int run_patchify(const void* X, int n, int S, int C, int P, void* Y, cudaStream_
 int run_vit_embed(const void* pe, const void* cls, const void* pos, int n, int L, int D, void* tok, cudaStream_t st) {
   if (D % 8 != 0) return set_error(MS_ERR_INVALID, "vit_embed: D % 8 == 0");
   const long long work = (long long)n * L * D / 8;
-  vit_embed_kernel<<<grid_cap(work, 256), 256, 0, st>>>(
+  launch_k(vit_embed_kernel, dim3(grid_cap(work, 256)), dim3(256), 0, st, 1, 
       reinterpret_cast<const __nv_bfloat16*>(pe), reinterpret_cast<const __nv_bfloat16*>(cls),
       reinterpret_cast<const __nv_bfloat16*>(pos), n, L, D, reinterpret_cast<__nv_bfloat16*>(tok));
   return check_launch("vit_embed_kernel");
@@ -383,7 +393,7 @@ int run_bert_embed(const int32_t* ids, long long n_tok, int L, const void* word,
   if (D != 768) return set_error(MS_ERR_INVALID, "bert_embed: D must be 768");
   if (n_tok <= 0) return MS_OK;
   const long long blocks = (n_tok * 32 + 255) / 256;
-  bert_embed_kernel<3><<<blocks, 256, 0, st>>>(ids, n_tok, L, reinterpret_cast<const __nv_bfloat16*>(word),
+  launch_k(bert_embed_kernel<3>, dim3((unsigned)blocks), dim3(256), 0, st, 1, ids, n_tok, L, reinterpret_cast<const __nv_bfloat16*>(word),
                                                reinterpret_cast<const __nv_bfloat16*>(pos),
                                                reinterpret_cast<const __nv_bfloat16*>(type0), gamma, beta,
                                                reinterpret_cast<__nv_bfloat16*>(Y), D, eps);

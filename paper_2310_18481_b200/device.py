@@ -43,6 +43,7 @@ class RowDesc(C.Structure):
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
 _SIGS = {
     "ms_abi_version": ([], C.c_int),
+    "ms_set_pdl": ([_I], C.c_int),
     "ms_last_error": ([], C.c_char_p),
     "ms_device_sync": ([], C.c_int),
     "ms_policy_select": ([_P, _P, _P, _I, _P, C.c_int64, _D, _I, _P, _P], C.c_int),
@@ -105,6 +106,12 @@ def lib():
             fn.restype = res
         _lib = h
     return _lib
+
+
+def set_pdl(enable: bool) -> bool:
+    """Programmatic dependent launch for op-program kernels (default on);
+    returns the previous setting.  Affects plans launched afterwards."""
+    return bool(lib().ms_set_pdl(int(bool(enable))))
 
 
 def check(rc: int, what: str) -> None:
@@ -255,7 +262,8 @@ def _auto_splitk(p, M, N, BN, num_kb, split_k, dev):
             split_k = max(1, min(num_kb // 4, SM_COUNT // tiles))
     if split_k > 1:
         ws_ld = -(-N // 4) * 4
-        ws = torch.empty(M, ws_ld, dtype=torch.float32, device=dev)
+        # zeroed once; the finalize kernel re-zeroes it after every launch
+        ws = torch.zeros(M, ws_ld, dtype=torch.float32, device=dev)
         check(lib().ms_gemm_plan_set_splitk(p.addr, split_k, ws.data_ptr(), ws_ld), "ms_gemm_plan_set_splitk")
         p.keep.append(ws)
         p.split_k = split_k
@@ -414,7 +422,74 @@ class Program:
 
     @property
     def n_launches(self) -> int:
-        return len(self.ops)
+        # a split-K GEMM is two launches (tiles + finalize)
+        return sum(2 if k == "gemm" and getattr(a, "split_k", 1) > 1 else 1 for k, a in self.ops)
+
+
+class StagedProgram:
+    """Native programs arranged as a sequence of stages; a stage's lanes are
+    independent (e.g. the branches of an Inception block) and run
+    concurrently on side streams, forked from and joined back into the
+    calling stream.  Captured in a CUDA graph this is a DAG, so small-batch
+    branches fill SMs the trunk leaves idle.  ``streams``/``events`` are
+    shared by every program of one encoder (its programs never overlap)."""
+
+    def __init__(self, lanes_ctx):
+        self.stages = []  # list[list[Program]]
+        self.ctx = lanes_ctx
+
+    def stage(self, *lanes):
+        lanes = [p for p in lanes if p is not None and p.ops]
+        if lanes:
+            self.stages.append(lanes)
+        return self
+
+    def seal(self):
+        for lanes in self.stages:
+            for p in lanes:
+                p.seal()
+        return self
+
+    @property
+    def ops(self):
+        return [op for lanes in self.stages for p in lanes for op in p.ops]
+
+    @property
+    def keep(self):
+        return [k for lanes in self.stages for p in lanes for k in p.keep]
+
+    @property
+    def n_launches(self) -> int:
+        return sum(p.n_launches for lanes in self.stages for p in lanes)
+
+    def run(self, stream=None):
+        torch = _torch()
+        main = torch.cuda.current_stream() if stream is None else stream
+        side, ev_fork, ev_join = self.ctx.streams, self.ctx.fork, self.ctx.join
+        for lanes in self.stages:
+            if len(lanes) == 1 or not self.ctx.concurrent:
+                for p in lanes:
+                    p.run(main)
+                continue
+            ev_fork.record(main)
+            for i, p in enumerate(lanes[1:]):
+                side[i].wait_event(ev_fork)
+                p.run(side[i])
+                ev_join[i].record(side[i])
+            lanes[0].run(main)
+            for i in range(len(lanes) - 1):
+                main.wait_event(ev_join[i])
+
+
+class LaneContext:
+    """Side streams + fork/join events for StagedProgram lanes."""
+
+    def __init__(self, n_side: int = 2, concurrent: bool = True):
+        torch = _torch()
+        self.concurrent = concurrent  # False: lanes run one after another (A/B)
+        self.streams = [torch.cuda.Stream() for _ in range(n_side)]
+        self.fork = torch.cuda.Event()
+        self.join = [torch.cuda.Event() for _ in range(n_side)]
 
 
 # ------------------------------------------------------------------ events

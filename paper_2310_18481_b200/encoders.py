@@ -295,6 +295,7 @@ class BNInceptionEncoder:
         self._pack()
         self._alloc()
         self._programs = {}
+        self._lanes = None  # side streams for the Inception branch lanes
 
     # -- weights on device
     def _pack(self):
@@ -374,7 +375,13 @@ class BNInceptionEncoder:
         return prog
 
     def _build(self, n_req: int):
+        """Trunk (stem, each block's merged 1x1, final pool) plus, per
+        Inception block, three concurrent lanes: the double-3x3 chain, the
+        3x3 branch and the pool branch (``device.StagedProgram``)."""
         from . import device as dv
+        if self._lanes is None:
+            self._lanes = dv.LaneContext(2)
+        SP = dv.StagedProgram(self._lanes)
         P = dv.Program()
         n = n_req * self.S
         size = self.mod.size
@@ -400,14 +407,20 @@ class BNInceptionEncoder:
         for L in self.layers:
             if L["kind"] != "block":
                 continue
-            self._block(P, L, n, h, c, cur, nxt)
+            lanes = self._block(P, L, n, h, c, cur, nxt)
+            SP.stage(P)
+            SP.stage(*lanes)
+            P = dv.Program()
             h = conv_out(h, 3, L["s"], 1) if L["s"] == 2 else h
             c = L["cout"]
             cur, nxt = nxt, cur
         P.segment_mean(cur, n_req, self.S, h * h, c, self.out, FEAT_DIM)
-        return P.seal()
+        SP.stage(P)
+        return SP.seal()
 
     def _block(self, P, L, n, h, cin, X, Y):
+        """Append the block's merged 1x1 GEMM to the trunk ``P``; return its
+        independent branch lanes (longest first: it stays on the trunk stream)."""
         from . import device as dv
         name, s = L["name"], L["s"]
         c1, c3r, c3, cdr, cd, proj = L["c1"], L["c3r"], L["c3"], L["cdr"], L["cd"], L["proj"]
@@ -438,27 +451,31 @@ class BNInceptionEncoder:
         tile_in = pick_conv_tile(n, h, h)
         tile_out = pick_conv_tile(n, o, o)
         # 3x3 branch (stride s) -> Y[:, c1 : c1+c3]
-        P.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
-                            self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
-                            tile=tile_out))
+        B3 = dv.Program()
+        B3.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
+                             self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
+                             tile=tile_out))
         # double 3x3: stride 1 then stride s -> Y[:, c1+c3 : c1+c3+cd]
-        P.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
-                            self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
-                            tile=tile_in))
-        P.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
-                            self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
-                            relu=True, tile=tile_out))
+        BD = dv.Program()
+        BD.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
+                             self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
+                             tile=tile_in))
+        BD.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
+                             self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
+                             relu=True, tile=tile_out))
         pc = c1 + c3 + cd
+        BP = dv.Program()
         if fold_pool:  # avgpool of the projected (pre-bias) branch + bias + ReLU
-            P.pool(Tq, n, h, h, proj, proj, 3, 1, 1, False, False, Yv, cout, pc,
-                   bias=self.b[name + "/pool_proj"], relu=True)
+            BP.pool(Tq, n, h, h, proj, proj, 3, 1, 1, False, False, Yv, cout, pc,
+                    bias=self.b[name + "/pool_proj"], relu=True)
         elif proj:  # max pool does not commute with the projection
             Tp = self.tp[: pix_in * cin].view(pix_in, cin)
-            P.pool(Xv, n, h, h, cin, cin, 3, 1, 1, False, True, Tp, cin, 0)
-            P.gemm(dv.plan_dense(Tp, self.w[name + "/pool_proj"], self.b[name + "/pool_proj"], Yv,
-                                 M=pix_in, K=cin, BN=pick_bn(proj), relu=True, col0=pc, ldd=cout))
+            BP.pool(Xv, n, h, h, cin, cin, 3, 1, 1, False, True, Tp, cin, 0)
+            BP.gemm(dv.plan_dense(Tp, self.w[name + "/pool_proj"], self.b[name + "/pool_proj"], Yv,
+                                  M=pix_in, K=cin, BN=pick_bn(proj), relu=True, col0=pc, ldd=cout))
         else:  # stride-2 max-pool pass-through into the concat
-            P.pool(Xv, n, h, h, cin, cin, 3, 2, 0, True, True, Yv, cout, pc)
+            BP.pool(Xv, n, h, h, cin, cin, 3, 2, 0, True, True, Yv, cout, pc)
+        return [BD, B3, BP]
 
     def flops(self, n_req: int) -> int:
         return n_req * request_flops(self.mod, self.S)

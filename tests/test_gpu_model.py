@@ -90,6 +90,31 @@ def test_tbn_graph_replay_matches_eager(built):
     assert torch.equal(a, b) and torch.equal(b, c)
 
 
+def test_tbn_pdl_and_branch_lanes_bitwise_stable(built):
+    """Programmatic dependent launch and the concurrent Inception branch
+    lanes change only scheduling: logits are bitwise identical with PDL off
+    (serial launches), on (eager) and on (CUDA graph with lane fork/join)."""
+    from paper_2310_18481_b200 import device as dv
+    from paper_2310_18481_b200.executor import build_tbn_model
+    model = build_tbn_model(max_req=12, n_slots=12)
+    rng = np.random.default_rng(3)
+    masks = rng.integers(1, 8, size=12)
+    slots = rng.permutation(12)
+    prev = dv.set_pdl(False)
+    try:
+        model.use_graphs = False
+        a = model.forward(slots, masks).clone()
+        dv.set_pdl(True)
+        b = model.forward(slots, masks).clone()
+        model.use_graphs = True
+        c = model.forward(slots, masks).clone()
+        d = model.forward(slots, masks).clone()
+    finally:
+        dv.set_pdl(prev)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(b, c) and torch.equal(c, d)
+
+
 def test_realtime_serving_batched_and_host_io(built):
     """Wall-clock serving on the device: every request accounted for, each
     completed job met its accuracy floor, batching merged jobs, and the
