@@ -43,8 +43,8 @@ extern "C" {
 #define MS_ERR_INVALID 1
 #define MS_ERR_CUDA 2
 
-#define MS_GEMM_PLAN_BYTES 1024
-#define MS_OP_BYTES 1152
+#define MS_GEMM_PLAN_BYTES 2048
+#define MS_OP_BYTES 2112
 
 #define MS_DROP (-1)
 
@@ -148,6 +148,10 @@ int ms_gemm_run(const void* plan, void* stream);
 int ms_gemm_plan_set_pair(void* plan, int enable);
 /* profiling aid: bit0 = skip the epilogue stores (mainloop-only timing) */
 int ms_gemm_plan_debug(void* plan, int flags);
+/* Debug: per-CTA %globaltimer stamps (8 x u64 per CTA: entry, prologue done,
+ * PDL wait done, first TMA issued, first data ready, last MMA commit, first
+ * accumulator ready, epilogue done) into buf[grid_x * 8], or NULL to stop. */
+int ms_gemm_plan_set_trace(void* plan, unsigned long long* buf);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
 
 /* ---- HBM-bound ops (NHWC bf16) ---------------------------------------- */

@@ -91,11 +91,36 @@ struct GemmParams {
   int ksplit, kb_per;
   float* ws;
   long long ws_ld;
+  unsigned long long* trace;  // debug: per-CTA %globaltimer stamps (kTraceSlots each) or null
+  int tma_store;    // 1: bf16 epilogue writes each 128 x 32 chunk with one TMA store (StoreMaps)
+  int stage_bytes;  // epilogue staging bytes in shared memory
 };
+
+// One bf16 output tensor map per epilogue segment (TMA stores, SWIZZLE_64B):
+// DENSE/GATHER 2-D {cols, M} box {32, 128}; CONV 4-D {cols, OW, OH, n} box
+// {32, bw, bh, bn}, so a conv tile's rows land at their (n, oh, ow) pixels and
+// out-of-range rows/columns are clipped by the TMA unit.
+struct alignas(64) StoreMaps {
+  CUtensorMap m[4];
+};
+constexpr int kStoreChunkBytes = kBM * 64;            // 128 rows x 32 bf16
+constexpr int kStoreBytes = 2 * kStoreChunkBytes;     // one chunk buffer per column group
+constexpr int kTraceSlots = 12;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GEMM_TRACE(slot)                                                      \
+  do {                                                                        \
+    if (p.trace != nullptr) p.trace[blockIdx.x * kTraceSlots + (slot)] = gtimer(); \
+  } while (0)
 
 struct alignas(64) GemmPlan {
   CUtensorMap tmA;
   CUtensorMap tmB;
+  StoreMaps tmD;
   GemmParams p;
   int grid_x, grid_y, smem_bytes, tmem_cols;
   const void* w_ptr;  // weight tensor (re-encoded for CTA-pair half boxes)
@@ -133,13 +158,39 @@ __device__ __forceinline__ TileIdx decode_tile(const GemmParams& p, int t, int n
   return r;
 }
 
+// Epilogue flavours (template parameter EPI):
+//   EPI_TMA    bf16 output, each 128 x 32 chunk staged (SW64) and written by one
+//              TMA store per 32-column chunk; up to 4 segments; optional residual
+//   EPI_F32    fp32 output, direct per-thread stores (logits heads)
+//   EPI_SPLITK fp32 partial sums -> workspace atomics (finalize applies bias/act)
+enum GemmEpi : int { EPI_TMA = 0, EPI_F32 = 1, EPI_SPLITK = 2 };
+
+template <int ACT>
+__device__ __forceinline__ void convert_chunk4(const uint32_t (&v)[32], const float* bch, uint32_t (&pk)[16]) {
+  const float4* b4 = reinterpret_cast<const float4*>(bch);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 b = b4[q];
+    pk[2 * q] = pack_bf16x2(activate(__uint_as_float(v[4 * q]) + b.x, ACT),
+                            activate(__uint_as_float(v[4 * q + 1]) + b.y, ACT));
+    pk[2 * q + 1] = pack_bf16x2(activate(__uint_as_float(v[4 * q + 2]) + b.z, ACT),
+                                activate(__uint_as_float(v[4 * q + 3]) + b.w, ACT));
+  }
+}
+
+// One kernel instantiation per (A-operand mode, epilogue, activation): each
+// carries only its own code (the generic kernel's every-mode/every-activation
+// epilogue was instruction-latency bound at ~1 us per 32-column chunk).
+template <int MODE, int EPI, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ GemmParams p) {
+                   const __grid_constant__ GemmParams p, const __grid_constant__ StoreMaps tmD) {
   // Persistent: CTA b processes tiles b, b + grid, ...; tile t -> (m = t / n_tiles,
   // n = t % n_tiles).  The smem ring (full/empty) and the two TMEM accumulator
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
+  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC;
+  if (threadIdx.x == 0) GEMM_TRACE(0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
   // (a uintptr_t round trip would turn every smem access into a generic LD)
@@ -147,13 +198,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stages = p.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + stages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + stages * p.b_bytes);
+  uint8_t* sstage = smB + stages * p.b_bytes;  // [p.stage_bytes], 1024-B aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sstage + p.stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);  // [kStageBytes], 16-B aligned
-  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);  // [N]
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [N], 16-B aligned
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -161,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_tiles = p.m_tiles * n_tiles * p.ksplit;
 
   if (threadIdx.x == 0) {
-    const uint32_t full_count = (p.mode == MODE_GATHER) ? 1 + 128 : 1;
+    const uint32_t full_count = (MODE == MODE_GATHER) ? 1 + 128 : 1;
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], full_count);
       mbar_init(&empty[s], 1);
@@ -173,15 +224,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    if (p.mode != MODE_GATHER) tma_prefetch_desc(&tmA);
+    if (MODE != MODE_GATHER) tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
   uint32_t acc_stride = 32;
   while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
   const uint32_t tmem_cols = 2 * acc_stride;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
-  for (int i = threadIdx.x; i < p.N && i < kMaxBias; i += blockDim.x)
-    sbias[i] = p.bias != nullptr ? p.bias[i] : 0.0f;
+  const int nb_pad = (p.N + 31) & ~31;
+  for (int i = threadIdx.x; i < nb_pad && i < kMaxBias; i += blockDim.x)
+    sbias[i] = (p.bias != nullptr && i < p.N) ? p.bias[i] : 0.0f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -189,20 +241,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   // PDL: this prologue overlapped the previous kernel's tail.  Trigger only
   // once TMEM is held: a dependent CTA that allocated first on this SM while
   // waiting for us would otherwise deadlock our tcgen05.alloc.
+  if (threadIdx.x == 0) GEMM_TRACE(1);
   pdl_trigger();
   pdl_wait();
+  if (threadIdx.x == 0) GEMM_TRACE(2);
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       int s = 0;
       uint32_t phase = 0;
-      const uint32_t tx = (p.mode == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
+      const uint32_t tx = (MODE == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const TileIdx ti = decode_tile(p, t, n_tiles);
         const int m_tile = ti.m, n_tile = ti.n;
         int n0 = 0, oh0 = 0, ow0 = 0;
-        if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC) {
+        if constexpr (kConv) {
           const int tw = m_tile % p.tiles_w;
           const int th = (m_tile / p.tiles_w) % p.tiles_h;
           const int tn = m_tile / (p.tiles_w * p.tiles_h);
@@ -215,15 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a_dst = smem_addr(smA + s * kABytes);
           const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
           mbar_arrive_expect_tx(&full[s], tx);
-          if (p.mode == MODE_DENSE) {
+          if constexpr (MODE == MODE_DENSE) {
             tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
-          } else if (p.mode == MODE_CONV) {
+          } else if constexpr (MODE == MODE_CONV) {
             const int tap = kb / p.cchunks;
             const int cc = kb - tap * p.cchunks;
             const int kh = tap / p.KW;
             const int kw = tap - kh * p.KW;
             tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
-          } else if (p.mode == MODE_CONV_SMALLC) {
+          } else if constexpr (MODE == MODE_CONV_SMALLC) {
             const int kh = kb / p.smallc_halves;
             const int half = kb - kh * p.smallc_halves;
             // ow0/oh0 already include -pad; W is pre-padded in memory so the
@@ -231,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(a_dst, &tmA, &full[s], half * kBK, (ow0 + p.pad) / p.stride, oh0 + kh, n0);
           }
           tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
+          if (t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(3);
           if (++s == stages) {
             s = 0;
             phase ^= 1;
@@ -253,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
         mbar_wait(&full[s], phase);
         tc_fence_after();
-        if (p.mode == MODE_GATHER) fence_proxy_async_smem();
+        if constexpr (MODE == MODE_GATHER) fence_proxy_async_smem();
+        if (lane == 0 && t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(4);
         if (lane == 0) {
           const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
@@ -263,7 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
           }
           umma_commit(&empty[s]);
-          if (kb == ti.kb1 - 1) umma_commit(&tfull[acc]);
+          if (kb == ti.kb1 - 1) {
+            umma_commit(&tfull[acc]);
+            GEMM_TRACE(5);
+          }
         }
         __syncwarp();
         if (++s == stages) {
@@ -279,7 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;               // TMEM lane quarter of this warp
     const int grp = (warp - 2) >> 2;      // column-chunk group: chunks c with c % 2 == grp
     const int r = q * 32 + lane;          // tile row owned by this thread
-    const bool gatherer = (p.mode == MODE_GATHER) && grp == 0;
+    const bool issuer = (warp == 2 + 4 * grp) && lane == 0;  // EPI_TMA store issuer
+    uint8_t* sbuf = sstage + grp * kStoreChunkBytes;         // EPI_TMA chunk buffer
+    uint8_t* srow = sbuf + r * 64;
+    const int sw = (r >> 1) & 3;  // SWIZZLE_64B phase of this row
     int s = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -287,46 +349,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const TileIdx ti = decode_tile(p, t, n_tiles);
       const int m_tile = ti.m, n_tile = ti.n;
-      if (gatherer) {
-        const int row = m_tile * kBM + r;
-        const int kb_per_mod = p.feat_dim / kBK;
-        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
-          mbar_wait(&empty[s], phase ^ 1);
-          const int k = kb / kb_per_mod;
-          const int off = (kb - k * kb_per_mod) * kBK;
-          const __nv_bfloat16* src = nullptr;
-          if (row < p.M) {
-            const int j = p.inv[(long long)k * p.inv_ld + row];
-            if (j >= 0) src = p.feat[k] + (long long)j * p.feat_dim + off;
-          }
-          const uint32_t dst = smem_addr(smA + s * kABytes) + r * 128;
+      if constexpr (MODE == MODE_GATHER) {
+        if (grp == 0) {
+          const int row = m_tile * kBM + r;
+          const int kb_per_mod = p.feat_dim / kBK;
+          for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
+            mbar_wait(&empty[s], phase ^ 1);
+            const int k = kb / kb_per_mod;
+            const int off = (kb - k * kb_per_mod) * kBK;
+            const __nv_bfloat16* src = nullptr;
+            if (row < p.M) {
+              const int j = p.inv[(long long)k * p.inv_ld + row];
+              if (j >= 0) src = p.feat[k] + (long long)j * p.feat_dim + off;
+            }
+            const uint32_t dst = smem_addr(smA + s * kABytes) + r * 128;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t phys = (uint32_t)(c ^ (r & 7));
-            cp_async_16(dst + phys * 16, src ? (const void*)(src + c * 8) : (const void*)p.feat[0],
-                        src ? 16u : 0u);
-          }
-          cp_async_mbar_arrive_noinc(&full[s]);
-          if (++s == stages) {
-            s = 0;
-            phase ^= 1;
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t phys = (uint32_t)(c ^ (r & 7));
+              cp_async_16(dst + phys * 16, src ? (const void*)(src + c * 8) : (const void*)p.feat[0],
+                          src ? 16u : 0u);
+            }
+            cp_async_mbar_arrive_noinc(&full[s]);
+            if (++s == stages) {
+              s = 0;
+              phase ^= 1;
+            }
           }
         }
       }
 
-      // output row for this thread (or -1)
+      // output row for this thread (or -1): residual / fp32 / split-K paths
       long long out_row = -1;
-      if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC) {
-        const int tw = m_tile % p.tiles_w;
-        const int th = (m_tile / p.tiles_w) % p.tiles_h;
-        const int tn = m_tile / (p.tiles_w * p.tiles_h);
-        const int per_img = p.bh * p.bw;
-        if (r < p.bn * per_img) {
-          const int i = r / per_img;
-          const int y = (r - i * per_img) / p.bw;
-          const int x = r - i * per_img - y * p.bw;
-          const int n = tn * p.bn + i, oh = th * p.bh + y, ow = tw * p.bw + x;
-          if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
+      if constexpr (kConv) {
+        if (EPI != EPI_TMA || p.residual != nullptr) {
+          const int tw = m_tile % p.tiles_w;
+          const int th = (m_tile / p.tiles_w) % p.tiles_h;
+          const int tn = m_tile / (p.tiles_w * p.tiles_h);
+          const int per_img = p.bh * p.bw;
+          if (r < p.bn * per_img) {
+            const int i = r / per_img;
+            const int y = (r - i * per_img) / p.bw;
+            const int x = r - i * per_img - y * p.bw;
+            const int n = tn * p.bn + i, oh = th * p.bh + y, ow = tw * p.bw + x;
+            if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
+          }
         }
       } else {
         const int row = m_tile * kBM + r;
@@ -335,131 +401,153 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (warp == 2 && lane == 0 && t == (int)blockIdx.x) GEMM_TRACE(6);
       const uint32_t t_base = tmem_base + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
       const int n_first = n_tile * p.BN;
-      for (int c = grp; c < p.BN / 32; c += 2) {
+      const int n_chunks = (min(p.BN, p.N - n_first) + 31) >> 5;
+      // chunks c = grp, grp + 2, ...: TMEM loads double-buffered so chunk c+2's
+      // load is in flight while chunk c is converted and stored
+      auto release_acc = [&]() {  // every TMEM read of this accumulator has completed
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      };
+      auto process = [&](const uint32_t (&v)[32], int c) {
         const int nb = n_first + c * 32;
-        if (nb >= p.N) break;  // warp-uniform
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
-        tmem_wait_ld();
-        if (p.debug_flags & 1) continue;
-        // rows outside the output still take part in the (warp-collective)
-        // staged store below; they are masked at the global write
-        const bool row_ok = out_row >= 0;
-        if (p.ksplit > 1) {
-          if (!row_ok) continue;  // partial sums: vector fp32 atomics into the workspace
-          float* w = p.ws + out_row * p.ws_ld + nb;
+        const bool tr0 = warp == 2 && lane == 0 && t == (int)blockIdx.x && c == grp;
+        if (tr0) GEMM_TRACE(8);
+        if constexpr (EPI == EPI_SPLITK) {
+          if (out_row >= 0) {
+            float* w = p.ws + out_row * p.ws_ld + nb;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (nb + j < p.N)
-              atomicAdd(reinterpret_cast<float4*>(w + j),
-                        make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                                    __uint_as_float(v[j + 3])));
+            for (int j = 0; j < 32; j += 4)
+              if (nb + j < p.N)
+                atomicAdd(reinterpret_cast<float4*>(w + j),
+                          make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                      __uint_as_float(v[j + 3])));
           }
-          continue;
-        }
-        // destination segment of this 32-column chunk (segments are 32-aligned)
-        void* seg_ptr = p.seg[0].ptr;
-        long long seg_ld = p.seg[0].ldd;
-        int seg_off = p.seg[0].col0 - p.seg[0].n_begin;
-        int seg_flags = p.seg[0].flags;
-#pragma unroll
-        for (int g = 1; g < 4; ++g) {
-          if (g < p.nseg && nb >= p.seg[g].n_begin) {
-            seg_ptr = p.seg[g].ptr;
-            seg_ld = p.seg[g].ldd;
-            seg_off = p.seg[g].col0 - p.seg[g].n_begin;
-            seg_flags = p.seg[g].flags;
-          }
-        }
-        const int act = (seg_flags & MS_SEG_NO_RELU) ? 0 : p.relu;
-        const long long base = out_row * seg_ld + seg_off + nb;
-        const bool full_chunk = nb + 32 <= p.N;
-        const float* bch = sbias + nb;
-        if (p.out_fp32) {
-          if (!row_ok) continue;
-          float* dst = reinterpret_cast<float*>(seg_ptr) + base;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float x = activate(__uint_as_float(v[j]) + (nb + j < p.N ? bch[j] : 0.0f), act);
-            if (nb + j < p.N) dst[j] = x;
-          }
-        } else {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(seg_ptr) + base;
-          uint32_t res[16];
-          if (p.residual != nullptr && full_chunk && row_ok) {
-            const uint4* r4 = reinterpret_cast<const uint4*>(p.residual + out_row * p.res_ld + nb);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint4 q4 = r4[j];
-              res[4 * j] = q4.x;
-              res[4 * j + 1] = q4.y;
-              res[4 * j + 2] = q4.z;
-              res[4 * j + 3] = q4.w;
-            }
-          }
-          uint32_t pk[16];
-          switch (act) {
-            case MS_ACT_RELU: convert_chunk<MS_ACT_RELU>(v, bch, pk); break;
-            case MS_ACT_GELU: convert_chunk<MS_ACT_GELU>(v, bch, pk); break;
-            case MS_ACT_TANH: convert_chunk<MS_ACT_TANH>(v, bch, pk); break;
-            default: convert_chunk<MS_ACT_NONE>(v, bch, pk);
-          }
-          if (p.residual != nullptr && full_chunk) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
-              const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(&res[j]);
-              // residual added in fp32 from the bf16-rounded branch output
-              pk[j] = pack_bf16x2(__bfloat162float(a2.x) + __bfloat162float(r2.x),
-                                  __bfloat162float(a2.y) + __bfloat162float(r2.y));
-            }
-          }
-          if (full_chunk) {
-            // coalesced write-back: stage the warp's 32 rows x 64 B in smem,
-            // then each store instruction covers 8 rows x 64 contiguous bytes
-            uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
-            uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-            __syncwarp();
-            const long long col = seg_off + nb;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int rr = i * 8 + (lane >> 2), piece = lane & 3;
-              const long long orow = __shfl_sync(0xffffffffu, out_row, rr);
-              const uint4 val = *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
-              if (orow >= 0)
-                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(seg_ptr) + orow * seg_ld + col +
-                                          piece * 8) = val;
-            }
-            __syncwarp();
-            continue;
-          }
-          if (full_chunk) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) d4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          } else if (row_ok) {
-            unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
+        } else if constexpr (EPI == EPI_F32) {
+          if (out_row >= 0) {
+            const Seg& S = p.seg[0];
+            float* dst = reinterpret_cast<float*>(S.ptr) + out_row * S.ldd + S.col0 - S.n_begin + nb;
+            const float* bch = sbias + nb;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (nb + j < p.N) d2[j] = (unsigned short)((pk[j >> 1] >> (16 * (j & 1))) & 0xffff);
+              if (nb + j < p.N) dst[j] = activate(__uint_as_float(v[j]) + bch[j], ACT);
+          }
+        } else {  // EPI_TMA
+          int g = 0;
+#pragma unroll
+          for (int gg = 1; gg < 4; ++gg)
+            if (gg < p.nseg && nb >= p.seg[gg].n_begin) g = gg;
+          uint32_t pk[16];
+          if (p.seg[g].flags & MS_SEG_NO_RELU)
+            convert_chunk4<MS_ACT_NONE>(v, sbias + nb, pk);
+          else
+            convert_chunk4<ACT>(v, sbias + nb, pk);
+          if (p.residual != nullptr && out_row >= 0) {
+            const __nv_bfloat16* rp = p.residual + out_row * p.res_ld + nb;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (nb + 2 * j < p.N) {  // pairs never straddle N (N is even)
+                const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+                const __nv_bfloat162 r2 = *reinterpret_cast<const __nv_bfloat162*>(rp + 2 * j);
+                pk[j] = pack_bf16x2(__bfloat162float(a2.x) + __bfloat162float(r2.x),
+                                    __bfloat162float(a2.y) + __bfloat162float(r2.y));
+              }
+            }
+          }
+          if (tr0) GEMM_TRACE(9);
+          if (issuer) bulk_wait_read0();  // the previous chunk's store has read the buffer
+          named_bar_sync(1 + grp, 128);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(srow + ((j ^ sw) << 4)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(1 + grp, 128);
+          if (issuer) {
+            const int c0 = nb - p.seg[g].n_begin;
+            if constexpr (kConv) {
+              const int tw = m_tile % p.tiles_w;
+              const int th = (m_tile / p.tiles_w) % p.tiles_h;
+              const int tn = m_tile / (p.tiles_w * p.tiles_h);
+              tma_store_4d(&tmD.m[g], smem_addr(sbuf), c0, tw * p.bw, th * p.bh, tn * p.bn);
+            } else {
+              tma_store_2d(&tmD.m[g], smem_addr(sbuf), c0, m_tile * kBM);
+            }
+            bulk_commit();
+            if (tr0) GEMM_TRACE(10);
           }
         }
+      };
+      uint32_t va[32], vb[32];
+      int c = grp;
+      if (c < n_chunks) tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), va);
+      while (c < n_chunks) {
+        tmem_wait_ld();
+        if (c + 2 < n_chunks)
+          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + 2) * 32), vb);
+        else
+          release_acc();
+        process(va, c);
+        c += 2;
+        if (c >= n_chunks) break;
+        tmem_wait_ld();
+        if (c + 2 < n_chunks)
+          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + 2) * 32), va);
+        else
+          release_acc();
+        process(vb, c);
+        c += 2;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
+      if (warp == 2 && lane == 0 && t == (int)blockIdx.x) GEMM_TRACE(11);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (EPI == EPI_TMA && issuer) bulk_wait0();
+    if (warp == 2 && lane == 0) GEMM_TRACE(7);
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+typedef void (*GemmKernelFn)(const CUtensorMap, const CUtensorMap, const GemmParams, const StoreMaps);
+
+template <int MODE, int EPI>
+static GemmKernelFn pick_act(int act) {
+  switch (act) {
+    case MS_ACT_RELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_RELU>;
+    case MS_ACT_GELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_GELU>;
+    case MS_ACT_TANH: return gemm_tc_kernel<MODE, EPI, MS_ACT_TANH>;
+    default: return gemm_tc_kernel<MODE, EPI, MS_ACT_NONE>;
+  }
+}
+
+// The instantiation for a plan (null if the combination is unsupported).
+static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
+  if (p.ksplit > 1) {
+    if (p.mode == MODE_DENSE) return gemm_tc_kernel<MODE_DENSE, EPI_SPLITK, MS_ACT_NONE>;
+    if (p.mode == MODE_GATHER) return gemm_tc_kernel<MODE_GATHER, EPI_SPLITK, MS_ACT_NONE>;
+    if (p.mode == MODE_CONV) return gemm_tc_kernel<MODE_CONV, EPI_SPLITK, MS_ACT_NONE>;
+    return nullptr;
+  }
+  if (p.out_fp32) {
+    if (p.mode == MODE_DENSE) return pick_act<MODE_DENSE, EPI_F32>(p.relu);
+    if (p.mode == MODE_GATHER) return pick_act<MODE_GATHER, EPI_F32>(p.relu);
+    return nullptr;
+  }
+  if (!p.tma_store) return nullptr;
+  switch (p.mode) {
+    case MODE_DENSE: return pick_act<MODE_DENSE, EPI_TMA>(p.relu);
+    case MODE_CONV: return pick_act<MODE_CONV, EPI_TMA>(p.relu);
+    case MODE_GATHER: return pick_act<MODE_GATHER, EPI_TMA>(p.relu);
+    case MODE_CONV_SMALLC: return pick_act<MODE_CONV_SMALLC, EPI_TMA>(p.relu);
+    default: return nullptr;
   }
 }
 
@@ -968,12 +1056,13 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   p.b_bytes = BN * kBK * 2;
   const int per_stage = kABytes + p.b_bytes;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
+  p.stage_bytes = p.tma_store ? kStoreBytes : 0;  // fp32 / split-K epilogues stage nothing
   // 227 KB usable: 1 KB alignment slack, barriers, epilogue staging, bias
-  int stages = (226 * 1024 - 1024 - 256 - kStageBytes - bias_bytes) / per_stage;
+  int stages = (226 * 1024 - 1024 - 256 - p.stage_bytes - bias_bytes) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + kStageBytes + bias_bytes;
+  P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 4) * 8 + 16 + bias_bytes;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
@@ -1009,6 +1098,38 @@ static int finish_conv1_rows(GemmPlan* P, const void* Wt, int num_wb) {
   return MS_OK;
 }
 
+// Encode one bf16 TMA store map per output segment (see StoreMaps).  Called
+// once the output geometry is known; leaves tma_store = 0 for fp32 outputs.
+static int encode_store_maps(GemmPlan* P) {
+  GemmParams& p = P->p;
+  p.tma_store = 0;
+  if (p.out_fp32) return MS_OK;
+  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC;
+  for (int g = 0; g < p.nseg; ++g) {
+    const Seg& S = p.seg[g];
+    const int w = S.n_end - S.n_begin;
+    if (w <= 0 || (S.col0 * 2) % 16 != 0 || (S.ldd * 2) % 16 != 0)
+      return set_error(MS_ERR_INVALID, "output segment must be 16-byte aligned (col0, ldd multiples of 8)");
+    void* base = reinterpret_cast<__nv_bfloat16*>(S.ptr) + S.col0;
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    int rc;
+    if (conv) {
+      cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)p.OW, (cuuint64_t)p.OH, (cuuint64_t)p.n_img};
+      cuuint64_t st[3] = {(cuuint64_t)S.ldd * 2, (cuuint64_t)S.ldd * 2 * p.OW, (cuuint64_t)S.ldd * 2 * p.OW * p.OH};
+      cuuint32_t box[4] = {32, (cuuint32_t)p.bw, (cuuint32_t)p.bh, (cuuint32_t)p.bn};
+      rc = encode_map(&P->tmD.m[g], 4, base, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_64B);
+    } else {
+      cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)p.M};
+      cuuint64_t st[1] = {(cuuint64_t)S.ldd * 2};
+      cuuint32_t box[2] = {32, (cuuint32_t)kBM};
+      rc = encode_map(&P->tmD.m[g], 2, base, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+    if (rc) return rc;
+  }
+  p.tma_store = 1;
+  return MS_OK;
+}
+
 static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D, long long ldd, int col0) {
   if (nseg <= 0 || segs == nullptr) {
     p.nseg = 1;
@@ -1021,11 +1142,6 @@ static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D
 }
 
 static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
-  static int attr_set = 0;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = 1;
-  }
   const GemmParams& p = P->p;
   if (p.mode == MODE_CONV1_ROWS) {
     static int c1_attr = 0;
@@ -1045,7 +1161,20 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
     launch_k(gemm_tc_pair_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 2, P->tmA, P->tmB, p);
     return check_launch("gemm_tc_pair_kernel");
   }
-  launch_k(gemm_tc_kernel, dim3(P->grid_x, P->grid_y), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p);
+  GemmKernelFn kern = gemm_kernel_for(p);
+  if (kern == nullptr) return set_error(MS_ERR_INVALID, "no GEMM kernel for this plan (mode/epilogue)");
+  static bool attr_done[64] = {};
+  static GemmKernelFn attr_fn[64] = {};
+  {  // opt every instantiation into 227 KB of dynamic shared memory once
+    int slot = 0;
+    while (slot < 64 && attr_fn[slot] != nullptr && attr_fn[slot] != kern) ++slot;
+    if (slot < 64 && !attr_done[slot]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr_fn[slot] = kern;
+      attr_done[slot] = true;
+    }
+  }
+  launch_k(kern, dim3(P->grid_x, P->grid_y), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p, P->tmD);
   int rc = check_launch("gemm_tc_kernel");
   if (rc || p.ksplit <= 1) return rc;
   const long long work = (long long)p.M * ((p.N + 3) / 4);
@@ -1086,6 +1215,7 @@ int ms_gemm_plan_dense(void* plan, const void* A, int M, int K, long long lda, c
   cuuint32_t es[2] = {1, 1};
   int rc = encode_map(&P->tmA, 2, A, dims, strides, box, es);
   if (rc) return rc;
+  if (int rc_store = encode_store_maps(P)) return rc_store;
   return finish_plan(P, W, K_pad, N, BN, K_pad / kBK, (M + kBM - 1) / kBM);
 }
 
@@ -1169,6 +1299,7 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
     num_kb = KH * KW * p.cchunks;
   }
   const int tiles_n = (n_img + bn - 1) / bn;
+  if (int rc_store = encode_store_maps(P)) return rc_store;
   return finish_plan(P, Wt, num_kb * kBK, Cout, BN, num_kb, tiles_n * p.tiles_h * p.tiles_w);
 }
 
@@ -1196,6 +1327,7 @@ int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv,
   for (int k = n_mod; k < 4; ++k) p.feat[k] = p.feat[0];
   set_segments(p, 0, nullptr, D, ldd, col0);
   const int K = n_mod * feat_dim;
+  if (int rc_store = encode_store_maps(P)) return rc_store;
   return finish_plan(P, W, K, N, BN, K / kBK, (M + kBM - 1) / kBM);
 }
 
@@ -1215,15 +1347,17 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
   GemmParams& p = P->p;
   if (ksplit < 1) return set_error(MS_ERR_INVALID, "ksplit must be >= 1");
   if (ksplit > 1) {
-    if (p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.nseg > 1 || ws == nullptr || ws_ld % 4 != 0 ||
-        ws_ld < p.N)
-      return set_error(MS_ERR_INVALID, "split-K needs a dense/gather single-segment plan and ws[M, ws_ld>=N, %4]");
+    if (p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV1_ROWS || p.pair || p.nseg > 1 || ws == nullptr ||
+        ws_ld % 4 != 0 || ws_ld < p.N)
+      return set_error(MS_ERR_INVALID,
+                       "split-K needs a dense/gather/conv single-segment plan and ws[M, ws_ld>=N, %4]");
   }
   const int kb_per = (p.num_kb + ksplit - 1) / ksplit;
   p.ksplit = (p.num_kb + kb_per - 1) / kb_per;  // no empty K parts
   p.kb_per = kb_per;
   p.ws = ws;
   p.ws_ld = ws_ld;
+  if (p.ksplit > 1) p.tma_store = 0;  // partial sums go to the fp32 workspace (layout unchanged)
   const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN) * p.ksplit;
   P->grid_x = tiles < sm_count() ? tiles : sm_count();
   return MS_OK;
@@ -1256,6 +1390,13 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   const int tiles = m_pairs * ((p.N + p.BN - 1) / p.BN);
   const int clusters = tiles < sm_count() / 2 ? tiles : sm_count() / 2;
   P->grid_x = 2 * clusters;
+  return MS_OK;
+}
+
+int ms_gemm_plan_set_trace(void* plan, unsigned long long* buf) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
+  P->p.trace = buf;
   return MS_OK;
 }
 

@@ -15,8 +15,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libmosel_b200.so"
-GEMM_PLAN_BYTES = 1024
-OP_BYTES = 1152
+GEMM_PLAN_BYTES = 2048
+OP_BYTES = 2112
 DROP = -1
 MS_ERR_CUDA_STATUS = 2
 
@@ -78,6 +78,7 @@ _SIGS = {
     "ms_gemm_plan_set_residual": ([_P, _P, _LL], C.c_int),
     "ms_gemm_plan_set_splitk": ([_P, _I, _P, _LL], C.c_int),
     "ms_gemm_plan_debug": ([_P, _I], C.c_int),
+    "ms_gemm_plan_set_trace": ([_P, _P], C.c_int),
     "ms_gemm_plan_set_pair": ([_P, _I], C.c_int),
     "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
     "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),
@@ -308,7 +309,7 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
 
 
 def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, bias, D, *, ldd,
-              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None):
+              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None, split_k=None):
     p = GemmPlan()
     nseg, sarr = _segments(segs)
     bn, bh, bw = tile
@@ -320,13 +321,27 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
     ow = (W_in + 2 * pad - KW) // stride + 1
     p.flops = 2 * n_img * oh * ow * Cout * KH * KW * C_in
     p.label = f"conv {KH}x{KW}/{stride} {C_in}->{Cout} {n_img}x{oh}x{ow}"
+    bn_, bh_, bw_ = tile
+    conv_tiles = -(-n_img // bn_) * -(-oh // bh_) * -(-ow // bw_)
+    if C_in >= 64 and (not segs or len(segs) == 1) and split_k is not None and split_k > 1:
+        # explicit only: splitting the (tap, channel-chunk) K loop of the small
+        # late layers measured SLOWER inside a pass (fp32 atomics + finalize
+        # outweigh the idle SMs it fills; tools/pass_ab.py, round 1)
+        k = split_k
+        if k > 1:
+            m_rows = n_img * oh * ow
+            ws_ld = -(-Cout // 4) * 4
+            ws = _torch().zeros(m_rows, ws_ld, dtype=_torch().float32, device=D.device)
+            check(lib().ms_gemm_plan_set_splitk(p.addr, k, ws.data_ptr(), ws_ld), "ms_gemm_plan_set_splitk")
+            p.keep.append(ws)
+            p.split_k = k
+            return p
     if C_in >= 64 and pair is not False:  # not the small-channel first layer
         if pair:
             p.set_pair()
         else:
             bn_, bh_, bw_ = tile
-            tiles = -(-n_img // bn_) * -(-oh // bh_) * -(-ow // bw_)
-            _auto_pair(p, tiles, BN, True)
+            _auto_pair(p, conv_tiles, BN, True)
     return p
 
 

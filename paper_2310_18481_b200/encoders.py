@@ -245,10 +245,17 @@ def pack_dense_weight(w):
     return out.contiguous()
 
 
-def pick_bn(n: int) -> int:
+def pick_bn(n: int, m_tiles: int | None = None, target_ctas: int = 96) -> int:
     """Tile width for N output columns: one tile when N <= 256, else the
-    fewest equal-ish tiles (multiples of 32)."""
+    fewest equal-ish tiles (multiples of 32).  With ``m_tiles`` given and too
+    few (m, n) tiles to occupy ``target_ctas`` SMs, split N further (tiles
+    >= 64 wide): each CTA's serial K loop shrinks and idle SMs take the rest.
+    (Not used by the TBN encoders: with modality streams and branch lanes
+    already sharing the SMs it measured slower, tools/pass_ab.py.)"""
     tiles = -(-n // 256)
+    if m_tiles is not None:
+        while m_tiles * tiles < target_ctas and -(-n // (tiles + 1)) >= 64:
+            tiles += 1
     bn = -(-n // tiles)
     return -(-bn // 32) * 32
 
@@ -268,6 +275,11 @@ def pick_conv_tile(n_img: int, oh: int, ow: int):
                 if best is None or key < best[0]:
                     best = (key, (bn, bh, bw))
     return best[1]
+
+
+def conv_m_tiles(n_img: int, o: int, tile) -> int:
+    bn, bh, bw = tile
+    return -(-n_img // bn) * -(-o // bh) * -(-o // bw)
 
 
 # ------------------------------------------------------------ device build

@@ -186,6 +186,35 @@ def test_conv_implicit_gemm_vs_torch(dev, n, H, Cin, Cout, k, s, pad, tile, BN):
     assert ok, (err, scale)
 
 
+@pytest.mark.parametrize("n,H,Cin,Cout,s,split", [
+    (5, 7, 160, 224, 1, 1), (5, 7, 160, 224, 1, 3), (3, 14, 192, 320, 2, 4), (2, 8, 224, 224, 1, 6),
+])
+def test_conv_split_k_into_concat_slice(dev, n, H, Cin, Cout, s, split):
+    """Split-K implicit-GEMM conv (fp32 workspace + finalize) writing a
+    channel slice of a wider concat output, as the Inception branches do; run
+    twice (the finalize re-zeroes the workspace)."""
+    g = torch.Generator().manual_seed(n * H + Cin + split)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, 3, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    OH = (H + 2 - 3) // s + 1
+    ldd, col0 = Cout + 96, 64
+    D = torch.full((n * OH * OH, ldd), 7.0, dtype=torch.bfloat16, device="cuda")
+    from paper_2310_18481_b200.encoders import pick_bn, pick_conv_tile
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, 3, 3, s, 1, packed.cuda(), Cout, b.cuda(), D, ldd=ldd, col0=col0,
+                      BN=pick_bn(Cout), relu=True, tile=pick_conv_tile(n, OH, OH), split_k=split)
+    assert getattr(p, "split_k", 1) == split
+    p.run()
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=s, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D[:, col0:col0 + Cout].cpu(), ref)
+    assert ok, (err, scale)
+    assert torch.all(D[:, :col0] == 7.0) and torch.all(D[:, col0 + Cout:] == 7.0)  # neighbours untouched
+
+
 def test_gather_concat_gemm_vs_torch(dev):
     g = torch.Generator().manual_seed(11)
     N, F, K = 300, 1024, 3

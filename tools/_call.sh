@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/pass_ab.py > gpurun_out/pass_ab.txt 2>&1; echo ab=$? >> gpurun_out/pass_ab.txt
+timeout 600 python tools/pass_ab.py --configs pdl+lanes > gpurun_out/pass_ab.txt 2>&1

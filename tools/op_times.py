@@ -1,6 +1,8 @@
 """Warm per-op device times of one masked TBN pass: every op of every
 encoder program (and the head) run alone between CUDA events, in program
-order, after a full warm-up pass.  Prints ops sorted by time with achieved
+order, after a full warm-up pass.  Each op is timed as REP back-to-back
+launches inside one CUDA graph (no host launch latency; PDL overlap between
+consecutive launches as in a pass graph).  Prints ops sorted by time with achieved
 TFLOP/s for GEMMs.
 
     python tools/op_times.py --n 96 [--mixed]
@@ -16,7 +18,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=96)
 ap.add_argument("--mixed", action="store_true")
 ap.add_argument("--top", type=int, default=45)
+ap.add_argument("--rep", type=int, default=10)
 a = ap.parse_args()
+REP = a.rep
 
 import torch  # noqa: E402
 
@@ -42,17 +46,28 @@ for k, (enc, c) in enumerate(zip(m.encoders, counts)):
         continue
     prog = enc.program(c)
     for i, (kind, op) in enumerate(prog.ops):
+        # the op repeated REP times inside one CUDA graph: device time per
+        # launch without host launch latency (as inside a pass graph)
         single = dv.Program()
-        single.ops = [(kind, op)]
+        single.ops = [(kind, op)] * REP
         single.keep = prog.keep
         single.seal()
         single.run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                single.run()
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
         ts = []
         for _ in range(5):
             e0.record()
-            single.run()
+            g.replay()
             e1.record()
-            ts.append(e0.elapsed_us(e1))
+            ts.append(e0.elapsed_us(e1) / REP)
         us = float(np.median(ts))
         fl = op.flops if kind == "gemm" else 0
         rows.append((us, k, i, kind, op.label if kind == "gemm" else "", fl))
