@@ -232,6 +232,10 @@ def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
     return jobs[rank::world]
 
 
+SCHED_MARGIN_US = 0
+POLICY_GRID_US = 1000
+
+
 def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
           host_clips=None, max_size=None, cost=None):
     from paper_2310_18481_b200.realtime import serve_realtime
@@ -243,7 +247,7 @@ def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world
     if cost is not None:
         cost.factor = 1.0
     return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed,
-                          cost=cost)
+                          cost=cost, sched_margin_us=SCHED_MARGIN_US, policy_grid_us=POLICY_GRID_US)
 
 
 def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print,
@@ -351,7 +355,6 @@ def our_arm(args):
     out_dir.mkdir(exist_ok=True)
     if rank == 0:
         save_profile(prof, out_dir / f"{args.workload}_b200_profile.yaml")
-    matrix = build_matrix(prof, range(1, args.max_job + 1), recommended_alphas(prof))
     full = prof.all_modalities_mask
     full1 = prof.part_latency_us(full, 1)
     log(f"[bench] profile: all-modality batch1 {full1} us, batch{args.profile_batch} "
@@ -365,7 +368,19 @@ def our_arm(args):
         cost = profile_pass_costs(model, reps=3)
         log(f"[bench] pass cost model: enc b1 {[round(r[0]) for r in cost.enc_us]} us, "
             f"b{max_req} {[round(r[-1]) for r in cost.enc_us]} us, head b{max_req} {cost.head_us[-1]:.0f} us")
-    rate, trials = find_rate(model, prof, matrix, deadline_ms, args.search_seconds, cap, args.max_job,
+    # the scheduler's latency table: the device profile (each part priced as
+    # if it ran alone, the reference's additive model) or, for the batched
+    # executor, the measured marginal per-request costs (profiler.marginal_profile)
+    sprof = prof
+    if cost is not None and args.serve_profile == "marginal":
+        from paper_2310_18481_b200.profiler import marginal_profile
+        sprof = marginal_profile(cost, mod_names, accuracy, max_batch=args.profile_batch)
+        if rank == 0:
+            save_profile(sprof, out_dir / f"{args.workload}_b200_serving_profile.yaml")
+        log(f"[bench] serving profile (marginal): all-modality b1 {sprof.part_latency_us(full, 1)} us, "
+            f"b{args.profile_batch} {sprof.part_latency_us(full, args.profile_batch)} us")
+    matrix = build_matrix(sprof, range(1, args.max_job + 1), recommended_alphas(sprof))
+    rate, trials = find_rate(model, sprof, matrix, deadline_ms, args.search_seconds, cap, args.max_job,
                              log, cost=cost)
     if pg is not None:  # every replica runs at the slowest replica's rate
         import torch.distributed as tdist
@@ -386,7 +401,7 @@ def our_arm(args):
         clocks.start()
         e_start, e_end = dv.Event(), dv.Event()
         e_start.record()
-        lg, st = serve(model, prof, matrix, rate, seconds, deadline_ms, 7, rank, world,
+        lg, st = serve(model, sprof, matrix, rate, seconds, deadline_ms, 7, rank, world,
                        max_size=args.max_job, cost=cost)
         e_end.record()
         torch.cuda.synchronize()
@@ -417,7 +432,7 @@ def our_arm(args):
     hc = HostClips(model)
     e2e_rate = rate
     for attempt in range(8):
-        lg2, st2 = serve(model, prof, matrix, e2e_rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
+        lg2, st2 = serve(model, sprof, matrix, e2e_rate, seconds, deadline_ms, 7, rank, world, host_clips=hc,
                          max_size=args.max_job, cost=cost)
         timed2 = [r for r in lg2.records if r.arrival_us >= t_lo]
         ok2 = sum(r.size for r in timed2 if not r.violated)
@@ -458,6 +473,9 @@ def our_arm(args):
                    "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
                    "policy": "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
                              " + cross-job batched device passes"),
+                   "sched_margin_ms": args.sched_margin_ms, "policy_grid_us": args.policy_grid_us,
+                   "latency_table": "device profile (parts priced alone)" if sprof is prof else
+                   "marginal batched per-request costs (profiler.marginal_profile)",
                    "step": f"one {win}s real-time serving window", "max_req": max_req,
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
@@ -497,11 +515,20 @@ def main():
     ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")
     ap.add_argument("--max-job", type=int, default=24, help="job size cap (matrix sizes 1..max_job)")
     ap.add_argument("--no-batching", action="store_true", help="one job per device pass")
+    ap.add_argument("--policy-grid-us", type=int, default=20,
+                    help="optimized policy knapsack quantum (reference: 1000)")
+    ap.add_argument("--sched-margin-ms", type=float, default=3.0,
+                    help="the scheduler plans against deadline - margin (scored on the true deadline)")
+    ap.add_argument("--serve-profile", default="marginal", choices=["marginal", "device"],
+                    help="scheduler latency table for batched serving")
     ap.add_argument("--slots", type=int, default=192)
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    global SCHED_MARGIN_US, POLICY_GRID_US
+    SCHED_MARGIN_US = int(args.sched_margin_ms * 1000)
+    POLICY_GRID_US = int(args.policy_grid_us)
     if args.impl == "reference":
         reference_arm(args)
     else:

@@ -75,6 +75,22 @@ int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t
                      const int64_t* deadline_us, int64_t dispatch_us, double factor, int N,
                      int32_t* choice, void* stream);
 
+/* ms_policy_apply <- scheduler.py:382-425 apply_policy(OPTIMIZED) over a whole
+ * EDF queue (detect_violation -> compute_budget -> reassign_optimized MCKP,
+ * scheduler.py:187-326 -> drops -> try_upgrade :366-379), one launch.
+ * Jobs in EDF order; candidate tables [n, C] (lat_us, credit, effective
+ * accuracy as double); assigned[n] in/out (-1 on return = dropped).
+ * has_running: the running job's estimated finish sets the dispatch time
+ * (scheduler.py:178-184).  grid_us = the knapsack quantum (reference 1000).
+ * ws: device scratch of ws_bytes (16 bytes per knapsack cell); *status
+ * (device) = 0 ok, 1 scratch too small, 2 scope exceeds 4096 job x
+ * candidate entries -- the caller then uses the host policy.  Bit-exact with
+ * the reference (tests/golden/queue_policy_cases.json). */
+int ms_policy_apply(int n, int C, const int64_t* lat_us, const int32_t* credit, const double* acc,
+                    const int32_t* n_cand, const int64_t* deadline_us, int32_t* assigned, int64_t now_us,
+                    int64_t running_finish_us, int has_running, double factor, int64_t grid_us, void* ws,
+                    long long ws_bytes, int32_t* status, void* stream);
+
 /* ---- request compaction ----------------------------
  * mask[N] (bit k = modality k present) ->
  *   idx[K*N]   : idx[k*N + j] = j-th request (ascending) that has modality k

@@ -45,6 +45,7 @@ class ServeStats:
     dropped_admit: int = 0     # requests with an empty frontier at admission
     late: int = 0              # requests completed after their deadline
     wall_s: float = 0.0
+    trace: list | None = None  # optional per-pass diagnostics (serve_realtime(trace=True))
 
 
 class HostClips:
@@ -59,7 +60,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
                    policy: Policy = Policy.OPTIMIZED, watermark: int = 2,
                    host_clips: HostClips | None = None, slot_seed: int = 0,
                    window_us: int = 4_000_000, depth: int = 2, cost=None,
-                   max_batch_requests: int | None = None, lead_us: int = 600):
+                   max_batch_requests: int | None = None, lead_us: int = 600, trace: bool = False,
+                   sched_margin_us: int = 0, policy_grid_us: int = 1000):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -81,6 +83,14 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     pass's observed time feeds both the scheduler EWMA (attributed to jobs
     in proportion to their predicted latency) and the cost model's EWMA.
 
+    ``sched_margin_us``: the scheduler (policy, dispatch drop rule, batch
+    formation) sees every deadline this much earlier than the request's true
+    deadline, so the reference policy predicts violations while a modality
+    downgrade can still prevent them (a pass, once launched, cannot be
+    changed); SLO attainment is always scored on the true deadline.
+    ``policy_grid_us``: the optimized policy's knapsack quantum (reference
+    1 ms; see ``policy.reassign_optimized``).
+
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
     from collections import deque
@@ -90,6 +100,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     fb = FeedbackState()
     records: list[JobRecord] = []
     stats = ServeStats()
+    if trace:
+        stats.trace = []
     stream = torch.cuda.current_stream()
     ev_zero = dv.Event()
     pending = list(enumerate(templates, start=1))
@@ -115,7 +127,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     def run_policy(now):
         nonlocal since_opt
         t = time.perf_counter()
-        for j in apply_policy(policy, queue, now, fb, pol_rng):
+        for j in apply_policy(policy, queue, now, fb, pol_rng, grid_us=policy_grid_us):
             drop(j)
             stats.dropped_policy += j.size
         stats.policy_host_us += (time.perf_counter() - t) * 1e6
@@ -189,6 +201,10 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         stats.passes += 1
         stats.requests += n
         preds = [[profile.part_latency_us(m, b) for m, b in j.assigned.strategy.parts] for j in batch]
+        if stats.trace is not None:
+            stats.trace.append({"pass": stats.passes - 1, "host_us": now_us(), "dispatch_us": now, "n": n,
+                                "jobs": [j.id for j in batch], "est_us": est_us, "queue": len(queue),
+                                "queued_req": sum(j.size for j in queue._jobs), "counts": list(counts)})
         inflight.append((batch, ev_s, ev_e, preds, tuple(counts), n))
         queue.running = batch[-1]  # the latest in-flight job sets the next dispatch time
         return True
@@ -198,6 +214,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         batch, ev_s, ev_e, preds, counts, n = inflight.popleft()
         end_us = int(round(ev_zero.elapsed_us(ev_e)))
         dur = max(1.0, ev_s.elapsed_us(ev_e))
+        if stats.trace is not None:
+            for tr in reversed(stats.trace):
+                if tr["jobs"] and tr["jobs"][0] == batch[0].id:
+                    tr.update(start_us=end_us - dur, end_us=end_us, seen_us=now_us())
+                    break
         stats.busy_us += dur
         if cost is not None:
             cost.observe(counts, n, dur)
@@ -214,10 +235,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             job.completion_us = end_us
             if queue.running is job:
                 queue.running = None
+            true_dl = job.deadline_us + sched_margin_us
             records.append(JobRecord(job.id, job.arrival_us, job.size, job.accuracy_slo,
                                      job.assigned.effective_accuracy, end_us, False,
-                                     end_us > job.deadline_us))
-            if end_us > job.deadline_us:
+                                     end_us > true_dl))
+            if end_us > true_dl:
                 stats.late += job.size
 
     while pos < len(pending) or len(queue) or inflight:
@@ -228,7 +250,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             jid, tpl = pending[pos]
             pos += 1
             cands = candidates_with_rounding(matrix, tpl.size, tpl.accuracy_slo)
-            job = Job(jid, tpl.arrival_us, tpl.size, tpl.accuracy_slo, tpl.deadline_us, cands)
+            job = Job(jid, tpl.arrival_us, tpl.size, tpl.accuracy_slo, tpl.deadline_us - sched_margin_us, cands)
             if not cands:
                 job.state = JobState.DROPPED
                 drop(job)

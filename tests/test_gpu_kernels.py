@@ -450,3 +450,29 @@ def test_conv_cta_pair_vs_torch(dev, n, H, Cin, Cout, k, s, pad, tile, BN):
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
     ok, err, scale = _close(D.cpu(), ref)
     assert ok, (err, scale)
+
+
+def test_coupled_queue_policy_on_device_matches_reference_goldens(dev):
+    """ms_policy_apply (the whole OPTIMIZED apply_policy in one launch) on
+    the 440 reference-generated EDF queues: every job's final candidate and
+    every drop bit-exact; then the fine-grid variant against the host mirror."""
+    import numpy as np
+    from queue_cases import build_queue, load_cases, outcome
+    from paper_2310_18481_b200.policy import DevicePolicy, Policy, apply_policy
+    pol = DevicePolicy(max_jobs=64, max_cand=64)
+    for case in load_cases():
+        q, jobs, fb = build_queue(case)
+        dropped = pol.apply(q, case["now_us"], fb)
+        assert outcome(jobs, dropped) == case["expected"], case["profile"]
+    assert pol.host_fallbacks == 0 and pol.launches > 400
+    # a 37 us knapsack quantum (the batched server's regime) vs the host mirror
+    fine = DevicePolicy(max_jobs=64, max_cand=64, grid_us=37, ws_bytes=512 << 20)
+    rng = np.random.default_rng(1)
+    for case in [c for i, c in enumerate(load_cases()) if i % 4 == 0]:
+        f = float(rng.uniform(0.3, 3.0))
+        case = dict(case, factor=f)
+        q1, j1, fb1 = build_queue(case)
+        q2, j2, fb2 = build_queue(case)
+        d1 = fine.apply(q1, case["now_us"], fb1)
+        d2 = apply_policy(Policy.OPTIMIZED, q2, case["now_us"], fb2, grid_us=37)
+        assert outcome(j1, d1) == outcome(j2, d2)

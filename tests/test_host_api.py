@@ -214,3 +214,17 @@ def test_request_masks_follow_canonical_parts():
         total = sum(b for _, b in parts)
         size = int(rng.integers(1, total + 1))
         assert request_masks(parts, size).tolist() == parts_for_requests(parts, size)[0].tolist()
+
+
+def test_coupled_queue_policy_matches_reference_goldens():
+    """Host mirror of apply_policy(OPTIMIZED) on 440 multi-job EDF queues
+    (2-40 jobs, drops, MCKP reassignments, upgrades) generated by the real
+    reference (tests/golden/make_queue_golden.py)."""
+    from queue_cases import build_queue, load_cases, outcome
+    from paper_2310_18481_b200.policy import Policy, apply_policy
+    cases = load_cases()
+    assert len(cases) >= 400
+    for case in cases:
+        q, jobs, fb = build_queue(case)
+        dropped = apply_policy(Policy.OPTIMIZED, q, case["now_us"], fb)
+        assert outcome(jobs, dropped) == case["expected"], case["profile"]

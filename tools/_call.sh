@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/pass_ab.py --configs pdl+lanes > gpurun_out/pass_ab.txt 2>&1
+python tools/policy_bench.py > gpurun_out/policy_bench.txt 2>&1
