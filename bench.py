@@ -232,8 +232,8 @@ def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
     return jobs[rank::world]
 
 
-SCHED_MARGIN_US = 0
-POLICY_GRID_US = 1000
+# serving-loop options (set from the command line in main())
+SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.25}
 
 
 def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
@@ -246,8 +246,13 @@ def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world
                 for j in jobs]
     if cost is not None:
         cost.factor = 1.0
-    return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed,
-                          cost=cost, sched_margin_us=SCHED_MARGIN_US, policy_grid_us=POLICY_GRID_US)
+    from paper_2310_18481_b200.policy import Policy
+    o = SERVE_OPTS
+    sel = o["selection"] if cost is not None else "policy"
+    return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed, cost=cost,
+                          policy=Policy.NONE if sel == "pass" else Policy.OPTIMIZED,
+                          sched_margin_us=o["sched_margin_us"], policy_grid_us=o["policy_grid_us"],
+                          selection=sel, max_pass_us=o["pass_frac"] * deadline_ms * 1000 if sel == "pass" else None)
 
 
 def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print,
@@ -471,8 +476,11 @@ def our_arm(args):
         "config": {"workload": desc,
                    "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
                    "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
-                   "policy": "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
-                             " + cross-job batched device passes"),
+                   "policy": ("per-request modality-subset argmax under the formed pass's deadline "
+                              f"(batched P5; pass <= {args.pass_frac} x deadline)")
+                   if (args.selection == "pass" and not args.no_batching) else
+                   "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
+                                                         " + cross-job batched device passes"),
                    "sched_margin_ms": args.sched_margin_ms, "policy_grid_us": args.policy_grid_us,
                    "latency_table": "device profile (parts priced alone)" if sprof is prof else
                    "marginal batched per-request costs (profiler.marginal_profile)",
@@ -515,9 +523,14 @@ def main():
     ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")
     ap.add_argument("--max-job", type=int, default=24, help="job size cap (matrix sizes 1..max_job)")
     ap.add_argument("--no-batching", action="store_true", help="one job per device pass")
-    ap.add_argument("--policy-grid-us", type=int, default=20,
+    ap.add_argument("--selection", default="pass", choices=["pass", "policy"],
+                    help="pass: per-request accuracy argmax under the formed pass's deadline (batched P5); "
+                         "policy: the reference OPTIMIZED policy on the queue")
+    ap.add_argument("--pass-frac", type=float, default=0.25,
+                    help="pass-selection cap on a pass's estimated time, as a fraction of the deadline")
+    ap.add_argument("--policy-grid-us", type=int, default=1000,
                     help="optimized policy knapsack quantum (reference: 1000)")
-    ap.add_argument("--sched-margin-ms", type=float, default=3.0,
+    ap.add_argument("--sched-margin-ms", type=float, default=0.0,
                     help="the scheduler plans against deadline - margin (scored on the true deadline)")
     ap.add_argument("--serve-profile", default="marginal", choices=["marginal", "device"],
                     help="scheduler latency table for batched serving")
@@ -526,9 +539,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    global SCHED_MARGIN_US, POLICY_GRID_US
-    SCHED_MARGIN_US = int(args.sched_margin_ms * 1000)
-    POLICY_GRID_US = int(args.policy_grid_us)
+    SERVE_OPTS.update(sched_margin_us=int(args.sched_margin_ms * 1000), policy_grid_us=int(args.policy_grid_us),
+                      selection=args.selection, pass_frac=args.pass_frac)
     if args.impl == "reference":
         reference_arm(args)
     else:

@@ -61,7 +61,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
                    host_clips: HostClips | None = None, slot_seed: int = 0,
                    window_us: int = 4_000_000, depth: int = 2, cost=None,
                    max_batch_requests: int | None = None, lead_us: int = 600, trace: bool = False,
-                   sched_margin_us: int = 0, policy_grid_us: int = 1000):
+                   sched_margin_us: int = 0, policy_grid_us: int = 1000, policy_at_dispatch: bool = False,
+                   device_policy=None, selection: str = "policy", max_pass_us: float | None = None):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -89,7 +90,27 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     downgrade can still prevent them (a pass, once launched, cannot be
     changed); SLO attainment is always scored on the true deadline.
     ``policy_grid_us``: the optimized policy's knapsack quantum (reference
-    1 ms; see ``policy.reassign_optimized``).
+    1 ms; see ``policy.reassign_optimized``).  ``policy_at_dispatch``: run
+    the policy once right before each pass is formed (instead of every
+    ``watermark`` arrivals), so it always sees the queue the pass will take.
+    ``device_policy``: a ``policy.DevicePolicy`` running the OPTIMIZED
+    policy on the GPU (one launch per pass).
+
+    ``selection="pass"`` (needs ``cost``; extension for the batched executor):
+    the per-request modality-subset choice is made when a pass is formed,
+    against the measured cost of THAT pass -- the north_star's policy step
+    (argmax accuracy under the request's remaining latency budget, SURVEY
+    §8a P5) with the budget coupled through the shared pass:
+      1. membership: queued jobs join in EDF order at their FASTEST frontier
+         candidate while the pass estimate meets every member's deadline;
+      2. upgrades: each member (EDF order, repeatedly) climbs its frontier
+         while the pass still meets every member's deadline AND the jobs left
+         queued could still meet theirs in one following all-fastest pass.
+    Idle GPU -> everyone at top accuracy; under load -> modalities dropped
+    exactly as far as the deadlines require.  ``max_pass_us`` caps a pass's
+    estimate in both steps (requests arriving during a pass wait for it and
+    then for their own: a pass of about half the deadline keeps them on
+    time).  The reference policies (``policy``) are not run in this mode.
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
@@ -127,7 +148,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     def run_policy(now):
         nonlocal since_opt
         t = time.perf_counter()
-        for j in apply_policy(policy, queue, now, fb, pol_rng, grid_us=policy_grid_us):
+        if device_policy is not None and policy is Policy.OPTIMIZED:
+            dropped = device_policy.apply(queue, now, fb)
+        else:
+            dropped = apply_policy(policy, queue, now, fb, pol_rng, grid_us=policy_grid_us)
+        for j in dropped:
             drop(j)
             stats.dropped_policy += j.size
         stats.policy_host_us += (time.perf_counter() - t) * 1e6
@@ -149,6 +174,8 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         if job is None:
             queue.running = inflight[-1][0][-1] if inflight else None
             return False
+        if selection == "pass" and cost is not None:
+            return dispatch_pass_select(now, job)
         batch = [job]
         mlist = [request_masks(job.assigned.strategy.parts, job.size)]
         counts = counts_of(mlist[0])
@@ -173,6 +200,67 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
                 tight = min(tight, cand.deadline_us)
             for j in batch:
                 j.est_finish_us = now + int(round(est_us))
+        return launch(now, batch, mlist, counts, n, est_us)
+
+    def cand_counts(j, idx):
+        """(masks, per-modality counts) of job j at frontier candidate idx (cached)."""
+        cache = getattr(j, "_cand_counts", None)
+        if cache is None:
+            cache = j._cand_counts = {}
+        if idx not in cache:
+            m = request_masks(j.candidates[idx].strategy.parts, j.size)
+            cache[idx] = (m, counts_of(m))
+        return cache[idx]
+
+    def dispatch_pass_select(now, head):
+        batch = [head]
+        head.assigned_idx = 0
+        counts = list(cand_counts(head, 0)[1])
+        n = head.size
+        tight = head.deadline_us
+        for cand in list(queue._jobs):  # 1. membership at the fastest candidates
+            if n + cand.size > cap:
+                break
+            c2 = [a + b for a, b in zip(counts, cand_counts(cand, 0)[1])]
+            e2 = cost.estimate_us(c2, n + cand.size)
+            if now + e2 > min(tight, cand.deadline_us) or (max_pass_us is not None and e2 > max_pass_us):
+                break
+            queue.remove(cand)
+            cand.state = JobState.RUNNING
+            cand.assigned_idx = 0
+            batch.append(cand)
+            counts, n = c2, n + cand.size
+            tight = min(tight, cand.deadline_us)
+        est = cost.estimate_us(counts, n)
+        rest = queue.jobs()
+        rest_counts = [0] * model.K
+        rest_n = 0
+        for j in rest:
+            rest_counts = [a + b for a, b in zip(rest_counts, cand_counts(j, 0)[1])]
+            rest_n += j.size
+        rest_fast = cost.estimate_us(rest_counts, min(rest_n, model.max_req)) if rest_n else 0.0
+        # the queued jobs that one following all-fastest pass can still serve on time
+        rest_dl = min((j.deadline_us for j in rest if j.deadline_us >= now + est + rest_fast), default=None)
+        moved = True
+        while moved:  # 2. upgrades
+            moved = False
+            for j in batch:
+                while j.assigned_idx + 1 < len(j.candidates):
+                    old = cand_counts(j, j.assigned_idx)[1]
+                    new = cand_counts(j, j.assigned_idx + 1)[1]
+                    c2 = [a - b + c for a, b, c in zip(counts, old, new)]
+                    e2 = cost.estimate_us(c2, n)
+                    if now + e2 > tight or (rest_dl is not None and now + e2 + rest_fast > rest_dl) or \
+                            (max_pass_us is not None and e2 > max_pass_us):
+                        break
+                    j.assigned_idx += 1
+                    counts, est, moved = c2, e2, True
+        for j in batch:
+            j.est_finish_us = now + int(round(est))
+        mlist = [cand_counts(j, j.assigned_idx)[0] for j in batch]
+        return launch(now, batch, mlist, counts, n, est)
+
+    def launch(now, batch, mlist, counts, n, est_us):
         nonlocal ring
         masks = np.concatenate(mlist)
         ev_s, ev_e = dv.Event(), dv.Event()
@@ -262,7 +350,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
             arrived = True
         while inflight and inflight[0][2].done():  # non-blocking completion checks
             finish()
-        if policy is not Policy.NONE and since_opt > 0 and len(queue) and \
+        if policy is not Policy.NONE and since_opt > 0 and len(queue) and not policy_at_dispatch and \
                 (since_opt >= watermark or not inflight):
             run_policy(now_us())
         while len(inflight) < depth and len(queue):
@@ -273,6 +361,11 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
                         sum(j.size for j in queue._jobs) < cap:
                     break  # let the batch grow; dispatch closer to the GPU freeing up
                 t = max(t, fin)
+            if policy_at_dispatch and policy is not Policy.NONE and since_opt > 0:
+                queue.running = inflight[-1][0][-1] if inflight else None
+                run_policy(now_us())
+                if not len(queue):
+                    break
             if not dispatch(t):
                 break
         if not inflight and not len(queue) and pos < len(pending):

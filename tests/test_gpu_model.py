@@ -141,3 +141,40 @@ def test_realtime_serving_batched_and_host_io(built):
     full = sum(model.row_bytes) * n_req
     assert 0 < st2.h2d_bytes <= full + 6 * n_req  # only present modalities are transferred
     assert st2.h2d_bytes % 2 == 0 and st2.d2h_bytes > 0
+
+
+def test_realtime_pass_selection_meets_slos(built):
+    """Batched pass-level selection (per-request accuracy argmax under the
+    formed pass's deadline): every served request meets its accuracy floor,
+    an idle GPU keeps every job at its most accurate candidate, and an
+    overloaded one drops modalities instead of missing deadlines."""
+    import paper_2310_18481_b200 as ms
+    from paper_2310_18481_b200.executor import build_tbn_model
+    from paper_2310_18481_b200.policy import Policy
+    from paper_2310_18481_b200.profiler import TBN_ACCURACY, marginal_profile, profile_pass_costs
+    from paper_2310_18481_b200.realtime import serve_realtime
+    model = build_tbn_model(max_req=32, n_slots=32)
+    cost = profile_pass_costs(model, reps=2)
+    prof = marginal_profile(cost, ("rgb", "flow", "audio"), TBN_ACCURACY, max_batch=4)
+    matrix = ms.build_matrix(prof, range(1, 9), ms.recommended_alphas(prof))
+
+    def run(qps, seed):
+        spec = ms.WorkloadSpec(kind="poisson", qps=qps, duration_s=1, deadline_ms=15, seed=seed)
+        jobs = [ms.JobTemplate(j.arrival_us, min(j.size, 8), j.accuracy_slo, j.deadline_us)
+                for j in ms.generate_jobs(spec, prof)]
+        cost.factor = 1.0
+        log, st = serve_realtime(model, prof, matrix, jobs, cost=cost, policy=Policy.NONE, selection="pass",
+                                 max_pass_us=0.25 * 15_000)
+        assert len(log.records) == len(jobs)
+        served = [r for r in log.records if not r.dropped]
+        assert all(r.achieved_accuracy >= r.accuracy_slo for r in served)
+        return log, served
+
+    log, served = run(200, 3)  # light load: top accuracy, on time
+    top = prof.combo_accuracy(prof.all_modalities_mask)
+    assert log.violation_ratio() == 0.0
+    assert sum(r.size for r in served if r.achieved_accuracy >= top - 1e-9) >= 0.95 * sum(r.size for r in served)
+    log, served = run(9000, 4)  # overload for an all-modality server of this size
+    dropped = sum(r.size for r in served if r.achieved_accuracy < top - 1e-9)
+    assert dropped > 0.3 * sum(r.size for r in served)
+    assert log.violation_ratio() < 0.05

@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-python tools/policy_bench.py > gpurun_out/policy_bench.txt 2>&1
+for f in 0.2 0.25; do for r in 16000 19000 22000; do
+python tools/serve_trace.py --rate $r --margin-ms 0 --selection pass --policy none --pass-frac $f 2>&1 | grep -v "^late"
+done; done > gpurun_out/serve_trace.txt

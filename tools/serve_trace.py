@@ -18,6 +18,11 @@ ap.add_argument("--deadline-ms", type=float, default=15)
 ap.add_argument("--profile", default="marginal")
 ap.add_argument("--margin-ms", type=float, default=3.0)
 ap.add_argument("--grid-us", type=int, default=20)
+ap.add_argument("--policy", default="optimized")
+ap.add_argument("--at-dispatch", type=int, default=1)
+ap.add_argument("--device-policy", type=int, default=0)
+ap.add_argument("--selection", default="policy")
+ap.add_argument("--pass-frac", type=float, default=0.0)
 a = ap.parse_args()
 import torch  # noqa: E402
 
@@ -30,6 +35,7 @@ from paper_2310_18481_b200.planner import build_matrix, recommended_alphas  # no
 from paper_2310_18481_b200.profiler import (TBN_ACCURACY, marginal_profile, profile_model,  # noqa: E402
                                             profile_pass_costs)
 from paper_2310_18481_b200.realtime import serve_realtime  # noqa: E402
+from paper_2310_18481_b200.policy import DevicePolicy, Policy  # noqa: E402
 
 names = ("rgb", "flow", "audio")
 model = build_tbn_model(max_req=96, n_slots=192)
@@ -43,11 +49,14 @@ from paper_2310_18481_b200.serving import JobTemplate  # noqa: E402
 jobs = [JobTemplate(j.arrival_us, min(j.size, 24), j.accuracy_slo, j.deadline_us) for j in jobs]
 cost.factor = 1.0
 log, st = serve_realtime(model, sprof, matrix, jobs, cost=cost, trace=True, sched_margin_us=int(a.margin_ms * 1000),
-                         policy_grid_us=a.grid_us)
+                         policy_grid_us=a.grid_us, policy=Policy(a.policy), policy_at_dispatch=bool(a.at_dispatch),
+                         device_policy=DevicePolicy(max_jobs=1024, max_cand=64, grid_us=a.grid_us) if a.device_policy
+                         else None, selection=a.selection,
+                         max_pass_us=a.pass_frac * a.deadline_ms * 1000 if a.pass_frac else None)
 late = [r for r in log.records if r.violated]
 served = [r for r in log.records if not r.dropped]
 fa = sprof.combo_accuracy(sprof.all_modalities_mask)
-print(f"grid {a.grid_us} us margin {a.margin_ms} ms: downgraded share {sum(r.size for r in served if r.achieved_accuracy < fa) / max(1, sum(r.size for r in served)):.3f}")
+print(f"selection={a.selection} pass_frac={a.pass_frac} {a.policy} at_dispatch={a.at_dispatch} dev={a.device_policy} grid {a.grid_us} us margin {a.margin_ms} ms: downgraded share {sum(r.size for r in served if r.achieved_accuracy < fa) / max(1, sum(r.size for r in served)):.3f}")
 print(f"rate {a.rate}: violation {log.violation_ratio():.4f} passes {st.passes} req/pass {st.requests / st.passes:.1f} "
       f"late {st.late} drops {st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} "
       f"policy {st.policy_host_us / max(1, st.policy_runs):.0f}us x{st.policy_runs} wall {st.wall_s:.2f}s")
