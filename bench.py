@@ -306,8 +306,15 @@ def dominant_gemm_roofline(model, peak_tflops):
     e1.record()
     us = e0.elapsed_us(e1) / n
     ach = fl / (us * 1e-6) / 1e12
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text()).get(plan.label)
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+    except Exception:
+        traffic = None
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
-            "frac": round(ach / peak_tflops, 4), "traffic": None,
+            "frac": round(ach / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
             "kernel": f"gemm_tc_kernel {plan.label}", "flop_per_launch": fl,
             "avg_launch_us": round(us, 2)}
 
