@@ -370,8 +370,19 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const int threads = (a.C / 8) * OW;
   if (a.k == 3 && (a.stride == 1 || a.stride == 2) && a.n_img <= 65535) {
     const int block = threads < 512 ? (threads + 31) / 32 * 32 : 512;
-    const int TH = 8;
-    dim3 grid((OH + TH - 1) / TH, a.n_img, (threads + block - 1) / block);
+    // output rows per thread: the largest of 8/4/2/1 whose grid fills its
+    // last wave of resident blocks to >= 85% (a 1.1-wave grid idles half the
+    // GPU in its tail); fewer rows cost only L2 re-reads of window rows
+    const int gz = (threads + block - 1) / block;
+    const int resident = 148 * (2048 / block);
+    int TH = 8;
+    for (int th = 8; th >= 1; th >>= 1) {
+      const long long blocks = (long long)((OH + th - 1) / th) * a.n_img * gz;
+      const double waves = (double)blocks / resident;
+      TH = th;
+      if (waves / ceil(waves) >= 0.85) break;
+    }
+    dim3 grid((OH + TH - 1) / TH, a.n_img, gz);
     auto X = reinterpret_cast<const __nv_bfloat16*>(a.X);
     auto Y = reinterpret_cast<__nv_bfloat16*>(a.Y);
     if (a.is_max && a.stride == 2)
