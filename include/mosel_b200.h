@@ -111,9 +111,10 @@ int ms_gather_rows(const void* src, long long row_bytes, const int32_t* slot, co
  * fly (halves host->device and HBM input bytes for video). */
 typedef struct MsRowDesc {
   long long lines;
-  int width, c_src, c_dst, pad_w;
+  int width, c_src, c_dst, pad_w; /* c_dst: 4 or a multiple of 8 */
   int src_u8;              /* 1: pool holds uint8 (frames, quantised flow) */
   float u8_scale, u8_bias; /* bf16 value = u8 * scale + bias */
+  int frame_h, pad_h;      /* frames of frame_h lines get pad_h zero rows above/below (0: none) */
 } MsRowDesc;
 int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                        const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows,
@@ -152,10 +153,12 @@ int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv,
 /* add a bf16 residual (same row mapping as the output, row stride res_ld)
  * after the activation: D = act(A W^T + b) + R */
 int ms_gemm_plan_set_residual(void* plan, const void* residual, long long res_ld);
-/* split K over `ksplit` CTAs per output tile (small-M GEMMs): partial sums
- * go to the caller's fp32 workspace ws[M, ws_ld] (ws_ld >= N, % 4 == 0),
- * then a finalize kernel applies bias/activation/residual; ms_gemm_run then
- * issues memset + GEMM + finalize.  Dense/gather single-segment plans only. */
+/* split K over `ksplit` CTAs per output tile (small-M GEMMs): each K part
+ * stores its partial sums into its own slab of the caller's fp32 workspace
+ * ws[ksplit, M, ws_ld] (ws_ld >= N, % 4 == 0); a finalize kernel adds the
+ * slabs in part order (bitwise reproducible) and applies bias/activation/
+ * residual; ms_gemm_run issues GEMM + finalize.  Dense/gather/conv
+ * single-segment plans. */
 int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld);
 int ms_gemm_run(const void* plan, void* stream);
 /* run the plan as 2-CTA clusters on SM pairs (tcgen05.mma.cta_group::2,

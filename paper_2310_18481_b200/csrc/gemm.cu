@@ -42,7 +42,20 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
-enum GemmMode : int { MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4 };
+enum GemmMode : int {
+  MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5
+};
+// MODE_CONV_C4: stride-2 first convolutions over 4-channel pixels (rgb 3 ->
+// 4, audio 1 -> 4) stored with `pad` zero rows AND columns around every
+// frame.  One output pixel's KW-tap window in one input row is 8 pixels x 4
+// channels = 64 contiguous bytes and consecutive output columns start 16
+// bytes apart: a 4-D tensor map {window 32 elems (64 B), output column
+// (16 B), padded input row (stride 2), image} with SWIZZLE_64B puts one
+// filter row's windows for the whole tile in the UMMA K-major SW64 layout.  A
+// K block = TWO filter rows = two such boxes in the two 8 KB halves of the
+// stage (K 0-31 | 32-63): K = ceil(KH/2) blocks of 64 (7x7: 4 instead of the
+// 7 of the 8-channel window mode -- 1.75x fewer MMAs, half the A bytes, and
+// the gather writes 8-byte pixels instead of 16).
 // MODE_CONV_SMALLC: first-layer convolutions with few channels (C8 = 8 or
 // 16 stored channels).  The input is stored W-padded by `pad` zero pixels on
 // each side, so for output pixel (oh, ow) and filter row kh the KW-tap
@@ -189,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // n = t % n_tiles).  The smem ring (full/empty) and the two TMEM accumulator
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
-  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC;
+  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4;
   if (threadIdx.x == 0) GEMM_TRACE(0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
@@ -283,6 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ow0/oh0 already include -pad; W is pre-padded in memory so the
             // column coordinate is the raw output column
             tma_load_4d(a_dst, &tmA, &full[s], half * kBK, (ow0 + p.pad) / p.stride, oh0 + kh, n0);
+          } else if constexpr (MODE == MODE_CONV_C4) {
+            // padded input row of (output row oh, filter row 2kb + l) = 2*oh + 2kb + l
+            const int c2 = (ow0 + p.pad) / 2, r0 = oh0 + p.pad + 2 * kb;
+            tma_load_4d(a_dst, &tmA, &full[s], 0, c2, r0, n0);
+            tma_load_4d(a_dst + kABytes / 2, &tmA, &full[s], 0, c2, r0 + 1, n0);
           }
           tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
           if (t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(3);
@@ -311,12 +329,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (MODE == MODE_GATHER) fence_proxy_async_smem();
         if (lane == 0 && t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(4);
         if (lane == 0) {
-          const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
+          if constexpr (MODE == MODE_CONV_C4) {  // two SW64 K halves of 32 (filter rows 2kb, 2kb+1)
+            const uint32_t a0 = smem_addr(smA + s * kABytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
-            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = umma_desc_sw64(a0 + (k >> 1) * (kABytes / 2)) + 2 * (k & 1);
+              umma_bf16(d_tmem, adesc, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+            }
+          } else {
+            const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+            }
           }
           umma_commit(&empty[s]);
           if (kb == ti.kb1 - 1) {
@@ -417,14 +444,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool tr0 = warp == 2 && lane == 0 && t == (int)blockIdx.x && c == grp;
         if (tr0) GEMM_TRACE(8);
         if constexpr (EPI == EPI_SPLITK) {
+          // this K part's partial sums -> its own workspace slab (plain stores;
+          // the finalize adds the slabs in part order: deterministic)
           if (out_row >= 0) {
-            float* w = p.ws + out_row * p.ws_ld + nb;
+            float* w = p.ws + ((long long)(ti.kb0 / p.kb_per) * p.M + out_row) * p.ws_ld + nb;
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
               if (nb + j < p.N)
-                atomicAdd(reinterpret_cast<float4*>(w + j),
-                          make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                                      __uint_as_float(v[j + 3])));
+                *reinterpret_cast<float4*>(w + j) =
+                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                __uint_as_float(v[j + 3]));
           }
         } else if constexpr (EPI == EPI_F32) {
           if (out_row >= 0) {
@@ -547,6 +576,7 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
     case MODE_CONV: return pick_act<MODE_CONV, EPI_TMA>(p.relu);
     case MODE_GATHER: return pick_act<MODE_GATHER, EPI_TMA>(p.relu);
     case MODE_CONV_SMALLC: return pick_act<MODE_CONV_SMALLC, EPI_TMA>(p.relu);
+    case MODE_CONV_C4: return pick_act<MODE_CONV_C4, EPI_TMA>(p.relu);
     default: return nullptr;
   }
 }
@@ -962,9 +992,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// split-K finalize: D = act(ws + bias) (+ residual), bf16 or fp32, one thread
-// per 4 columns.  It re-zeroes the workspace as it reads it, so the next
-// launch needs no memset (the plan's workspace starts zeroed).
+// split-K finalize: D = act(sum_k ws[k] + bias) (+ residual), bf16 or fp32,
+// one thread per 4 columns; the K-part slabs are added in part order, so the
+// result is bitwise reproducible (no atomics, no workspace zeroing).
 __global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
   pdl_trigger();
   pdl_wait();
@@ -975,10 +1005,14 @@ __global__ void splitk_finalize_kernel(const __grid_constant__ GemmParams p) {
        t += (long long)gridDim.x * blockDim.x) {
     const long long row = t / n4;
     const int n = (int)(t - row * n4) * 4;
-    float4* wsp = reinterpret_cast<float4*>(p.ws + row * p.ws_ld + n);
-    const float4 a = *wsp;
-    *wsp = make_float4(0.0f, 0.0f, 0.0f, 0.0f);  // leave the workspace zeroed for the next launch
-    const float av[4] = {a.x, a.y, a.z, a.w};
+    float av[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < p.ksplit; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(p.ws + ((long long)k * p.M + row) * p.ws_ld + n);
+      av[0] += a.x;
+      av[1] += a.y;
+      av[2] += a.z;
+      av[3] += a.w;
+    }
     for (int j = 0; j < 4 && n + j < p.N; ++j) {
       float x = activate(av[j] + (p.bias ? p.bias[n + j] : 0.0f), p.relu);
       if (p.residual) x += __bfloat162float(p.residual[row * p.res_ld + n + j]);
@@ -1104,7 +1138,7 @@ static int encode_store_maps(GemmPlan* P) {
   GemmParams& p = P->p;
   p.tma_store = 0;
   if (p.out_fp32) return MS_OK;
-  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC;
+  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4;
   for (int g = 0; g < p.nseg; ++g) {
     const Seg& S = p.seg[g];
     const int w = S.n_end - S.n_begin;
@@ -1225,7 +1259,7 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   if (plan == nullptr || X == nullptr || Wt == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
   if (stride < 1 || stride > 2 || bn * bh * bw > kBM || bn < 1 || bh < 1 || bw < 1)
     return set_error(MS_ERR_INVALID, "bad conv tile / stride");
-  if ((c_stride * 2) % 16 != 0) return set_error(MS_ERR_INVALID, "channel stride*2 must be a multiple of 16");
+  if ((c_stride * 2) % 16 != 0 && C != 4) return set_error(MS_ERR_INVALID, "channel stride*2 must be a multiple of 16");
   const int OH = (H + 2 * pad - KH) / stride + 1;
   const int OW = (W_in + 2 * pad - KW) / stride + 1;
   GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
@@ -1255,7 +1289,21 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
                            (cuuint64_t)c_stride * 2 * W_in * H};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   int num_kb;
-  if (C < kBK) {
+  if (C == 4) {
+    // X is [n_img, H + 2*pad, W_in + 2*pad, 4]: rows and columns pre-padded
+    if (stride != 2 || KW > 8 || KH > 8) return set_error(MS_ERR_INVALID, "4-channel conv needs stride 2, KH/KW <= 8");
+    p.mode = MODE_CONV_C4;
+    p.a_bytes = bn * bh * bw * 128;
+    num_kb = (KH + 1) / 2;
+    const long long wp = W_in + 2LL * pad, hp = H + 2LL * pad;
+    const long long pitch = wp * 4 * 2;
+    cuuint64_t d4[4] = {32, (cuuint64_t)OW, (cuuint64_t)hp, (cuuint64_t)n_img};
+    cuuint64_t s4[3] = {16, (cuuint64_t)pitch, (cuuint64_t)(pitch * hp)};
+    cuuint32_t b4[4] = {32, (cuuint32_t)bw, (cuuint32_t)(bh * 2), (cuuint32_t)bn};
+    cuuint32_t e4[4] = {1, 1, 2, 1};
+    int rc = encode_map(&P->tmA, 4, X, d4, s4, b4, e4, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  } else if (C < kBK) {
     // X is [n_img, H, W_in + 2*pad, C] (W pre-padded with zeros)
     if (C != 8 && C != 16) return set_error(MS_ERR_INVALID, "small-channel conv needs C == 8 or 16 (padded)");
     if (KW > 8) return set_error(MS_ERR_INVALID, "small-channel conv supports KW <= 8");
@@ -1350,7 +1398,7 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
     if (p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV1_ROWS || p.pair || p.nseg > 1 || ws == nullptr ||
         ws_ld % 4 != 0 || ws_ld < p.N)
       return set_error(MS_ERR_INVALID,
-                       "split-K needs a dense/gather/conv single-segment plan and ws[M, ws_ld>=N, %4]");
+                       "split-K needs a dense/gather/conv single-segment plan and ws[ksplit, M, ws_ld>=N, %4]");
   }
   const int kb_per = (p.num_kb + ksplit - 1) / ksplit;
   p.ksplit = (p.num_kb + kb_per - 1) / kb_per;  // no empty K parts

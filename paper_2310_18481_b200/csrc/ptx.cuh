@@ -186,6 +186,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;                  // SWIZZLE_128B
   return d;
 }
+// UMMA smem descriptor, K-major, 64-byte swizzle: 8-row x 64 B atoms, SBO =
+// 512 B between 8-row groups (32 bf16 of K per row; +32 B = +16 K)
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(512 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;  // SWIZZLE_64B
+  return d;
+}
 // UMMA descriptor, K-major, no swizzle (INTERLEAVE): core matrices of 8 rows
 // x 16 B stored contiguously; SBO = byte stride between 8-row groups (M),
 // LBO = byte stride between core matrices along K.

@@ -9,6 +9,8 @@
 //     contiguous modality-grouped sub-batches.
 #include <cstdint>
 
+#include <type_traits>
+
 #include "mosel_b200.h"
 #include "ptx.cuh"
 #include "runtime.h"
@@ -186,25 +188,32 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_
 // loads, then each thread emits whole destination pixels (c_dst/8 16-B
 // stores, zero pad channels / pad pixels), converting uint8 on the fly.
 constexpr int kMaxLineBytes = 16384;
-template <bool U8>
+// V = channels per vector store: 8 (uint4, c_dst % 8 == 0) or 4 (uint2, c_dst == 4).
+// frame_h > 0: the source lines are frames of frame_h rows and every frame
+// gets pad_h zero rows above and below in the destination (rows the kernel
+// never writes: the destination buffer is zeroed once at allocation).
+template <bool U8, int V>
 __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __restrict__ src_v, long long lines,
                                                               int width, int c_src, int c_dst, int pad_w,
                                                               float u8_scale, float u8_bias,
                                                               const int32_t* __restrict__ slot,
                                                               const int32_t* __restrict__ idx,
                                                               const int32_t* __restrict__ count,
-                                                              uint4* __restrict__ dst) {
+                                                              void* __restrict__ dst_v, int frame_h, int pad_h) {
+  typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
+  vec_t* dst = reinterpret_cast<vec_t*>(dst_v);
   const int n = *count;
   const int esz = U8 ? 1 : 2;
   const int line_bytes = width * c_src * esz;
-  const int g8 = c_dst / 8;
+  const int gv = c_dst / V;
   const int wd = width + 2 * pad_w;
+  const long long dst_lines = frame_h > 0 ? lines + (lines / frame_h) * 2LL * pad_h : lines;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
     int r = idx[j];
     if (slot) r = slot[r];
     const unsigned char* srow = reinterpret_cast<const unsigned char*>(src_v) + (long long)r * lines * line_bytes;
-    uint4* drow = dst + (long long)j * lines * wd * g8;
+    vec_t* drow = dst + (long long)j * dst_lines * wd * gv;
     const int per = min(32, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
     for (long long ln0 = (long long)blockIdx.x * per; ln0 < lines; ln0 += (long long)gridDim.x * per) {
       const int nl = (int)min((long long)per, lines - ln0);
@@ -213,17 +222,19 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
       for (int i = threadIdx.x; i < nl * line_bytes / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(line_buf)[i] = __ldcs(s4 + i);
       __syncthreads();
-      uint4* d = drow + ln0 * wd * g8;
       for (int q = threadIdx.x; q < nl * wd; q += blockDim.x) {
         const int li = q / wd, px = q - li * wd;
+        const long long ln = ln0 + li;
+        const long long dl = frame_h > 0 ? (ln / frame_h) * (frame_h + 2LL * pad_h) + pad_h + ln % frame_h : ln;
+        vec_t* d = drow + (dl * wd + px) * gv;
         const int x = px - pad_w;
         const unsigned char* lb = line_buf + li * line_bytes;
-        for (int g = 0; g < g8; ++g) {
+        for (int g = 0; g < gv; ++g) {
           unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           if (x >= 0 && x < width) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int c = g * 8 + i;
+            for (int i = 0; i < V; ++i) {
+              const int c = g * V + i;
               if (c < c_src) {
                 if (U8) {
                   const __nv_bfloat16 b = __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
@@ -234,8 +245,11 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
               }
             }
           }
-          d[(long long)q * g8 + g] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
-                                      v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+          if constexpr (V == 8)
+            d[g] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
+                              v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+          else
+            d[g] = make_uint2(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16));
         }
       }
     }
@@ -287,9 +301,12 @@ __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, lo
 
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
-                             cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f) {
-  if (c_dst % 8 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
-    return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0, pad_w >= 0");
+                             cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f,
+                             int frame_h = 0, int pad_h = 0) {
+  if ((c_dst % 8 != 0 && c_dst != 4) || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
+    return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0 or c_dst == 4, pad_w >= 0");
+  if (frame_h < 0 || pad_h < 0 || (frame_h > 0 && lines % frame_h != 0))
+    return set_error(MS_ERR_INVALID, "gather: frame_h must divide lines, pad_h >= 0");
   if (max_rows <= 0) return MS_OK;
   const int gy = max_rows < 65535 ? max_rows : 65535;
   const long long line_bytes = (long long)width * c_src * (src_u8 ? 1 : 2);
@@ -298,13 +315,25 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     long long bx = (lines + per - 1) / per;
     if (bx > 64) bx = 64;
     if (bx < 1) bx = 1;
-    if (src_u8)
-      gather_rows_pad_kernel<true><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-          src, lines, width, c_src, c_dst, pad_w, u8_scale, u8_bias, slot, idx, count, reinterpret_cast<uint4*>(dst));
-    else
-      gather_rows_pad_kernel<false><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-          src, lines, width, c_src, c_dst, pad_w, 1.0f, 0.0f, slot, idx, count, reinterpret_cast<uint4*>(dst));
+    const dim3 grid((unsigned)bx, (unsigned)gy);
+    const float sc = src_u8 ? u8_scale : 1.0f, bi = src_u8 ? u8_bias : 0.0f;
+    if (c_dst == 4) {
+      if (src_u8)
+        gather_rows_pad_kernel<true, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                              idx, count, dst, frame_h, pad_h);
+      else
+        gather_rows_pad_kernel<false, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                               idx, count, dst, frame_h, pad_h);
+    } else if (src_u8) {
+      gather_rows_pad_kernel<true, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                            idx, count, dst, frame_h, pad_h);
+    } else {
+      gather_rows_pad_kernel<false, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                             idx, count, dst, frame_h, pad_h);
+    }
   } else {
+    if (c_dst % 8 != 0 || frame_h > 0)
+      return set_error(MS_ERR_INVALID, "gather: 4-channel / frame-padded rows need 16-B aligned source lines");
     const long long work = lines * (width + 2LL * pad_w) * (c_dst / 8);
     long long bx = (work + 255) / 256;
     if (bx > 1024) bx = 1024;
@@ -390,11 +419,13 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
     if (X == nullptr || G == nullptr || rows == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
     const MsRowDesc& r = rows[k];
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
-    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && bytes % 16 == 0)
+    const bool framed = r.frame_h > 0 && r.pad_h > 0;
+    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && bytes % 16 == 0)
       rc = gather_launch(X[k], bytes, slot, idx + (long long)k * N, counts + k, N, G[k], st);
     else
       rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, slot, idx + (long long)k * N,
-                             counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias);
+                             counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias, framed ? r.frame_h : 0,
+                             framed ? r.pad_h : 0);
     if (rc) return rc;
   }
   return MS_OK;

@@ -37,7 +37,8 @@ class Segment(C.Structure):
 
 class RowDesc(C.Structure):
     _fields_ = [("lines", C.c_longlong), ("width", C.c_int), ("c_src", C.c_int), ("c_dst", C.c_int),
-                ("pad_w", C.c_int), ("src_u8", C.c_int), ("u8_scale", C.c_float), ("u8_bias", C.c_float)]
+                ("pad_w", C.c_int), ("src_u8", C.c_int), ("u8_scale", C.c_float), ("u8_bias", C.c_float),
+                ("frame_h", C.c_int), ("pad_h", C.c_int)]
 
 
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
@@ -265,8 +266,8 @@ def _auto_splitk(p, M, N, BN, num_kb, split_k, dev):
             split_k = max(1, min(num_kb // 4, SM_COUNT // tiles))
     if split_k > 1:
         ws_ld = -(-N // 4) * 4
-        # zeroed once; the finalize kernel re-zeroes it after every launch
-        ws = torch.zeros(M, ws_ld, dtype=torch.float32, device=dev)
+        # one [M, ws_ld] fp32 slab per K part (summed in order by the finalize)
+        ws = torch.empty(split_k * M, ws_ld, dtype=torch.float32, device=dev)
         check(lib().ms_gemm_plan_set_splitk(p.addr, split_k, ws.data_ptr(), ws_ld), "ms_gemm_plan_set_splitk")
         p.keep.append(ws)
         p.split_k = split_k
@@ -333,7 +334,7 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
         if k > 1:
             m_rows = n_img * oh * ow
             ws_ld = -(-Cout // 4) * 4
-            ws = _torch().zeros(m_rows, ws_ld, dtype=_torch().float32, device=D.device)
+            ws = _torch().empty(k * m_rows, ws_ld, dtype=_torch().float32, device=D.device)
             check(lib().ms_gemm_plan_set_splitk(p.addr, k, ws.data_ptr(), ws_ld), "ms_gemm_plan_set_splitk")
             p.keep.append(ws)
             p.split_k = k

@@ -67,9 +67,16 @@ class ModalitySpec:
 
     @property
     def cpad(self) -> int:
-        """Stored channels: padded to a multiple of 8 (16-B pixels) so the
-        first conv can read frames with TMA directly (MODE_CONV_SMALLC)."""
-        return -(-self.channels // 8) * 8
+        """Stored channels of the first conv's input: 4 for <= 4 real channels
+        (8-byte pixels: MODE_CONV_C4, one 128-B K block per filter-row pair),
+        else a multiple of 8 (16-B pixels, MODE_CONV_SMALLC)."""
+        return 4 if self.channels <= 4 else -(-self.channels // 8) * 8
+
+    @property
+    def row_pad(self) -> int:
+        """Zero rows above/below each frame in the first conv's input
+        (MODE_CONV_C4 pads rows itself instead of TMA out-of-bounds fill)."""
+        return CONV1_PAD if self.cpad == 4 else 0
 
     def frame_elems(self) -> int:
         return self.size * self.size * self.cpad
@@ -226,6 +233,18 @@ def pack_smallc_weight(w, cpad: int):
     return wp.reshape(cout, kh * 8 * cpad).contiguous()
 
 
+def pack_c4_weight(w):
+    """[cout, cin <= 4, kh <= 8, kw <= 8] -> [cout, ceil(kh/2) * 64]: K block
+    kb holds filter rows (2kb, 2kb+1), each as 8 window pixels x 4 channels
+    (MODE_CONV_C4's K order; missing rows/taps/channels are zero)."""
+    import torch
+    cout, cin, kh, kw = w.shape
+    nkb = -(-kh // 2)
+    wp = torch.zeros(cout, nkb * 2, 8, 4, dtype=torch.bfloat16)
+    wp[:, :kh, :kw, :cin] = w.permute(0, 2, 3, 1)
+    return wp.reshape(cout, nkb * 64).contiguous()
+
+
 def pack_im2col_weight(w, k_pad: int):
     """[cout, cin, k, k] -> [cout, k_pad] in im2col order (kh, kw, c)."""
     import torch
@@ -318,7 +337,8 @@ class BNInceptionEncoder:
         self.b = {}
         for name, (w, b) in W.items():
             if name == "conv1":
-                self.w[name] = pack_smallc_weight(w, self.mod.cpad).to(d)
+                cp = self.mod.cpad
+                self.w[name] = (pack_c4_weight(w) if cp == 4 else pack_smallc_weight(w, cp)).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
             else:
@@ -374,8 +394,11 @@ class BNInceptionEncoder:
         self.td2 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.tp = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.out = torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d)
-        # conv1 input: W-padded by CONV1_PAD zero pixels per side (the gather pads)
-        self.x = torch.zeros(n_img, size, size + 2 * CONV1_PAD, self.mod.cpad, dtype=bf, device=d)
+        # conv1 input: W-padded by CONV1_PAD zero pixels per side (the gather
+        # pads) and, for 4-channel frames, row-padded too (zero rows written
+        # once here, never touched by the gather)
+        rp = self.mod.row_pad
+        self.x = torch.zeros(n_img, size + 2 * rp, size + 2 * CONV1_PAD, self.mod.cpad, dtype=bf, device=d)
 
     def program(self, n_req: int):
         if n_req in self._programs:

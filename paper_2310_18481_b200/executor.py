@@ -62,8 +62,8 @@ class MaskedModel:
         self.encoders = encoders
         self.head = head
         self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
-        # (lines, width, c_src, c_dst, pad_w[, src_u8, u8_scale, u8_bias])
-        self.rows = [tuple(r) + (0, 1.0, 0.0)[len(r) - 5:] if len(r) < 8 else tuple(r) for r in rows]
+        # (lines, width, c_src, c_dst, pad_w[, src_u8, u8_scale, u8_bias[, frame_h, pad_h]])
+        self.rows = [tuple(r) + (0, 1.0, 0.0, 0, 0)[len(r) - 5:] for r in rows]
         self.src_bytes = [1 if r[5] else 2 for r in self.rows]
         self.row_bytes = [int(r[0] * r[1] * r[2] * b) for r, b in zip(self.rows, self.src_bytes)]
         self.K = len(encoders)
@@ -212,8 +212,10 @@ class MaskedModel:
         channels) + written (padded channels), + 2N mask bytes + 4*sum N_k
         index bytes."""
         counts = self.counts_for(np.asarray(masks))
-        rows = sum((rb + 2 * r[0] * (r[1] + 2 * r[4]) * r[3]) * c
-                   for r, rb, c in zip(self.rows, self.row_bytes, counts))
+        # written lines include the frame row padding (MsRowDesc frame_h / pad_h)
+        dst_lines = [r[0] + (r[0] // r[8]) * 2 * r[9] if r[8] and r[9] else r[0] for r in self.rows]
+        rows = sum((rb + 2 * dl * (r[1] + 2 * r[4]) * r[3]) * c
+                   for r, rb, dl, c in zip(self.rows, self.row_bytes, dst_lines, counts))
         return rows + 2 * len(masks) + 4 * sum(counts)
 
 
@@ -234,10 +236,12 @@ def build_tbn_model(max_req: int, n_slots: int, seeds=(101, 102, 103), fusion_se
         shape = (n_slots, segments, m.size, m.size, m.channels)
         if m.uint8:
             pools.append(torch.randint(0, 256, shape, generator=g, device=device, dtype=torch.uint8))
-            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD, 1, U8_SCALE, U8_BIAS))
+            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD, 1, U8_SCALE, U8_BIAS,
+                         m.size, m.row_pad))
         else:
             pools.append(torch.randn(shape, generator=g, device=device).to(torch.bfloat16))
-            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD))
+            rows.append((segments * m.size, m.size, m.channels, m.cpad, CONV1_PAD, 0, 1.0, 0.0, m.size,
+                         m.row_pad))
     return MaskedModel(encs, head, pools, rows, max_req, device)
 
 

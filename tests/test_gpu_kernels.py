@@ -414,6 +414,68 @@ def test_gather_staged_lines_u8_and_bf16(dev, c_src, c_dst, u8, width):
     assert torch.count_nonzero(dst) == 0
 
 
+@pytest.mark.parametrize("c_src,u8,width", [(3, True, 224), (1, False, 256), (3, False, 40)])
+def test_gather_four_channel_frames_with_row_padding(dev, c_src, u8, width):
+    """4-channel (8-byte) destination pixels with frame row padding
+    (MsRowDesc frame_h/pad_h): each frame's rows land between pad_h rows the
+    gather never writes, W-pad columns and the pad channel are zeroed."""
+    import ctypes
+    L = dev.lib()
+    frames, fh, pad, pad_h = 2, 3, 3, 2
+    lines = frames * fh
+    if u8:
+        pool = torch.randint(0, 256, (5, lines, width, c_src), dtype=torch.uint8).cuda()
+        ref_pool = (pool.float() / 64.0 - 2.0).to(torch.bfloat16)
+    else:
+        pool = _bf(torch.randn(5, lines, width, c_src)).cuda()
+        ref_pool = pool
+    cnt = torch.tensor([3], dtype=torch.int32, device="cuda")
+    dst = torch.full((3, frames, fh + 2 * pad_h, width + 2 * pad, 4), 5.0, dtype=torch.bfloat16, device="cuda")
+    rows = (dev.RowDesc * 1)(dev.RowDesc(lines, width, c_src, 4, pad, int(u8), 1.0 / 64.0, -2.0, fh, pad_h))
+    mask = torch.ones(5, dtype=torch.int16, device="cuda")
+    mask[1] = 0
+    mask[2] = 0
+    X = (ctypes.c_void_p * 1)(pool.data_ptr())
+    G = (ctypes.c_void_p * 1)(dst.data_ptr())
+    ix = torch.empty(5, dtype=torch.int32, device="cuda")
+    inv = torch.empty(5, dtype=torch.int32, device="cuda")
+    offs = torch.empty(3, dtype=torch.int32, device="cuda")
+    perm = torch.empty(5, dtype=torch.int32, device="cuda")
+    dev.check(L.ms_compact(mask.data_ptr(), 5, 1, X, rows, None, G, ix.data_ptr(), inv.data_ptr(),
+                           cnt.data_ptr(), offs.data_ptr(), perm.data_ptr(), dev.stream_ptr()), "compact")
+    torch.cuda.synchronize()
+    exp = ref_pool[torch.tensor([0, 3, 4]).cuda()].view(3, frames, fh, width, c_src)
+    body = dst[:, :, pad_h:pad_h + fh]
+    assert torch.equal(body[:, :, :, pad:pad + width, :c_src], exp)
+    body[:, :, :, pad:pad + width, :c_src] = 0
+    assert torch.count_nonzero(body) == 0  # W-pad columns and pad channels zeroed
+    assert torch.all(dst[:, :, :pad_h] == 5.0) and torch.all(dst[:, :, pad_h + fh:] == 5.0)  # pad rows untouched
+
+
+@pytest.mark.parametrize("n,H,Cin,tile", [(2, 32, 3, (1, 8, 16)), (2, 64, 1, (1, 4, 32)), (5, 224, 3, (1, 8, 16)),
+                                          (3, 256, 1, (1, 8, 16))])
+def test_conv_four_channel_row_padded_vs_torch(dev, n, H, Cin, tile):
+    """7x7/2 first-layer conv over 4-channel, row- and column-padded frames
+    (MODE_CONV_C4: 5-D TMA, one 128-B K block per filter-row pair)."""
+    from paper_2310_18481_b200.encoders import pack_c4_weight
+    g = torch.Generator().manual_seed(H + Cin + 7)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    X = torch.zeros(n, H + 6, H + 6, 4, dtype=torch.bfloat16)
+    X[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+    OH = (H + 6 - 7) // 2 + 1
+    D = torch.zeros(n * OH * OH, 64, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X.cuda(), n, H, H, 4, 4, 7, 7, 2, 3, pack_c4_weight(w).cuda(), 64,
+                      b.cuda(), D, ldd=64, BN=64, relu=True, tile=tile)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=2, padding=3).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, 64)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
 @pytest.mark.parametrize("M,K,N,BN", [(1000, 1024, 256, 256), (300, 192, 96, 96), (128, 64, 64, 64), (517, 576, 352, 192)])
 def test_gemm_cta_pair_dense_vs_torch(dev, M, K, N, BN):
     """2-CTA clusters (tcgen05.mma.cta_group::2, M=256 tiles)."""
