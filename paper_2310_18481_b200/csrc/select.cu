@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
                                                               void* __restrict__ dst_v, int frame_h, int pad_h) {
   typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
+  __shared__ long long s_dline[32];
   vec_t* dst = reinterpret_cast<vec_t*>(dst_v);
   const int n = *count;
   const int esz = U8 ? 1 : 2;
@@ -221,12 +222,20 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
       const uint4* s4 = reinterpret_cast<const uint4*>(srow + ln0 * line_bytes);
       for (int i = threadIdx.x; i < nl * line_bytes / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(line_buf)[i] = __ldcs(s4 + i);
+      if (threadIdx.x < nl) {  // destination line of each staged line (frame row padding)
+        const long long ln = ln0 + threadIdx.x;
+        s_dline[threadIdx.x] = frame_h > 0 ? (ln / frame_h) * (frame_h + 2LL * pad_h) + pad_h + ln % frame_h : ln;
+      }
       __syncthreads();
-      for (int q = threadIdx.x; q < nl * wd; q += blockDim.x) {
-        const int li = q / wd, px = q - li * wd;
-        const long long ln = ln0 + li;
-        const long long dl = frame_h > 0 ? (ln / frame_h) * (frame_h + 2LL * pad_h) + pad_h + ln % frame_h : ln;
-        vec_t* d = drow + (dl * wd + px) * gv;
+      int li = threadIdx.x / wd, px = threadIdx.x - li * wd;  // (line, pixel), advanced without divisions
+      const int step_l = blockDim.x / wd, step_p = blockDim.x - step_l * wd;
+      for (; li < nl; li += step_l, px += step_p) {
+        if (px >= wd) {
+          px -= wd;
+          ++li;
+          if (li >= nl) break;
+        }
+        vec_t* d = drow + (s_dline[li] * wd + px) * gv;
         const int x = px - pad_w;
         const unsigned char* lb = line_buf + li * line_bytes;
         for (int g = 0; g < gv; ++g) {
