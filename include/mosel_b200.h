@@ -75,6 +75,15 @@ int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t
                      const int64_t* deadline_us, int64_t dispatch_us, double factor, int N,
                      int32_t* choice, void* stream);
 
+/* ms_strategy_dp <- strategy.py:139-177 _DpTables (offline stage, SURVEY
+ * §8f #2): the exact min-latency / min-part-count table over (requests
+ * covered r <= max_size, credit index c < max_size*unit+1) for items
+ * (batch, latency_us, credit // gcd) in canonical order.  lat/cnt are device
+ * arrays [max_size+1, max_size*unit+1]; unreachable = 2^62 / INT32_MAX, as in
+ * the reference.  Query/back-walk stay on the host (byte-identical matrices). */
+int ms_strategy_dp(int n_items, const int32_t* batch, const int64_t* lat_us, const int32_t* credit_idx, int max_size,
+                   int unit, int64_t* lat, int32_t* cnt, void* stream);
+
 /* ms_policy_apply <- scheduler.py:382-425 apply_policy(OPTIMIZED) over a whole
  * EDF queue (detect_violation -> compute_budget -> reassign_optimized MCKP,
  * scheduler.py:187-326 -> drops -> try_upgrade :366-379), one launch.

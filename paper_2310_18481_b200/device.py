@@ -45,6 +45,7 @@ _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
 _SIGS = {
     "ms_abi_version": ([], C.c_int),
     "ms_set_pdl": ([_I], C.c_int),
+    "ms_strategy_dp": ([_I, _P, _P, _P, _I, _I, _P, _P, _P], C.c_int),
     "ms_policy_apply": ([_I, _I, _P, _P, _P, _P, _P, _P, C.c_int64, C.c_int64, _I, _D, C.c_int64, _P, _LL,
                          _P, _P], C.c_int),
     "ms_last_error": ([], C.c_char_p),

@@ -538,3 +538,26 @@ def test_coupled_queue_policy_on_device_matches_reference_goldens(dev):
         d1 = fine.apply(q1, case["now_us"], fb1)
         d2 = apply_policy(Policy.OPTIMIZED, q2, case["now_us"], fb2, grid_us=37)
         assert outcome(j1, d1) == outcome(j2, d2)
+
+
+def test_strategy_dp_on_device_matches_reference_matrices(dev, tmp_path):
+    """ms_strategy_dp (offline min-latency table, strategy.py:139-177) builds
+    the identical (latency, part-count) table, and the matrices built from it
+    are byte-identical to the reference's documents; then a large table
+    (S=64, K=4 synthetic) against the host mirror."""
+    from pathlib import Path
+    import numpy as np
+    from paper_2310_18481_b200.planner import (DeviceTable, _Table, build_matrix_device, recommended_alphas,
+                                              save_matrix)
+    from paper_2310_18481_b200.registry import SynthSpec, load_profile, synth_profile
+    golden = Path(__file__).resolve().parent / "golden"
+    for path in sorted((golden / "profiles").glob("*.yaml")):
+        prof = load_profile(path)
+        d, h = DeviceTable(prof, 8), _Table(prof, 8)
+        assert np.array_equal(d.lat, h.lat) and np.array_equal(d.cnt, h.cnt), path.stem
+        out = tmp_path / f"{path.stem}.json"
+        save_matrix(build_matrix_device(prof, range(1, 9), recommended_alphas(prof)), out)
+        assert out.read_text() == (golden / "matrices" / f"{path.stem}.json").read_text(), path.stem
+    prof = synth_profile(SynthSpec(n_modalities=4, max_batch=8), 3)
+    d, h = DeviceTable(prof, 64), _Table(prof, 64)
+    assert np.array_equal(d.lat, h.lat) and np.array_equal(d.cnt, h.cnt)
