@@ -577,8 +577,12 @@ class FusionHead:
         P = dv.Program()
         P.gemm(dv.plan_gather(list(feats), inv, self.w1, self.b1, self.h, M=n_req,
                               feat_dim=self.feat_dim, BN=256, relu=True))
-        P.gemm(dv.plan_dense(self.h, self.w2, self.b2, self.logits, M=n_req, K=FUSION_HIDDEN,
-                             BN=pick_bn(self.n_classes), out_fp32=True))
+        # the fp32 logits leave through the split-K finalize (coalesced rows)
+        # instead of the per-thread fp32 epilogue; K parts fill idle SMs
+        bn2 = pick_bn(self.n_classes)
+        tiles = -(-n_req // 128) * -(-self.n_classes // bn2)
+        P.gemm(dv.plan_dense(self.h, self.w2, self.b2, self.logits, M=n_req, K=FUSION_HIDDEN, BN=bn2,
+                             out_fp32=True, split_k=max(2, min(FUSION_HIDDEN // 64, 148 // tiles))))
         self._programs[key] = P.seal()
         return self._programs[key]
 
