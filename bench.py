@@ -428,8 +428,8 @@ def our_arm(args):
         agg = _allreduce(pg, [ok_req, tot_req], op="sum")
         if agg[0] >= 0.99 * agg[1]:
             break
-        log(f"[bench] attainment {agg[0] / max(1, agg[1]):.4f} < 0.99 at {rate:.1f} req/s: backing off 5%")
-        rate *= 0.95
+        log(f"[bench] attainment {agg[0] / max(1, agg[1]):.4f} < 0.99 at {rate:.1f} req/s: backing off 3%")
+        rate *= 0.97
     timed_s = args.steps * win
     from paper_2310_18481_b200.records import MetricsLog
     tlog = MetricsLog(lg.window_us, tuple(timed))
@@ -439,8 +439,9 @@ def our_arm(args):
     attainment = agg[0] / max(1, agg[1])
 
     # ---- e2e through the public API with host buffers: same serving, clips
-    # H2D (present modalities only) + logits D2H inside each pass; PCIe can
-    # bind before the GPU does, so back off (10 %/step) to its own >=99 % rate
+    # H2D (present modalities only, one DMA per modality ring per pass) +
+    # logits D2H inside each pass; PCIe can bind before the GPU does, so back
+    # off (4 %/step) to its own >=99 % rate
     hc = HostClips(model)
     e2e_rate = rate
     for attempt in range(8):
@@ -452,8 +453,8 @@ def our_arm(args):
         agg2 = _allreduce(pg, [ok2, tot2], op="sum")
         if agg2[0] >= 0.99 * agg2[1]:
             break
-        log(f"[bench] e2e attainment {agg2[0] / max(1, agg2[1]):.4f} at {e2e_rate:.1f} req/s: backing off 10%")
-        e2e_rate *= 0.9
+        log(f"[bench] e2e attainment {agg2[0] / max(1, agg2[1]):.4f} at {e2e_rate:.1f} req/s: backing off 4%")
+        e2e_rate *= 0.96
     e2e_value = agg2[0] / agg_t[0]
     n_steps_total = args.warmup + args.steps
 
@@ -524,7 +525,7 @@ def main():
     ap.add_argument("--workload", default="tbn", choices=["tbn", "vqa", "mlp"],
                     help="tbn = configs[1] (the headline); vqa = configs[2]; mlp = configs[0]")
     ap.add_argument("--window-s", type=float, default=1.0)
-    ap.add_argument("--search-seconds", type=float, default=2.0)
+    ap.add_argument("--search-seconds", type=float, default=3.0)
     ap.add_argument("--deadline-ms", type=float, default=15.0,
                     help="fixed per-request latency budget (deadline - arrival)")
     ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")

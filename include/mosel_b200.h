@@ -124,6 +124,7 @@ typedef struct MsRowDesc {
   int src_u8;              /* 1: pool holds uint8 (frames, quantised flow) */
   float u8_scale, u8_bias; /* bf16 value = u8 * scale + bias */
   int frame_h, pad_h;      /* frames of frame_h lines get pad_h zero rows above/below (0: none) */
+  int slot_off;            /* this modality's request->pool-row map is slot[slot_off + request] */
 } MsRowDesc;
 int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                        const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows,

@@ -429,10 +429,11 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
     const MsRowDesc& r = rows[k];
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
     const bool framed = r.frame_h > 0 && r.pad_h > 0;
+    const int32_t* sk = slot ? slot + r.slot_off : nullptr;  // per-modality pool rows
     if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && bytes % 16 == 0)
-      rc = gather_launch(X[k], bytes, slot, idx + (long long)k * N, counts + k, N, G[k], st);
+      rc = gather_launch(X[k], bytes, sk, idx + (long long)k * N, counts + k, N, G[k], st);
     else
-      rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, slot, idx + (long long)k * N,
+      rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, sk, idx + (long long)k * N,
                              counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias, framed ? r.frame_h : 0,
                              framed ? r.pad_h : 0);
     if (rc) return rc;

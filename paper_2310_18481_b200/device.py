@@ -38,7 +38,7 @@ class Segment(C.Structure):
 class RowDesc(C.Structure):
     _fields_ = [("lines", C.c_longlong), ("width", C.c_int), ("c_src", C.c_int), ("c_dst", C.c_int),
                 ("pad_w", C.c_int), ("src_u8", C.c_int), ("u8_scale", C.c_float), ("u8_bias", C.c_float),
-                ("frame_h", C.c_int), ("pad_h", C.c_int)]
+                ("frame_h", C.c_int), ("pad_h", C.c_int), ("slot_off", C.c_int)]
 
 
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double

@@ -64,20 +64,22 @@ class MaskedModel:
         self.pools = pools  # per modality: [n_slots, ...] bf16, row = one request
         # (lines, width, c_src, c_dst, pad_w[, src_u8, u8_scale, u8_bias[, frame_h, pad_h]])
         self.rows = [tuple(r) + (0, 1.0, 0.0, 0, 0)[len(r) - 5:] for r in rows]
+        # modality k's request -> pool-row map lives at slot_d[k*max_req : k*max_req + n]
+        self.rows = [r[:10] + (k * max_req,) for k, r in enumerate(self.rows)]
         self.src_bytes = [1 if r[5] else 2 for r in self.rows]
         self.row_bytes = [int(r[0] * r[1] * r[2] * b) for r, b in zip(self.rows, self.src_bytes)]
         self.K = len(encoders)
         self.max_req = max_req
         K, n = self.K, max_req
         self.mask_d = torch.zeros(n, dtype=torch.int16, device=self.dev)
-        self.slot_d = torch.zeros(n, dtype=torch.int32, device=self.dev)
+        self.slot_d = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
         self.idx = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
         self.inv = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
         self.counts = torch.zeros(K, dtype=torch.int32, device=self.dev)
         self.offs = torch.zeros((1 << K) + 1, dtype=torch.int32, device=self.dev)
         self.perm = torch.zeros(n, dtype=torch.int32, device=self.dev)
         self.mask_h = torch.zeros(n, dtype=torch.int16).pin_memory()
-        self.slot_h = torch.zeros(n, dtype=torch.int32).pin_memory()
+        self.slot_h = torch.zeros(K * n, dtype=torch.int32).pin_memory()
         import ctypes
         self._X = (ctypes.c_void_p * K)(*[p.data_ptr() for p in pools])
         self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
@@ -105,11 +107,16 @@ class MaskedModel:
         if n > self.max_req:
             raise ValueError(f"batch of {n} exceeds capacity {self.max_req}")
         self.mask_h[:n] = self.torch.as_tensor(np.asarray(masks, dtype=np.int16))
-        self.slot_h[:n] = self.torch.as_tensor(np.asarray(slots, dtype=np.int32))
+        sl = np.asarray(slots, dtype=np.int32)
+        if sl.ndim == 1:  # the same pool row for every modality
+            sl = np.broadcast_to(sl, (self.K, n))
+        sh = self.slot_h.numpy().reshape(self.K, self.max_req)
+        sh[:, :n] = sl
         s = stream or self.torch.cuda.current_stream()
         with self.torch.cuda.stream(s):
             self.mask_d[:n].copy_(self.mask_h[:n], non_blocking=True)
-            self.slot_d[:n].copy_(self.slot_h[:n], non_blocking=True)
+            self.slot_d.view(self.K, self.max_req)[:, :n].copy_(self.slot_h.view(self.K, self.max_req)[:, :n],
+                                                              non_blocking=True)
 
     # -- device pass ------------------------------------------------------
     def _compact(self, n: int):
@@ -195,7 +202,8 @@ class MaskedModel:
         self.torch.cuda.synchronize()
 
     def forward(self, slots, masks):
-        """One masked pass; returns the logits view [N, 397] (async)."""
+        """One masked pass; returns the logits view [N, 397] (async).
+        ``slots``: pool row per request ([N]) or per modality and request ([K, N])."""
         masks = np.asarray(masks)
         n = len(masks)
         counts = self.counts_for(masks)

@@ -131,7 +131,7 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
     since_opt = 0
     logits_host = torch.empty(model.max_req, model.head.logits.shape[1], dtype=torch.float32).pin_memory()
     copy_stream = torch.cuda.Stream() if host_clips is not None else None
-    ring = 0  # host-IO path: each pass uses fresh pool slots (no overlap with in-flight passes)
+    rings = [0] * model.K  # host-IO path: per-modality pool rings (fresh rows per pass)
     pol_rng = np.random.default_rng([0, list(Policy).index(policy)])
 
     torch.cuda.synchronize()
@@ -261,22 +261,33 @@ def serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templat
         return launch(now, batch, mlist, counts, n, est)
 
     def launch(now, batch, mlist, counts, n, est_us):
-        nonlocal ring
         masks = np.concatenate(mlist)
         ev_s, ev_e = dv.Event(), dv.Event()
         if host_clips is not None:
             # H2D of the present modalities' clips on a copy stream (overlaps the
-            # previous pass); the pass waits for it
-            slots = (ring + np.arange(n)) % model.n_slots
-            ring = (ring + n) % model.n_slots
+            # previous pass); the pass waits for it.  Each modality has its own
+            # ring in the pinned host buffer and in the HBM pool: the pass's
+            # requests that use modality k occupy consecutive rows of ring k,
+            # so ONE DMA per modality (two on wrap-around) moves them, and the
+            # compaction gather reads them through that modality's row map.
+            ns = model.n_slots
+            slots = np.zeros((model.K, n), dtype=np.int32)
             with torch.cuda.stream(copy_stream):
                 for k in range(model.K):
-                    for i in np.flatnonzero((masks.astype(np.int64) >> k) & 1):
-                        sl = int(slots[i])
-                        model.pools[k][sl].copy_(host_clips.host[k][sl], non_blocking=True)
-                        stats.h2d_bytes += host_clips.row_bytes[k]
+                    present = np.flatnonzero((masks.astype(np.int64) >> k) & 1)
+                    c = len(present)
+                    if not c:
+                        continue
+                    r0 = rings[k]
+                    slots[k, present] = (r0 + np.arange(c)) % ns
+                    rings[k] = (r0 + c) % ns
+                    first = min(c, ns - r0)
+                    model.pools[k][r0:r0 + first].copy_(host_clips.host[k][r0:r0 + first], non_blocking=True)
+                    if first < c:
+                        model.pools[k][: c - first].copy_(host_clips.host[k][: c - first], non_blocking=True)
+                    stats.h2d_bytes += c * host_clips.row_bytes[k]
             stream.wait_stream(copy_stream)
-            stats.h2d_bytes += n * 6  # masks + slots
+            stats.h2d_bytes += n * 2 + model.K * n * 4  # masks + per-modality row maps
         else:
             slots = rng.integers(0, model.n_slots, size=n)
         ev_s.record()
