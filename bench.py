@@ -406,7 +406,7 @@ def our_arm(args):
     seconds = (args.warmup + args.steps) * win
     from paper_2310_18481_b200 import device as dv
     clocks = ClockSampler(local)
-    for attempt in range(4):
+    for attempt in range(6):
         if pg is not None:
             pg.barrier()
         torch.cuda.synchronize()

@@ -104,6 +104,91 @@ __device__ __forceinline__ void pool_hrow(const __nv_bfloat16* __restrict__ X, l
   }
 }
 
+// max pooling keeps its row state as packed bf16x2: max is exact in bf16, so
+// this is bit-identical to the fp32 path with a third of the registers (more
+// resident warps = more loads in flight; the kernel is latency bound)
+__device__ __forceinline__ void pool_hrow_max2(const __nv_bfloat16* __restrict__ X, long long img, int H, int W,
+                                               long long xcs, int g, int ih, int w0, __nv_bfloat162 (&h)[4]) {
+  const __nv_bfloat162 ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) h[j] = ninf;
+  if (ih < 0 || ih >= H) return;
+  uint4 v[3];
+#pragma unroll
+  for (int dx = 0; dx < 3; ++dx) {  // issue the three loads before reducing
+    const int iw = w0 + dx;
+    v[dx] = (iw >= 0 && iw < W) ? __ldg(reinterpret_cast<const uint4*>(X + ((img * H + ih) * W + iw) * xcs + g * 8))
+                                : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+  }
+#pragma unroll
+  for (int dx = 0; dx < 3; ++dx) {
+    const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v[dx]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = __hmax2(h[j], e[j]);
+  }
+}
+
+template <int STRIDE>
+__global__ void __launch_bounds__(512, 3) pool3_rows_max_kernel(const __nv_bfloat16* __restrict__ X, int H, int W,
+                                                               int C, long long xcs, int pad, int OH, int OW, int TH,
+                                                               __nv_bfloat16* __restrict__ Y, long long ycs,
+                                                               int ycol0, const float* __restrict__ bias, int relu) {
+  pdl_trigger();
+  pdl_wait();
+  const int cg = C / 8;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;  // (column, channel group)
+  if (t >= cg * OW) return;
+  const int g = t % cg, ow = t / cg;
+  const long long img = blockIdx.y;
+  const int oh0 = blockIdx.x * TH;
+  const int oh1 = min(OH, oh0 + TH);
+  const int w0 = ow * STRIDE - pad;
+  __nv_bfloat162 h0[4], h1[4], h2[4];
+  int r0 = oh0 * STRIDE - pad;
+  pool_hrow_max2(X, img, H, W, xcs, g, r0, w0, h0);
+  pool_hrow_max2(X, img, H, W, xcs, g, r0 + 1, w0, h1);
+  pool_hrow_max2(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+  for (int oh = oh0; oh < oh1; ++oh) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 m = __hmax2(__hmax2(h0[j], h1[j]), h2[j]);
+      if (bias != nullptr || relu) {
+        float a = __low2float(m), b = __high2float(m);
+        if (bias != nullptr) {
+          a += bias[g * 8 + 2 * j];
+          b += bias[g * 8 + 2 * j + 1];
+        }
+        if (relu) {
+          a = fmaxf(a, 0.0f);
+          b = fmaxf(b, 0.0f);
+        }
+        pk[j] = pack_bf16x2(a, b);
+      } else {
+        pk[j] = *reinterpret_cast<const uint32_t*>(&m);
+      }
+    }
+    *reinterpret_cast<uint4*>(Y + ((img * OH + oh) * OW + ow) * ycs + ycol0 + g * 8) =
+        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    if (oh + 1 < oh1) {
+      r0 += STRIDE;
+      if (STRIDE == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          h0[j] = h1[j];
+          h1[j] = h2[j];
+        }
+        pool_hrow_max2(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h0[j] = h2[j];
+        pool_hrow_max2(X, img, H, W, xcs, g, r0 + 1, w0, h1);
+        pool_hrow_max2(X, img, H, W, xcs, g, r0 + 2, w0, h2);
+      }
+    }
+  }
+}
+
 template <bool MAX, int STRIDE>
 __global__ void __launch_bounds__(512) pool3_rows_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C, long long xcs,
                                   int pad, int OH, int OW, int TH, __nv_bfloat16* __restrict__ Y,
@@ -386,11 +471,11 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
     auto X = reinterpret_cast<const __nv_bfloat16*>(a.X);
     auto Y = reinterpret_cast<__nv_bfloat16*>(a.Y);
     if (a.is_max && a.stride == 2)
-      launch_k(pool3_rows_kernel<true, 2>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
-                                                        a.ycol0, a.bias, a.relu);
+      launch_k(pool3_rows_max_kernel<2>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y,
+               a.ycs, a.ycol0, a.bias, a.relu);
     else if (a.is_max)
-      launch_k(pool3_rows_kernel<true, 1>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
-                                                        a.ycol0, a.bias, a.relu);
+      launch_k(pool3_rows_max_kernel<1>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y,
+               a.ycs, a.ycol0, a.bias, a.relu);
     else if (a.stride == 2)
       launch_k(pool3_rows_kernel<false, 2>, grid, dim3(block), 0, st, 1, X, a.H, a.W, a.C, a.xcs, a.pad, OH, OW, TH, Y, a.ycs,
                                                          a.ycol0, a.bias, a.relu);

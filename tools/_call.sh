@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-timeout 1300 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+python tools/op_times.py --n 32 --top 200 > gpurun_out/op32g.txt 2>&1
