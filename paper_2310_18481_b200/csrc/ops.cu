@@ -128,6 +128,75 @@ __device__ __forceinline__ void pool_hrow_max2(const __nv_bfloat16* __restrict__
   }
 }
 
+// 3x3 / stride 1 / pad 1 AVERAGE pooling (count_include_pad: / 9) of the
+// narrow projection branches (32-128 channels), + bias + ReLU, into a channel
+// slice of the block output.  A CTA stages TH+2 input rows of one frame
+// (zero-padded at the borders) in shared memory with coalesced 16-B loads,
+// then every output (pixel, 8 channels) is summed from shared memory in fp32.
+// The register-streaming kernel spent most of its time waiting on dependent
+// row loads for these tiny rows.
+constexpr int kAvgSmem = 40 * 1024;
+__global__ void __launch_bounds__(256) avgpool3_s1_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C,
+                                                         long long xcs, int TH, __nv_bfloat16* __restrict__ Y,
+                                                         long long ycs, int ycol0, const float* __restrict__ bias,
+                                                         int relu) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(16) uint4 tile[];  // [TH+2][W+2][C/8] x 16 B
+  const int cg = C / 8;
+  const int wp = W + 2;
+  const long long img = blockIdx.y;
+  const int oh0 = blockIdx.x * TH;
+  const int rows = TH + 2;
+  for (int i = threadIdx.x; i < rows * wp * cg; i += blockDim.x) {
+    const int g = i % cg;
+    const int x = (i / cg) % wp - 1;
+    const int r = i / (cg * wp);
+    const int ih = oh0 - 1 + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (ih >= 0 && ih < H && x >= 0 && x < W)
+      v = __ldg(reinterpret_cast<const uint4*>(X + ((img * H + ih) * W + x) * xcs + g * 8));
+    tile[i] = v;
+  }
+  __syncthreads();
+  const int oh1 = min(H, oh0 + TH);
+  for (int i = threadIdx.x; i < (oh1 - oh0) * W * cg; i += blockDim.x) {
+    const int g = i % cg;
+    const int x = (i / cg) % W;
+    const int r = i / (cg * W);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const uint4 v = tile[((r + dy) * wp + x + dx) * cg + g];
+        const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(e[j]);
+          acc[2 * j] += f.x;
+          acc[2 * j + 1] += f.y;
+        }
+      }
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float a = acc[2 * j] * (1.0f / 9.0f), b = acc[2 * j + 1] * (1.0f / 9.0f);
+      if (bias != nullptr) {
+        a += bias[g * 8 + 2 * j];
+        b += bias[g * 8 + 2 * j + 1];
+      }
+      if (relu) {
+        a = fmaxf(a, 0.0f);
+        b = fmaxf(b, 0.0f);
+      }
+      pk[j] = pack_bf16x2(a, b);
+    }
+    *reinterpret_cast<uint4*>(Y + ((img * H + oh0 + r) * W + x) * ycs + ycol0 + g * 8) =
+        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
 template <int STRIDE>
 __global__ void __launch_bounds__(512, 3) pool3_rows_max_kernel(const __nv_bfloat16* __restrict__ X, int H, int W,
                                                                int C, long long xcs, int pad, int OH, int OW, int TH,
@@ -453,6 +522,19 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const int OH = pool_out(a.H, a.k, a.stride, a.pad, a.ceil_mode);
   const int OW = pool_out(a.W, a.k, a.stride, a.pad, a.ceil_mode);
   const int threads = (a.C / 8) * OW;
+  if (!a.is_max && a.k == 3 && a.stride == 1 && a.pad == 1 && a.n_img <= 65535 &&
+      3 * (a.W + 2) * a.C * 2 <= kAvgSmem) {
+    // the fp32 sums of 9 taps: order per output (dy, dx) = the oracle's window order up to fp32 rounding
+    const int row_bytes = (a.W + 2) * a.C * 2;
+    int TH = kAvgSmem / row_bytes - 2;
+    if (TH > a.H) TH = a.H;
+    if (TH < 1) TH = 1;
+    dim3 grid((a.H + TH - 1) / TH, a.n_img);
+    const size_t smem = (size_t)(TH + 2) * row_bytes;
+    launch_k(avgpool3_s1_kernel, grid, dim3(256), smem, st, 1, reinterpret_cast<const __nv_bfloat16*>(a.X), a.H,
+             a.W, a.C, a.xcs, TH, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0, a.bias, a.relu);
+    return check_launch("avgpool3_s1_kernel");
+  }
   if (a.k == 3 && (a.stride == 1 || a.stride == 2) && a.n_img <= 65535) {
     const int block = threads < 512 ? (threads + 31) / 32 * 32 : 512;
     // output rows per thread: the largest of 8/4/2/1 whose grid fills its

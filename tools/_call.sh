@@ -1,3 +1,2 @@
-for f in 0.2 0.25 0.3; do for r in 16500 18000; do
-python tools/serve_trace.py --rate $r --selection pass --policy none --pass-frac $f --margin-ms 0 2>&1 | grep -E "selection|^rate"
-done; done > gpurun_out/serve_trace.txt
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+python tools/op_times.py --n 64 --mask 1 --top 60 > gpurun_out/op64r.txt 2>&1

@@ -15,6 +15,7 @@ ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--mod", type=int, default=0)
 ap.add_argument("--op", type=int, default=20)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--mask", type=int, default=7)
 a = ap.parse_args()
 import torch  # noqa: E402
 
@@ -26,7 +27,7 @@ from paper_2310_18481_b200.executor import build_tbn_model  # noqa: E402
 
 m = build_tbn_model(max_req=a.n, n_slots=a.n)
 m.use_graphs = False
-masks = np.full(a.n, 7, dtype=np.int16)
+masks = np.full(a.n, a.mask, dtype=np.int16)
 m.forward(np.arange(a.n), masks)
 torch.cuda.synchronize()
 prog = m.encoders[a.mod].program(a.n)

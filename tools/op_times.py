@@ -17,6 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=96)
 ap.add_argument("--mixed", action="store_true")
+ap.add_argument("--mask", type=int, default=7)
 ap.add_argument("--top", type=int, default=45)
 ap.add_argument("--rep", type=int, default=10)
 a = ap.parse_args()
@@ -32,7 +33,7 @@ from paper_2310_18481_b200.executor import build_tbn_model  # noqa: E402
 
 m = build_tbn_model(max_req=a.n, n_slots=max(8, a.n))
 rng = np.random.default_rng(0)
-masks = rng.integers(1, 8, size=a.n).astype(np.int16) if a.mixed else np.full(a.n, 7, dtype=np.int16)
+masks = rng.integers(1, 8, size=a.n).astype(np.int16) if a.mixed else np.full(a.n, a.mask, dtype=np.int16)
 slots = np.arange(a.n) % m.n_slots
 m.use_graphs = False
 for _ in range(2):
