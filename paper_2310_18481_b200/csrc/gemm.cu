@@ -39,12 +39,26 @@ constexpr int kStageRowBytes = 80;                         // 64 B of bf16 + 16 
 constexpr int kStageWarpBytes = 32 * kStageRowBytes;       // one warp's 32 x 32 bf16 chunk
 constexpr int kStageBytes = kEpiWarps * kStageWarpBytes;   // epilogue staging buffers
 constexpr int kBM = 128;
+constexpr int kMaxHaloStages = 16;
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int {
-  MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5
+  MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5,
+  MODE_CONV_HALO = 6
 };
+// MODE_CONV_HALO: 3x3 / stride 1 / pad 1 convolutions over images at least
+// 14 pixels wide.  The output tile is bh whole image rows of P pixels (P =
+// the image width + 2 rounded up to 8, so bh * P = 128).  Per 64-channel
+// chunk ONE TMA box loads the (bh + 2) x P halo of input pixels (zero fill at
+// the borders) into shared memory, and each of the 9 taps is an MMA whose A
+// operand is the same tile read from a start address shifted by
+// (dy * P + dx) rows of 128 B -- a K-major SW128 descriptor may start at any
+// 128-B row (tools/umma_probe.py: the swizzle is address based), and 8-row
+// groups stay 1024 B apart across halo rows because P is a multiple of 8.
+// A traffic drops ~6x versus one box per tap; only the weights stream per
+// tap.  Output columns >= OW (and rows >= OH) read wrapped halo pixels and
+// are clipped by the TMA store.
 // MODE_CONV_C4: stride-2 first convolutions over 4-channel pixels (rgb 3 ->
 // 4, audio 1 -> 4) stored with `pad` zero rows AND columns around every
 // frame.  One output pixel's KW-tap window in one input row is 8 pixels x 4
@@ -106,6 +120,7 @@ struct GemmParams {
   long long ws_ld;
   unsigned long long* trace;  // debug: per-CTA %globaltimer stamps (kTraceSlots each) or null
   int tma_store;    // 1: bf16 epilogue writes each 128 x 32 chunk with one TMA store (StoreMaps)
+  int halo_slot;    // MODE_CONV_HALO: bytes of one halo buffer (2 buffers precede the weight ring)
   int stage_bytes;  // epilogue staging bytes in shared memory
 };
 
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // n = t % n_tiles).  The smem ring (full/empty) and the two TMEM accumulator
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
-  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4;
+  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4 || MODE == MODE_CONV_HALO;
   if (threadIdx.x == 0) GEMM_TRACE(0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
@@ -210,13 +225,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
   uint8_t* smA = smem;
-  uint8_t* smB = smem + stages * kABytes;
+  uint8_t* smB = smem + (MODE == MODE_CONV_HALO ? 2 * p.halo_slot : stages * kABytes);
   uint8_t* sstage = smB + stages * p.b_bytes;  // [p.stage_bytes], 1024-B aligned
   uint64_t* full = reinterpret_cast<uint64_t*>(sstage + p.stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* afull = tempty + 2;   // MODE_CONV_HALO halo buffers
+  uint64_t* aempty = afull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [N], 16-B aligned
 
   const int warp = threadIdx.x >> 5;
@@ -233,6 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&afull[a], 1);
+      mbar_init(&aempty[a], 1);
     }
     fence_barrier_init();
   }
@@ -260,7 +279,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) GEMM_TRACE(2);
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (MODE == MODE_CONV_HALO && lane == 0) {
+      // ------------------------------------- TMA producer (halo + per-tap weights)
+      int s = 0, hs = 0;
+      uint32_t phase = 0, hphase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const TileIdx ti = decode_tile(p, t, n_tiles);
+        const int th = ti.m % p.tiles_h;
+        const int img = ti.m / p.tiles_h;
+        for (int cc = 0; cc < p.cchunks; ++cc) {
+          mbar_wait(&aempty[hs], hphase ^ 1);
+          mbar_arrive_expect_tx(&afull[hs], p.a_bytes);
+          tma_load_4d(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
+          for (int tap = 0; tap < 9; ++tap) {
+            mbar_wait(&empty[s], phase ^ 1);
+            mbar_arrive_expect_tx(&full[s], p.b_bytes);
+            tma_load_2d(smem_addr(smB + s * p.b_bytes), &tmB, &full[s], (tap * p.cchunks + cc) * kBK,
+                        ti.n * p.BN);
+            if (++s == stages) {
+              s = 0;
+              phase ^= 1;
+            }
+          }
+          if (++hs == 2) {
+            hs = 0;
+            hphase ^= 1;
+          }
+        }
+      }
+    } else if (MODE != MODE_CONV_HALO && lane == 0) {
       // ------------------------------------------------ TMA producer
       int s = 0;
       uint32_t phase = 0;
@@ -310,6 +357,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+    }
+  } else if (warp == 1 && MODE == MODE_CONV_HALO) {
+    // ------------------------------------ MMA issuer: 9 shifted views per halo
+    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)p.BN);
+    int s = 0, hs = 0;
+    uint32_t phase = 0, hphase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int P = p.bw;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
+      for (int cc = 0; cc < p.cchunks; ++cc) {
+        mbar_wait(&afull[hs], hphase);
+        tc_fence_after();
+        const uint32_t halo = smem_addr(smA + hs * p.halo_slot);
+        for (int tap = 0; tap < 9; ++tap) {
+          mbar_wait(&full[s], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const int dy = tap / 3, dx = tap - 3 * (tap / 3);
+            const uint64_t adesc = umma_desc_sw128(halo + (uint32_t)((dy * P + dx) * 128));
+            const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+            umma_commit(&empty[s]);
+            if (tap == 8) {
+              umma_commit(&aempty[hs]);
+              if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+            }
+          }
+          __syncwarp();
+          if (++s == stages) {
+            s = 0;
+            phase ^= 1;
+          }
+        }
+        if (++hs == 2) {
+          hs = 0;
+          hphase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp == 1) {
     // -------------------------------------------------- MMA issuer
@@ -577,6 +670,7 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
     case MODE_GATHER: return pick_act<MODE_GATHER, EPI_TMA>(p.relu);
     case MODE_CONV_SMALLC: return pick_act<MODE_CONV_SMALLC, EPI_TMA>(p.relu);
     case MODE_CONV_C4: return pick_act<MODE_CONV_C4, EPI_TMA>(p.relu);
+    case MODE_CONV_HALO: return pick_act<MODE_CONV_HALO, EPI_TMA>(p.relu);
     default: return nullptr;
   }
 }
@@ -1092,11 +1186,11 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
   p.stage_bytes = p.tma_store ? kStoreBytes : 0;  // fp32 / split-K epilogues stage nothing
   // 227 KB usable: 1 KB alignment slack, barriers, epilogue staging, bias
-  int stages = (226 * 1024 - 1024 - 256 - p.stage_bytes - bias_bytes) / per_stage;
+  int stages = (226 * 1024 - 1024 - 288 - p.stage_bytes - bias_bytes) / per_stage;
   if (stages > 8) stages = 8;
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 4) * 8 + 16 + bias_bytes;
+  P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
@@ -1138,7 +1232,7 @@ static int encode_store_maps(GemmPlan* P) {
   GemmParams& p = P->p;
   p.tma_store = 0;
   if (p.out_fp32) return MS_OK;
-  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4;
+  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4 || p.mode == MODE_CONV_HALO;
   for (int g = 0; g < p.nseg; ++g) {
     const Seg& S = p.seg[g];
     const int w = S.n_end - S.n_begin;
@@ -1349,6 +1443,41 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   const int tiles_n = (n_img + bn - 1) / bn;
   if (int rc_store = encode_store_maps(P)) return rc_store;
   return finish_plan(P, Wt, num_kb * kBK, Cout, BN, num_kb, tiles_n * p.tiles_h * p.tiles_w);
+}
+
+int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
+                           const void* Wt, int Cout, int BN, const float* bias, int relu, void* D, long long ldd,
+                           int col0, int nseg, const MsSegment* segs) {
+  if (W_in < 14 || C < 64) return set_error(MS_ERR_INVALID, "halo conv: width >= 14 and >= 64 input channels");
+  const int P = ((W_in + 2) + 7) / 8 * 8;
+  if (128 % P != 0) return set_error(MS_ERR_INVALID, "halo conv: padded row width must divide 128 (W <= 62)");
+  const int bh = 128 / P;
+  // a 3x3/1/1 conv plan with (1 image x bh rows x P columns) output tiles; then
+  // the A map becomes one (bh + 2) x P halo box per 64-channel chunk
+  int rc = ms_gemm_plan_conv(plan, X, n_img, H, W_in, C, c_stride, 3, 3, 1, 1, Wt, Cout, BN, bias, relu, D, ldd,
+                             col0, nseg, segs, 1, bh, P);
+  if (rc) return rc;
+  GemmPlan* Pl = reinterpret_cast<GemmPlan*>(plan);
+  GemmParams& p = Pl->p;
+  if (p.mode != MODE_CONV || p.tiles_w != 1) return set_error(MS_ERR_INVALID, "halo conv: unexpected tiling");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W_in, (cuuint64_t)H, (cuuint64_t)n_img};
+  cuuint64_t strides[3] = {(cuuint64_t)c_stride * 2, (cuuint64_t)c_stride * 2 * W_in,
+                           (cuuint64_t)c_stride * 2 * W_in * H};
+  cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)P, (cuuint32_t)(bh + 2), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  rc = encode_map(&Pl->tmA, 4, X, dims, strides, box, es);
+  if (rc) return rc;
+  p.mode = MODE_CONV_HALO;
+  p.a_bytes = kBK * P * (bh + 2) * 2;
+  // + 2 rows: the last tap's shifted view of the last M rows reads past the halo
+  p.halo_slot = ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024;
+  const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
+  int stages = (226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes) / p.b_bytes;
+  if (stages > kMaxHaloStages) stages = kMaxHaloStages;  // weights-only stages are small: go deep
+  if (stages < 2) return set_error(MS_ERR_INVALID, "halo conv: weights tile does not fit");
+  p.stages = stages;
+  Pl->smem_bytes = 1024 + 2 * p.halo_slot + stages * p.b_bytes + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
+  return MS_OK;
 }
 
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,

@@ -59,6 +59,7 @@ _SIGS = {
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
                            _I, _I, _P, _I, _I, _I], C.c_int),
+    "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -314,7 +315,19 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
 
 
 def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, bias, D, *, ldd,
-              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None, split_k=None):
+              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None, split_k=None, halo=False):
+    """Implicit-GEMM conv plan.  ``halo=True`` (3x3/1/1, width 14..62, >= 64
+    channels): one halo box per channel chunk, taps as shifted smem views."""
+    if halo:
+        p = GemmPlan()
+        nseg, sarr = _segments(segs)
+        check(lib().ms_gemm_plan_conv_halo(p.addr, ptr(X), n_img, H, W_in, C_in, c_stride, ptr(Wt), Cout, BN,
+                                           ptr(bias), int(relu), ptr(D), ldd, col0, nseg, sarr),
+              "ms_gemm_plan_conv_halo")
+        p.keep = [X, Wt, bias, D, segs]
+        p.flops = 2 * n_img * H * W_in * Cout * 9 * C_in
+        p.label = f"conv 3x3/1 {C_in}->{Cout} {n_img}x{H}x{W_in} halo"
+        return p
     p = GemmPlan()
     nseg, sarr = _segments(segs)
     bn, bh, bw = tile

@@ -431,9 +431,12 @@ class BNInceptionEncoder:
         P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
         P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
                              M=n * h2 * h2, K=64, BN=64, relu=True))
+        # conv2 (56x56 rgb/flow): halo reuse measured 1.08-1.09x faster than the
+        # tap-box 2-SM kernel (tools/halo_bench.py); narrower layers lose more to
+        # the ceil8(W+2)-wide tiles than they gain, audio's 64+2 does not tile 128
         P.gemm(dv.plan_conv(self.a_c2r, n, h2, h2, 64, 64, 3, 3, 1, 1, self.w["conv2"], 192,
                             self.b["conv2"], self.a_c2, ldd=192, BN=192, relu=True,
-                            tile=pick_conv_tile(n, h2, h2)))
+                            tile=pick_conv_tile(n, h2, h2), halo=42 <= h2 <= 62))
         h = pool_out(h2, 3, 2, 0, True)
         cur = self.ping
         P.pool(self.a_c2, n, h2, h2, 192, 192, 3, 2, 0, True, True, cur, 192, 0)

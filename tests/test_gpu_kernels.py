@@ -561,3 +561,28 @@ def test_strategy_dp_on_device_matches_reference_matrices(dev, tmp_path):
     prof = synth_profile(SynthSpec(n_modalities=4, max_batch=8), 3)
     d, h = DeviceTable(prof, 64), _Table(prof, 64)
     assert np.array_equal(d.lat, h.lat) and np.array_equal(d.cnt, h.cnt)
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout,BN", [(3, 14, 64, 96, 96), (2, 28, 96, 96, 96), (2, 28, 160, 224, 224),
+                                             (1, 56, 64, 192, 192), (2, 14, 192, 320, 160), (4, 28, 64, 64, 64)])
+def test_conv_halo_vs_torch(dev, n, H, Cin, Cout, BN):
+    """3x3/1/1 implicit GEMM with halo reuse (MODE_CONV_HALO): the 9 taps are
+    shifted shared-memory views of one (bh+2) x ceil8(W+2) halo box per
+    64-channel chunk; output written into a channel slice of a wider tensor."""
+    g = torch.Generator().manual_seed(n * H + Cin + 11)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, 3, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    ldd, col0 = Cout + 64, 32
+    D = torch.full((n * H * H, ldd), 3.0, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, 3, 3, 1, 1, packed.cuda(), Cout, b.cuda(), D, ldd=ldd, col0=col0,
+                      BN=BN, relu=True, halo=True)
+    p.run()
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=1, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D[:, col0:col0 + Cout].cpu(), ref)
+    assert ok, (err, scale)
+    assert torch.all(D[:, :col0] == 3.0) and torch.all(D[:, col0 + Cout:] == 3.0)
