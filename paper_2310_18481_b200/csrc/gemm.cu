@@ -121,6 +121,7 @@ struct GemmParams {
   unsigned long long* trace;  // debug: per-CTA %globaltimer stamps (kTraceSlots each) or null
   int tma_store;    // 1: bf16 epilogue writes each 128 x 32 chunk with one TMA store (StoreMaps)
   int halo_slot;    // MODE_CONV_HALO: bytes of one halo buffer (2 buffers precede the weight ring)
+  int b_resident;   // MODE_CONV_HALO: all 9 x cchunks weight tiles stay in smem for the CTA's lifetime
   int stage_bytes;  // epilogue staging bytes in shared memory
 };
 
@@ -283,6 +284,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------- TMA producer (halo + per-tap weights)
       int s = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
+      if (p.b_resident) {  // the whole weight matrix (one N tile) once, before the first halo
+        mbar_arrive_expect_tx(&full[0], 9 * p.cchunks * p.b_bytes);
+        for (int kb = 0; kb < 9 * p.cchunks; ++kb)
+          tma_load_2d(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK, 0);
+      }
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const TileIdx ti = decode_tile(p, t, n_tiles);
         const int th = ti.m % p.tiles_h;
@@ -291,6 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&aempty[hs], hphase ^ 1);
           mbar_arrive_expect_tx(&afull[hs], p.a_bytes);
           tma_load_4d(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
+          if (p.b_resident) {
+            if (++hs == 2) {
+              hs = 0;
+              hphase ^= 1;
+            }
+            continue;
+          }
           for (int tap = 0; tap < 9; ++tap) {
             mbar_wait(&empty[s], phase ^ 1);
             mbar_arrive_expect_tx(&full[s], p.b_bytes);
@@ -366,6 +379,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const int P = p.bw;
+    if (p.b_resident) {
+      mbar_wait(&full[0], 0);
+      tc_fence_after();
+    }
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -374,6 +391,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&afull[hs], hphase);
         tc_fence_after();
         const uint32_t halo = smem_addr(smA + hs * p.halo_slot);
+        if (p.b_resident) {  // 9 taps straight from the resident weights
+          if (lane == 0) {
+#pragma unroll 1
+            for (int tap = 0; tap < 9; ++tap) {
+              const int dy = tap / 3, dx = tap - 3 * (tap / 3);
+              const uint64_t adesc = umma_desc_sw128(halo + (uint32_t)((dy * P + dx) * 128));
+              const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + (tap * p.cchunks + cc) * p.b_bytes));
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+            }
+            umma_commit(&aempty[hs]);
+            if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++hs == 2) {
+            hs = 0;
+            hphase ^= 1;
+          }
+          continue;
+        }
         for (int tap = 0; tap < 9; ++tap) {
           mbar_wait(&full[s], phase);
           tc_fence_after();
@@ -558,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < p.N) dst[j] = activate(__uint_as_float(v[j]) + bch[j], ACT);
           }
         } else {  // EPI_TMA
+          if (p.debug_flags & 1) return;  // debug: accumulate only (no convert / store)
           int g = 0;
 #pragma unroll
           for (int gg = 1; gg < 4; ++gg)
@@ -1472,8 +1511,11 @@ int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in
   // + 2 rows: the last tap's shifted view of the last M rows reads past the halo
   p.halo_slot = ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
-  int stages = (226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes) / p.b_bytes;
-  if (stages > kMaxHaloStages) stages = kMaxHaloStages;  // weights-only stages are small: go deep
+  const int room = 226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes;
+  // one N tile whose 9 x cchunks weight blocks fit: keep them resident
+  p.b_resident = (p.N <= p.BN && 9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
+  int stages = p.b_resident ? 9 * p.cchunks : room / p.b_bytes;
+  if (!p.b_resident && stages > kMaxHaloStages) stages = kMaxHaloStages;  // weights-only stages are small
   if (stages < 2) return set_error(MS_ERR_INVALID, "halo conv: weights tile does not fit");
   p.stages = stages;
   Pl->smem_bytes = 1024 + 2 * p.halo_slot + stages * p.b_bytes + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;

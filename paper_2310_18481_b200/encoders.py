@@ -488,16 +488,22 @@ class BNInceptionEncoder:
                              K=cin, BN=pick_bn(nm), relu=True, segs=segs))
         tile_in = pick_conv_tile(n, h, h)
         tile_out = pick_conv_tile(n, o, o)
+
+        def halo_ok(cin_, cout_, stride_):
+            # halo + resident weights (one N tile, 9 x 64-ch blocks in smem):
+            # 1.36x the tap-box kernel at 28x28 (tools/halo_bench.py)
+            pitch = -(-(h + 2) // 8) * 8  # halo row width: must tile the 128-row M block
+            return stride_ == 1 and 14 < h <= 30 and 128 % pitch == 0 and cin_ <= 64 and cout_ <= 128
         # 3x3 branch (stride s) -> Y[:, c1 : c1+c3]
         B3 = dv.Program()
         B3.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
                              self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
-                             tile=tile_out))
+                             tile=tile_out, halo=halo_ok(c3r, c3, s)))
         # double 3x3: stride 1 then stride s -> Y[:, c1+c3 : c1+c3+cd]
         BD = dv.Program()
         BD.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
                              self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
-                             tile=tile_in))
+                             tile=tile_in, halo=halo_ok(cdr, cd, 1)))
         BD.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
                              self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
                              relu=True, tile=tile_out))
