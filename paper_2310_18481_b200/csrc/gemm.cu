@@ -284,10 +284,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------- TMA producer (halo + per-tap weights)
       int s = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
-      if (p.b_resident) {  // the whole weight matrix (one N tile) once, before the first halo
+      if (p.b_resident) {  // this CTA's N tile of weights once, before the first halo
+        // (grid is a multiple of n_tiles, so every tile t of this CTA has n = t % n_tiles fixed)
+        const int n_tile = (int)(blockIdx.x % n_tiles);
         mbar_arrive_expect_tx(&full[0], 9 * p.cchunks * p.b_bytes);
         for (int kb = 0; kb < 9 * p.cchunks; ++kb)
-          tma_load_2d(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK, 0);
+          tma_load_2d(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK, n_tile * p.BN);
       }
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const TileIdx ti = decode_tile(p, t, n_tiles);
@@ -1512,10 +1514,20 @@ int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in
   p.halo_slot = ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
   const int room = 226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes;
-  // one N tile whose 9 x cchunks weight blocks fit: keep them resident
-  p.b_resident = (p.N <= p.BN && 9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
+  // an N tile whose 9 x cchunks weight blocks fit stays resident; each CTA
+  // then serves one N tile (grid rounded to a multiple of the N tiles).
+  // Splitting N to make the weights fit measured slower (halo reloads per N
+  // tile + narrower MMAs; profiles/r01_halo_bench.txt): one N tile only.
+  const int n_tiles = (p.N + p.BN - 1) / p.BN;
+  p.b_resident = (n_tiles == 1 && 9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
   int stages = p.b_resident ? 9 * p.cchunks : room / p.b_bytes;
   if (!p.b_resident && stages > kMaxHaloStages) stages = kMaxHaloStages;  // weights-only stages are small
+  if (p.b_resident) {
+    const int tiles = p.m_tiles * n_tiles;
+    int g = tiles < sm_count() ? tiles : sm_count();
+    g = (g / n_tiles) * n_tiles;
+    Pl->grid_x = g < n_tiles ? n_tiles : g;
+  }
   if (stages < 2) return set_error(MS_ERR_INVALID, "halo conv: weights tile does not fit");
   p.stages = stages;
   Pl->smem_bytes = 1024 + 2 * p.halo_slot + stages * p.b_bytes + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;

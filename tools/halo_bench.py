@@ -49,13 +49,17 @@ for n, H, cin, cout in [(192, 28, 96, 96), (192, 28, 64, 96), (192, 28, 64, 64),
     BN = pick_bn(cout)
     p0 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, W, cout, b, D, ldd=cout, BN=BN,
                       tile=pick_conv_tile(n, H, H))
-    p1 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, W, cout, b, D, ldd=cout, BN=BN, halo=True)
+    # halo: the widest N tile whose 9 x cchunks weight blocks fit in smem (resident)
+    BNh = BN
+    while BNh > 32 and 9 * (cc // 64) * BNh * 128 > 150 * 1024:
+        BNh -= 32
+    p1 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, W, cout, b, D, ldd=cout, BN=BNh, halo=True)
     t0, t1 = timed(p0.run), timed(p1.run)
     dv.check(dv.lib().ms_gemm_plan_debug(p0.addr, 1), "dbg")
     dv.check(dv.lib().ms_gemm_plan_debug(p1.addr, 1), "dbg")
     t0n, t1n = timed(p0.run), timed(p1.run)
     fl = p0.flops
     print(f"n={n:3d} {H}x{H} {cin:3d}->{cout:3d}: tap-box{' pair' if getattr(p0, 'pair', False) else '     '} "
-          f"{t0:7.1f} us {fl / t0 / 1e6:6.0f} TF/s | halo {t1:7.1f} us {fl / t1 / 1e6:6.0f} TF/s  x{t0 / t1:.2f}"
+          f"{t0:7.1f} us {fl / t0 / 1e6:6.0f} TF/s | halo BN={BNh} {t1:7.1f} us {fl / t1 / 1e6:6.0f} TF/s  x{t0 / t1:.2f}"
           f" | no-epilogue: tap-box {t0n:6.1f} us halo {t1n:6.1f} us",
           flush=True)
