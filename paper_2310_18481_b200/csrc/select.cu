@@ -227,6 +227,44 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
         s_dline[threadIdx.x] = frame_h > 0 ? (ln / frame_h) * (frame_h + 2LL * pad_h) + pad_h + ln % frame_h : ln;
       }
       __syncthreads();
+      if constexpr (V == 4) {
+        if ((wd & 1) == 0 && gv == 1) {  // 4-channel pixels: two per thread, one 16-B store
+          const int wq = wd >> 1;
+          int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
+          const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
+          for (; li < nl; li += step_l, pq += step_p) {
+            if (pq >= wq) {
+              pq -= wq;
+              ++li;
+              if (li >= nl) break;
+            }
+            const unsigned char* lb = line_buf + li * line_bytes;
+            unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = 2 * pq + h - pad_w;
+              if (x >= 0 && x < width) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  if (c < c_src) {
+                    if (U8) {
+                      const __nv_bfloat16 b =
+                          __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+                      v[4 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
+                    } else {
+                      v[4 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+                    }
+                  }
+                }
+              }
+            }
+            *reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq)) =
+                make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
+                           v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+          }
+          continue;
+        }
+      }
       int li = threadIdx.x / wd, px = threadIdx.x - li * wd;  // (line, pixel), advanced without divisions
       const int step_l = blockDim.x / wd, step_p = blockDim.x - step_l * wd;
       for (; li < nl; li += step_l, px += step_p) {
