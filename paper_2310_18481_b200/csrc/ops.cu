@@ -135,7 +135,7 @@ __device__ __forceinline__ void pool_hrow_max2(const __nv_bfloat16* __restrict__
 // then every output (pixel, 8 channels) is summed from shared memory in fp32.
 // The register-streaming kernel spent most of its time waiting on dependent
 // row loads for these tiny rows.
-constexpr int kAvgSmem = 40 * 1024;
+constexpr int kAvgSmem = 48 * 1024;
 __global__ void __launch_bounds__(256) avgpool3_s1_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C,
                                                          long long xcs, int TH, __nv_bfloat16* __restrict__ Y,
                                                          long long ycs, int ycol0, const float* __restrict__ bias,
@@ -160,24 +160,48 @@ __global__ void __launch_bounds__(256) avgpool3_s1_kernel(const __nv_bfloat16* _
   }
   __syncthreads();
   const int oh1 = min(H, oh0 + TH);
+  // separable box sum: vertical 3-row sums of every staged column (fp32, in
+  // shared memory after the bf16 tile), then 3 horizontal neighbours per
+  // output -- 2.7x fewer instructions than 9 taps per output
+  float4* vsum = reinterpret_cast<float4*>(tile + rows * wp * cg);  // [TH][W+2][cg] x 8 floats (2 float4)
+  for (int i = threadIdx.x; i < (oh1 - oh0) * wp * cg; i += blockDim.x) {
+    const int g = i % cg;
+    const int xc = (i / cg) % wp;
+    const int r = i / (cg * wp);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      const uint4 v = tile[((r + dy) * wp + xc) * cg + g];
+      const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(e[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    vsum[2 * i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    vsum[2 * i + 1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < (oh1 - oh0) * W * cg; i += blockDim.x) {
     const int g = i % cg;
     const int x = (i / cg) % W;
     const int r = i / (cg * W);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const uint4 v = tile[((r + dy) * wp + x + dx) * cg + g];
-        const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(e[j]);
-          acc[2 * j] += f.x;
-          acc[2 * j + 1] += f.y;
-        }
-      }
+    for (int dx = 0; dx < 3; ++dx) {
+      const int vi = (r * wp + x + dx) * cg + g;
+      const float4 a = vsum[2 * vi], b = vsum[2 * vi + 1];
+      acc[0] += a.x;
+      acc[1] += a.y;
+      acc[2] += a.z;
+      acc[3] += a.w;
+      acc[4] += b.x;
+      acc[5] += b.y;
+      acc[6] += b.z;
+      acc[7] += b.w;
+    }
     uint32_t pk[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -523,14 +547,14 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const int OW = pool_out(a.W, a.k, a.stride, a.pad, a.ceil_mode);
   const int threads = (a.C / 8) * OW;
   if (!a.is_max && a.k == 3 && a.stride == 1 && a.pad == 1 && a.n_img <= 65535 &&
-      3 * (a.W + 2) * a.C * 2 <= kAvgSmem) {
+      5 * (a.W + 2) * a.C * 2 <= kAvgSmem) {
     // the fp32 sums of 9 taps: order per output (dy, dx) = the oracle's window order up to fp32 rounding
-    const int row_bytes = (a.W + 2) * a.C * 2;
-    int TH = kAvgSmem / row_bytes - 2;
+    const int row_bytes = (a.W + 2) * a.C * 2;  // bf16 staged row; its fp32 vertical sums take 2x
+    int TH = (kAvgSmem - 2 * row_bytes) / (3 * row_bytes);
     if (TH > a.H) TH = a.H;
     if (TH < 1) TH = 1;
     dim3 grid((a.H + TH - 1) / TH, a.n_img);
-    const size_t smem = (size_t)(TH + 2) * row_bytes;
+    const size_t smem = (size_t)(TH + 2) * row_bytes + (size_t)TH * row_bytes * 2;
     launch_k(avgpool3_s1_kernel, grid, dim3(256), smem, st, 1, reinterpret_cast<const __nv_bfloat16*>(a.X), a.H,
              a.W, a.C, a.xcs, TH, reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0, a.bias, a.relu);
     return check_launch("avgpool3_s1_kernel");
