@@ -87,3 +87,10 @@ for r in late[:40]:
               f"n {tr['n']} est {tr['est_us']} queue {tr['queue']}/{tr['queued_req']}")
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/serve_trace.json").write_text(json.dumps({"trace": st.trace, "late": out}))
+
+# mask composition of the served passes (for profiling a representative pass)
+comp = [t["counts"] for t in st.trace if "counts" in t]
+if comp:
+    c = np.array(comp)
+    print("per-pass modality counts (rgb, flow, audio): mean", np.round(c.mean(0), 1).tolist(),
+          "p50 n", float(np.median([t["n"] for t in st.trace])))
