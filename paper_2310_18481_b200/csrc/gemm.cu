@@ -45,8 +45,13 @@ constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int {
   MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5,
-  MODE_CONV_HALO = 6
+  MODE_CONV_HALO = 6, MODE_CONV_C12 = 7
 };
+// MODE_CONV_C12: the 10-channel flow stack stored as 12-channel pixels (row
+// and column padded like C4).  One filter row's window is 8 pixels x 12 ch =
+// 96 elements = three 32-element SW64 boxes; K blocks take the 21 halves
+// (row, part) two at a time (K 672 + 32 zero-weight, vs 896 for 16-channel
+// pixels), consecutive output columns 48 B apart.
 // MODE_CONV_HALO: 3x3 / stride 1 / pad 1 convolutions over images at least
 // 14 pixels wide.  The output tile is bh whole image rows of P pixels (P =
 // the image width + 2 rounded up to 8, so bh * P = 128).  Per 64-channel
@@ -218,7 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // n = t % n_tiles).  The smem ring (full/empty) and the two TMEM accumulator
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
-  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4 || MODE == MODE_CONV_HALO;
+  constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4 ||
+                          MODE == MODE_CONV_HALO || MODE == MODE_CONV_C12;
   if (threadIdx.x == 0) GEMM_TRACE(0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
@@ -363,6 +369,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int c2 = (ow0 + p.pad) / 2, r0 = oh0 + p.pad + 2 * kb;
             tma_load_4d(a_dst, &tmA, &full[s], 0, c2, r0, n0);
             tma_load_4d(a_dst + kABytes / 2, &tmA, &full[s], 0, c2, r0 + 1, n0);
+          } else if constexpr (MODE == MODE_CONV_C12) {
+            // halves h = 2kb, 2kb+1 of the (filter row, 32-element part) sequence;
+            // the one past the last (zero weights) re-reads a valid box
+            const int c2 = (ow0 + p.pad) / 2;
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+              const int h = min(2 * kb + l, p.smallc_halves - 1);
+              const int row = h / 3, part = h - 3 * (h / 3);
+              tma_load_4d(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, c2, oh0 + p.pad + row, n0);
+            }
           }
           tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
           if (t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(3);
@@ -463,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(4);
         if (lane == 0) {
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
-          if constexpr (MODE == MODE_CONV_C4) {  // two SW64 K halves of 32 (filter rows 2kb, 2kb+1)
+          if constexpr (MODE == MODE_CONV_C4 || MODE == MODE_CONV_C12) {  // two SW64 K halves of 32
             const uint32_t a0 = smem_addr(smA + s * kABytes);
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
@@ -712,6 +728,7 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
     case MODE_CONV_SMALLC: return pick_act<MODE_CONV_SMALLC, EPI_TMA>(p.relu);
     case MODE_CONV_C4: return pick_act<MODE_CONV_C4, EPI_TMA>(p.relu);
     case MODE_CONV_HALO: return pick_act<MODE_CONV_HALO, EPI_TMA>(p.relu);
+    case MODE_CONV_C12: return pick_act<MODE_CONV_C12, EPI_TMA>(p.relu);
     default: return nullptr;
   }
 }
@@ -1273,7 +1290,8 @@ static int encode_store_maps(GemmPlan* P) {
   GemmParams& p = P->p;
   p.tma_store = 0;
   if (p.out_fp32) return MS_OK;
-  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4 || p.mode == MODE_CONV_HALO;
+  const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4 ||
+                    p.mode == MODE_CONV_HALO || p.mode == MODE_CONV_C12;
   for (int g = 0; g < p.nseg; ++g) {
     const Seg& S = p.seg[g];
     const int w = S.n_end - S.n_begin;
@@ -1394,7 +1412,8 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   if (plan == nullptr || X == nullptr || Wt == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
   if (stride < 1 || stride > 2 || bn * bh * bw > kBM || bn < 1 || bh < 1 || bw < 1)
     return set_error(MS_ERR_INVALID, "bad conv tile / stride");
-  if ((c_stride * 2) % 16 != 0 && C != 4) return set_error(MS_ERR_INVALID, "channel stride*2 must be a multiple of 16");
+  if ((c_stride * 2) % 16 != 0 && C != 4 && C != 12)
+    return set_error(MS_ERR_INVALID, "channel stride*2 must be a multiple of 16");
   const int OH = (H + 2 * pad - KH) / stride + 1;
   const int OW = (W_in + 2 * pad - KW) / stride + 1;
   GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
@@ -1424,7 +1443,22 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
                            (cuuint64_t)c_stride * 2 * W_in * H};
   cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   int num_kb;
-  if (C == 4) {
+  if (C == 12) {
+    // X is [n_img, H + 2*pad, W_in + 2*pad, 12]: rows and columns pre-padded
+    if (stride != 2 || KW > 8 || KH > 8) return set_error(MS_ERR_INVALID, "12-channel conv needs stride 2, KH/KW <= 8");
+    p.mode = MODE_CONV_C12;
+    p.a_bytes = bn * bh * bw * 128;
+    p.smallc_halves = 3 * KH;            // 32-element parts of the filter-row windows
+    num_kb = (3 * KH + 1) / 2;
+    const long long wp = W_in + 2LL * pad, hp = H + 2LL * pad;
+    const long long pitch = wp * 12 * 2;
+    cuuint64_t d4[4] = {96, (cuuint64_t)OW, (cuuint64_t)hp, (cuuint64_t)n_img};
+    cuuint64_t s4[3] = {48, (cuuint64_t)pitch, (cuuint64_t)(pitch * hp)};
+    cuuint32_t b4[4] = {32, (cuuint32_t)bw, (cuuint32_t)(bh * 2), (cuuint32_t)bn};
+    cuuint32_t e4[4] = {1, 1, 2, 1};
+    int rc = encode_map(&P->tmA, 4, X, d4, s4, b4, e4, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  } else if (C == 4) {
     // X is [n_img, H + 2*pad, W_in + 2*pad, 4]: rows and columns pre-padded
     if (stride != 2 || KW > 8 || KH > 8) return set_error(MS_ERR_INVALID, "4-channel conv needs stride 2, KH/KW <= 8");
     p.mode = MODE_CONV_C4;

@@ -350,8 +350,8 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
                              cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f,
                              int frame_h = 0, int pad_h = 0) {
-  if ((c_dst % 8 != 0 && c_dst != 4) || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
-    return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 8 == 0 or c_dst == 4, pad_w >= 0");
+  if (c_dst % 4 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
+    return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 4 == 0, pad_w >= 0");
   if (frame_h < 0 || pad_h < 0 || (frame_h > 0 && lines % frame_h != 0))
     return set_error(MS_ERR_INVALID, "gather: frame_h must divide lines, pad_h >= 0");
   if (max_rows <= 0) return MS_OK;
@@ -364,7 +364,7 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     if (bx < 1) bx = 1;
     const dim3 grid((unsigned)bx, (unsigned)gy);
     const float sc = src_u8 ? u8_scale : 1.0f, bi = src_u8 ? u8_bias : 0.0f;
-    if (c_dst == 4) {
+    if (c_dst % 8 != 0) {  // 8-byte vector stores (4-channel groups)
       if (src_u8)
         gather_rows_pad_kernel<true, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
                                                               idx, count, dst, frame_h, pad_h);

@@ -69,14 +69,18 @@ class ModalitySpec:
     def cpad(self) -> int:
         """Stored channels of the first conv's input: 4 for <= 4 real channels
         (8-byte pixels: MODE_CONV_C4, one 128-B K block per filter-row pair),
-        else a multiple of 8 (16-B pixels, MODE_CONV_SMALLC)."""
-        return 4 if self.channels <= 4 else -(-self.channels // 8) * 8
+        12 for 5-12 (MODE_CONV_C12), else a multiple of 8 (MODE_CONV_SMALLC)."""
+        if self.channels <= 4:
+            return 4
+        if self.channels <= 12:
+            return 12  # 24-byte pixels: MODE_CONV_C12 (three 32-element parts per filter row)
+        return -(-self.channels // 8) * 8
 
     @property
     def row_pad(self) -> int:
         """Zero rows above/below each frame in the first conv's input
-        (MODE_CONV_C4 pads rows itself instead of TMA out-of-bounds fill)."""
-        return CONV1_PAD if self.cpad == 4 else 0
+        (MODE_CONV_C4/C12 pad rows themselves instead of TMA out-of-bounds fill)."""
+        return CONV1_PAD if self.cpad in (4, 12) else 0
 
     def frame_elems(self) -> int:
         return self.size * self.size * self.cpad
@@ -245,6 +249,20 @@ def pack_c4_weight(w):
     return wp.reshape(cout, nkb * 64).contiguous()
 
 
+def pack_c12_weight(w):
+    """[cout, cin <= 12, kh <= 8, kw <= 8] -> [cout, ceil(3*kh/2) * 64]: K =
+    (filter row, 8 window pixels x 12 channels = 96) rows back to back, zero
+    padded to whole 64-element blocks (MODE_CONV_C12's K order)."""
+    import torch
+    cout, cin, kh, kw = w.shape
+    nkb = -(-3 * kh // 2)
+    wp = torch.zeros(cout, kh, 8, 12, dtype=torch.bfloat16)
+    wp[:, :, :kw, :cin] = w.permute(0, 2, 3, 1)
+    out = torch.zeros(cout, nkb * 64, dtype=torch.bfloat16)
+    out[:, : kh * 96] = wp.reshape(cout, kh * 96)
+    return out.contiguous()
+
+
 def pack_im2col_weight(w, k_pad: int):
     """[cout, cin, k, k] -> [cout, k_pad] in im2col order (kh, kw, c)."""
     import torch
@@ -338,7 +356,8 @@ class BNInceptionEncoder:
         for name, (w, b) in W.items():
             if name == "conv1":
                 cp = self.mod.cpad
-                self.w[name] = (pack_c4_weight(w) if cp == 4 else pack_smallc_weight(w, cp)).to(d)
+                packer = {4: pack_c4_weight, 12: pack_c12_weight}.get(cp)
+                self.w[name] = (packer(w) if packer else pack_smallc_weight(w, cp)).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
             else:

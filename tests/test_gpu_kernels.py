@@ -452,6 +452,29 @@ def test_gather_four_channel_frames_with_row_padding(dev, c_src, u8, width):
     assert torch.all(dst[:, :, :pad_h] == 5.0) and torch.all(dst[:, :, pad_h + fh:] == 5.0)  # pad rows untouched
 
 
+@pytest.mark.parametrize("n,H,Cin,tile", [(2, 32, 10, (1, 8, 16)), (3, 224, 10, (1, 8, 16)), (2, 64, 12, (1, 4, 32))])
+def test_conv_twelve_channel_row_padded_vs_torch(dev, n, H, Cin, tile):
+    """7x7/2 first-layer conv over 12-channel row+column padded frames (flow:
+    MODE_CONV_C12, three 32-element SW64 parts per filter row)."""
+    from paper_2310_18481_b200.encoders import pack_c12_weight
+    g = torch.Generator().manual_seed(H + Cin + 17)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    X = torch.zeros(n, H + 6, H + 6, 12, dtype=torch.bfloat16)
+    X[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+    OH = (H + 6 - 7) // 2 + 1
+    D = torch.zeros(n * OH * OH, 64, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X.cuda(), n, H, H, 12, 12, 7, 7, 2, 3, pack_c12_weight(w).cuda(), 64,
+                      b.cuda(), D, ldd=64, BN=64, relu=True, tile=tile)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=2, padding=3).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, 64)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
+
+
 @pytest.mark.parametrize("n,H,Cin,tile", [(2, 32, 3, (1, 8, 16)), (2, 64, 1, (1, 4, 32)), (5, 224, 3, (1, 8, 16)),
                                           (3, 256, 1, (1, 8, 16))])
 def test_conv_four_channel_row_padded_vs_torch(dev, n, H, Cin, tile):
