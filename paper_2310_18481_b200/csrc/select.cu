@@ -228,6 +228,47 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
       }
       __syncthreads();
       if constexpr (V == 4) {
+        if ((wd & 1) == 0 && gv == 3) {  // 12-channel pixels: two per thread, three 16-B stores
+          const int wq = wd >> 1;
+          int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
+          const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
+          for (; li < nl; li += step_l, pq += step_p) {
+            if (pq >= wq) {
+              pq -= wq;
+              ++li;
+              if (li >= nl) break;
+            }
+            const unsigned char* lb = line_buf + li * line_bytes;
+            unsigned short v[24];
+#pragma unroll
+            for (int i = 0; i < 24; ++i) v[i] = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = 2 * pq + h - pad_w;
+              if (x >= 0 && x < width) {
+#pragma unroll
+                for (int c = 0; c < 12; ++c) {
+                  if (c < c_src) {
+                    if (U8) {
+                      const __nv_bfloat16 b =
+                          __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+                      v[12 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
+                    } else {
+                      v[12 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+                    }
+                  }
+                }
+              }
+            }
+            uint4* d4 = reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq) * 3);
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              d4[q] = make_uint4(v[8 * q] | ((unsigned)v[8 * q + 1] << 16), v[8 * q + 2] | ((unsigned)v[8 * q + 3] << 16),
+                                 v[8 * q + 4] | ((unsigned)v[8 * q + 5] << 16),
+                                 v[8 * q + 6] | ((unsigned)v[8 * q + 7] << 16));
+          }
+          continue;
+        }
         if ((wd & 1) == 0 && gv == 1) {  // 4-channel pixels: two per thread, one 16-B store
           const int wq = wd >> 1;
           int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
