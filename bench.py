@@ -233,7 +233,7 @@ def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
 
 
 # serving-loop options (set from the command line in main())
-SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.25}
+SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.2}
 
 
 def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
@@ -534,7 +534,7 @@ def main():
     ap.add_argument("--selection", default="pass", choices=["pass", "policy"],
                     help="pass: per-request accuracy argmax under the formed pass's deadline (batched P5); "
                          "policy: the reference OPTIMIZED policy on the queue")
-    ap.add_argument("--pass-frac", type=float, default=0.25,
+    ap.add_argument("--pass-frac", type=float, default=0.2,
                     help="pass-selection cap on a pass's estimated time, as a fraction of the deadline")
     ap.add_argument("--policy-grid-us", type=int, default=1000,
                     help="optimized policy knapsack quantum (reference: 1000)")
