@@ -157,6 +157,11 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
                       const MsSegment* segs, int bn, int bh, int bw);
 /* masked late-fusion concat GEMM: row i, K slice k*F..(k+1)*F reads
  * feat[k][inv[k*inv_ld + i]] or zeros when inv == -1. */
+/* 3x3 implicit-GEMM conv for input channels a multiple of 32 but not of 64:
+ * K = 9 * C exactly, weights [Cout, ceil64(9*C)] in (tap, channel) order. */
+int ms_gemm_plan_conv_k32(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride, int KH,
+                          int KW, int stride, int pad, const void* Wt, int Cout, int BN, const float* bias, int relu,
+                          void* D, long long ldd, int col0, int nseg, const MsSegment* segs, int bn, int bh, int bw);
 /* 3x3 / stride 1 / pad 1 implicit-GEMM conv with halo reuse (widths 14..62,
  * >= 64 input channels): one TMA box of (bh+2) input rows x ceil8(W+2)
  * pixels per 64-channel chunk, the 9 taps read as shifted views of it;

@@ -45,8 +45,12 @@ constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int {
   MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5,
-  MODE_CONV_HALO = 6, MODE_CONV_C12 = 7
+  MODE_CONV_HALO = 6, MODE_CONV_C12 = 7, MODE_CONV_K32 = 8
 };
+// MODE_CONV_K32: implicit-GEMM conv whose input channel count is a multiple
+// of 32 but not of 64 (96, 160, 224): K runs over (tap, 32-channel part)
+// halves, two per K block (SW64 boxes, like C4/C12), so K = 9 * Cin exactly
+// instead of 9 * ceil64(Cin) (25 % / 17 % / 12.5 % fewer MMAs).
 // MODE_CONV_C12: the 10-channel flow stack stored as 12-channel pixels (row
 // and column padded like C4).  One filter row's window is 8 pixels x 12 ch =
 // 96 elements = three 32-element SW64 boxes; K blocks take the 21 halves
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // buffers (tfull/tempty) carry their phases across tiles, so the TMA
   // producer prefetches the next tile while the epilogue drains this one.
   constexpr bool kConv = MODE == MODE_CONV || MODE == MODE_CONV_SMALLC || MODE == MODE_CONV_C4 ||
-                          MODE == MODE_CONV_HALO || MODE == MODE_CONV_C12;
+                          MODE == MODE_CONV_HALO || MODE == MODE_CONV_C12 || MODE == MODE_CONV_K32;
   if (threadIdx.x == 0) GEMM_TRACE(0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
@@ -379,6 +383,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int row = h / 3, part = h - 3 * (h / 3);
               tma_load_4d(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, c2, oh0 + p.pad + row, n0);
             }
+          } else if constexpr (MODE == MODE_CONV_K32) {
+            // halves (tap, 32-channel part), two per K block; past the end: a valid box (zero weights)
+            const int parts = p.cchunks;  // 32-channel parts per tap
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+              const int h = min(2 * kb + l, 9 * parts - 1);
+              const int tap = h / parts, part = h - tap * parts;
+              const int kh = tap / 3, kw = tap - 3 * (tap / 3);
+              tma_load_4d(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, ow0 + kw, oh0 + kh, n0);
+            }
           }
           tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
           if (t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(3);
@@ -479,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(4);
         if (lane == 0) {
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
-          if constexpr (MODE == MODE_CONV_C4 || MODE == MODE_CONV_C12) {  // two SW64 K halves of 32
+          if constexpr (MODE == MODE_CONV_C4 || MODE == MODE_CONV_C12 || MODE == MODE_CONV_K32) {  // 2 SW64 halves
             const uint32_t a0 = smem_addr(smA + s * kABytes);
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
@@ -729,6 +743,7 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
     case MODE_CONV_C4: return pick_act<MODE_CONV_C4, EPI_TMA>(p.relu);
     case MODE_CONV_HALO: return pick_act<MODE_CONV_HALO, EPI_TMA>(p.relu);
     case MODE_CONV_C12: return pick_act<MODE_CONV_C12, EPI_TMA>(p.relu);
+    case MODE_CONV_K32: return pick_act<MODE_CONV_K32, EPI_TMA>(p.relu);
     default: return nullptr;
   }
 }
@@ -1291,7 +1306,7 @@ static int encode_store_maps(GemmPlan* P) {
   p.tma_store = 0;
   if (p.out_fp32) return MS_OK;
   const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4 ||
-                    p.mode == MODE_CONV_HALO || p.mode == MODE_CONV_C12;
+                    p.mode == MODE_CONV_HALO || p.mode == MODE_CONV_C12 || p.mode == MODE_CONV_K32;
   for (int g = 0; g < p.nseg; ++g) {
     const Seg& S = p.seg[g];
     const int w = S.n_end - S.n_begin;
@@ -1518,6 +1533,40 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
   const int tiles_n = (n_img + bn - 1) / bn;
   if (int rc_store = encode_store_maps(P)) return rc_store;
   return finish_plan(P, Wt, num_kb * kBK, Cout, BN, num_kb, tiles_n * p.tiles_h * p.tiles_w);
+}
+
+int ms_gemm_plan_conv_k32(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride, int KH,
+                          int KW, int stride, int pad, const void* Wt, int Cout, int BN, const float* bias, int relu,
+                          void* D, long long ldd, int col0, int nseg, const MsSegment* segs, int bn, int bh, int bw) {
+  if (C % 32 != 0 || C % 64 == 0 || KH * KW != 9)
+    return set_error(MS_ERR_INVALID, "k32 conv: 3x3 with input channels a multiple of 32 but not of 64");
+  int rc = ms_gemm_plan_conv(plan, X, n_img, H, W_in, C, c_stride, KH, KW, stride, pad, Wt, Cout, BN, bias, relu, D,
+                             ldd, col0, nseg, segs, bn, bh, bw);
+  if (rc) return rc;
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  GemmParams& p = P->p;
+  if (p.mode != MODE_CONV) return set_error(MS_ERR_INVALID, "k32 conv: unexpected mode");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W_in, (cuuint64_t)H, (cuuint64_t)n_img};
+  cuuint64_t strides[3] = {(cuuint64_t)c_stride * 2, (cuuint64_t)c_stride * 2 * W_in,
+                           (cuuint64_t)c_stride * 2 * W_in * H};
+  cuuint32_t box[4] = {32, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  rc = encode_map(&P->tmA, 4, X, dims, strides, box, es, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  p.mode = MODE_CONV_K32;
+  p.cchunks = C / 32;  // 32-channel parts per tap
+  p.num_kb = (9 * p.cchunks + 1) / 2;
+  p.kb_per = p.num_kb;
+  // weights [Cout, num_kb * 64]: K = tap * C + c, zero padded to whole blocks
+  cuuint64_t wd[2] = {(cuuint64_t)(p.num_kb * kBK), (cuuint64_t)Cout};
+  cuuint64_t ws[1] = {(cuuint64_t)p.num_kb * kBK * 2};
+  cuuint32_t wb[2] = {(cuuint32_t)kBK, (cuuint32_t)p.BN};
+  cuuint32_t we[2] = {1, 1};
+  rc = encode_map(&P->tmB, 2, Wt, wd, ws, wb, we);
+  if (rc) return rc;
+  P->w_kpad = p.num_kb * kBK;
+  if (p.stages > p.num_kb) p.stages = p.num_kb < 2 ? 2 : p.num_kb;
+  return MS_OK;
 }
 
 int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,

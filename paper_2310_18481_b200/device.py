@@ -59,6 +59,8 @@ _SIGS = {
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
                            _I, _I, _P, _I, _I, _I], C.c_int),
+    "ms_gemm_plan_conv_k32": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
+                               _I, _I, _P, _I, _I, _I], C.c_int),
     "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
@@ -315,9 +317,25 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
 
 
 def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, bias, D, *, ldd,
-              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None, split_k=None, halo=False):
+              col0=0, BN=128, relu=True, segs=None, tile=(1, 8, 16), pair=None, split_k=None, halo=False,
+              k32=False):
     """Implicit-GEMM conv plan.  ``halo=True`` (3x3/1/1, width 14..62, >= 64
-    channels): one halo box per channel chunk, taps as shifted smem views."""
+    channels): one halo box per channel chunk, taps as shifted smem views.
+    ``k32=True`` (3x3, channels a multiple of 32 but not 64): K = 9*C exactly;
+    ``Wt`` then comes from ``encoders.pack_conv_weight_k32``."""
+    if k32:
+        p = GemmPlan()
+        nseg, sarr = _segments(segs)
+        bn, bh, bw = tile
+        check(lib().ms_gemm_plan_conv_k32(p.addr, ptr(X), n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad,
+                                          ptr(Wt), Cout, BN, ptr(bias), int(relu), ptr(D), ldd, col0, nseg, sarr,
+                                          bn, bh, bw), "ms_gemm_plan_conv_k32")
+        p.keep = [X, Wt, bias, D, segs]
+        oh = (H + 2 * pad - KH) // stride + 1
+        ow = (W_in + 2 * pad - KW) // stride + 1
+        p.flops = 2 * n_img * oh * ow * Cout * KH * KW * C_in
+        p.label = f"conv {KH}x{KW}/{stride} {C_in}->{Cout} {n_img}x{oh}x{ow} k32"
+        return p
     if halo:
         p = GemmPlan()
         nseg, sarr = _segments(segs)

@@ -226,6 +226,17 @@ def pack_conv_weight(w):
     return out.reshape(cout, k * k * cc).contiguous()
 
 
+def pack_conv_weight_k32(w):
+    """[cout, cin, k, k] -> [cout, ceil64(k*k*cin)] in (tap, channel) order
+    with no per-tap channel padding (MODE_CONV_K32's K order)."""
+    import torch
+    cout, cin, k, _ = w.shape
+    kk = k * k * cin
+    out = torch.zeros(cout, -(-kk // 64) * 64, dtype=torch.bfloat16)
+    out[:, :kk] = w.permute(0, 2, 3, 1).reshape(cout, kk)
+    return out.contiguous()
+
+
 def pack_smallc_weight(w, cpad: int):
     """[cout, cin, kh, kw] -> [cout, kh * 8 * cpad]: K ordered (kh, window
     pixel j < 8, channel) with channels zero-padded to ``cpad`` and taps
@@ -360,6 +371,10 @@ class BNInceptionEncoder:
                 self.w[name] = (packer(w) if packer else pack_smallc_weight(w, cp)).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
+            elif w.shape[1] % 64 and w.shape[1] % 32 == 0:
+                # 96/160/224 input channels: K = 9*C without per-tap padding
+                # (MODE_CONV_K32, 1.04-1.14x, profiles/r01_k32_bench.txt)
+                self.w[name] = pack_conv_weight_k32(w).to(d)
             else:
                 self.w[name] = pack_conv_weight(w).to(d)
             self.b[name] = b.to(d)
@@ -513,19 +528,22 @@ class BNInceptionEncoder:
             # 1.36x the tap-box kernel at 28x28 (tools/halo_bench.py)
             pitch = -(-(h + 2) // 8) * 8  # halo row width: must tile the 128-row M block
             return stride_ == 1 and 14 < h <= 30 and 128 % pitch == 0 and cin_ <= 64 and cout_ <= 128
+
+        def k32(cin_):  # matches the weight packing in _pack
+            return cin_ % 64 != 0 and cin_ % 32 == 0
         # 3x3 branch (stride s) -> Y[:, c1 : c1+c3]
         B3 = dv.Program()
         B3.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
                              self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
-                             tile=tile_out, halo=halo_ok(c3r, c3, s)))
+                             tile=tile_out, halo=halo_ok(c3r, c3, s), k32=k32(c3r)))
         # double 3x3: stride 1 then stride s -> Y[:, c1+c3 : c1+c3+cd]
         BD = dv.Program()
         BD.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
                              self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
-                             tile=tile_in, halo=halo_ok(cdr, cd, 1)))
+                             tile=tile_in, halo=halo_ok(cdr, cd, 1), k32=k32(cdr)))
         BD.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
                              self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
-                             relu=True, tile=tile_out))
+                             relu=True, tile=tile_out, k32=k32(cd)))
         pc = c1 + c3 + cd
         BP = dv.Program()
         if fold_pool:  # avgpool of the projected (pre-bias) branch + bias + ReLU

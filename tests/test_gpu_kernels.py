@@ -609,3 +609,26 @@ def test_conv_halo_vs_torch(dev, n, H, Cin, Cout, BN):
     ok, err, scale = _close(D[:, col0:col0 + Cout].cpu(), ref)
     assert ok, (err, scale)
     assert torch.all(D[:, :col0] == 3.0) and torch.all(D[:, col0 + Cout:] == 3.0)
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout,s,tile", [(3, 28, 96, 96, 1, (1, 4, 28)), (2, 28, 96, 96, 2, (1, 8, 14)),
+                                                 (2, 14, 160, 224, 1, (1, 7, 14)), (2, 7, 224, 224, 1, (2, 7, 7))])
+def test_conv_k32_vs_torch(dev, n, H, Cin, Cout, s, tile):
+    """3x3 conv with K over (tap, 32-channel part) halves (MODE_CONV_K32): no
+    per-tap channel padding for 96/160/224 input channels."""
+    from paper_2310_18481_b200.encoders import pack_conv_weight_k32, pick_bn
+    g = torch.Generator().manual_seed(n * H + Cin + 23)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(Cout, Cin, 3, 3, generator=g) * (2.0 / (Cin * 9)) ** 0.5)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    OH = (H + 2 - 3) // s + 1
+    D = torch.zeros(n * OH * OH, Cout, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, 3, 3, s, 1, pack_conv_weight_k32(w).cuda(), Cout, b.cuda(), D,
+                      ldd=Cout, BN=pick_bn(Cout), relu=True, tile=tile, k32=True)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=s, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D.cpu(), ref)
+    assert ok, (err, scale)
