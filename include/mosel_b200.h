@@ -169,6 +169,16 @@ int ms_gemm_plan_conv_k32(void* plan, const void* X, int n_img, int H, int W_in,
 int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
                            const void* Wt, int Cout, int BN, const float* bias, int relu, void* D, long long ldd,
                            int col0, int nseg, const MsSegment* segs);
+/* Fused stem: 7x7 (KH <= 8) / stride-2 conv over pre-padded 4-channel pixels
+ * X [n_img, H + 2*pad, W + 2*pad, 4] bf16 (output width <= 128), 64 output
+ * channels, + bias + ReLU, then the 3x3 / stride-2 / ceil-mode max pool, in
+ * ONE kernel: Y = pooled [n_img, PH, PW] rows of ldy elements at y_col0.  The
+ * input rows are the A operand as they lie (no-swizzle K-major descriptors
+ * with overlapping core matrices); each input row feeds both conv rows of a
+ * pair through N = 128 MMAs.  Wt: 9 x [128, 32] bf16 row-pair weights in the
+ * no-swizzle core-matrix order (encoders.pack_stem_weight), 16-B aligned. */
+int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, const void* Wt,
+                           const float* bias, void* Y, long long ldy, int y_col0);
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                         int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
                         int out_fp32, void* D, long long ldd, int col0);
@@ -195,6 +205,8 @@ int ms_gemm_plan_debug(void* plan, int flags);
 int ms_gemm_plan_set_trace(void* plan, unsigned long long* buf);
 /* Debug probe of shifted K-major SW128 UMMA operand descriptors (tools/umma_probe.py). */
 int ms_debug_umma_shift(const void* A, const void* W, float* D, int shift, int sbo, int use_base, void* stream);
+/* debug: clocks for `count` back-to-back M=128 K=16 MMAs of width n with A layout `mode` (tools/umma_rate.py) */
+int ms_debug_umma_rate(int mode, int n, int count, long long* cycles, void* stream);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
 
 /* ---- HBM-bound ops (NHWC bf16) ---------------------------------------- */

@@ -24,6 +24,7 @@
 // The epilogue routes 32-column chunks to up to 4 destination segments so
 // merged 1x1 branch GEMMs write straight into Inception concat slices.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "mosel_b200.h"
@@ -45,7 +46,7 @@ constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int {
   MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5,
-  MODE_CONV_HALO = 6, MODE_CONV_C12 = 7, MODE_CONV_K32 = 8
+  MODE_CONV_HALO = 6, MODE_CONV_C12 = 7, MODE_CONV_K32 = 8, MODE_STEM_POOL = 9
 };
 // MODE_CONV_K32: implicit-GEMM conv whose input channel count is a multiple
 // of 32 but not of 64 (96, 160, 224): K runs over (tap, 32-channel part)
@@ -131,7 +132,13 @@ struct GemmParams {
   int tma_store;    // 1: bf16 epilogue writes each 128 x 32 chunk with one TMA store (StoreMaps)
   int halo_slot;    // MODE_CONV_HALO: bytes of one halo buffer (2 buffers precede the weight ring)
   int b_resident;   // MODE_CONV_HALO: all 9 x cchunks weight tiles stay in smem for the CTA's lifetime
+  int warp_store;   // EPI_TMA: each epilogue warp stores its own 32 rows (no cross-warp barrier)
   int stage_bytes;  // epilogue staging bytes in shared memory
+  // MODE_STEM_POOL: raw pre-padded 4-channel input rows, fused 3x3/2 max pool
+  const uint8_t* xraw;
+  const uint8_t* wraw;  // MODE_STEM_POOL: row-pair weights (encoders.pack_stem_weight)
+  long long x_pitch;   // bytes of one padded input row
+  int Hp, PH, PW, units;
 };
 
 // One bf16 output tensor map per epilogue segment (TMA stores, SWIZZLE_64B):
@@ -651,6 +658,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (tr0) GEMM_TRACE(9);
+          if (p.warp_store) {
+            // this warp's 32 rows x 32 columns: own 2 KB slice, own TMA store,
+            // no barrier with the other warps of the group
+            if (lane == 0) bulk_wait_read0();  // my previous store has read my slice
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(srow + ((j ^ sw) << 4)) =
+                  make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int c0 = nb - p.seg[g].n_begin;
+              const uint32_t src = smem_addr(sbuf + q * 32 * 64);
+              if constexpr (kConv) {
+                const int tw = m_tile % p.tiles_w;
+                const int th = (m_tile / p.tiles_w) % p.tiles_h;
+                const int tn = m_tile / (p.tiles_w * p.tiles_h);
+                const int r0 = q * 32;
+                if (r0 < p.bh * p.bw) {
+                  const int x = tw * p.bw + (p.bw >= 32 ? r0 % p.bw : 0);
+                  const int y = th * p.bh + r0 / p.bw;
+                  tma_store_4d(&tmD.m[g], src, c0, x, y, tn * p.bn);
+                }
+              } else {
+                tma_store_2d(&tmD.m[g], src, c0, m_tile * kBM + q * 32);
+              }
+              bulk_commit();
+            }
+            return;
+          }
           if (issuer) bulk_wait_read0();  // the previous chunk's store has read the buffer
           named_bar_sync(1 + grp, 128);
 #pragma unroll
@@ -699,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (EPI == EPI_TMA && issuer) bulk_wait0();
+    if (EPI == EPI_TMA && (issuer || (p.warp_store && lane == 0))) bulk_wait0();
     if (warp == 2 && lane == 0) GEMM_TRACE(7);
   }
   __syncthreads();
@@ -1159,6 +1197,328 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------------
+// MODE_STEM_POOL: the 7x7/2 first convolution over 4-channel pixels (rgb 3 ->
+// 4, audio 1 -> 4) FUSED with the 3x3/2 ceil-mode max pool that follows it.
+// The unpooled conv output (4x the pooled bytes) never reaches HBM.
+//
+// A operand straight from the raw input rows: output pixel ow's window in a
+// padded input row starts at byte 16*ow (stride 2 x 4 ch x 2 B) and is 32
+// contiguous bf16 (8 pixels x 4 ch).  That is exactly the K-major
+// SWIZZLE_NONE UMMA layout with 8-row x 16-B core matrices, LBO (K step
+// between core matrices) = 16 B and SBO (8-row group step) = 128 B: core
+// matrices overlap in memory, which the tensor core does not mind.  A conv
+// row is 14 MMAs (M = 128 >= OW output pixels, N = 64, K = 16) on shifted
+// descriptors into the rows brought in by ONE bulk copy -- no im2col, no
+// overlapping TMA boxes.  Weights (64 x 256, K = (kh, 8 px, 4 ch), the C4
+// packing) stay resident.
+//
+// Work: a CTA owns a contiguous range of pooled rows (image, i).  Pooled row i
+// takes conv rows 2i..2i+2 and consecutive pooled rows share conv row 2i+2,
+// so the CTA's walk is one tile per pooled row: CLOSE(i) = conv rows 2i+1 and
+// 2i+2 (two accumulators of one 128-column TMEM slot, input rows 4i+2..4i+10
+// in one bulk copy), preceded by OPEN(i) = conv row 2i where a run starts
+// (the range's first row or an image's first row).  One producer / MMA /
+// epilogue handshake per tile, not per conv row: the per-handshake barrier
+// latency of the three single-threaded roles, not the MMAs, bounded the
+// one-row-per-handshake version (measured: 122 us skeleton-bound).  The
+// epilogue converts (bias, bf16), max-pools horizontally and keeps the
+// vertical max in registers; ReLU is applied once to the pooled value (it
+// commutes with max, as does the bf16 rounding: result == pool(bf16(relu(conv)))).
+//
+// kOverlap (output width <= 112): the A descriptor's 8-row-group stride is 7
+// pixels (SBO 112 B) instead of 8, so consecutive row groups share one pixel
+// and each warp's 32 TMEM lanes hold 29 consecutive conv pixels 28q..28q+28 --
+// exactly the support of its 14 pooled pixels 14q..14q+13.  The horizontal
+// pool is then two warp shuffles per register: no shared-memory row, no
+// barrier between epilogue warps.  (M = 128 rows still buy 113 distinct
+// pixels, as many as 112 linear rows.)  Otherwise (audio, 128 wide) the
+// converted rows go through a swizzled shared-memory row buffer.
+constexpr int kStemSlots = 4;              // TMEM slots of 128 columns (two conv rows)
+constexpr int kStemKH = 7;                 // 7x7 filters (plan-checked)
+constexpr int kStemMaxRows = 9;            // input rows of a CLOSE tile
+constexpr int kStemWRow = 128 * 32 * 2;      // one input row's [W_j ; W_(j-2)]: 128 n x 32 k
+constexpr int kStemWBytes = kStemMaxRows * kStemWRow;
+constexpr int kStemRowBuf = 128 * 128;     // <= 128 conv pixels x 64 ch bf16
+constexpr int kStemEpiWarps = 16;          // 4 per TMEM lane quarter, 16 channels each
+constexpr int kStemCh = 64 / (kStemEpiWarps / 4);
+constexpr int kStemThreads = 64 + 32 * kStemEpiWarps;
+
+__device__ __forceinline__ uint32_t bf16x2_max(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint4 bf16x8_max(uint4 a, uint4 b) {
+  return make_uint4(bf16x2_max(a.x, b.x), bf16x2_max(a.y, b.y), bf16x2_max(a.z, b.z), bf16x2_max(a.w, b.w));
+}
+
+// The CTA's tile walk: units u0..u1-1, an OPEN tile before a unit that starts a
+// run.  Tile = (img, i, open); conv rows: OPEN -> {2i}; CLOSE -> {2i+1, 2i+2 < OH}.
+struct StemWalk {
+  int u, u1, PH, OH, img, i;
+  bool open;
+  __device__ __forceinline__ void begin(int u0_, int u1_, int PH_, int OH_) {
+    u1 = u1_; PH = PH_; OH = OH_; u = u0_;
+    img = u / PH;  // the only division: later units step (img, i) incrementally
+    i = u - img * PH;
+    open = true;   // a run starts: conv row 2i is not carried over
+  }
+  __device__ __forceinline__ bool valid() const { return u < u1; }
+  __device__ __forceinline__ void next() {
+    if (open) { open = false; return; }  // OPEN(i) -> CLOSE(i)
+    ++u;
+    if (++i == PH) {
+      i = 0;
+      ++img;
+      open = true;  // a new image starts a run
+    }
+  }
+  __device__ __forceinline__ int row0() const { return open ? 2 * i : 2 * i + 1; }
+  __device__ __forceinline__ int nrows() const { return open ? 1 : (2 * i + 2 < OH ? 2 : 1); }
+};
+
+template <bool kOverlap>
+__global__ void __launch_bounds__(kStemThreads, 1)
+    stem_pool_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  const int stages = p.stages;
+  const int a_stride = p.b_bytes;  // bytes per stage (9 padded input rows, 128-B rounded)
+  uint8_t* smW = smem;
+  uint8_t* smA = smW + kStemWBytes;
+  uint8_t* rbuf = smA + stages * a_stride + 256;  // + slack: rows >= OW of the last tap read past a stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + (kOverlap ? 0 : kStemRowBuf));
+  uint64_t* empty = full + stages;
+  uint64_t* wbar = empty + stages;
+  uint64_t* tfull = wbar + 1;
+  uint64_t* tempty = tfull + kStemSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kStemSlots);
+  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int OH = p.OH, OW = p.OW, PH = p.PH, PW = p.PW;
+  const int u0 = (int)((long long)p.units * blockIdx.x / gridDim.x);
+  const int u1 = (int)((long long)p.units * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(wbar, 1);
+    for (int s = 0; s < kStemSlots; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kStemEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x < 64) sbias[threadIdx.x] = p.bias ? p.bias[threadIdx.x] : 0.0f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
+  if (warp == 0 && lane == 0) {  // weights are constants: load them before waiting on the producer grid
+    mbar_arrive_expect_tx(wbar, kStemWBytes);
+    for (int j = 0; j < kStemMaxRows; ++j)
+      bulk_load(smem_addr(smW + j * kStemWRow), p.wraw + j * kStemWRow, kStemWRow, wbar);
+  }
+  pdl_wait();
+
+  StemWalk w;
+  w.begin(u0, u1, PH, OH);
+  // debug: CTA 0's first 32 tiles, stamps (MMA ready, MMA issued, epilogue ready, epilogue done)
+  auto trace = [&](int k, int slot_) {
+    if (p.trace != nullptr && blockIdx.x == 0 && k < 32) p.trace[k * 8 + slot_] = gtimer();
+  };
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------- producer
+      int s = 0, kp = 0;
+      uint32_t phase = 0;
+      for (; w.valid(); w.next(), ++kp) {
+        // conv rows row0 .. row0+n-1 read padded input rows 2*row0 .. 2*(row0+n-1)+6
+        const uint32_t bytes = (uint32_t)((2 * w.nrows() + 5) * p.x_pitch);
+        mbar_wait(&empty[s], phase ^ 1);
+        trace(kp, 4);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_load(smem_addr(smA + s * a_stride), p.xraw + ((long long)w.img * p.Hp + 2 * w.row0()) * p.x_pitch,
+                  bytes, &full[s]);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------ MMA issuer
+    const uint32_t idesc = umma_idesc_bf16_m128(128);
+    // descriptors built once: per (input row j, K half h) only the start-address
+    // field moves (+(j - j0)*pitch + 32h bytes for A, +j*8 KB + 256h for B)
+    const uint64_t a_desc0 = umma_desc_interleave(smem_addr(smA), 16, kOverlap ? 112 : 128);
+    const uint64_t b_desc0 = umma_desc_interleave(smem_addr(smW), 128, 512);
+    const uint32_t pitch16 = (uint32_t)(p.x_pitch >> 4), stage16 = (uint32_t)(a_stride >> 4);
+    mbar_wait(wbar, 0);
+    tc_fence_after();
+    int s = 0, k = 0;
+    uint32_t phase = 0;
+    for (; w.valid(); w.next(), ++k) {
+      const int slot = k & (kStemSlots - 1);
+      const int n = w.nrows();
+      mbar_wait(&tempty[slot], (uint32_t)(((k / kStemSlots) & 1) ^ 1));
+      mbar_wait(&full[s], phase);
+      tc_fence_after();
+      if (lane == 0) trace(k, 0);
+      {
+        // the conv-row pair (r, r+1): OPEN = (2i-1, 2i) needs input rows j = 2..8
+        // only, CLOSE = (2i+1, 2i+2) rows 0..8 (0..6 when 2i+2 is past the map).
+        // Warp-uniform issue (elect.sync inside each instruction): the issuing
+        // warp shares its scheduler with busy epilogue warps, so every
+        // instruction on this path costs.
+        const uint64_t ad = a_desc0 + (uint64_t)(s * stage16);
+        const uint32_t d = tmem_base + (uint32_t)(slot * 128);
+        const int j0 = w.open ? 2 : 0, j1 = j0 + 2 * n + 4;
+        const uint32_t a_lo = (uint32_t)ad, a_hi = (uint32_t)(ad >> 32);
+        const uint32_t b_lo = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
+        for (int j = j0; j <= j1; ++j)
+          umma_bf16_x2_elect(d, a_lo + (uint32_t)(j - j0) * pitch16, a_hi, b_lo + (uint32_t)j * (kStemWRow / 16), b_hi,
+                             16, idesc, j != j0);
+        umma_commit_elect(&empty[s]);
+        umma_commit_elect(&tfull[slot]);
+        if (lane == 0) trace(k, 1);
+      }
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  } else if constexpr (kOverlap) {  // ------------- epilogue warps 2..17 (overlapping row groups)
+    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, 16-channel chunk
+    const int x = 7 * (lane >> 3) + (lane & 7);   // this lane's conv pixel within the warp's 29
+    auto lane_of = [](int y) { return y < 28 ? (y / 7) * 8 + y % 7 : 31; };
+    const int src1 = lane_of(min(x + 1, 28)), src2 = lane_of(min(x + 2, 28));
+    const int jj = x >> 1;                          // pooled pixel (local) when this lane owns one
+    const bool owner = (lane & 7) < 7 && (x & 1) == 0 && x <= 26 && 14 * q + jj < PW;
+    const bool three = 28 * q + x + 2 < OW;         // ceil mode: the last window may be 2 wide
+    const Seg& Y = p.seg[0];
+    const uint32_t t_lane = tmem_base + (uint32_t)(c * kStemCh) + ((uint32_t)(q * 32) << 16);
+    const float* bch = sbias + c * kStemCh;
+    uint32_t carry[kStemCh / 2];  // conv row 2i of the open pooled row, bf16(acc + bias), per pixel
+    for (int k = 0; w.valid(); w.next(), ++k) {
+      const int slot = k & (kStemSlots - 1);
+      const int n = w.nrows();
+      mbar_wait(&tfull[slot], (uint32_t)((k / kStemSlots) & 1));
+      tc_fence_after();
+      if (warp == 2 && lane == 0) trace(k, 2);
+      uint32_t v0[kStemCh], v1[kStemCh];
+      // OPEN: row 2i is the pair's second row (columns 64..127)
+      tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
+      if (n == 2) tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + 64), v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[slot]);
+      if (w.open) {  // conv row 2i opens pooled row i
+#pragma unroll
+        for (int e = 0; e < kStemCh / 2; ++e)
+          carry[e] = pack_bf16x2(__uint_as_float(v0[2 * e]) + bch[2 * e], __uint_as_float(v0[2 * e + 1]) + bch[2 * e + 1]);
+        continue;
+      }
+      // CLOSE: vertical max of rows 2i, 2i+1 (, 2i+2) per pixel, then the
+      // horizontal 3-max across lanes; row 2i+2 opens pooled row i+1
+      __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(Y.ptr) +
+                         (((long long)w.img * PH + w.i) * PW + 14 * q + jj) * Y.ldd + Y.col0 + c * kStemCh;
+#pragma unroll
+      for (int g = 0; g < kStemCh / 8; ++g) {
+        uint32_t o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int e = 4 * g + t;
+          uint32_t m = bf16x2_max(carry[e], pack_bf16x2(__uint_as_float(v0[2 * e]) + bch[2 * e],
+                                                        __uint_as_float(v0[2 * e + 1]) + bch[2 * e + 1]));
+          if (n == 2) {
+            const uint32_t r2 = pack_bf16x2(__uint_as_float(v1[2 * e]) + bch[2 * e],
+                                            __uint_as_float(v1[2 * e + 1]) + bch[2 * e + 1]);
+            m = bf16x2_max(m, r2);
+            carry[e] = r2;
+          }
+          const uint32_t m1 = __shfl_sync(0xffffffffu, m, src1);
+          const uint32_t m2 = __shfl_sync(0xffffffffu, m, src2);
+          uint32_t h = bf16x2_max(m, m1);
+          if (three) h = bf16x2_max(h, m2);
+          o[t] = bf16x2_max(h, 0u);  // ReLU
+        }
+        if (owner) *reinterpret_cast<uint4*>(y + 8 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      if (warp == 2 && lane == 0) trace(k, 3);
+    }
+  } else {  // ----------------------------- epilogue warps 2..17 (linear rows, smem horizontal pool)
+    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, 16-channel chunk
+    const int ow = q * 32 + lane;
+    const int tid = threadIdx.x - 64;             // 0..511
+    const int n_items = PW * 8;                   // pooled pixels x 8 16-B channel groups
+    const Seg& Y = p.seg[0];
+    const uint32_t t_lane = tmem_base + (uint32_t)(c * kStemCh) + ((uint32_t)(q * 32) << 16);
+    const float* bch = sbias + c * kStemCh;
+    uint32_t carry[kStemCh / 2];
+    for (int k = 0; w.valid(); w.next(), ++k) {
+      const int slot = k & (kStemSlots - 1);
+      const int n = w.nrows();
+      mbar_wait(&tfull[slot], (uint32_t)((k / kStemSlots) & 1));
+      tc_fence_after();
+      uint32_t v0[kStemCh], v1[kStemCh];
+      // OPEN: row 2i is the pair's second row (columns 64..127)
+      tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
+      if (n == 2) tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + 64), v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[slot]);
+      if (w.open) {
+#pragma unroll
+        for (int e = 0; e < kStemCh / 2; ++e)
+          carry[e] = pack_bf16x2(__uint_as_float(v0[2 * e]) + bch[2 * e], __uint_as_float(v0[2 * e + 1]) + bch[2 * e + 1]);
+        continue;
+      }
+      // vertical max per pixel -> the row buffer (swizzled 16-B groups)
+      uint32_t m[kStemCh / 2];
+#pragma unroll
+      for (int e = 0; e < kStemCh / 2; ++e) {
+        m[e] = bf16x2_max(carry[e], pack_bf16x2(__uint_as_float(v0[2 * e]) + bch[2 * e],
+                                                __uint_as_float(v0[2 * e + 1]) + bch[2 * e + 1]));
+        if (n == 2) {
+          const uint32_t r2 = pack_bf16x2(__uint_as_float(v1[2 * e]) + bch[2 * e],
+                                          __uint_as_float(v1[2 * e + 1]) + bch[2 * e + 1]);
+          m[e] = bf16x2_max(m[e], r2);
+          carry[e] = r2;
+        }
+      }
+      if (ow < OW) {
+        uint8_t* row = rbuf + ow * 128;
+#pragma unroll
+        for (int t = 0; t < kStemCh / 8; ++t)
+          *reinterpret_cast<uint4*>(row + ((((c * (kStemCh / 8) + t) ^ (ow & 7))) << 4)) =
+              make_uint4(m[4 * t], m[4 * t + 1], m[4 * t + 2], m[4 * t + 3]);
+      }
+      named_bar_sync(1, 32 * kStemEpiWarps);
+      __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(Y.ptr) + ((long long)w.img * PH + w.i) * PW * Y.ldd + Y.col0;
+      for (int it = tid; it < n_items; it += 32 * kStemEpiWarps) {
+        const int j = it >> 3, g = it & 7;
+        const int x0 = 2 * j;
+        const uint8_t* b0 = rbuf + x0 * 128;
+        uint4 h = bf16x8_max(*reinterpret_cast<const uint4*>(b0 + ((g ^ (x0 & 7)) << 4)),
+                             *reinterpret_cast<const uint4*>(b0 + 128 + ((g ^ ((x0 + 1) & 7)) << 4)));
+        if (x0 + 2 < OW) h = bf16x8_max(h, *reinterpret_cast<const uint4*>(b0 + 256 + ((g ^ ((x0 + 2) & 7)) << 4)));
+        *reinterpret_cast<uint4*>(yrow + (long long)j * Y.ldd + 8 * g) = bf16x8_max(h, make_uint4(0, 0, 0, 0));
+      }
+      named_bar_sync(1, 32 * kStemEpiWarps);  // rbuf is rewritten by the next CLOSE tile
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
 // split-K finalize: D = act(sum_k ws[k] + bias) (+ residual), bf16 or fp32,
 // one thread per 4 columns; the K-part slabs are added in part order, so the
 // result is bitwise reproducible (no atomics, no workspace zeroing).
@@ -1307,6 +1667,17 @@ static int encode_store_maps(GemmPlan* P) {
   if (p.out_fp32) return MS_OK;
   const bool conv = p.mode == MODE_CONV || p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV_C4 ||
                     p.mode == MODE_CONV_HALO || p.mode == MODE_CONV_C12 || p.mode == MODE_CONV_K32;
+  // per-warp stores (each epilogue warp stores its own 32 rows, no group
+  // barrier) for dense / gather rows.  Conv tiles keep one 128-row box per
+  // group: per-warp 4-D boxes measured slower there (halo 3x3 at 56^2:
+  // 135 vs 129 us; tools/op_times.py with MS_NO_WARP_STORE=1 as the A/B).
+  // The conv coordinates of the per-warp path are kept for the A/B.
+  static const bool no_warp_store = getenv("MS_NO_WARP_STORE") != nullptr;
+  static const bool conv_warp_store = getenv("MS_CONV_WARP_STORE") != nullptr;
+  p.warp_store = (!no_warp_store && (!conv || (conv_warp_store && p.bn == 1 && (p.bw % 32 == 0 || 32 % p.bw == 0) &&
+                                               (p.bh * p.bw) % 32 == 0)))
+                     ? 1
+                     : 0;
   for (int g = 0; g < p.nseg; ++g) {
     const Seg& S = p.seg[g];
     const int w = S.n_end - S.n_begin;
@@ -1319,11 +1690,15 @@ static int encode_store_maps(GemmPlan* P) {
       cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)p.OW, (cuuint64_t)p.OH, (cuuint64_t)p.n_img};
       cuuint64_t st[3] = {(cuuint64_t)S.ldd * 2, (cuuint64_t)S.ldd * 2 * p.OW, (cuuint64_t)S.ldd * 2 * p.OW * p.OH};
       cuuint32_t box[4] = {32, (cuuint32_t)p.bw, (cuuint32_t)p.bh, (cuuint32_t)p.bn};
+      if (p.warp_store) {
+        box[1] = (cuuint32_t)(p.bw >= 32 ? 32 : p.bw);
+        box[2] = (cuuint32_t)(p.bw >= 32 ? 1 : 32 / p.bw);
+      }
       rc = encode_map(&P->tmD.m[g], 4, base, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_64B);
     } else {
       cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)p.M};
       cuuint64_t st[1] = {(cuuint64_t)S.ldd * 2};
-      cuuint32_t box[2] = {32, (cuuint32_t)kBM};
+      cuuint32_t box[2] = {32, (cuuint32_t)(p.warp_store ? 32 : kBM)};
       rc = encode_map(&P->tmD.m[g], 2, base, dims, st, box, es, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     if (rc) return rc;
@@ -1353,6 +1728,19 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
     }
     launch_k(conv1_rows_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p);
     return check_launch("conv1_rows_kernel");
+  }
+  if (p.mode == MODE_STEM_POOL) {
+    static int stem_attr = 0;
+    if (!stem_attr) {
+      cudaFuncSetAttribute(stem_pool_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(stem_pool_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      stem_attr = 1;
+    }
+    if (p.OW <= 112)
+      launch_k(stem_pool_kernel<true>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
+    else
+      launch_k(stem_pool_kernel<false>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
+    return check_launch("stem_pool_kernel");
   }
   if (p.pair) {
     static int pair_attr = 0;
@@ -1721,6 +2109,66 @@ int ms_gemm_plan_debug(void* plan, int flags) {
   return MS_OK;
 }
 
+// 7x7/2 conv over pre-padded 4-channel pixels + bias + ReLU + 3x3/2 ceil-mode
+// max pool in one kernel (MODE_STEM_POOL).  X: [n_img, H + 2*pad, W + 2*pad, 4]
+// bf16; Wt: [64, 256] bf16 in the C4 packing (K = (kh, 8 px, 4 ch)); Y: pooled
+// [n_img, PH, PW] rows of ldy elements, 64 channels at y_col0.
+int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, const void* Wt,
+                           const float* bias, void* Y, long long ldy, int y_col0) {
+  if (plan == nullptr || X == nullptr || Wt == nullptr || Y == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
+  if (KH != kStemKH || n_img < 1) return set_error(MS_ERR_INVALID, "stem conv needs a 7x7 filter, n_img >= 1");
+  const int OH = (H + 2 * pad - KH) / 2 + 1, OW = (W_in + 2 * pad - KH) / 2 + 1;
+  if (OW > kBM || OH < 3 || OW < 3) return set_error(MS_ERR_INVALID, "stem conv needs 3 <= output width <= 128");
+  if (H + 2 * pad < 2 * OH + 5)  // the last conv row's 7 input rows lie inside the padded frame
+    return set_error(MS_ERR_INVALID, "stem conv: padded frame too short");
+  const long long pitch = (long long)(W_in + 2 * pad) * 4 * 2;
+  if (pitch % 16 != 0) return set_error(MS_ERR_INVALID, "padded stem row must be a multiple of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(X) & 15) != 0 || (reinterpret_cast<uintptr_t>(Y) & 15) != 0 || (ldy % 8) != 0 ||
+      (y_col0 % 8) != 0)
+    return set_error(MS_ERR_INVALID, "stem input and output rows must be 16-B aligned");
+  // ceil-mode 3x3/2 pool without padding: the last window starts inside the map
+  const int PH = (OH - 3 + 1) / 2 + 1, PW = (OW - 3 + 1) / 2 + 1;
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  memset(P, 0, sizeof(GemmPlan));
+  GemmParams& p = P->p;
+  p.mode = MODE_STEM_POOL;
+  p.N = 64;
+  p.BN = 64;
+  p.bias = bias;
+  p.relu = MS_ACT_RELU;
+  p.n_img = n_img;
+  p.OH = OH;
+  p.OW = OW;
+  p.stride = 2;
+  p.pad = pad;
+  p.KW = KH;
+  p.M = n_img * OH * OW;
+  p.xraw = reinterpret_cast<const uint8_t*>(X);
+  p.x_pitch = pitch;
+  p.Hp = H + 2 * pad;
+  p.PH = PH;
+  p.PW = PW;
+  p.units = n_img * PH;
+  p.a_bytes = (int)(kStemMaxRows * pitch);       // a CLOSE tile's input rows
+  p.b_bytes = (p.a_bytes + 127) / 128 * 128;     // stage stride
+  p.nseg = 1;
+  p.seg[0] = Seg{0, 64, Y, ldy, y_col0, 0};
+  if ((reinterpret_cast<uintptr_t>(Wt) & 15) != 0) return set_error(MS_ERR_INVALID, "stem weights must be 16-B aligned");
+  p.wraw = reinterpret_cast<const uint8_t*>(Wt);
+  P->w_ptr = Wt;
+  const bool overlap = OW <= 112;
+  const int fixed = 1024 + kStemWBytes + 256 + (overlap ? 0 : kStemRowBuf) + 1024;
+  int stages = (226 * 1024 - fixed) / p.b_bytes;
+  if (stages > 8) stages = 8;
+  if (stages < 2) return set_error(MS_ERR_INVALID, "stem rows too wide for shared memory");
+  p.stages = stages;
+  P->smem_bytes = fixed + stages * p.b_bytes;
+  P->grid_x = p.units < sm_count() ? p.units : sm_count();
+  P->grid_y = 1;
+  P->tmem_cols = 512;
+  return MS_OK;
+}
+
 int ms_gemm_run(const void* plan, void* stream) {
   if (plan == nullptr) return set_error(MS_ERR_INVALID, "null plan");
   return launch_plan(reinterpret_cast<const GemmPlan*>(plan), reinterpret_cast<cudaStream_t>(stream));
@@ -1817,4 +2265,55 @@ extern "C" int ms_debug_umma_shift(const void* A /* [256, 64] bf16 */, const voi
   umma_shift_probe_kernel<<<1, 128, 50 * 1024, reinterpret_cast<cudaStream_t>(stream)>>>(ta, tb, D, shift, sbo,
                                                                                            use_base);
   return check_launch("umma_shift_probe_kernel");
+}
+
+// ------------------------------------------------------------------------
+// Debug probe (tools/umma_rate.py): issue rate of back-to-back
+// tcgen05.mma (M=128, K=16) from one thread into one accumulator, for an A
+// descriptor of layout `mode` (0 = SW128 K-major, 1 = no-swizzle LBO 16 /
+// SBO 128, 2 = no-swizzle LBO 16 / SBO 112, 3 = no-swizzle LBO 128 / SBO 256
+// canonical) and width n.  Operands are uninitialised shared memory: only the
+// timing is meaningful.  cycles[0] = clocks from the first issue to the
+// commit's completion.
+namespace mosel {
+__global__ void __launch_bounds__(128, 1) umma_rate_kernel(int mode, int n, int count, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_addr(smem), b0 = smem_addr(smem + 64 * 1024);
+    uint64_t ad;
+    if (mode == 0) ad = umma_desc_sw128(a0);
+    else if (mode == 1) ad = umma_desc_interleave(a0, 16, 128);
+    else if (mode == 2) ad = umma_desc_interleave(a0, 16, 112);
+    else ad = umma_desc_interleave(a0, 128, 256);
+    const uint64_t bd = umma_desc_sw128(b0);
+    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)n);
+    const long long t0 = clock64();
+    for (int i = 0; i < count; ++i) umma_bf16(tb, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i != 0);
+    umma_commit(&mbar);
+    mbar_wait(&mbar, 0);
+    cycles[0] = clock64() - t0;
+  }
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tb, 256);
+}
+}  // namespace mosel
+
+extern "C" int ms_debug_umma_rate(int mode, int n, int count, long long* cycles, void* stream) {
+  using namespace mosel;
+  cudaFuncSetAttribute(umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  umma_rate_kernel<<<1, 128, 150 * 1024, reinterpret_cast<cudaStream_t>(stream)>>>(mode, n, count, cycles);
+  return check_launch("umma_rate_kernel");
 }

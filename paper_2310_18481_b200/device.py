@@ -62,6 +62,7 @@ _SIGS = {
     "ms_gemm_plan_conv_k32": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
                                _I, _I, _P, _I, _I, _I], C.c_int),
     "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
+    "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -87,6 +88,7 @@ _SIGS = {
     "ms_gemm_plan_debug": ([_P, _I], C.c_int),
     "ms_gemm_plan_set_trace": ([_P, _P], C.c_int),
     "ms_debug_umma_shift": ([_P, _P, _P, _I, _I, _I, _P], C.c_int),
+    "ms_debug_umma_rate": ([_I, _I, _I, _P, _P], C.c_int),
     "ms_gemm_plan_set_pair": ([_P, _I], C.c_int),
     "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
     "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),
@@ -378,6 +380,20 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
         else:
             bn_, bh_, bw_ = tile
             _auto_pair(p, conv_tiles, BN, True)
+    return p
+
+
+def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0):
+    """Fused 7x7/2 conv (4-channel pre-padded pixels, 64 out, ReLU) + 3x3/2
+    ceil max pool (``ms_gemm_plan_stem_pool``); ``Wt`` is the C4 packing."""
+    p = GemmPlan()
+    check(lib().ms_gemm_plan_stem_pool(p.addr, ptr(X), n_img, H, W_in, KH, pad, ptr(Wt), ptr(bias), ptr(Y), ldy,
+                                       col0), "ms_gemm_plan_stem_pool")
+    p.keep = [X, Wt, bias, Y]
+    oh = (H + 2 * pad - KH) // 2 + 1
+    ow = (W_in + 2 * pad - KH) // 2 + 1
+    p.flops = 2 * n_img * oh * ow * 64 * KH * KH * 4
+    p.label = f"stem conv {KH}x{KH}/2 4->64 {n_img}x{oh}x{ow} + maxpool"
     return p
 
 

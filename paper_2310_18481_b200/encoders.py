@@ -28,6 +28,8 @@ generators so the oracle rebuilds them bit-identically.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -260,6 +262,26 @@ def pack_c4_weight(w):
     return wp.reshape(cout, nkb * 64).contiguous()
 
 
+def pack_stem_weight(w):
+    """[64, cin <= 4, 7, 7] -> the fused stem's row-pair weights (MODE_STEM_POOL):
+    for each of the 9 input rows j of a conv-row pair (r, r+1), B_j = [W_j ;
+    W_(j-2)] (128 x 32: output channels of row r, then of row r+1; W_kh =
+    filter row kh as 8 window pixels x 4 channels, zero outside 0..6), stored
+    in the no-swizzle UMMA core-matrix order (8 n x 8 k blocks of 128 B; K
+    step 128 B, N step 512 B), 9 x 8 KB."""
+    import torch
+    cout, cin, kh, kw = w.shape
+    assert cout == 64 and kh == 7 and kw <= 8 and cin <= 4
+    wk = torch.zeros(9, 64, 8, 4, dtype=torch.float32)       # filter rows, padded to 9 (7, 8 zero)
+    wk[:kh, :, :kw, :cin] = w.float().permute(2, 0, 3, 1)
+    wk = wk.reshape(9, 64, 32)
+    b = torch.zeros(9, 128, 32, dtype=torch.float32)
+    b[:, :64] = wk                                            # row r: W_j
+    b[2:, 64:] = wk[:7]                                       # row r+1: W_(j-2)
+    b = b.reshape(9, 16, 8, 4, 8).permute(0, 1, 3, 2, 4)     # (j, n/8, k/8, n%8, k%8)
+    return b.reshape(-1).to(torch.bfloat16).contiguous()
+
+
 def pack_c12_weight(w):
     """[cout, cin <= 12, kh <= 8, kw <= 8] -> [cout, ceil(3*kh/2) * 64]: K =
     (filter row, 8 window pixels x 12 channels = 96) rows back to back, zero
@@ -356,6 +378,8 @@ class BNInceptionEncoder:
         self._alloc()
         self._programs = {}
         self._lanes = None  # side streams for the Inception branch lanes
+        # conv1 + pool1 as one kernel for 4-channel frames (MS_NO_FUSED_STEM=1: A/B)
+        self.fused_stem = os.environ.get("MS_NO_FUSED_STEM") is None
 
     # -- weights on device
     def _pack(self):
@@ -369,6 +393,8 @@ class BNInceptionEncoder:
                 cp = self.mod.cpad
                 packer = {4: pack_c4_weight, 12: pack_c12_weight}.get(cp)
                 self.w[name] = (packer(w) if packer else pack_smallc_weight(w, cp)).to(d)
+                if cp == 4:
+                    self.w["stem"] = pack_stem_weight(w).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
             elif w.shape[1] % 64 and w.shape[1] % 32 == 0:
@@ -458,11 +484,18 @@ class BNInceptionEncoder:
         # stem: the few-channel 7x7/2 conv reads the frames directly with TMA
         # (channels padded to 8 in memory; no im2col round trip)
         cp = self.mod.cpad
-        P.gemm(dv.plan_conv(self.x, n, size, size, cp, cp, 7, 7, 2, 3, self.w["conv1"], 64,
-                            self.b["conv1"], self.a_c1, ldd=64, BN=64, relu=True,
-                            tile=pick_conv_tile(n, h1, h1)))
         h2 = pool_out(h1, 3, 2, 0, True)
-        P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
+        if cp == 4 and h1 <= 128 and self.fused_stem:
+            # 4-channel frames: conv1 + bias + ReLU + pool1 in one kernel that
+            # feeds the raw padded input rows to the tensor cores (csrc/gemm.cu
+            # MODE_STEM_POOL); the unpooled map never reaches HBM
+            P.gemm(dv.plan_stem_pool(self.x, n, size, size, 7, 3, self.w["stem"], self.b["conv1"], self.a_p1,
+                                     ldy=64))
+        else:
+            P.gemm(dv.plan_conv(self.x, n, size, size, cp, cp, 7, 7, 2, 3, self.w["conv1"], 64,
+                                self.b["conv1"], self.a_c1, ldd=64, BN=64, relu=True,
+                                tile=pick_conv_tile(n, h1, h1)))
+            P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
         P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
                              M=n * h2 * h2, K=64, BN=64, relu=True))
         # conv2 (56x56 rgb/flow): halo reuse measured 1.08-1.09x faster than the

@@ -499,6 +499,39 @@ def test_conv_four_channel_row_padded_vs_torch(dev, n, H, Cin, tile):
     assert ok, (err, scale)
 
 
+@pytest.mark.parametrize("n,H,Cin", [(2, 32, 3), (2, 64, 1), (3, 30, 3), (5, 224, 3), (3, 256, 1), (1, 224, 3)])
+def test_stem_conv_pool_fused_vs_unfused_and_torch(dev, n, H, Cin):
+    """MODE_STEM_POOL: 7x7/2 conv (raw padded rows as no-swizzle UMMA
+    operands) + ReLU + 3x3/2 ceil max pool in one kernel == the C4 conv
+    kernel followed by the pool, and == torch within bf16 tolerance."""
+    from paper_2310_18481_b200.encoders import pack_c4_weight, pack_stem_weight
+    g = torch.Generator().manual_seed(H + Cin + 11)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    X = torch.zeros(n, H + 6, H + 6, 4, dtype=torch.bfloat16)
+    X[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+    Xd, Wd, bd = X.cuda(), pack_c4_weight(w).cuda(), b.cuda()
+    OH = (H + 6 - 7) // 2 + 1
+    PH = -(-(OH - 3) // 2) + 1
+    Y = torch.full((n * PH * PH, 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    dev.plan_stem_pool(Xd, n, H, H, 7, 3, pack_stem_weight(w).cuda(), bd, Y, ldy=64).run()
+    D = torch.zeros(n * OH * OH, 64, dtype=torch.bfloat16, device="cuda")
+    dev.plan_conv(Xd, n, H, H, 4, 4, 7, 7, 2, 3, Wd, 64, bd, D, ldd=64, BN=64, relu=True, tile=(1, 8, 16)).run()
+    torch.cuda.synchronize()
+    pooled = torch.nn.functional.max_pool2d(D.float().reshape(n, OH, OH, 64).permute(0, 3, 1, 2), 3, 2,
+                                            ceil_mode=True)
+    pooled = pooled.permute(0, 2, 3, 1).reshape(-1, 64)
+    assert torch.isfinite(Y.float()).all()
+    # same bf16 conv values, max is exact: allow one bf16 ulp for accumulation order
+    diff = (Y.float().cpu() - pooled.cpu()).abs()
+    assert float((diff > pooled.cpu().abs() * 2 ** -7 + 1e-6).float().mean()) == 0.0, float(diff.max())
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=2, padding=3).clamp_min(0)
+    ref = torch.nn.functional.max_pool2d(ref, 3, 2, ceil_mode=True).permute(0, 2, 3, 1).reshape(-1, 64)
+    ok, err, scale = _close(Y.cpu(), ref)
+    assert ok, (err, scale)
+
+
 @pytest.mark.parametrize("M,K,N,BN", [(1000, 1024, 256, 256), (300, 192, 96, 96), (128, 64, 64, 64), (517, 576, 352, 192)])
 def test_gemm_cta_pair_dense_vs_torch(dev, M, K, N, BN):
     """2-CTA clusters (tcgen05.mma.cta_group::2, M=256 tiles)."""
