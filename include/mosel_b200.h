@@ -125,6 +125,8 @@ typedef struct MsRowDesc {
   float u8_scale, u8_bias; /* bf16 value = u8 * scale + bias */
   int frame_h, pad_h;      /* frames of frame_h lines get pad_h zero rows above/below (0: none) */
   int slot_off;            /* this modality's request->pool-row map is slot[slot_off + request] */
+  long long plane_stride;  /* > 0 (c_dst == 12 only): write three 4-channel planes, plane q at
+                              G + q * plane_stride elements (the fused stem's input layout) */
 } MsRowDesc;
 int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                        const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows,
@@ -176,9 +178,13 @@ int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in
  * input rows are the A operand as they lie (no-swizzle K-major descriptors
  * with overlapping core matrices); each input row feeds both conv rows of a
  * pair through N = 128 MMAs.  Wt: 9 x [128, 32] bf16 row-pair weights in the
- * no-swizzle core-matrix order (encoders.pack_stem_weight), 16-B aligned. */
-int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, const void* Wt,
-                           const float* bias, void* Y, long long ldy, int y_col0);
+ * no-swizzle core-matrix order (encoders.pack_stem_weight), 16-B aligned.
+ * planes = 3 (flow, up to 12 channels): X holds three 4-channel planes
+ * plane_stride elements apart (ms_compact's planar gather), N = 64 MMAs per
+ * (conv row, filter row, plane), Wt = encoders.pack_stem_weight_planes. */
+int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, int planes,
+                           long long plane_stride, const void* Wt, const float* bias, void* Y, long long ldy,
+                           int y_col0);
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                         int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
                         int out_fp32, void* D, long long ldd, int col0);

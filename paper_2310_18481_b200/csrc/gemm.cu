@@ -137,6 +137,8 @@ struct GemmParams {
   // MODE_STEM_POOL: raw pre-padded 4-channel input rows, fused 3x3/2 max pool
   const uint8_t* xraw;
   const uint8_t* wraw;  // MODE_STEM_POOL: row-pair weights (encoders.pack_stem_weight)
+  long long x_plane;    // MODE_STEM_POOL with planes: bytes between 4-channel input planes
+  int planes, plane_bytes;
   long long x_pitch;   // bytes of one padded input row
   int Hp, PH, PW, units;
 };
@@ -1239,6 +1241,7 @@ constexpr int kStemKH = 7;                 // 7x7 filters (plan-checked)
 constexpr int kStemMaxRows = 9;            // input rows of a CLOSE tile
 constexpr int kStemWRow = 128 * 32 * 2;      // one input row's [W_j ; W_(j-2)]: 128 n x 32 k
 constexpr int kStemWBytes = kStemMaxRows * kStemWRow;
+constexpr int kStemWBlk = 64 * 32 * 2;      // planes variant: one (filter row, plane) 64 n x 32 k block
 constexpr int kStemRowBuf = 128 * 128;     // <= 128 conv pixels x 64 ch bf16
 constexpr int kStemEpiWarps = 16;          // 4 per TMEM lane quarter, 16 channels each
 constexpr int kStemCh = 64 / (kStemEpiWarps / 4);
@@ -1277,7 +1280,7 @@ struct StemWalk {
   __device__ __forceinline__ int nrows() const { return open ? 1 : (2 * i + 2 < OH ? 2 : 1); }
 };
 
-template <bool kOverlap>
+template <bool kOverlap, int kPlanes>
 __global__ void __launch_bounds__(kStemThreads, 1)
     stem_pool_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1285,7 +1288,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   const int stages = p.stages;
   const int a_stride = p.b_bytes;  // bytes per stage (9 padded input rows, 128-B rounded)
   uint8_t* smW = smem;
-  uint8_t* smA = smW + kStemWBytes;
+  constexpr int kWBytes = kPlanes == 1 ? kStemWBytes : kStemKH * kPlanes * kStemWBlk;
+  uint8_t* smA = smW + kWBytes;
   uint8_t* rbuf = smA + stages * a_stride + 256;  // + slack: rows >= OW of the last tap read past a stage
   uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + (kOverlap ? 0 : kStemRowBuf));
   uint64_t* empty = full + stages;
@@ -1319,9 +1323,9 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
   if (warp == 0 && lane == 0) {  // weights are constants: load them before waiting on the producer grid
-    mbar_arrive_expect_tx(wbar, kStemWBytes);
-    for (int j = 0; j < kStemMaxRows; ++j)
-      bulk_load(smem_addr(smW + j * kStemWRow), p.wraw + j * kStemWRow, kStemWRow, wbar);
+    mbar_arrive_expect_tx(wbar, kWBytes);
+    for (int o = 0; o < kWBytes; o += 8192)
+      bulk_load(smem_addr(smW + o), p.wraw + o, min(8192, kWBytes - o), wbar);
   }
   pdl_wait();
 
@@ -1340,9 +1344,11 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         const uint32_t bytes = (uint32_t)((2 * w.nrows() + 5) * p.x_pitch);
         mbar_wait(&empty[s], phase ^ 1);
         trace(kp, 4);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_load(smem_addr(smA + s * a_stride), p.xraw + ((long long)w.img * p.Hp + 2 * w.row0()) * p.x_pitch,
-                  bytes, &full[s]);
+        mbar_arrive_expect_tx(&full[s], bytes * kPlanes);
+        const uint8_t* src = p.xraw + ((long long)w.img * p.Hp + 2 * w.row0()) * p.x_pitch;
+#pragma unroll
+        for (int pl = 0; pl < kPlanes; ++pl)
+          bulk_load(smem_addr(smA + s * a_stride + pl * p.plane_bytes), src + pl * p.x_plane, bytes, &full[s]);
         if (++s == stages) {
           s = 0;
           phase ^= 1;
@@ -1350,7 +1356,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
     }
   } else if (warp == 1) {  // ------------------------------------ MMA issuer
-    const uint32_t idesc = umma_idesc_bf16_m128(128);
+    const uint32_t idesc = umma_idesc_bf16_m128(kPlanes == 1 ? 128 : 64);
     // descriptors built once: per (input row j, K half h) only the start-address
     // field moves (+(j - j0)*pitch + 32h bytes for A, +j*8 KB + 256h for B)
     const uint64_t a_desc0 = umma_desc_interleave(smem_addr(smA), 16, kOverlap ? 112 : 128);
@@ -1378,9 +1384,25 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         const int j0 = w.open ? 2 : 0, j1 = j0 + 2 * n + 4;
         const uint32_t a_lo = (uint32_t)ad, a_hi = (uint32_t)(ad >> 32);
         const uint32_t b_lo = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
-        for (int j = j0; j <= j1; ++j)
-          umma_bf16_x2_elect(d, a_lo + (uint32_t)(j - j0) * pitch16, a_hi, b_lo + (uint32_t)j * (kStemWRow / 16), b_hi,
-                             16, idesc, j != j0);
+        if constexpr (kPlanes == 1) {
+          for (int j = j0; j <= j1; ++j)
+            umma_bf16_x2_elect(d, a_lo + (uint32_t)(j - j0) * pitch16, a_hi, b_lo + (uint32_t)j * (kStemWRow / 16),
+                               b_hi, 16, idesc, j != j0);
+        } else {
+          // channel planes: per conv row, N = 64 MMAs over (filter row, plane);
+          // weights W[kh][plane] 64 x 32 blocks (encoders.pack_stem_weight_planes)
+          const uint32_t plane16 = (uint32_t)(p.plane_bytes >> 4);
+          for (int dr = 0; dr < n; ++dr) {
+            const uint32_t dd = d + (uint32_t)(w.open ? 64 : 64 * dr);
+            const uint32_t ar = a_lo + (uint32_t)(2 * dr) * pitch16;
+            for (int kh = 0; kh < kStemKH; ++kh)
+#pragma unroll
+              for (int pl = 0; pl < kPlanes; ++pl)
+                umma_bf16_x2_elect(dd, ar + (uint32_t)kh * pitch16 + (uint32_t)pl * plane16, a_hi,
+                                   b_lo + (uint32_t)((kh * kPlanes + pl) * (kStemWBlk / 16)), b_hi, 16, idesc,
+                                   (kh | pl) != 0);
+          }
+        }
         umma_commit_elect(&empty[s]);
         umma_commit_elect(&tfull[slot]);
         if (lane == 0) trace(k, 1);
@@ -1732,14 +1754,17 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
   if (p.mode == MODE_STEM_POOL) {
     static int stem_attr = 0;
     if (!stem_attr) {
-      cudaFuncSetAttribute(stem_pool_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(stem_pool_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(stem_pool_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(stem_pool_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(stem_pool_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       stem_attr = 1;
     }
-    if (p.OW <= 112)
-      launch_k(stem_pool_kernel<true>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
+    if (p.planes == 3)
+      launch_k(stem_pool_kernel<true, 3>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
+    else if (p.OW <= 112)
+      launch_k(stem_pool_kernel<true, 1>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
     else
-      launch_k(stem_pool_kernel<false>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
+      launch_k(stem_pool_kernel<false, 1>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
     return check_launch("stem_pool_kernel");
   }
   if (p.pair) {
@@ -2113,8 +2138,9 @@ int ms_gemm_plan_debug(void* plan, int flags) {
 // max pool in one kernel (MODE_STEM_POOL).  X: [n_img, H + 2*pad, W + 2*pad, 4]
 // bf16; Wt: [64, 256] bf16 in the C4 packing (K = (kh, 8 px, 4 ch)); Y: pooled
 // [n_img, PH, PW] rows of ldy elements, 64 channels at y_col0.
-int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, const void* Wt,
-                           const float* bias, void* Y, long long ldy, int y_col0) {
+int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, int planes,
+                           long long plane_stride, const void* Wt, const float* bias, void* Y, long long ldy,
+                           int y_col0) {
   if (plan == nullptr || X == nullptr || Wt == nullptr || Y == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
   if (KH != kStemKH || n_img < 1) return set_error(MS_ERR_INVALID, "stem conv needs a 7x7 filter, n_img >= 1");
   const int OH = (H + 2 * pad - KH) / 2 + 1, OW = (W_in + 2 * pad - KH) / 2 + 1;
@@ -2149,15 +2175,22 @@ int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in
   p.PH = PH;
   p.PW = PW;
   p.units = n_img * PH;
-  p.a_bytes = (int)(kStemMaxRows * pitch);       // a CLOSE tile's input rows
-  p.b_bytes = (p.a_bytes + 127) / 128 * 128;     // stage stride
+  if (planes != 1 && planes != 3) return set_error(MS_ERR_INVALID, "stem conv: planes must be 1 or 3");
+  if (planes == 3 && (OW > 112 || plane_stride <= 0 || (plane_stride * 2) % 16 != 0))
+    return set_error(MS_ERR_INVALID, "stem conv: 3 planes need output width <= 112 and a 16-B plane stride");
+  p.planes = planes;
+  p.x_plane = plane_stride * 2;
+  p.a_bytes = (int)(kStemMaxRows * pitch);       // a CLOSE tile's input rows (per plane)
+  p.plane_bytes = (p.a_bytes + 127) / 128 * 128;
+  p.b_bytes = planes * p.plane_bytes;            // stage stride
   p.nseg = 1;
   p.seg[0] = Seg{0, 64, Y, ldy, y_col0, 0};
   if ((reinterpret_cast<uintptr_t>(Wt) & 15) != 0) return set_error(MS_ERR_INVALID, "stem weights must be 16-B aligned");
   p.wraw = reinterpret_cast<const uint8_t*>(Wt);
   P->w_ptr = Wt;
   const bool overlap = OW <= 112;
-  const int fixed = 1024 + kStemWBytes + 256 + (overlap ? 0 : kStemRowBuf) + 1024;
+  const int w_bytes = planes == 1 ? kStemWBytes : kStemKH * planes * kStemWBlk;
+  const int fixed = 1024 + w_bytes + 256 + (overlap ? 0 : kStemRowBuf) + 1024;
   int stages = (226 * 1024 - fixed) / p.b_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) return set_error(MS_ERR_INVALID, "stem rows too wide for shared memory");

@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
                                                               const int32_t* __restrict__ slot,
                                                               const int32_t* __restrict__ idx,
                                                               const int32_t* __restrict__ count,
-                                                              void* __restrict__ dst_v, int frame_h, int pad_h) {
+                                                              void* __restrict__ dst_v, int frame_h, int pad_h,
+                                                              long long plane_vecs) {
   typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
   __shared__ long long s_dline[32];
@@ -259,6 +260,16 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
                   }
                 }
               }
+            }
+            if (plane_vecs > 0) {  // planar: channels 4q..4q+3 of both pixels -> plane q
+              const long long pix = ((long long)j * dst_lines + s_dline[li]) * wd + 2 * pq;
+#pragma unroll
+              for (int q = 0; q < 3; ++q)
+                *reinterpret_cast<uint4*>(dst + q * plane_vecs + pix) =
+                    make_uint4(v[4 * q] | ((unsigned)v[4 * q + 1] << 16), v[4 * q + 2] | ((unsigned)v[4 * q + 3] << 16),
+                               v[12 + 4 * q] | ((unsigned)v[12 + 4 * q + 1] << 16),
+                               v[12 + 4 * q + 2] | ((unsigned)v[12 + 4 * q + 3] << 16));
+              continue;
             }
             uint4* d4 = reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq) * 3);
 #pragma unroll
@@ -390,7 +401,7 @@ __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, lo
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
                              cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f,
-                             int frame_h = 0, int pad_h = 0) {
+                             int frame_h = 0, int pad_h = 0, long long plane_stride = 0) {
   if (c_dst % 4 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
     return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 4 == 0, pad_w >= 0");
   if (frame_h < 0 || pad_h < 0 || (frame_h > 0 && lines % frame_h != 0))
@@ -398,6 +409,9 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
   if (max_rows <= 0) return MS_OK;
   const int gy = max_rows < 65535 ? max_rows : 65535;
   const long long line_bytes = (long long)width * c_src * (src_u8 ? 1 : 2);
+  if (plane_stride > 0 && (c_dst != 12 || ((width + 2 * pad_w) & 1) != 0 || line_bytes % 16 != 0 ||
+                           line_bytes > kMaxLineBytes || plane_stride % 4 != 0))
+    return set_error(MS_ERR_INVALID, "gather: planar output needs 12 destination channels, even padded width");
   if (line_bytes % 16 == 0 && line_bytes <= kMaxLineBytes) {
     const long long per = line_bytes > 0 ? (kMaxLineBytes / line_bytes < 32 ? kMaxLineBytes / line_bytes : 32) : 1;
     long long bx = (lines + per - 1) / per;
@@ -408,16 +422,16 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     if (c_dst % 8 != 0) {  // 8-byte vector stores (4-channel groups)
       if (src_u8)
         gather_rows_pad_kernel<true, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                              idx, count, dst, frame_h, pad_h);
+                                                              idx, count, dst, frame_h, pad_h, plane_stride / 4);
       else
         gather_rows_pad_kernel<false, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                               idx, count, dst, frame_h, pad_h);
+                                                               idx, count, dst, frame_h, pad_h, plane_stride / 4);
     } else if (src_u8) {
       gather_rows_pad_kernel<true, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                            idx, count, dst, frame_h, pad_h);
+                                                            idx, count, dst, frame_h, pad_h, plane_stride / 4);
     } else {
       gather_rows_pad_kernel<false, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                             idx, count, dst, frame_h, pad_h);
+                                                             idx, count, dst, frame_h, pad_h, plane_stride / 4);
     }
   } else {
     if (c_dst % 8 != 0 || frame_h > 0)
@@ -509,12 +523,12 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
     const bool framed = r.frame_h > 0 && r.pad_h > 0;
     const int32_t* sk = slot ? slot + r.slot_off : nullptr;  // per-modality pool rows
-    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && bytes % 16 == 0)
+    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && r.plane_stride == 0 && bytes % 16 == 0)
       rc = gather_launch(X[k], bytes, sk, idx + (long long)k * N, counts + k, N, G[k], st);
     else
       rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, sk, idx + (long long)k * N,
                              counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias, framed ? r.frame_h : 0,
-                             framed ? r.pad_h : 0);
+                             framed ? r.pad_h : 0, r.plane_stride);
     if (rc) return rc;
   }
   return MS_OK;

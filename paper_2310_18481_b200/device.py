@@ -38,7 +38,7 @@ class Segment(C.Structure):
 class RowDesc(C.Structure):
     _fields_ = [("lines", C.c_longlong), ("width", C.c_int), ("c_src", C.c_int), ("c_dst", C.c_int),
                 ("pad_w", C.c_int), ("src_u8", C.c_int), ("u8_scale", C.c_float), ("u8_bias", C.c_float),
-                ("frame_h", C.c_int), ("pad_h", C.c_int), ("slot_off", C.c_int)]
+                ("frame_h", C.c_int), ("pad_h", C.c_int), ("slot_off", C.c_int), ("plane_stride", C.c_longlong)]
 
 
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
@@ -62,7 +62,7 @@ _SIGS = {
     "ms_gemm_plan_conv_k32": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
                                _I, _I, _P, _I, _I, _I], C.c_int),
     "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
-    "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _LL, _I], C.c_int),
+    "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _I, _LL, _P, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -383,17 +383,18 @@ def plan_conv(X, n_img, H, W_in, C_in, c_stride, KH, KW, stride, pad, Wt, Cout, 
     return p
 
 
-def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0):
-    """Fused 7x7/2 conv (4-channel pre-padded pixels, 64 out, ReLU) + 3x3/2
-    ceil max pool (``ms_gemm_plan_stem_pool``); ``Wt`` is the C4 packing."""
+def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0, planes=1, plane_stride=0):
+    """Fused 7x7/2 conv (4-channel pre-padded pixels, or three 4-channel
+    planes, 64 out, ReLU) + 3x3/2 ceil max pool (``ms_gemm_plan_stem_pool``);
+    ``Wt`` from ``encoders.pack_stem_weight`` (``_planes`` for 3 planes)."""
     p = GemmPlan()
-    check(lib().ms_gemm_plan_stem_pool(p.addr, ptr(X), n_img, H, W_in, KH, pad, ptr(Wt), ptr(bias), ptr(Y), ldy,
-                                       col0), "ms_gemm_plan_stem_pool")
+    check(lib().ms_gemm_plan_stem_pool(p.addr, ptr(X), n_img, H, W_in, KH, pad, planes, plane_stride, ptr(Wt),
+                                       ptr(bias), ptr(Y), ldy, col0), "ms_gemm_plan_stem_pool")
     p.keep = [X, Wt, bias, Y]
     oh = (H + 2 * pad - KH) // 2 + 1
     ow = (W_in + 2 * pad - KH) // 2 + 1
-    p.flops = 2 * n_img * oh * ow * 64 * KH * KH * 4
-    p.label = f"stem conv {KH}x{KH}/2 4->64 {n_img}x{oh}x{ow} + maxpool"
+    p.flops = 2 * n_img * oh * ow * 64 * KH * KH * 4 * planes
+    p.label = f"stem conv {KH}x{KH}/2 {4 * planes}->64 {n_img}x{oh}x{ow} + maxpool"
     return p
 
 

@@ -282,6 +282,21 @@ def pack_stem_weight(w):
     return b.reshape(-1).to(torch.bfloat16).contiguous()
 
 
+def pack_stem_weight_planes(w, planes: int = 3):
+    """[64, cin <= 4*planes, 7, 7] -> the planar fused stem's weights: per
+    (filter row kh, 4-channel plane) a 64 x 32 block (8 window pixels x 4
+    channels of that plane), no-swizzle core-matrix order (K step 128 B, N step
+    512 B), blocks in (kh, plane) order."""
+    import torch
+    cout, cin, kh, kw = w.shape
+    assert cout == 64 and kh == 7 and kw <= 8 and cin <= 4 * planes
+    wk = torch.zeros(kh, 64, 8, 4 * planes, dtype=torch.float32)
+    wk[:, :, :kw, :cin] = w.float().permute(2, 0, 3, 1)
+    wk = wk.reshape(kh, 64, 8, planes, 4).permute(0, 3, 1, 2, 4).reshape(kh, planes, 64, 32)
+    b = wk.reshape(kh, planes, 8, 8, 4, 8).permute(0, 1, 2, 4, 3, 5)  # (kh, pl, n/8, k/8, n%8, k%8)
+    return b.reshape(-1).to(torch.bfloat16).contiguous()
+
+
 def pack_c12_weight(w):
     """[cout, cin <= 12, kh <= 8, kw <= 8] -> [cout, ceil(3*kh/2) * 64]: K =
     (filter row, 8 window pixels x 12 channels = 96) rows back to back, zero
@@ -374,12 +389,12 @@ class BNInceptionEncoder:
         self.dev = torch.device(device)
         self.layers = bninception_layers(modality.channels, modality.size)
         self.weights_cpu = bninception_weights(modality.channels, modality.size, seed)
+        # conv1 + pool1 as one kernel (MS_NO_FUSED_STEM=1: the conv + pool pair, for A/B)
+        self.fused_stem = os.environ.get("MS_NO_FUSED_STEM") is None
         self._pack()
         self._alloc()
         self._programs = {}
         self._lanes = None  # side streams for the Inception branch lanes
-        # conv1 + pool1 as one kernel for 4-channel frames (MS_NO_FUSED_STEM=1: A/B)
-        self.fused_stem = os.environ.get("MS_NO_FUSED_STEM") is None
 
     # -- weights on device
     def _pack(self):
@@ -395,6 +410,8 @@ class BNInceptionEncoder:
                 self.w[name] = (packer(w) if packer else pack_smallc_weight(w, cp)).to(d)
                 if cp == 4:
                     self.w["stem"] = pack_stem_weight(w).to(d)
+                elif cp == 12:
+                    self.w["stem"] = pack_stem_weight_planes(w).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
             elif w.shape[1] % 64 and w.shape[1] % 32 == 0:
@@ -459,6 +476,16 @@ class BNInceptionEncoder:
         # once here, never touched by the gather)
         rp = self.mod.row_pad
         self.x = torch.zeros(n_img, size + 2 * rp, size + 2 * CONV1_PAD, self.mod.cpad, dtype=bf, device=d)
+        # fused stem: 4-channel frames as they are; 12-channel (flow) frames as
+        # three 4-channel planes in the same buffer (ms_compact writes them)
+        h1 = conv_out(size, 7, 2, 3)
+        cp = self.mod.cpad
+        self.stem_planes = 0
+        if self.fused_stem and cp == 4 and h1 <= 128:
+            self.stem_planes = 1
+        elif self.fused_stem and cp == 12 and h1 <= 112:
+            self.stem_planes = 3
+        self.x_plane_stride = n_img * (size + 2 * rp) * (size + 2 * CONV1_PAD) * 4 if self.stem_planes == 3 else 0
 
     def program(self, n_req: int):
         if n_req in self._programs:
@@ -485,12 +512,12 @@ class BNInceptionEncoder:
         # (channels padded to 8 in memory; no im2col round trip)
         cp = self.mod.cpad
         h2 = pool_out(h1, 3, 2, 0, True)
-        if cp == 4 and h1 <= 128 and self.fused_stem:
-            # 4-channel frames: conv1 + bias + ReLU + pool1 in one kernel that
-            # feeds the raw padded input rows to the tensor cores (csrc/gemm.cu
-            # MODE_STEM_POOL); the unpooled map never reaches HBM
+        if self.stem_planes:
+            # conv1 + bias + ReLU + pool1 in one kernel that feeds the raw padded
+            # input rows to the tensor cores (csrc/gemm.cu MODE_STEM_POOL; flow
+            # as three 4-channel planes); the unpooled map never reaches HBM
             P.gemm(dv.plan_stem_pool(self.x, n, size, size, 7, 3, self.w["stem"], self.b["conv1"], self.a_p1,
-                                     ldy=64))
+                                     ldy=64, planes=self.stem_planes, plane_stride=self.x_plane_stride))
         else:
             P.gemm(dv.plan_conv(self.x, n, size, size, cp, cp, 7, 7, 2, 3, self.w["conv1"], 64,
                                 self.b["conv1"], self.a_c1, ldd=64, BN=64, relu=True,

@@ -65,7 +65,9 @@ class MaskedModel:
         # (lines, width, c_src, c_dst, pad_w[, src_u8, u8_scale, u8_bias[, frame_h, pad_h]])
         self.rows = [tuple(r) + (0, 1.0, 0.0, 0, 0)[len(r) - 5:] for r in rows]
         # modality k's request -> pool-row map lives at slot_d[k*max_req : k*max_req + n]
-        self.rows = [r[:10] + (k * max_req,) for k, r in enumerate(self.rows)]
+        # + slot_off, + plane_stride (an encoder whose stem reads 4-channel planes)
+        self.rows = [r[:10] + (k * max_req, int(getattr(e, "x_plane_stride", 0)))
+                     for k, (r, e) in enumerate(zip(self.rows, encoders))]
         self.src_bytes = [1 if r[5] else 2 for r in self.rows]
         self.row_bytes = [int(r[0] * r[1] * r[2] * b) for r, b in zip(self.rows, self.src_bytes)]
         self.K = len(encoders)

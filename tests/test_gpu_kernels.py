@@ -532,6 +532,68 @@ def test_stem_conv_pool_fused_vs_unfused_and_torch(dev, n, H, Cin):
     assert ok, (err, scale)
 
 
+@pytest.mark.parametrize("n,H,Cin", [(2, 32, 10), (3, 224, 10), (2, 64, 12)])
+def test_stem_conv_pool_three_planes_vs_torch(dev, n, H, Cin):
+    """MODE_STEM_POOL over three 4-channel planes (flow's 10 channels padded
+    to 12): same fused conv + ReLU + max pool, planar input layout."""
+    from paper_2310_18481_b200.encoders import pack_stem_weight_planes
+    g = torch.Generator().manual_seed(H + Cin + 17)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    Hp = H + 6
+    X = torch.zeros(3, n, Hp, Hp, 4, dtype=torch.bfloat16)
+    xp = torch.zeros(n, Hp, Hp, 12, dtype=torch.bfloat16)
+    xp[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+    for q in range(3):
+        X[q] = xp[..., 4 * q:4 * q + 4]
+    OH = (H + 6 - 7) // 2 + 1
+    PH = -(-(OH - 3) // 2) + 1
+    Y = torch.full((n * PH * PH, 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    dev.plan_stem_pool(X.cuda(), n, H, H, 7, 3, pack_stem_weight_planes(w).cuda(), b.cuda(), Y, ldy=64, planes=3,
+                       plane_stride=n * Hp * Hp * 4).run()
+    torch.cuda.synchronize()
+    assert torch.isfinite(Y.float()).all()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=2, padding=3).clamp_min(0)
+    ref = torch.nn.functional.max_pool2d(ref, 3, 2, ceil_mode=True).permute(0, 2, 3, 1).reshape(-1, 64)
+    ok, err, scale = _close(Y.cpu(), ref)
+    assert ok, (err, scale)
+
+
+def test_gather_planar_twelve_channels(dev):
+    """ms_compact's planar 12-channel gather (plane q = channels 4q..4q+3) ==
+    the interleaved gather split into planes."""
+    torch.manual_seed(5)
+    N, S, Hs, Ws, C = 3, 2, 6, 16, 10
+    pool = torch.randint(0, 256, (4, S, Hs, Ws, C), dtype=torch.uint8, device="cuda")
+    mask = torch.tensor([1, 1, 1], dtype=torch.int16, device="cuda")
+    slot = torch.tensor([2, 0, 3], dtype=torch.int32, device="cuda")
+    pad, ph = 3, 3
+    Hp, Wp = Hs + 2 * ph, Ws + 2 * pad
+    outs = []
+    for planar in (False, True):
+        G = torch.zeros(N * S * Hp * Wp * 12, dtype=torch.bfloat16, device="cuda")
+        stride = N * S * Hp * Wp * 4 if planar else 0
+        rows = (dev.RowDesc * 1)(dev.RowDesc(S * Hs, Ws, C, 12, pad, 1, 1.0 / 64.0, -2.0, Hs, ph, 0, stride))
+        idx = torch.zeros(N, dtype=torch.int32, device="cuda")
+        inv = torch.zeros(N, dtype=torch.int32, device="cuda")
+        counts = torch.zeros(1, dtype=torch.int32, device="cuda")
+        offs = torch.zeros(3, dtype=torch.int32, device="cuda")
+        perm = torch.zeros(N, dtype=torch.int32, device="cuda")
+        import ctypes
+        Xp = (ctypes.c_void_p * 1)(pool.data_ptr())
+        Gp = (ctypes.c_void_p * 1)(G.data_ptr())
+        dev.check(dev.lib().ms_compact(mask.data_ptr(), N, 1, Xp, rows, slot.data_ptr(), Gp, idx.data_ptr(),
+                                       inv.data_ptr(), counts.data_ptr(), offs.data_ptr(), perm.data_ptr(),
+                                       dev.stream_ptr()), "ms_compact")
+        torch.cuda.synchronize()
+        outs.append(G.cpu())
+    inter = outs[0].reshape(N * S, Hp, Wp, 12)
+    planar = outs[1].reshape(3, N * S, Hp, Wp, 4)
+    for q in range(3):
+        assert torch.equal(planar[q], inter[..., 4 * q:4 * q + 4])
+
+
 @pytest.mark.parametrize("M,K,N,BN", [(1000, 1024, 256, 256), (300, 192, 96, 96), (128, 64, 64, 64), (517, 576, 352, 192)])
 def test_gemm_cta_pair_dense_vs_torch(dev, M, K, N, BN):
     """2-CTA clusters (tcgen05.mma.cta_group::2, M=256 tiles)."""
