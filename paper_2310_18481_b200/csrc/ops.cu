@@ -3,6 +3,7 @@
 // whole encoder forward in one native call, CUDA-event helpers for the
 // profiler, and the error plumbing.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "mosel_b200.h"
@@ -135,6 +136,79 @@ __device__ __forceinline__ void pool_hrow_max2(const __nv_bfloat16* __restrict__
 // then every output (pixel, 8 channels) is summed from shared memory in fp32.
 // The register-streaming kernel spent most of its time waiting on dependent
 // row loads for these tiny rows.
+// 3x3 / stride 1 / pad 1 average pool (count_include_pad) + bias + ReLU,
+// register-blocked: one thread = one (image, column, 8-channel group) and
+// kAvgRows output rows; its (kAvgRows + 2) x 3 input loads are independent
+// (all issued up front), neighbouring threads read neighbouring 16-B groups.
+// No shared memory, no block barriers, no divisions in the loop.  Replaces
+// the smem-staged kernel, which was bound by its three barrier-separated
+// phases and index arithmetic on these small (28^2 / 14^2 / 7^2) maps.
+constexpr int kAvgRows = 4;
+__global__ void __launch_bounds__(256) avgpool3_s1_reg_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H,
+                                                             int W, int C, long long xcs, __nv_bfloat16* __restrict__ Y,
+                                                             long long ycs, int ycol0, const float* __restrict__ bias,
+                                                             int relu) {
+  pdl_trigger();
+  pdl_wait();
+  const int cg = C >> 3;
+  const int rb_n = (H + kAvgRows - 1) / kAvgRows;
+  const long long total = (long long)n_img * rb_n * W * cg;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(t % cg);
+    long long u = t / cg;
+    const int x = (int)(u % W);
+    u /= W;
+    const int rb = (int)(u % rb_n);
+    const long long img = u / rb_n;
+    const int oh0 = rb * kAvgRows;
+    float hs[kAvgRows + 2][8];
+#pragma unroll
+    for (int r = 0; r < kAvgRows + 2; ++r) {
+      const int ih = oh0 - 1 + r;
+      uint4 v[3];
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int xx = x - 1 + dx;
+        v[dx] = (ih >= 0 && ih < H && xx >= 0 && xx < W)
+                    ? __ldg(reinterpret_cast<const uint4*>(X + ((img * H + ih) * W + xx) * xcs + g * 8))
+                    : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v[dx])[j]);
+          s2.x += f.x;
+          s2.y += f.y;
+        }
+        hs[r][2 * j] = s2.x;
+        hs[r][2 * j + 1] = s2.y;
+      }
+    }
+    float bv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bv[j] = bias != nullptr ? bias[g * 8 + j] : 0.0f;
+#pragma unroll
+    for (int r = 0; r < kAvgRows; ++r) {
+      if (oh0 + r >= H) break;
+      uint32_t pk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float a = (hs[r][2 * j] + hs[r + 1][2 * j] + hs[r + 2][2 * j]) * (1.0f / 9.0f) + bv[2 * j];
+        float b = (hs[r][2 * j + 1] + hs[r + 1][2 * j + 1] + hs[r + 2][2 * j + 1]) * (1.0f / 9.0f) + bv[2 * j + 1];
+        if (relu) {
+          a = fmaxf(a, 0.0f);
+          b = fmaxf(b, 0.0f);
+        }
+        pk[j] = pack_bf16x2(a, b);
+      }
+      *reinterpret_cast<uint4*>(Y + ((img * H + oh0 + r) * W + x) * ycs + ycol0 + g * 8) =
+          make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+}
+
 constexpr int kAvgSmem = 48 * 1024;
 __global__ void __launch_bounds__(256) avgpool3_s1_kernel(const __nv_bfloat16* __restrict__ X, int H, int W, int C,
                                                          long long xcs, int TH, __nv_bfloat16* __restrict__ Y,
@@ -546,6 +620,16 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const int OH = pool_out(a.H, a.k, a.stride, a.pad, a.ceil_mode);
   const int OW = pool_out(a.W, a.k, a.stride, a.pad, a.ceil_mode);
   const int threads = (a.C / 8) * OW;
+  static const bool avg_smem = getenv("MS_AVGPOOL_SMEM") != nullptr;  // A/B: the smem-staged kernel
+  if (!a.is_max && a.k == 3 && a.stride == 1 && a.pad == 1 && !avg_smem) {
+    const long long items = (long long)a.n_img * ((a.H + kAvgRows - 1) / kAvgRows) * a.W * (a.C / 8);
+    long long blocks = (items + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    launch_k(avgpool3_s1_reg_kernel, dim3((unsigned)blocks), dim3(256), 0, st, 1,
+             reinterpret_cast<const __nv_bfloat16*>(a.X), a.n_img, a.H, a.W, a.C, a.xcs,
+             reinterpret_cast<__nv_bfloat16*>(a.Y), a.ycs, a.ycol0, a.bias, a.relu);
+    return check_launch("avgpool3_s1_reg_kernel");
+  }
   if (!a.is_max && a.k == 3 && a.stride == 1 && a.pad == 1 && a.n_img <= 65535 &&
       5 * (a.W + 2) * a.C * 2 <= kAvgSmem) {
     // the fp32 sums of 9 taps: order per output (dy, dx) = the oracle's window order up to fp32 rounding
@@ -624,7 +708,7 @@ using namespace mosel;
 
 extern "C" {
 
-int ms_abi_version(void) { return 2; }
+int ms_abi_version(void) { return 3; }
 int ms_set_pdl(int enable) {
   const int prev = g_pdl;
   g_pdl = enable ? 1 : 0;

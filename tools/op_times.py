@@ -71,7 +71,13 @@ for k, (enc, c) in enumerate(zip(m.encoders, counts)):
             ts.append(e0.elapsed_us(e1) / REP)
         us = float(np.median(ts))
         fl = op.flops if kind == "gemm" else 0
-        rows.append((us, k, i, kind, op.label if kind == "gemm" else "", fl))
+        if kind == "gemm":
+            lab = op.label
+        elif kind == "pool":
+            lab = f"{'max' if op[10] else 'avg'} {op[6]}x{op[6]}/{op[7]} C={op[4]} {op[1]}x{op[2]}x{op[3]}"
+        else:
+            lab = ""
+        rows.append((us, k, i, kind, lab, fl))
 tot = sum(r[0] for r in rows)
 gem = [r for r in rows if r[3] == "gemm"]
 gt = sum(r[0] for r in gem)
