@@ -133,6 +133,8 @@ struct GemmParams {
   int halo_slot;    // MODE_CONV_HALO: bytes of one halo buffer (2 buffers precede the weight ring)
   int b_resident;   // MODE_CONV_HALO: all 9 x cchunks weight tiles stay in smem for the CTA's lifetime
   int warp_store;   // EPI_TMA: each epilogue warp stores its own 32 rows (no cross-warp barrier)
+  int direct_store; // EPI_TMA conv tiles: registers -> global, no smem staging (A/B only, MS_DIRECT_STORE:
+                    // measured 13 % slower on conv2 at 56^2 than the TMA-store epilogue)
   int stage_bytes;  // epilogue staging bytes in shared memory
   // MODE_STEM_POOL: raw pre-padded 4-channel input rows, fused 3x3/2 max pool
   const uint8_t* xraw;
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // output row for this thread (or -1): residual / fp32 / split-K paths
       long long out_row = -1;
       if constexpr (kConv) {
-        if (EPI != EPI_TMA || p.residual != nullptr) {
+        if (EPI != EPI_TMA || p.residual != nullptr || p.direct_store) {
           const int tw = m_tile % p.tiles_w;
           const int th = (m_tile / p.tiles_w) % p.tiles_h;
           const int tn = m_tile / (p.tiles_w * p.tiles_h);
@@ -660,6 +662,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (tr0) GEMM_TRACE(9);
+          if (p.direct_store) {
+            // registers -> global (64 contiguous bytes per row): no shared-memory
+            // staging traffic competing with the MMAs' operand reads
+            if (out_row >= 0) {
+              const Seg& S = p.seg[g];
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(S.ptr) + out_row * S.ldd + S.col0 + (nb - S.n_begin);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (nb + 8 * j < S.n_end)
+                  *reinterpret_cast<uint4*>(dst + 8 * j) = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            }
+            return;
+          }
           if (p.warp_store) {
             // this warp's 32 rows x 32 columns: own 2 KB slice, own TMA store,
             // no barrier with the other warps of the group
@@ -1694,6 +1709,8 @@ static int encode_store_maps(GemmPlan* P) {
   // group: per-warp 4-D boxes measured slower there (halo 3x3 at 56^2:
   // 135 vs 129 us; tools/op_times.py with MS_NO_WARP_STORE=1 as the A/B).
   // The conv coordinates of the per-warp path are kept for the A/B.
+  static const bool direct = getenv("MS_DIRECT_STORE") != nullptr;
+  p.direct_store = (direct && conv) ? 1 : 0;
   static const bool no_warp_store = getenv("MS_NO_WARP_STORE") != nullptr;
   static const bool conv_warp_store = getenv("MS_CONV_WARP_STORE") != nullptr;
   p.warp_store = (!no_warp_store && (!conv || (conv_warp_store && p.bn == 1 && (p.bw % 32 == 0 || 32 % p.bw == 0) &&
