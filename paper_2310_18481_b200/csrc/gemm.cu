@@ -1258,9 +1258,19 @@ constexpr int kStemWRow = 128 * 32 * 2;      // one input row's [W_j ; W_(j-2)]:
 constexpr int kStemWBytes = kStemMaxRows * kStemWRow;
 constexpr int kStemWBlk = 64 * 32 * 2;      // planes variant: one (filter row, plane) 64 n x 32 k block
 constexpr int kStemRowBuf = 128 * 128;     // <= 128 conv pixels x 64 ch bf16
-constexpr int kStemEpiWarps = 16;          // 4 per TMEM lane quarter, 16 channels each
+#ifndef STEM_EPI_WARPS
+#define STEM_EPI_WARPS 8
+#endif
+constexpr int kStemEpiWarps = STEM_EPI_WARPS;  // 2 per TMEM lane quarter, 32 channels each (8: 1.1x over 16 for rgb -- fewer warps competing with the MMA warp for issue slots)
 constexpr int kStemCh = 64 / (kStemEpiWarps / 4);
 constexpr int kStemThreads = 64 + 32 * kStemEpiWarps;
+template <int N>
+__device__ __forceinline__ void stem_tmem_ld(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16)
+    tmem_ld_32x32b_x16(taddr, r);
+  else
+    tmem_ld_32x32b_x32(taddr, r);
+}
 
 __device__ __forceinline__ uint32_t bf16x2_max(uint32_t a, uint32_t b) {
   __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
@@ -1447,8 +1457,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       if (warp == 2 && lane == 0) trace(k, 2);
       uint32_t v0[kStemCh], v1[kStemCh];
       // OPEN: row 2i is the pair's second row (columns 64..127)
-      tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
-      if (n == 2) tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + 64), v1);
+      stem_tmem_ld(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
+      if (n == 2) stem_tmem_ld(t_lane + (uint32_t)(slot * 128 + 64), v1);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -1503,8 +1513,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       tc_fence_after();
       uint32_t v0[kStemCh], v1[kStemCh];
       // OPEN: row 2i is the pair's second row (columns 64..127)
-      tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
-      if (n == 2) tmem_ld_32x32b_x16(t_lane + (uint32_t)(slot * 128 + 64), v1);
+      stem_tmem_ld(t_lane + (uint32_t)(slot * 128 + (w.open ? 64 : 0)), v0);
+      if (n == 2) stem_tmem_ld(t_lane + (uint32_t)(slot * 128 + 64), v1);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
