@@ -1437,8 +1437,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         phase ^= 1;
       }
     }
-  } else if constexpr (kOverlap) {  // ------------- epilogue warps 2..17 (overlapping row groups)
-    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, 16-channel chunk
+  } else if constexpr (kOverlap) {  // ------------- epilogue warps (overlapping row groups)
+    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, kStemCh-channel chunk
     const int x = 7 * (lane >> 3) + (lane & 7);   // this lane's conv pixel within the warp's 29
     auto lane_of = [](int y) { return y < 28 ? (y / 7) * 8 + y % 7 : 31; };
     const int src1 = lane_of(min(x + 1, 28)), src2 = lane_of(min(x + 2, 28));
@@ -1497,10 +1497,10 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       }
       if (warp == 2 && lane == 0) trace(k, 3);
     }
-  } else {  // ----------------------------- epilogue warps 2..17 (linear rows, smem horizontal pool)
-    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, 16-channel chunk
+  } else {  // ----------------------------- epilogue warps (linear rows, smem horizontal pool)
+    const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, kStemCh-channel chunk
     const int ow = q * 32 + lane;
-    const int tid = threadIdx.x - 64;             // 0..511
+    const int tid = threadIdx.x - 64;             // 0 .. 32 * kStemEpiWarps - 1
     const int n_items = PW * 8;                   // pooled pixels x 8 16-B channel groups
     const Seg& Y = p.seg[0];
     const uint32_t t_lane = tmem_base + (uint32_t)(c * kStemCh) + ((uint32_t)(q * 32) << 16);
