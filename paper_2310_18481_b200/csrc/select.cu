@@ -200,7 +200,14 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
                                                               const int32_t* __restrict__ idx,
                                                               const int32_t* __restrict__ count,
                                                               void* __restrict__ dst_v, int frame_h, int pad_h,
-                                                              long long plane_vecs) {
+                                                              long long plane_vecs, int per_cap, int pdl_mode) {
+  // PDL chain across one pass's gathers (ms_compact, pdl_mode 1 then 2): the first waits for the
+  // index kernel, then lets the next gather start; later gathers start at
+  // once and wait for their predecessor only before exiting, so gathers of
+  // different modalities overlap and the last one's completion still implies
+  // all of them (what a PDL successor's griddepcontrol.wait observes)
+  if (pdl_mode != 2) pdl_wait();  // 0: standalone launch, 1: first of a chain
+  pdl_trigger();
   typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
   __shared__ long long s_dline[32];
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
     if (slot) r = slot[r];
     const unsigned char* srow = reinterpret_cast<const unsigned char*>(src_v) + (long long)r * lines * line_bytes;
     vec_t* drow = dst + (long long)j * dst_lines * wd * gv;
-    const int per = min(32, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
+    const int per = min(per_cap, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
     for (long long ln0 = (long long)blockIdx.x * per; ln0 < lines; ln0 += (long long)gridDim.x * per) {
       const int nl = (int)min((long long)per, lines - ln0);
       __syncthreads();
@@ -353,6 +360,7 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
       }
     }
   }
+  if (pdl_mode == 2) pdl_wait();
 }
 
 // generic fallback (line not 16-B aligned or too long): one thread = one
@@ -401,7 +409,7 @@ __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, lo
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
                              cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f,
-                             int frame_h = 0, int pad_h = 0, long long plane_stride = 0) {
+                             int frame_h = 0, int pad_h = 0, long long plane_stride = 0, int pdl_mode = 0) {
   if (c_dst % 4 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
     return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 4 == 0, pad_w >= 0");
   if (frame_h < 0 || pad_h < 0 || (frame_h > 0 && lines % frame_h != 0))
@@ -413,7 +421,9 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
                            line_bytes > kMaxLineBytes || plane_stride % 4 != 0))
     return set_error(MS_ERR_INVALID, "gather: planar output needs 12 destination channels, even padded width");
   if (line_bytes % 16 == 0 && line_bytes <= kMaxLineBytes) {
-    const long long per = line_bytes > 0 ? (kMaxLineBytes / line_bytes < 32 ? kMaxLineBytes / line_bytes : 32) : 1;
+    static const int per_env = getenv("MS_GATHER_LINES") ? atoi(getenv("MS_GATHER_LINES")) : 0;  // A/B
+    const int per_cap = per_env > 0 ? per_env : 32;
+    const long long per = line_bytes > 0 ? (kMaxLineBytes / line_bytes < per_cap ? kMaxLineBytes / line_bytes : per_cap) : 1;
     long long bx = (lines + per - 1) / per;
     if (bx > 64) bx = 64;
     if (bx < 1) bx = 1;
@@ -421,17 +431,17 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     const float sc = src_u8 ? u8_scale : 1.0f, bi = src_u8 ? u8_bias : 0.0f;
     if (c_dst % 8 != 0) {  // 8-byte vector stores (4-channel groups)
       if (src_u8)
-        gather_rows_pad_kernel<true, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                              idx, count, dst, frame_h, pad_h, plane_stride / 4);
+        launch_k(gather_rows_pad_kernel<true, 4>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                              idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
       else
-        gather_rows_pad_kernel<false, 4><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                               idx, count, dst, frame_h, pad_h, plane_stride / 4);
+        launch_k(gather_rows_pad_kernel<false, 4>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                               idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
     } else if (src_u8) {
-      gather_rows_pad_kernel<true, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                            idx, count, dst, frame_h, pad_h, plane_stride / 4);
+      launch_k(gather_rows_pad_kernel<true, 8>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                            idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
     } else {
-      gather_rows_pad_kernel<false, 8><<<grid, 256, 0, st>>>(src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                             idx, count, dst, frame_h, pad_h, plane_stride / 4);
+      launch_k(gather_rows_pad_kernel<false, 8>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
+                                                             idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
     }
   } else {
     if (c_dst % 8 != 0 || frame_h > 0)
@@ -517,18 +527,22 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
   int rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bool chained = false;  // the previous launch was a padded gather of this chain
   for (int k = 0; k < K; ++k) {
     if (X == nullptr || G == nullptr || rows == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
     const MsRowDesc& r = rows[k];
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
     const bool framed = r.frame_h > 0 && r.pad_h > 0;
     const int32_t* sk = slot ? slot + r.slot_off : nullptr;  // per-modality pool rows
-    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && r.plane_stride == 0 && bytes % 16 == 0)
+    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && r.plane_stride == 0 && bytes % 16 == 0) {
       rc = gather_launch(X[k], bytes, sk, idx + (long long)k * N, counts + k, N, G[k], st);
-    else
+      chained = false;  // a plain launch ends the PDL chain (the next gather waits at its start again)
+    } else {
       rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, sk, idx + (long long)k * N,
                              counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias, framed ? r.frame_h : 0,
-                             framed ? r.pad_h : 0, r.plane_stride);
+                             framed ? r.pad_h : 0, r.plane_stride, chained ? 2 : 1);
+      chained = true;
+    }
     if (rc) return rc;
   }
   return MS_OK;
