@@ -133,6 +133,7 @@ struct GemmParams {
   int halo_slot;    // MODE_CONV_HALO: bytes of one halo buffer (2 buffers precede the weight ring)
   int b_resident;   // MODE_CONV_HALO: all 9 x cchunks weight tiles stay in smem for the CTA's lifetime
   int warp_store;   // EPI_TMA: each epilogue warp stores its own 32 rows (no cross-warp barrier)
+  int tile_groups;  // EPI_TMA, BN <= 64: the two epilogue warp groups take alternate tiles
   int direct_store; // EPI_TMA conv tiles: registers -> global, no smem staging (A/B only, MS_DIRECT_STORE:
                     // measured 13 % slower on conv2 at 56^2 than the TMA-store epilogue)
   int stage_bytes;  // epilogue staging bytes in shared memory
@@ -271,7 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+      // one arrive per epilogue warp (per warp of the owning group with tile groups)
+      mbar_init(&tempty[a], (EPI == EPI_TMA && MODE != MODE_GATHER && p.tile_groups) ? kEpiWarps / 2 : kEpiWarps);
       mbar_init(&afull[a], 1);
       mbar_init(&aempty[a], 1);
     }
@@ -547,7 +549,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    // tile groups (narrow tiles, BN <= 64): the two warp groups take
+    // alternate tiles (group g = accumulator g) and all of a tile's chunks,
+    // so two tiles' epilogues run at once instead of one tile's two halves
+    const bool tg = EPI == EPI_TMA && MODE != MODE_GATHER && p.tile_groups;
+    const int cs = tg ? 1 : 2;  // chunk step
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      if (tg && acc != grp) {  // the other group's tile
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       const TileIdx ti = decode_tile(p, t, n_tiles);
       const int m_tile = ti.m, n_tile = ti.n;
       if constexpr (MODE == MODE_GATHER) {
@@ -730,26 +742,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       uint32_t va[32], vb[32];
-      int c = grp;
+      int c = tg ? 0 : grp;
       if (c < n_chunks) tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), va);
       while (c < n_chunks) {
         tmem_wait_ld();
-        if (c + 2 < n_chunks)
-          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + 2) * 32), vb);
+        if (c + cs < n_chunks)
+          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + cs) * 32), vb);
         else
           release_acc();
         process(va, c);
-        c += 2;
+        c += cs;
         if (c >= n_chunks) break;
         tmem_wait_ld();
-        if (c + 2 < n_chunks)
-          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + 2) * 32), va);
+        if (c + cs < n_chunks)
+          tmem_ld_32x32b_x32(t_base + (uint32_t)((c + cs) * 32), va);
         else
           release_acc();
         process(vb, c);
-        c += 2;
+        c += cs;
       }
-      if (grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
+      if (!tg && grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
       if (warp == 2 && lane == 0 && t == (int)blockIdx.x) GEMM_TRACE(11);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -1658,6 +1670,8 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   int rc = encode_map(&P->tmB, 2, W, dims, strides, box, es);
   if (rc) return rc;
   p.BN = BN;
+  static const bool no_tile_groups = getenv("MS_NO_TILE_GROUPS") != nullptr;  // A/B switch for tools
+  p.tile_groups = (!no_tile_groups && BN <= 64 && p.mode != MODE_GATHER && !p.out_fp32) ? 1 : 0;
   p.num_kb = num_kb;
   p.ksplit = 1;
   p.kb_per = num_kb;
