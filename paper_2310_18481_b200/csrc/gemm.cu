@@ -1671,7 +1671,8 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   if (rc) return rc;
   p.BN = BN;
   static const bool no_tile_groups = getenv("MS_NO_TILE_GROUPS") != nullptr;  // A/B switch for tools
-  p.tile_groups = (!no_tile_groups && BN <= 64 && p.mode != MODE_GATHER && !p.out_fp32) ? 1 : 0;
+  static const int tg_max_bn = getenv("MS_TILE_GROUPS_BN") ? atoi(getenv("MS_TILE_GROUPS_BN")) : 64;
+  p.tile_groups = (!no_tile_groups && BN <= tg_max_bn && p.mode != MODE_GATHER && !p.out_fp32) ? 1 : 0;
   p.num_kb = num_kb;
   p.ksplit = 1;
   p.kb_per = num_kb;
