@@ -268,11 +268,12 @@ def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, 
         trials.append((q, v))
         log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f} "
             f"req/pass {st.requests / max(1, st.passes):.1f} late {st.late} drop(policy/dispatch/admit) "
-            f"{st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} policy {st.policy_host_us / max(1, st.policy_runs):.0f}us x{st.policy_runs}")
-        if 0.01 < v < 0.05:  # near the limit one Poisson burst decides a short window: re-draw once
+            f"{st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} policy host {st.policy_host_us / max(1, st.policy_runs):.0f}us "
+            f"x{st.policy_runs}, device pass_select {st.policy_device_us / max(1, st.policy_launches):.1f}us x{st.policy_launches}")
+        if 0.005 < v <= 0.01:  # near the limit one Poisson burst decides a short window: confirm on a re-draw
             lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 2000 + it, max_size=max_size,
                            cost=cost)
-            v = min(v, lg.violation_ratio())
+            v = max(v, lg.violation_ratio())
             log(f"  rate {q:9.1f} req/s -> re-drawn arrivals: violation {lg.violation_ratio():.4f}")
         if v <= 0.01:
             lo = q
@@ -489,7 +490,8 @@ def our_arm(args):
         "config": {"workload": desc,
                    "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
                    "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
-                   "policy": ("per-request modality-subset argmax under the formed pass's deadline "
+                   "policy": ("device pass formation ms_pass_select (pass_select_kernel, one warp per "
+                              "formation): per-job modality-subset argmax under the formed pass's deadlines "
                               f"(batched P5; pass <= {args.pass_frac} x deadline)")
                    if (args.selection == "pass" and not args.no_batching) else
                    "optimized (EDF + MCKP + upgrade)" + ("" if args.no_batching else
@@ -501,6 +503,11 @@ def our_arm(args):
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
         "slo_attainment": round(attainment, 5),
+        "slo_met": bool(agg[0] >= 0.99 * agg[1]),
+        "policy_step": {"kernel": "pass_select_kernel (ms_pass_select)", "launches": st.policy_launches,
+                        "device_us_mean": round(st.policy_device_us / max(1, st.policy_launches), 2),
+                        "host_us_mean": round(st.policy_host_us / max(1, st.policy_runs), 2),
+                        "passes": st.passes},
         "requests_with_modalities_dropped": drop_share,
         "latency_ms": {"p50": None if pct[50] is None else round(pct[50] / 1000, 3),
                        "p99": None if pct[99] is None else round(pct[99] / 1000, 3)},
@@ -511,7 +518,8 @@ def our_arm(args):
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "offered_rate_per_gpu": round(e2e_rate, 1),
                 "h2d_bytes_per_step": int(st2.h2d_bytes / n_steps_total),
                 "d2h_bytes_per_step": int(st2.d2h_bytes / n_steps_total),
-                "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5)},
+                "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5),
+                "slo_met": bool(agg2[0] >= 0.99 * agg2[1])},
         "clocks": clk, "cpu_baseline": cpu,
         "search": [(round(q, 1), round(v, 4)) for q, v in trials],
         "profile_us": {prof.combo_label(m): [prof.part_latency_us(m, 1),

@@ -75,6 +75,52 @@ int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t
                      const int64_t* deadline_us, int64_t dispatch_us, double factor, int N,
                      int32_t* choice, void* stream);
 
+/* ---- pass-level selection (the batched executor's policy step) ---------
+ * ms_pass_select <- the per-request argmax of scheduler.py:382-425 on a
+ * one-job scope (ms_policy_select above) with the latency
+ * budget coupled through ONE shared device pass: the batched executor's
+ * policy step (SURVEY §8f #4 cross-job batching; the reference never
+ * batches across jobs, and next_dispatch scheduler.py:428-449
+ * still pops and drop-checks the head on the host).  One warp per problem:
+ *   1. membership: the head + queued jobs in EDF order join at their fastest
+ *      candidate while n <= cap, now + est <= every member's deadline and
+ *      est <= max_pass_ns (< 0: none) -- warp prefix scans, first misfit ends;
+ *   2. the jobs left queued: rest_fast = est(their fastest counts), rest_dl =
+ *      earliest rest deadline >= now + est + rest_fast;
+ *   3. each member in EDF order takes the LARGEST frontier index >= its
+ *      current one whose pass estimate keeps every member, the rest and the
+ *      cap on time (one warp ballot over its candidates), until none moves.
+ * est(counts) = round_half_even(raw(sum_k w[k]*counts[k]) * factor) with raw
+ * the integer piecewise-linear pass time of MsPassCost.  Restated bit-exactly
+ * by oracle/selection.py pass_select.
+ * Problem p: jobs prob_job_off[p] .. +prob_n_jobs[p] (index 0 = the head),
+ * now (us) and EWMA factor.  Job j: size, deadline (us), n_cand frontier
+ * entries whose per-modality request counts are cand_counts[(job_cand_off[j]
+ * + c) * K + k] and whose per-request masks are req_masks[job_mask_off[j] +
+ * c * size + i].  Outputs: out_choice[j] = chosen index for members, -1
+ * otherwise; out_summary[p * MS_PASS_SUMMARY + ...] = {members, requests,
+ * counts[K]}; out_est_ns[p]; out_mask[p * out_mask_ld + r] = the pass's
+ * per-request masks (members in order).  Inputs/outputs may be device or
+ * pinned (mapped) host memory: the serving loop hands the kernel its pinned
+ * staging buffers directly (no memcpy), only out_mask lives in HBM. */
+#define MS_PASS_MAX_K 8
+#define MS_PASS_MAX_PTS 32
+#define MS_PASS_MAX_MEMBERS 1024
+#define MS_PASS_SUMMARY (2 + MS_PASS_MAX_K)
+typedef struct MsPassCost {
+  int K, n_pts;
+  int32_t w[MS_PASS_MAX_K];   /* work of one request's modality k, in 1/1024 all-modality requests */
+  int64_t u[MS_PASS_MAX_PTS]; /* knots: work (same units), strictly increasing */
+  int64_t t_ns[MS_PASS_MAX_PTS]; /* measured pass time at each knot (ns), non-decreasing */
+} MsPassCost;
+int ms_pass_select(int n_prob, const int32_t* prob_job_off, const int32_t* prob_n_jobs,
+                   const int64_t* prob_now_us, const double* prob_factor, const int32_t* job_size,
+                   const int64_t* job_deadline_us, const int32_t* job_n_cand, const int32_t* job_cand_off,
+                   const int32_t* job_mask_off, const int16_t* cand_counts, const uint16_t* req_masks,
+                   const MsPassCost* cost, int cap, int64_t max_pass_ns, int32_t* out_choice,
+                   int32_t* out_summary, int64_t* out_est_ns, uint16_t* out_mask, long long out_mask_ld,
+                   void* stream);
+
 /* ms_strategy_dp <- strategy.py:139-177 _DpTables (offline stage, SURVEY
  * §8f #2): the exact min-latency / min-part-count table over (requests
  * covered r <= max_size, credit index c < max_size*unit+1) for items
@@ -135,6 +181,14 @@ int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, i
 int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
                const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
                int32_t* combo_offsets, int32_t* perm, void* stream);
+
+/* as ms_compact, but modality k's compacted position j reads pool row
+ * (ring_base[k] + j) % n_ring (ring_base: HOST array [K]) instead of a slot
+ * map: the serving loop's per-modality input rings, where a pass's clips of
+ * modality k occupy consecutive ring rows (one DMA per modality) */
+int ms_compact_ring(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+                    const int32_t* ring_base, int n_ring, void* const* G, int32_t* idx, int32_t* inv,
+                    int32_t* counts, int32_t* combo_offsets, int32_t* perm, void* stream);
 
 /* ---- tcgen05 GEMM plans (encoders, fusion head) -----------------------
  * W is [N rows, K_pad] bf16 K-major (zero padded).  bias fp32[N] or NULL,

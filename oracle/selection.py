@@ -194,3 +194,119 @@ def compact(masks: np.ndarray, n_modalities: int):
 def dropped_modalities(mask: int, n_modalities: int) -> int:
     """profile.py:157-159 — dropped set = all_mask & ~mask."""
     return ((1 << n_modalities) - 1) & ~mask
+
+
+# --------------------------------------------------------------------------
+# Pass-level selection (the served policy step of the batched executor)
+#
+# The reference never batches across jobs (SPEC.md:398); SURVEY §8f #4 asks
+# for a cost model of its own.  This is the restatement that pins the device
+# kernel ``ms_pass_select`` (csrc/select.cu) bit-for-bit.  Its per-member step
+# is P5 (above) with the budget coupled through the shared pass: the largest
+# frontier index whose PASS estimate meets every member's deadline, the jobs
+# left queued, and the pass-length cap.  Integer arithmetic throughout except
+# the fp64 EWMA factor, applied exactly like scheduler.py:82-83 (one fp64
+# multiply, round half-even).
+
+
+def pass_raw_ns(u: int, pts_u, pts_t) -> int:
+    """Piecewise-linear pass time (ns) at work ``u`` (1/1024-request units):
+    clamped to the first point below it, extrapolated past the last;
+    integer floor division (all terms non-negative)."""
+    n = len(pts_u)
+    if n == 1 or u <= pts_u[0]:
+        return int(pts_t[0])
+    i = 0
+    while i + 2 < n and u > pts_u[i + 1]:
+        i += 1
+    return int(pts_t[i]) + (int(pts_t[i + 1]) - int(pts_t[i])) * (u - int(pts_u[i])) // \
+        (int(pts_u[i + 1]) - int(pts_u[i]))
+
+
+def pass_estimate_ns(counts, w, pts_u, pts_t, factor: float) -> int:
+    """round(raw(sum_k w_k * counts_k) * factor), half-even like Python round."""
+    u = 0
+    for wk, c in zip(w, counts):
+        u += int(wk) * int(c)
+    return round(pass_raw_ns(u, pts_u, pts_t) * factor)
+
+
+def pass_select(jobs, now_us: int, w, pts_u, pts_t, factor: float, cap: int,
+                max_pass_ns: int):
+    """One pass formation.
+
+    ``jobs``: the head (already popped by next_dispatch, scheduler.py:428-449)
+    followed by the queued jobs in EDF order, each ``(size, deadline_us,
+    cand_counts[C][K], cand_masks[C][size])``; candidates are the job's
+    frontier (latency up, credit strictly up, strategy.py:540-567).
+
+      1. membership: queued jobs join in EDF order at their fastest candidate
+         while n <= cap, now + est <= every member's deadline and
+         est <= max_pass (max_pass_ns < 0: no cap); the first misfit ends it;
+      2. rest = the jobs left queued: rest_fast = est(their fastest counts),
+         rest_dl = the earliest rest deadline >= now + est + rest_fast
+         (the jobs one following all-fastest pass can still serve);
+      3. upgrades: each member in EDF order takes the LARGEST candidate index
+         >= its current one whose pass estimate keeps now + est <= tight
+         (the members' earliest deadline), now + est + rest_fast <= rest_dl
+         and est <= max_pass; repeated until no member moves.
+
+    Returns (members M, choices[M], est_ns, counts[K], masks[n_req]).
+    """
+    K = len(w)
+    now_ns = now_us * 1000
+
+    def est(c):
+        return pass_estimate_ns(c, w, pts_u, pts_t, factor)
+
+    size0, dl0, cc0, _ = jobs[0]
+    counts = [int(x) for x in cc0[0]]
+    n = int(size0)
+    tight = int(dl0)
+    m = 1
+    for size, dl, cc, _ in jobs[1:]:
+        if n + size > cap:
+            break
+        c2 = [a + int(b) for a, b in zip(counts, cc[0])]
+        e2 = est(c2)
+        if now_ns + e2 > min(tight, int(dl)) * 1000 or (max_pass_ns >= 0 and e2 > max_pass_ns):
+            break
+        counts, n, tight, m = c2, n + int(size), min(tight, int(dl)), m + 1
+    e_mem = est(counts)
+    rest = jobs[m:]
+    rest_counts = [0] * K
+    for _, _, cc, _ in rest:
+        rest_counts = [a + int(b) for a, b in zip(rest_counts, cc[0])]
+    rest_fast = est(rest_counts) if rest else 0
+    rest_dl = None
+    for _, dl, _, _ in rest:
+        if int(dl) * 1000 >= now_ns + e_mem + rest_fast:
+            rest_dl = int(dl) if rest_dl is None else min(rest_dl, int(dl))
+
+    def feasible(e):
+        if now_ns + e > tight * 1000:
+            return False
+        if rest_dl is not None and now_ns + e + rest_fast > rest_dl * 1000:
+            return False
+        return max_pass_ns < 0 or e <= max_pass_ns
+
+    choice = [0] * m
+    moved = True
+    while moved:
+        moved = False
+        for j in range(m):
+            cc = jobs[j][2]
+            cur = choice[j]
+            base = [a - int(b) for a, b in zip(counts, cc[cur])]
+            best = -1
+            for c in range(cur + 1, len(cc)):
+                if feasible(est([a + int(b) for a, b in zip(base, cc[c])])):
+                    best = c
+            if best > cur:
+                choice[j] = best
+                counts = [a + int(b) for a, b in zip(base, cc[best])]
+                moved = True
+    masks = []
+    for j in range(m):
+        masks.extend(int(x) for x in jobs[j][3][choice[j]])
+    return m, choice, est(counts), counts, masks

@@ -708,7 +708,7 @@ using namespace mosel;
 
 extern "C" {
 
-int ms_abi_version(void) { return 3; }
+int ms_abi_version(void) { return 4; }
 int ms_set_pdl(int enable) {
   const int prev = g_pdl;
   g_pdl = enable ? 1 : 0;

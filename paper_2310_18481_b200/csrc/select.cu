@@ -7,6 +7,7 @@
 //     prefix sums), inverse maps, a stable counting sort by combo
 //     (strategy.py:54-60 canonical order), and vectorised row gathers into
 //     contiguous modality-grouped sub-batches.
+#include <climits>
 #include <cstdint>
 
 #include <type_traits>
@@ -59,6 +60,251 @@ __global__ void policy_select_kernel(const int64_t* __restrict__ lat_us, const i
     out = best;  // optimum then try_upgrade: largest est <= B
   }
   choice[job] = out;
+}
+
+// ------------------------------------------------------ pass-level selection
+// ms_pass_select (mosel_b200.h): one warp per pass-formation problem.  The
+// per-member step is P5's argmax (policy_select_kernel above) over PASS
+// estimates: lane c evaluates "the pass with this job at candidate c", the
+// ballot's highest feasible bit is the choice.  Work u is linear in the
+// counts, so a candidate is staged as its work u (int) in shared memory and
+// a member's move changes the pass work by u_new - u_old.
+
+constexpr int kPassStage = 7168;  // staged member candidates (28 KB); beyond: recomputed from global
+
+__device__ __forceinline__ long long pass_raw_ns(long long u, const MsPassCost& c) {
+  if (c.n_pts == 1 || u <= c.u[0]) return c.t_ns[0];
+  int i = 0;
+  while (i + 2 < c.n_pts && u > c.u[i + 1]) ++i;
+  return c.t_ns[i] + (c.t_ns[i + 1] - c.t_ns[i]) * (u - c.u[i]) / (c.u[i + 1] - c.u[i]);
+}
+
+// round_half_even(raw * factor): one fp64 multiply, as Python's round(int * float)
+__device__ __forceinline__ long long pass_est_ns(long long u, const MsPassCost& c, double factor) {
+  return __double2ll_rn(__dmul_rn((double)pass_raw_ns(u, c), factor));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T y = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += y;
+  }
+  return v;
+}
+
+__device__ __forceinline__ long long warp_incl_min(long long v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const long long y = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v = min(v, y);
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  return v;
+}
+
+__global__ void __launch_bounds__(32)
+    pass_select_kernel(const int32_t* __restrict__ prob_job_off, const int32_t* __restrict__ prob_n_jobs,
+                       const int64_t* __restrict__ prob_now_us, const double* __restrict__ prob_factor,
+                       const int32_t* __restrict__ job_size, const int64_t* __restrict__ job_deadline_us,
+                       const int32_t* __restrict__ job_n_cand, const int32_t* __restrict__ job_cand_off,
+                       const int32_t* __restrict__ job_mask_off, const int16_t* __restrict__ cand_counts,
+                       const uint16_t* __restrict__ req_masks, const __grid_constant__ MsPassCost cost_p, int cap,
+                       long long max_pass_ns, int32_t* __restrict__ out_choice, int32_t* __restrict__ out_summary,
+                       int64_t* __restrict__ out_est_ns, uint16_t* __restrict__ out_mask, long long out_mask_ld) {
+  __shared__ MsPassCost cost;
+  __shared__ int s_choice[MS_PASS_MAX_MEMBERS];
+  __shared__ int s_ncand[MS_PASS_MAX_MEMBERS];
+  __shared__ int s_uoff[MS_PASS_MAX_MEMBERS + 1];
+  __shared__ int s_roff[MS_PASS_MAX_MEMBERS + 1];
+  __shared__ int s_u[kPassStage];
+  const int p = blockIdx.x, lane = threadIdx.x;
+  {
+    const int* src = reinterpret_cast<const int*>(&cost_p);
+    int* dst = reinterpret_cast<int*>(&cost);
+    for (int i = lane; i < (int)(sizeof(MsPassCost) / 4); i += 32) dst[i] = src[i];
+  }
+  __syncwarp();
+  const int K = cost.K;
+  const int j0 = prob_job_off[p], Q = prob_n_jobs[p];
+  const long long now_ns = (long long)prob_now_us[p] * 1000;
+  const double f = prob_factor[p];
+  int32_t* summ = out_summary + (long long)p * MS_PASS_SUMMARY;
+  if (Q <= 0) {
+    if (lane < MS_PASS_SUMMARY) summ[lane] = 0;
+    if (lane == 0) out_est_ns[p] = 0;
+    return;
+  }
+  // work of job j's candidate c, from the (global or mapped host) count table
+  auto cand_u = [&](int j, int c) -> int {
+    const int16_t* cc = cand_counts + (long long)(job_cand_off[j] + c) * K;
+    int u = 0;
+    for (int k = 0; k < K; ++k) u += cost.w[k] * (int)cc[k];
+    return u;
+  };
+
+  // ---- 1. membership: prefix scans over the queue, 32 jobs per step
+  long long u_mem = cand_u(j0, 0);
+  int n = job_size[j0];
+  long long tight = job_deadline_us[j0];
+  int M = Q;
+  for (int base = 1; base < Q; base += 32) {
+    const int j = base + lane;
+    const bool valid = j < Q;
+    const int s = valid ? job_size[j0 + j] : 0;
+    const long long d = valid ? (long long)job_deadline_us[j0 + j] : LLONG_MAX;
+    const long long u = valid ? cand_u(j0 + j, 0) : 0;
+    const int n_j = n + warp_incl_scan(s, lane);
+    const long long u_j = u_mem + warp_incl_scan(u, lane);
+    const long long t_j = min(tight, warp_incl_min(d, lane));
+    bool fail = !valid || n_j > cap;
+    if (!fail) {
+      const long long e = pass_est_ns(u_j, cost, f);
+      fail = now_ns + e > t_j * 1000 || (max_pass_ns >= 0 && e > max_pass_ns);
+    }
+    const unsigned bal = __ballot_sync(kFull, fail);
+    const int last = bal ? __ffs(bal) - 2 : 31;  // last member lane of this step (-1: none)
+    if (last >= 0) {
+      n = __shfl_sync(kFull, n_j, last);
+      u_mem = __shfl_sync(kFull, u_j, last);
+      tight = __shfl_sync(kFull, t_j, last);
+    }
+    if (bal) {
+      M = base + last + 1;
+      break;
+    }
+  }
+  const long long e_mem = pass_est_ns(u_mem, cost, f);
+
+  // ---- 2. the jobs left queued: fastest-pass work and the earliest deadline it can still meet
+  long long rest_u = 0;
+  for (int j = M + lane; j < Q; j += 32) rest_u += cand_u(j0 + j, 0);
+  rest_u = warp_sum(rest_u);
+  const long long rest_fast = M < Q ? pass_est_ns(rest_u, cost, f) : 0;
+  long long rest_dl = LLONG_MAX;  // none
+  for (int j = M + lane; j < Q; j += 32) {
+    const long long d = job_deadline_us[j0 + j];
+    if (d * 1000 >= now_ns + e_mem + rest_fast) rest_dl = min(rest_dl, d);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) rest_dl = min(rest_dl, __shfl_xor_sync(kFull, rest_dl, d));
+
+  // ---- stage the members' frontiers (work per candidate) and request offsets
+  for (int base = 0; base < M; base += 32) {
+    const int j = base + lane;
+    const int nc = j < M ? job_n_cand[j0 + j] : 0;
+    const int sz = j < M ? job_size[j0 + j] : 0;
+    const int nc_incl = warp_incl_scan(nc, lane), sz_incl = warp_incl_scan(sz, lane);
+    const int nc_base = base ? s_uoff[base] : 0, sz_base = base ? s_roff[base] : 0;
+    __syncwarp();
+    if (j < M) {
+      s_ncand[j] = nc;
+      s_choice[j] = 0;
+      s_uoff[j + 1] = nc_base + nc_incl;
+      s_roff[j + 1] = sz_base + sz_incl;
+    }
+    if (base == 0 && lane == 0) s_uoff[0] = s_roff[0] = 0;
+    __syncwarp();
+  }
+  const int n_stage = s_uoff[M];
+  const bool staged = n_stage <= kPassStage;
+  if (staged) {
+    for (int t = lane; t < n_stage; t += 32) {  // flattened (member, candidate): independent loads
+      int lo = 0, hi = M - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_uoff[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+      s_u[t] = cand_u(j0 + lo, t - s_uoff[lo]);
+    }
+  }
+  __syncwarp();
+  auto U = [&](int j, int c) -> int { return staged ? s_u[s_uoff[j] + c] : cand_u(j0 + j, c); };
+
+  // ---- 3. upgrades: per member (EDF order) the largest feasible frontier index
+  const long long tight_ns = tight * 1000;
+  const long long rest_ns = rest_dl == LLONG_MAX ? LLONG_MAX : rest_dl * 1000;
+  long long u_cur = u_mem;
+  bool moved = true;
+  while (moved) {
+    moved = false;
+    for (int j = 0; j < M; ++j) {
+      const int nc = s_ncand[j], cur = s_choice[j];
+      if (cur + 1 >= nc) continue;
+      const long long ub = u_cur - U(j, cur);
+      int best = -1;
+      long long ubest = 0;
+      for (int c0 = cur + 1; c0 < nc; c0 += 32) {
+        const int c = c0 + lane;
+        bool ok = false;
+        long long uc = 0;
+        if (c < nc) {
+          uc = ub + U(j, c);
+          const long long e = pass_est_ns(uc, cost, f);
+          ok = now_ns + e <= tight_ns && (rest_ns == LLONG_MAX || now_ns + e + rest_fast <= rest_ns) &&
+               (max_pass_ns < 0 || e <= max_pass_ns);
+        }
+        const unsigned bal = __ballot_sync(kFull, ok);
+        if (bal) {
+          const int hb = 31 - __clz(bal);
+          best = c0 + hb;
+          ubest = __shfl_sync(kFull, uc, hb);
+        }
+      }
+      if (best > cur) {
+        __syncwarp();
+        if (lane == 0) s_choice[j] = best;
+        __syncwarp();
+        u_cur = ubest;
+        moved = true;
+      }
+    }
+  }
+
+  // ---- outputs: choices, summary (members, requests, counts), estimate, masks
+  int cnt[MS_PASS_MAX_K];
+#pragma unroll
+  for (int k = 0; k < MS_PASS_MAX_K; ++k) cnt[k] = 0;
+  for (int j = lane; j < Q; j += 32) {
+    const int ch = j < M ? s_choice[j] : -1;
+    out_choice[j0 + j] = ch;
+    if (ch >= 0) {
+      const int16_t* cc = cand_counts + (long long)(job_cand_off[j0 + j] + ch) * K;
+      for (int k = 0; k < K; ++k) cnt[k] += cc[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < MS_PASS_MAX_K; ++k) cnt[k] = warp_sum(cnt[k]);
+  const int n_req = s_roff[M];
+  if (lane == 0) {
+    summ[0] = M;
+    summ[1] = n_req;
+    out_est_ns[p] = pass_est_ns(u_cur, cost, f);
+  }
+  if (lane < MS_PASS_MAX_K) {
+    int v = 0;
+#pragma unroll
+    for (int k = 0; k < MS_PASS_MAX_K; ++k)
+      if (k == lane) v = cnt[k];
+    summ[2 + lane] = lane < K ? v : 0;
+  }
+  uint16_t* om = out_mask + (long long)p * out_mask_ld;
+  for (int r = lane; r < n_req; r += 32) {  // flattened requests: member by binary search
+    int lo = 0, hi = M - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_roff[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int sz = s_roff[lo + 1] - s_roff[lo];
+    om[r] = req_masks[job_mask_off[j0 + lo] + (long long)s_choice[lo] * sz + (r - s_roff[lo])];
+  }
 }
 
 // ---------------------------------------------------------------- compaction
@@ -154,14 +400,23 @@ __global__ void __launch_bounds__(kCompactThreads)
   }
 }
 
-// dst[j] = src[slot ? slot[idx[j]] : idx[j]], j < *count; blockIdx.y = row
+// source pool row of compacted position j: ring mode (n_ring > 0) walks the
+// pool ring from ring_base (the serving loop's per-modality input rings),
+// else the request's row through the optional slot map
+__device__ __forceinline__ int gather_src_row(int j, const int32_t* __restrict__ slot, const int32_t* __restrict__ idx,
+                                              int ring_base, int n_ring) {
+  if (n_ring > 0) return (int)(((long long)ring_base + j) % n_ring);
+  const int r = idx[j];
+  return slot ? slot[r] : r;
+}
+
+// dst[j] = src[row(j)], j < *count; blockIdx.y = row
 __global__ void gather_rows_kernel(const uint4* __restrict__ src, long long row_vecs, const int32_t* __restrict__ slot,
                                    const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
-                                   uint4* __restrict__ dst) {
+                                   uint4* __restrict__ dst, int ring_base, int n_ring) {
   const int n = *count;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
-    int r = idx[j];
-    if (slot) r = slot[r];
+    const int r = gather_src_row(j, slot, idx, ring_base, n_ring);
     const uint4* s = src + (long long)r * row_vecs;
     uint4* d = dst + (long long)j * row_vecs;
     const long long step = (long long)gridDim.x * blockDim.x;
@@ -200,7 +455,8 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
                                                               const int32_t* __restrict__ idx,
                                                               const int32_t* __restrict__ count,
                                                               void* __restrict__ dst_v, int frame_h, int pad_h,
-                                                              long long plane_vecs, int per_cap, int pdl_mode) {
+                                                              long long plane_vecs, int per_cap, int pdl_mode,
+                                                              int ring_base, int n_ring) {
   // PDL chain across one pass's gathers (ms_compact, pdl_mode 1 then 2): the first waits for the
   // index kernel, then lets the next gather start; later gathers start at
   // once and wait for their predecessor only before exiting, so gathers of
@@ -219,8 +475,7 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
   const int wd = width + 2 * pad_w;
   const long long dst_lines = frame_h > 0 ? lines + (lines / frame_h) * 2LL * pad_h : lines;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
-    int r = idx[j];
-    if (slot) r = slot[r];
+    const int r = gather_src_row(j, slot, idx, ring_base, n_ring);
     const unsigned char* srow = reinterpret_cast<const unsigned char*>(src_v) + (long long)r * lines * line_bytes;
     vec_t* drow = dst + (long long)j * dst_lines * wd * gv;
     const int per = min(per_cap, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
@@ -369,15 +624,15 @@ template <bool U8>
 __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, long long lines, int width, int c_src,
                                               int c_dst, int pad_w, float u8_scale, float u8_bias,
                                               const int32_t* __restrict__ slot, const int32_t* __restrict__ idx,
-                                              const int32_t* __restrict__ count, uint4* __restrict__ dst) {
+                                              const int32_t* __restrict__ count, uint4* __restrict__ dst,
+                                              int ring_base, int n_ring) {
   const int n = *count;
   const int g8 = c_dst / 8;
   const int wd = width + 2 * pad_w;
   const long long work = lines * wd * g8;
   const long long src_row = lines * width * c_src;
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
-    int r = idx[j];
-    if (slot) r = slot[r];
+    const int r = gather_src_row(j, slot, idx, ring_base, n_ring);
     uint4* d = dst + (long long)j * work;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < work;
          t += (long long)gridDim.x * blockDim.x) {
@@ -409,7 +664,8 @@ __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, lo
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
                              const int32_t* slot, const int32_t* idx, const int32_t* count, int max_rows, void* dst,
                              cudaStream_t st, int src_u8 = 0, float u8_scale = 1.0f, float u8_bias = 0.0f,
-                             int frame_h = 0, int pad_h = 0, long long plane_stride = 0, int pdl_mode = 0) {
+                             int frame_h = 0, int pad_h = 0, long long plane_stride = 0, int pdl_mode = 0,
+                             int ring_base = 0, int n_ring = 0) {
   if (c_dst % 4 != 0 || c_src > c_dst || c_src < 1 || pad_w < 0 || width < 1)
     return set_error(MS_ERR_INVALID, "gather: need 1 <= c_src <= c_dst, c_dst % 4 == 0, pad_w >= 0");
   if (frame_h < 0 || pad_h < 0 || (frame_h > 0 && lines % frame_h != 0))
@@ -422,7 +678,7 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     return set_error(MS_ERR_INVALID, "gather: planar output needs 12 destination channels, even padded width");
   if (line_bytes % 16 == 0 && line_bytes <= kMaxLineBytes) {
     static const int per_env = getenv("MS_GATHER_LINES") ? atoi(getenv("MS_GATHER_LINES")) : 0;  // A/B
-    const int per_cap = per_env > 0 ? per_env : 32;
+    const int per_cap = per_env > 0 && per_env < 32 ? per_env : 32;  // s_dline holds 32 lines
     const long long per = line_bytes > 0 ? (kMaxLineBytes / line_bytes < per_cap ? kMaxLineBytes / line_bytes : per_cap) : 1;
     long long bx = (lines + per - 1) / per;
     if (bx > 64) bx = 64;
@@ -432,16 +688,16 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     if (c_dst % 8 != 0) {  // 8-byte vector stores (4-channel groups)
       if (src_u8)
         launch_k(gather_rows_pad_kernel<true, 4>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                              idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
+                                                              idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode, ring_base, n_ring);
       else
         launch_k(gather_rows_pad_kernel<false, 4>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                               idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
+                                                               idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode, ring_base, n_ring);
     } else if (src_u8) {
       launch_k(gather_rows_pad_kernel<true, 8>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                            idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
+                                                            idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode, ring_base, n_ring);
     } else {
       launch_k(gather_rows_pad_kernel<false, 8>, grid, dim3(256), 0, st, 1, src, lines, width, c_src, c_dst, pad_w, sc, bi, slot,
-                                                             idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode);
+                                                             idx, count, dst, frame_h, pad_h, plane_stride / 4, per_cap, pdl_mode, ring_base, n_ring);
     }
   } else {
     if (c_dst % 8 != 0 || frame_h > 0)
@@ -452,16 +708,19 @@ static int gather_pad_launch(const void* src, long long lines, int width, int c_
     if (bx < 1) bx = 1;
     if (src_u8)
       gather_rows_pad_scalar_kernel<true><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-          src, lines, width, c_src, c_dst, pad_w, u8_scale, u8_bias, slot, idx, count, reinterpret_cast<uint4*>(dst));
+          src, lines, width, c_src, c_dst, pad_w, u8_scale, u8_bias, slot, idx, count, reinterpret_cast<uint4*>(dst),
+          ring_base, n_ring);
     else
       gather_rows_pad_scalar_kernel<false><<<dim3((unsigned)bx, (unsigned)gy), 256, 0, st>>>(
-          src, lines, width, c_src, c_dst, pad_w, 1.0f, 0.0f, slot, idx, count, reinterpret_cast<uint4*>(dst));
+          src, lines, width, c_src, c_dst, pad_w, 1.0f, 0.0f, slot, idx, count, reinterpret_cast<uint4*>(dst),
+          ring_base, n_ring);
   }
   return check_launch("gather_rows_pad_kernel");
 }
 
 static int gather_launch(const void* src, long long row_bytes, const int32_t* slot, const int32_t* idx,
-                         const int32_t* count, int max_rows, void* dst, cudaStream_t st) {
+                         const int32_t* count, int max_rows, void* dst, cudaStream_t st, int ring_base = 0,
+                         int n_ring = 0) {
   if (row_bytes % 16 != 0) return set_error(MS_ERR_INVALID, "row_bytes must be a multiple of 16");
   if (max_rows <= 0) return MS_OK;
   const long long vecs = row_bytes / 16;
@@ -471,7 +730,7 @@ static int gather_launch(const void* src, long long row_bytes, const int32_t* sl
   int gy = max_rows < 65535 ? max_rows : 65535;
   dim3 grid((unsigned)bx, (unsigned)gy);
   gather_rows_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), vecs, slot, idx, count,
-                                           reinterpret_cast<uint4*>(dst));
+                                           reinterpret_cast<uint4*>(dst), ring_base, n_ring);
   return check_launch("gather_rows_kernel");
 }
 
@@ -495,6 +754,37 @@ int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t
   policy_select_kernel<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       lat_us, n_cand, C, deadline_us, (long long)dispatch_us, factor, N, choice);
   return check_launch("policy_select_kernel");
+}
+
+int ms_pass_select(int n_prob, const int32_t* prob_job_off, const int32_t* prob_n_jobs,
+                   const int64_t* prob_now_us, const double* prob_factor, const int32_t* job_size,
+                   const int64_t* job_deadline_us, const int32_t* job_n_cand, const int32_t* job_cand_off,
+                   const int32_t* job_mask_off, const int16_t* cand_counts, const uint16_t* req_masks,
+                   const MsPassCost* cost, int cap, int64_t max_pass_ns, int32_t* out_choice,
+                   int32_t* out_summary, int64_t* out_est_ns, uint16_t* out_mask, long long out_mask_ld,
+                   void* stream) {
+  if (n_prob < 0) return set_error(MS_ERR_INVALID, "pass_select: n_prob must be >= 0");
+  if (n_prob == 0) return MS_OK;
+  if (!prob_job_off || !prob_n_jobs || !prob_now_us || !prob_factor || !job_size || !job_deadline_us ||
+      !job_n_cand || !job_cand_off || !job_mask_off || !cand_counts || !req_masks || !cost || !out_choice ||
+      !out_summary || !out_est_ns || !out_mask)
+    return set_error(MS_ERR_INVALID, "pass_select: null pointer");
+  if (cost->K < 1 || cost->K > MS_PASS_MAX_K) return set_error(MS_ERR_INVALID, "pass_select: K must be in 1..8");
+  if (cost->n_pts < 1 || cost->n_pts > MS_PASS_MAX_PTS)
+    return set_error(MS_ERR_INVALID, "pass_select: n_pts must be in 1..32");
+  for (int i = 0; i < cost->n_pts; ++i) {
+    if (cost->t_ns[i] < 0 || (i && (cost->u[i] <= cost->u[i - 1] || cost->t_ns[i] < cost->t_ns[i - 1])))
+      return set_error(MS_ERR_INVALID, "pass_select: knots must have increasing work and non-decreasing time");
+  }
+  for (int k = 0; k < cost->K; ++k)
+    if (cost->w[k] < 0) return set_error(MS_ERR_INVALID, "pass_select: negative work weight");
+  if (cap < 1 || cap > MS_PASS_MAX_MEMBERS) return set_error(MS_ERR_INVALID, "pass_select: cap must be in 1..1024");
+  if (out_mask_ld < cap) return set_error(MS_ERR_INVALID, "pass_select: out_mask_ld < cap");
+  pass_select_kernel<<<(unsigned)n_prob, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+           prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size, job_deadline_us, job_n_cand, job_cand_off,
+           job_mask_off, cand_counts, req_masks, *cost, cap, (long long)max_pass_ns, out_choice, out_summary,
+           out_est_ns, out_mask, out_mask_ld);
+  return check_launch("pass_select_kernel");
 }
 
 int ms_compact_index(const uint16_t* mask, int N, int K, int32_t* idx, int32_t* inv, int32_t* counts,
@@ -521,9 +811,9 @@ int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, i
                            reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
-               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
-               int32_t* combo_offsets, int32_t* perm, void* stream) {
+static int compact_impl(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+                        const int32_t* slot, const int32_t* ring_base, int n_ring, void* const* G, int32_t* idx,
+                        int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm, void* stream) {
   int rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -534,18 +824,36 @@ int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const M
     const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
     const bool framed = r.frame_h > 0 && r.pad_h > 0;
     const int32_t* sk = slot ? slot + r.slot_off : nullptr;  // per-modality pool rows
+    const int rb = n_ring > 0 ? ring_base[k] : 0;
     if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && r.plane_stride == 0 && bytes % 16 == 0) {
-      rc = gather_launch(X[k], bytes, sk, idx + (long long)k * N, counts + k, N, G[k], st);
+      rc = gather_launch(X[k], bytes, sk, idx + (long long)k * N, counts + k, N, G[k], st, rb, n_ring);
       chained = false;  // a plain launch ends the PDL chain (the next gather waits at its start again)
     } else {
       rc = gather_pad_launch(X[k], r.lines, r.width, r.c_src, r.c_dst, r.pad_w, sk, idx + (long long)k * N,
                              counts + k, N, G[k], st, r.src_u8, r.u8_scale, r.u8_bias, framed ? r.frame_h : 0,
-                             framed ? r.pad_h : 0, r.plane_stride, chained ? 2 : 1);
+                             framed ? r.pad_h : 0, r.plane_stride, chained ? 2 : 1, rb, n_ring);
       chained = true;
     }
     if (rc) return rc;
   }
   return MS_OK;
+}
+
+int ms_compact(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+               const int32_t* slot, void* const* G, int32_t* idx, int32_t* inv, int32_t* counts,
+               int32_t* combo_offsets, int32_t* perm, void* stream) {
+  return compact_impl(mask, N, K, X, rows, slot, nullptr, 0, G, idx, inv, counts, combo_offsets, perm, stream);
+}
+
+int ms_compact_ring(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+                    const int32_t* ring_base, int n_ring, void* const* G, int32_t* idx, int32_t* inv,
+                    int32_t* counts, int32_t* combo_offsets, int32_t* perm, void* stream) {
+  if (n_ring < 1 || !ring_base) return set_error(MS_ERR_INVALID, "compact_ring: need n_ring >= 1 and ring_base[K]");
+  for (int k = 0; k < K && k < kMaxK; ++k)
+    if (ring_base[k] < 0 || ring_base[k] >= n_ring)
+      return set_error(MS_ERR_INVALID, "compact_ring: ring_base out of range");
+  return compact_impl(mask, N, K, X, rows, nullptr, ring_base, n_ring, G, idx, inv, counts, combo_offsets, perm,
+                      stream);
 }
 
 }  // extern "C"

@@ -42,6 +42,31 @@ class RowDesc(C.Structure):
 
 
 _P, _I, _LL, _D = C.c_void_p, C.c_int, C.c_longlong, C.c_double
+
+PASS_MAX_K, PASS_MAX_PTS, PASS_MAX_MEMBERS = 8, 32, 1024
+PASS_SUMMARY = 2 + PASS_MAX_K
+
+
+class PassCost(C.Structure):
+    """MsPassCost: integer pass-time model of ms_pass_select (mosel_b200.h)."""
+    _fields_ = [("K", C.c_int), ("n_pts", C.c_int), ("w", C.c_int32 * PASS_MAX_K),
+                ("u", C.c_int64 * PASS_MAX_PTS), ("t_ns", C.c_int64 * PASS_MAX_PTS)]
+
+    @classmethod
+    def make(cls, w, u, t_ns):
+        c = cls()
+        c.K, c.n_pts = len(w), len(u)
+        if not (1 <= c.K <= PASS_MAX_K and 1 <= c.n_pts <= PASS_MAX_PTS and len(t_ns) == c.n_pts):
+            raise ValueError("PassCost: K in 1..8, 1..32 knots")
+        for i, v in enumerate(w):
+            c.w[i] = int(v)
+        for i, (a, b) in enumerate(zip(u, t_ns)):
+            c.u[i], c.t_ns[i] = int(a), int(b)
+        return c
+
+    def table(self):
+        """(w, u, t_ns) as Python int lists (the oracle's arguments)."""
+        return (list(self.w[: self.K]), list(self.u[: self.n_pts]), list(self.t_ns[: self.n_pts]))
 _SIGS = {
     "ms_abi_version": ([], C.c_int),
     "ms_set_pdl": ([_I], C.c_int),
@@ -55,6 +80,9 @@ _SIGS = {
     "ms_gather_rows": ([_P, _LL, _P, _P, _P, _I, _P, _P], C.c_int),
     "ms_gather_rows_pad": ([_P, _LL, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P], C.c_int),
     "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_compact_ring": ([_P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ms_pass_select": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, C.c_int64, _P, _P, _P, _P,
+                        _LL, _P], C.c_int),
     "ms_gemm_plan_dense": ([_P, _P, _I, _I, _LL, _P, _I, _I, _I, _P, _I, _I, _P, _LL, _I, _I, _P],
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
@@ -183,6 +211,17 @@ def policy_select(lat_us, credit, n_cand, deadline_us, dispatch_us: int, factor:
     if out is not None:
         return out
     return res.cpu().numpy()
+
+
+def pass_select(n_prob, prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size, job_deadline_us,
+                job_n_cand, job_cand_off, job_mask_off, cand_counts, req_masks, cost: PassCost, cap: int,
+                max_pass_ns: int, out_choice, out_summary, out_est_ns, out_mask, out_mask_ld: int, stream=None):
+    """ms_pass_select on raw addresses (device or pinned host memory): every
+    array argument is an integer address (``tensor.data_ptr()``)."""
+    check(lib().ms_pass_select(int(n_prob), prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size,
+                               job_deadline_us, job_n_cand, job_cand_off, job_mask_off, cand_counts, req_masks,
+                               C.byref(cost), int(cap), int(max_pass_ns), out_choice, out_summary, out_est_ns,
+                               out_mask, int(out_mask_ld), stream_ptr(stream)), "ms_pass_select")
 
 
 # -------------------------------------------------------------- compaction

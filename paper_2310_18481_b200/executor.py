@@ -51,6 +51,8 @@ def request_masks(parts, size: int) -> np.ndarray:
 class MaskedModel:
     """Encoders + fusion head + resident input pool + compaction buffers."""
 
+    STAGE_RING = 4
+
     def __init__(self, encoders, head, pools, rows, max_req: int, device="cuda"):
         """``rows[k] = (lines, width, c_src, c_dst, pad_w)``: one request of
         modality k is ``lines`` x ``width`` pixels of ``c_src`` channels in the
@@ -80,8 +82,18 @@ class MaskedModel:
         self.counts = torch.zeros(K, dtype=torch.int32, device=self.dev)
         self.offs = torch.zeros((1 << K) + 1, dtype=torch.int32, device=self.dev)
         self.perm = torch.zeros(n, dtype=torch.int32, device=self.dev)
-        self.mask_h = torch.zeros(n, dtype=torch.int16).pin_memory()
-        self.slot_h = torch.zeros(K * n, dtype=torch.int32).pin_memory()
+        # pinned staging ring for stage_inputs: slot i is rewritten only after
+        # the H2D copies that last read it have executed (its event)
+        self._stage_h = [(torch.zeros(n, dtype=torch.int16).pin_memory(),
+                          torch.zeros(K * n, dtype=torch.int32).pin_memory(), torch.cuda.Event())
+                         for _ in range(self.STAGE_RING)]
+        self._stage_i = 0
+        # device mask ring for passes formed on the device (ms_pass_select
+        # writes row i, the pass's compaction reads it; ring_ev[i] is recorded
+        # after that compaction so the next writer of row i can wait on it)
+        self.mask_ring = torch.zeros(self.STAGE_RING, n, dtype=torch.int16, device=self.dev)
+        self.ring_ev = [torch.cuda.Event() for _ in range(self.STAGE_RING)]
+        self.ring_used = [False] * self.STAGE_RING
         import ctypes
         self._X = (ctypes.c_void_p * K)(*[p.data_ptr() for p in pools])
         self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
@@ -104,21 +116,26 @@ class MaskedModel:
 
     def stage_inputs(self, slots, masks, stream=None):
         """Copy one batch's slots/masks into the fixed device buffers (H2D
-        from pinned memory; stream-ordered)."""
+        from a pinned staging ring; stream-ordered).  The host rewrites a
+        staging slot only after the copies that last read it have run."""
         n = len(masks)
         if n > self.max_req:
             raise ValueError(f"batch of {n} exceeds capacity {self.max_req}")
-        self.mask_h[:n] = self.torch.as_tensor(np.asarray(masks, dtype=np.int16))
+        mask_h, slot_h, ev = self._stage_h[self._stage_i]
+        self._stage_i = (self._stage_i + 1) % len(self._stage_h)
+        ev.synchronize()
+        mask_h[:n] = self.torch.as_tensor(np.asarray(masks, dtype=np.int16))
         sl = np.asarray(slots, dtype=np.int32)
         if sl.ndim == 1:  # the same pool row for every modality
             sl = np.broadcast_to(sl, (self.K, n))
-        sh = self.slot_h.numpy().reshape(self.K, self.max_req)
+        sh = slot_h.numpy().reshape(self.K, self.max_req)
         sh[:, :n] = sl
         s = stream or self.torch.cuda.current_stream()
         with self.torch.cuda.stream(s):
-            self.mask_d[:n].copy_(self.mask_h[:n], non_blocking=True)
-            self.slot_d.view(self.K, self.max_req)[:, :n].copy_(self.slot_h.view(self.K, self.max_req)[:, :n],
+            self.mask_d[:n].copy_(mask_h[:n], non_blocking=True)
+            self.slot_d.view(self.K, self.max_req)[:, :n].copy_(slot_h.view(self.K, self.max_req)[:, :n],
                                                               non_blocking=True)
+            ev.record(s)
 
     # -- device pass ------------------------------------------------------
     def _compact(self, n: int):
@@ -127,6 +144,18 @@ class MaskedModel:
                               self.slot_d.data_ptr(), self._G, self.idx.data_ptr(),
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
                               self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
+
+    def _compact_ring(self, n: int, mask_ptr: int, bases):
+        """Compaction of a pass whose masks are already on the device
+        (``mask_ptr``), modality k's compacted rows read from the pool ring
+        at ``bases[k]`` (ms_compact_ring)."""
+        import ctypes
+        L = dv.lib()
+        rb = (ctypes.c_int32 * self.K)(*[int(b) for b in bases])
+        dv.check(L.ms_compact_ring(mask_ptr, n, self.K, self._X, self._ROWS, rb, self.n_slots, self._G,
+                                   self.idx.data_ptr(), self.inv.data_ptr(), self.counts.data_ptr(),
+                                   self.offs.data_ptr(), self.perm.data_ptr(), dv.stream_ptr()),
+                 "ms_compact_ring")
 
     def _head(self, n: int):
         inv = self.inv[: self.K * n].view(self.K, n)
@@ -162,14 +191,33 @@ class MaskedModel:
             self._graphs[key] = g
         return g
 
-    def run_staged(self, n: int, counts):
+    def run_ring(self, n: int, counts, slot: int, bases):
+        """One pass formed on the device: masks in ``mask_ring[slot]``
+        (written by ms_pass_select), pool rows from the per-modality rings
+        at ``bases``; ``ring_ev[slot]`` marks the row free again."""
+        ptr = self.mask_ring[slot].data_ptr()
+
+        def compact():
+            self._compact_ring(n, ptr, bases)
+            self.ring_ev[slot].record()
+            self.ring_used[slot] = True
+
+        self.run_staged(n, counts, compact=compact)
+
+    def run_staged(self, n: int, counts, compact=None):
         """Compaction (direct launches), then one graph per present
         modality's encoder (keyed by its compacted count) and one for the
         fusion head (keyed by n): O(K * max_req) captures in total."""
+        if compact is None:
+            compact = lambda: self._compact(n)  # noqa: E731
         if not self.use_graphs:
-            self._launch(n, counts)
+            compact()
+            for enc, nk in zip(self.encoders, counts):
+                if nk:
+                    enc.program(nk).run()
+            self._head(n).run()
             return
-        self._compact(n)
+        compact()
         torch = self.torch
         main = torch.cuda.current_stream()
         present = [k for k, nk in enumerate(counts) if nk]

@@ -130,6 +130,20 @@ class PassCostModel:
         r = observed_us / max(1.0, self.raw_us(counts, n))
         self.factor = (1.0 - self.weight) * self.factor + self.weight * r
 
+    def device_table(self):
+        """The integer pass-time model ``ms_pass_select`` evaluates
+        (``dv.PassCost``): per-request work of modality k in 1/1024 of an
+        all-modality request (``work_w``), and the measured all-modality
+        passes as knots (work, ns), non-decreasing; below the first knot the
+        first time (this model's ``max(1, work)`` clamp), past the last the
+        last segment extrapolated."""
+        if len(self.pass_all) < 1:
+            raise ValueError("device_table needs measured whole passes (profile_pass_costs)")
+        w = [int(round(x * 1024)) for x in self.work_w]
+        u = [int(n) * 1024 for n, _ in self.pass_all]
+        t = np.maximum.accumulate([int(round(v * 1000.0)) for _, v in self.pass_all]).tolist()
+        return dv.PassCost.make(w, u, t)
+
     def to_json(self):
         return {"enc_us": self.enc_us, "head_us": self.head_us, "compact_us": self.compact_us,
                 "pass_all_us": self.pass_all, "work_w": self.work_w}

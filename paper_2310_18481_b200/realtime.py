@@ -46,6 +46,9 @@ class ServeStats:
     late: int = 0              # requests completed after their deadline
     wall_s: float = 0.0
     trace: list | None = None  # optional per-pass diagnostics (serve_realtime(trace=True))
+    policy_launches: int = 0   # ms_pass_select launches (device policy step)
+    policy_device_us: float = 0.0
+    formations: list | None = None
 
 
 class HostClips:
@@ -62,7 +65,8 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                    window_us: int = 4_000_000, depth: int = 2, cost=None,
                    max_batch_requests: int | None = None, lead_us: int = 600, trace: bool = False,
                    sched_margin_us: int = 0, policy_grid_us: int = 1000, policy_at_dispatch: bool = False,
-                   device_policy=None, selection: str = "policy", max_pass_us: float | None = None):
+                   device_policy=None, selection: str = "policy", max_pass_us: float | None = None,
+                   record_formations: bool = False):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -97,20 +101,27 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
     policy on the GPU (one launch per pass).
 
     ``selection="pass"`` (needs ``cost``; extension for the batched executor):
-    the per-request modality-subset choice is made when a pass is formed,
-    against the measured cost of THAT pass -- the north_star's policy step
-    (argmax accuracy under the request's remaining latency budget, SURVEY
-    §8a P5) with the budget coupled through the shared pass:
+    the per-request modality-subset choice is made on the DEVICE when a pass
+    is formed, against the measured cost of THAT pass: ``ms_pass_select``
+    (``batcher.DevicePassSelector``; restated by oracle/selection.py
+    pass_select) -- the north_star's policy step (P5's argmax accuracy under
+    the request's remaining latency budget) with the budget
+    coupled through the shared pass:
       1. membership: queued jobs join in EDF order at their FASTEST frontier
          candidate while the pass estimate meets every member's deadline;
-      2. upgrades: each member (EDF order, repeatedly) climbs its frontier
-         while the pass still meets every member's deadline AND the jobs left
-         queued could still meet theirs in one following all-fastest pass.
-    Idle GPU -> everyone at top accuracy; under load -> modalities dropped
-    exactly as far as the deadlines require.  ``max_pass_us`` caps a pass's
-    estimate in both steps (requests arriving during a pass wait for it and
-    then for their own: a pass of about half the deadline keeps them on
-    time).  The reference policies (``policy``) are not run in this mode.
+      2. upgrades: each member (EDF order, repeatedly) moves to the most
+         accurate candidate whose pass still meets every member's deadline
+         AND lets the jobs left queued meet theirs in one following
+         all-fastest pass.
+    The kernel writes the pass's per-request masks into the device mask ring
+    the compaction reads, and every modality's clips come from its pool ring
+    (``ms_compact_ring``): no per-request host staging.  Idle GPU ->
+    everyone at top accuracy; under load -> modalities dropped exactly as far
+    as the deadlines require.  ``max_pass_us`` caps a pass's estimate in both
+    steps (requests arriving during a pass wait for it and then for their
+    own).  The reference policies (``policy``) are not run in this mode.
+    ``record_formations``: keep every formation's inputs and outputs
+    (``stats.formations``) for the oracle replay.
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
@@ -160,6 +171,16 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         since_opt = 0
 
     cap = min(max_batch_requests or model.max_req, model.max_req)
+    selector = fcache = None
+    if selection == "pass":
+        if cost is None:
+            raise ValueError("selection='pass' needs a PassCostModel (cost=)")
+        from .batcher import DevicePassSelector, FrontierCache
+        fcache = FrontierCache(matrix, model.K)
+        selector = DevicePassSelector(model.K, cost.device_table(), cap,
+                                      -1 if max_pass_us is None else int(round(max_pass_us * 1000)),
+                                      model.mask_ring, record=record_formations)
+    ring_i = 0
 
     def counts_of(masks):
         m = masks.astype(np.int64)
@@ -202,63 +223,67 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                 j.est_finish_us = now + int(round(est_us))
         return launch(now, batch, mlist, counts, n, est_us)
 
-    def cand_counts(j, idx):
-        """(masks, per-modality counts) of job j at frontier candidate idx (cached)."""
-        cache = getattr(j, "_cand_counts", None)
-        if cache is None:
-            cache = j._cand_counts = {}
-        if idx not in cache:
-            m = request_masks(j.candidates[idx].strategy.parts, j.size)
-            cache[idx] = (m, counts_of(m))
-        return cache[idx]
-
     def dispatch_pass_select(now, head):
-        batch = [head]
-        head.assigned_idx = 0
-        counts = list(cand_counts(head, 0)[1])
-        n = head.size
-        tight = head.deadline_us
-        for cand in list(queue._jobs):  # 1. membership at the fastest candidates
-            if n + cand.size > cap:
-                break
-            c2 = [a + b for a, b in zip(counts, cand_counts(cand, 0)[1])]
-            e2 = cost.estimate_us(c2, n + cand.size)
-            if now + e2 > min(tight, cand.deadline_us) or (max_pass_us is not None and e2 > max_pass_us):
-                break
-            queue.remove(cand)
-            cand.state = JobState.RUNNING
-            cand.assigned_idx = 0
-            batch.append(cand)
-            counts, n = c2, n + cand.size
-            tight = min(tight, cand.deadline_us)
-        est = cost.estimate_us(counts, n)
-        rest = queue.jobs()
-        rest_counts = [0] * model.K
-        rest_n = 0
-        for j in rest:
-            rest_counts = [a + b for a, b in zip(rest_counts, cand_counts(j, 0)[1])]
-            rest_n += j.size
-        rest_fast = cost.estimate_us(rest_counts, min(rest_n, model.max_req)) if rest_n else 0.0
-        # the queued jobs that one following all-fastest pass can still serve on time
-        rest_dl = min((j.deadline_us for j in rest if j.deadline_us >= now + est + rest_fast), default=None)
-        moved = True
-        while moved:  # 2. upgrades
-            moved = False
-            for j in batch:
-                while j.assigned_idx + 1 < len(j.candidates):
-                    old = cand_counts(j, j.assigned_idx)[1]
-                    new = cand_counts(j, j.assigned_idx + 1)[1]
-                    c2 = [a - b + c for a, b, c in zip(counts, old, new)]
-                    e2 = cost.estimate_us(c2, n)
-                    if now + e2 > tight or (rest_dl is not None and now + e2 + rest_fast > rest_dl) or \
-                            (max_pass_us is not None and e2 > max_pass_us):
-                        break
-                    j.assigned_idx += 1
-                    counts, est, moved = c2, e2, True
-        for j in batch:
-            j.est_finish_us = now + int(round(est))
-        mlist = [cand_counts(j, j.assigned_idx)[0] for j in batch]
-        return launch(now, batch, mlist, counts, n, est)
+        """Form the pass on the device (ms_pass_select) and launch it."""
+        nonlocal ring_i
+        slot = ring_i % len(model.ring_ev)
+        ring_i += 1
+        t = time.perf_counter()
+        r = selector.select([head] + queue._jobs, now, cost.factor, slot,
+                            slot_free=model.ring_ev[slot] if model.ring_used[slot] else None)
+        stats.policy_host_us += (time.perf_counter() - t) * 1e6
+        stats.policy_runs += 1
+        batch = [head] + queue.pop_front(r.members - 1)
+        fin = now + (r.est_ns + 500) // 1000
+        for j, c in zip(batch, r.choices):
+            j.assigned_idx = int(c)
+            j.state = JobState.RUNNING
+            j.est_finish_us = fin
+        q = len(batch) + len(queue)
+        stats.h2d_bytes += 24 * q + 32  # the kernel reads the pinned job tables in place (mapped)
+        stats.d2h_bytes += 4 * q + 4 * (2 + model.K) + 8
+        return launch_ring(now, batch, r.counts, r.requests, r.est_ns / 1000.0, slot)
+
+    def launch_ring(now, batch, counts, n, est_us, slot):
+        """A device-formed pass: masks already in model.mask_ring[slot];
+        modality k's clips are the next counts[k] rows of its pool ring (the
+        host-IO path first DMAs exactly those rows from pinned memory)."""
+        ns = model.n_slots
+        bases = list(rings)
+        ev_s, ev_e = dv.Event(), dv.Event()
+        if host_clips is not None:
+            with torch.cuda.stream(copy_stream):
+                for k in range(model.K):
+                    c = counts[k]
+                    if not c:
+                        continue
+                    r0 = bases[k]
+                    first = min(c, ns - r0)
+                    model.pools[k][r0:r0 + first].copy_(host_clips.host[k][r0:r0 + first], non_blocking=True)
+                    if first < c:
+                        model.pools[k][: c - first].copy_(host_clips.host[k][: c - first], non_blocking=True)
+                    stats.h2d_bytes += c * host_clips.row_bytes[k]
+            stream.wait_stream(copy_stream)
+        for k in range(model.K):
+            rings[k] = (bases[k] + counts[k]) % ns
+        ev_s.record()
+        model.run_ring(n, counts, slot, bases)
+        if host_clips is not None:
+            logits_host[:n].copy_(model.head.logits[:n], non_blocking=True)
+            stats.d2h_bytes += n * model.head.logits.shape[1] * 4
+        ev_e.record()
+        stats.gpu_launches += model.launches_per_pass(tuple(counts)) + 1  # + ms_pass_select
+        stats.passes += 1
+        stats.requests += n
+        preds = [[profile.part_latency_us(m, b) for m, b in j.assigned.strategy.parts] for j in batch]
+        if stats.trace is not None:
+            stats.trace.append({"pass": stats.passes - 1, "host_us": now_us(), "dispatch_us": now, "n": n,
+                                "jobs": [j.id for j in batch], "est_us": est_us, "queue": len(queue),
+                                "queued_req": sum(j.size for j in queue._jobs), "counts": list(counts),
+                                "bases": bases})
+        inflight.append((batch, ev_s, ev_e, preds, tuple(counts), n))
+        queue.running = batch[-1]
+        return True
 
     def launch(now, batch, mlist, counts, n, est_us):
         masks = np.concatenate(mlist)
@@ -348,8 +373,12 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         while pos < len(pending) and pending[pos][1].arrival_us <= now:
             jid, tpl = pending[pos]
             pos += 1
-            cands = candidates_with_rounding(matrix, tpl.size, tpl.accuracy_slo)
+            if selector is not None:
+                cands, pack = fcache.lookup(tpl.size, tpl.accuracy_slo)
+            else:
+                cands, pack = candidates_with_rounding(matrix, tpl.size, tpl.accuracy_slo), None
             job = Job(jid, tpl.arrival_us, tpl.size, tpl.accuracy_slo, tpl.deadline_us - sched_margin_us, cands)
+            job.pack = pack
             if not cands:
                 job.state = JobState.DROPPED
                 drop(job)
@@ -386,6 +415,11 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                 time.sleep((wait - 100) / 1e6)
     torch.cuda.synchronize()
     stats.wall_s = time.perf_counter() - t0
+    if selector is not None:
+        stats.policy_launches = selector.launches
+        stats.policy_device_us = selector.device_us
+        if record_formations:
+            stats.formations = selector.records
     log = MetricsLog(window_us, tuple(sorted(records, key=lambda r: r.id)))
     return log, stats
 

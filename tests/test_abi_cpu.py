@@ -42,7 +42,7 @@ def test_python_binding_covers_the_header(lib):
 
 def test_abi_version_and_error_plumbing(lib):
     from paper_2310_18481_b200 import device
-    assert lib.ms_abi_version() == 3
+    assert lib.ms_abi_version() == 4
     # invalid arguments are rejected before any CUDA call, with a message
     rc = lib.ms_policy_select(None, None, None, 0, None, 0, 1.0, 4, None, None)
     assert rc == 1
