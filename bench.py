@@ -269,7 +269,8 @@ def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, 
         log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f} "
             f"req/pass {st.requests / max(1, st.passes):.1f} late {st.late} drop(policy/dispatch/admit) "
             f"{st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} policy host {st.policy_host_us / max(1, st.policy_runs):.0f}us "
-            f"x{st.policy_runs}, device pass_select {st.policy_device_us / max(1, st.policy_launches):.1f}us x{st.policy_launches}")
+            f"x{st.policy_runs}, device pass_select {st.policy_device_us / max(1, st.policy_launches):.1f}us "
+            f"(kernel {st.policy_kernel_us / max(1, st.policy_launches):.1f}us) x{st.policy_launches}")
         if 0.005 < v <= 0.01:  # near the limit one Poisson burst decides a short window: confirm on a re-draw
             lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 2000 + it, max_size=max_size,
                            cost=cost)
@@ -506,6 +507,7 @@ def our_arm(args):
         "slo_met": bool(agg[0] >= 0.99 * agg[1]),
         "policy_step": {"kernel": "pass_select_kernel (ms_pass_select)", "launches": st.policy_launches,
                         "device_us_mean": round(st.policy_device_us / max(1, st.policy_launches), 2),
+                        "kernel_us_mean": round(st.policy_kernel_us / max(1, st.policy_launches), 2),
                         "host_us_mean": round(st.policy_host_us / max(1, st.policy_runs), 2),
                         "passes": st.passes},
         "requests_with_modalities_dropped": drop_share,

@@ -102,7 +102,9 @@ int ms_policy_select(const int64_t* lat_us, const int32_t* credit, const int32_t
  * counts[K]}; out_est_ns[p]; out_mask[p * out_mask_ld + r] = the pass's
  * per-request masks (members in order).  Inputs/outputs may be device or
  * pinned (mapped) host memory: the serving loop hands the kernel its pinned
- * staging buffers directly (no memcpy), only out_mask lives in HBM. */
+ * staging buffers directly (no memcpy), only out_mask lives in HBM.
+ * out_clock (may be NULL): [2p], [2p+1] = the problem's start / end on the
+ * device's global timer (ns) -- the kernel's own time, apart from queueing. */
 #define MS_PASS_MAX_K 8
 #define MS_PASS_MAX_PTS 32
 #define MS_PASS_MAX_MEMBERS 1024
@@ -119,7 +121,7 @@ int ms_pass_select(int n_prob, const int32_t* prob_job_off, const int32_t* prob_
                    const int32_t* job_mask_off, const int16_t* cand_counts, const uint16_t* req_masks,
                    const MsPassCost* cost, int cap, int64_t max_pass_ns, int32_t* out_choice,
                    int32_t* out_summary, int64_t* out_est_ns, uint16_t* out_mask, long long out_mask_ld,
-                   void* stream);
+                   int64_t* out_clock, void* stream);
 
 /* ms_strategy_dp <- strategy.py:139-177 _DpTables (offline stage, SURVEY
  * §8f #2): the exact min-latency / min-part-count table over (requests

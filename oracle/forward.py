@@ -15,8 +15,11 @@ is the frozen restatement they are checked against:
 * the device stores every activation in bf16, so the oracle rounds to bf16
   at exactly those points (conv+ReLU outputs, pool outputs, the segment
   consensus features, the fusion hidden layer) and nowhere else;
-* weights come from the model definition's seeded generators
-  (``encoders.*_weights``), i.e. the same numbers, not the same code path.
+* the BN-Inception layer table and every weight generator are restated in
+  ``oracle/bninception.py`` independently of the product (Ioffe & Szegedy
+  2015 as TSN ships it; the paper's own widths reproduce SURVEY Appendix C's
+  MAC counts), so a wrong product layer table or weight order fails parity;
+  only the configs[2] towers still take their weights from the product.
 
 Missing-modality rule (builder contract): a request's absent
 modality contributes a zero block to the concat, i.e. its FC1 columns are
@@ -28,8 +31,11 @@ from __future__ import annotations
 import torch
 import torch.nn.functional as F
 
-from paper_2310_18481_b200.encoders import (FEAT_DIM, bninception_layers, bninception_weights,
-                                            fusion_weights, mlp_weights)
+from oracle import bninception as bni
+
+FEAT_DIM = 1024
+N_CLASSES = 97 + 300  # EPIC-100 verbs + nouns
+FUSION_HIDDEN = 512
 
 
 def _bf(x):
@@ -41,37 +47,42 @@ def _conv(x, wb, s, p):
     return _bf(F.relu(F.conv2d(x, w.float(), b, stride=s, padding=p)))
 
 
-def bninception_forward(frames, weights, cin: int, size: int):
+def bninception_forward(frames, weights, cin: int, size: int, table=bni.TSN):
     """frames: float tensor [n, cin, H, W] (bf16-representable values).
-    Returns per-frame features after global average pooling, fp32 [n, 1024]
-    (not yet rounded)."""
+    Returns per-frame feature maps after the last block, fp32 [n, 1024, h, w]
+    (not yet pooled or rounded)."""
     x = frames.float()
-    for L in bninception_layers(cin, size):
-        k = L["kind"]
-        if k == "conv":
-            x = _conv(x, weights[L["name"]], L["s"], L["p"])
-        elif k == "pool":
-            x = F.max_pool2d(x, L["k"], L["s"], L["p"], ceil_mode=L["ceil"])
-        elif k == "block":
-            n, s = L["name"], L["s"]
-            outs = []
-            if L["c1"]:
-                outs.append(_conv(x, weights[n + "/1x1"], 1, 0))
-            t = _conv(x, weights[n + "/3x3_reduce"], 1, 0)
-            outs.append(_conv(t, weights[n + "/3x3"], s, 1))
-            t = _conv(x, weights[n + "/d3x3_reduce"], 1, 0)
-            t = _conv(t, weights[n + "/d3x3_a"], 1, 1)
-            outs.append(_conv(t, weights[n + "/d3x3_b"], s, 1))
-            if L["pool"] == "avg":
-                pooled = _bf(F.avg_pool2d(x, 3, 1, 1, count_include_pad=True))
-                outs.append(_conv(pooled, weights[n + "/pool_proj"], 1, 0))
-            elif L["pool"] == "maxproj":
-                pooled = F.max_pool2d(x, 3, 1, 1)
-                outs.append(_conv(pooled, weights[n + "/pool_proj"], 1, 0))
-            else:
-                outs.append(F.max_pool2d(x, 3, 2, 0, ceil_mode=True))
-            x = torch.cat(outs, 1)
+    for layer in bni.stem(cin):
+        if len(layer) == 1:  # 3x3/2 max pool, ceil mode
+            x = F.max_pool2d(x, 3, 2, 0, ceil_mode=True)
+        else:
+            name, _, _, k, s, p = layer
+            x = _conv(x, weights[name], s, p)
+    for n in bni.ORDER:
+        c1, c3r, c3, cdr, cd, pk, proj, s = table[n]
+        outs = []
+        if c1:
+            outs.append(_conv(x, weights[n + "/1x1"], 1, 0))
+        t = _conv(x, weights[n + "/3x3_reduce"], 1, 0)
+        outs.append(_conv(t, weights[n + "/3x3"], s, 1))
+        t = _conv(x, weights[n + "/d3x3_reduce"], 1, 0)
+        t = _conv(t, weights[n + "/d3x3_a"], 1, 1)
+        outs.append(_conv(t, weights[n + "/d3x3_b"], s, 1))
+        if pk == "avg":
+            pooled = _bf(F.avg_pool2d(x, 3, 1, 1, count_include_pad=True))
+            outs.append(_conv(pooled, weights[n + "/pool_proj"], 1, 0))
+        elif pk == "maxproj":
+            outs.append(_conv(F.max_pool2d(x, 3, 1, 1), weights[n + "/pool_proj"], 1, 0))
+        else:
+            outs.append(F.max_pool2d(x, 3, 2, 0, ceil_mode=True))
+        x = torch.cat(outs, 1)
     return x
+
+
+def fusion_weights(n_mod: int, feat_dim: int, seed: int, n_classes: int = N_CLASSES):
+    """FC1 (n_mod*feat_dim -> 512, He) + head (512 -> n_classes, LeCun)."""
+    (w1, b1), (w2, b2) = bni.dense_weights((n_mod * feat_dim, FUSION_HIDDEN, n_classes), seed, scale_last=1)
+    return w1, b1, w2, b2
 
 
 def encode_requests(clips, weights, cin: int, size: int, segments: int):
@@ -114,7 +125,7 @@ class OracleTBN:
     def __init__(self, modalities, seeds, fusion_seed: int, segments: int):
         self.mods = modalities
         self.S = segments
-        self.enc_w = [bninception_weights(m.channels, m.size, s) for m, s in zip(modalities, seeds)]
+        self.enc_w = [bni.weights(m.channels, s) for m, s in zip(modalities, seeds)]
         self.fus_w = fusion_weights(len(modalities), FEAT_DIM, fusion_seed)
 
     def logits(self, clips_per_mod, masks):
@@ -136,7 +147,7 @@ class OracleMLP:
     """configs[0]: per-modality MLP towers + masked fusion head."""
 
     def __init__(self, in_dims, seeds, fusion_seed: int, hidden=(1024, 1024)):
-        self.towers = [mlp_weights((d,) + tuple(hidden), s) for d, s in zip(in_dims, seeds)]
+        self.towers = [bni.dense_weights((d,) + tuple(hidden), s) for d, s in zip(in_dims, seeds)]
         self.fus_w = fusion_weights(len(in_dims), hidden[-1], fusion_seed)
 
     def logits(self, inputs, masks):

@@ -209,18 +209,23 @@ def dropped_modalities(mask: int, n_modalities: int) -> int:
 # multiply, round half-even).
 
 
+SLOPE_SHIFT = 20
+
+
 def pass_raw_ns(u: int, pts_u, pts_t) -> int:
     """Piecewise-linear pass time (ns) at work ``u`` (1/1024-request units):
-    clamped to the first point below it, extrapolated past the last;
-    integer floor division (all terms non-negative)."""
+    clamped to the first knot below it, the first segment whose right knot is
+    >= u, the last segment extrapolated past it; each segment's slope is held
+    in 2^-20 ns per work unit, floor((dt << 20) / du), and applied with an
+    arithmetic shift (all terms non-negative)."""
     n = len(pts_u)
     if n == 1 or u <= pts_u[0]:
         return int(pts_t[0])
     i = 0
     while i + 2 < n and u > pts_u[i + 1]:
         i += 1
-    return int(pts_t[i]) + (int(pts_t[i + 1]) - int(pts_t[i])) * (u - int(pts_u[i])) // \
-        (int(pts_u[i + 1]) - int(pts_u[i]))
+    slope = ((int(pts_t[i + 1]) - int(pts_t[i])) << SLOPE_SHIFT) // (int(pts_u[i + 1]) - int(pts_u[i]))
+    return int(pts_t[i]) + (((u - int(pts_u[i])) * slope) >> SLOPE_SHIFT)
 
 
 def pass_estimate_ns(counts, w, pts_u, pts_t, factor: float) -> int:

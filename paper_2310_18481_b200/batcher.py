@@ -116,6 +116,8 @@ class DevicePassSelector:
         self._prob = torch.zeros(4, dtype=torch.int64).pin_memory()  # job_off, n_jobs (i32 x2), now, factor
         self._summary = torch.zeros(dv.PASS_SUMMARY, dtype=torch.int32).pin_memory()
         self._est = torch.zeros(1, dtype=torch.int64).pin_memory()
+        self._clock = torch.zeros(2, dtype=torch.int64).pin_memory()  # kernel start/end (device global timer)
+        self.kernel_us = 0.0
         self._grow(256, 4096, 16384)
 
     def _grow(self, jobs: int, rows: int, masks: int):
@@ -174,11 +176,13 @@ class DevicePassSelector:
                            self._ncand.data_ptr(), self._coff.data_ptr(), self._moff.data_ptr(), self._cc.data_ptr(),
                            self._rm.data_ptr(), self.cost, self.cap, self.max_pass_ns, self._choice.data_ptr(),
                            self._summary.data_ptr(), self._est.data_ptr(), self.mask_ring[slot].data_ptr(),
-                           self.mask_ring.shape[1], stream=self.stream)
+                           self.mask_ring.shape[1], stream=self.stream, out_clock=self._clock.data_ptr())
             self.ev1.record(self.stream)
         self.ev1.synchronize()
         self.launches += 1
         self.device_us += self.ev0.elapsed_time(self.ev1) * 1000.0
+        clk = self._clock.numpy()
+        self.kernel_us += (int(clk[1]) - int(clk[0])) / 1000.0
         summ = self._summary.numpy()
         m, n = int(summ[0]), int(summ[1])
         res = PassChoice(m, n, tuple(int(x) for x in summ[2:2 + self.K]), int(self._est.numpy()[0]),

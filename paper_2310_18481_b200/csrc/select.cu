@@ -67,21 +67,47 @@ __global__ void policy_select_kernel(const int64_t* __restrict__ lat_us, const i
 // per-member step is P5's argmax (policy_select_kernel above) over PASS
 // estimates: lane c evaluates "the pass with this job at candidate c", the
 // ballot's highest feasible bit is the choice.  Work u is linear in the
-// counts, so a candidate is staged as its work u (int) in shared memory and
-// a member's move changes the pass work by u_new - u_old.
+// counts, so a candidate is staged as its work u and a member's move changes
+// the pass work by u_new - u_old.
+//
+// The kernel is memory-latency bound (a few thousand instructions), so its
+// shape is "few dependent round trips": the first cap+32 jobs' fields land in
+// shared memory in one sweep, all their candidates' counts in a second
+// (independent flattened loads), the masks in a third -- the three phases
+// (membership, rest, upgrades) then run from shared memory.  Jobs past the
+// staged window (a queue longer than the pass can take) are streamed.  Shared
+// memory is sized by the cap (~12 KB at cap 96) so the warp can co-reside with
+// the encoder GEMMs' CTAs on an SM instead of waiting for one to drain.
 
-constexpr int kPassStage = 7168;  // staged member candidates (28 KB); beyond: recomputed from global
+__host__ __device__ constexpr int pass_stage_jobs(int cap) { return cap + 32; }
+__host__ __device__ constexpr int pass_stage_cands(int cap) { return 8 * cap < 256 ? 256 : (8 * cap < 8192 ? 8 * cap : 8192); }
+__host__ __device__ constexpr size_t pass_align8(size_t x) { return (x + 7) & ~(size_t)7; }
+__host__ __device__ constexpr size_t pass_smem_bytes(int cap, int K) {
+  return pass_align8(sizeof(MsPassCost)) + 8 * MS_PASS_MAX_PTS + pass_align8((size_t)8 * pass_stage_jobs(cap)) +
+         pass_align8((size_t)4 * (5 * (size_t)pass_stage_jobs(cap) + 1)) +                 // size, nc, cand off (g/l), mask off
+         pass_align8((size_t)4 * (2 * (size_t)cap + 1)) +                                   // choice, request offsets
+         pass_align8((size_t)4 * pass_stage_cands(cap)) + pass_align8((size_t)2 * K * pass_stage_cands(cap));
+}
 
-__device__ __forceinline__ long long pass_raw_ns(long long u, const MsPassCost& c) {
+// piecewise-linear pass time with each segment's slope in 2^-20 ns per work
+// unit (computed once per launch: no division on the hot path); the first
+// segment whose right knot is >= u, clamped below the first knot, the last
+// segment extrapolated
+constexpr int kSlopeShift = 20;
+__device__ __forceinline__ long long pass_raw_ns(long long u, const MsPassCost& c, const long long* slope) {
   if (c.n_pts == 1 || u <= c.u[0]) return c.t_ns[0];
-  int i = 0;
-  while (i + 2 < c.n_pts && u > c.u[i + 1]) ++i;
-  return c.t_ns[i] + (c.t_ns[i + 1] - c.t_ns[i]) * (u - c.u[i]) / (c.u[i + 1] - c.u[i]);
+  int lo = 0, hi = c.n_pts - 2;  // binary search: first i with u <= u[i+1]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (u <= c.u[mid + 1]) hi = mid; else lo = mid + 1;
+  }
+  return c.t_ns[lo] + (((u - c.u[lo]) * slope[lo]) >> kSlopeShift);
 }
 
 // round_half_even(raw * factor): one fp64 multiply, as Python's round(int * float)
-__device__ __forceinline__ long long pass_est_ns(long long u, const MsPassCost& c, double factor) {
-  return __double2ll_rn(__dmul_rn((double)pass_raw_ns(u, c), factor));
+__device__ __forceinline__ long long pass_est_ns(long long u, const MsPassCost& c, const long long* slope,
+                                                 double factor) {
+  return __double2ll_rn(__dmul_rn((double)pass_raw_ns(u, c, slope), factor));
 }
 
 template <typename T>
@@ -110,6 +136,22 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// largest i in [0, n) with off[i] <= t (off ascending, off[0] = 0)
+__device__ __forceinline__ int pass_owner(const int* off, int n, int t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(32)
     pass_select_kernel(const int32_t* __restrict__ prob_job_off, const int32_t* __restrict__ prob_n_jobs,
                        const int64_t* __restrict__ prob_now_us, const double* __restrict__ prob_factor,
@@ -118,21 +160,41 @@ __global__ void __launch_bounds__(32)
                        const int32_t* __restrict__ job_mask_off, const int16_t* __restrict__ cand_counts,
                        const uint16_t* __restrict__ req_masks, const __grid_constant__ MsPassCost cost_p, int cap,
                        long long max_pass_ns, int32_t* __restrict__ out_choice, int32_t* __restrict__ out_summary,
-                       int64_t* __restrict__ out_est_ns, uint16_t* __restrict__ out_mask, long long out_mask_ld) {
-  __shared__ MsPassCost cost;
-  __shared__ int s_choice[MS_PASS_MAX_MEMBERS];
-  __shared__ int s_ncand[MS_PASS_MAX_MEMBERS];
-  __shared__ int s_uoff[MS_PASS_MAX_MEMBERS + 1];
-  __shared__ int s_roff[MS_PASS_MAX_MEMBERS + 1];
-  __shared__ int s_u[kPassStage];
+                       int64_t* __restrict__ out_est_ns, uint16_t* __restrict__ out_mask, long long out_mask_ld,
+                       int64_t* __restrict__ out_clock) {
+  const long long t_start = global_ns();
+  const int SJ = pass_stage_jobs(cap), SC = pass_stage_cands(cap);
+  extern __shared__ __align__(16) unsigned char pass_smem[];
+  unsigned char* sp = pass_smem;
+  MsPassCost& cost = *reinterpret_cast<MsPassCost*>(sp);
+  sp += pass_align8(sizeof(MsPassCost));
+  long long* s_slope = reinterpret_cast<long long*>(sp);
+  sp += 8 * MS_PASS_MAX_PTS;
+  long long* s_dl = reinterpret_cast<long long*>(sp);
+  sp += pass_align8((size_t)8 * SJ);
+  int* s_size = reinterpret_cast<int*>(sp);
+  int* s_nc = s_size + SJ;
+  int* s_cg = s_nc + SJ;      // global candidate offset
+  int* s_moff = s_cg + SJ;    // global mask offset
+  int* s_coff = s_moff + SJ;  // staged candidate offset (exclusive scan of s_nc), SJ + 1
+  sp += pass_align8((size_t)4 * (5 * (size_t)SJ + 1));
+  int* s_choice = reinterpret_cast<int*>(sp);
+  int* s_roff = s_choice + cap;  // request offsets of the members, cap + 1
+  sp += pass_align8((size_t)4 * (2 * (size_t)cap + 1));
+  int* s_u = reinterpret_cast<int*>(sp);
+  sp += pass_align8((size_t)4 * SC);
+  int16_t* s_cnt = reinterpret_cast<int16_t*>(sp);
+
   const int p = blockIdx.x, lane = threadIdx.x;
   {
     const int* src = reinterpret_cast<const int*>(&cost_p);
     int* dst = reinterpret_cast<int*>(&cost);
     for (int i = lane; i < (int)(sizeof(MsPassCost) / 4); i += 32) dst[i] = src[i];
+    if (lane + 1 < cost_p.n_pts)
+      s_slope[lane] = ((cost_p.t_ns[lane + 1] - cost_p.t_ns[lane]) << kSlopeShift) /
+                      (cost_p.u[lane + 1] - cost_p.u[lane]);
   }
-  __syncwarp();
-  const int K = cost.K;
+  const int K = cost_p.K;
   const int j0 = prob_job_off[p], Q = prob_n_jobs[p];
   const long long now_ns = (long long)prob_now_us[p] * 1000;
   const double f = prob_factor[p];
@@ -142,31 +204,75 @@ __global__ void __launch_bounds__(32)
     if (lane == 0) out_est_ns[p] = 0;
     return;
   }
-  // work of job j's candidate c, from the (global or mapped host) count table
-  auto cand_u = [&](int j, int c) -> int {
-    const int16_t* cc = cand_counts + (long long)(job_cand_off[j] + c) * K;
+
+  // ---- stage the first nj jobs (one sweep of independent loads) ...
+  const int nj = min(Q, SJ);
+  for (int j = lane; j < nj; j += 32) {
+    s_size[j] = job_size[j0 + j];
+    s_nc[j] = job_n_cand[j0 + j];
+    s_cg[j] = job_cand_off[j0 + j];
+    s_moff[j] = job_mask_off[j0 + j];
+    s_dl[j] = job_deadline_us[j0 + j];
+  }
+  __syncwarp();
+  for (int base = 0; base < nj; base += 32) {
+    const int j = base + lane;
+    const int nc = j < nj ? s_nc[j] : 0;
+    const int incl = warp_incl_scan(nc, lane);
+    const int prev = base ? s_coff[base] : 0;
+    __syncwarp();
+    if (j < nj) s_coff[j + 1] = prev + incl;
+    if (j == 0) s_coff[0] = 0;
+    __syncwarp();
+  }
+  // ... and all their candidates' counts (flattened, independent loads)
+  const int n_stage = s_coff[nj];
+  const bool staged = n_stage <= SC;
+  if (staged) {
+    for (int t = lane; t < n_stage; t += 32) {
+      const int j = pass_owner(s_coff, nj, t);
+      const int16_t* cc = cand_counts + (long long)(s_cg[j] + t - s_coff[j]) * K;
+      int u = 0;
+      for (int k = 0; k < K; ++k) {
+        const int16_t v = cc[k];
+        s_cnt[t * K + k] = v;
+        u += cost.w[k] * (int)v;
+      }
+      s_u[t] = u;
+    }
+  }
+  __syncwarp();
+  // accessors: staged jobs from shared memory, the rest streamed from global
+  auto size_of = [&](int j) -> int { return j < nj ? s_size[j] : job_size[j0 + j]; };
+  auto dl_of = [&](int j) -> long long { return j < nj ? s_dl[j] : (long long)job_deadline_us[j0 + j]; };
+  auto cand_cnt = [&](int j, int c, int k) -> int {
+    if (staged && j < nj) return s_cnt[(s_coff[j] + c) * K + k];
+    return cand_counts[(long long)((j < nj ? s_cg[j] : job_cand_off[j0 + j]) + c) * K + k];
+  };
+  auto U = [&](int j, int c) -> int {
+    if (staged && j < nj) return s_u[s_coff[j] + c];
     int u = 0;
-    for (int k = 0; k < K; ++k) u += cost.w[k] * (int)cc[k];
+    for (int k = 0; k < K; ++k) u += cost.w[k] * cand_cnt(j, c, k);
     return u;
   };
 
   // ---- 1. membership: prefix scans over the queue, 32 jobs per step
-  long long u_mem = cand_u(j0, 0);
-  int n = job_size[j0];
-  long long tight = job_deadline_us[j0];
+  long long u_mem = U(0, 0);
+  int n = size_of(0);
+  long long tight = dl_of(0);
   int M = Q;
   for (int base = 1; base < Q; base += 32) {
     const int j = base + lane;
     const bool valid = j < Q;
-    const int s = valid ? job_size[j0 + j] : 0;
-    const long long d = valid ? (long long)job_deadline_us[j0 + j] : LLONG_MAX;
-    const long long u = valid ? cand_u(j0 + j, 0) : 0;
+    const int s = valid ? size_of(j) : 0;
+    const long long d = valid ? dl_of(j) : LLONG_MAX;
+    const long long u = valid ? U(j, 0) : 0;
     const int n_j = n + warp_incl_scan(s, lane);
     const long long u_j = u_mem + warp_incl_scan(u, lane);
     const long long t_j = min(tight, warp_incl_min(d, lane));
     bool fail = !valid || n_j > cap;
     if (!fail) {
-      const long long e = pass_est_ns(u_j, cost, f);
+      const long long e = pass_est_ns(u_j, cost, s_slope, f);
       fail = now_ns + e > t_j * 1000 || (max_pass_ns >= 0 && e > max_pass_ns);
     }
     const unsigned bal = __ballot_sync(kFull, fail);
@@ -181,52 +287,35 @@ __global__ void __launch_bounds__(32)
       break;
     }
   }
-  const long long e_mem = pass_est_ns(u_mem, cost, f);
+  const long long e_mem = pass_est_ns(u_mem, cost, s_slope, f);
 
   // ---- 2. the jobs left queued: fastest-pass work and the earliest deadline it can still meet
   long long rest_u = 0;
-  for (int j = M + lane; j < Q; j += 32) rest_u += cand_u(j0 + j, 0);
+  for (int j = M + lane; j < Q; j += 32) rest_u += U(j, 0);
   rest_u = warp_sum(rest_u);
-  const long long rest_fast = M < Q ? pass_est_ns(rest_u, cost, f) : 0;
+  const long long rest_fast = M < Q ? pass_est_ns(rest_u, cost, s_slope, f) : 0;
   long long rest_dl = LLONG_MAX;  // none
   for (int j = M + lane; j < Q; j += 32) {
-    const long long d = job_deadline_us[j0 + j];
+    const long long d = dl_of(j);
     if (d * 1000 >= now_ns + e_mem + rest_fast) rest_dl = min(rest_dl, d);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) rest_dl = min(rest_dl, __shfl_xor_sync(kFull, rest_dl, d));
 
-  // ---- stage the members' frontiers (work per candidate) and request offsets
+  // members' request offsets (M <= cap <= nj: all staged jobs)
   for (int base = 0; base < M; base += 32) {
     const int j = base + lane;
-    const int nc = j < M ? job_n_cand[j0 + j] : 0;
-    const int sz = j < M ? job_size[j0 + j] : 0;
-    const int nc_incl = warp_incl_scan(nc, lane), sz_incl = warp_incl_scan(sz, lane);
-    const int nc_base = base ? s_uoff[base] : 0, sz_base = base ? s_roff[base] : 0;
+    const int sz = j < M ? s_size[j] : 0;
+    const int incl = warp_incl_scan(sz, lane);
+    const int prev = base ? s_roff[base] : 0;
     __syncwarp();
     if (j < M) {
-      s_ncand[j] = nc;
+      s_roff[j + 1] = prev + incl;
       s_choice[j] = 0;
-      s_uoff[j + 1] = nc_base + nc_incl;
-      s_roff[j + 1] = sz_base + sz_incl;
     }
-    if (base == 0 && lane == 0) s_uoff[0] = s_roff[0] = 0;
+    if (j == 0) s_roff[0] = 0;
     __syncwarp();
   }
-  const int n_stage = s_uoff[M];
-  const bool staged = n_stage <= kPassStage;
-  if (staged) {
-    for (int t = lane; t < n_stage; t += 32) {  // flattened (member, candidate): independent loads
-      int lo = 0, hi = M - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_uoff[mid] <= t) lo = mid; else hi = mid - 1;
-      }
-      s_u[t] = cand_u(j0 + lo, t - s_uoff[lo]);
-    }
-  }
-  __syncwarp();
-  auto U = [&](int j, int c) -> int { return staged ? s_u[s_uoff[j] + c] : cand_u(j0 + j, c); };
 
   // ---- 3. upgrades: per member (EDF order) the largest feasible frontier index
   const long long tight_ns = tight * 1000;
@@ -236,7 +325,7 @@ __global__ void __launch_bounds__(32)
   while (moved) {
     moved = false;
     for (int j = 0; j < M; ++j) {
-      const int nc = s_ncand[j], cur = s_choice[j];
+      const int nc = s_nc[j], cur = s_choice[j];
       if (cur + 1 >= nc) continue;
       const long long ub = u_cur - U(j, cur);
       int best = -1;
@@ -247,7 +336,7 @@ __global__ void __launch_bounds__(32)
         long long uc = 0;
         if (c < nc) {
           uc = ub + U(j, c);
-          const long long e = pass_est_ns(uc, cost, f);
+          const long long e = pass_est_ns(uc, cost, s_slope, f);
           ok = now_ns + e <= tight_ns && (rest_ns == LLONG_MAX || now_ns + e + rest_fast <= rest_ns) &&
                (max_pass_ns < 0 || e <= max_pass_ns);
         }
@@ -276,17 +365,24 @@ __global__ void __launch_bounds__(32)
     const int ch = j < M ? s_choice[j] : -1;
     out_choice[j0 + j] = ch;
     if (ch >= 0) {
-      const int16_t* cc = cand_counts + (long long)(job_cand_off[j0 + j] + ch) * K;
-      for (int k = 0; k < K; ++k) cnt[k] += cc[k];
+#pragma unroll
+      for (int k = 0; k < MS_PASS_MAX_K; ++k)
+        if (k < K) cnt[k] += cand_cnt(j, ch, k);
     }
   }
 #pragma unroll
   for (int k = 0; k < MS_PASS_MAX_K; ++k) cnt[k] = warp_sum(cnt[k]);
   const int n_req = s_roff[M];
+  uint16_t* om = out_mask + (long long)p * out_mask_ld;
+  for (int r = lane; r < n_req; r += 32) {  // flattened requests: member by binary search
+    const int j = pass_owner(s_roff, M, r);
+    const int sz = s_roff[j + 1] - s_roff[j];
+    om[r] = req_masks[s_moff[j] + (long long)s_choice[j] * sz + (r - s_roff[j])];
+  }
   if (lane == 0) {
     summ[0] = M;
     summ[1] = n_req;
-    out_est_ns[p] = pass_est_ns(u_cur, cost, f);
+    out_est_ns[p] = pass_est_ns(u_cur, cost, s_slope, f);
   }
   if (lane < MS_PASS_MAX_K) {
     int v = 0;
@@ -295,15 +391,9 @@ __global__ void __launch_bounds__(32)
       if (k == lane) v = cnt[k];
     summ[2 + lane] = lane < K ? v : 0;
   }
-  uint16_t* om = out_mask + (long long)p * out_mask_ld;
-  for (int r = lane; r < n_req; r += 32) {  // flattened requests: member by binary search
-    int lo = 0, hi = M - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_roff[mid] <= r) lo = mid; else hi = mid - 1;
-    }
-    const int sz = s_roff[lo + 1] - s_roff[lo];
-    om[r] = req_masks[job_mask_off[j0 + lo] + (long long)s_choice[lo] * sz + (r - s_roff[lo])];
+  if (out_clock != nullptr && lane == 0) {
+    out_clock[2 * p] = t_start;
+    out_clock[2 * p + 1] = global_ns();
   }
 }
 
@@ -762,7 +852,7 @@ int ms_pass_select(int n_prob, const int32_t* prob_job_off, const int32_t* prob_
                    const int32_t* job_mask_off, const int16_t* cand_counts, const uint16_t* req_masks,
                    const MsPassCost* cost, int cap, int64_t max_pass_ns, int32_t* out_choice,
                    int32_t* out_summary, int64_t* out_est_ns, uint16_t* out_mask, long long out_mask_ld,
-                   void* stream) {
+                   int64_t* out_clock, void* stream) {
   if (n_prob < 0) return set_error(MS_ERR_INVALID, "pass_select: n_prob must be >= 0");
   if (n_prob == 0) return MS_OK;
   if (!prob_job_off || !prob_n_jobs || !prob_now_us || !prob_factor || !job_size || !job_deadline_us ||
@@ -777,13 +867,22 @@ int ms_pass_select(int n_prob, const int32_t* prob_job_off, const int32_t* prob_
       return set_error(MS_ERR_INVALID, "pass_select: knots must have increasing work and non-decreasing time");
   }
   for (int k = 0; k < cost->K; ++k)
-    if (cost->w[k] < 0) return set_error(MS_ERR_INVALID, "pass_select: negative work weight");
+    if (cost->w[k] < 0 || cost->w[k] > 65536) return set_error(MS_ERR_INVALID, "pass_select: work weight out of 0..65536");
+  if (cost->u[0] < 0 || cost->u[cost->n_pts - 1] > (1LL << 30) || cost->t_ns[cost->n_pts - 1] > (1LL << 36))
+    return set_error(MS_ERR_INVALID, "pass_select: knots out of range (work <= 2^30, time <= 2^36 ns)");
   if (cap < 1 || cap > MS_PASS_MAX_MEMBERS) return set_error(MS_ERR_INVALID, "pass_select: cap must be in 1..1024");
   if (out_mask_ld < cap) return set_error(MS_ERR_INVALID, "pass_select: out_mask_ld < cap");
-  pass_select_kernel<<<(unsigned)n_prob, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  const size_t smem = pass_smem_bytes(cap, cost->K);
+  static int smem_opt = 0;
+  if (smem > 48 * 1024 && smem_opt < (int)smem) {
+    if (cudaFuncSetAttribute(pass_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return check_launch("pass_select_kernel smem attribute");
+    smem_opt = (int)smem;
+  }
+  pass_select_kernel<<<(unsigned)n_prob, 32, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
            prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size, job_deadline_us, job_n_cand, job_cand_off,
            job_mask_off, cand_counts, req_masks, *cost, cap, (long long)max_pass_ns, out_choice, out_summary,
-           out_est_ns, out_mask, out_mask_ld);
+           out_est_ns, out_mask, out_mask_ld, out_clock);
   return check_launch("pass_select_kernel");
 }
 

@@ -82,7 +82,7 @@ _SIGS = {
     "ms_compact": ([_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_compact_ring": ([_P, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "ms_pass_select": ([_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, C.c_int64, _P, _P, _P, _P,
-                        _LL, _P], C.c_int),
+                        _LL, _P, _P], C.c_int),
     "ms_gemm_plan_dense": ([_P, _P, _I, _I, _LL, _P, _I, _I, _I, _P, _I, _I, _P, _LL, _I, _I, _P],
                            C.c_int),
     "ms_gemm_plan_conv": ([_P, _P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _P, _I, _I, _P, _I, _P, _LL,
@@ -215,13 +215,14 @@ def policy_select(lat_us, credit, n_cand, deadline_us, dispatch_us: int, factor:
 
 def pass_select(n_prob, prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size, job_deadline_us,
                 job_n_cand, job_cand_off, job_mask_off, cand_counts, req_masks, cost: PassCost, cap: int,
-                max_pass_ns: int, out_choice, out_summary, out_est_ns, out_mask, out_mask_ld: int, stream=None):
+                max_pass_ns: int, out_choice, out_summary, out_est_ns, out_mask, out_mask_ld: int, stream=None,
+                out_clock=None):
     """ms_pass_select on raw addresses (device or pinned host memory): every
     array argument is an integer address (``tensor.data_ptr()``)."""
     check(lib().ms_pass_select(int(n_prob), prob_job_off, prob_n_jobs, prob_now_us, prob_factor, job_size,
                                job_deadline_us, job_n_cand, job_cand_off, job_mask_off, cand_counts, req_masks,
                                C.byref(cost), int(cap), int(max_pass_ns), out_choice, out_summary, out_est_ns,
-                               out_mask, int(out_mask_ld), stream_ptr(stream)), "ms_pass_select")
+                               out_mask, int(out_mask_ld), out_clock, stream_ptr(stream)), "ms_pass_select")
 
 
 # -------------------------------------------------------------- compaction

@@ -191,6 +191,27 @@ class MaskedModel:
             self._graphs[key] = g
         return g
 
+    def ring_upload(self, host_pools, counts, bases, stream):
+        """Host-IO path: DMA modality k's next ``counts[k]`` ring rows (from
+        ``bases[k]``, wrapping) from the pinned host pools into the HBM pool
+        on ``stream`` -- one copy per modality (two on wrap-around).
+        Returns the bytes moved."""
+        torch = self.torch
+        ns = self.n_slots
+        moved = 0
+        with torch.cuda.stream(stream):
+            for k in range(self.K):
+                c = int(counts[k])
+                if not c:
+                    continue
+                r0 = int(bases[k])
+                first = min(c, ns - r0)
+                self.pools[k][r0:r0 + first].copy_(host_pools[k][r0:r0 + first], non_blocking=True)
+                if first < c:
+                    self.pools[k][: c - first].copy_(host_pools[k][: c - first], non_blocking=True)
+                moved += c * self.row_bytes[k]
+        return moved
+
     def run_ring(self, n: int, counts, slot: int, bases):
         """One pass formed on the device: masks in ``mask_ring[slot]``
         (written by ms_pass_select), pool rows from the per-modality rings

@@ -47,7 +47,8 @@ class ServeStats:
     wall_s: float = 0.0
     trace: list | None = None  # optional per-pass diagnostics (serve_realtime(trace=True))
     policy_launches: int = 0   # ms_pass_select launches (device policy step)
-    policy_device_us: float = 0.0
+    policy_device_us: float = 0.0   # launch -> result on the selection stream (CUDA events)
+    policy_kernel_us: float = 0.0   # the kernel's own time (device global timer)
     formations: list | None = None
 
 
@@ -252,17 +253,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         bases = list(rings)
         ev_s, ev_e = dv.Event(), dv.Event()
         if host_clips is not None:
-            with torch.cuda.stream(copy_stream):
-                for k in range(model.K):
-                    c = counts[k]
-                    if not c:
-                        continue
-                    r0 = bases[k]
-                    first = min(c, ns - r0)
-                    model.pools[k][r0:r0 + first].copy_(host_clips.host[k][r0:r0 + first], non_blocking=True)
-                    if first < c:
-                        model.pools[k][: c - first].copy_(host_clips.host[k][: c - first], non_blocking=True)
-                    stats.h2d_bytes += c * host_clips.row_bytes[k]
+            stats.h2d_bytes += model.ring_upload(host_clips.host, counts, bases, copy_stream)
             stream.wait_stream(copy_stream)
         for k in range(model.K):
             rings[k] = (bases[k] + counts[k]) % ns
@@ -418,6 +409,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
     if selector is not None:
         stats.policy_launches = selector.launches
         stats.policy_device_us = selector.device_us
+        stats.policy_kernel_us = selector.kernel_us
         if record_formations:
             stats.formations = selector.records
     log = MetricsLog(window_us, tuple(sorted(records, key=lambda r: r.id)))

@@ -181,3 +181,111 @@ def test_realtime_pass_selection_meets_slos(built):
     total = sum(r.size for r in served)
     assert dropped > 0.2 * total, (dropped, total, log.violation_ratio())
     assert log.violation_ratio() < 0.15, (dropped, total, log.violation_ratio())
+
+
+def _oracle_rows(orc, model, rows_per_mod, masks, pick):
+    """Oracle logits for the requests ``pick`` (each request's logits depend
+    only on its own clips): rows_per_mod[k][i] = pool row of request i."""
+    clips = [p.cpu()[torch.as_tensor(np.asarray(r)[pick]).long()] for p, r in zip(model.pools, rows_per_mod)]
+    return orc.logits(clips, torch.as_tensor(np.asarray(masks)[pick]))
+
+
+@pytest.fixture(scope="module")
+def tbn96(built):
+    from paper_2310_18481_b200.executor import build_tbn_model
+    return build_tbn_model(max_req=96, n_slots=192)
+
+
+def test_tbn_bench_operating_point_passes_vs_oracle(tbn96):
+    """The bench's operating configuration (max_req 96: 2-SM pair tiles,
+    split-K, halo/K32 convs, per-count CUDA graphs with concurrent branch
+    lanes): a full 96-request mixed pass and a 61-request pass with the
+    served modality mix (all rgb, ~60 % flow, ~40 % audio), both through the
+    graphs; grouping bit-exact, logits vs the oracle on 32 sampled requests
+    of each (covering every combo present)."""
+    from oracle.forward import OracleTBN
+    from paper_2310_18481_b200.encoders import TBN_MODALITIES
+    model = tbn96
+    orc = OracleTBN(TBN_MODALITIES, (101, 102, 103), 199, 3)
+    rng = np.random.default_rng(11)
+    mixed = rng.integers(1, 8, size=96)
+    served = 1 | (rng.random(61) < 0.6) * 2 | (rng.random(61) < 0.4) * 4
+    for masks in (mixed, served):
+        n = len(masks)
+        slots = rng.permutation(model.n_slots)[:n]
+        logits = model.forward(slots, masks).clone()
+        torch.cuda.synchronize()
+        idx = model.idx[: 3 * n].view(3, n).cpu().numpy()
+        for k in range(3):
+            exp = np.flatnonzero((masks >> k) & 1)
+            assert np.array_equal(idx[k, : len(exp)], exp)
+        pick = np.sort(np.concatenate([np.flatnonzero(masks == m)[:2] for m in range(1, 8)] +
+                                       [rng.permutation(n)[:32]]))[:32]
+        pick = np.unique(pick)
+        ref = _oracle_rows(orc, model, [slots] * 3, masks, pick)
+        rel, agree = _check_logits(logits[pick], ref)
+        print(f"TBN n={n}: max rel err {rel:.2e}, top-1 agreement {agree:.4f} on {len(pick)} rows")
+
+
+def test_tbn_ring_path_host_io_logits_vs_oracle(tbn96):
+    """The e2e host-IO path exactly as the server runs it: a pass formed on
+    the device (ms_pass_select writes the masks into the mask ring), each
+    modality's clips DMA'd into its pool ring at the ring base, compaction in
+    ring mode; distinct data in every host row, so a wrong row map fails.
+    Logits vs the oracle on the rows actually copied."""
+    from oracle.forward import OracleTBN
+    from oracle import selection as orc_sel
+    from paper_2310_18481_b200 import device as dv
+    from paper_2310_18481_b200.batcher import DevicePassSelector
+    from paper_2310_18481_b200.encoders import TBN_MODALITIES
+    model = tbn96
+    ns = model.n_slots
+    g = torch.Generator().manual_seed(5)
+    host = []
+    for p in model.pools:  # fresh, distinct host rows (pinned)
+        h = (torch.randint(0, 256, p.shape, generator=g, dtype=torch.uint8) if p.dtype == torch.uint8 else
+             torch.randn(p.shape, generator=g).to(p.dtype))
+        host.append(h.pin_memory())
+    # one formation: three jobs whose fastest candidates use different modalities
+    cost = dv.PassCost.make([300, 330, 390], [1024, 96 * 1024], [400_000, 6_400_000])
+    sel = DevicePassSelector(3, cost, 96, -1, model.mask_ring)
+
+    class J:
+        def __init__(self, size, dl, masks):
+            from paper_2310_18481_b200.batcher import FrontierPack
+            self.deadline_us = dl
+            self.pack = FrontierPack.__new__(FrontierPack)
+            m = np.asarray(masks, np.uint16)
+            self.pack.size, self.pack.n_cand = size, m.shape[0]
+            self.pack.masks = m.reshape(-1)
+            self.pack.counts = np.stack([((m >> k) & 1).sum(1) for k in range(3)], 1).astype(np.int16)
+
+    jobs = [J(20, 50_000, [[1] * 20, [3] * 20, [7] * 20]), J(25, 50_000, [[4] * 25, [5] * 25]),
+            J(30, 50_000, [[2] * 30, [6] * 10 + [7] * 20])]
+    bases = [ns - 7, 3, ns - 40]  # wrap-around on rgb and audio
+    r = sel.select(jobs, 0, 1.0, slot=0)
+    w, u, t = cost.table()
+    ref_sel = orc_sel.pass_select([(j.pack.size, j.deadline_us, j.pack.counts,
+                                    j.pack.masks.reshape(j.pack.n_cand, j.pack.size)) for j in jobs],
+                                  0, w, u, t, 1.0, 96, -1)
+    assert (r.members, r.choices.tolist(), r.est_ns, list(r.counts)) == ref_sel[:4]
+    masks = np.asarray(ref_sel[4])
+    cs = torch.cuda.Stream()
+    model.ring_upload(host, r.counts, bases, cs)
+    torch.cuda.current_stream().wait_stream(cs)
+    model.run_ring(r.requests, r.counts, 0, bases)
+    logits = model.head.logits[: r.requests].clone()
+    torch.cuda.synchronize()
+    assert np.array_equal(model.mask_ring[0, : r.requests].cpu().numpy().view(np.uint16), masks)
+    # request i's modality-k row: (base_k + position of i among modality-k requests) % ns
+    rows = []
+    for k in range(3):
+        has = (masks >> k) & 1
+        pos = np.cumsum(has) - 1
+        rows.append(np.where(has == 1, (bases[k] + pos) % ns, 0))
+    orc = OracleTBN(TBN_MODALITIES, (101, 102, 103), 199, 3)
+    pick = np.unique(np.concatenate([np.flatnonzero(masks == m)[:4] for m in range(1, 8)]))
+    clips = [h[torch.as_tensor(rr[pick]).long()] for h, rr in zip(host, rows)]
+    ref = orc.logits(clips, torch.as_tensor(masks[pick].astype(np.int64)))
+    rel, agree = _check_logits(logits[pick], ref)
+    print(f"ring host-IO pass: {r.requests} requests, counts {r.counts}, rel err {rel:.2e} on {len(pick)} rows")

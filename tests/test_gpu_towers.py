@@ -95,3 +95,27 @@ def test_vqa_two_tower_vs_oracle():
     assert err < 2e-2, err
     assert torch.equal(logits.cpu().argmax(1), ref.argmax(1))
     print(f"VQA two-tower: max rel err {err:.2e}")
+
+
+def test_vqa_two_tower_vs_oracle_32_requests():
+    """configs[2] at a serving-sized pass: 32 requests, image tower dropped
+    for a third of them, pool rows shuffled."""
+    from oracle.forward import OracleVQA
+    from paper_2310_18481_b200 import build
+    build.build()
+    from paper_2310_18481_b200.towers import build_vqa_model
+    model = build_vqa_model(max_req=32, n_slots=40)
+    rng = np.random.default_rng(7)
+    masks = rng.choice([3, 2, 1], size=32, p=[0.5, 0.35, 0.15])
+    slots = rng.permutation(40)[:32]
+    logits = model.forward(slots, masks).clone()
+    torch.cuda.synchronize()
+    orc = OracleVQA()
+    sl = torch.as_tensor(slots).long()
+    ref = orc.logits(model.pools[0].cpu()[sl].float(), model.pools[1].cpu()[sl], torch.as_tensor(masks))
+    scale = ref.abs().max().item()
+    err = (logits.cpu() - ref).abs().max().item()
+    assert err <= 2e-2 * scale, (err, scale)
+    srt = ref.sort(1, descending=True).values
+    agree = (logits.cpu().argmax(1) == ref.argmax(1)) | (srt[:, 0] - srt[:, 1] <= 2e-2 * scale)
+    assert agree.float().mean().item() >= 0.999

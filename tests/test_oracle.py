@@ -96,3 +96,34 @@ def test_compaction_restatement_properties():
     assert np.all(np.diff(masks[perm]) >= 0)
     assert sum(n for _, _, n in chunks) == len(masks)
     assert orc.dropped_modalities(0b0101, 3) == 0b010
+
+
+def test_oracle_bninception_table_is_pinned():
+    """The oracle's own BN-Inception table: Ioffe & Szegedy's printed widths
+    reproduce SURVEY Appendix C's analytic MACs (2.032 / 2.307 / 2.551 GMAC
+    per frame, 69 convs); the TSN widths the models use differ only in
+    4c/4d's 1x1 and match the product's independent table and FLOP count."""
+    from oracle import bninception as bni
+    from paper_2310_18481_b200 import encoders as enc
+    got = [round(bni.macs(c, s, bni.IOFFE) / 1e9, 3) for c, s in ((3, 224), (10, 224), (1, 256))]
+    assert got == [2.032, 2.307, 2.551]
+    assert len(bni.convs(3, bni.IOFFE)) == len(bni.convs(3, bni.TSN)) == 69
+    assert {b for b in bni.ORDER if bni.IOFFE[b] != bni.TSN[b]} == {"4c", "4d"}
+    for m in enc.TBN_MODALITIES:
+        assert bni.macs(m.channels, m.size) == enc.bninception_macs(m.channels, m.size)
+
+
+def test_oracle_weights_match_the_model_definition():
+    import torch
+    from oracle import bninception as bni
+    from oracle.forward import fusion_weights
+    from paper_2310_18481_b200 import encoders as enc
+    ow = bni.weights(10, 102)
+    pw = enc.bninception_weights(10, 224, 102)
+    assert list(ow) == list(pw)
+    for k in ow:
+        assert torch.equal(ow[k][0], pw[k][0]) and torch.equal(ow[k][1], pw[k][1]), k
+    for a, b in zip(fusion_weights(3, 1024, 199), enc.fusion_weights(3, 1024, 199)):
+        assert torch.equal(a, b)
+    for (a, b), (c, d) in zip(bni.dense_weights((1024, 1024, 1024), 201), enc.mlp_weights((1024, 1024, 1024), 201)):
+        assert torch.equal(a, c) and torch.equal(b, d)

@@ -106,7 +106,7 @@ def test_abi_pass_select_rejects_bad_arguments():
     assert ctypes.sizeof(device.PassCost) == 552
     cost = device.PassCost.make([300, 330, 390], [1024, 2048], [400_000, 450_000])
     dummy = ctypes.c_void_p(16)
-    args = [1] + [dummy] * 11 + [ctypes.byref(cost), 96, -1] + [dummy] * 4 + [96, None]
+    args = [1] + [dummy] * 11 + [ctypes.byref(cost), 96, -1] + [dummy] * 4 + [96, None, None]
     bad = list(args)
     bad[13] = 0  # cap
     assert L.ms_pass_select(*bad) == 1 and b"cap" in L.ms_last_error()
