@@ -224,22 +224,38 @@ def reference_arm(args):
 # ------------------------------------------------------------------ our arm
 
 
-def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1):
+TRACE = ROOT / "tests" / "golden" / "serving" / "bursty_trace.csv"
+TRACE_MIN_FRAC = 0.25  # the trace is mapped to [0.25 x peak, peak] requests/s (map_trace_to_qps)
+MULTS = (1.0, 1.5, 3.0)  # varying budgets: per-job deadline = deadline_ms x one of these
+
+
+def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1, arrivals="poisson", mults=None):
+    """The job stream of one serving window: Poisson at ``qps`` requests/s, or
+    the bursty trace (configs[3]) with ``qps`` its peak; ``mults``: varying
+    per-job budgets deadline_ms x mults."""
     from paper_2310_18481_b200.serving import WorkloadSpec, generate_jobs
-    spec = WorkloadSpec(kind="poisson", qps=qps * world, duration_s=max(1, int(np.ceil(seconds))),
-                        deadline_ms=deadline_ms, seed=seed)
+    dur = max(1, int(np.ceil(seconds)))
+    if arrivals == "trace":
+        spec = WorkloadSpec(kind="trace", trace_path=str(TRACE), min_qps=int(round(TRACE_MIN_FRAC * qps * world)),
+                            max_qps=int(round(qps * world)), duration_s=dur, deadline_ms=deadline_ms, seed=seed,
+                            deadline_mults=mults)
+    else:
+        spec = WorkloadSpec(kind="poisson", qps=qps * world, duration_s=dur, deadline_ms=deadline_ms, seed=seed,
+                            deadline_mults=mults)
     jobs = [j for j in generate_jobs(spec, profile) if j.arrival_us < seconds * 1e6]
     return jobs[rank::world]
 
 
 # serving-loop options (set from the command line in main())
-SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.2}
+SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.2,
+              "arrivals": "poisson", "mults": None, "top_only": False}
 
 
 def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world=1,
           host_clips=None, max_size=None, cost=None):
     from paper_2310_18481_b200.realtime import serve_realtime
-    jobs = make_jobs(profile, qps, seconds, deadline_ms, seed, rank, world)
+    o = SERVE_OPTS
+    jobs = make_jobs(profile, qps, seconds, deadline_ms, seed, rank, world, o["arrivals"], o["mults"])
     if max_size:
         from paper_2310_18481_b200.serving import JobTemplate
         jobs = [JobTemplate(j.arrival_us, min(j.size, max_size), j.accuracy_slo, j.deadline_us)
@@ -247,12 +263,14 @@ def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world
     if cost is not None:
         cost.factor = 1.0
     from paper_2310_18481_b200.policy import Policy
-    o = SERVE_OPTS
     sel = o["selection"] if cost is not None else "policy"
+    # the pass-length cap scales with the tightest budget in play
+    tight_ms = deadline_ms * (min(o["mults"]) if o["mults"] else 1.0)
     return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed, cost=cost,
                           policy=Policy.NONE if sel == "pass" else Policy.OPTIMIZED,
                           sched_margin_us=o["sched_margin_us"], policy_grid_us=o["policy_grid_us"],
-                          selection=sel, max_pass_us=o["pass_frac"] * deadline_ms * 1000 if sel == "pass" else None)
+                          selection=sel, max_pass_us=o["pass_frac"] * tight_ms * 1000 if sel == "pass" else None,
+                          top_only=o["top_only"])
 
 
 def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print,
@@ -465,9 +483,65 @@ def our_arm(args):
     e2e_value = agg2[0] / agg_t[0]
     n_steps_total = args.warmup + args.steps
 
+    # ---- the modality-agnostic baseline: the same batched server with
+    # selection off (every job at its most accurate, all-modality candidate;
+    # the reference's ``none`` policy) at its own >= 99 % rate -- what
+    # selection buys (MOSEL's headline gain)
+    baseline = None
+    if not args.no_baseline:
+        SERVE_OPTS["top_only"] = True
+        b_rate, b_trials = find_rate(model, sprof, matrix, deadline_ms, args.search_seconds, 0.5 * rate, args.max_job,
+                                     log, cost=cost)
+        if pg is not None:
+            import torch.distributed as tdist
+            t = torch.tensor([b_rate], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+            b_rate = float(t.item())
+        for attempt in range(6):
+            lg3, st3 = serve(model, sprof, matrix, b_rate, seconds, deadline_ms, 7, rank, world,
+                             max_size=args.max_job, cost=cost)
+            timed3 = [r for r in lg3.records if r.arrival_us >= t_lo]
+            agg3 = _allreduce(pg, [sum(r.size for r in timed3 if not r.violated), sum(r.size for r in timed3)],
+                              op="sum")
+            if agg3[0] >= 0.99 * agg3[1]:
+                break
+            log(f"[bench] baseline attainment {agg3[0] / max(1, agg3[1]):.4f} at {b_rate:.1f} req/s: backing off 3%")
+            b_rate *= 0.97
+        SERVE_OPTS["top_only"] = False
+        from paper_2310_18481_b200.records import MetricsLog as _ML
+        pct3 = _ML(lg3.window_us, tuple(timed3)).jct_percentiles_us((50, 99))
+        baseline = {"policy": "no selection: every job at its most accurate (all-modality) candidate in the same "
+                              "batched server (the reference's none policy)",
+                    "value": round(agg3[0] / agg_t[0], 2), "offered_rate_per_gpu": round(b_rate, 1),
+                    "slo_attainment": round(agg3[0] / max(1, agg3[1]), 5), "slo_met": bool(agg3[0] >= 0.99 * agg3[1]),
+                    "latency_ms": {"p50": None if pct3[50] is None else round(pct3[50] / 1000, 3),
+                                   "p99": None if pct3[99] is None else round(pct3[99] / 1000, 3)},
+                    "search": [(round(q, 1), round(v, 4)) for q, v in b_trials]}
+        log(f"[bench] no-selection baseline {baseline['value']:.1f} req/s -> selection gain "
+            f"{value / max(1e-9, baseline['value']):.2f}x")
+
     # ---- roofline of the dominant kernel + compaction
-    roof = dominant_gemm_roofline(model, peaks.get("bf16_tflops"))
+    single = dominant_gemm_roofline(model, peaks.get("bf16_tflops"))
     comp = compaction_roofline(model, peaks.get("hbm_gbs"), max_req)
+    # pass-level (the headline roofline): algorithmic FLOP of every pass served
+    # in the timed region / the sum of those passes' CUDA-event durations, vs
+    # the SUSTAINED bf16 peak (the passes run back to back for seconds)
+    sust = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    ach = st.pass_flops / max(1.0, st.busy_us) / 1e6
+    pass_traffic = None
+    try:  # DRAM bytes of one served-mix pass (all launches) from the committed ncu capture
+        pt = json.loads((ROOT / "profiles" / "r02_pass_traffic.json").read_text())
+        pass_traffic = {"bytes_per_pass": pt["dram_bytes"], "counts": pt["counts"],
+                        "algorithmic_input_bytes": pt.get("algorithmic_bytes")}
+    except Exception:
+        pass_traffic = None
+    roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": sust, "unit": "TFLOP/s",
+            "frac": round(ach / sust, 4), "traffic": pass_traffic,
+            "kernel": "whole served pass (compaction + per-modality encoders + fusion head), FLOP-weighted over "
+                      f"the {st.passes} passes of the timed region",
+            "flop_per_pass_mean": int(st.pass_flops / max(1, st.passes)),
+            "avg_pass_us": round(st.busy_us / max(1, st.passes), 1),
+            "per_template": "profiles/r02_pass_templates.md", "single_launch": single}
 
     # modality-dropping share: requests served without some modality
     drop_share = None
@@ -490,7 +564,11 @@ def our_arm(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": desc,
                    "deadline_ms": deadline_ms, "offered_rate_per_gpu": round(rate, 1),
-                   "arrivals": f"Poisson, job sizes round(max(1,N(1,6))) capped at {args.max_job}",
+                   "arrivals": (f"bursty trace {TRACE.name} mapped to [{TRACE_MIN_FRAC} x peak, peak] "
+                                f"(map_trace_to_qps), offered_rate = peak" if args.arrivals == "trace" else "Poisson")
+                               + f", job sizes round(max(1,N(1,6))) capped at {args.max_job}",
+                   "budgets": (f"varying: deadline_ms x {tuple(MULTS)} per job" if args.budgets == "varying"
+                               else "fixed per-request deadline"),
                    "policy": ("device pass formation ms_pass_select (pass_select_kernel, one warp per "
                               "formation): per-job modality-subset argmax under the formed pass's deadlines "
                               f"(batched P5; pass <= {args.pass_frac} x deadline)")
@@ -503,6 +581,8 @@ def our_arm(args):
                    "step": f"one {win}s real-time serving window", "max_req": max_req,
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
+        "no_selection_baseline": baseline,
+        "selection_gain": None if not baseline else round(value / max(1e-9, baseline["value"]), 3),
         "slo_attainment": round(attainment, 5),
         "slo_met": bool(agg[0] >= 0.99 * agg[1]),
         "policy_step": {"kernel": "pass_select_kernel (ms_pass_select)", "launches": st.policy_launches,
@@ -557,13 +637,19 @@ def main():
                     help="the scheduler plans against deadline - margin (scored on the true deadline)")
     ap.add_argument("--serve-profile", default="marginal", choices=["marginal", "device"],
                     help="scheduler latency table for batched serving")
+    ap.add_argument("--arrivals", default="poisson", choices=["poisson", "trace"],
+                    help="configs[3]: 'trace' = the bursty trace mapped to [0.25 x peak, peak]")
+    ap.add_argument("--budgets", default="fixed", choices=["fixed", "varying"],
+                    help="configs[3]: 'varying' = per-job deadline_ms x {1.0, 1.5, 3.0}")
+    ap.add_argument("--no-baseline", action="store_true", help="skip the no-selection (all-modality) baseline")
     ap.add_argument("--slots", type=int, default=192)
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     SERVE_OPTS.update(sched_margin_us=int(args.sched_margin_ms * 1000), policy_grid_us=int(args.policy_grid_us),
-                      selection=args.selection, pass_frac=args.pass_frac)
+                      selection=args.selection, pass_frac=args.pass_frac, arrivals=args.arrivals,
+                      mults=MULTS if args.budgets == "varying" else None)
     if args.impl == "reference":
         reference_arm(args)
     else:

@@ -54,11 +54,15 @@ class FrontierCache:
     scaled_accuracy(slo)), so (size, that count) keys the cache; rounded-up
     sizes are computed per call."""
 
-    def __init__(self, matrix: StrategyMatrix, K: int):
+    def __init__(self, matrix: StrategyMatrix, K: int, top_only: bool = False):
+        """``top_only``: every job keeps only its most accurate candidate (the
+        reference's ``none`` policy: no modality is ever dropped) -- the
+        modality-agnostic baseline MOSEL is measured against."""
         from .policy import candidates_with_rounding
         self._cwr = candidates_with_rounding
         self.matrix = matrix
         self.K = K
+        self.top_only = top_only
         self._alpha_scaled = sorted(scaled_accuracy(a) for a in matrix.alphas)
         self._sizes = set(matrix.sizes)
         self._cache = {}
@@ -70,10 +74,14 @@ class FrontierCache:
             hit = self._cache.get(key)
             if hit is None:
                 cands = candidates_for_job(self.matrix, size, slo)
+                if self.top_only:
+                    cands = cands[-1:]
                 hit = (cands, FrontierPack(cands, size, self.K) if cands else None)
                 self._cache[key] = hit
             return hit
         cands = self._cwr(self.matrix, size, slo)
+        if self.top_only:
+            cands = cands[-1:]
         return cands, (FrontierPack(cands, size, self.K) if cands else None)
 
 

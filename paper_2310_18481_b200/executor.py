@@ -283,8 +283,12 @@ class MaskedModel:
         return self.head.logits[:n]
 
     def flops(self, masks) -> int:
-        counts = self.counts_for(np.asarray(masks))
-        return sum(e.flops(c) for e, c in zip(self.encoders, counts)) + self.head.flops(len(masks))
+        return self.flops_counts(self.counts_for(np.asarray(masks)), len(masks))
+
+    def flops_counts(self, counts, n: int) -> int:
+        """Algorithmic FLOP of one pass: every present modality's encoder over
+        its compacted count (real channels) + the fusion head over n."""
+        return sum(e.flops(c) for e, c in zip(self.encoders, counts) if c) + self.head.flops(n)
 
     def compaction_bytes(self, masks) -> int:
         """per present (request, modality) the row read (real

@@ -49,6 +49,7 @@ class ServeStats:
     policy_launches: int = 0   # ms_pass_select launches (device policy step)
     policy_device_us: float = 0.0   # launch -> result on the selection stream (CUDA events)
     policy_kernel_us: float = 0.0   # the kernel's own time (device global timer)
+    pass_flops: int = 0             # algorithmic FLOP of the completed passes (roofline numerator)
     formations: list | None = None
 
 
@@ -67,7 +68,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                    max_batch_requests: int | None = None, lead_us: int = 600, trace: bool = False,
                    sched_margin_us: int = 0, policy_grid_us: int = 1000, policy_at_dispatch: bool = False,
                    device_policy=None, selection: str = "policy", max_pass_us: float | None = None,
-                   record_formations: bool = False):
+                   record_formations: bool = False, top_only: bool = False):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -122,7 +123,9 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
     steps (requests arriving during a pass wait for it and then for their
     own).  The reference policies (``policy``) are not run in this mode.
     ``record_formations``: keep every formation's inputs and outputs
-    (``stats.formations``) for the oracle replay.
+    (``stats.formations``) for the oracle replay.  ``top_only``: every job
+    keeps only its most accurate (all-modality) candidate -- the same batched
+    server with selection switched off, the modality-agnostic baseline.
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
@@ -177,7 +180,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         if cost is None:
             raise ValueError("selection='pass' needs a PassCostModel (cost=)")
         from .batcher import DevicePassSelector, FrontierCache
-        fcache = FrontierCache(matrix, model.K)
+        fcache = FrontierCache(matrix, model.K, top_only=top_only)
         selector = DevicePassSelector(model.K, cost.device_table(), cap,
                                       -1 if max_pass_us is None else int(round(max_pass_us * 1000)),
                                       model.mask_ring, record=record_formations)
@@ -335,6 +338,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                     tr.update(start_us=end_us - dur, end_us=end_us, seen_us=now_us())
                     break
         stats.busy_us += dur
+        stats.pass_flops += model.flops_counts(counts, n)
         if cost is not None:
             cost.observe(counts, n, dur)
         flat = [p for ps in preds for p in ps]
