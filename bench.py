@@ -266,11 +266,17 @@ def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world
     sel = o["selection"] if cost is not None else "policy"
     # the pass-length cap scales with the tightest budget in play
     tight_ms = deadline_ms * (min(o["mults"]) if o["mults"] else 1.0)
+    refresher = None
+    if sel == "pass" and o.get("refresh"):  # re-profile from served passes, hot-swap the matrix
+        from paper_2310_18481_b200.refresh import ProfileRefresher
+        r = o["refresh"]
+        refresher = ProfileRefresher(cost, r["modalities"], r["accuracy"], r["max_batch"], r["sizes"], r["alphas"],
+                                     period_s=r["period_s"])
     return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed, cost=cost,
                           policy=Policy.NONE if sel == "pass" else Policy.OPTIMIZED,
                           sched_margin_us=o["sched_margin_us"], policy_grid_us=o["policy_grid_us"],
                           selection=sel, max_pass_us=o["pass_frac"] * tight_ms * 1000 if sel == "pass" else None,
-                          top_only=o["top_only"])
+                          top_only=o["top_only"], refresher=refresher)
 
 
 def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, log=print,
@@ -417,6 +423,10 @@ def our_arm(args):
         log(f"[bench] serving profile (marginal): all-modality b1 {sprof.part_latency_us(full, 1)} us, "
             f"b{args.profile_batch} {sprof.part_latency_us(full, args.profile_batch)} us")
     matrix = build_matrix(sprof, range(1, args.max_job + 1), recommended_alphas(sprof))
+    if cost is not None and args.refresh_s > 0 and args.serve_profile == "marginal":
+        SERVE_OPTS["refresh"] = {"modalities": mod_names, "accuracy": accuracy, "max_batch": args.profile_batch,
+                                 "sizes": tuple(range(1, args.max_job + 1)), "alphas": matrix.alphas,
+                                 "period_s": args.refresh_s}
     rate, trials = find_rate(model, sprof, matrix, deadline_ms, args.search_seconds, cap, args.max_job,
                              log, cost=cost)
     if pg is not None:  # every replica runs at the slowest replica's rate
@@ -581,6 +591,12 @@ def our_arm(args):
                    "step": f"one {win}s real-time serving window", "max_req": max_req,
                    "parallelism": f"replicas x{world} (no collective)",
                    "l2": "clip pool + activations >> 126 MB L2 (inputs larger than L2)"},
+        "refresh": None if not st.refreshes else {
+            "period_s": args.refresh_s, "swaps": len(st.refreshes),
+            "build_ms_mean": round(1000 * float(np.mean([r.build_s for r in st.refreshes])), 1),
+            "what": "served-pass CUDA-event durations -> re-fitted pass cost knots -> marginal profile -> "
+                    "device-DP matrix (fingerprint-checked) hot-swapped between formations",
+            "last_knots_us": [(n, round(t, 1)) for n, t in st.refreshes[-1].knots_after]},
         "no_selection_baseline": baseline,
         "selection_gain": None if not baseline else round(value / max(1e-9, baseline["value"]), 3),
         "slo_attainment": round(attainment, 5),
@@ -642,6 +658,8 @@ def main():
     ap.add_argument("--budgets", default="fixed", choices=["fixed", "varying"],
                     help="configs[3]: 'varying' = per-job deadline_ms x {1.0, 1.5, 3.0}")
     ap.add_argument("--no-baseline", action="store_true", help="skip the no-selection (all-modality) baseline")
+    ap.add_argument("--refresh-s", type=float, default=2.0,
+                    help="profiler -> matrix refresh period during serving (0: off)")
     ap.add_argument("--slots", type=int, default=192)
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--cpu-steps", type=int, default=6)

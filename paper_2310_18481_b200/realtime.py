@@ -50,6 +50,7 @@ class ServeStats:
     policy_device_us: float = 0.0   # launch -> result on the selection stream (CUDA events)
     policy_kernel_us: float = 0.0   # the kernel's own time (device global timer)
     pass_flops: int = 0             # algorithmic FLOP of the completed passes (roofline numerator)
+    refreshes: list | None = None   # matrix hot-swaps during the run (refresh.Refresh)
     formations: list | None = None
 
 
@@ -68,7 +69,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                    max_batch_requests: int | None = None, lead_us: int = 600, trace: bool = False,
                    sched_margin_us: int = 0, policy_grid_us: int = 1000, policy_at_dispatch: bool = False,
                    device_policy=None, selection: str = "policy", max_pass_us: float | None = None,
-                   record_formations: bool = False, top_only: bool = False):
+                   record_formations: bool = False, top_only: bool = False, refresher=None):
     """Serve ``templates`` (JobTemplates, arrival-sorted) in real time.
 
     ``depth`` jobs may be in flight on the GPU stream at once: the next job
@@ -126,6 +127,10 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
     (``stats.formations``) for the oracle replay.  ``top_only``: every job
     keeps only its most accurate (all-modality) candidate -- the same batched
     server with selection switched off, the modality-agnostic baseline.
+    ``refresher``: a ``refresh.ProfileRefresher``: served
+    passes re-profile the cost model, a background thread rebuilds the
+    serving profile and matrix, and the loop swaps them in between two
+    formations (``stats.refreshes``).
 
     Returns (MetricsLog, ServeStats).  Job ids are 1-based stream order.
     """
@@ -176,6 +181,9 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
 
     cap = min(max_batch_requests or model.max_req, model.max_req)
     selector = fcache = None
+    if refresher is not None:
+        stats.refreshes = []
+    FrontierCache = None
     if selection == "pass":
         if cost is None:
             raise ValueError("selection='pass' needs a PassCostModel (cost=)")
@@ -339,6 +347,8 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                     break
         stats.busy_us += dur
         stats.pass_flops += model.flops_counts(counts, n)
+        if refresher is not None:
+            refresher.observe(counts, n, dur)
         if cost is not None:
             cost.observe(counts, n, dur)
         flat = [p for ps in preds for p in ps]
@@ -385,6 +395,15 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
             arrived = True
         while inflight and inflight[0][2].done():  # non-blocking completion checks
             finish()
+        if refresher is not None and selector is not None:
+            res = refresher.poll()
+            if res is not None:  # hot-swap between two formations
+                cost, profile, matrix = res.cost, res.profile, res.matrix
+                fcache = FrontierCache(matrix, model.K, top_only=top_only)
+                selector.cost = cost.device_table()
+                stats.refreshes.append(res)
+            elif refresher.due(now / 1e6):
+                refresher.start(now / 1e6)
         if policy is not Policy.NONE and since_opt > 0 and len(queue) and not policy_at_dispatch and \
                 (since_opt >= watermark or not inflight):
             run_policy(now_us())
@@ -410,6 +429,8 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
                 time.sleep((wait - 100) / 1e6)
     torch.cuda.synchronize()
     stats.wall_s = time.perf_counter() - t0
+    if refresher is not None:
+        refresher.close()
     if selector is not None:
         stats.policy_launches = selector.launches
         stats.policy_device_us = selector.device_us

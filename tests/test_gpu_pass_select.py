@@ -116,3 +116,46 @@ def test_served_formations_replay_bit_exact(dev):
         served = [r for r in log.records if not r.dropped]
         assert all(r.achieved_accuracy >= r.accuracy_slo for r in served)
     assert n_form >= 1000, n_form
+
+
+def test_refresh_loop_hot_swaps_matrix_without_slo_dip(dev, tmp_path):
+    """a serving run whose cost model starts 25 % optimistic
+    re-profiles itself from its own passes' CUDA-event times, rebuilds the
+    serving profile + matrix on the device in the background and swaps them
+    in mid-run: >= 1 swap, the re-fitted knots move toward the measured
+    passes, the run stays >= 99 % on time, and every swapped matrix is
+    byte-identical to a host-DP rebuild of its profile with a matching
+    fingerprint (strategy.py:505-520)."""
+    import paper_2310_18481_b200 as ms
+    from paper_2310_18481_b200.executor import build_tbn_model
+    from paper_2310_18481_b200.planner import build_matrix, save_matrix
+    from paper_2310_18481_b200.policy import Policy
+    from paper_2310_18481_b200.profiler import (TBN_ACCURACY, PassCostModel, marginal_profile,
+                                                profile_pass_costs)
+    from paper_2310_18481_b200.realtime import serve_realtime
+    from paper_2310_18481_b200.refresh import ProfileRefresher
+    model = build_tbn_model(max_req=96, n_slots=192)
+    true = profile_pass_costs(model, reps=2)
+    skew = PassCostModel(true.enc_us, true.head_us, true.compact_us, pass_all_us=[(n, 0.75 * t) for n, t in true.pass_all])
+    mods = ("rgb", "flow", "audio")
+    prof = marginal_profile(skew, mods, TBN_ACCURACY, max_batch=8)
+    matrix = ms.build_matrix(prof, range(1, 25), ms.recommended_alphas(prof))
+    ref = ProfileRefresher(skew, mods, TBN_ACCURACY, 8, range(1, 25), matrix.alphas, period_s=0.5)
+    spec = ms.WorkloadSpec(kind="poisson", qps=12000, duration_s=4, deadline_ms=15, seed=9)
+    jobs = [ms.JobTemplate(j.arrival_us, min(j.size, 24), j.accuracy_slo, j.deadline_us)
+            for j in ms.generate_jobs(spec, prof)]
+    log, st = serve_realtime(model, prof, matrix, jobs, cost=skew, policy=Policy.NONE, selection="pass",
+                             max_pass_us=3000, refresher=ref)
+    assert len(st.refreshes) >= 1
+    assert log.violation_ratio() <= 0.01, log.violation_ratio()
+    for r in st.refreshes:
+        assert r.matrix.profile_fingerprint == r.profile.fingerprint()
+        save_matrix(r.matrix, tmp_path / "dev.json")
+        save_matrix(build_matrix(r.profile, range(1, 25), matrix.alphas), tmp_path / "host.json")
+        assert (tmp_path / "dev.json").read_bytes() == (tmp_path / "host.json").read_bytes()
+    # the busiest knot moved toward the measured pass time
+    last = dict(st.refreshes[-1].knots_after)
+    moved = [n for n, t in skew.pass_all if last[n] != t]
+    assert moved
+    for n in moved:
+        assert abs(last[n] - true.pass_all_us(n)) < abs(0.75 * true.pass_all_us(n) - true.pass_all_us(n))

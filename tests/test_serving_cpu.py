@@ -3,6 +3,7 @@ the marginal (batched) latency table fed to the reference scheduler, and the
 knapsack-quantum extension of the reference's OPTIMIZED policy."""
 
 import numpy as np
+import pytest
 
 from paper_2310_18481_b200.planner import build_matrix, recommended_alphas
 from paper_2310_18481_b200.policy import Policy, apply_policy
@@ -60,3 +61,21 @@ def test_fine_knapsack_grid_downgrades_where_the_1ms_grid_drops():
     d2 = apply_policy(Policy.OPTIMIZED, q2, 0, FeedbackState(), grid_us=50)
     assert len(d1) > len(d2) == 0
     assert any(j.assigned_idx == 0 for j in q2.jobs())
+
+
+def test_refresher_refit_scales_knots_toward_observations():
+    """The refresh loop's re-fit (refresh.py): knots with enough nearby
+    observations take the median observed/modelled ratio; the others keep
+    their time; the result is non-decreasing."""
+    from paper_2310_18481_b200.profiler import PassCostModel
+    from paper_2310_18481_b200.refresh import ProfileRefresher
+    enc = [[100.0 + i for i in range(96)]] * 3
+    cost = PassCostModel(enc, [20.0] * 96, 10.0, pass_all_us=[(1, 400.0), (8, 800.0), (32, 2000.0), (96, 6000.0)])
+    r = ProfileRefresher(cost, ("a", "b", "c"), (0.5,) * 7, 8, range(1, 9), (0.0, 0.5), min_obs=4)
+    for _ in range(10):  # observed 20 % slower near n = 8 (work 8)
+        r.observe([8, 8, 8], 8, 960.0)
+    obs = r._obs
+    knots = r.refit(obs)
+    assert dict(knots)[8] == pytest.approx(960.0)
+    assert dict(knots)[1] == 400.0 and dict(knots)[96] == 6000.0
+    assert all(b[1] >= a[1] for a, b in zip(knots, knots[1:]))

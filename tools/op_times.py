@@ -20,6 +20,7 @@ ap.add_argument("--mixed", action="store_true")
 ap.add_argument("--mask", type=int, default=7)
 ap.add_argument("--top", type=int, default=45)
 ap.add_argument("--rep", type=int, default=10)
+ap.add_argument("--counts", type=int, nargs=3, default=None, help="per-modality request counts (served mix)")
 a = ap.parse_args()
 REP = a.rep
 
@@ -34,6 +35,11 @@ from paper_2310_18481_b200.executor import build_tbn_model  # noqa: E402
 m = build_tbn_model(max_req=a.n, n_slots=max(8, a.n))
 rng = np.random.default_rng(0)
 masks = rng.integers(1, 8, size=a.n).astype(np.int16) if a.mixed else np.full(a.n, a.mask, dtype=np.int16)
+if a.counts:
+    masks = np.zeros(a.n, dtype=np.int16)
+    for k, c in enumerate(a.counts):
+        masks[rng.permutation(a.n)[:c]] |= 1 << k
+    masks[masks == 0] = 1
 slots = np.arange(a.n) % m.n_slots
 m.use_graphs = False
 for _ in range(2):
@@ -77,6 +83,10 @@ for k, (enc, c) in enumerate(zip(m.encoders, counts)):
             lab = f"{'max' if op[10] else 'avg'} {op[6]}x{op[6]}/{op[7]} C={op[4]} {op[1]}x{op[2]}x{op[3]}"
         else:
             lab = ""
+        if kind == "gemm":
+            info = op.info()
+            lab += f" [grid {info['grid_x']}x{info['grid_y']} st{info['stages']} smem{info['smem_bytes'] // 1024}K" \
+                   f"{' pair' if getattr(op, 'pair', False) else ''}{' sk' + str(op.split_k) if op.split_k > 1 else ''}]"
         rows.append((us, k, i, kind, lab, fl))
 tot = sum(r[0] for r in rows)
 gem = [r for r in rows if r[3] == "gemm"]
