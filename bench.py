@@ -271,7 +271,7 @@ def serve(model, profile, matrix, qps, seconds, deadline_ms, seed, rank=0, world
         from paper_2310_18481_b200.refresh import ProfileRefresher
         r = o["refresh"]
         refresher = ProfileRefresher(cost, r["modalities"], r["accuracy"], r["max_batch"], r["sizes"], r["alphas"],
-                                     period_s=r["period_s"])
+                                     period_s=r["period_s"], top_only=o["top_only"])
     return serve_realtime(model, profile, matrix, jobs, host_clips=host_clips, slot_seed=seed, cost=cost,
                           policy=Policy.NONE if sel == "pass" else Policy.OPTIMIZED,
                           sched_margin_us=o["sched_margin_us"], policy_grid_us=o["policy_grid_us"],

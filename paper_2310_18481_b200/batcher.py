@@ -67,6 +67,26 @@ class FrontierCache:
         self._sizes = set(matrix.sizes)
         self._cache = {}
 
+    def warm_iter(self):
+        """Fill every (profiled size, alpha count) entry, one per step (a
+        frontier depends on the SLO only through that count): afterwards
+        lookups during serving never miss."""
+        for size in sorted(self._sizes):
+            for c in range(len(self._alpha_scaled) + 1):
+                if (size, c) in self._cache:
+                    continue
+                # an SLO whose scaled value bisects to c
+                s_scaled = self._alpha_scaled[c] if c < len(self._alpha_scaled) else self._alpha_scaled[-1] + 1
+                slo = s_scaled / 1e4
+                if bisect.bisect_left(self._alpha_scaled, scaled_accuracy(slo)) != c:
+                    continue  # float round trip landed elsewhere: leave it to lookup()
+                self.lookup(size, slo)
+                yield size, c
+
+    def warm(self) -> None:
+        for _ in self.warm_iter():
+            pass
+
     def lookup(self, size: int, slo: float):
         """(candidates, FrontierPack or None when empty)."""
         if size in self._sizes:

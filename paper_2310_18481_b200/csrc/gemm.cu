@@ -197,8 +197,20 @@ __device__ __forceinline__ void convert_chunk(const uint32_t (&v)[32], const flo
 struct TileIdx {
   int m, n, kb0, kb1;
 };
-__device__ __forceinline__ TileIdx decode_tile(const GemmParams& p, int t, int n_tiles) {
+// PAIR: t enumerates (m pair, n) tiles; CTA `rank` of the pair owns M tile
+// 2 * pair + rank (the peer of an odd last pair reads and writes nothing:
+// its boxes lie wholly out of bounds -- TMA zero-fills / clips them)
+template <int PAIR>
+__device__ __forceinline__ TileIdx decode_tile(const GemmParams& p, int t, int n_tiles, uint32_t rank) {
   TileIdx r;
+  if (PAIR) {
+    const int mp = t / n_tiles;
+    r.m = 2 * mp + (int)rank;
+    r.n = t - mp * n_tiles;
+    r.kb0 = 0;
+    r.kb1 = p.num_kb;
+    return r;
+  }
   const int kp = t % p.ksplit;
   const int mn = t / p.ksplit;
   r.m = mn / n_tiles;
@@ -231,7 +243,18 @@ __device__ __forceinline__ void convert_chunk4(const uint32_t (&v)[32], const fl
 // One kernel instantiation per (A-operand mode, epilogue, activation): each
 // carries only its own code (the generic kernel's every-mode/every-activation
 // epilogue was instruction-latency bound at ~1 us per 32-column chunk).
-template <int MODE, int EPI, int ACT>
+//
+// PAIR = 1: CTA-pair variant (clusters of 2 on an SM pair,
+// tcgen05.mma.cta_group::2, M = 256 per instruction).  Each CTA loads its own
+// 128-row A block (or halo) and HALF of the BN weight rows, so the weight
+// bytes each SM pulls from L2 halve (the 3x3 convs below 56^2 are L2-read
+// bound: ~42 B/clk/SM with every SM loading, MEASURED_PEAKS / B300 notes), and
+// an N <= 96 MMA is no longer A-operand SMEM-read bound.  Protocol:
+//   full[s], afull[h] (leader) : one arrive.expect_tx of BOTH CTAs' bytes; the
+//                                peer's TMA completes on the leader's barrier
+//   empty[s], aempty[h], tfull : multicast tcgen05.commit from the leader
+//   tempty[a] (leader)         : both CTAs' epilogue warps arrive (remote)
+template <int MODE, int EPI, int ACT, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ GemmParams p, const __grid_constant__ StoreMaps tmD) {
@@ -262,7 +285,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_tiles = (p.N + p.BN - 1) / p.BN;
-  const int num_tiles = p.m_tiles * n_tiles * p.ksplit;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int num_tiles = PAIR ? ((p.m_tiles + 1) / 2) * n_tiles : p.m_tiles * n_tiles * p.ksplit;
+  const int cta0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // this CTA's (pair's) first tile
+  const int ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // the leader's barrier for a pair's shared completions (own barrier otherwise)
 
   if (threadIdx.x == 0) {
     const uint32_t full_count = (MODE == MODE_GATHER) ? 1 + 128 : 1;
@@ -272,8 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      // one arrive per epilogue warp (per warp of the owning group with tile groups)
-      mbar_init(&tempty[a], (EPI == EPI_TMA && MODE != MODE_GATHER && p.tile_groups) ? kEpiWarps / 2 : kEpiWarps);
+      // one arrive per epilogue warp (per warp of the owning group with tile
+      // groups), from both CTAs of a pair
+      mbar_init(&tempty[a], ((EPI == EPI_TMA && MODE != MODE_GATHER && p.tile_groups) ? kEpiWarps / 2 : kEpiWarps) *
+                                (PAIR ? 2 : 1));
       mbar_init(&afull[a], 1);
       mbar_init(&aempty[a], 1);
     }
@@ -286,12 +316,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t acc_stride = 32;
   while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
   const uint32_t tmem_cols = 2 * acc_stride;
-  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 1) {
+    if (PAIR)
+      tmem_alloc_pair(tmem_slot, tmem_cols);
+    else
+      tmem_alloc(tmem_slot, tmem_cols);
+  }
   const int nb_pad = (p.N + 31) & ~31;
   for (int i = threadIdx.x; i < nb_pad && i < kMaxBias; i += blockDim.x)
     sbias[i] = (p.bias != nullptr && i < p.N) ? p.bias[i] : 0.0f;
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // barrier inits + TMEM allocation visible to the pair
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // PDL: this prologue overlapped the previous kernel's tail.  Trigger only
@@ -309,19 +347,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0, hphase = 0;
       if (p.b_resident) {  // this CTA's N tile of weights once, before the first halo
         // (grid is a multiple of n_tiles, so every tile t of this CTA has n = t % n_tiles fixed)
-        const int n_tile = (int)(blockIdx.x % n_tiles);
-        mbar_arrive_expect_tx(&full[0], 9 * p.cchunks * p.b_bytes);
-        for (int kb = 0; kb < 9 * p.cchunks; ++kb)
-          tma_load_2d(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK, n_tile * p.BN);
+        const int n_tile = cta0 % n_tiles;
+        if (leader) mbar_arrive_expect_tx(&full[0], 9 * p.cchunks * p.b_bytes * (PAIR ? 2 : 1));
+        for (int kb = 0; kb < 9 * p.cchunks; ++kb) {
+          if (PAIR)
+            tma_load_2d_pair(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK,
+                             n_tile * p.BN + (int)rank * (p.BN / 2));
+          else
+            tma_load_2d(smem_addr(smB + kb * p.b_bytes), &tmB, &full[0], kb * kBK, n_tile * p.BN);
+        }
       }
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const TileIdx ti = decode_tile(p, t, n_tiles);
+      for (int t = cta0; t < num_tiles; t += ncta) {
+        const TileIdx ti = decode_tile<PAIR>(p, t, n_tiles, rank);
         const int th = ti.m % p.tiles_h;
         const int img = ti.m / p.tiles_h;
         for (int cc = 0; cc < p.cchunks; ++cc) {
           mbar_wait(&aempty[hs], hphase ^ 1);
-          mbar_arrive_expect_tx(&afull[hs], p.a_bytes);
-          tma_load_4d(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&afull[hs], 2 * p.a_bytes);
+            tma_load_4d_pair(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
+          } else {
+            mbar_arrive_expect_tx(&afull[hs], p.a_bytes);
+            tma_load_4d(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
+          }
           if (p.b_resident) {
             if (++hs == 2) {
               hs = 0;
@@ -331,9 +379,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int tap = 0; tap < 9; ++tap) {
             mbar_wait(&empty[s], phase ^ 1);
-            mbar_arrive_expect_tx(&full[s], p.b_bytes);
-            tma_load_2d(smem_addr(smB + s * p.b_bytes), &tmB, &full[s], (tap * p.cchunks + cc) * kBK,
-                        ti.n * p.BN);
+            if (PAIR) {
+              if (leader) mbar_arrive_expect_tx(&full[s], 2 * p.b_bytes);
+              tma_load_2d_pair(smem_addr(smB + s * p.b_bytes), &tmB, &full[s], (tap * p.cchunks + cc) * kBK,
+                               ti.n * p.BN + (int)rank * (p.BN / 2));
+            } else {
+              mbar_arrive_expect_tx(&full[s], p.b_bytes);
+              tma_load_2d(smem_addr(smB + s * p.b_bytes), &tmB, &full[s], (tap * p.cchunks + cc) * kBK,
+                          ti.n * p.BN);
+            }
             if (++s == stages) {
               s = 0;
               phase ^= 1;
@@ -350,8 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t phase = 0;
       const uint32_t tx = (MODE == MODE_GATHER ? 0 : p.a_bytes) + p.b_bytes;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const TileIdx ti = decode_tile(p, t, n_tiles);
+      for (int t = cta0; t < num_tiles; t += ncta) {
+        const TileIdx ti = decode_tile<PAIR>(p, t, n_tiles, rank);
         const int m_tile = ti.m, n_tile = ti.n;
         int n0 = 0, oh0 = 0, ow0 = 0;
         if constexpr (kConv) {
@@ -366,15 +420,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], phase ^ 1);
           const uint32_t a_dst = smem_addr(smA + s * kABytes);
           const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
-          mbar_arrive_expect_tx(&full[s], tx);
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full[s], 2 * tx);
+          } else {
+            mbar_arrive_expect_tx(&full[s], tx);
+          }
           if constexpr (MODE == MODE_DENSE) {
-            tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
+            if (PAIR)
+              tma_load_2d_pair(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
+            else
+              tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
           } else if constexpr (MODE == MODE_CONV) {
             const int tap = kb / p.cchunks;
             const int cc = kb - tap * p.cchunks;
             const int kh = tap / p.KW;
             const int kw = tap - kh * p.KW;
-            tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
+            if (PAIR)
+              tma_load_4d_pair(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
+            else
+              tma_load_4d(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
           } else if constexpr (MODE == MODE_CONV_SMALLC) {
             const int kh = kb / p.smallc_halves;
             const int half = kb - kh * p.smallc_halves;
@@ -404,11 +468,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int h = min(2 * kb + l, 9 * parts - 1);
               const int tap = h / parts, part = h - tap * parts;
               const int kh = tap / 3, kw = tap - 3 * (tap / 3);
-              tma_load_4d(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, ow0 + kw, oh0 + kh, n0);
+              if (PAIR)
+                tma_load_4d_pair(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, ow0 + kw, oh0 + kh, n0);
+              else
+                tma_load_4d(a_dst + l * (kABytes / 2), &tmA, &full[s], part * 32, ow0 + kw, oh0 + kh, n0);
             }
           }
-          tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
-          if (t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(3);
+          if (PAIR)
+            tma_load_2d_pair(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN + (int)rank * (p.BN / 2));
+          else
+            tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN);
+          if (t == cta0 && kb == ti.kb0) GEMM_TRACE(3);
           if (++s == stages) {
             s = 0;
             phase ^= 1;
@@ -416,9 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1 && MODE == MODE_CONV_HALO) {
+  } else if (warp == 1 && MODE == MODE_CONV_HALO && leader) {
     // ------------------------------------ MMA issuer: 9 shifted views per halo
-    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)p.BN);
+    const uint32_t idesc = PAIR ? umma_idesc_bf16_m256((uint32_t)p.BN) : umma_idesc_bf16_m128((uint32_t)p.BN);
     int s = 0, hs = 0;
     uint32_t phase = 0, hphase = 0;
     int acc = 0;
@@ -428,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[0], 0);
       tc_fence_after();
     }
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cta0; t < num_tiles; t += ncta) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
@@ -444,11 +514,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t adesc = umma_desc_sw128(halo + (uint32_t)((dy * P + dx) * 128));
               const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + (tap * p.cchunks + cc) * p.b_bytes));
 #pragma unroll
-              for (int k = 0; k < kBK / 16; ++k)
-                umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+              for (int k = 0; k < kBK / 16; ++k) {
+                if (PAIR)
+                  umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+                else
+                  umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+              }
             }
-            umma_commit(&aempty[hs]);
-            if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+            if (PAIR) {
+              umma_commit_pair(&aempty[hs], 0x3);
+              if (cc == p.cchunks - 1) umma_commit_pair(&tfull[acc], 0x3);
+            } else {
+              umma_commit(&aempty[hs]);
+              if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+            }
           }
           __syncwarp();
           if (++hs == 2) {
@@ -465,12 +544,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t adesc = umma_desc_sw128(halo + (uint32_t)((dy * P + dx) * 128));
             const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
-            umma_commit(&empty[s]);
-            if (tap == 8) {
-              umma_commit(&aempty[hs]);
-              if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+            for (int k = 0; k < kBK / 16; ++k) {
+              if (PAIR)
+                umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+              else
+                umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cc | tap | k) != 0);
+            }
+            if (PAIR) {
+              umma_commit_pair(&empty[s], 0x3);
+              if (tap == 8) {
+                umma_commit_pair(&aempty[hs], 0x3);
+                if (cc == p.cchunks - 1) umma_commit_pair(&tfull[acc], 0x3);
+              }
+            } else {
+              umma_commit(&empty[s]);
+              if (tap == 8) {
+                umma_commit(&aempty[hs]);
+                if (cc == p.cchunks - 1) umma_commit(&tfull[acc]);
+              }
             }
           }
           __syncwarp();
@@ -487,15 +578,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && MODE != MODE_CONV_HALO && leader) {
     // -------------------------------------------------- MMA issuer
-    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)p.BN);
+    const uint32_t idesc = PAIR ? umma_idesc_bf16_m256((uint32_t)p.BN) : umma_idesc_bf16_m128((uint32_t)p.BN);
     int s = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const TileIdx ti = decode_tile(p, t, n_tiles);
+    for (int t = cta0; t < num_tiles; t += ncta) {
+      const TileIdx ti = decode_tile<PAIR>(p, t, n_tiles, rank);
       mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
@@ -503,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], phase);
         tc_fence_after();
         if constexpr (MODE == MODE_GATHER) fence_proxy_async_smem();
-        if (lane == 0 && t == (int)blockIdx.x && kb == ti.kb0) GEMM_TRACE(4);
+        if (lane == 0 && t == cta0 && kb == ti.kb0) GEMM_TRACE(4);
         if (lane == 0) {
           const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
           if constexpr (MODE == MODE_CONV_C4 || MODE == MODE_CONV_C12 || MODE == MODE_CONV_K32) {  // 2 SW64 halves
@@ -511,20 +602,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
               const uint64_t adesc = umma_desc_sw64(a0 + (k >> 1) * (kABytes / 2)) + 2 * (k & 1);
-              umma_bf16(d_tmem, adesc, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+              if (PAIR)
+                umma_bf16_pair(d_tmem, adesc, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+              else
+                umma_bf16(d_tmem, adesc, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
             }
           } else {
             const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
               // +32 bytes per 16-element K step inside the swizzled row (>>4 = 2)
-              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+              if (PAIR)
+                umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
+              else
+                umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != ti.kb0) || k != 0);
             }
           }
-          umma_commit(&empty[s]);
-          if (kb == ti.kb1 - 1) {
-            umma_commit(&tfull[acc]);
-            GEMM_TRACE(5);
+          if (PAIR) {
+            umma_commit_pair(&empty[s], 0x3);
+            if (kb == ti.kb1 - 1) umma_commit_pair(&tfull[acc], 0x3);
+          } else {
+            umma_commit(&empty[s]);
+            if (kb == ti.kb1 - 1) {
+              umma_commit(&tfull[acc]);
+              GEMM_TRACE(5);
+            }
           }
         }
         __syncwarp();
@@ -536,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-  } else {
+  } else if (warp >= 2) {
     // ---------------------- warps 2..9: gather (2..5) + epilogue (all 8)
     const int q = warp & 3;               // TMEM lane quarter of this warp
     const int grp = (warp - 2) >> 2;      // column-chunk group: chunks c with c % 2 == grp
@@ -554,13 +656,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // so two tiles' epilogues run at once instead of one tile's two halves
     const bool tg = EPI == EPI_TMA && MODE != MODE_GATHER && p.tile_groups;
     const int cs = tg ? 1 : 2;  // chunk step
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    // a pair's accumulator-empty barriers live in the leader CTA
+    const uint32_t tempty_bar0 = PAIR ? mapa_shared(smem_addr(&tempty[0]), 0) : 0u;
+    for (int t = cta0; t < num_tiles; t += ncta) {
       if (tg && acc != grp) {  // the other group's tile
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         continue;
       }
-      const TileIdx ti = decode_tile(p, t, n_tiles);
+      const TileIdx ti = decode_tile<PAIR>(p, t, n_tiles, rank);
       const int m_tile = ti.m, n_tile = ti.n;
       if constexpr (MODE == MODE_GATHER) {
         if (grp == 0) {
@@ -614,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (warp == 2 && lane == 0 && t == (int)blockIdx.x) GEMM_TRACE(6);
+      if (warp == 2 && lane == 0 && t == cta0) GEMM_TRACE(6);
       const uint32_t t_base = tmem_base + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
       const int n_first = n_tile * p.BN;
       const int n_chunks = (min(p.BN, p.N - n_first) + 31) >> 5;
@@ -623,11 +727,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto release_acc = [&]() {  // every TMEM read of this accumulator has completed
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(tempty_bar0 + (uint32_t)acc * 8u);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
       };
       auto process = [&](const uint32_t (&v)[32], int c) {
         const int nb = n_first + c * 32;
-        const bool tr0 = warp == 2 && lane == 0 && t == (int)blockIdx.x && c == grp;
+        const bool tr0 = warp == 2 && lane == 0 && t == cta0 && c == grp;
         if (tr0) GEMM_TRACE(8);
         if constexpr (EPI == EPI_SPLITK) {
           // this K part's partial sums -> its own workspace slab (plain stores;
@@ -762,38 +871,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         c += cs;
       }
       if (!tg && grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
-      if (warp == 2 && lane == 0 && t == (int)blockIdx.x) GEMM_TRACE(11);
+      if (warp == 2 && lane == 0 && t == cta0) GEMM_TRACE(11);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
     if (EPI == EPI_TMA && (issuer || (p.warp_store && lane == 0))) bulk_wait0();
     if (warp == 2 && lane == 0) GEMM_TRACE(7);
   }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols);
+  if (PAIR) {
+    tc_fence_before();
+    cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, tmem_cols);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc(tmem_base, tmem_cols);
+    }
   }
 }
 
 typedef void (*GemmKernelFn)(const CUtensorMap, const CUtensorMap, const GemmParams, const StoreMaps);
 
-template <int MODE, int EPI>
+template <int MODE, int EPI, int PAIR = 0>
 static GemmKernelFn pick_act(int act) {
   switch (act) {
-    case MS_ACT_RELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_RELU>;
-    case MS_ACT_GELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_GELU>;
-    case MS_ACT_TANH: return gemm_tc_kernel<MODE, EPI, MS_ACT_TANH>;
-    default: return gemm_tc_kernel<MODE, EPI, MS_ACT_NONE>;
+    case MS_ACT_RELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_RELU, PAIR>;
+    case MS_ACT_GELU: return gemm_tc_kernel<MODE, EPI, MS_ACT_GELU, PAIR>;
+    case MS_ACT_TANH: return gemm_tc_kernel<MODE, EPI, MS_ACT_TANH, PAIR>;
+    default: return gemm_tc_kernel<MODE, EPI, MS_ACT_NONE, PAIR>;
   }
 }
 
 // The instantiation for a plan (null if the combination is unsupported).
 static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
+  if (p.pair) {  // CTA pairs: bf16 TMA-store epilogue only (set_pair checks)
+    switch (p.mode) {
+      case MODE_DENSE: return pick_act<MODE_DENSE, EPI_TMA, 1>(p.relu);
+      case MODE_CONV: return pick_act<MODE_CONV, EPI_TMA, 1>(p.relu);
+      case MODE_CONV_K32: return pick_act<MODE_CONV_K32, EPI_TMA, 1>(p.relu);
+      case MODE_CONV_HALO: return pick_act<MODE_CONV_HALO, EPI_TMA, 1>(p.relu);
+      default: return nullptr;
+    }
+  }
   if (p.ksplit > 1) {
-    if (p.mode == MODE_DENSE) return gemm_tc_kernel<MODE_DENSE, EPI_SPLITK, MS_ACT_NONE>;
-    if (p.mode == MODE_GATHER) return gemm_tc_kernel<MODE_GATHER, EPI_SPLITK, MS_ACT_NONE>;
-    if (p.mode == MODE_CONV) return gemm_tc_kernel<MODE_CONV, EPI_SPLITK, MS_ACT_NONE>;
+    if (p.mode == MODE_DENSE) return gemm_tc_kernel<MODE_DENSE, EPI_SPLITK, MS_ACT_NONE, 0>;
+    if (p.mode == MODE_GATHER) return gemm_tc_kernel<MODE_GATHER, EPI_SPLITK, MS_ACT_NONE, 0>;
+    if (p.mode == MODE_CONV) return gemm_tc_kernel<MODE_CONV, EPI_SPLITK, MS_ACT_NONE, 0>;
     return nullptr;
   }
   if (p.out_fp32) {
@@ -815,241 +942,6 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
   }
 }
 
-
-// ------------------------------------------------------------------------
-// CTA-pair (2-SM) variant for DENSE / CONV plans: clusters of 2 CTAs on an
-// SM pair compute 256 x BN tiles with tcgen05.mma.cta_group::2 (M = 256),
-// issued by the leader CTA only.  Each CTA loads its own 128-row A block and
-// HALF of the BN weight rows, so each tensor instruction does twice the work
-// of the single-SM kernel and weight traffic per CTA halves.  Protocol:
-//   full[s]   (leader)  : count 2 = one arrive.expect_tx per CTA; both CTAs'
-//                         TMA bytes complete on it (.cta_group::2 loads)
-//   empty[s]  (each CTA): multicast tcgen05.commit from the leader
-//   tfull[a]  (each CTA): multicast commit after a tile's last K block
-//   tempty[a] (leader)  : count 2*kEpiWarps, peer epilogue arrives remotely
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ GemmParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  const int stages = p.stages;
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + stages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smB + stages * p.b_bytes);
-  uint64_t* empty = full + stages;
-  uint64_t* tfull = empty + stages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);
-  sstage += (16u - (smem_addr(sstage) & 15u)) & 15u;
-  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int n_tiles = (p.N + p.BN - 1) / p.BN;
-  const int m_pairs = (p.m_tiles + 1) / 2;
-  const int num_tiles = m_pairs * n_tiles;
-  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const int half_bn = p.BN / 2;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < stages; ++i) {
-      mbar_init(&full[i], 1);  // leader's arrive.expect_tx of BOTH CTAs' bytes
-      mbar_init(&empty[i], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-  }
-  uint32_t acc_stride = 32;
-  while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
-  const uint32_t tmem_cols = 2 * acc_stride;
-  if (warp == 1) tmem_alloc_pair(tmem_slot, tmem_cols);
-  for (int i = threadIdx.x; i < p.N; i += blockDim.x) sbias[i] = p.bias != nullptr ? p.bias[i] : 0.0f;
-  tc_fence_before();
-  cluster_sync_all();  // barrier inits + TMEM allocation visible to the pair
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
-  pdl_wait();
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------------------------------- TMA producer (both CTAs)
-      int s = 0;
-      uint32_t phase = 0;
-      const uint32_t tx = p.a_bytes + p.b_bytes;  // this CTA's bytes
-      for (int t = cluster; t < num_tiles; t += n_clusters) {
-        const int m_tile = (t / n_tiles) * 2 + (int)rank, n_tile = t % n_tiles;
-        int n0 = 0, oh0 = 0, ow0 = 0;
-        if (p.mode == MODE_CONV) {
-          const int tw = m_tile % p.tiles_w;
-          const int th = (m_tile / p.tiles_w) % p.tiles_h;
-          const int tn = m_tile / (p.tiles_w * p.tiles_h);
-          n0 = tn * p.bn;
-          oh0 = th * p.bh * p.stride - p.pad;
-          ow0 = tw * p.bw * p.stride - p.pad;
-        }
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&empty[s], phase ^ 1);
-          const uint32_t a_dst = smem_addr(smA + s * kABytes);
-          const uint32_t b_dst = smem_addr(smB + s * p.b_bytes);
-          // only the leader arrives, expecting both CTAs' bytes; the peer's TMA
-          // completes on the leader's barrier (tx may transiently go negative)
-          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * tx);
-          if (p.mode == MODE_DENSE) {
-            tma_load_2d_pair(a_dst, &tmA, &full[s], kb * kBK, m_tile * kBM);
-          } else {
-            const int tap = kb / p.cchunks;
-            const int cc = kb - tap * p.cchunks;
-            const int kh = tap / p.KW;
-            const int kw = tap - kh * p.KW;
-            tma_load_4d_pair(a_dst, &tmA, &full[s], cc * kBK, ow0 + kw, oh0 + kh, n0);
-          }
-          tma_load_2d_pair(b_dst, &tmB, &full[s], kb * kBK, n_tile * p.BN + (int)rank * half_bn);
-          if (++s == stages) {
-            s = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (rank == 0) {  // ---------------------------------------- MMA issuer (leader only)
-      const uint32_t idesc = umma_idesc_bf16_m256((uint32_t)p.BN);
-      int s = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += n_clusters) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);  // both CTAs drained this buffer
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&full[s], phase);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
-            const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-            umma_commit_pair(&empty[s], 0x3);
-            if (kb == p.num_kb - 1) umma_commit_pair(&tfull[acc], 0x3);
-          }
-          __syncwarp();
-          if (++s == stages) {
-            s = 0;
-            phase ^= 1;
-          }
-        }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
-    }
-  } else {  // -------------------------------------------- epilogue warps 2..9 (both CTAs)
-    const int q = warp & 3, grp = (warp - 2) >> 2;
-    const int r = q * 32 + lane;
-    const uint32_t tempty_leader0 = mapa_shared(smem_addr(&tempty[0]), 0);
-    const uint32_t tempty_leader1 = mapa_shared(smem_addr(&tempty[1]), 0);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
-    for (int t = cluster; t < num_tiles; t += n_clusters) {
-      const int m_tile = (t / n_tiles) * 2 + (int)rank, n_tile = t % n_tiles;
-      long long out_row = -1;
-      if (p.mode == MODE_CONV) {
-        const int tw = m_tile % p.tiles_w;
-        const int th = (m_tile / p.tiles_w) % p.tiles_h;
-        const int tn = m_tile / (p.tiles_w * p.tiles_h);
-        const int per_img = p.bh * p.bw;
-        if (r < p.bn * per_img) {
-          const int i = r / per_img;
-          const int y = (r - i * per_img) / p.bw;
-          const int x = r - i * per_img - y * p.bw;
-          const int n = tn * p.bn + i, oh = th * p.bh + y, ow = tw * p.bw + x;
-          if (n < p.n_img && oh < p.OH && ow < p.OW) out_row = ((long long)n * p.OH + oh) * p.OW + ow;
-        }
-      } else {
-        const int row = m_tile * kBM + r;
-        if (m_tile < p.m_tiles && row < p.M) out_row = row;
-      }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t_base = tmem_base + (uint32_t)acc * acc_stride + ((uint32_t)(q * 32) << 16);
-      const int n_first = n_tile * p.BN;
-      for (int c = grp; c < p.BN / 32; c += 2) {
-        const int nb = n_first + c * 32;
-        if (nb >= p.N) break;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), v);
-        tmem_wait_ld();
-        if (p.debug_flags & 1) continue;
-        void* seg_ptr = p.seg[0].ptr;
-        long long seg_ld = p.seg[0].ldd;
-        int seg_off = p.seg[0].col0 - p.seg[0].n_begin;
-        int seg_flags = p.seg[0].flags;
-#pragma unroll
-        for (int g = 1; g < 4; ++g) {
-          if (g < p.nseg && nb >= p.seg[g].n_begin) {
-            seg_ptr = p.seg[g].ptr;
-            seg_ld = p.seg[g].ldd;
-            seg_off = p.seg[g].col0 - p.seg[g].n_begin;
-            seg_flags = p.seg[g].flags;
-          }
-        }
-        const int act = (seg_flags & MS_SEG_NO_RELU) ? 0 : p.relu;
-        const float* bch = sbias + nb;
-        uint32_t pk[16];
-        switch (act) {
-          case MS_ACT_RELU: convert_chunk<MS_ACT_RELU>(v, bch, pk); break;
-          case MS_ACT_GELU: convert_chunk<MS_ACT_GELU>(v, bch, pk); break;
-          case MS_ACT_TANH: convert_chunk<MS_ACT_TANH>(v, bch, pk); break;
-          default: convert_chunk<MS_ACT_NONE>(v, bch, pk);
-        }
-        if (nb + 32 <= p.N) {  // staged, coalesced write-back
-          uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          __syncwarp();
-          const long long col = seg_off + nb;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rr = i * 8 + (lane >> 2), piece = lane & 3;
-            const long long orow = __shfl_sync(0xffffffffu, out_row, rr);
-            const uint4 val = *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
-            if (orow >= 0)
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(seg_ptr) + orow * seg_ld + col + piece * 8) =
-                  val;
-          }
-          __syncwarp();
-        } else if (out_row >= 0) {
-          unsigned short* d2 = reinterpret_cast<unsigned short*>(
-              reinterpret_cast<__nv_bfloat16*>(seg_ptr) + out_row * seg_ld + seg_off + nb);
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < p.N) d2[j] = (unsigned short)((pk[j >> 1] >> (16 * (j & 1))) & 0xffff);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem_base, tmem_cols);
-  }
-}
 
 // ------------------------------------------------------------------------
 // MODE_CONV1_ROWS: the few-channel first convolution (7x7/2 over 8/16 padded
@@ -1655,6 +1547,13 @@ static int sm_count() {
   return n;
 }
 
+// pipeline depth cap (MS_MAX_STAGES: probe switch for tools/mainloop_probe.py)
+static int max_stages() {
+  const char* e = getenv("MS_MAX_STAGES");
+  const int v = e ? atoi(e) : 0;
+  return v >= 2 ? v : 8;
+}
+
 static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int BN, int num_kb, int grid_x) {
   GemmParams& p = P->p;
   if (BN % 32 != 0 || BN < 32 || BN > 256) return set_error(MS_ERR_INVALID, "BN must be a multiple of 32 in [32, 256]");
@@ -1682,7 +1581,7 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   p.stage_bytes = p.tma_store ? kStoreBytes : 0;  // fp32 / split-K epilogues stage nothing
   // 227 KB usable: 1 KB alignment slack, barriers, epilogue staging, bias
   int stages = (226 * 1024 - 1024 - 288 - p.stage_bytes - bias_bytes) / per_stage;
-  if (stages > 8) stages = 8;
+  if (stages > max_stages()) stages = max_stages();
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   p.stages = stages;
   P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
@@ -1809,15 +1708,6 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
       launch_k(stem_pool_kernel<false, 1>, dim3(P->grid_x), dim3(kStemThreads), P->smem_bytes, stream, 1, p);
     return check_launch("stem_pool_kernel");
   }
-  if (p.pair) {
-    static int pair_attr = 0;
-    if (!pair_attr) {
-      cudaFuncSetAttribute(gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      pair_attr = 1;
-    }
-    launch_k(gemm_tc_pair_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 2, P->tmA, P->tmB, p);
-    return check_launch("gemm_tc_pair_kernel");
-  }
   GemmKernelFn kern = gemm_kernel_for(p);
   if (kern == nullptr) return set_error(MS_ERR_INVALID, "no GEMM kernel for this plan (mode/epilogue)");
   static bool attr_done[64] = {};
@@ -1831,7 +1721,8 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
       attr_done[slot] = true;
     }
   }
-  launch_k(kern, dim3(P->grid_x, P->grid_y), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p, P->tmD);
+  launch_k(kern, dim3(P->grid_x, P->grid_y), dim3(kThreads), P->smem_bytes, stream, p.pair ? 2 : 1, P->tmA, P->tmB, p,
+           P->tmD);
   int rc = check_launch("gemm_tc_kernel");
   if (rc || p.ksplit <= 1) return rc;
   const long long work = (long long)p.M * ((p.N + 3) / 4);
@@ -2136,10 +2027,10 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
   if (P == nullptr) return set_error(MS_ERR_INVALID, "null plan");
   GemmParams& p = P->p;
-  if (!enable) return MS_OK;
-  if ((p.mode != MODE_DENSE && p.mode != MODE_CONV) || p.ksplit > 1 || p.residual != nullptr || p.out_fp32 ||
-      p.BN % 32 != 0)
-    return set_error(MS_ERR_INVALID, "CTA-pair mode needs a dense/conv bf16 plan without split-K/residual");
+  if (!enable || p.pair) return MS_OK;
+  if ((p.mode != MODE_DENSE && p.mode != MODE_CONV && p.mode != MODE_CONV_K32 && p.mode != MODE_CONV_HALO) ||
+      p.ksplit > 1 || p.out_fp32 || !p.tma_store || p.BN % 32 != 0)
+    return set_error(MS_ERR_INVALID, "CTA-pair mode needs a dense/conv/k32/halo bf16 plan without split-K");
   // the weight box becomes BN/2 rows per CTA
   cuuint64_t dims[2] = {(cuuint64_t)P->w_kpad, (cuuint64_t)P->w_rows};
   cuuint64_t strides[1] = {(cuuint64_t)P->w_kpad * 2};
@@ -2149,16 +2040,31 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   if (rc) return rc;
   p.pair = 1;
   p.b_bytes = (p.BN / 2) * kBK * 2;
-  const int per_stage = kABytes + p.b_bytes;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
-  int stages = (226 * 1024 - 1024 - 256 - 32 - kStageBytes - bias_bytes) / per_stage;
-  if (stages > 8) stages = 8;
-  p.stages = stages;
-  P->smem_bytes = 1024 + stages * per_stage + (2 * stages + 4) * 8 + 16 + 32 + kStageBytes + bias_bytes;
-  const int m_pairs = (p.m_tiles + 1) / 2;
-  const int tiles = m_pairs * ((p.N + p.BN - 1) / p.BN);
-  const int clusters = tiles < sm_count() / 2 ? tiles : sm_count() / 2;
+  const int n_tiles = (p.N + p.BN - 1) / p.BN;
+  const int pair_tiles = ((p.m_tiles + 1) / 2) * n_tiles;
+  int clusters = pair_tiles < sm_count() / 2 ? pair_tiles : sm_count() / 2;
+  if (p.mode == MODE_CONV_HALO) {
+    const int room = 226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes;
+    // half of the weights per CTA: layers whose full tile did not fit can now stay resident
+    p.b_resident = (n_tiles == 1 && 9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
+    int stages = p.b_resident ? 9 * p.cchunks : room / p.b_bytes;
+    if (!p.b_resident && stages > kMaxHaloStages) stages = kMaxHaloStages;
+    if (stages < 2) return set_error(MS_ERR_INVALID, "halo pair: weights tile does not fit");
+    p.stages = stages;
+    P->smem_bytes = 1024 + 2 * p.halo_slot + stages * p.b_bytes + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
+    if (p.b_resident) clusters = clusters / n_tiles * n_tiles < n_tiles ? n_tiles : clusters / n_tiles * n_tiles;
+  } else {
+    const int per_stage = kABytes + p.b_bytes;
+    int stages = (226 * 1024 - 1024 - 288 - p.stage_bytes - bias_bytes) / per_stage;
+    if (stages > max_stages()) stages = max_stages();
+    if (stages > p.num_kb) stages = p.num_kb < 2 ? 2 : p.num_kb;
+    p.stages = stages;
+    P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
+  }
+  if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "pair plan exceeds 227 KB shared memory");
   P->grid_x = 2 * clusters;
+  P->grid_y = 1;
   return MS_OK;
 }
 

@@ -357,10 +357,14 @@ class DeviceExecutor:
     latency-feedback EWMA (scheduler.py:86-91).
     """
 
-    def __init__(self, model: MaskedModel, timing: str = "measured", slot_seed: int = 0):
+    def __init__(self, model: MaskedModel, timing: str = "measured", slot_seed: int = 0, record: int = 0):
+        """``record``: keep (job id, assigned credit, masks, slots) of every
+        pass and the logits of the first ``record`` passes in ``trace``."""
         if timing not in ("virtual", "measured"):
             raise ValueError("timing must be 'virtual' or 'measured'")
         self.model = model
+        self.record = record
+        self.trace = [] if record else None
         self.timing = timing
         self.rng = np.random.default_rng(slot_seed)
         self.ev0, self.ev1 = dv.Event(), dv.Event()
@@ -381,6 +385,9 @@ class DeviceExecutor:
         self.requests += job.size
         self.device_us += us
         self.last_logits = logits
+        if self.trace is not None:
+            keep = logits[: job.size].float().cpu() if len(self.trace) < self.record else None
+            self.trace.append((job.id, job.assigned.credit, masks.copy(), slots.copy(), keep))
         preds = [profile.part_latency_us(m, b) for m, b in parts]
         if self.timing == "virtual":
             return [(p, max(1, round(p * discrepancy))) for p in preds]

@@ -396,10 +396,12 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         while inflight and inflight[0][2].done():  # non-blocking completion checks
             finish()
         if refresher is not None and selector is not None:
+            if len(inflight) >= depth or not len(queue):
+                refresher.advance()  # host slack: the GPU queue is full (or nothing to form)
             res = refresher.poll()
             if res is not None:  # hot-swap between two formations
                 cost, profile, matrix = res.cost, res.profile, res.matrix
-                fcache = FrontierCache(matrix, model.K, top_only=top_only)
+                fcache = res.fcache
                 selector.cost = cost.device_table()
                 stats.refreshes.append(res)
             elif refresher.due(now / 1e6):

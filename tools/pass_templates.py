@@ -20,6 +20,7 @@ sys.path.insert(0, str(ROOT))
 ap = argparse.ArgumentParser()
 ap.add_argument("--counts", type=int, nargs=3, default=(61, 36, 24))
 ap.add_argument("--rep", type=int, default=10)
+ap.add_argument("--ops", action="store_true", help="also print one row per op")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -69,6 +70,7 @@ def template(kind, op):
 
 
 rows = []
+oprows = []
 for k, (enc, c) in enumerate(zip(m.encoders, counts)):
     if not c:
         continue
@@ -95,6 +97,10 @@ for k, (enc, c) in enumerate(zip(m.encoders, counts)):
             e1.record()
             ts.append(e0.elapsed_us(e1) / a.rep)
         rows.append((template(kind, op), float(np.median(ts)), op.flops if kind == "gemm" else 0))
+        if a.ops:
+            lab = op.label if kind == "gemm" else f"{kind} {op[1:6]}"
+            inf = op.info() if kind == "gemm" else {}
+            oprows.append((k, i, lab, rows[-1][1], rows[-1][2], inf))
 tot = sum(r[1] for r in rows)
 fl = sum(r[2] for r in rows)
 agg = {}
@@ -112,3 +118,8 @@ print("|---|---|---|---|---|---|---|")
 for t, (nop, us, f) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     tf = f / us / 1e6 if f else 0.0
     print(f"| {t} | {nop} | {us:.0f} | {us / tot:.3f} | {tf:.0f} | {tf / burst:.3f} | {tf / sust:.3f} |")
+if a.ops:
+    print("\n| enc | op | label | grid | stages | us | TFLOP/s |")
+    print("|---|---|---|---|---|---|---|")
+    for k, i, lab, us, f, inf in oprows:
+        print(f"| {k} | {i} | {lab} | {inf.get('grid_x', '')} | {inf.get('stages', '')} | {us:.1f} | {f / us / 1e6:.0f} |")
