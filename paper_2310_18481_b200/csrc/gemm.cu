@@ -1537,6 +1537,12 @@ static int encode_map(CUtensorMap* m, int rank, const void* base, const cuuint64
   return MS_OK;
 }
 
+int encode_bf16_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims,
+                    const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* estride,
+                    CUtensorMapSwizzle swz) {
+  return encode_map(m, rank, base, dims, strides_bytes, box, estride, swz);
+}
+
 static int sm_count() {
   static int n = 0;
   if (n == 0) {

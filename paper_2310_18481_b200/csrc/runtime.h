@@ -43,6 +43,9 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+// gemm.cu: cuTensorMapEncodeTiled for a bf16 tensor (driver entry point)
+int encode_bf16_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+                    const cuuint32_t* box, const cuuint32_t* estride, CUtensorMapSwizzle swz);
 // transformer.cu
 int run_layernorm(const void* X, long long ldx, long long rows, const float* gamma, const float* beta, void* Y,
                   long long ldy, int C, float eps, cudaStream_t st);

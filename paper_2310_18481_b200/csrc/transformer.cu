@@ -5,11 +5,10 @@
 //   * layernorm_kernel      — one warp per row, fp32 statistics, bf16 out,
 //                             arbitrary input/output row strides (so the
 //                             final LN can read only the CLS rows)
-//   * attention_kernel      — fused softmax(Q K^T * scale) V per (sequence,
-//                             head, 64-query block), FlashAttention-2 style
-//                             online softmax on mma.sync m16n8k16 bf16 tensor
-//                             ops with ldmatrix fragments; attention is ~4 %
-//                             of ViT-B FLOPs, the rest is on tcgen05
+//   * attention_tc_kernel   — fused softmax(Q K^T * scale) V per (sequence,
+//                             head): both contractions tcgen05.mma with S and
+//                             the output in TMEM, P staged as the SMEM A
+//                             operand (L <= 256 keys)
 //   * patchify_kernel       — NHWC image -> [patches, (kh, kw, c)] rows
 //   * vit_embed_kernel      — [CLS | patch embeddings] + position embeddings
 //   * bert_embed_kernel     — word + position + type embeddings, then LN
@@ -77,161 +76,179 @@ __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ X, long long 
 }
 
 // ------------------------------------------------------------- attention
+// softmax(Q K^T * scale) V on the 5th-gen tensor cores, one CTA per
+// (sequence, head), L <= 256 keys (ViT-B/16: 197, BERT: 40):
+//   TMA    Q block [128 x 64], K [Lk16 x 64] (SW128 K-major) and V rows
+//          (unswizzled staging) from the packed QKV activations;
+//   V^T    all 128 threads transpose V into K-major SW128 chunks of 64 keys
+//          (the B operand of P V), zero past L;
+//   S      tcgen05.mma M=128, N=Lk16, K=64 -> TMEM (one query row per lane);
+//   P      each thread reads its row from TMEM (tcgen05.ld), masks keys >= L,
+//          exp2 with the running max, sums in fp32 and stores P (bf16) into
+//          SW128 K-major SMEM chunks -- the A operand of the second MMA;
+//   O      tcgen05.mma M=128, N=64, K=Lk64 into TMEM columns the consumed S
+//          occupied; epilogue scales by 1/rowsum and stores bf16 rows.
+// Both contractions are UMMA (UTCHMMA); query blocks of 128 loop in the CTA
+// so K and V^T are loaded once per (sequence, head).
 constexpr int kHd = 64;    // head dim
-constexpr int kBq = 64;    // queries per block (4 warps x 16)
-constexpr int kBk = 64;    // keys per iteration
-constexpr int kPad = 8;    // smem row padding (bank-conflict-free ldmatrix)
+constexpr int kAttnMaxL = 256;
+constexpr int kAttnThreads = 128;
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
+struct AttnMaps {
+  CUtensorMap q, k, v;
+};
 
-// qkv rows: [Q(H*64) | K(H*64) | V(H*64)] per token, row stride ld;
-// out rows: H*64 per token, row stride ldo.  grid (ceil(L/64), H, n_seq).
-__global__ void __launch_bounds__(128) attention_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int L,
-                                                        int H, __nv_bfloat16* __restrict__ out, long long ldo,
-                                                        float scale_log2) {
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attention_tc_kernel(const __grid_constant__ AttnMaps maps, int L, int Lk16, int Lk64, int D,
+                        __nv_bfloat16* __restrict__ out, long long ldo, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  const int nchunk = Lk64 / 64;
+  uint8_t* sQ = smem;                                   // 16 KB
+  uint8_t* sK = sQ + 128 * 128;                         // Lk16 x 128 B (rounded to 1 KB)
+  uint8_t* sVT = sK + ((Lk16 * 128 + 1023) & ~1023);    // nchunk x (64 x 128 B)
+  uint8_t* sP = sVT + nchunk * 8192;                    // nchunk x (128 x 128 B); V staging first
+  uint64_t* bar_ld = reinterpret_cast<uint64_t*>(sP + nchunk * 16384);
+  uint64_t* bar_mma = bar_ld + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = blockIdx.x;
+  const long long row0 = (long long)blockIdx.y * L;
+
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  if (tid == 0) {
+    mbar_init(bar_ld, 1);
+    mbar_init(bar_mma, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
-  __shared__ __align__(16) __nv_bfloat16 sQ[kBq][kHd + kPad];
-  __shared__ __align__(16) __nv_bfloat16 sK[kBk][kHd + kPad];
-  __shared__ __align__(16) __nv_bfloat16 sV[kBk][kHd + kPad];
-  const int qb = blockIdx.x, h = blockIdx.y;
-  const long long seq = blockIdx.z;
-  const __nv_bfloat16* base = qkv + seq * L * ld;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int D = H * kHd;
-
-  for (int i = tid; i < kBq * kHd / 8; i += 128) {
-    const int r = i >> 3, c8 = (i & 7) * 8;
-    const int q = qb * kBq + r;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (q < L) v = *reinterpret_cast<const uint4*>(base + (long long)q * ld + h * kHd + c8);
-    *reinterpret_cast<uint4*>(&sQ[r][c8]) = v;
+  uint32_t ph_ld = 0, ph_mma = 0;
+  if (tid == 0) {
+    tma_prefetch_desc(&maps.q);
+    mbar_arrive_expect_tx(bar_ld, 2u * (uint32_t)Lk16 * 128u);
+    tma_load_2d(smem_addr(sK), &maps.k, bar_ld, D + h * kHd, (int)row0);
+    tma_load_2d(smem_addr(sP), &maps.v, bar_ld, 2 * D + h * kHd, (int)row0);
   }
+  mbar_wait(bar_ld, ph_ld);
+  ph_ld ^= 1;
+  // V^T: element (d, key) of chunk key/64 at d*128 + swizzled 16-B group of key%64
+  const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(sP);
+  for (int idx = tid; idx < kHd * (Lk64 / 8); idx += kAttnThreads) {
+    const int d = idx & (kHd - 1), key0 = (idx >> 6) * 8;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k0 = key0 + 2 * j;
+      const __nv_bfloat16 lo = k0 < L ? sV[k0 * kHd + d] : __float2bfloat16(0.0f);
+      const __nv_bfloat16 hi = k0 + 1 < L ? sV[(k0 + 1) * kHd + d] : __float2bfloat16(0.0f);
+      w[j] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+    }
+    const int grp = (key0 & 63) >> 3;
+    *reinterpret_cast<uint4*>(sVT + (key0 >> 6) * 8192 + d * 128 + ((grp ^ (d & 7)) << 4)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_proxy_async_smem();
   __syncthreads();
-  // Q fragments for this warp's 16 rows, 4 k-steps of 16 dims
-  uint32_t qf[4][4];
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    const int r = warp * 16 + (lane & 15), c = ks * 16 + (lane >> 4) * 8;
-    ldsm_x4(smem_addr(&sQ[r][c]), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
-  }
-  float o[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
-  const int g = lane >> 2, t4 = lane & 3;
 
-  for (int k0 = 0; k0 < L; k0 += kBk) {
+  const uint32_t idesc_s = umma_idesc_bf16_m128((uint32_t)Lk16);
+  const uint32_t idesc_o = umma_idesc_bf16_m128((uint32_t)kHd);
+  const int r = warp * 32 + lane;  // this thread's query row in the block (TMEM lane)
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  uint8_t* prow = sP + r * 128;
+  for (int q0 = 0; q0 < L; q0 += 128) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar_ld, 128u * 128u);
+      tma_load_2d(smem_addr(sQ), &maps.q, bar_ld, h * kHd, (int)(row0 + q0));
+    }
+    mbar_wait(bar_ld, ph_ld);
+    ph_ld ^= 1;
+    tc_fence_after();
+    if (warp == 0) {  // S = Q K^T (4 K=16 steps over the head dim)
+      const uint64_t qd = umma_desc_sw128(smem_addr(sQ)), kd = umma_desc_sw128(smem_addr(sK));
+#pragma unroll
+      for (int k = 0; k < kHd / 16; ++k) umma_bf16_elect(tmem, qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+      umma_commit_elect(bar_mma);
+    }
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    // row max over the valid keys
+    float mx = -INFINITY;
+    for (int c0 = 0; c0 < Lk16; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < L) mx = fmaxf(mx, __uint_as_float(v[j]));
+    }
+    const float mxs = mx * scale_log2;
+    float sum = 0.0f;
+    for (int c0 = 0; c0 < Lk64; c0 += 16) {
+      uint32_t pk[8];
+      if (c0 < Lk16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float p0 = c0 + 2 * j < L ? exp2f(__uint_as_float(v[2 * j]) * scale_log2 - mxs) : 0.0f;
+          const float p1 = c0 + 2 * j + 1 < L ? exp2f(__uint_as_float(v[2 * j + 1]) * scale_log2 - mxs) : 0.0f;
+          sum += p0 + p1;
+          pk[j] = pack_bf16x2(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[j] = 0u;
+      }
+      uint8_t* chunk = prow + (c0 >> 6) * 16384;
+      const int g0 = (c0 & 63) >> 3;
+      *reinterpret_cast<uint4*>(chunk + ((g0 ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4*>(chunk + (((g0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
     __syncthreads();
-    for (int i = tid; i < kBk * kHd / 8; i += 128) {
-      const int r = i >> 3, c8 = (i & 7) * 8;
-      const int k = k0 + r;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (k < L) {
-        kv = *reinterpret_cast<const uint4*>(base + (long long)k * ld + D + h * kHd + c8);
-        vv = *reinterpret_cast<const uint4*>(base + (long long)k * ld + 2 * D + h * kHd + c8);
+    tc_fence_after();
+    if (warp == 0) {  // O = P V over the key chunks, into the consumed S columns
+      for (int kc = 0; kc < nchunk; ++kc) {
+        const uint64_t pd = umma_desc_sw128(smem_addr(sP + kc * 16384));
+        const uint64_t vd = umma_desc_sw128(smem_addr(sVT + kc * 8192));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_bf16_elect(tmem, pd + 2 * k, vd + 2 * k, idesc_o, (kc | k) != 0);
       }
-      *reinterpret_cast<uint4*>(&sK[r][c8]) = kv;
-      *reinterpret_cast<uint4*>(&sV[r][c8]) = vv;
+      umma_commit_elect(bar_mma);
     }
-    __syncthreads();
-    // S = Q K^T : 16 rows x 64 keys (8 n-tiles of 8 keys)
-    float sc[8][4];
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+    const int q = q0 + r;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
+    for (int half = 0; half < 2; ++half) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr + (uint32_t)(half * 32), v);
+      tmem_wait_ld();
+      if (q < L) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (row0 + q) * ldo + h * kHd + half * 32);
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-#pragma unroll
-      for (int np = 0; np < 4; ++np) {  // two n-tiles per ldmatrix.x4
-        uint32_t b0, b1, b2, b3;
-        const int r = np * 16 + (lane & 7) + ((lane >> 4) << 3), c = ks * 16 + ((lane >> 3) & 1) * 8;
-        ldsm_x4(smem_addr(&sK[r][c]), b0, b1, b2, b3);
-        mma_bf16(sc[2 * np], qf[ks], b0, b1);
-        mma_bf16(sc[2 * np + 1], qf[ks], b2, b3);
-      }
-    }
-    // mask keys beyond L, online softmax (rows g and g+8 of the warp tile)
-    float mx0 = m0, mx1 = m1;
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      const int kc = k0 + nt * 8 + 2 * t4;
-      if (kc >= L) sc[nt][0] = sc[nt][2] = -INFINITY;
-      if (kc + 1 >= L) sc[nt][1] = sc[nt][3] = -INFINITY;
-      mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]) * scale_log2);
-      mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]) * scale_log2);
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float a0 = exp2f(m0 - mx0), a1 = exp2f(m1 - mx1);
-    m0 = mx0;
-    m1 = mx1;
-    float s0 = 0.0f, s1 = 0.0f;
-    uint32_t pf[8][2];  // P as bf16 pairs: [n-tile][row g / row g+8]
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      const float p00 = exp2f(sc[nt][0] * scale_log2 - m0), p01 = exp2f(sc[nt][1] * scale_log2 - m0);
-      const float p10 = exp2f(sc[nt][2] * scale_log2 - m1), p11 = exp2f(sc[nt][3] * scale_log2 - m1);
-      s0 += p00 + p01;
-      s1 += p10 + p11;
-      pf[nt][0] = pack_bf16x2(p00, p01);
-      pf[nt][1] = pack_bf16x2(p10, p11);
-    }
-    l0 = l0 * a0 + s0;
-    l1 = l1 * a1 + s1;
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) {
-      o[dt][0] *= a0;
-      o[dt][1] *= a0;
-      o[dt][2] *= a1;
-      o[dt][3] *= a1;
-    }
-    // O += P V : k = keys (4 steps of 16), n = 64 dims (8 tiles)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const uint32_t af[4] = {pf[2 * kk][0], pf[2 * kk][1], pf[2 * kk + 1][0], pf[2 * kk + 1][1]};
-#pragma unroll
-      for (int dp = 0; dp < 4; ++dp) {  // two dim tiles per ldmatrix.x4.trans
-        uint32_t b0, b1, b2, b3;
-        const int r = kk * 16 + (lane & 15), c = dp * 16 + (lane >> 4) * 8;
-        ldsm_x4_t(smem_addr(&sV[r][c]), b0, b1, b2, b3);
-        mma_bf16(o[2 * dp], af, b0, b1);
-        mma_bf16(o[2 * dp + 1], af, b2, b3);
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * j]) * inv, __uint_as_float(v[8 * j + 1]) * inv),
+                              pack_bf16x2(__uint_as_float(v[8 * j + 2]) * inv, __uint_as_float(v[8 * j + 3]) * inv),
+                              pack_bf16x2(__uint_as_float(v[8 * j + 4]) * inv, __uint_as_float(v[8 * j + 5]) * inv),
+                              pack_bf16x2(__uint_as_float(v[8 * j + 6]) * inv, __uint_as_float(v[8 * j + 7]) * inv));
       }
     }
+    tc_fence_before();
+    __syncthreads();  // TMEM, sQ and sP are reused by the next query block
+    tc_fence_after();
   }
-  // finalize: row sums across the quad, normalise, store
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float inv0 = l0 > 0.0f ? 1.0f / l0 : 0.0f, inv1 = l1 > 0.0f ? 1.0f / l1 : 0.0f;
-  const int q0 = qb * kBq + warp * 16 + g, q1 = q0 + 8;
-#pragma unroll
-  for (int dt = 0; dt < 8; ++dt) {
-    const int c = h * kHd + dt * 8 + 2 * t4;
-    if (q0 < L)
-      *reinterpret_cast<uint32_t*>(out + (seq * L + q0) * ldo + c) = pack_bf16x2(o[dt][0] * inv0, o[dt][1] * inv0);
-    if (q1 < L)
-      *reinterpret_cast<uint32_t*>(out + (seq * L + q1) * ldo + c) = pack_bf16x2(o[dt][2] * inv1, o[dt][3] * inv1);
-  }
+  if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
 // ------------------------------------------------------------- embeddings
@@ -364,11 +381,27 @@ int run_attention(const void* qkv, long long ld, int L, int H, int n_seq, void* 
                   cudaStream_t st) {
   if (ld % 8 != 0 || ldo % 8 != 0 || L < 1 || H < 1 || n_seq < 0)
     return set_error(MS_ERR_INVALID, "attention: bad shape/stride");
+  if (L > kAttnMaxL) return set_error(MS_ERR_INVALID, "attention: sequence length above 256 keys");
   if (n_seq == 0) return MS_OK;
-  dim3 grid((L + kBq - 1) / kBq, H, n_seq);
-  launch_k(attention_kernel, grid, dim3(128), 0, st, 1, reinterpret_cast<const __nv_bfloat16*>(qkv), ld, L, H,
-                                         reinterpret_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
-  return check_launch("attention_kernel");
+  const int D = H * kHd, Lk16 = (L + 15) / 16 * 16, Lk64 = (L + 63) / 64 * 64;
+  AttnMaps maps;
+  const cuuint64_t dims[2] = {(cuuint64_t)(3 * D), (cuuint64_t)n_seq * L};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t es[2] = {1, 1};
+  const cuuint32_t bq[2] = {kHd, 128}, bk[2] = {kHd, (cuuint32_t)Lk16};
+  int rc = encode_bf16_map(&maps.q, 2, qkv, dims, strides, bq, es, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = encode_bf16_map(&maps.k, 2, qkv, dims, strides, bk, es, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = encode_bf16_map(&maps.v, 2, qkv, dims, strides, bk, es, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (rc) return rc;
+  const int smem = 1024 + 128 * 128 + ((Lk16 * 128 + 1023) & ~1023) + (Lk64 / 64) * (8192 + 16384) + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  launch_k(attention_tc_kernel, dim3(H, n_seq), dim3(kAttnThreads), smem, st, 1, maps, L, Lk16, Lk64, D,
+           reinterpret_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
+  return check_launch("attention_tc_kernel");
 }
 
 int run_patchify(const void* X, int n, int S, int C, int P, void* Y, cudaStream_t st) {

@@ -40,13 +40,17 @@ def test_layernorm(dev, rows, C, ldx):
     assert _close(Y, ref, 1e-2)[0]
 
 
-@pytest.mark.parametrize("L,n", [(197, 3), (40, 5), (64, 2), (1, 4)])
-def test_attention_vs_torch(dev, L, n):
+@pytest.mark.parametrize("L,n,pad", [(197, 3, 0), (40, 5, 0), (64, 2, 0), (1, 4, 0), (256, 2, 0), (129, 3, 64),
+                                     (200, 7, 0)])
+def test_attention_vs_torch(dev, L, n, pad):
+    """The tcgen05 attention (UMMA for Q K^T and P V, S/O in TMEM): every
+    query block / key-chunk boundary, L = 1 .. 256, padded row strides."""
     Lb = dev.lib()
     H = 12
-    qkv = torch.randn(n * L, 3 * H * 64).to(torch.bfloat16).cuda()
+    qkv_full = torch.randn(n * L, 3 * H * 64 + pad).to(torch.bfloat16).cuda()
+    qkv = qkv_full[:, : 3 * H * 64]
     out = torch.zeros(n * L, H * 64, dtype=torch.bfloat16, device="cuda")
-    dev.check(Lb.ms_attention(qkv.data_ptr(), 3 * H * 64, L, H, n, out.data_ptr(), H * 64, 0.125,
+    dev.check(Lb.ms_attention(qkv.data_ptr(), 3 * H * 64 + pad, L, H, n, out.data_ptr(), H * 64, 0.125,
                               dev.stream_ptr()), "attention")
     torch.cuda.synchronize()
     q, k, v = qkv.float().cpu().reshape(n, L, 3, H, 64).permute(2, 0, 3, 1, 4)
@@ -54,6 +58,13 @@ def test_attention_vs_torch(dev, L, n):
     ref = ref.permute(0, 2, 1, 3).reshape(n * L, H * 64)
     ok, err, scale = _close(out, ref)
     assert ok, (err, scale)
+
+
+def test_attention_rejects_long_sequences(dev):
+    qkv = torch.zeros(300, 3 * 64, dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros(300, 64, dtype=torch.bfloat16, device="cuda")
+    rc = dev.lib().ms_attention(qkv.data_ptr(), 3 * 64, 300, 1, 1, out.data_ptr(), 64, 0.125, dev.stream_ptr())
+    assert rc != 0
 
 
 def test_gemm_gelu_tanh_residual(dev):
