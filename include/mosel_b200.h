@@ -139,14 +139,17 @@ int ms_strategy_dp(int n_items, const int32_t* batch, const int64_t* lat_us, con
  * accuracy as double); assigned[n] in/out (-1 on return = dropped).
  * has_running: the running job's estimated finish sets the dispatch time
  * (scheduler.py:178-184).  grid_us = the knapsack quantum (reference 1000).
- * ws: device scratch of ws_bytes (16 bytes per knapsack cell); *status
- * (device) = 0 ok, 1 scratch too small, 2 scope exceeds 4096 job x
- * candidate entries -- the caller then uses the host policy.  Bit-exact with
- * the reference (tests/golden/queue_policy_cases.json). */
+ * ws: device scratch of ws_bytes (16 bytes per knapsack cell; a queue never
+ * needs more than (n + 1) * (floor((max deadline - dispatch) / grid_us) + 1)
+ * cells); *status (device) = 0 ok, 1 scratch too small (a caller error).
+ * n <= ms_policy_max_jobs(C) (per-job tables in shared memory).  Bit-exact
+ * with the reference (tests/golden/queue_policy_cases.json). */
 int ms_policy_apply(int n, int C, const int64_t* lat_us, const int32_t* credit, const double* acc,
                     const int32_t* n_cand, const int64_t* deadline_us, int32_t* assigned, int64_t now_us,
                     int64_t running_finish_us, int has_running, double factor, int64_t grid_us, void* ws,
                     long long ws_bytes, int32_t* status, void* stream);
+/* the longest queue ms_policy_apply takes with C candidate columns (0 if C is out of range) */
+int ms_policy_max_jobs(int C);
 
 /* ---- request compaction ----------------------------
  * mask[N] (bit k = modality k present) ->

@@ -77,7 +77,7 @@ __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ X, long long 
 
 // ------------------------------------------------------------- attention
 // softmax(Q K^T * scale) V on the 5th-gen tensor cores, one CTA per
-// (sequence, head), L <= 256 keys (ViT-B/16: 197, BERT: 40):
+// (head, sequence, 128-query block), L <= 256 keys (ViT-B/16: 197, BERT: 40):
 //   TMA    Q block [128 x 64], K [Lk16 x 64] (SW128 K-major) and V rows
 //          (unswizzled staging) from the packed QKV activations;
 //   V^T    all 128 threads transpose V into K-major SW128 chunks of 64 keys
@@ -88,11 +88,19 @@ __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ X, long long 
 //          SW128 K-major SMEM chunks -- the A operand of the second MMA;
 //   O      tcgen05.mma M=128, N=64, K=Lk64 into TMEM columns the consumed S
 //          occupied; epilogue scales by 1/rowsum and stores bf16 rows.
-// Both contractions are UMMA (UTCHMMA); query blocks of 128 loop in the CTA
-// so K and V^T are loaded once per (sequence, head).
+// Both contractions are UMMA (UTCHMMA).  One CTA per (head, sequence, query
+// block of 128); Q, K and the V staging rows share the P region, so a CTA
+// takes <= 100 KB and two run per SM; S rows come out of TMEM 64 columns per
+// round trip.
 constexpr int kHd = 64;    // head dim
 constexpr int kAttnMaxL = 256;
-constexpr int kAttnThreads = 128;
+constexpr int kAttnThreads = 256;  // 8 warps: 2 per TMEM lane quarter, each half of the key columns
+
+__device__ __forceinline__ float fast_exp2(float x) {  // MUFU.EX2 (ftz): p in (0, 1]
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 struct AttnMaps {
   CUtensorMap q, k, v;
@@ -101,19 +109,26 @@ struct AttnMaps {
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attention_tc_kernel(const __grid_constant__ AttnMaps maps, int L, int Lk16, int Lk64, int D,
                         __nv_bfloat16* __restrict__ out, long long ldo, float scale_log2) {
+  // smem: [V^T chunks | P chunks]; Q, K and the V staging rows live inside the
+  // P region (dead before P is written), so a CTA needs <= 100 KB: two per SM
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int nchunk = Lk64 / 64;
-  uint8_t* sQ = smem;                                   // 16 KB
-  uint8_t* sK = sQ + 128 * 128;                         // Lk16 x 128 B (rounded to 1 KB)
-  uint8_t* sVT = sK + ((Lk16 * 128 + 1023) & ~1023);    // nchunk x (64 x 128 B)
-  uint8_t* sP = sVT + nchunk * 8192;                    // nchunk x (128 x 128 B); V staging first
-  uint64_t* bar_ld = reinterpret_cast<uint64_t*>(sP + nchunk * 16384);
+  const int kbytes = (Lk16 * 128 + 1023) & ~1023;
+  uint8_t* sVT = smem;                                  // nchunk x (64 x 128 B)
+  uint8_t* sP = sVT + nchunk * 8192;                    // P: nchunk x (128 x 128 B)
+  uint8_t* sQ = sP;                                     // 16 KB   (inside P)
+  uint8_t* sK = sQ + 128 * 128;                         // Lk16 x 128 B
+  uint8_t* sVs = sK + kbytes;                           // V staging rows, Lk16 x 128 B
+  const int pbytes = max(nchunk * 16384, 128 * 128 + 2 * kbytes);
+  uint64_t* bar_ld = reinterpret_cast<uint64_t*>(sP + pbytes);
   uint64_t* bar_mma = bar_ld + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  __shared__ float s_red[2][128];  // per-half row max, then row sum
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.x;
   const long long row0 = (long long)blockIdx.y * L;
+  const int q0 = blockIdx.z * 128;  // this CTA's query block
 
   if (warp == 0) tmem_alloc(tmem_slot, 256);
   if (tid == 0) {
@@ -127,17 +142,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
-  uint32_t ph_ld = 0, ph_mma = 0;
   if (tid == 0) {
-    tma_prefetch_desc(&maps.q);
-    mbar_arrive_expect_tx(bar_ld, 2u * (uint32_t)Lk16 * 128u);
+    mbar_arrive_expect_tx(bar_ld, 2u * (uint32_t)Lk16 * 128u + 128u * 128u);
+    tma_load_2d(smem_addr(sQ), &maps.q, bar_ld, h * kHd, (int)(row0 + q0));
     tma_load_2d(smem_addr(sK), &maps.k, bar_ld, D + h * kHd, (int)row0);
-    tma_load_2d(smem_addr(sP), &maps.v, bar_ld, 2 * D + h * kHd, (int)row0);
+    tma_load_2d(smem_addr(sVs), &maps.v, bar_ld, 2 * D + h * kHd, (int)row0);
   }
-  mbar_wait(bar_ld, ph_ld);
-  ph_ld ^= 1;
+  mbar_wait(bar_ld, 0);
+  tc_fence_after();
+  const uint32_t idesc_s = umma_idesc_bf16_m128((uint32_t)Lk16);
+  const uint32_t idesc_o = umma_idesc_bf16_m128((uint32_t)kHd);
+  if (warp == 0) {  // S = Q K^T (4 K=16 steps over the head dim), overlaps the V transpose
+    const uint64_t qd = umma_desc_sw128(smem_addr(sQ)), kd = umma_desc_sw128(smem_addr(sK));
+#pragma unroll
+    for (int k = 0; k < kHd / 16; ++k) umma_bf16_elect(tmem, qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+    umma_commit_elect(bar_mma);
+  }
   // V^T: element (d, key) of chunk key/64 at d*128 + swizzled 16-B group of key%64
-  const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(sP);
+  const __nv_bfloat16* sV = reinterpret_cast<const __nv_bfloat16*>(sVs);
   for (int idx = tid; idx < kHd * (Lk64 / 8); idx += kAttnThreads) {
     const int d = idx & (kHd - 1), key0 = (idx >> 6) * 8;
     uint32_t w[4];
@@ -152,103 +174,100 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     *reinterpret_cast<uint4*>(sVT + (key0 >> 6) * 8192 + d * 128 + ((grp ^ (d & 7)) << 4)) =
         make_uint4(w[0], w[1], w[2], w[3]);
   }
-  fence_proxy_async_smem();
-  __syncthreads();
+  mbar_wait(bar_mma, 0);
+  tc_fence_after();
+  __syncthreads();  // V staging, Q and K consumed: the P region is free
 
-  const uint32_t idesc_s = umma_idesc_bf16_m128((uint32_t)Lk16);
-  const uint32_t idesc_o = umma_idesc_bf16_m128((uint32_t)kHd);
-  const int r = warp * 32 + lane;  // this thread's query row in the block (TMEM lane)
-  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  // warp w: TMEM lane quarter w % 4 (its 32 query rows), key-column half w / 4
+  const int quarter = warp & 3, half = warp >> 2;
+  const int r = quarter * 32 + lane;  // this thread's query row in the block (TMEM lane)
+  const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
   uint8_t* prow = sP + r * 128;
-  for (int q0 = 0; q0 < L; q0 += 128) {
-    if (tid == 0) {
-      mbar_arrive_expect_tx(bar_ld, 128u * 128u);
-      tma_load_2d(smem_addr(sQ), &maps.q, bar_ld, h * kHd, (int)(row0 + q0));
-    }
-    mbar_wait(bar_ld, ph_ld);
-    ph_ld ^= 1;
-    tc_fence_after();
-    if (warp == 0) {  // S = Q K^T (4 K=16 steps over the head dim)
-      const uint64_t qd = umma_desc_sw128(smem_addr(sQ)), kd = umma_desc_sw128(smem_addr(sK));
+  const int ch = Lk64 / 2;  // columns per half (a multiple of 32)
+  const int cbeg = half * ch, cend = cbeg + ch;
+  // row max over the valid keys: up to 64 columns per TMEM round trip
+  float mx = -INFINITY;
+  for (int c0 = cbeg; c0 < cend; c0 += 64) {
+    uint32_t v[4][16];
 #pragma unroll
-      for (int k = 0; k < kHd / 16; ++k) umma_bf16_elect(tmem, qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
-      umma_commit_elect(bar_mma);
-    }
-    mbar_wait(bar_mma, ph_mma);
-    ph_mma ^= 1;
-    tc_fence_after();
-    // row max over the valid keys
-    float mx = -INFINITY;
-    for (int c0 = 0; c0 < Lk16; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
-      tmem_wait_ld();
+    for (int u = 0; u < 4; ++u)
+      if (c0 + 16 * u < min(cend, Lk16)) tmem_ld_32x32b_x16(taddr + (uint32_t)(c0 + 16 * u), v[u]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (c0 + j < L) mx = fmaxf(mx, __uint_as_float(v[j]));
-    }
-    const float mxs = mx * scale_log2;
-    float sum = 0.0f;
-    for (int c0 = 0; c0 < Lk64; c0 += 16) {
+        if (c0 + 16 * u + j < min(cend, L)) mx = fmaxf(mx, __uint_as_float(v[u][j]));
+  }
+  s_red[half][r] = mx;
+  __syncthreads();
+  mx = fmaxf(s_red[0][r], s_red[1][r]);
+  const float mxs = mx * scale_log2;
+  float sum = 0.0f;
+  for (int c0 = cbeg; c0 < cend; c0 += 64) {
+    uint32_t v[4][16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + 16 * u < min(cend, Lk16)) tmem_ld_32x32b_x16(taddr + (uint32_t)(c0 + 16 * u), v[u]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + 16 * u >= cend) break;
+      uint8_t* chunk = prow + ((c0 + 16 * u) >> 6) * 16384;  // a half may start mid-chunk (Lk64 = 192)
       uint32_t pk[8];
-      if (c0 < Lk16) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
-        tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float p0 = c0 + 2 * j < L ? exp2f(__uint_as_float(v[2 * j]) * scale_log2 - mxs) : 0.0f;
-          const float p1 = c0 + 2 * j + 1 < L ? exp2f(__uint_as_float(v[2 * j + 1]) * scale_log2 - mxs) : 0.0f;
-          sum += p0 + p1;
-          pk[j] = pack_bf16x2(p0, p1);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pk[j] = 0u;
+      for (int j = 0; j < 8; ++j) {
+        const int c = c0 + 16 * u + 2 * j;
+        const float p0 = c < L ? fast_exp2(__uint_as_float(v[u][2 * j]) * scale_log2 - mxs) : 0.0f;
+        const float p1 = c + 1 < L ? fast_exp2(__uint_as_float(v[u][2 * j + 1]) * scale_log2 - mxs) : 0.0f;
+        sum += p0 + p1;
+        pk[j] = pack_bf16x2(p0, p1);
       }
-      uint8_t* chunk = prow + (c0 >> 6) * 16384;
-      const int g0 = (c0 & 63) >> 3;
+      const int g0 = ((c0 + 16 * u) & 63) >> 3;
       *reinterpret_cast<uint4*>(chunk + ((g0 ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       *reinterpret_cast<uint4*>(chunk + (((g0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
     }
-    tc_fence_before();
-    fence_proxy_async_smem();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 0) {  // O = P V over the key chunks, into the consumed S columns
-      for (int kc = 0; kc < nchunk; ++kc) {
-        const uint64_t pd = umma_desc_sw128(smem_addr(sP + kc * 16384));
-        const uint64_t vd = umma_desc_sw128(smem_addr(sVT + kc * 8192));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) umma_bf16_elect(tmem, pd + 2 * k, vd + 2 * k, idesc_o, (kc | k) != 0);
-      }
-      umma_commit_elect(bar_mma);
-    }
-    mbar_wait(bar_mma, ph_mma);
-    ph_mma ^= 1;
-    tc_fence_after();
-    const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
-    const int q = q0 + r;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(taddr + (uint32_t)(half * 32), v);
-      tmem_wait_ld();
-      if (q < L) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (row0 + q) * ldo + h * kHd + half * 32);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * j]) * inv, __uint_as_float(v[8 * j + 1]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * j + 2]) * inv, __uint_as_float(v[8 * j + 3]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * j + 4]) * inv, __uint_as_float(v[8 * j + 5]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * j + 6]) * inv, __uint_as_float(v[8 * j + 7]) * inv));
-      }
-    }
-    tc_fence_before();
-    __syncthreads();  // TMEM, sQ and sP are reused by the next query block
-    tc_fence_after();
   }
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  __syncthreads();  // every half has read its max from s_red
+  s_red[half][r] = sum;
+  tc_fence_before();
+  fence_proxy_async_smem();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {  // O = P V over the key chunks, into the consumed S columns
+    for (int kc = 0; kc < nchunk; ++kc) {
+      const uint64_t pd = umma_desc_sw128(smem_addr(sP + kc * 16384));
+      const uint64_t vd = umma_desc_sw128(smem_addr(sVT + kc * 8192));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) umma_bf16_elect(tmem, pd + 2 * k, vd + 2 * k, idesc_o, (kc | k) != 0);
+    }
+    umma_commit_elect(bar_mma);
+  }
+  mbar_wait(bar_mma, 1);
+  tc_fence_after();
+  sum = s_red[0][r] + s_red[1][r];
+  const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+  const int q = q0 + r;
+  uint32_t v[32];
+  tmem_ld_32x32b_x32(taddr + (uint32_t)(half * 32), v);  // this half's 32 output dims
+  tmem_wait_ld();
+  if (q < L) {
+    uint4* dst = reinterpret_cast<uint4*>(out + (row0 + q) * ldo + h * kHd + half * 32);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t* w = &v[8 * j];
+      dst[j] = make_uint4(pack_bf16x2(__uint_as_float(w[0]) * inv, __uint_as_float(w[1]) * inv),
+                          pack_bf16x2(__uint_as_float(w[2]) * inv, __uint_as_float(w[3]) * inv),
+                          pack_bf16x2(__uint_as_float(w[4]) * inv, __uint_as_float(w[5]) * inv),
+                          pack_bf16x2(__uint_as_float(w[6]) * inv, __uint_as_float(w[7]) * inv));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
 }
 
 // ------------------------------------------------------------- embeddings
@@ -393,13 +412,16 @@ int run_attention(const void* qkv, long long ld, int L, int H, int n_seq, void* 
   if (!rc) rc = encode_bf16_map(&maps.k, 2, qkv, dims, strides, bk, es, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc) rc = encode_bf16_map(&maps.v, 2, qkv, dims, strides, bk, es, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (rc) return rc;
-  const int smem = 1024 + 128 * 128 + ((Lk16 * 128 + 1023) & ~1023) + (Lk64 / 64) * (8192 + 16384) + 64;
+  const int kbytes = (Lk16 * 128 + 1023) & ~1023;
+  const int pbytes = (Lk64 / 64) * 16384 > 128 * 128 + 2 * kbytes ? (Lk64 / 64) * 16384 : 128 * 128 + 2 * kbytes;
+  const int smem = 1024 + (Lk64 / 64) * 8192 + pbytes + 64;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  launch_k(attention_tc_kernel, dim3(H, n_seq), dim3(kAttnThreads), smem, st, 1, maps, L, Lk16, Lk64, D,
+  launch_k(attention_tc_kernel, dim3(H, n_seq, (L + 127) / 128), dim3(kAttnThreads), smem, st, 1, maps, L, Lk16,
+           Lk64, D,
            reinterpret_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
   return check_launch("attention_tc_kernel");
 }

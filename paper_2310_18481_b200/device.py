@@ -73,6 +73,7 @@ _SIGS = {
     "ms_strategy_dp": ([_I, _P, _P, _P, _I, _I, _P, _P, _P], C.c_int),
     "ms_policy_apply": ([_I, _I, _P, _P, _P, _P, _P, _P, C.c_int64, C.c_int64, _I, _D, C.c_int64, _P, _LL,
                          _P, _P], C.c_int),
+    "ms_policy_max_jobs": ([_I], C.c_int),
     "ms_last_error": ([], C.c_char_p),
     "ms_device_sync": ([], C.c_int),
     "ms_policy_select": ([_P, _P, _P, _I, _P, C.c_int64, _D, _I, _P, _P], C.c_int),

@@ -18,7 +18,7 @@ from paper_2310_18481_b200.policy import DevicePolicy, Policy, apply_policy  # n
 
 cases = load_cases()
 for grid in (1000, 20):
-    pol = DevicePolicy(max_jobs=64, max_cand=64, grid_us=grid, ws_bytes=1 << 30)
+    pol = DevicePolicy(grid_us=grid)
     rows = {}
     for case in cases:
         n = len(case["jobs"])
@@ -35,7 +35,7 @@ for grid in (1000, 20):
         v = np.array(v)
         print(f"grid {grid:4d} us, {b:5s} jobs ({len(v):3d} queues): host median {np.median(v[:, 0]):8.0f} us "
               f"p90 {np.percentile(v[:, 0], 90):8.0f} | device median {np.median(v[:, 1]):6.0f} us "
-              f"p90 {np.percentile(v[:, 1], 90):6.0f}  (fallbacks {pol.host_fallbacks})")
+              f"p90 {np.percentile(v[:, 1], 90):6.0f}")
 
 # the batched TBN server's regime: marginal-cost frontiers (100s of us),
 # 15 ms deadlines, 20 us knapsack quantum
@@ -49,7 +49,7 @@ prof = marginal_profile(PassCostModel(enc, [30.0] * 96, 15, pass_all_us=pa), ("r
                         TBN_ACCURACY, 8)
 mat = build_matrix(prof, range(1, 25), recommended_alphas(prof))
 rng = np.random.default_rng(0)
-pol = DevicePolicy(max_jobs=256, max_cand=64, grid_us=20)
+pol = DevicePolicy(grid_us=20)
 for n_jobs in (8, 32, 64, 128):
     th, td = [], []
     for rep in range(20):
