@@ -537,6 +537,144 @@ constexpr int kMaxLineBytes = 16384;
 // frame_h > 0: the source lines are frames of frame_h rows and every frame
 // gets pad_h zero rows above and below in the destination (rows the kernel
 // never writes: the destination buffer is zeroed once at allocation).
+//
+// One staged unit of a padded gather: nl source lines (in line_buf, their
+// destination lines in s_dline) of compacted request j -> converted, padded
+// destination pixels (V = channels per vector store: 8 or 4).
+template <bool U8, int V>
+__device__ __forceinline__ void pad_store_lines(const unsigned char* __restrict__ line_buf,
+                                                const long long* __restrict__ s_dline, int nl, int line_bytes,
+                                                int width, int c_src, int gv, int wd, int pad_w, float u8_scale,
+                                                float u8_bias, long long plane_vecs, long long j,
+                                                long long dst_lines, void* __restrict__ dst_v) {
+  typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
+  vec_t* dst = reinterpret_cast<vec_t*>(dst_v);
+  vec_t* drow = dst + j * dst_lines * wd * gv;
+  if constexpr (V == 4) {
+    if ((wd & 1) == 0 && gv == 3) {  // 12-channel pixels: two per thread, three 16-B stores
+      const int wq = wd >> 1;
+      int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
+      const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
+      for (; li < nl; li += step_l, pq += step_p) {
+        if (pq >= wq) {
+          pq -= wq;
+          ++li;
+          if (li >= nl) break;
+        }
+        const unsigned char* lb = line_buf + li * line_bytes;
+        unsigned short v[24];
+#pragma unroll
+        for (int i = 0; i < 24; ++i) v[i] = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int x = 2 * pq + h - pad_w;
+          if (x >= 0 && x < width) {
+#pragma unroll
+            for (int c = 0; c < 12; ++c) {
+              if (c < c_src) {
+                if (U8) {
+                  const __nv_bfloat16 b =
+                      __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+                  v[12 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
+                } else {
+                  v[12 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+                }
+              }
+            }
+          }
+        }
+        if (plane_vecs > 0) {  // planar: channels 4q..4q+3 of both pixels -> plane q
+          const long long pix = ((long long)j * dst_lines + s_dline[li]) * wd + 2 * pq;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            *reinterpret_cast<uint4*>(dst + q * plane_vecs + pix) =
+                make_uint4(v[4 * q] | ((unsigned)v[4 * q + 1] << 16), v[4 * q + 2] | ((unsigned)v[4 * q + 3] << 16),
+                           v[12 + 4 * q] | ((unsigned)v[12 + 4 * q + 1] << 16),
+                           v[12 + 4 * q + 2] | ((unsigned)v[12 + 4 * q + 3] << 16));
+          continue;
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq) * 3);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          d4[q] = make_uint4(v[8 * q] | ((unsigned)v[8 * q + 1] << 16), v[8 * q + 2] | ((unsigned)v[8 * q + 3] << 16),
+                             v[8 * q + 4] | ((unsigned)v[8 * q + 5] << 16),
+                             v[8 * q + 6] | ((unsigned)v[8 * q + 7] << 16));
+      }
+      return;
+    }
+    if ((wd & 1) == 0 && gv == 1) {  // 4-channel pixels: two per thread, one 16-B store
+      const int wq = wd >> 1;
+      int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
+      const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
+      for (; li < nl; li += step_l, pq += step_p) {
+        if (pq >= wq) {
+          pq -= wq;
+          ++li;
+          if (li >= nl) break;
+        }
+        const unsigned char* lb = line_buf + li * line_bytes;
+        unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int x = 2 * pq + h - pad_w;
+          if (x >= 0 && x < width) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (c < c_src) {
+                if (U8) {
+                  const __nv_bfloat16 b =
+                      __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+                  v[4 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
+                } else {
+                  v[4 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+                }
+              }
+            }
+          }
+        }
+        *reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq)) =
+            make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
+                       v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+      }
+      return;
+    }
+  }
+  int li = threadIdx.x / wd, px = threadIdx.x - li * wd;  // (line, pixel), advanced without divisions
+  const int step_l = blockDim.x / wd, step_p = blockDim.x - step_l * wd;
+  for (; li < nl; li += step_l, px += step_p) {
+    if (px >= wd) {
+      px -= wd;
+      ++li;
+      if (li >= nl) break;
+    }
+    vec_t* d = drow + (s_dline[li] * wd + px) * gv;
+    const int x = px - pad_w;
+    const unsigned char* lb = line_buf + li * line_bytes;
+    for (int g = 0; g < gv; ++g) {
+      unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (x >= 0 && x < width) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          const int c = g * V + i;
+          if (c < c_src) {
+            if (U8) {
+              const __nv_bfloat16 b = __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
+              v[i] = *reinterpret_cast<const unsigned short*>(&b);
+            } else {
+              v[i] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
+            }
+          }
+        }
+      }
+      if constexpr (V == 8)
+        d[g] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
+                          v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+      else
+        d[g] = make_uint2(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16));
+    }
+  }
+}
+
 template <bool U8, int V>
 __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __restrict__ src_v, long long lines,
                                                               int width, int c_src, int c_dst, int pad_w,
@@ -554,10 +692,8 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
   // all of them (what a PDL successor's griddepcontrol.wait observes)
   if (pdl_mode != 2) pdl_wait();  // 0: standalone launch, 1: first of a chain
   pdl_trigger();
-  typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
   __shared__ long long s_dline[32];
-  vec_t* dst = reinterpret_cast<vec_t*>(dst_v);
   const int n = *count;
   const int esz = U8 ? 1 : 2;
   const int line_bytes = width * c_src * esz;
@@ -567,7 +703,6 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
   for (int j = blockIdx.y; j < n; j += gridDim.y) {
     const int r = gather_src_row(j, slot, idx, ring_base, n_ring);
     const unsigned char* srow = reinterpret_cast<const unsigned char*>(src_v) + (long long)r * lines * line_bytes;
-    vec_t* drow = dst + (long long)j * dst_lines * wd * gv;
     const int per = min(per_cap, max(1, kMaxLineBytes / line_bytes));  // lines staged per round
     for (long long ln0 = (long long)blockIdx.x * per; ln0 < lines; ln0 += (long long)gridDim.x * per) {
       const int nl = (int)min((long long)per, lines - ln0);
@@ -580,129 +715,8 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
         s_dline[threadIdx.x] = frame_h > 0 ? (ln / frame_h) * (frame_h + 2LL * pad_h) + pad_h + ln % frame_h : ln;
       }
       __syncthreads();
-      if constexpr (V == 4) {
-        if ((wd & 1) == 0 && gv == 3) {  // 12-channel pixels: two per thread, three 16-B stores
-          const int wq = wd >> 1;
-          int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
-          const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
-          for (; li < nl; li += step_l, pq += step_p) {
-            if (pq >= wq) {
-              pq -= wq;
-              ++li;
-              if (li >= nl) break;
-            }
-            const unsigned char* lb = line_buf + li * line_bytes;
-            unsigned short v[24];
-#pragma unroll
-            for (int i = 0; i < 24; ++i) v[i] = 0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int x = 2 * pq + h - pad_w;
-              if (x >= 0 && x < width) {
-#pragma unroll
-                for (int c = 0; c < 12; ++c) {
-                  if (c < c_src) {
-                    if (U8) {
-                      const __nv_bfloat16 b =
-                          __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
-                      v[12 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
-                    } else {
-                      v[12 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
-                    }
-                  }
-                }
-              }
-            }
-            if (plane_vecs > 0) {  // planar: channels 4q..4q+3 of both pixels -> plane q
-              const long long pix = ((long long)j * dst_lines + s_dline[li]) * wd + 2 * pq;
-#pragma unroll
-              for (int q = 0; q < 3; ++q)
-                *reinterpret_cast<uint4*>(dst + q * plane_vecs + pix) =
-                    make_uint4(v[4 * q] | ((unsigned)v[4 * q + 1] << 16), v[4 * q + 2] | ((unsigned)v[4 * q + 3] << 16),
-                               v[12 + 4 * q] | ((unsigned)v[12 + 4 * q + 1] << 16),
-                               v[12 + 4 * q + 2] | ((unsigned)v[12 + 4 * q + 3] << 16));
-              continue;
-            }
-            uint4* d4 = reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq) * 3);
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-              d4[q] = make_uint4(v[8 * q] | ((unsigned)v[8 * q + 1] << 16), v[8 * q + 2] | ((unsigned)v[8 * q + 3] << 16),
-                                 v[8 * q + 4] | ((unsigned)v[8 * q + 5] << 16),
-                                 v[8 * q + 6] | ((unsigned)v[8 * q + 7] << 16));
-          }
-          continue;
-        }
-        if ((wd & 1) == 0 && gv == 1) {  // 4-channel pixels: two per thread, one 16-B store
-          const int wq = wd >> 1;
-          int li = threadIdx.x / wq, pq = threadIdx.x - li * wq;
-          const int step_l = blockDim.x / wq, step_p = blockDim.x - step_l * wq;
-          for (; li < nl; li += step_l, pq += step_p) {
-            if (pq >= wq) {
-              pq -= wq;
-              ++li;
-              if (li >= nl) break;
-            }
-            const unsigned char* lb = line_buf + li * line_bytes;
-            unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int x = 2 * pq + h - pad_w;
-              if (x >= 0 && x < width) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                  if (c < c_src) {
-                    if (U8) {
-                      const __nv_bfloat16 b =
-                          __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
-                      v[4 * h + c] = *reinterpret_cast<const unsigned short*>(&b);
-                    } else {
-                      v[4 * h + c] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
-                    }
-                  }
-                }
-              }
-            }
-            *reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq)) =
-                make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
-                           v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
-          }
-          continue;
-        }
-      }
-      int li = threadIdx.x / wd, px = threadIdx.x - li * wd;  // (line, pixel), advanced without divisions
-      const int step_l = blockDim.x / wd, step_p = blockDim.x - step_l * wd;
-      for (; li < nl; li += step_l, px += step_p) {
-        if (px >= wd) {
-          px -= wd;
-          ++li;
-          if (li >= nl) break;
-        }
-        vec_t* d = drow + (s_dline[li] * wd + px) * gv;
-        const int x = px - pad_w;
-        const unsigned char* lb = line_buf + li * line_bytes;
-        for (int g = 0; g < gv; ++g) {
-          unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          if (x >= 0 && x < width) {
-#pragma unroll
-            for (int i = 0; i < V; ++i) {
-              const int c = g * V + i;
-              if (c < c_src) {
-                if (U8) {
-                  const __nv_bfloat16 b = __float2bfloat16_rn(fmaf((float)lb[x * c_src + c], u8_scale, u8_bias));
-                  v[i] = *reinterpret_cast<const unsigned short*>(&b);
-                } else {
-                  v[i] = reinterpret_cast<const unsigned short*>(lb)[x * c_src + c];
-                }
-              }
-            }
-          }
-          if constexpr (V == 8)
-            d[g] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
-                              v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
-          else
-            d[g] = make_uint2(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16));
-        }
-      }
+      pad_store_lines<U8, V>(line_buf, s_dline, nl, line_bytes, width, c_src, gv, wd, pad_w, u8_scale, u8_bias,
+                             plane_vecs, j, dst_lines, dst_v);
     }
   }
   if (pdl_mode == 2) pdl_wait();
@@ -747,6 +761,205 @@ __global__ void gather_rows_pad_scalar_kernel(const void* __restrict__ src_v, lo
       }
       d[t] = make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16),
                         v[4] | ((unsigned)v[5] << 16), v[6] | ((unsigned)v[7] << 16));
+    }
+  }
+}
+
+// ---------------------------------------------------- fused compaction
+// ms_compact in ONE persistent launch (index + every modality's gather):
+// every CTA recomputes the per-modality compacted index from the masks in
+// shared memory (N <= 1024: a few ballots), CTA 0 also writes the global
+// idx / inv / counts / combo offsets / perm; then all CTAs walk one unit list
+// spanning the modalities -- unit = (modality k, compacted request j, a chunk
+// of <= 16 KB of source lines, or of row bytes for plain copies) -- so the
+// work is balanced across modalities with no launch or PDL-chain gaps, and
+// the next unit's lines are loaded into registers while the current unit is
+// converted and stored (loads in flight behind the stores).
+constexpr int kFusedMaxN = 1024;
+constexpr int kFusedThreads = 256;
+constexpr int kFusedVecs = kMaxLineBytes / 16 / kFusedThreads;  // 16-B vectors per thread per unit (4)
+
+struct FusedMod {
+  const unsigned char* X;
+  void* G;
+  const int32_t* slot;  // request -> pool row (nullptr: identity), already offset by slot_off
+  long long lines, plane_vecs, row_vecs, dst_lines;
+  int width, c_src, c_dst, pad_w, src_u8, frame_h, pad_h, ring_base;
+  int kind;  // 0 none, 1 plain row copy, 2 padded
+  int per;   // lines (padded) or 16-B vectors (plain) per unit
+  int chunks, line_bytes;
+  float u8_scale, u8_bias;
+};
+struct FusedArgs {
+  const uint16_t* mask;
+  int N, K, n_ring;
+  int32_t *idx, *inv, *counts, *offsets, *perm;
+  FusedMod m[kMaxK];
+};
+
+__global__ void __launch_bounds__(kFusedThreads, 4) compact_fused_kernel(const __grid_constant__ FusedArgs a) {
+  __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
+  __shared__ long long s_dline[32];
+  __shared__ int16_t s_idx[kMaxK][kFusedMaxN];
+  __shared__ int s_wt[kMaxK][kFusedThreads / 32];
+  __shared__ int s_base[kMaxK];
+  __shared__ int s_hist[1 << kMaxK];
+  pdl_wait();
+  pdl_trigger();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int N = a.N, K = a.K, bins = 1 << K;
+  const unsigned lt = (1u << lane) - 1u;
+  const bool writer = blockIdx.x == 0;
+  if (t < K) s_base[t] = 0;
+  if (writer)
+    for (int b = t; b < bins; b += kFusedThreads) s_hist[b] = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < N; c0 += kFusedThreads) {
+    const int i = c0 + t;
+    const int m = i < N ? (int)a.mask[i] : 0;
+    if (writer && i < N) atomicAdd(&s_hist[m & (bins - 1)], 1);
+    unsigned bal[kMaxK];
+    for (int k = 0; k < K; ++k) {
+      bal[k] = __ballot_sync(kFull, i < N && ((m >> k) & 1));
+      if (lane == 0) s_wt[k][warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    if (t < K) {  // exclusive scan of the 8 warp totals of modality t
+      int acc = s_base[t];
+      for (int w = 0; w < kFusedThreads / 32; ++w) {
+        const int v = s_wt[t][w];
+        s_wt[t][w] = acc;
+        acc += v;
+      }
+      s_base[t] = acc;
+    }
+    __syncthreads();
+    if (i < N) {
+      for (int k = 0; k < K; ++k) {
+        int pos = -1;
+        if ((m >> k) & 1) {
+          pos = s_wt[k][warp] + __popc(bal[k] & lt);
+          s_idx[k][pos] = (int16_t)i;
+          if (writer) a.idx[(long long)k * N + pos] = i;
+        }
+        if (writer) a.inv[(long long)k * N + i] = pos;
+      }
+    }
+    __syncthreads();
+  }
+  if (writer) {
+    if (t < K) a.counts[t] = s_base[t];
+    if (t == 0) {  // combo offsets (exclusive scan of the histogram, bins <= 256)
+      int acc = 0;
+      for (int b = 0; b < bins; ++b) {
+        a.offsets[b] = acc;
+        const int h = s_hist[b];
+        s_hist[b] = acc;  // becomes the placement cursor
+        acc += h;
+      }
+      a.offsets[bins] = acc;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < N; c0 += kFusedThreads) {  // stable counting sort by mask
+      const int i = c0 + t;
+      const int m = i < N ? (int)a.mask[i] & (bins - 1) : bins;
+      const unsigned peers = __match_any_sync(kFull, m);
+      const int rank = __popc(peers & lt), leader = __ffs(peers) - 1;
+      for (int w = 0; w < kFusedThreads / 32; ++w) {
+        if (warp == w && i < N) {
+          int base = 0;
+          if (lane == leader) base = atomicAdd(&s_hist[m], __popc(peers));
+          base = __shfl_sync(peers, base, leader);
+          a.perm[base + rank] = i;
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // ---- units across modalities
+  long long ubase[kMaxK + 1];
+  ubase[0] = 0;
+  for (int k = 0; k < K; ++k) ubase[k + 1] = ubase[k] + (a.m[k].kind ? (long long)s_base[k] * a.m[k].chunks : 0);
+  const long long U = ubase[K];
+  uint4 pre[kFusedVecs];
+  int pre_n = 0;  // 16-B vectors prefetched into registers for the next unit
+  auto locate = [&](long long u, int& k, int& j, int& c) {
+    k = 0;
+    while (u >= ubase[k + 1]) ++k;
+    const long long local = u - ubase[k];
+    j = (int)(local / a.m[k].chunks);
+    c = (int)(local - (long long)j * a.m[k].chunks);
+  };
+  auto src_row = [&](int k, int j) -> long long {
+    const FusedMod& M = a.m[k];
+    if (a.n_ring > 0) return ((long long)M.ring_base + j) % a.n_ring;
+    const int r = s_idx[k][j];
+    return M.slot ? M.slot[r] : r;
+  };
+  auto prefetch = [&](long long u) {  // padded units only: their staged lines, into registers
+    pre_n = 0;
+    if (u >= U) return;
+    int k, j, c;
+    locate(u, k, j, c);
+    const FusedMod& M = a.m[k];
+    if (M.kind != 2) return;
+    const long long ln0 = (long long)c * M.per;
+    const int nl = (int)min((long long)M.per, M.lines - ln0);
+    const int nv = nl * M.line_bytes / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(M.X + (src_row(k, j) * M.lines + ln0) * M.line_bytes);
+#pragma unroll
+    for (int q = 0; q < kFusedVecs; ++q) {
+      const int v = t + q * kFusedThreads;
+      if (v < nv) pre[q] = __ldcs(s4 + v);
+    }
+    pre_n = nv;
+  };
+  long long u = blockIdx.x;
+  prefetch(u);
+  for (; u < U; u += gridDim.x) {
+    int k, j, c;
+    locate(u, k, j, c);
+    const FusedMod& M = a.m[k];
+    if (M.kind == 1) {  // plain row copy: one chunk of 16-B vectors
+      const long long v0 = (long long)c * M.per, v1 = min(M.row_vecs, v0 + M.per);
+      const uint4* s4 = reinterpret_cast<const uint4*>(M.X) + src_row(k, j) * M.row_vecs;
+      uint4* d4 = reinterpret_cast<uint4*>(M.G) + (long long)j * M.row_vecs;
+      for (long long v = v0 + t; v < v1; v += kFusedThreads) d4[v] = __ldcs(s4 + v);
+      prefetch(u + gridDim.x);
+      continue;
+    }
+    const long long ln0 = (long long)c * M.per;
+    const int nl = (int)min((long long)M.per, M.lines - ln0);
+    __syncthreads();  // the previous unit's stores have read line_buf
+#pragma unroll
+    for (int q = 0; q < kFusedVecs; ++q) {
+      const int v = t + q * kFusedThreads;
+      if (v < pre_n) reinterpret_cast<uint4*>(line_buf)[v] = pre[q];
+    }
+    if (t < nl) {
+      const long long ln = ln0 + t;
+      s_dline[t] = M.frame_h > 0 ? (ln / M.frame_h) * (M.frame_h + 2LL * M.pad_h) + M.pad_h + ln % M.frame_h : ln;
+    }
+    __syncthreads();
+    prefetch(u + gridDim.x);  // next unit's loads in flight behind this unit's stores
+    const int wd = M.width + 2 * M.pad_w;
+    if (M.c_dst % 8 != 0) {
+      const int gv = M.c_dst / 4;
+      if (M.src_u8)
+        pad_store_lines<true, 4>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, M.u8_scale,
+                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G);
+      else
+        pad_store_lines<false, 4>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, 1.0f, 0.0f,
+                                  M.plane_vecs, j, M.dst_lines, M.G);
+    } else {
+      const int gv = M.c_dst / 8;
+      if (M.src_u8)
+        pad_store_lines<true, 8>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, M.u8_scale,
+                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G);
+      else
+        pad_store_lines<false, 8>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, 1.0f, 0.0f,
+                                  M.plane_vecs, j, M.dst_lines, M.G);
     }
   }
 }
@@ -910,10 +1123,85 @@ int ms_gather_rows_pad(const void* src, long long lines, int width, int c_src, i
                            reinterpret_cast<cudaStream_t>(stream));
 }
 
+// the single-launch path (compact_fused_kernel) when every row fits it
+static int compact_fused(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
+                         const int32_t* slot, const int32_t* ring_base, int n_ring, void* const* G, int32_t* idx,
+                         int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm, cudaStream_t st,
+                         bool* done) {
+  *done = false;
+  static const bool off = getenv("MS_COMPACT_UNFUSED") != nullptr;  // A/B switch for tools/compact_time.py
+  if (off || N > kFusedMaxN || K > kMaxK || N < 1) return MS_OK;
+  FusedArgs a;
+  memset(&a, 0, sizeof a);
+  a.mask = mask;
+  a.N = N;
+  a.K = K;
+  a.n_ring = n_ring;
+  a.idx = idx;
+  a.inv = inv;
+  a.counts = counts;
+  a.offsets = combo_offsets;
+  a.perm = perm;
+  long long work = 0;
+  for (int k = 0; k < K; ++k) {
+    FusedMod& M = a.m[k];
+    if (X == nullptr || G == nullptr || rows == nullptr || X[k] == nullptr || G[k] == nullptr) continue;
+    const MsRowDesc& r = rows[k];
+    const bool framed = r.frame_h > 0 && r.pad_h > 0;
+    M.X = reinterpret_cast<const unsigned char*>(X[k]);
+    M.G = G[k];
+    M.slot = slot ? slot + r.slot_off : nullptr;
+    M.ring_base = n_ring > 0 ? ring_base[k] : 0;
+    const long long bytes = r.lines * (long long)r.width * r.c_src * 2;
+    if (!r.src_u8 && r.c_src == r.c_dst && r.pad_w == 0 && !framed && r.plane_stride == 0 && bytes % 16 == 0) {
+      M.kind = 1;
+      M.row_vecs = bytes / 16;
+      M.per = kMaxLineBytes / 16;
+      M.chunks = (int)((M.row_vecs + M.per - 1) / M.per);
+      work += bytes;
+      continue;
+    }
+    const long long line_bytes = (long long)r.width * r.c_src * (r.src_u8 ? 1 : 2);
+    if (r.c_dst % 4 != 0 || r.c_src > r.c_dst || r.c_src < 1 || r.pad_w < 0 || r.width < 1 || line_bytes % 16 != 0 ||
+        line_bytes > kMaxLineBytes || (framed && r.lines % r.frame_h != 0))
+      return MS_OK;  // not a fused shape: the per-modality launches handle (or reject) it
+    if (r.plane_stride > 0 && (r.c_dst != 12 || ((r.width + 2 * r.pad_w) & 1) != 0 || r.plane_stride % 4 != 0))
+      return MS_OK;
+    M.kind = 2;
+    M.lines = r.lines;
+    M.width = r.width;
+    M.c_src = r.c_src;
+    M.c_dst = r.c_dst;
+    M.pad_w = r.pad_w;
+    M.src_u8 = r.src_u8;
+    M.u8_scale = r.src_u8 ? r.u8_scale : 1.0f;
+    M.u8_bias = r.src_u8 ? r.u8_bias : 0.0f;
+    M.frame_h = framed ? r.frame_h : 0;
+    M.pad_h = framed ? r.pad_h : 0;
+    M.plane_vecs = r.plane_stride / 4;
+    M.line_bytes = (int)line_bytes;
+    M.per = (int)(kMaxLineBytes / line_bytes < 32 ? kMaxLineBytes / line_bytes : 32);
+    M.chunks = (int)((r.lines + M.per - 1) / M.per);
+    M.dst_lines = framed ? r.lines + (r.lines / r.frame_h) * 2LL * r.pad_h : r.lines;
+    work += r.lines * line_bytes;
+  }
+  // a few CTAs per SM, no more than the work needs at max occupancy
+  long long blocks = (work * N / 2 + kMaxLineBytes - 1) / kMaxLineBytes;
+  if (blocks > 148LL * 4) blocks = 148LL * 4;  // one resident wave (<= 64 registers x 256 threads: 4 CTAs per SM)
+  if (blocks < 1) blocks = 1;
+  launch_k(compact_fused_kernel, dim3((unsigned)blocks), dim3(kFusedThreads), 0, st, 1, a);
+  *done = true;
+  return check_launch("compact_fused_kernel");
+}
+
 static int compact_impl(const uint16_t* mask, int N, int K, const void* const* X, const MsRowDesc* rows,
                         const int32_t* slot, const int32_t* ring_base, int n_ring, void* const* G, int32_t* idx,
                         int32_t* inv, int32_t* counts, int32_t* combo_offsets, int32_t* perm, void* stream) {
-  int rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
+  bool done = false;
+  int rc = compact_fused(mask, N, K, X, rows, slot, ring_base, n_ring, G, idx, inv, counts, combo_offsets, perm,
+                         reinterpret_cast<cudaStream_t>(stream), &done);
+  if (rc || done) return rc;
+  rc = ms_compact_index(mask, N, K, idx, inv, counts, combo_offsets, perm, stream);
   if (rc) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bool chained = false;  // the previous launch was a padded gather of this chain

@@ -776,3 +776,58 @@ def test_conv_k32_vs_torch(dev, n, H, Cin, Cout, s, tile):
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
     ok, err, scale = _close(D.cpu(), ref)
     assert ok, (err, scale)
+
+
+def test_fused_compaction_multi_modality_slots_vs_torch(dev):
+    """The single-launch ms_compact (index + all modalities' gathers in one
+    persistent kernel, units spanning modalities): plain bf16 rows, uint8
+    4-channel framed rows and planar 12-channel rows through per-modality
+    slot maps, N = 700 mixed masks -- every gathered row equals the torch
+    gather, index outputs equal the oracle."""
+    import ctypes
+    L = dev.lib()
+    N, K = 700, 3
+    rng = np.random.default_rng(5)
+    masks = rng.integers(1, 1 << K, size=N)
+    mask = torch.as_tensor(masks.astype(np.int16)).cuda()
+    pool0 = _bf(torch.randn(900, 256)).cuda()
+    fr, fh, w, pad, pad_h = 2, 5, 48, 3, 3  # 16-B aligned u8 lines (48 x 3, 48 x 10)
+    pool1 = torch.randint(0, 256, (800, fr * fh, w, 3), dtype=torch.uint8).cuda()
+    pool2 = torch.randint(0, 256, (750, fr * fh, w, 10), dtype=torch.uint8).cuda()
+    slot = torch.as_tensor(np.concatenate([rng.permutation(900)[:N], rng.permutation(800)[:N],
+                                           rng.permutation(750)[:N]]).astype(np.int32)).cuda()
+    G0 = torch.zeros(N, 256, dtype=torch.bfloat16, device="cuda")
+    G1 = torch.zeros(N, fr, fh + 2 * pad_h, w + 2 * pad, 4, dtype=torch.bfloat16, device="cuda")
+    G2 = torch.zeros(3, N * fr * fh, w + 2 * pad, 4, dtype=torch.bfloat16, device="cuda")
+    rows = (dev.RowDesc * 3)(dev.RowDesc(1, 1, 256, 256, 0, 0, 1.0, 0.0, 0, 0, 0),
+                             dev.RowDesc(fr * fh, w, 3, 4, pad, 1, 1.0 / 64.0, -2.0, fh, pad_h, N),
+                             dev.RowDesc(fr * fh, w, 10, 12, pad, 1, 1.0 / 64.0, -2.0, 0, 0, 2 * N,
+                                         N * fr * fh * (w + 2 * pad) * 4))
+    X = (ctypes.c_void_p * 3)(pool0.data_ptr(), pool1.data_ptr(), pool2.data_ptr())
+    G = (ctypes.c_void_p * 3)(G0.data_ptr(), G1.data_ptr(), G2.data_ptr())
+    ix = torch.empty(K * N, dtype=torch.int32, device="cuda")
+    inv = torch.empty(K * N, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(K, dtype=torch.int32, device="cuda")
+    offs = torch.empty((1 << K) + 1, dtype=torch.int32, device="cuda")
+    perm = torch.empty(N, dtype=torch.int32, device="cuda")
+    dev.check(L.ms_compact(mask.data_ptr(), N, K, X, rows, slot.data_ptr(), G, ix.data_ptr(), inv.data_ptr(),
+                           cnt.data_ptr(), offs.data_ptr(), perm.data_ptr(), dev.stream_ptr()), "compact")
+    torch.cuda.synchronize()
+    e_idx, e_inv, e_counts = orc.compact(masks.astype(np.int64), K)
+    assert cnt.cpu().tolist() == e_counts.tolist()
+    assert np.array_equal(perm.cpu().numpy(), np.argsort(masks, kind="stable"))
+    for k in range(K):
+        assert np.array_equal(inv.view(K, N)[k].cpu().numpy(), e_inv[k])
+    s = slot.long()
+    c0, c1, c2 = (int(x) for x in e_counts)
+    r0 = s[:N][torch.as_tensor(e_idx[0]).long().cuda()]
+    assert torch.equal(G0[:c0], pool0[r0])
+    r1 = s[N:2 * N][torch.as_tensor(e_idx[1]).long().cuda()]
+    exp1 = (pool1[r1].float() / 64.0 - 2.0).to(torch.bfloat16).view(c1, fr, fh, w, 3)
+    assert torch.equal(G1[:c1, :, pad_h:pad_h + fh, pad:pad + w, :3], exp1)
+    r2 = s[2 * N:][torch.as_tensor(e_idx[2]).long().cuda()]
+    exp2 = (pool2[r2].float() / 64.0 - 2.0).to(torch.bfloat16).view(c2 * fr * fh, w, 10)
+    full = torch.zeros(c2 * fr * fh, w, 12, dtype=torch.bfloat16, device="cuda")
+    full[..., :10] = exp2
+    for q in range(3):
+        assert torch.equal(G2[q, :c2 * fr * fh, pad:pad + w], full[..., 4 * q:4 * q + 4])
