@@ -268,10 +268,6 @@ int ms_gemm_plan_debug(void* plan, int flags);
  * PDL wait done, first TMA issued, first data ready, last MMA commit, first
  * accumulator ready, epilogue done) into buf[grid_x * 8], or NULL to stop. */
 int ms_gemm_plan_set_trace(void* plan, unsigned long long* buf);
-/* Debug probe of shifted K-major SW128 UMMA operand descriptors (tools/umma_probe.py). */
-int ms_debug_umma_shift(const void* A, const void* W, float* D, int shift, int sbo, int use_base, void* stream);
-/* debug: clocks for `count` back-to-back M=128 K=16 MMAs of width n with A layout `mode` (tools/umma_rate.py) */
-int ms_debug_umma_rate(int mode, int n, int count, long long* cycles, void* stream);
 int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, int* smem_bytes);
 
 /* ---- HBM-bound ops (NHWC bf16) ---------------------------------------- */

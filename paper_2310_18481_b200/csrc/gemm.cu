@@ -45,7 +45,7 @@ constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 
 enum GemmMode : int {
-  MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV1_ROWS = 4, MODE_CONV_C4 = 5,
+  MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV_C4 = 5,
   MODE_CONV_HALO = 6, MODE_CONV_C12 = 7, MODE_CONV_K32 = 8, MODE_STEM_POOL = 9
 };
 // MODE_CONV_K32: implicit-GEMM conv whose input channel count is a multiple
@@ -111,7 +111,6 @@ struct GemmParams {
   // CONV geometry
   int n_img, OH, OW, stride, pad, KW, cchunks, bn, bh, bw, tiles_w, tiles_h;
   int smallc_halves, smallc_jpb;  // K blocks per filter row, window pixels per K block
-  int H_in;                       // input height (MODE_CONV1_ROWS)
   int pair;                       // 1: CTA-pair (cta_group::2) kernel
   // GATHER
   const __nv_bfloat16* feat[4];
@@ -944,181 +943,6 @@ static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
 
 
 // ------------------------------------------------------------------------
-// MODE_CONV1_ROWS: the few-channel first convolution (7x7/2 over 8/16 padded
-// channels) streamed input row by input row.  One CTA owns whole images; a
-// K block is (input row hi, window half) = ONE overlapping-stride TMA box of
-// all OW output windows (128 B each).  Every input row is loaded ONCE and
-// feeds each output row whose 7-row window contains it (up to 4), each into
-// its own TMEM accumulator: 8 accumulators of 64 columns form a ring over
-// output rows, retired to the epilogue as soon as their last input row has
-// been consumed.  Versus one box per (output row, kh) this cuts the A-operand
-// (L2->SMEM) traffic ~3.4x, which is what bounds this layer (N = Cout = 64).
-constexpr int kC1Slots = 8;
-constexpr int kC1WBytes = 64 * 128;  // one (kh, half) weight block: 64 co x 64 k
-
-__global__ void __launch_bounds__(kThreads, 1)
-    conv1_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const __grid_constant__ GemmParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  const int KH = p.num_kb / p.smallc_halves;  // num_kb = KH * halves weight blocks
-  const int halves = p.smallc_halves;
-  const int stages = p.stages;
-  uint8_t* smW = smem;                                    // [KH*halves][8 KB], resident
-  uint8_t* smA = smW + p.num_kb * kC1WBytes;              // [stages][16 KB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smA + stages * kABytes);
-  uint64_t* empty = full + stages;
-  uint64_t* wbar = empty + stages;
-  uint64_t* tfull = wbar + 1;
-  uint64_t* tempty = tfull + kC1Slots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kC1Slots);
-  uint8_t* sstage = reinterpret_cast<uint8_t*>(tmem_slot + 4);
-  sstage += (16u - (smem_addr(sstage) & 15u)) & 15u;  // 16-B aligned staging rows
-  float* sbias = reinterpret_cast<float*>(sstage + kStageBytes);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int H = p.H_in, OH = p.OH, OW = p.OW, S = p.stride, PAD = p.pad;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(wbar, 1);
-    for (int i = 0; i < kC1Slots; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  for (int i = threadIdx.x; i < p.N; i += blockDim.x) sbias[i] = p.bias ? p.bias[i] : 0.0f;
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
-  pdl_wait();
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------------------------------- TMA producer
-      mbar_arrive_expect_tx(wbar, p.num_kb * kC1WBytes);
-      for (int wb = 0; wb < p.num_kb; ++wb) tma_load_2d(smem_addr(smW + wb * kC1WBytes), &tmB, wbar, wb * kBK, 0);
-      int s = 0;
-      uint32_t phase = 0;
-      for (int img = blockIdx.x; img < p.n_img; img += gridDim.x)
-        for (int hi = 0; hi < H; ++hi)
-          for (int hf = 0; hf < halves; ++hf) {
-            mbar_wait(&empty[s], phase ^ 1);
-            mbar_arrive_expect_tx(&full[s], p.a_bytes);
-            tma_load_4d(smem_addr(smA + s * kABytes), &tmA, &full[s], hf * kBK, 0, hi, img);
-            if (++s == stages) {
-              s = 0;
-              phase ^= 1;
-            }
-          }
-    }
-  } else if (warp == 1) {  // ------------------------------------ MMA issuer
-    const uint32_t idesc = umma_idesc_bf16_m128(64);
-    mbar_wait(wbar, 0);
-    tc_fence_after();
-    int s = 0;
-    uint32_t phase = 0;
-    int rbase = 0;  // this CTA's output-row counter (ring slot = r & 7, use = r >> 3)
-    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, rbase += OH) {
-      for (int hi = 0; hi < H; ++hi) {
-        for (int hf = 0; hf < halves; ++hf) {
-          mbar_wait(&full[s], phase);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint64_t adesc = umma_desc_sw128(smem_addr(smA + s * kABytes));
-            // kh = hi + PAD - S*oh: walk the contributing output rows directly
-            const int t0 = hi + PAD;
-            int oh_hi = S == 2 ? (t0 >> 1) : t0;             // kh = t0 - S*oh >= 0
-            int oh_lo = S == 2 ? ((t0 - KH + 2) >> 1) : t0 - KH + 1;  // kh <= KH-1
-            if (oh_lo < 0) oh_lo = 0;
-            if (oh_hi > OH - 1) oh_hi = OH - 1;
-            for (int oh = oh_lo; oh <= oh_hi; ++oh) {
-              const int kh = t0 - S * oh;
-              const int r = rbase + oh;
-              const int slot = r & (kC1Slots - 1);
-              const int first_in = max(0, oh * S - PAD);
-              const int last_in = min(H - 1, oh * S - PAD + KH - 1);
-              const bool first = (hi == first_in) && hf == 0;
-              if (first) {  // accumulator slot must have been drained by the epilogue
-                mbar_wait(&tempty[slot], (uint32_t)(((r >> 3) & 1) ^ 1));
-                tc_fence_after();
-              }
-              const uint64_t bdesc = umma_desc_sw128(smem_addr(smW + (kh * halves + hf) * kC1WBytes));
-              const uint32_t d = tmem_base + (uint32_t)slot * 64;
-#pragma unroll
-              for (int k = 0; k < kBK / 16; ++k) umma_bf16(d, adesc + 2 * k, bdesc + 2 * k, idesc, !(first && k == 0));
-              if (hi == last_in && hf == halves - 1) umma_commit(&tfull[slot]);
-            }
-            umma_commit(&empty[s]);
-          }
-          __syncwarp();
-          if (++s == stages) {
-            s = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else {  // -------------------------------------------- epilogue warps 2..9
-    const int q = warp & 3, c = (warp - 2) >> 2;  // lane quarter, 32-column chunk
-    const int ow = q * 32 + lane;
-    int rbase = 0;
-    uint8_t* st = sstage + (warp - 2) * kStageWarpBytes;
-    for (int img = blockIdx.x; img < p.n_img; img += gridDim.x, rbase += OH) {
-      for (int oh = 0; oh < OH; ++oh) {
-        const int r = rbase + oh;
-        const int slot = r & (kC1Slots - 1);
-        mbar_wait(&tfull[slot], (uint32_t)((r >> 3) & 1));
-        tc_fence_after();
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + (uint32_t)(slot * 64 + c * 32) + ((uint32_t)(q * 32) << 16), v);
-        tmem_wait_ld();
-        uint32_t pk[16];
-        const float* bch = sbias + c * 32;
-        if (p.relu)
-          convert_chunk<MS_ACT_RELU>(v, bch, pk);
-        else
-          convert_chunk<MS_ACT_NONE>(v, bch, pk);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[slot]);  // TMEM slot free; data is in registers
-        uint4* mine = reinterpret_cast<uint4*>(st + lane * kStageRowBytes);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) mine[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        __syncwarp();
-        const Seg& D = p.seg[0];
-        const long long row0 = ((long long)img * OH + oh) * OW;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = i * 8 + (lane >> 2), piece = lane & 3;
-          const int oc = q * 32 + rr;
-          if (oc < OW)
-            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D.ptr) + (row0 + oc) * D.ldd + D.col0 +
-                                      c * 32 + piece * 8) =
-                *reinterpret_cast<const uint4*>(st + rr * kStageRowBytes + piece * 16);
-        }
-        __syncwarp();
-      }
-    }
-    (void)ow;
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
-  }
-}
-
-// ------------------------------------------------------------------------
 // MODE_STEM_POOL: the 7x7/2 first convolution over 4-channel pixels (rgb 3 ->
 // 4, audio 1 -> 4) FUSED with the 3x3/2 ceil-mode max pool that follows it.
 // The unpooled conv output (4x the pooled bytes) never reaches HBM.
@@ -1602,32 +1426,6 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   return MS_OK;
 }
 
-static int finish_conv1_rows(GemmPlan* P, const void* Wt, int num_wb) {
-  GemmParams& p = P->p;
-  cuuint64_t dims[2] = {(cuuint64_t)(num_wb * kBK), 64};
-  cuuint64_t strides[1] = {(cuuint64_t)num_wb * kBK * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, 64};
-  cuuint32_t es[2] = {1, 1};
-  int rc = encode_map(&P->tmB, 2, Wt, dims, strides, box, es);
-  if (rc) return rc;
-  p.BN = 64;
-  p.num_kb = num_wb;
-  p.ksplit = 1;
-  p.kb_per = num_wb;
-  const int fixed = 1024 + num_wb * kC1WBytes + 256 + kStageBytes + 64 * 4 + (4 + 2 * kC1Slots) * 8 + 32;
-  int stages = (226 * 1024 - fixed) / kABytes;
-  if (stages > 8) stages = 8;
-  if (stages < 2) return set_error(MS_ERR_INVALID, "conv1 rows: weights do not fit in shared memory");
-  p.stages = stages;
-  P->smem_bytes = fixed + stages * kABytes;
-  P->grid_x = p.n_img < sm_count() ? p.n_img : sm_count();
-  P->grid_y = 1;
-  P->tmem_cols = 512;
-  return MS_OK;
-}
-
-// Encode one bf16 TMA store map per output segment (see StoreMaps).  Called
-// once the output geometry is known; leaves tma_store = 0 for fp32 outputs.
 static int encode_store_maps(GemmPlan* P) {
   GemmParams& p = P->p;
   p.tma_store = 0;
@@ -1689,15 +1487,6 @@ static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D
 
 static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
   const GemmParams& p = P->p;
-  if (p.mode == MODE_CONV1_ROWS) {
-    static int c1_attr = 0;
-    if (!c1_attr) {
-      cudaFuncSetAttribute(conv1_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      c1_attr = 1;
-    }
-    launch_k(conv1_rows_kernel, dim3(P->grid_x), dim3(kThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p);
-    return check_launch("conv1_rows_kernel");
-  }
   if (p.mode == MODE_STEM_POOL) {
     static int stem_attr = 0;
     if (!stem_attr) {
@@ -1856,26 +1645,8 @@ int ms_gemm_plan_conv(void* plan, const void* X, int n_img, int H, int W_in, int
     cuuint64_t s5[3] = {(cuuint64_t)C * 2 * stride, (cuuint64_t)(wp * C * 2), (cuuint64_t)(wp * C * 2 * H)};
     cuuint32_t b5[4] = {(cuuint32_t)kBK, (cuuint32_t)bw, (cuuint32_t)(bh * stride), (cuuint32_t)bn};
     cuuint32_t e5[4] = {1, 1, (cuuint32_t)stride, 1};
-    // row-streaming kernel: selected with BN == 64 + bit 30 of `relu` (opt-in; measured
-    // on par with the window kernel at large batch, worse at small batch)
-    const bool rows_mode = OW <= kBM && Cout == 64 && BN == 64 && nseg <= 1 && (relu & (1 << 30));
-    relu &= ~(1 << 30);
-    p.relu = relu;
-    if (rows_mode) {  // row-streaming kernel: one box = all OW windows of one input row
-      b5[1] = (cuuint32_t)OW;
-      b5[2] = 1;
-      b5[3] = 1;
-      e5[2] = 1;
-      p.a_bytes = OW * 128;
-    }
     int rc = encode_map(&P->tmA, 4, X, d5, s5, b5, e5);
     if (rc) return rc;
-    if (rows_mode) {
-      p.mode = MODE_CONV1_ROWS;
-      p.H_in = H;
-      set_segments(p, 0, nullptr, D, ldd, col0);
-      return finish_conv1_rows(P, Wt, KH * p.smallc_halves);
-    }
   } else {
     cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(bw * stride), (cuuint32_t)(bh * stride), (cuuint32_t)bn};
     int rc = encode_map(&P->tmA, 4, X, dims, strides, box, es);
@@ -2013,7 +1784,7 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
   GemmParams& p = P->p;
   if (ksplit < 1) return set_error(MS_ERR_INVALID, "ksplit must be >= 1");
   if (ksplit > 1) {
-    if (p.mode == MODE_CONV_SMALLC || p.mode == MODE_CONV1_ROWS || p.pair || p.nseg > 1 || ws == nullptr ||
+    if (p.mode == MODE_CONV_SMALLC || p.pair || p.nseg > 1 || ws == nullptr ||
         ws_ld % 4 != 0 || ws_ld < p.N)
       return set_error(MS_ERR_INVALID,
                        "split-K needs a dense/gather/conv single-segment plan and ws[ksplit, M, ws_ld>=N, %4]");
@@ -2172,135 +1943,3 @@ int ms_gemm_plan_info(const void* plan, int* grid_x, int* grid_y, int* stages, i
 }
 
 }  // extern "C"
-
-// ------------------------------------------------------------------------
-// Debug probe (tools/umma_probe.py): does a K-major SW128 A descriptor whose
-// start address is shifted by `shift` 128-byte rows (with the descriptor's
-// base-offset field = shift & 7, and an explicit SBO) read rows
-// [shift, shift + 128) of a TMA-written tile?  This is the addressing a
-// halo-reusing 3x3 conv needs (taps = shifted windows of one smem tile).
-namespace mosel {
-__global__ void __launch_bounds__(128, 1) umma_shift_probe_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                                  const __grid_constant__ CUtensorMap tmB,
-                                                                  float* D, int shift, int sbo, int use_base) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = smem;                 // 256 rows x 128 B
-  uint8_t* sB = smem + 256 * 128;     // 64 rows x 128 B
-  __shared__ uint64_t bar, mbar;
-  __shared__ uint32_t tslot;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_init(&mbar, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(&tslot, 64);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tb = tslot;
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, 256 * 128 + 64 * 128);
-    tma_load_2d(smem_addr(sA), &tmA, &bar, 0, 0);
-    tma_load_2d(smem_addr(sA + 128 * 128), &tmA, &bar, 0, 128);
-    tma_load_2d(smem_addr(sB), &tmB, &bar, 0, 0);
-  }
-  mbar_wait(&bar, 0);
-  tc_fence_after();
-  if (threadIdx.x == 0) {
-    const uint32_t a_addr = smem_addr(sA) + (uint32_t)shift * 128u;
-    uint64_t adesc = 0;
-    adesc |= (uint64_t)((a_addr & 0x3FFFF) >> 4);
-    adesc |= (uint64_t)1 << 16;
-    adesc |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    adesc |= (uint64_t)1 << 46;
-    if (use_base) adesc |= (uint64_t)((a_addr >> 7) & 7) << 49;
-    adesc |= (uint64_t)2 << 61;
-    const uint64_t bdesc = umma_desc_sw128(smem_addr(sB));
-    const uint32_t idesc = umma_idesc_bf16_m128(64);
-    for (int k = 0; k < 4; ++k) umma_bf16(tb, adesc + 2 * k, bdesc + 2 * k, idesc, k != 0);
-    umma_commit(&mbar);
-  }
-  mbar_wait(&mbar, 0);
-  tc_fence_after();
-  for (int c = 0; c < 2; ++c) {
-    uint32_t v[32];
-    tmem_ld_32x32b_x32(tb + (uint32_t)(c * 32) + ((uint32_t)(warp * 32) << 16), v);
-    tmem_wait_ld();
-    for (int j = 0; j < 32; ++j) D[(warp * 32 + lane) * 64 + c * 32 + j] = __uint_as_float(v[j]);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tb, 64);
-}
-}  // namespace mosel
-
-extern "C" int ms_debug_umma_shift(const void* A /* [256, 64] bf16 */, const void* W /* [64, 64] bf16 */,
-                                   float* D /* [128, 64] */, int shift, int sbo, int use_base, void* stream) {
-  using namespace mosel;
-  CUtensorMap ta, tb;
-  cuuint64_t da[2] = {64, 256}, sa[1] = {128};
-  cuuint32_t ba[2] = {64, 128}, es[2] = {1, 1};
-  int rc = encode_map(&ta, 2, A, da, sa, ba, es);
-  if (rc) return rc;
-  cuuint64_t db[2] = {64, 64}, sb[1] = {128};
-  cuuint32_t bb[2] = {64, 64};
-  rc = encode_map(&tb, 2, W, db, sb, bb, es);
-  if (rc) return rc;
-  cudaFuncSetAttribute(umma_shift_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  umma_shift_probe_kernel<<<1, 128, 50 * 1024, reinterpret_cast<cudaStream_t>(stream)>>>(ta, tb, D, shift, sbo,
-                                                                                           use_base);
-  return check_launch("umma_shift_probe_kernel");
-}
-
-// ------------------------------------------------------------------------
-// Debug probe (tools/umma_rate.py): issue rate of back-to-back
-// tcgen05.mma (M=128, K=16) from one thread into one accumulator, for an A
-// descriptor of layout `mode` (0 = SW128 K-major, 1 = no-swizzle LBO 16 /
-// SBO 128, 2 = no-swizzle LBO 16 / SBO 112, 3 = no-swizzle LBO 128 / SBO 256
-// canonical) and width n.  Operands are uninitialised shared memory: only the
-// timing is meaningful.  cycles[0] = clocks from the first issue to the
-// commit's completion.
-namespace mosel {
-__global__ void __launch_bounds__(128, 1) umma_rate_kernel(int mode, int n, int count, long long* cycles) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t mbar;
-  __shared__ uint32_t tslot;
-  const int warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(&tslot, 256);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tb = tslot;
-  if (threadIdx.x == 0) {
-    const uint32_t a0 = smem_addr(smem), b0 = smem_addr(smem + 64 * 1024);
-    uint64_t ad;
-    if (mode == 0) ad = umma_desc_sw128(a0);
-    else if (mode == 1) ad = umma_desc_interleave(a0, 16, 128);
-    else if (mode == 2) ad = umma_desc_interleave(a0, 16, 112);
-    else ad = umma_desc_interleave(a0, 128, 256);
-    const uint64_t bd = umma_desc_sw128(b0);
-    const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)n);
-    const long long t0 = clock64();
-    for (int i = 0; i < count; ++i) umma_bf16(tb, ad + 2 * (i & 3), bd + 2 * (i & 3), idesc, i != 0);
-    umma_commit(&mbar);
-    mbar_wait(&mbar, 0);
-    cycles[0] = clock64() - t0;
-  }
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tb, 256);
-}
-}  // namespace mosel
-
-extern "C" int ms_debug_umma_rate(int mode, int n, int count, long long* cycles, void* stream) {
-  using namespace mosel;
-  cudaFuncSetAttribute(umma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-  umma_rate_kernel<<<1, 128, 150 * 1024, reinterpret_cast<cudaStream_t>(stream)>>>(mode, n, count, cycles);
-  return check_launch("umma_rate_kernel");
-}

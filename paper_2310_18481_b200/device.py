@@ -116,8 +116,6 @@ _SIGS = {
     "ms_gemm_plan_set_splitk": ([_P, _I, _P, _LL], C.c_int),
     "ms_gemm_plan_debug": ([_P, _I], C.c_int),
     "ms_gemm_plan_set_trace": ([_P, _P], C.c_int),
-    "ms_debug_umma_shift": ([_P, _P, _P, _I, _I, _I, _P], C.c_int),
-    "ms_debug_umma_rate": ([_I, _I, _I, _P, _P], C.c_int),
     "ms_gemm_plan_set_pair": ([_P, _I], C.c_int),
     "ms_layernorm": ([_P, _LL, _LL, _P, _P, _P, _LL, _I, C.c_float, _P], C.c_int),
     "ms_attention": ([_P, _LL, _I, _I, _I, _P, _LL, C.c_float, _P], C.c_int),

@@ -133,8 +133,9 @@ class MaskedModel:
         s = stream or self.torch.cuda.current_stream()
         with self.torch.cuda.stream(s):
             self.mask_d[:n].copy_(mask_h[:n], non_blocking=True)
-            self.slot_d.view(self.K, self.max_req)[:, :n].copy_(slot_h.view(self.K, self.max_req)[:, :n],
-                                                              non_blocking=True)
+            # the whole [K, max_req] block: one contiguous DMA (a strided [:, :n]
+            # slice made torch launch an elementwise copy kernel on every pass)
+            self.slot_d.copy_(slot_h, non_blocking=True)
             ev.record(s)
 
     # -- device pass ------------------------------------------------------
@@ -289,6 +290,15 @@ class MaskedModel:
         """Algorithmic FLOP of one pass: every present modality's encoder over
         its compacted count (real channels) + the fusion head over n."""
         return sum(e.flops(c) for e, c in zip(self.encoders, counts) if c) + self.head.flops(n)
+
+    def compaction_bytes_rw(self, masks):
+        """(bytes read, bytes written) of compaction_bytes: the rows read with
+        the masks and the index reads; the padded rows and index lists written."""
+        counts = self.counts_for(np.asarray(masks))
+        dst_lines = [r[0] + (r[0] // r[8]) * 2 * r[9] if r[8] and r[9] else r[0] for r in self.rows]
+        rd = sum(rb * c for rb, c in zip(self.row_bytes, counts)) + 2 * len(masks)
+        wr = sum(2 * dl * (r[1] + 2 * r[4]) * r[3] * c for r, dl, c in zip(self.rows, dst_lines, counts))
+        return rd, wr + 4 * sum(counts)
 
     def compaction_bytes(self, masks) -> int:
         """per present (request, modality) the row read (real

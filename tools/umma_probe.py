@@ -10,6 +10,7 @@ from paper_2310_18481_b200 import build  # noqa: E402
 
 build.build()
 from paper_2310_18481_b200 import device as dv  # noqa: E402
+import _probes  # noqa: E402
 
 g = torch.Generator().manual_seed(0)
 A = torch.randn(256, 64, generator=g).to(torch.bfloat16)
@@ -20,7 +21,7 @@ for sbo in (1024, 1280, 2048):
     for use_base in (0, 1):
         res = []
         for shift in (0, 1, 3, 7, 8, 10, 13):
-            dv.check(dv.lib().ms_debug_umma_shift(Ad.data_ptr(), Wd.data_ptr(), D.data_ptr(), shift, sbo, use_base,
+            dv.check(_probes.lib().ms_debug_umma_shift(Ad.data_ptr(), Wd.data_ptr(), D.data_ptr(), shift, sbo, use_base,
                                                   dv.stream_ptr()), "probe")
             torch.cuda.synchronize()
             # expected: row m reads A row  shift + (m // 8) * (sbo // 128) + m % 8

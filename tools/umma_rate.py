@@ -11,6 +11,7 @@ from paper_2310_18481_b200 import build  # noqa: E402
 
 build.build()
 from paper_2310_18481_b200 import device as dv  # noqa: E402
+import _probes  # noqa: E402
 
 cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
 names = {0: "SW128", 1: "interleave LBO16/SBO128", 2: "interleave LBO16/SBO112", 3: "interleave LBO128/SBO256"}
@@ -18,7 +19,7 @@ for mode in (0, 1, 2, 3):
     for n in (64, 128, 256):
         res = []
         for count in (64, 1024):
-            dv.check(dv.lib().ms_debug_umma_rate(mode, n, count, cyc.data_ptr(), dv.stream_ptr()), "rate")
+            dv.check(_probes.lib().ms_debug_umma_rate(mode, n, count, cyc.data_ptr(), dv.stream_ptr()), "rate")
             torch.cuda.synchronize()
             res.append(int(cyc.item()))
         per = (res[1] - res[0]) / (1024 - 64)
