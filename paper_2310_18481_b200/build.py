@@ -47,10 +47,10 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
     tmp = PKG / "build"
     tmp.mkdir(exist_ok=True)
-    for src in SOURCES:
+
+    def compile_one(src):  # one nvcc per translation unit, in parallel
         obj = tmp / (Path(src).stem + ".o")
         cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,7 +60,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             sys.stderr.write(r.stderr)
         (tmp / (Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     out = LIB.with_suffix(".so.tmp")
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            *objs, "-o", str(out)]

@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int img = ti.m / p.tiles_h;
         for (int cc = 0; cc < p.cchunks; ++cc) {
           mbar_wait(&aempty[hs], hphase ^ 1);
+          if (t == cta0 && cc == 0) GEMM_TRACE(3);
           if (PAIR) {
             if (leader) mbar_arrive_expect_tx(&afull[hs], 2 * p.a_bytes);
             tma_load_4d_pair(smem_addr(smA + hs * p.halo_slot), &tmA, &afull[hs], cc * kBK, -1, th * p.bh - 1, img);
@@ -504,6 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cc = 0; cc < p.cchunks; ++cc) {
         mbar_wait(&afull[hs], hphase);
         tc_fence_after();
+        if (lane == 0 && t == cta0 && cc == 0) GEMM_TRACE(4);
+        if (lane == 0 && t + ncta >= num_tiles && cc == p.cchunks - 1) GEMM_TRACE(5);
         const uint32_t halo = smem_addr(smA + hs * p.halo_slot);
         if (p.b_resident) {  // 9 taps straight from the resident weights
           if (lane == 0) {

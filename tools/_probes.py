@@ -6,7 +6,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 SRC = ROOT / "tools" / "probes.cu"
-LIB = ROOT / "tools" / "_probes.so"
+LIB = ROOT / "tools" / "libprobes.so"
 
 
 def lib():

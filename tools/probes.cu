@@ -134,7 +134,22 @@ __global__ void __launch_bounds__(128, 1) umma_rate_kernel(int mode, int n, int 
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_addr(smem), b0 = smem_addr(smem + 64 * 1024);
     uint64_t ad;
-    if (mode == 0) ad = umma_desc_sw128(a0);
+    // mode 4 + r: SW128 starting r 128-B rows into the tile (halo tap views);
+    // mode 20 / 21: the 9 tap shifts of a halo of pitch 16 / 32, rotating
+    const int pitch = mode == 20 ? 16 : 32;
+    uint64_t tap_desc[9];
+    for (int t = 0; t < 9; ++t) tap_desc[t] = umma_desc_sw128(a0 + (uint32_t)(((t / 3) * pitch + t % 3) * 128));
+    if (mode >= 20) {
+      const uint64_t bd = umma_desc_sw128(b0);
+      const uint32_t idesc = umma_idesc_bf16_m128((uint32_t)n);
+      const long long t0 = clock64();
+      for (int i = 0; i < count; ++i) umma_bf16(tb, tap_desc[(i >> 2) % 9] + 2 * (i & 3), bd + 2 * (i & 3), idesc, i != 0);
+      umma_commit(&mbar);
+      mbar_wait(&mbar, 0);
+      cycles[0] = clock64() - t0;
+    } else {
+    if (mode >= 4) ad = umma_desc_sw128(a0 + (uint32_t)(mode - 4) * 128u);
+    else if (mode == 0) ad = umma_desc_sw128(a0);
     else if (mode == 1) ad = umma_desc_interleave(a0, 16, 128);
     else if (mode == 2) ad = umma_desc_interleave(a0, 16, 112);
     else ad = umma_desc_interleave(a0, 128, 256);
@@ -145,6 +160,7 @@ __global__ void __launch_bounds__(128, 1) umma_rate_kernel(int mode, int n, int 
     umma_commit(&mbar);
     mbar_wait(&mbar, 0);
     cycles[0] = clock64() - t0;
+    }
   }
   __syncthreads();
   if (warp == 0) tmem_dealloc(tb, 256);
