@@ -346,7 +346,7 @@ def dominant_gemm_roofline(model, peak_tflops):
         traffic = None
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(ach / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
-            "kernel": f"gemm_tc_kernel {plan.label}", "flop_per_launch": fl,
+            "kernel": plan.label if "kernel" in plan.label else f"gemm_tc_kernel {plan.label}", "flop_per_launch": fl,
             "avg_launch_us": round(us, 2)}
 
 

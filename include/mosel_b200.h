@@ -244,6 +244,16 @@ int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in
 int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in, int KH, int pad, int planes,
                            long long plane_stride, const void* Wt, const float* bias, void* Y, long long ldy,
                            int y_col0);
+/* Fused 3x3 / stride-1 / pad-1 conv + bias + ReLU + 3x3 / stride-2 ceil-mode
+ * max pool (BN-Inception conv2 + pool2; reference consumer: the modality
+ * encoder whose latency profile.py:96-212 tabulates).  X [n_img, H, W, C]
+ * NHWC bf16 with 55 <= W <= 62 (halo rows of 64 pixels) and C >= 64 (pixel
+ * stride c_stride), Wt [Cout, 9 * ceil64(C)] tap-major (encoders
+ * .pack_conv_weight), Cout in {128, 192, 256}; Y = pooled [n_img, PH, PW]
+ * rows of ldy elements at y_col0.  Bitwise equal to the halo conv followed
+ * by ms_pool (same accumulation order); the unpooled map never reaches HBM. */
+int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
+                           const void* Wt, int Cout, const float* bias, void* Y, long long ldy, int y_col0);
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                         int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
                         int out_fp32, void* D, long long ldd, int col0);

@@ -17,8 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmosel_b200.so"
-SOURCES = ["select.cu", "gemm.cu", "ops.cu", "transformer.cu", "policy.cu", "strategy.cu"]
-HEADERS = ["ptx.cuh", "runtime.h"]
+SOURCES = ["select.cu", "gemm.cu", "convpool.cu", "ops.cu", "transformer.cu", "policy.cu", "strategy.cu"]
+HEADERS = ["ptx.cuh", "runtime.h", "gemm_plan.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -92,6 +92,7 @@ _SIGS = {
                                _I, _I, _P, _I, _I, _I], C.c_int),
     "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
     "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _I, _LL, _P, _P, _P, _LL, _I], C.c_int),
+    "ms_gemm_plan_conv_pool": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -434,6 +435,20 @@ def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0, plan
     ow = (W_in + 2 * pad - KH) // 2 + 1
     p.flops = 2 * n_img * oh * ow * 64 * KH * KH * 4 * planes
     p.label = f"stem conv {KH}x{KH}/2 {4 * planes}->64 {n_img}x{oh}x{ow} + maxpool"
+    return p
+
+
+def plan_conv_pool(X, n_img, H, W_in, C_in, c_stride, Wt, Cout, bias, Y, *, ldy, col0=0):
+    """Fused 3x3/1/1 conv + bias + ReLU + 3x3/2 ceil max pool
+    (``ms_gemm_plan_conv_pool``, widths 55..62): the pooled map is written to
+    ``Y`` ([n_img, PH, PW] rows of ``ldy``), the conv map never reaches HBM.
+    ``Wt`` from ``encoders.pack_conv_weight``."""
+    p = GemmPlan()
+    check(lib().ms_gemm_plan_conv_pool(p.addr, ptr(X), n_img, H, W_in, C_in, c_stride, ptr(Wt), Cout, ptr(bias),
+                                       ptr(Y), ldy, col0), "ms_gemm_plan_conv_pool")
+    p.keep = [X, Wt, bias, Y]
+    p.flops = 2 * n_img * H * W_in * Cout * 9 * C_in
+    p.label = f"conv_pool_kernel conv 3x3/1 {C_in}->{Cout} {n_img}x{H}x{W_in} + maxpool 3x3/2"
     return p
 
 

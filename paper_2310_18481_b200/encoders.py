@@ -391,6 +391,8 @@ class BNInceptionEncoder:
         self.weights_cpu = bninception_weights(modality.channels, modality.size, seed)
         # conv1 + pool1 as one kernel (MS_NO_FUSED_STEM=1: the conv + pool pair, for A/B)
         self.fused_stem = os.environ.get("MS_NO_FUSED_STEM") is None
+        # conv2 + pool2 as one kernel (MS_NO_FUSED_POOL2=1: the conv + pool pair, for A/B)
+        self.fused_pool2 = os.environ.get("MS_NO_FUSED_POOL2") is None
         self._pack()
         self._alloc()
         self._programs = {}
@@ -453,7 +455,8 @@ class BNInceptionEncoder:
         h2 = pool_out(h1, 3, 2, 0, True)
         self.a_p1 = buf(n_img * h2 * h2, 64)
         self.a_c2r = buf(n_img * h2 * h2, 64)
-        self.a_c2 = buf(n_img * h2 * h2, 192)
+        # the unpooled conv2 map exists only without the fused conv2 + pool2 kernel
+        self.a_c2 = None if (self.fused_pool2 and 55 <= h2 <= 62) else buf(n_img * h2 * h2, 192)
         self.blocks = {}
         # ping-pong block outputs + scratch sized for the largest block
         max_pix_c = 0
@@ -528,12 +531,18 @@ class BNInceptionEncoder:
         # conv2 (56x56 rgb/flow): halo reuse measured 1.08-1.09x faster than the
         # tap-box 2-SM kernel (tools/halo_bench.py); narrower layers lose more to
         # the ceil8(W+2)-wide tiles than they gain, audio's 64+2 does not tile 128
-        P.gemm(dv.plan_conv(self.a_c2r, n, h2, h2, 64, 64, 3, 3, 1, 1, self.w["conv2"], 192,
-                            self.b["conv2"], self.a_c2, ldd=192, BN=192, relu=True,
-                            tile=pick_conv_tile(n, h2, h2), halo=42 <= h2 <= 62))
         h = pool_out(h2, 3, 2, 0, True)
         cur = self.ping
-        P.pool(self.a_c2, n, h2, h2, 192, 192, 3, 2, 0, True, True, cur, 192, 0)
+        if self.fused_pool2 and 55 <= h2 <= 62:
+            # conv2 + ReLU + pool2 in one kernel (csrc/convpool.cu): the 56^2 x 192
+            # map never reaches HBM; bitwise equal to the pair below (1.43x, 183 frames)
+            P.gemm(dv.plan_conv_pool(self.a_c2r, n, h2, h2, 64, 64, self.w["conv2"], 192, self.b["conv2"],
+                                     cur, ldy=192))
+        else:
+            P.gemm(dv.plan_conv(self.a_c2r, n, h2, h2, 64, 64, 3, 3, 1, 1, self.w["conv2"], 192,
+                                self.b["conv2"], self.a_c2, ldd=192, BN=192, relu=True,
+                                tile=pick_conv_tile(n, h2, h2), halo=42 <= h2 <= 62))
+            P.pool(self.a_c2, n, h2, h2, 192, 192, 3, 2, 0, True, True, cur, 192, 0)
         c = 192
         nxt = self.pong
         for L in self.layers:

@@ -831,3 +831,42 @@ def test_fused_compaction_multi_modality_slots_vs_torch(dev):
     full[..., :10] = exp2
     for q in range(3):
         assert torch.equal(G2[q, :c2 * fr * fh, pad:pad + w], full[..., 4 * q:4 * q + 4])
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout", [(3, 56, 64, 192), (2, 55, 64, 128), (1, 62, 128, 256), (5, 56, 64, 192)])
+def test_conv_pool_fused_vs_torch_and_unfused(dev, n, H, Cin, Cout):
+    """ms_gemm_plan_conv_pool (conv2 + pool2 in one kernel): equal to torch
+    fp32 maxpool(relu(conv)) within the bf16 tolerance, and BITWISE equal to
+    the unfused halo conv + ms_pool pair (same accumulation order); the
+    pooled rows land in a channel slice of a wider tensor, nothing else is
+    touched.  H = 55 (odd) and 62 (ceil-mode last window 2 wide)."""
+    g = torch.Generator().manual_seed(n * H + Cin + 41)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, 3, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    PH = (H - 3 + 1) // 2 + 1
+    ldy, col0 = Cout + 32, 16
+    Y = torch.full((n * PH * PH, ldy), 5.0, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv_pool(X, n, H, H, Cin, Cin, packed.cuda(), Cout, b.cuda(), Y, ldy=ldy, col0=col0)
+    p.run()
+    p.run()
+    # unfused: halo conv -> full map, then the 3x3/2 ceil max pool
+    D = torch.empty(n * H * H, Cout, dtype=torch.bfloat16, device="cuda")
+    q = dev.plan_conv(X, n, H, H, Cin, Cin, 3, 3, 1, 1, packed.cuda(), Cout, b.cuda(), D, ldd=Cout,
+                      BN=Cout, relu=True, halo=True)
+    q.run()
+    Y2 = torch.empty(n * PH * PH, Cout, dtype=torch.bfloat16, device="cuda")
+    P = dev.Program()
+    P.pool(D, n, H, H, Cout, Cout, 3, 2, 0, True, True, Y2, Cout, 0)
+    P.seal()
+    P.run()
+    torch.cuda.synchronize()
+    got = Y[:, col0:col0 + Cout]
+    assert torch.equal(got, Y2), (got.float() - Y2.float()).abs().max().item()
+    assert torch.all(Y[:, :col0] == 5.0) and torch.all(Y[:, col0 + Cout:] == 5.0)
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=1, padding=1).clamp_min(0)
+    ref = torch.nn.functional.max_pool2d(ref, 3, 2, 0, ceil_mode=True)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(got.cpu(), ref)
+    assert ok, (err, scale)

@@ -15,6 +15,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=183)
 ap.add_argument("--inner", type=int, default=10)
+ap.add_argument("--only", default="")
 a = ap.parse_args()
 import torch  # noqa: E402
 
@@ -49,11 +50,13 @@ def timed(fn, inner=a.inner):
     return float(np.median(ts))
 
 
-SHAPES = [(28, 64, 64), (28, 64, 96), (28, 96, 96), (14, 64, 96), (14, 96, 128), (14, 128, 128),
+SHAPES = [(56, 64, 192), (28, 64, 64), (28, 64, 96), (28, 96, 96), (14, 64, 96), (14, 96, 128), (14, 128, 128),
           (14, 128, 160), (14, 160, 160), (14, 128, 192), (14, 160, 192), (14, 192, 192), (14, 192, 256)]
 n = a.n
 torch.manual_seed(0)
 for H, cin, cout in SHAPES:
+    if a.only and f"{H}:{cin}:{cout}" not in a.only.split(","):
+        continue
     X = torch.randn(n, H, H, cin, device="cuda").to(torch.bfloat16)
     w = torch.randn(cout, cin, 3, 3) * (2.0 / (9 * cin)) ** 0.5
     b = torch.randn(cout, device="cuda") * 0.1
