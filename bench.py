@@ -23,8 +23,9 @@ Our arm, per rank (replicas only; no data-path collective):
      pinned memory and logits D2H inside the timed region;
   6. roofline: the dominant encoder GEMM launch timed alone with CUDA
      events (FLOP / time vs measured bf16 peak); compaction gather vs HBM;
-  7. cpu_baseline (rank 0): the CPU oracle (reference path restated) on a
-     bounded sample, all host threads.
+  7. cpu_baseline (rank 0): the reference path on the host cores serving the
+     same jobs under the same deadlines -- the CPU oracle's measured latency
+     table driving the reference simulator loop (bounded, all host threads).
 """
 
 from __future__ import annotations
@@ -147,75 +148,112 @@ def _allreduce(pg, vals, op="max"):
 # ------------------------------------------------------------- reference arm
 
 
-def cpu_reference_step(orc, rng, n_req, pools_cpu, matrix, profile):
-    """One bounded CPU step of the reference path: selection (oracle P5 on
-    each job's frontier) + the CPU forward for the chosen masks."""
+def cpu_profile(orc, pools, max_batch, reps=1):
+    """The CPU oracle's own latency table (profile.py's latency_us[mask-1]
+    [batch-1]): every modality subset timed at batches 1 and 2 on the host
+    cores (median of ``reps``), larger batches extrapolated linearly."""
     import torch
-    from oracle import selection
-    from paper_2310_18481_b200.executor import request_masks
-    from paper_2310_18481_b200.policy import candidates_with_rounding
-    slo = round(float(rng.uniform(profile.min_accuracy, profile.max_accuracy)), 4)
-    cands = candidates_with_rounding(matrix, n_req, slo)
-    lat = [c.latency_us for c in cands]
-    budget = int(rng.integers(lat[0], 2 * lat[-1] + 1))
-    choice = selection.policy_select_one(lat, budget, 0, 1.0)
-    if choice < 0:
-        choice = 0
-    masks = request_masks(cands[choice].strategy.parts, n_req)
-    slots = rng.integers(0, pools_cpu[0].shape[0], size=n_req)
-    clips = [p[torch.as_tensor(slots)].float() for p in pools_cpu]
-    return orc.logits(clips, torch.as_tensor(masks.astype(np.int64))), masks
+    from paper_2310_18481_b200.profiler import TBN_ACCURACY
+    from paper_2310_18481_b200.registry import ModelProfile
+    lat = []
+    for mask in range(1, 8):
+        t = []
+        for b in (1, 2):
+            clips = [p[:b].float() for p in pools]
+            m = torch.full((b,), mask, dtype=torch.int64)
+            orc.logits(clips, m)  # warm
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                orc.logits(clips, m)
+                ts.append(time.perf_counter() - t0)
+            t.append(float(np.median(ts)) * 1e6)
+        l1, l2 = t[0], max(t)
+        lat.append(tuple(int(round(l1 + (b - 1) * (l2 - l1))) for b in range(1, max_batch + 1)))
+    return ModelProfile("tbn-cpu-oracle", ("rgb", "flow", "audio"), max_batch, tuple(lat), TBN_ACCURACY)
 
 
-def cpu_baseline_arm(steps, warmup, n_req=2, seconds_cap=30.0):
-    """The oracle (reference path restated) on the host cores."""
+def cpu_baseline_arm(deadline_ms=15.0, max_job=24, seeds=3, seconds=20, cap_s=120.0):
+    """The reference path on the host cores, serving the SAME jobs under the
+    SAME deadlines as the GPU arm: the CPU oracle's measured latency table
+    (cpu_profile) drives the reference's own simulator loop (sim.py:241-397,
+    OPTIMIZED policy, its default 70 ms optimizer overhead) over the bench's
+    Poisson job stream (sizes round(max(1, N(1,6))) capped at max_job,
+    uniform accuracy SLOs, fixed deadline); the value is the highest offered
+    rate whose violation ratio, pooled over ``seeds`` arrival draws, stays
+    <= 1 % -- 0 when even one request at a time misses the deadline.
+    ``throughput_without_deadlines`` = requests/s the oracle computes back to
+    back at its best batch (context, not the metric)."""
     import torch
     from oracle.forward import OracleTBN
     from paper_2310_18481_b200.encoders import SEGMENTS, TBN_MODALITIES
     from paper_2310_18481_b200.planner import build_matrix, recommended_alphas
-    from paper_2310_18481_b200.profiler import TBN_ACCURACY
-    from paper_2310_18481_b200.registry import ModelProfile
+    from paper_2310_18481_b200.policy import Policy
+    from paper_2310_18481_b200.serving import JobTemplate, SimConfig, run
+    t_start = time.perf_counter()
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
     g = torch.Generator().manual_seed(0)
-    pools = [torch.randn(4, SEGMENTS, m.size, m.size, m.channels, generator=g).to(torch.bfloat16)
+    pools = [torch.randn(2, SEGMENTS, m.size, m.size, m.channels, generator=g).to(torch.bfloat16)
              for m in TBN_MODALITIES]
     orc = OracleTBN(TBN_MODALITIES, (101, 102, 103), 199, SEGMENTS)
-    # a synthetic table with the device profile's shape (accuracies fixed)
-    lat = tuple(tuple(1000 * (m.bit_count()) * b for b in range(1, 9)) for m in range(1, 8))
-    prof = ModelProfile("tbn-cpu", ("rgb", "flow", "audio"), 8, lat, TBN_ACCURACY)
-    matrix = build_matrix(prof, range(1, 9), recommended_alphas(prof))
-    rng = np.random.default_rng(0)
-    for _ in range(warmup):
-        cpu_reference_step(orc, rng, n_req, pools, matrix, prof)
-    t0 = time.perf_counter()
-    done = 0
-    n_steps = 0
-    for _ in range(steps):
-        cpu_reference_step(orc, rng, n_req, pools, matrix, prof)
-        done += n_req
-        n_steps += 1
-        if time.perf_counter() - t0 > seconds_cap:
+    prof = cpu_profile(orc, pools, max_batch=8)
+    matrix = build_matrix(prof, range(1, max_job + 1), recommended_alphas(prof))
+    trials = []
+
+    def violation(q):
+        viol = tot = 0
+        for sd in range(seeds):
+            jobs = make_jobs(prof, q, seconds, deadline_ms, 4000 + sd)
+            jobs = [JobTemplate(j.arrival_us, min(j.size, max_job), j.accuracy_slo, j.deadline_us) for j in jobs]
+            log = run(SimConfig(prof, matrix, Policy.OPTIMIZED, seed=sd), jobs)
+            viol += log.violated_requests
+            tot += log.total_requests
+        v = viol / max(1, tot)
+        trials.append((round(q, 3), round(v, 4)))
+        return v
+
+    lo, hi, q = 0.0, None, 1.0
+    while time.perf_counter() - t_start < cap_s and len(trials) < 24:
+        if violation(q) <= 0.01:
+            lo = q
+            q = q * 2 if hi is None else (lo + hi) / 2
+        else:
+            hi = q
+            if lo == 0.0 and q <= 1.0 / 64:
+                break  # not even a trickle of single requests meets the deadline
+            q = (lo + hi) / 2 if lo > 0 else q / 4
+        if hi is not None and lo > 0 and hi - lo <= 0.04 * hi:
             break
-    dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n_steps} steps x {n_req} TBN requests (selection + 3-segment BN-Inception "
-                      f"forward for the chosen masks + fusion), torch fp32 on {cores} threads",
-            "seconds": dt, "steps": n_steps}
+    full = prof.all_modalities_mask
+    fastest_ms = min(prof.part_latency_us(m, 1) for m in range(1, 8)) / 1000.0
+    best = max(b / (prof.part_latency_us(full, b) / 1e6) for b in range(1, prof.max_batch + 1))
+    return {"value": round(lo, 3), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"same jobs and deadlines as the GPU arm ({deadline_ms:g} ms, sizes capped at {max_job}, "
+                       f"{seeds} Poisson seeds x {seconds} s per rate) served by the reference simulator loop with "
+                       f"the CPU oracle's measured latency table (torch fp32, {cores} threads; batch 1/2 timed, "
+                       f"larger batches extrapolated)"),
+            "fastest_candidate_ms": round(fastest_ms, 2),
+            "all_modality_request_ms": round(prof.part_latency_us(full, 1) / 1000.0, 2),
+            "throughput_without_deadlines": round(best, 2), "trials": trials,
+            "seconds": time.perf_counter() - t_start, "steps": len(trials)}
 
 
 def reference_arm(args):
     world, rank, _ = _dist()
     if rank != 0:
         return
-    cb = cpu_baseline_arm(args.steps, args.warmup, n_req=2, seconds_cap=240.0)
+    cb = cpu_baseline_arm(deadline_ms=args.deadline_ms, max_job=args.max_job)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": cb["steps"], "warmup": args.warmup,
             "ms_per_step": 1000.0 * cb["seconds"] / max(1, cb["steps"]), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": "configs[1] TBN BN-Inception rgb/flow/audio, EPIC-shaped clips",
-                       "path": "oracle port of the reference hot path on host cores"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": "configs[1] TBN BN-Inception rgb/flow/audio, EPIC-shaped clips, fixed per-request "
+                                   "deadline", "deadline_ms": args.deadline_ms,
+                       "path": "oracle port of the reference hot path on host cores: the reference simulator "
+                               "loop serving the bench's job stream with the CPU forward's measured latencies"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "fastest_candidate_ms",
+                                                "all_modality_request_ms", "throughput_without_deadlines")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -247,6 +285,7 @@ def make_jobs(profile, qps, seconds, deadline_ms, seed, rank=0, world=1, arrival
 
 
 # serving-loop options (set from the command line in main())
+SEEDS_PER_RATE = 3  # arrival draws per offered rate in the rate search
 SERVE_OPTS = {"sched_margin_us": 0, "policy_grid_us": 1000, "selection": "pass", "pass_frac": 0.2,
               "arrivals": "poisson", "mults": None, "top_only": False}
 
@@ -286,20 +325,25 @@ def find_rate(model, profile, matrix, deadline_ms, seconds, hi_guess, max_size, 
     q = hi_guess
     trials = []
     for it in range(14):
-        lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 1000 + it, max_size=max_size,
-                       cost=cost)
-        v = lg.violation_ratio()
-        trials.append((q, v))
-        log(f"  rate {q:9.1f} req/s -> violation {v:.4f} util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f} "
+        # >= 3 arrival draws per offered rate, violation pooled over
+        # the draws; a rate already far over the limit on its first draw stops there
+        viol = tot = 0
+        per_seed = []
+        for sd in range(SEEDS_PER_RATE):
+            lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 1000 * (sd + 1) + it, max_size=max_size,
+                           cost=cost)
+            viol += lg.violated_requests
+            tot += lg.total_requests
+            per_seed.append(round(lg.violation_ratio(), 4))
+            if sd == 0 and lg.violation_ratio() > 0.03:
+                break
+        v = viol / max(1, tot)
+        trials.append((q, round(v, 4), per_seed))
+        log(f"  rate {q:9.1f} req/s -> violation {v:.4f} (draws {per_seed}) util {st.busy_us / 1e6 / max(st.wall_s, 1e-9):.2f} "
             f"req/pass {st.requests / max(1, st.passes):.1f} late {st.late} drop(policy/dispatch/admit) "
             f"{st.dropped_policy}/{st.dropped_dispatch}/{st.dropped_admit} policy host {st.policy_host_us / max(1, st.policy_runs):.0f}us "
             f"x{st.policy_runs}, device pass_select {st.policy_device_us / max(1, st.policy_launches):.1f}us "
             f"(kernel {st.policy_kernel_us / max(1, st.policy_launches):.1f}us) x{st.policy_launches}")
-        if 0.005 < v <= 0.01:  # near the limit one Poisson burst decides a short window: confirm on a re-draw
-            lg, st = serve(model, profile, matrix, q, seconds, deadline_ms, 2000 + it, max_size=max_size,
-                           cost=cost)
-            v = max(v, lg.violation_ratio())
-            log(f"  rate {q:9.1f} req/s -> re-drawn arrivals: violation {lg.violation_ratio():.4f}")
         if v <= 0.01:
             lo = q
             q = q * 2 if hi is None else (lo + hi) / 2
@@ -543,7 +587,7 @@ def our_arm(args):
                     "slo_attainment": round(agg3[0] / max(1, agg3[1]), 5), "slo_met": bool(agg3[0] >= 0.99 * agg3[1]),
                     "latency_ms": {"p50": None if pct3[50] is None else round(pct3[50] / 1000, 3),
                                    "p99": None if pct3[99] is None else round(pct3[99] / 1000, 3)},
-                    "search": [(round(q, 1), round(v, 4)) for q, v in b_trials]}
+                    "search": [(round(q, 1), v, d) for q, v, d in b_trials]}
         log(f"[bench] no-selection baseline {baseline['value']:.1f} req/s -> selection gain "
             f"{value / max(1e-9, baseline['value']):.2f}x")
 
@@ -579,8 +623,9 @@ def our_arm(args):
                            sum(r.size for r in served), 4)
     cpu = None
     if rank == 0 and not args.no_cpu and args.workload == "tbn":
-        cpu = cpu_baseline_arm(steps=args.cpu_steps, warmup=1, n_req=2, seconds_cap=25.0)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = cpu_baseline_arm(deadline_ms=deadline_ms, max_job=args.max_job, cap_s=60.0)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "fastest_candidate_ms",
+                                   "all_modality_request_ms", "throughput_without_deadlines", "trials")}
 
     if rank != 0:
         return
@@ -636,7 +681,7 @@ def our_arm(args):
                 "slo_attainment": round(agg2[0] / max(1, agg2[1]), 5),
                 "slo_met": bool(agg2[0] >= 0.99 * agg2[1])},
         "clocks": clk, "cpu_baseline": cpu,
-        "search": [(round(q, 1), round(v, 4)) for q, v in trials],
+        "search": [(round(q, 1), v, d) for q, v, d in trials], "seeds_per_rate": SEEDS_PER_RATE,
         "profile_us": {prof.combo_label(m): [prof.part_latency_us(m, 1),
                                              prof.part_latency_us(m, args.profile_batch)]
                        for m in range(1, full + 1)},
@@ -653,7 +698,7 @@ def main():
     ap.add_argument("--workload", default="tbn", choices=["tbn", "vqa", "mlp"],
                     help="tbn = configs[1] (the headline); vqa = configs[2]; mlp = configs[0]")
     ap.add_argument("--window-s", type=float, default=1.0)
-    ap.add_argument("--search-seconds", type=float, default=3.0)
+    ap.add_argument("--search-seconds", type=float, default=2.0, help="window per arrival draw in the rate search")
     ap.add_argument("--deadline-ms", type=float, default=15.0,
                     help="fixed per-request latency budget (deadline - arrival)")
     ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")
@@ -679,7 +724,6 @@ def main():
                     help="profiler -> matrix refresh period during serving (0: off)")
     ap.add_argument("--slots", type=int, default=192)
     ap.add_argument("--profile-batch", type=int, default=8)
-    ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     SERVE_OPTS.update(sched_margin_us=int(args.sched_margin_ms * 1000), policy_grid_us=int(args.policy_grid_us),

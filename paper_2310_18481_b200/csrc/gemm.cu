@@ -1686,7 +1686,8 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   if (p.mode == MODE_CONV_HALO) {
     const int room = 226 * 1024 - 1024 - 288 - 2 * p.halo_slot - p.stage_bytes - bias_bytes;
     // half of the weights per CTA: layers whose full tile did not fit can now stay resident
-    p.b_resident = (n_tiles == 1 && 9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
+    // (with several N tiles the grid is a multiple of n_tiles, so each pair keeps one N tile)
+    p.b_resident = (9 * p.cchunks * p.b_bytes <= room) ? 1 : 0;
     int stages = p.b_resident ? 9 * p.cchunks : room / p.b_bytes;
     if (!p.b_resident && stages > kMaxHaloStages) stages = kMaxHaloStages;
     if (stages < 2) return set_error(MS_ERR_INVALID, "halo pair: weights tile does not fit");

@@ -439,6 +439,16 @@ class BNInceptionEncoder:
             self.w[n + "/merged"] = torch.cat([self.w[p] for p in parts], 0).contiguous()
             self.b[n + "/merged"] = torch.cat(biases, 0).contiguous()
 
+    def _w64(self, name):
+        """3x3 weights with each tap's channels padded to 64 (the halo layout),
+        for layers whose default packing is MODE_CONV_K32's."""
+        if not hasattr(self, "_w64_cache"):
+            self._w64_cache = {}
+        if name not in self._w64_cache:
+            w, _ = self.weights_cpu[name]
+            self._w64_cache[name] = pack_conv_weight(w).to(self.dev)
+        return self._w64_cache[name]
+
     # -- activation buffers at capacity
     def _alloc(self):
         import torch
@@ -600,19 +610,38 @@ class BNInceptionEncoder:
 
         def k32(cin_):  # matches the weight packing in _pack
             return cin_ % 64 != 0 and cin_ % 32 == 0
+
+        def conv3(X_, cin_, cout_, stride_, wname, D_, ldd_, col0_, tile_):
+            """3x3 conv plan: halo (+ CTA pair) where measured faster, else tap-box / K32."""
+            if halo_ok(cin_, cout_, stride_):
+                return dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, 1, 1, self.w[wname], cout_, self.b[wname], D_,
+                                    ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, halo=True)
+            if halo_pair_ok(cin_, stride_):
+                p_ = dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, 1, 1, self._w64(wname), cout_, self.b[wname], D_,
+                                  ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, halo=True)
+                return p_.set_pair(True)
+            return dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, stride_, 1, self.w[wname], cout_, self.b[wname], D_,
+                                ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, tile=tile_, k32=k32(cin_))
+
+        def halo_pair_ok(cin_, stride_):
+            """Halo tiles on CTA pairs with half of the (64-padded) weights
+            resident per SM: at 28x28 96->96 1.26x the K32 tap-box kernel
+            (tools/conv_variants.py, profiles/r02_conv_variants.txt); at 14x14
+            the tap-box kernels win for every served shape (A/B: MS_HALO14_PAIR)."""
+            if stride_ != 1 or 128 % (-(-(h + 2) // 8) * 8) != 0:
+                return False
+            if 14 < h <= 30:
+                return cin_ == 96 and os.environ.get("MS_NO_HALO28_PAIR") is None
+            if h == 14:
+                return os.environ.get("MS_HALO14_PAIR") is not None
+            return False
         # 3x3 branch (stride s) -> Y[:, c1 : c1+c3]
         B3 = dv.Program()
-        B3.gemm(dv.plan_conv(T3, n, h, h, c3r, c3r, 3, 3, s, 1, self.w[name + "/3x3"], c3,
-                             self.b[name + "/3x3"], Yv, ldd=cout, col0=c1, BN=pick_bn(c3), relu=True,
-                             tile=tile_out, halo=halo_ok(c3r, c3, s), k32=k32(c3r)))
+        B3.gemm(conv3(T3, c3r, c3, s, name + "/3x3", Yv, cout, c1, tile_out))
         # double 3x3: stride 1 then stride s -> Y[:, c1+c3 : c1+c3+cd]
         BD = dv.Program()
-        BD.gemm(dv.plan_conv(Td, n, h, h, cdr, cdr, 3, 3, 1, 1, self.w[name + "/d3x3_a"], cd,
-                             self.b[name + "/d3x3_a"], Td2, ldd=cd, BN=pick_bn(cd), relu=True,
-                             tile=tile_in, halo=halo_ok(cdr, cd, 1), k32=k32(cdr)))
-        BD.gemm(dv.plan_conv(Td2, n, h, h, cd, cd, 3, 3, s, 1, self.w[name + "/d3x3_b"], cd,
-                             self.b[name + "/d3x3_b"], Yv, ldd=cout, col0=c1 + c3, BN=pick_bn(cd),
-                             relu=True, tile=tile_out, k32=k32(cd)))
+        BD.gemm(conv3(Td, cdr, cd, 1, name + "/d3x3_a", Td2, cd, 0, tile_in))
+        BD.gemm(conv3(Td2, cd, cd, s, name + "/d3x3_b", Yv, cout, c1 + c3, tile_out))
         pc = c1 + c3 + cd
         BP = dv.Program()
         if fold_pool:  # avgpool of the projected (pre-bias) branch + bias + ReLU

@@ -870,3 +870,26 @@ def test_conv_pool_fused_vs_torch_and_unfused(dev, n, H, Cin, Cout):
     ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
     ok, err, scale = _close(got.cpu(), ref)
     assert ok, (err, scale)
+
+
+@pytest.mark.parametrize("n,H,Cin,Cout", [(3, 28, 96, 96), (2, 14, 128, 128), (1, 56, 64, 192), (3, 28, 64, 96)])
+def test_conv_halo_pair_vs_torch(dev, n, H, Cin, Cout):
+    """Halo conv on CTA pairs (cta_group::2, M = 256; half of the weights per
+    SM, resident when they fit -- the encoders' 28x28 96->96 layers), into a
+    channel slice; odd image counts leave the last pair's peer without rows."""
+    g = torch.Generator().manual_seed(n * H + Cin + 53)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w, packed = _conv_weights(Cout, Cin, 3, g)
+    b = torch.randn(Cout, generator=g) * 0.1
+    X = x.permute(0, 2, 3, 1).contiguous().cuda()
+    ldd, col0 = Cout + 32, 16
+    D = torch.full((n * H * H, ldd), 3.0, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_conv(X, n, H, H, Cin, Cin, 3, 3, 1, 1, packed.cuda(), Cout, b.cuda(), D, ldd=ldd, col0=col0,
+                      BN=Cout, relu=True, halo=True).set_pair(True)
+    p.run()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=1, padding=1).clamp_min(0)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, Cout)
+    ok, err, scale = _close(D[:, col0:col0 + Cout].cpu(), ref)
+    assert ok, (err, scale)
+    assert torch.all(D[:, :col0] == 3.0) and torch.all(D[:, col0 + Cout:] == 3.0)

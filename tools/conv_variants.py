@@ -73,10 +73,16 @@ for H, cin, cout in SHAPES:
     ref = D0.clone()
     fl = p0.flops
     line = f"{H:2d}x{H} {cin:3d}->{cout:3d} {'k32' if k32 else 'tap'} {t0:6.1f} us {fl / t0 / 1e6:5.0f} TF/s"
-    for name, pair in (("halo", False), ("halo-pair", True)):
+    cc = -(-cin // 64)
+    bns = -(-cout // 32) * 32
+    while bns > 32 and 9 * cc * (bns // 2) * 128 > 150 * 1024:  # half of the weights resident per CTA
+        bns -= 32
+    for name, pair, bn_ in (("halo", False, BN), ("halo-pair", True, BN), (f"halo-pair BN{bns}", True, bns)):
+        if name.startswith("halo-pair BN") and bns == BN:
+            continue
         D1 = torch.empty_like(D0)
         try:
-            p1 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, W64, cout, b, D1, ldd=cout, BN=BN, halo=True)
+            p1 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, W64, cout, b, D1, ldd=cout, BN=bn_, halo=True)
             if pair:
                 p1.set_pair(True)
         except Exception as ex:  # noqa: BLE001
