@@ -383,7 +383,9 @@ def dominant_gemm_roofline(model, peak_tflops):
     ach = fl / (us * 1e-6) / 1e12
     traffic = None
     try:  # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text()).get(plan.label)
+        t = None
+        for f in ("r02_traffic.json", "r01_traffic.json"):
+            t = t or json.loads((ROOT / "profiles" / f).read_text()).get(plan.label)
         if t:
             traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
     except Exception:
