@@ -247,7 +247,8 @@ int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in
 /* Fused 3x3 / stride-1 / pad-1 conv + bias + ReLU + 3x3 / stride-2 ceil-mode
  * max pool (BN-Inception conv2 + pool2; reference consumer: the modality
  * encoder whose latency profile.py:96-212 tabulates).  X [n_img, H, W, C]
- * NHWC bf16 with 55 <= W <= 62 (halo rows of 64 pixels) and C >= 64 (pixel
+ * NHWC bf16 with 55 <= W <= 62 (halo rows of 64 pixels) or W == 64 (one
+ * tap box per (chunk, tap)), and C >= 64 (pixel
  * stride c_stride), Wt [Cout, 9 * ceil64(C)] tap-major (encoders
  * .pack_conv_weight), Cout in {128, 192, 256}; Y = pooled [n_img, PH, PW]
  * rows of ldy elements at y_col0.  Bitwise equal to the halo conv followed

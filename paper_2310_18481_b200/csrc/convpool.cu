@@ -71,8 +71,12 @@ struct PoolWalk {  // conv rows: OPEN -> {2i} (tile rows 2i-1, 2i); CLOSE -> {2i
   __device__ __forceinline__ bool second_row() const { return open || 2 * i + 2 < OH; }
 };
 
-// CPG: 32-channel chunks per epilogue group (N = 64 * CPG output channels)
-template <int CPG>
+// CPG: 32-channel chunks per epilogue group (N = 64 * CPG output channels).
+// kHalo: halo tiles (W 55..62, pitch 64); else (W == 64) tap boxes: per
+// (chunk, tap) one {64 ch, 64 px, 2 rows} TMA box at the tap-shifted
+// coordinate beside the weights in each pipeline stage (OOB zero fill = the
+// padding) -- the same M-row mapping y * 64 + x, every column real.
+template <int CPG, bool kHalo>
 __global__ void __launch_bounds__(kCPThreads, 1)
     conv_pool_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmParams p) {
@@ -81,8 +85,8 @@ __global__ void __launch_bounds__(kCPThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
-  uint8_t* smA = smem;                                   // 2 halo slots
-  uint8_t* smB = smA + 2 * p.halo_slot;                  // weight ring
+  uint8_t* smA = smem;                                   // 2 halo slots | tap-box A ring
+  uint8_t* smB = smA + (kHalo ? 2 * p.halo_slot : stages * kABytes);  // weight ring
   uint8_t* xbuf = smB + stages * p.b_bytes;              // [2 groups][64 px][kXRow]
   uint32_t* bnd = reinterpret_cast<uint32_t*>(xbuf + 2 * 64 * kXRow);  // [2 groups][CPG * 16]
   uint64_t* full = reinterpret_cast<uint64_t*>(bnd + 2 * CPG * 16);
@@ -129,7 +133,22 @@ __global__ void __launch_bounds__(kCPThreads, 1)
     if (lane == 0) {  // ----------------------------------------- TMA producer
       int s = 0, hs = 0;
       uint32_t phase = 0, hphase = 0;
-      for (; w.valid(); w.next()) {
+      for (; w.valid() && !kHalo; w.next()) {
+        for (int cc = 0; cc < p.cchunks; ++cc) {
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap - 3 * (tap / 3);
+            mbar_wait(&empty[s], phase ^ 1);
+            mbar_arrive_expect_tx(&full[s], kABytes + p.b_bytes);
+            tma_load_4d(smem_addr(smA + s * kABytes), &tmA, &full[s], cc * kBK, dx - 1, w.tile_row0() + dy - 1, w.img);
+            tma_load_2d(smem_addr(smB + s * p.b_bytes), &tmB, &full[s], (tap * p.cchunks + cc) * kBK, 0);
+            if (++s == stages) {
+              s = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+      for (; w.valid() && kHalo; w.next()) {
         for (int cc = 0; cc < p.cchunks; ++cc) {
           mbar_wait(&aempty[hs], hphase ^ 1);
           mbar_arrive_expect_tx(&afull[hs], p.a_bytes);
@@ -160,22 +179,25 @@ __global__ void __launch_bounds__(kCPThreads, 1)
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(slot * 256);
       for (int cc = 0; cc < p.cchunks; ++cc) {
-        mbar_wait(&afull[hs], hphase);
-        tc_fence_after();
+        if (kHalo) {
+          mbar_wait(&afull[hs], hphase);
+          tc_fence_after();
+        }
         const uint32_t halo = smem_addr(smA + hs * p.halo_slot);
         for (int tap = 0; tap < 9; ++tap) {
           mbar_wait(&full[s], phase);
           tc_fence_after();
           if (lane == 0) {
             const int dy = tap / 3, dx = tap - 3 * (tap / 3);
-            const uint64_t adesc = umma_desc_sw128(halo + (uint32_t)((dy * kCPPitch + dx) * 128));
+            const uint64_t adesc = kHalo ? umma_desc_sw128(halo + (uint32_t)((dy * kCPPitch + dx) * 128))
+                                         : umma_desc_sw128(smem_addr(smA + s * kABytes));
             const uint64_t bdesc = umma_desc_sw128(smem_addr(smB + s * p.b_bytes));
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
               umma_bf16(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (cc | tap | kk) != 0);
             umma_commit(&empty[s]);
             if (tap == 8) {
-              umma_commit(&aempty[hs]);
+              if (kHalo) umma_commit(&aempty[hs]);
               if (cc == p.cchunks - 1) umma_commit(&tfull[slot]);
             }
           }
@@ -185,7 +207,7 @@ __global__ void __launch_bounds__(kCPThreads, 1)
             phase ^= 1;
           }
         }
-        if (++hs == 2) {
+        if (kHalo && ++hs == 2) {
           hs = 0;
           hphase ^= 1;
         }
@@ -338,18 +360,18 @@ int smem_fixed_bytes() {
 int launch_conv_pool(const GemmPlan* P, cudaStream_t stream) {
   const GemmParams& p = P->p;
   static bool attr = false;
+  void (*const kerns[2][3])(CUtensorMap, CUtensorMap, GemmParams) = {
+      {conv_pool_kernel<2, false>, conv_pool_kernel<3, false>, conv_pool_kernel<4, false>},
+      {conv_pool_kernel<2, true>, conv_pool_kernel<3, true>, conv_pool_kernel<4, true>}};
   if (!attr) {
-    cudaFuncSetAttribute(conv_pool_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(conv_pool_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(conv_pool_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (auto& row : kerns)
+      for (auto k : row) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  switch (p.N) {
-    case 128: launch_k(conv_pool_kernel<2>, dim3(P->grid_x), dim3(kCPThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p); break;
-    case 192: launch_k(conv_pool_kernel<3>, dim3(P->grid_x), dim3(kCPThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p); break;
-    case 256: launch_k(conv_pool_kernel<4>, dim3(P->grid_x), dim3(kCPThreads), P->smem_bytes, stream, 1, P->tmA, P->tmB, p); break;
-    default: return set_error(MS_ERR_INVALID, "conv+pool: N must be 128, 192 or 256");
-  }
+  const int c = p.N / 64 - 2;
+  if (c < 0 || c > 2 || p.N % 64) return set_error(MS_ERR_INVALID, "conv+pool: N must be 128, 192 or 256");
+  launch_k(kerns[p.halo_slot > 0 ? 1 : 0][c], dim3(P->grid_x), dim3(kCPThreads), P->smem_bytes, stream, 1, P->tmA,
+           P->tmB, p);
   return check_launch("conv_pool_kernel");
 }
 
@@ -361,8 +383,9 @@ extern "C" int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int 
                                       const void* Wt, int Cout, const float* bias, void* Y, long long ldy, int y_col0) {
   if (plan == nullptr || X == nullptr || Wt == nullptr || Y == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
   if (Cout != 128 && Cout != 192 && Cout != 256) return set_error(MS_ERR_INVALID, "conv+pool: Cout must be 128, 192 or 256");
-  if (((W_in + 2) + 7) / 8 * 8 != kCPPitch || H < 3 || n_img < 1)
-    return set_error(MS_ERR_INVALID, "conv+pool: input width must be 55..62 (halo rows of 64 pixels), H >= 3");
+  const bool halo = ((W_in + 2) + 7) / 8 * 8 == kCPPitch;  // 55..62: halo rows of 64 pixels
+  if ((!halo && W_in != kCPPitch) || H < 3 || n_img < 1)
+    return set_error(MS_ERR_INVALID, "conv+pool: input width must be 55..62 (halo) or 64 (tap boxes), H >= 3");
   if (C < 64 || (c_stride * 2) % 16 != 0) return set_error(MS_ERR_INVALID, "conv+pool: >= 64 channels, 16-B pixel stride");
   if ((reinterpret_cast<uintptr_t>(Y) & 15) != 0 || ldy % 8 != 0 || y_col0 % 8 != 0)
     return set_error(MS_ERR_INVALID, "conv+pool: output rows must be 16-B aligned");
@@ -389,7 +412,7 @@ extern "C" int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int 
   p.seg[0] = Seg{0, Cout, Y, ldy, y_col0, 0};
   cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W_in, (cuuint64_t)H, (cuuint64_t)n_img};
   cuuint64_t strides[3] = {(cuuint64_t)c_stride * 2, (cuuint64_t)c_stride * 2 * W_in, (cuuint64_t)c_stride * 2 * W_in * H};
-  cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)kCPPitch, (cuuint32_t)kCPHaloRows, 1};
+  cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)kCPPitch, (cuuint32_t)(halo ? kCPHaloRows : 2), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   int rc = encode_bf16_map(&P->tmA, 4, X, dims, strides, box, es, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
@@ -403,19 +426,19 @@ extern "C" int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int 
   P->w_ptr = Wt;
   P->w_kpad = K;
   P->w_rows = Cout;
-  p.a_bytes = kBK * kCPPitch * kCPHaloRows * 2;
+  p.a_bytes = kBK * kCPPitch * (halo ? kCPHaloRows : 2) * 2;
   // + 2 rows of slack: the last tap's view of the last M rows reads past the halo (wrapped, unused pixels)
-  p.halo_slot = ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024;
+  p.halo_slot = halo ? ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024 : 0;  // 0: tap-box A ring
   p.b_bytes = Cout * kBK * 2;
   const int cpg = Cout / 64;
   const int fixed = cpg == 2 ? smem_fixed_bytes<2>() : cpg == 3 ? smem_fixed_bytes<3>() : smem_fixed_bytes<4>();
-  int stages = (226 * 1024 - fixed - 2 * p.halo_slot) / p.b_bytes;
+  int stages = (226 * 1024 - fixed - 2 * p.halo_slot) / (p.b_bytes + (halo ? 0 : kABytes));
   if (stages > 9) stages = 9;
   if (stages < 2) return set_error(MS_ERR_INVALID, "conv+pool: weight stages do not fit in shared memory");
   p.stages = stages;
   p.num_kb = 9 * p.cchunks;
   p.ksplit = 1;
-  P->smem_bytes = fixed + 2 * p.halo_slot + stages * p.b_bytes + stages * 16;
+  P->smem_bytes = fixed + 2 * p.halo_slot + stages * (p.b_bytes + (halo ? 0 : kABytes)) + stages * 16;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "conv+pool plan exceeds 227 KB shared memory");
   const int sms = sm_count();
   P->grid_x = p.units < sms ? p.units : sms;

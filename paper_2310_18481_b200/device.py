@@ -440,7 +440,7 @@ def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0, plan
 
 def plan_conv_pool(X, n_img, H, W_in, C_in, c_stride, Wt, Cout, bias, Y, *, ldy, col0=0):
     """Fused 3x3/1/1 conv + bias + ReLU + 3x3/2 ceil max pool
-    (``ms_gemm_plan_conv_pool``, widths 55..62): the pooled map is written to
+    (``ms_gemm_plan_conv_pool``, widths 55..62 or 64): the pooled map is written to
     ``Y`` ([n_img, PH, PW] rows of ``ldy``), the conv map never reaches HBM.
     ``Wt`` from ``encoders.pack_conv_weight``."""
     p = GemmPlan()

@@ -466,7 +466,7 @@ class BNInceptionEncoder:
         self.a_p1 = buf(n_img * h2 * h2, 64)
         self.a_c2r = buf(n_img * h2 * h2, 64)
         # the unpooled conv2 map exists only without the fused conv2 + pool2 kernel
-        self.a_c2 = None if (self.fused_pool2 and 55 <= h2 <= 62) else buf(n_img * h2 * h2, 192)
+        self.a_c2 = None if (self.fused_pool2 and (55 <= h2 <= 62 or h2 == 64)) else buf(n_img * h2 * h2, 192)
         self.blocks = {}
         # ping-pong block outputs + scratch sized for the largest block
         max_pix_c = 0
@@ -543,9 +543,10 @@ class BNInceptionEncoder:
         # the ceil8(W+2)-wide tiles than they gain, audio's 64+2 does not tile 128
         h = pool_out(h2, 3, 2, 0, True)
         cur = self.ping
-        if self.fused_pool2 and 55 <= h2 <= 62:
-            # conv2 + ReLU + pool2 in one kernel (csrc/convpool.cu): the 56^2 x 192
-            # map never reaches HBM; bitwise equal to the pair below (1.43x, 183 frames)
+        if self.fused_pool2 and (55 <= h2 <= 62 or h2 == 64):
+            # conv2 + ReLU + pool2 in one kernel (csrc/convpool.cu; halo tiles at 56^2,
+            # tap boxes at audio's 64^2): the unpooled x 192 map never reaches HBM;
+            # bitwise equal to the pair below (rgb 56^2 at 183 frames: 1.43x)
             P.gemm(dv.plan_conv_pool(self.a_c2r, n, h2, h2, 64, 64, self.w["conv2"], 192, self.b["conv2"],
                                      cur, ldy=192))
         else:

@@ -41,17 +41,22 @@ def timed(fn, inner=10):
     return float(np.median(ts))
 
 
-H, cin, cout = 56, 64, 192
-for n in (183, 108, 48):
+cin, cout = 64, 192
+for H, n in ((56, 183), (56, 108), (56, 48), (64, 72)):
     X = torch.randn(n, H, H, cin, device="cuda").to(torch.bfloat16)
     w = torch.randn(cout, cin, 3, 3) * (2.0 / (9 * cin)) ** 0.5
     Wt = pack_conv_weight(w).to("cuda")
     b = torch.randn(cout, device="cuda") * 0.1
     D = torch.empty(n * H * H, cout, device="cuda", dtype=torch.bfloat16)
-    PH = 28
+    PH = (H - 3 + 1) // 2 + 1
     Y = torch.empty(n * PH * PH, cout, device="cuda", dtype=torch.bfloat16)
     Y2 = torch.empty_like(Y)
-    conv = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, Wt, cout, b, D, ldd=cout, BN=cout, halo=True)
+    if H == 64:  # audio's conv2: tap boxes (halo rows of 72 do not tile 128)
+        from paper_2310_18481_b200.encoders import pick_conv_tile
+        conv = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, Wt, cout, b, D, ldd=cout, BN=cout,
+                            tile=pick_conv_tile(n, H, H))
+    else:
+        conv = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, Wt, cout, b, D, ldd=cout, BN=cout, halo=True)
     P = dv.Program()
     P.gemm(conv)
     P.pool(D, n, H, H, cout, cout, 3, 2, 0, True, True, Y2, cout, 0)
@@ -63,6 +68,6 @@ for n in (183, 108, 48):
     torch.cuda.synchronize()
     same = torch.equal(Y, Y2)
     fl = conv.flops
-    print(f"n={n:3d}: halo conv {t_conv:6.1f} us + pool = {t_pair:6.1f} us | fused {t_fused:6.1f} us "
+    print(f"{H}x{H} n={n:3d}: conv {t_conv:6.1f} us + pool = {t_pair:6.1f} us | fused {t_fused:6.1f} us "
           f"({fl / t_fused / 1e6:.0f} TF/s)  x{t_pair / t_fused:.2f}  grid {fused.info()['grid_x']} "
           f"stages {fused.info()['stages']}  {'bitwise equal' if same else 'MISMATCH'}", flush=True)
