@@ -138,73 +138,82 @@ __device__ __forceinline__ void pool_hrow_max2(const __nv_bfloat16* __restrict__
 // row loads for these tiny rows.
 // 3x3 / stride 1 / pad 1 average pool (count_include_pad) + bias + ReLU,
 // register-blocked: one thread = one (image, column, 8-channel group) and
-// kAvgRows output rows; its (kAvgRows + 2) x 3 input loads are independent
-// (all issued up front), neighbouring threads read neighbouring 16-B groups.
-// No shared memory, no block barriers, no divisions in the loop.  Replaces
-// the smem-staged kernel, which was bound by its three barrier-separated
-// phases and index arithmetic on these small (28^2 / 14^2 / 7^2) maps.
+// kAvgRows output rows, walking them with a rolling window of three
+// horizontal 3-sums (each row's 3 loads issued together); neighbouring
+// threads read neighbouring 16-B groups.  No shared memory, no barriers, and
+// <= 40 registers (__launch_bounds__(256, 6)): a block fits beside a resident
+// GEMM CTA (320 threads x <= 168 registers, ~200 KB smem) on the same SM, so
+// the Inception pool lanes run in the issue slots the GEMMs leave idle
+// instead of waiting for whole SMs.
 constexpr int kAvgRows = 4;
-__global__ void __launch_bounds__(256) avgpool3_s1_reg_kernel(const __nv_bfloat16* __restrict__ X, int n_img, int H,
-                                                             int W, int C, long long xcs, __nv_bfloat16* __restrict__ Y,
-                                                             long long ycs, int ycol0, const float* __restrict__ bias,
-                                                             int relu) {
+// 4 channels (8 bytes) per thread keep the three rolling fp32 row sums in 12 registers
+__device__ __forceinline__ void avg_hrow(const __nv_bfloat16* __restrict__ X, long long img, int H, int W,
+                                         long long xcs, int g, int ih, int x, float (&h)[4]) {
+  uint2 v[3];
+#pragma unroll
+  for (int dx = 0; dx < 3; ++dx) {
+    const int xx = x - 1 + dx;
+    v[dx] = (ih >= 0 && ih < H && xx >= 0 && xx < W)
+                ? __ldg(reinterpret_cast<const uint2*>(X + ((img * H + ih) * W + xx) * xcs + g * 4))
+                : make_uint2(0u, 0u);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v[dx])[j]);
+      s2.x += f.x;
+      s2.y += f.y;
+    }
+    h[2 * j] = s2.x;
+    h[2 * j + 1] = s2.y;
+  }
+}
+__global__ void __launch_bounds__(256, 6) avgpool3_s1_reg_kernel(const __nv_bfloat16* __restrict__ X, int n_img,
+                                                                int H, int W, int C, long long xcs,
+                                                                __nv_bfloat16* __restrict__ Y, long long ycs,
+                                                                int ycol0, const float* __restrict__ bias, int relu) {
   pdl_trigger();
   pdl_wait();
-  const int cg = C >> 3;
+  const int cg = C >> 2;
   const int rb_n = (H + kAvgRows - 1) / kAvgRows;
-  const long long total = (long long)n_img * rb_n * W * cg;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(t % cg);
-    long long u = t / cg;
-    const int x = (int)(u % W);
+  const int total = n_img * rb_n * W * cg;  // < 2^31 (host-checked)
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int g = t % cg;
+    int u = t / cg;
+    const int x = u % W;
     u /= W;
-    const int rb = (int)(u % rb_n);
+    const int rb = u % rb_n;
     const long long img = u / rb_n;
     const int oh0 = rb * kAvgRows;
-    float hs[kAvgRows + 2][8];
+    float bv[4];
 #pragma unroll
-    for (int r = 0; r < kAvgRows + 2; ++r) {
-      const int ih = oh0 - 1 + r;
-      uint4 v[3];
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const int xx = x - 1 + dx;
-        v[dx] = (ih >= 0 && ih < H && xx >= 0 && xx < W)
-                    ? __ldg(reinterpret_cast<const uint4*>(X + ((img * H + ih) * W + xx) * xcs + g * 8))
-                    : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int dx = 0; dx < 3; ++dx) {
-          const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v[dx])[j]);
-          s2.x += f.x;
-          s2.y += f.y;
-        }
-        hs[r][2 * j] = s2.x;
-        hs[r][2 * j + 1] = s2.y;
-      }
-    }
-    float bv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) bv[j] = bias != nullptr ? bias[g * 8 + j] : 0.0f;
-#pragma unroll
+    for (int j = 0; j < 4; ++j) bv[j] = bias != nullptr ? __ldg(bias + g * 4 + j) : 0.0f;
+    float h0[4], h1[4], h2[4];
+    avg_hrow(X, img, H, W, xcs, g, oh0 - 1, x, h0);
+    avg_hrow(X, img, H, W, xcs, g, oh0, x, h1);
+#pragma unroll 1
     for (int r = 0; r < kAvgRows; ++r) {
       if (oh0 + r >= H) break;
-      uint32_t pk[4];
+      avg_hrow(X, img, H, W, xcs, g, oh0 + r + 1, x, h2);
+      uint32_t pk[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float a = (hs[r][2 * j] + hs[r + 1][2 * j] + hs[r + 2][2 * j]) * (1.0f / 9.0f) + bv[2 * j];
-        float b = (hs[r][2 * j + 1] + hs[r + 1][2 * j + 1] + hs[r + 2][2 * j + 1]) * (1.0f / 9.0f) + bv[2 * j + 1];
+      for (int j = 0; j < 2; ++j) {
+        float a = (h0[2 * j] + h1[2 * j] + h2[2 * j]) * (1.0f / 9.0f) + bv[2 * j];
+        float b = (h0[2 * j + 1] + h1[2 * j + 1] + h2[2 * j + 1]) * (1.0f / 9.0f) + bv[2 * j + 1];
         if (relu) {
           a = fmaxf(a, 0.0f);
           b = fmaxf(b, 0.0f);
         }
         pk[j] = pack_bf16x2(a, b);
       }
-      *reinterpret_cast<uint4*>(Y + ((img * H + oh0 + r) * W + x) * ycs + ycol0 + g * 8) =
-          make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint2*>(Y + ((img * H + oh0 + r) * W + x) * ycs + ycol0 + g * 4) = make_uint2(pk[0], pk[1]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        h0[j] = h1[j];
+        h1[j] = h2[j];
+      }
     }
   }
 }
@@ -296,7 +305,7 @@ __global__ void __launch_bounds__(256) avgpool3_s1_kernel(const __nv_bfloat16* _
 }
 
 template <int STRIDE>
-__global__ void __launch_bounds__(512, 3) pool3_rows_max_kernel(const __nv_bfloat16* __restrict__ X, int H, int W,
+__global__ void __launch_bounds__(256, 6) pool3_rows_max_kernel(const __nv_bfloat16* __restrict__ X, int H, int W,
                                                                int C, long long xcs, int pad, int OH, int OW, int TH,
                                                                __nv_bfloat16* __restrict__ Y, long long ycs,
                                                                int ycol0, const float* __restrict__ bias, int relu) {
@@ -622,7 +631,8 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
   const int threads = (a.C / 8) * OW;
   static const bool avg_smem = getenv("MS_AVGPOOL_SMEM") != nullptr;  // A/B: the smem-staged kernel
   if (!a.is_max && a.k == 3 && a.stride == 1 && a.pad == 1 && !avg_smem) {
-    const long long items = (long long)a.n_img * ((a.H + kAvgRows - 1) / kAvgRows) * a.W * (a.C / 8);
+    const long long items = (long long)a.n_img * ((a.H + kAvgRows - 1) / kAvgRows) * a.W * (a.C / 4);
+    if (items >= (1LL << 31)) return set_error(MS_ERR_INVALID, "avg pool: too many work items");
     long long blocks = (items + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     launch_k(avgpool3_s1_reg_kernel, dim3((unsigned)blocks), dim3(256), 0, st, 1,
@@ -644,7 +654,10 @@ static int run_pool(const PoolArgs& a, cudaStream_t st) {
     return check_launch("avgpool3_s1_kernel");
   }
   if (a.k == 3 && (a.stride == 1 || a.stride == 2) && a.n_img <= 65535) {
-    const int block = threads < 512 ? (threads + 31) / 32 * 32 : 512;
+    // <= 256 threads x <= 40 registers: max-pool blocks fit beside a resident
+    // GEMM CTA (see avgpool3_s1_reg_kernel); the other pool kernels keep 512
+    const int cap = a.is_max ? 256 : 512;
+    const int block = threads < cap ? (threads + 31) / 32 * 32 : cap;
     // output rows per thread: the largest of 8/4/2/1 whose grid fills its
     // last wave of resident blocks to >= 85% (a 1.1-wave grid idles half the
     // GPU in its tail); fewer rows cost only L2 re-reads of window rows
