@@ -111,8 +111,12 @@ __device__ __forceinline__ void convert_chunk4(const uint32_t (&v)[32], const fl
 //                                peer's TMA completes on the leader's barrier
 //   empty[s], aempty[h], tfull : multicast tcgen05.commit from the leader
 //   tempty[a] (leader)         : both CTAs' epilogue warps arrive (remote)
-template <int MODE, int EPI, int ACT, int PAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+// OCC = 2: an instantiation capped at 96 registers, so that two CTAs (of this
+// or another op of a concurrent Inception branch lane) fit on one SM when the
+// plan also keeps its shared memory <= ~113 KB and its TMEM <= 256 columns
+// (GemmParams::occ2; tools/ab.sh MS_OCC2=1).
+template <int MODE, int EPI, int ACT, int PAIR, int OCC = 1>
+__global__ void __launch_bounds__(kThreads, OCC)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ GemmParams p, const __grid_constant__ StoreMaps tmD) {
   // Persistent: CTA b processes tiles b, b + grid, ...; tile t -> (m = t / n_tiles,
@@ -172,7 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   uint32_t acc_stride = 32;
   while (acc_stride < (uint32_t)p.BN) acc_stride <<= 1;
-  const uint32_t tmem_cols = 2 * acc_stride;
+  // two accumulators (the epilogue of tile i overlaps the MMAs of tile i+1), one
+  // for a wide-N plan launched two CTAs per SM (the co-resident CTA fills the gap)
+  const int n_acc = p.single_acc ? 1 : 2;
+  const uint32_t tmem_cols = (uint32_t)n_acc * acc_stride;
   if (warp == 1) {
     if (PAIR)
       tmem_alloc_pair(tmem_slot, tmem_cols);
@@ -435,8 +442,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           hphase ^= 1;
         }
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == n_acc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   } else if (warp == 1 && MODE != MODE_CONV_HALO && leader) {
     // -------------------------------------------------- MMA issuer
@@ -495,8 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == n_acc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   } else if (warp >= 2) {
     // ---------------------- warps 2..9: gather (2..5) + epilogue (all 8)
@@ -520,8 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tempty_bar0 = PAIR ? mapa_shared(smem_addr(&tempty[0]), 0) : 0u;
     for (int t = cta0; t < num_tiles; t += ncta) {
       if (tg && acc != grp) {  // the other group's tile
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (++acc == n_acc) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
         continue;
       }
       const TileIdx ti = decode_tile<PAIR>(p, t, n_tiles, rank);
@@ -732,8 +745,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (!tg && grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
       if (warp == 2 && lane == 0 && t == cta0) GEMM_TRACE(11);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == n_acc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
     if (EPI == EPI_TMA && (issuer || (p.warp_store && lane == 0))) bulk_wait0();
     if (warp == 2 && lane == 0) GEMM_TRACE(7);
@@ -768,6 +783,14 @@ static GemmKernelFn pick_act(int act) {
 
 // The instantiation for a plan (null if the combination is unsupported).
 static GemmKernelFn gemm_kernel_for(const GemmParams& p) {
+  if (p.occ2 && !p.pair && p.ksplit <= 1 && !p.out_fp32 && p.tma_store && p.relu == MS_ACT_RELU) {
+    switch (p.mode) {
+      case MODE_DENSE: return gemm_tc_kernel<MODE_DENSE, EPI_TMA, MS_ACT_RELU, 0, 2>;
+      case MODE_CONV: return gemm_tc_kernel<MODE_CONV, EPI_TMA, MS_ACT_RELU, 0, 2>;
+      case MODE_CONV_K32: return gemm_tc_kernel<MODE_CONV_K32, EPI_TMA, MS_ACT_RELU, 0, 2>;
+      default: break;
+    }
+  }
   if (p.pair) {  // CTA pairs: bf16 TMA-store epilogue only (set_pair checks)
     switch (p.mode) {
       case MODE_DENSE: return pick_act<MODE_DENSE, EPI_TMA, 1>(p.relu);
@@ -1274,16 +1297,33 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   int stages = (226 * 1024 - 1024 - 288 - p.stage_bytes - bias_bytes) / per_stage;
   if (stages > max_stages()) stages = max_stages();
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
+  // two CTAs per SM (see gemm_tc_kernel's OCC): TMEM <= 256 columns, <= 112 KB of
+  // shared memory (>= 3 stages; more measured no faster on the feed-limited
+  // convs, profiles/r02_stages.txt)
+  static const bool occ2_env = getenv("MS_OCC2") == nullptr || atoi(getenv("MS_OCC2")) != 0;  // default on
+  const int per_occ2 = (112 * 1024 - 1024 - p.stage_bytes - (2 * 3 + 8) * 8 - 16 - bias_bytes) / per_stage;
+  static const bool occ2_wide = getenv("MS_OCC2_NARROW") == nullptr;  // A/B: BN <= 128 plans only
+  p.occ2 = (occ2_env && (BN <= 128 || occ2_wide) && per_occ2 >= 3 && p.tma_store && !p.out_fp32 &&
+            p.relu == MS_ACT_RELU && (p.mode == MODE_DENSE || p.mode == MODE_CONV || p.mode == MODE_CONV_K32))
+               ? 1
+               : 0;
+  p.single_acc = (p.occ2 && BN > 128) ? 1 : 0;  // TMEM: 2 x 128 or 1 x 256 columns per CTA
+  if (p.occ2 && stages > per_occ2) stages = per_occ2;
   p.stages = stages;
   P->smem_bytes = 1024 + stages * per_stage + p.stage_bytes + (2 * stages + 8) * 8 + 16 + bias_bytes;
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
-  P->grid_x = tiles < sm_count() ? tiles : sm_count();
+  // two of this kernel's own CTAs per SM where the tiles are plentiful
+  // (MS_OCC2_GRID: 0 never, 1 always, default: >= 4 tiles per SM)
+  static const int occ2_grid = getenv("MS_OCC2_GRID") ? atoi(getenv("MS_OCC2_GRID")) : 2;
+  const bool grid2 = p.occ2 && (occ2_grid == 1 || (occ2_grid == 2 && tiles >= 4 * sm_count()));
+  const int max_ctas = grid2 ? 2 * sm_count() : sm_count();
+  P->grid_x = tiles < max_ctas ? tiles : max_ctas;
   P->grid_y = 1;
   int tc = 32;
   while (tc < BN) tc <<= 1;
-  P->tmem_cols = 2 * tc;
+  P->tmem_cols = (p.single_acc ? 1 : 2) * tc;
   return MS_OK;
 }
 
@@ -1577,6 +1617,15 @@ int ms_gemm_plan_conv_halo(void* plan, const void* X, int n_img, int H, int W_in
   rc = encode_map(&Pl->tmA, 4, X, dims, strides, box, es);
   if (rc) return rc;
   p.mode = MODE_CONV_HALO;
+  p.occ2 = 0;  // halo plans keep one CTA per SM (resident weights / halo ring)
+  p.single_acc = 0;
+  {
+    int tc = 32;
+    while (tc < p.BN) tc <<= 1;
+    Pl->tmem_cols = 2 * tc;
+    const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN);
+    Pl->grid_x = tiles < sm_count() ? tiles : sm_count();
+  }
   p.a_bytes = kBK * P * (bh + 2) * 2;
   // + 2 rows: the last tap's shifted view of the last M rows reads past the halo
   p.halo_slot = ((p.a_bytes + 2 * 128) + 1023) / 1024 * 1024;
@@ -1656,7 +1705,12 @@ int ms_gemm_plan_set_splitk(void* plan, int ksplit, float* ws, long long ws_ld) 
   p.kb_per = kb_per;
   p.ws = ws;
   p.ws_ld = ws_ld;
-  if (p.ksplit > 1) p.tma_store = 0;  // partial sums go to the fp32 workspace (layout unchanged)
+  if (p.ksplit > 1) {
+    p.tma_store = 0;  // partial sums go to the fp32 workspace (layout unchanged)
+    p.occ2 = 0;
+    p.single_acc = 0;
+  }
+  // (grid recomputed below for the split tiles)
   const int tiles = p.m_tiles * ((p.N + p.BN - 1) / p.BN) * p.ksplit;
   P->grid_x = tiles < sm_count() ? tiles : sm_count();
   return MS_OK;
@@ -1678,6 +1732,8 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   int rc = encode_map(&P->tmB, 2, P->w_ptr, dims, strides, box, es);
   if (rc) return rc;
   p.pair = 1;
+  p.occ2 = 0;
+  p.single_acc = 0;
   p.b_bytes = (p.BN / 2) * kBK * 2;
   const int bias_bytes = ((p.N + 31) / 32) * 32 * 4;
   const int n_tiles = (p.N + p.BN - 1) / p.BN;

@@ -114,6 +114,8 @@ struct GemmParams {
   int direct_store; // EPI_TMA conv tiles: registers -> global, no smem staging (A/B only, MS_DIRECT_STORE:
                     // measured 13 % slower on conv2 at 56^2 than the TMA-store epilogue)
   int stage_bytes;  // epilogue staging bytes in shared memory
+  int occ2;         // launch the 2-CTAs-per-SM instantiation (OCC = 2)
+  int single_acc;   // one TMEM accumulator (occ2 plans with BN > 128)
   // MODE_STEM_POOL: raw pre-padded 4-channel input rows, fused 3x3/2 max pool
   const uint8_t* xraw;
   const uint8_t* wraw;  // MODE_STEM_POOL: row-pair weights (encoders.pack_stem_weight)
