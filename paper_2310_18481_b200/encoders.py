@@ -604,10 +604,13 @@ class BNInceptionEncoder:
         tile_out = pick_conv_tile(n, o, o)
 
         def halo_ok(cin_, cout_, stride_):
-            # halo + resident weights (one N tile, 9 x 64-ch blocks in smem):
-            # 1.36x the tap-box kernel at 28x28 (tools/halo_bench.py)
+            # halo + resident weights (one N tile, 9 x 64-ch blocks in smem): 1.36x the
+            # one-CTA-per-SM tap-box kernel at 28x28 alone, but with tap-box plans
+            # launched two CTAs per SM (OCC=2) the served pass is 2.2 % faster
+            # without it (profiles/r02_ab_halo28.txt): opt-in (MS_HALO28=1)
             pitch = -(-(h + 2) // 8) * 8  # halo row width: must tile the 128-row M block
-            return stride_ == 1 and 14 < h <= 30 and 128 % pitch == 0 and cin_ <= 64 and cout_ <= 128
+            return (stride_ == 1 and 14 < h <= 30 and 128 % pitch == 0 and cin_ <= 64 and cout_ <= 128
+                    and os.environ.get("MS_HALO28") is not None)
 
         def k32(cin_):  # matches the weight packing in _pack
             return cin_ % 64 != 0 and cin_ % 32 == 0
@@ -626,13 +629,15 @@ class BNInceptionEncoder:
 
         def halo_pair_ok(cin_, stride_):
             """Halo tiles on CTA pairs with half of the (64-padded) weights
-            resident per SM: at 28x28 96->96 1.26x the K32 tap-box kernel
-            (tools/conv_variants.py, profiles/r02_conv_variants.txt); at 14x14
-            the tap-box kernels win for every served shape (A/B: MS_HALO14_PAIR)."""
+            resident per SM: at 28x28 96->96 1.26x the one-CTA-per-SM K32
+            kernel (profiles/r02_conv_variants.txt), but slower than the K32
+            kernel two CTAs per SM in the served pass (opt-in: MS_HALO28_PAIR);
+            at 14x14 the tap-box kernels win for every served shape
+            (MS_HALO14_PAIR)."""
             if stride_ != 1 or 128 % (-(-(h + 2) // 8) * 8) != 0:
                 return False
             if 14 < h <= 30:
-                return cin_ == 96 and os.environ.get("MS_NO_HALO28_PAIR") is None
+                return cin_ == 96 and os.environ.get("MS_HALO28_PAIR") is not None
             if h == 14:
                 return os.environ.get("MS_HALO14_PAIR") is not None
             return False
