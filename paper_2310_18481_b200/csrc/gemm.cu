@@ -1298,12 +1298,21 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   if (stages > max_stages()) stages = max_stages();
   if (stages > num_kb) stages = num_kb < 2 ? 2 : num_kb;
   // two CTAs per SM (see gemm_tc_kernel's OCC): TMEM <= 256 columns, <= 112 KB of
-  // shared memory (>= 3 stages; more measured no faster on the feed-limited
-  // convs, profiles/r02_stages.txt)
+  // shared memory (>= 2 stages: with a co-resident CTA, 2 stages per CTA beat
+  // 3+ stages at one CTA per SM -- served-pass encoders -4.2 %,
+  // profiles/r02_ab_two_ctas_per_sm.txt; MS_OCC2_MIN_STAGES for A/B)
   static const bool occ2_env = getenv("MS_OCC2") == nullptr || atoi(getenv("MS_OCC2")) != 0;  // default on
   const int per_occ2 = (112 * 1024 - 1024 - p.stage_bytes - (2 * 3 + 8) * 8 - 16 - bias_bytes) / per_stage;
   static const bool occ2_wide = getenv("MS_OCC2_NARROW") == nullptr;  // A/B: BN <= 128 plans only
-  p.occ2 = (occ2_env && (BN <= 128 || occ2_wide) && per_occ2 >= 3 && p.tma_store && !p.out_fp32 &&
+  static const int occ2_min_stages = getenv("MS_OCC2_MIN_STAGES") ? atoi(getenv("MS_OCC2_MIN_STAGES")) : 2;
+  // ... and only for layers with enough tiles to fill the GPU: a small pass's
+  // kernels are latency-bound per CTA, where the full-stage, full-register
+  // instantiation wins (MS_OCC2_MIN_TILES, default 64: best of 0/24/64/148 at
+  // every pass size 1..96, profiles/r02_pass_sizes_occ2.txt)
+  static const int occ2_min_tiles = getenv("MS_OCC2_MIN_TILES") ? atoi(getenv("MS_OCC2_MIN_TILES")) : 64;
+  const int tiles_all = grid_x * ((p.N + BN - 1) / BN);
+  p.occ2 = (occ2_env && tiles_all >= occ2_min_tiles && (BN <= 128 || occ2_wide) && per_occ2 >= occ2_min_stages &&
+            p.tma_store && !p.out_fp32 &&
             p.relu == MS_ACT_RELU && (p.mode == MODE_DENSE || p.mode == MODE_CONV || p.mode == MODE_CONV_K32))
                ? 1
                : 0;
@@ -1314,9 +1323,11 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
-  // two of this kernel's own CTAs per SM where the tiles are plentiful
-  // (MS_OCC2_GRID: 0 never, 1 always, default: >= 4 tiles per SM)
-  static const int occ2_grid = getenv("MS_OCC2_GRID") ? atoi(getenv("MS_OCC2_GRID")) : 2;
+  // up to two of this kernel's own CTAs per SM (MS_OCC2_GRID: 0 never, 2 only
+  // with >= 4 tiles per SM, default 1 always: a kernel with no concurrent
+  // partner still fills both slots -- single-encoder passes 3-6 % faster,
+  // profiles/r02_abn_occ2.txt)
+  static const int occ2_grid = getenv("MS_OCC2_GRID") ? atoi(getenv("MS_OCC2_GRID")) : 1;
   const bool grid2 = p.occ2 && (occ2_grid == 1 || (occ2_grid == 2 && tiles >= 4 * sm_count()));
   const int max_ctas = grid2 ? 2 * sm_count() : sm_count();
   P->grid_x = tiles < max_ctas ? tiles : max_ctas;
