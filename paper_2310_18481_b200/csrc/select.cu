@@ -541,12 +541,31 @@ constexpr int kMaxLineBytes = 16384;
 // One staged unit of a padded gather: nl source lines (in line_buf, their
 // destination lines in s_dline) of compacted request j -> converted, padded
 // destination pixels (V = channels per vector store: 8 or 4).
+// uint8 -> bf16 without I2F: 0x4B000000 | b is the float 2^23 + b exactly, so
+// fmaf(it, scale, bias2) with bias2 = bias - 2^23 * scale rounds once to the
+// same value as fmaf((float)b, scale, bias) whenever 2^23 * scale is a power
+// of two and bias2 is exact in fp32 (the host checks: u8_bias2 is NaN
+// otherwise and the caller keeps the I2F path).  Two values per cvt.
+__device__ __forceinline__ uint32_t u8x2_bf16(uint32_t b0, uint32_t b1, float scale, float bias2) {
+  const float f0 = fmaf(__uint_as_float(0x4B000000u | b0), scale, bias2);
+  const float f1 = fmaf(__uint_as_float(0x4B000000u | b1), scale, bias2);
+  const __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t u8x1_bf16(uint32_t b0, float scale, float bias2) {
+  const float f0 = fmaf(__uint_as_float(0x4B000000u | b0), scale, bias2);
+  const __nv_bfloat162 h = __floats2bfloat162_rn(f0, 0.0f);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 template <bool U8, int V>
 __device__ __forceinline__ void pad_store_lines(const unsigned char* __restrict__ line_buf,
                                                 const long long* __restrict__ s_dline, int nl, int line_bytes,
                                                 int width, int c_src, int gv, int wd, int pad_w, float u8_scale,
                                                 float u8_bias, long long plane_vecs, long long j,
-                                                long long dst_lines, void* __restrict__ dst_v) {
+                                                long long dst_lines, void* __restrict__ dst_v,
+                                                float u8_bias2) {
+  const bool fast = U8 && u8_bias2 == u8_bias2;  // not NaN: the exact I2F-free conversion applies
   typedef typename std::conditional<V == 8, uint4, uint2>::type vec_t;
   vec_t* dst = reinterpret_cast<vec_t*>(dst_v);
   vec_t* drow = dst + j * dst_lines * wd * gv;
@@ -562,6 +581,28 @@ __device__ __forceinline__ void pad_store_lines(const unsigned char* __restrict_
           if (li >= nl) break;
         }
         const unsigned char* lb = line_buf + li * line_bytes;
+        const int x0 = 2 * pq - pad_w;
+        if (fast && c_src == 10 && plane_vecs > 0 && x0 >= 0 && x0 + 1 < width) {
+          // flow interior: 2 pixels x 10 channels -> three planes of 2 x 4 (8, 9, 0, 0 in plane 2)
+          const unsigned char* q0 = lb + x0 * 10;
+          uint32_t w[12];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const unsigned char* qq = q0 + 10 * h;
+            w[6 * h + 0] = u8x2_bf16(qq[0], qq[1], u8_scale, u8_bias2);
+            w[6 * h + 1] = u8x2_bf16(qq[2], qq[3], u8_scale, u8_bias2);
+            w[6 * h + 2] = u8x2_bf16(qq[4], qq[5], u8_scale, u8_bias2);
+            w[6 * h + 3] = u8x2_bf16(qq[6], qq[7], u8_scale, u8_bias2);
+            w[6 * h + 4] = u8x2_bf16(qq[8], qq[9], u8_scale, u8_bias2);
+            w[6 * h + 5] = 0u;
+          }
+          const long long pix = ((long long)j * dst_lines + s_dline[li]) * wd + 2 * pq;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            *reinterpret_cast<uint4*>(dst + q * plane_vecs + pix) =
+                make_uint4(w[2 * q], w[2 * q + 1], w[6 + 2 * q], w[6 + 2 * q + 1]);
+          continue;
+        }
         unsigned short v[24];
 #pragma unroll
         for (int i = 0; i < 24; ++i) v[i] = 0;
@@ -613,6 +654,14 @@ __device__ __forceinline__ void pad_store_lines(const unsigned char* __restrict_
           if (li >= nl) break;
         }
         const unsigned char* lb = line_buf + li * line_bytes;
+        const int x0 = 2 * pq - pad_w;
+        if (fast && c_src == 3 && x0 >= 0 && x0 + 1 < width) {  // rgb interior: 2 pixels x (3 ch + 0)
+          const unsigned char* q0 = lb + x0 * 3;
+          *reinterpret_cast<uint4*>(drow + (s_dline[li] * wd + 2 * pq)) =
+              make_uint4(u8x2_bf16(q0[0], q0[1], u8_scale, u8_bias2), u8x1_bf16(q0[2], u8_scale, u8_bias2),
+                         u8x2_bf16(q0[3], q0[4], u8_scale, u8_bias2), u8x1_bf16(q0[5], u8_scale, u8_bias2));
+          continue;
+        }
         unsigned short v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -716,7 +765,7 @@ __global__ void __launch_bounds__(256) gather_rows_pad_kernel(const void* __rest
       }
       __syncthreads();
       pad_store_lines<U8, V>(line_buf, s_dline, nl, line_bytes, width, c_src, gv, wd, pad_w, u8_scale, u8_bias,
-                             plane_vecs, j, dst_lines, dst_v);
+                             plane_vecs, j, dst_lines, dst_v, __int_as_float(0x7fc00000));
     }
   }
   if (pdl_mode == 2) pdl_wait();
@@ -789,6 +838,7 @@ struct FusedMod {
   int per;   // lines (padded) or 16-B vectors (plain) per unit
   int chunks, line_bytes;
   float u8_scale, u8_bias;
+  float u8_bias2;  // bias - 2^23 * scale when exact (the I2F-free conversion), else NaN
 };
 struct FusedArgs {
   const uint16_t* mask;
@@ -948,18 +998,18 @@ __global__ void __launch_bounds__(kFusedThreads, 4) compact_fused_kernel(const _
       const int gv = M.c_dst / 4;
       if (M.src_u8)
         pad_store_lines<true, 4>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, M.u8_scale,
-                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G);
+                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G, M.u8_bias2);
       else
         pad_store_lines<false, 4>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, 1.0f, 0.0f,
-                                  M.plane_vecs, j, M.dst_lines, M.G);
+                                  M.plane_vecs, j, M.dst_lines, M.G, 0.0f);
     } else {
       const int gv = M.c_dst / 8;
       if (M.src_u8)
         pad_store_lines<true, 8>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, M.u8_scale,
-                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G);
+                                 M.u8_bias, M.plane_vecs, j, M.dst_lines, M.G, M.u8_bias2);
       else
         pad_store_lines<false, 8>(line_buf, s_dline, nl, M.line_bytes, M.width, M.c_src, gv, wd, M.pad_w, 1.0f, 0.0f,
-                                  M.plane_vecs, j, M.dst_lines, M.G);
+                                  M.plane_vecs, j, M.dst_lines, M.G, 0.0f);
     }
   }
 }
@@ -1176,6 +1226,14 @@ static int compact_fused(const uint16_t* mask, int N, int K, const void* const* 
     M.src_u8 = r.src_u8;
     M.u8_scale = r.src_u8 ? r.u8_scale : 1.0f;
     M.u8_bias = r.src_u8 ? r.u8_bias : 0.0f;
+    M.u8_bias2 = nanf("");
+    if (r.src_u8) {  // exactness of the I2F-free conversion (see u8x2_bf16)
+      int e = 0;
+      const double m = frexp((double)r.u8_scale, &e);
+      const double P = ldexp((double)r.u8_scale, 23);
+      const double b2 = (double)r.u8_bias - P;
+      if (m == 0.5 && (double)(float)P == P && (double)(float)b2 == b2 && !getenv("MS_GATHER_I2F")) M.u8_bias2 = (float)b2;
+    }
     M.frame_h = framed ? r.frame_h : 0;
     M.pad_h = framed ? r.pad_h : 0;
     M.plane_vecs = r.plane_stride / 4;

@@ -584,6 +584,18 @@ class StagedProgram:
     def n_launches(self) -> int:
         return sum(p.n_launches for lanes in self.stages for p in lanes)
 
+    def first(self):
+        """Stage 0 alone (a StagedProgram view sharing the sealed programs)."""
+        v = StagedProgram(self.ctx)
+        v.stages = self.stages[:1]
+        return v
+
+    def tail(self):
+        """Every stage after stage 0 (a StagedProgram view)."""
+        v = StagedProgram(self.ctx)
+        v.stages = self.stages[1:]
+        return v
+
     def run(self, stream=None):
         torch = _torch()
         main = torch.cuda.current_stream() if stream is None else stream

@@ -483,7 +483,8 @@ class BNInceptionEncoder:
         self.td = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.td2 = torch.empty(n_img * max_tmp, dtype=bf, device=d)
         self.tp = torch.empty(n_img * max_tmp, dtype=bf, device=d)
-        self.out = torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d)
+        self.outs = [torch.empty(self.max_req, FEAT_DIM, dtype=bf, device=d) for _ in range(2)]
+        self.out = self.outs[0]
         # conv1 input: W-padded by CONV1_PAD zero pixels per side (the gather
         # pads) and, for 4-channel frames, row-padded too (zero rows written
         # once here, never touched by the gather)
@@ -500,16 +501,22 @@ class BNInceptionEncoder:
             self.stem_planes = 3
         self.x_plane_stride = n_img * (size + 2 * rp) * (size + 2 * CONV1_PAD) * 4 if self.stem_planes == 3 else 0
 
-    def program(self, n_req: int):
-        if n_req in self._programs:
-            return self._programs[n_req]
+    # features of pass parity p land in outs[p]: with passes pipelined the next
+    # pass's encoder may finish before the previous pass's fusion head has read
+    # its features (executor.MaskedModel.run_ring)
+    supports_parity = True
+
+    def program(self, n_req: int, parity: int = 0):
+        key = (n_req, parity)
+        if key in self._programs:
+            return self._programs[key]
         if not 1 <= n_req <= self.max_req:
             raise ValueError(f"n_req {n_req} outside 1..{self.max_req}")
-        prog = self._build(n_req)
-        self._programs[n_req] = prog
+        prog = self._build(n_req, parity)
+        self._programs[key] = prog
         return prog
 
-    def _build(self, n_req: int):
+    def _build(self, n_req: int, parity: int = 0):
         """Trunk (stem, each block's merged 1x1, final pool) plus, per
         Inception block, three concurrent lanes: the double-3x3 chain, the
         3x3 branch and the pool branch (``device.StagedProgram``)."""
@@ -525,6 +532,8 @@ class BNInceptionEncoder:
         # (channels padded to 8 in memory; no im2col round trip)
         cp = self.mod.cpad
         h2 = pool_out(h1, 3, 2, 0, True)
+        # stage 0 = the ops that read the gathered input self.x (the stem): the
+        # executor can release self.x to the next pass's compaction after it
         if self.stem_planes:
             # conv1 + bias + ReLU + pool1 in one kernel that feeds the raw padded
             # input rows to the tensor cores (csrc/gemm.cu MODE_STEM_POOL; flow
@@ -535,6 +544,9 @@ class BNInceptionEncoder:
             P.gemm(dv.plan_conv(self.x, n, size, size, cp, cp, 7, 7, 2, 3, self.w["conv1"], 64,
                                 self.b["conv1"], self.a_c1, ldd=64, BN=64, relu=True,
                                 tile=pick_conv_tile(n, h1, h1)))
+        SP.stage(P)
+        P = dv.Program()
+        if not self.stem_planes:
             P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
         P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
                              M=n * h2 * h2, K=64, BN=64, relu=True))
@@ -566,7 +578,7 @@ class BNInceptionEncoder:
             h = conv_out(h, 3, L["s"], 1) if L["s"] == 2 else h
             c = L["cout"]
             cur, nxt = nxt, cur
-        P.segment_mean(cur, n_req, self.S, h * h, c, self.out, FEAT_DIM)
+        P.segment_mean(cur, n_req, self.S, h * h, c, self.outs[parity], FEAT_DIM)
         SP.stage(P)
         return SP.seal()
 
@@ -598,8 +610,11 @@ class BNInceptionEncoder:
             Tq = self.tp[: pix_in * proj].view(pix_in, proj)
             segs.append((nm, nm + proj, Tq, proj, 0, dv.SEG_NO_RELU))
             nm += proj
+        bn_m = pick_bn(nm)
+        if os.environ.get("MS_DENSE_BN128") is not None and bn_m > 128:  # A/B: narrower tiles (OCC=2 eligible)
+            bn_m = -(-nm // -(-nm // 128) // 32) * 32
         P.gemm(dv.plan_dense(Xv, self.w[name + "/merged"], self.b[name + "/merged"], Yv, M=pix_in,
-                             K=cin, BN=pick_bn(nm), relu=True, segs=segs))
+                             K=cin, BN=bn_m, relu=True, segs=segs))
         tile_in = pick_conv_tile(n, h, h)
         tile_out = pick_conv_tile(n, o, o)
 
@@ -612,8 +627,10 @@ class BNInceptionEncoder:
             return (stride_ == 1 and 14 < h <= 30 and 128 % pitch == 0 and cin_ <= 64 and cout_ <= 128
                     and os.environ.get("MS_HALO28") is not None)
 
+        no_k32 = os.environ.get("MS_NO_K32") is not None  # A/B: 64-padded tap-box instead of K32
+
         def k32(cin_):  # matches the weight packing in _pack
-            return cin_ % 64 != 0 and cin_ % 32 == 0
+            return cin_ % 64 != 0 and cin_ % 32 == 0 and not no_k32
 
         def conv3(X_, cin_, cout_, stride_, wname, D_, ldd_, col0_, tile_):
             """3x3 conv plan: halo (+ CTA pair) where measured faster, else tap-box / K32."""
@@ -624,7 +641,8 @@ class BNInceptionEncoder:
                 p_ = dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, 1, 1, self._w64(wname), cout_, self.b[wname], D_,
                                   ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, halo=True)
                 return p_.set_pair(True)
-            return dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, stride_, 1, self.w[wname], cout_, self.b[wname], D_,
+            wt = self._w64(wname) if (no_k32 and cin_ % 64) else self.w[wname]
+            return dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, stride_, 1, wt, cout_, self.b[wname], D_,
                                 ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, tile=tile_, k32=k32(cin_))
 
         def halo_pair_ok(cin_, stride_):

@@ -77,11 +77,11 @@ class MaskedModel:
         K, n = self.K, max_req
         self.mask_d = torch.zeros(n, dtype=torch.int16, device=self.dev)
         self.slot_d = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
-        self.idx = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
-        self.inv = torch.zeros(K * n, dtype=torch.int32, device=self.dev)
-        self.counts = torch.zeros(K, dtype=torch.int32, device=self.dev)
-        self.offs = torch.zeros((1 << K) + 1, dtype=torch.int32, device=self.dev)
-        self.perm = torch.zeros(n, dtype=torch.int32, device=self.dev)
+        # compaction index outputs, one set per pass parity (pipelined passes:
+        # the next pass's compaction runs while this pass's head still reads inv)
+        self._ix = [tuple(torch.zeros(sz, dtype=torch.int32, device=self.dev)
+                          for sz in (K * n, K * n, K, (1 << K) + 1, n)) for _ in range(2)]
+        self.idx, self.inv, self.counts, self.offs, self.perm = self._ix[0]
         # pinned staging ring for stage_inputs: slot i is rewritten only after
         # the H2D copies that last read it have executed (its event)
         self._stage_h = [(torch.zeros(n, dtype=torch.int16).pin_memory(),
@@ -104,6 +104,13 @@ class MaskedModel:
         self._side = [torch.cuda.Stream() for _ in range(K)]
         self._ev_c = torch.cuda.Event()
         self._ev_k = [torch.cuda.Event() for _ in range(K)]
+        # pipelined device-formed passes (run_ring_pipelined; MS_PIPELINE=0: off, for A/B)
+        import os
+        self._pipeline = os.environ.get("MS_PIPELINE", "1") != "0"
+        self._parity = 0
+        self._cstream = torch.cuda.Stream()
+        self._ev_stem = [torch.cuda.Event() for _ in range(K)]
+        self._ev_cpar = [torch.cuda.Event() for _ in range(2)]
 
     @property
     def n_slots(self) -> int:
@@ -146,21 +153,21 @@ class MaskedModel:
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
                               self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
 
-    def _compact_ring(self, n: int, mask_ptr: int, bases):
+    def _compact_ring(self, n: int, mask_ptr: int, bases, parity: int = 0, stream=None):
         """Compaction of a pass whose masks are already on the device
         (``mask_ptr``), modality k's compacted rows read from the pool ring
-        at ``bases[k]`` (ms_compact_ring)."""
+        at ``bases[k]`` (ms_compact_ring), index outputs of ``parity``."""
         import ctypes
         L = dv.lib()
         rb = (ctypes.c_int32 * self.K)(*[int(b) for b in bases])
+        idx, inv, counts, offs, perm = self._ix[parity]
         dv.check(L.ms_compact_ring(mask_ptr, n, self.K, self._X, self._ROWS, rb, self.n_slots, self._G,
-                                   self.idx.data_ptr(), self.inv.data_ptr(), self.counts.data_ptr(),
-                                   self.offs.data_ptr(), self.perm.data_ptr(), dv.stream_ptr()),
-                 "ms_compact_ring")
+                                   idx.data_ptr(), inv.data_ptr(), counts.data_ptr(), offs.data_ptr(),
+                                   perm.data_ptr(), dv.stream_ptr(stream)), "ms_compact_ring")
 
-    def _head(self, n: int):
-        inv = self.inv[: self.K * n].view(self.K, n)
-        return self.head.program(n, [e.out for e in self.encoders], inv)
+    def _head(self, n: int, parity: int = 0):
+        inv = self._ix[parity][1][: self.K * n].view(self.K, n)
+        return self.head.program(n, [e.outs[parity] if hasattr(e, "outs") else e.out for e in self.encoders], inv)
 
     def _launch(self, n: int, counts):
         """All kernels of one pass for a staged batch of n requests, eagerly."""
@@ -180,6 +187,7 @@ class MaskedModel:
         g = self._graphs.get(key)
         if g is None:
             torch = self.torch
+            torch.cuda.synchronize()  # the warm run shares activation buffers with in-flight passes
             fn()  # warm: builds plans and tensor maps outside capture
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
@@ -213,11 +221,20 @@ class MaskedModel:
                 moved += c * self.row_bytes[k]
         return moved
 
-    def run_ring(self, n: int, counts, slot: int, bases):
+    @property
+    def pipelined(self) -> bool:
+        """Consecutive device-formed passes overlap (run_ring_pipelined)."""
+        return (self._pipeline and self.use_graphs and self.parallel_modalities
+                and all(getattr(e, "supports_parity", False) for e in self.encoders))
+
+    def run_ring(self, n: int, counts, slot: int, bases, upload_ev=None):
         """One pass formed on the device: masks in ``mask_ring[slot]``
         (written by ms_pass_select), pool rows from the per-modality rings
         at ``bases``; ``ring_ev[slot]`` marks the row free again."""
         ptr = self.mask_ring[slot].data_ptr()
+        if self.pipelined:
+            self.run_ring_pipelined(n, counts, slot, bases, ptr, upload_ev)
+            return
 
         def compact():
             self._compact_ring(n, ptr, bases)
@@ -225,6 +242,45 @@ class MaskedModel:
             self.ring_used[slot] = True
 
         self.run_staged(n, counts, compact=compact)
+
+    def run_ring_pipelined(self, n: int, counts, slot: int, bases, mask_ptr: int, upload_ev=None):
+        """Pass P+1 overlapping pass P.  Each modality's encoder always runs on
+        its own stream (so P+1's encoder k follows P's encoder k), split into
+        its stem graph (the only reader of the gathered input) and the rest;
+        P+1's compaction runs on the compaction stream as soon as every
+        modality's latest stem has consumed its input (and the pass's clips
+        are uploaded), with index outputs and encoder features double-buffered
+        by pass parity; only the fusion head runs on the calling stream, after
+        its pass's encoders.  So P+1's gather overlaps P's encoders and P+1's
+        encoders start while P's last layers and head still run."""
+        torch = self.torch
+        par = self._parity
+        self._parity ^= 1
+        main = torch.cuda.current_stream()
+        cs = self._cstream
+        for ev in self._ev_stem:  # every gathered input consumed by its stem
+            cs.wait_event(ev)
+        if upload_ev is not None:
+            cs.wait_event(upload_ev)
+        self._compact_ring(n, mask_ptr, bases, parity=par, stream=cs)
+        self._ev_cpar[par].record(cs)
+        self.ring_ev[slot].record(cs)
+        self.ring_used[slot] = True
+        present = [k for k, nk in enumerate(counts) if nk]
+        for k in present:
+            sp = self.encoders[k].program(counts[k], par)
+            ga = self._graph(("stem", k, counts[k], par), sp.first().run)
+            gb = self._graph(("rest", k, counts[k], par), sp.tail().run)
+            side = self._side[k]
+            side.wait_event(self._ev_cpar[par])
+            with torch.cuda.stream(side):
+                ga.replay()
+                self._ev_stem[k].record(side)
+                gb.replay()
+            self._ev_k[k].record(side)
+        for k in present:
+            main.wait_event(self._ev_k[k])
+        self._graph(("head", n, par), self._head(n, par).run).replay()
 
     def run_staged(self, n: int, counts, compact=None):
         """Compaction (direct launches), then one graph per present
@@ -263,14 +319,31 @@ class MaskedModel:
                 main.wait_event(self._ev_k[k])
         head.replay()
 
+    def ensure_warm(self, max_n: int | None = None):
+        """warm_graphs once per model (a graph captured lazily while passes are
+        in flight costs a device sync + capture: milliseconds of serving)."""
+        top = min(max_n or self.max_req, self.max_req)
+        if getattr(self, "_warm_top", 0) < top:
+            self.warm_graphs(top)
+
     def warm_graphs(self, max_n: int | None = None):
         """Capture every encoder/head graph up to ``max_n`` requests."""
         top = min(max_n or self.max_req, self.max_req)
+        self._warm_top = max(getattr(self, "_warm_top", 0), top)
         for k, enc in enumerate(self.encoders):
             for nk in range(1, top + 1):
                 self._graph(("enc", k, nk), enc.program(nk).run)
         for n in range(1, top + 1):
             self._graph(("head", n), self._head(n).run)
+        if self.pipelined:  # run_ring_pipelined's stem / rest / head graphs, both parities
+            for par in (0, 1):
+                for k, enc in enumerate(self.encoders):
+                    for nk in range(1, top + 1):
+                        sp = enc.program(nk, par)
+                        self._graph(("stem", k, nk, par), sp.first().run)
+                        self._graph(("rest", k, nk, par), sp.tail().run)
+                for n in range(1, top + 1):
+                    self._graph(("head", n, par), self._head(n, par).run)
         self.torch.cuda.synchronize()
 
     def forward(self, slots, masks):
