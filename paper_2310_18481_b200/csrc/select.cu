@@ -584,16 +584,20 @@ __device__ __forceinline__ void pad_store_lines(const unsigned char* __restrict_
         const int x0 = 2 * pq - pad_w;
         if (fast && c_src == 10 && plane_vecs > 0 && x0 >= 0 && x0 + 1 < width) {
           // flow interior: 2 pixels x 10 channels -> three planes of 2 x 4 (8, 9, 0, 0 in plane 2)
-          const unsigned char* q0 = lb + x0 * 10;
+          // 10 * x0 is even: the 20 source bytes are ten aligned 16-bit loads,
+          // each split into two magic floats by byte permutes
+          const unsigned short* q0 = reinterpret_cast<const unsigned short*>(lb + x0 * 10);
           uint32_t w[12];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const unsigned char* qq = q0 + 10 * h;
-            w[6 * h + 0] = u8x2_bf16(qq[0], qq[1], u8_scale, u8_bias2);
-            w[6 * h + 1] = u8x2_bf16(qq[2], qq[3], u8_scale, u8_bias2);
-            w[6 * h + 2] = u8x2_bf16(qq[4], qq[5], u8_scale, u8_bias2);
-            w[6 * h + 3] = u8x2_bf16(qq[6], qq[7], u8_scale, u8_bias2);
-            w[6 * h + 4] = u8x2_bf16(qq[8], qq[9], u8_scale, u8_bias2);
+#pragma unroll
+            for (int e = 0; e < 5; ++e) {
+              const uint32_t v = q0[5 * h + e];
+              const float f0 = fmaf(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)), u8_scale, u8_bias2);
+              const float f1 = fmaf(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)), u8_scale, u8_bias2);
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(f0, f1);
+              w[6 * h + e] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
             w[6 * h + 5] = 0u;
           }
           const long long pix = ((long long)j * dst_lines + s_dline[li]) * wd + 2 * pq;
@@ -927,72 +931,76 @@ __global__ void __launch_bounds__(kFusedThreads, 4) compact_fused_kernel(const _
     }
   }
 
-  // ---- units across modalities
-  long long ubase[kMaxK + 1];
-  ubase[0] = 0;
-  for (int k = 0; k < K; ++k) ubase[k + 1] = ubase[k] + (a.m[k].kind ? (long long)s_base[k] * a.m[k].chunks : 0);
-  const long long U = ubase[K];
-  uint4 pre[kFusedVecs];
+  // ---- units across modalities.  The per-modality descriptors and unit
+  // offsets live in shared memory (a dynamically indexed __grid_constant__
+  // field is a serialized constant-cache load; a local array spills).
+  __shared__ FusedMod s_m[kMaxK];
+  __shared__ long long s_ub[kMaxK + 1];
+  for (int w = t; w < K * (int)(sizeof(FusedMod) / 4); w += kFusedThreads)
+    reinterpret_cast<uint32_t*>(s_m)[w] = reinterpret_cast<const uint32_t*>(a.m)[w];
+  if (t == 0) {
+    s_ub[0] = 0;
+    for (int k = 0; k < K; ++k) s_ub[k + 1] = s_ub[k] + (a.m[k].kind ? (long long)s_base[k] * a.m[k].chunks : 0);
+  }
+  __syncthreads();
+  const long long U = s_ub[K];
+  uint4 pre0 = make_uint4(0, 0, 0, 0), pre1 = pre0, pre2 = pre0, pre3 = pre0;
+  static_assert(kFusedVecs == 4, "prefetch registers");
   int pre_n = 0;  // 16-B vectors prefetched into registers for the next unit
-  auto locate = [&](long long u, int& k, int& j, int& c) {
-    k = 0;
-    while (u >= ubase[k + 1]) ++k;
-    const long long local = u - ubase[k];
-    j = (int)(local / a.m[k].chunks);
-    c = (int)(local - (long long)j * a.m[k].chunks);
-  };
-  auto src_row = [&](int k, int j) -> long long {
-    const FusedMod& M = a.m[k];
-    if (a.n_ring > 0) return ((long long)M.ring_base + j) % a.n_ring;
-    const int r = s_idx[k][j];
-    return M.slot ? M.slot[r] : r;
-  };
-  auto prefetch = [&](long long u) {  // padded units only: their staged lines, into registers
-    pre_n = 0;
-    if (u >= U) return;
-    int k, j, c;
-    locate(u, k, j, c);
-    const FusedMod& M = a.m[k];
-    if (M.kind != 2) return;
-    const long long ln0 = (long long)c * M.per;
-    const int nl = (int)min((long long)M.per, M.lines - ln0);
-    const int nv = nl * M.line_bytes / 16;
-    const uint4* s4 = reinterpret_cast<const uint4*>(M.X + (src_row(k, j) * M.lines + ln0) * M.line_bytes);
-#pragma unroll
-    for (int q = 0; q < kFusedVecs; ++q) {
-      const int v = t + q * kFusedThreads;
-      if (v < nv) pre[q] = __ldcs(s4 + v);
-    }
-    pre_n = nv;
-  };
   long long u = blockIdx.x;
-  prefetch(u);
+#define MS_FUSED_LOCATE(u_, k_, j_, c_)                                    \
+  int k_ = 0;                                                              \
+  while ((u_) >= s_ub[k_ + 1]) ++k_;                                       \
+  const int j_ = (int)(((u_)-s_ub[k_]) / s_m[k_].chunks);                  \
+  const int c_ = (int)(((u_)-s_ub[k_]) - (long long)j_ * s_m[k_].chunks);
+#define MS_FUSED_SRC_ROW(k_, j_)                                                                  \
+  (a.n_ring > 0 ? ((long long)s_m[k_].ring_base + (j_)) % a.n_ring                               \
+                : (s_m[k_].slot ? (long long)s_m[k_].slot[s_idx[k_][j_]] : (long long)s_idx[k_][j_]))
+#define MS_FUSED_PREFETCH(u_)                                                                        \
+  do {                                                                                               \
+    pre_n = 0;                                                                                       \
+    if ((u_) < U) {                                                                                  \
+      MS_FUSED_LOCATE(u_, pk, pj, pc)                                                                \
+      const FusedMod& PM = s_m[pk];                                                                  \
+      if (PM.kind == 2) {                                                                            \
+        const long long pl0 = (long long)pc * PM.per;                                               \
+        const int pnl = (int)min((long long)PM.per, PM.lines - pl0);                                \
+        const int nv = pnl * PM.line_bytes / 16;                                                     \
+        const uint4* s4 = reinterpret_cast<const uint4*>(PM.X + (MS_FUSED_SRC_ROW(pk, pj) * PM.lines + pl0) * \
+                                                         PM.line_bytes);                             \
+        if (t < nv) pre0 = __ldcs(s4 + t);                                                           \
+        if (t + kFusedThreads < nv) pre1 = __ldcs(s4 + t + kFusedThreads);                           \
+        if (t + 2 * kFusedThreads < nv) pre2 = __ldcs(s4 + t + 2 * kFusedThreads);                   \
+        if (t + 3 * kFusedThreads < nv) pre3 = __ldcs(s4 + t + 3 * kFusedThreads);                   \
+        pre_n = nv;                                                                                  \
+      }                                                                                              \
+    }                                                                                                \
+  } while (0)
+  MS_FUSED_PREFETCH(u);
   for (; u < U; u += gridDim.x) {
-    int k, j, c;
-    locate(u, k, j, c);
-    const FusedMod& M = a.m[k];
+    MS_FUSED_LOCATE(u, k, j, c)
+    const FusedMod& M = s_m[k];
     if (M.kind == 1) {  // plain row copy: one chunk of 16-B vectors
       const long long v0 = (long long)c * M.per, v1 = min(M.row_vecs, v0 + M.per);
-      const uint4* s4 = reinterpret_cast<const uint4*>(M.X) + src_row(k, j) * M.row_vecs;
+      const uint4* s4 = reinterpret_cast<const uint4*>(M.X) + MS_FUSED_SRC_ROW(k, j) * M.row_vecs;
       uint4* d4 = reinterpret_cast<uint4*>(M.G) + (long long)j * M.row_vecs;
       for (long long v = v0 + t; v < v1; v += kFusedThreads) d4[v] = __ldcs(s4 + v);
-      prefetch(u + gridDim.x);
+      MS_FUSED_PREFETCH(u + gridDim.x);
       continue;
     }
     const long long ln0 = (long long)c * M.per;
     const int nl = (int)min((long long)M.per, M.lines - ln0);
     __syncthreads();  // the previous unit's stores have read line_buf
-#pragma unroll
-    for (int q = 0; q < kFusedVecs; ++q) {
-      const int v = t + q * kFusedThreads;
-      if (v < pre_n) reinterpret_cast<uint4*>(line_buf)[v] = pre[q];
-    }
+    if (t < pre_n) reinterpret_cast<uint4*>(line_buf)[t] = pre0;
+    if (t + kFusedThreads < pre_n) reinterpret_cast<uint4*>(line_buf)[t + kFusedThreads] = pre1;
+    if (t + 2 * kFusedThreads < pre_n) reinterpret_cast<uint4*>(line_buf)[t + 2 * kFusedThreads] = pre2;
+    if (t + 3 * kFusedThreads < pre_n) reinterpret_cast<uint4*>(line_buf)[t + 3 * kFusedThreads] = pre3;
     if (t < nl) {
       const long long ln = ln0 + t;
       s_dline[t] = M.frame_h > 0 ? (ln / M.frame_h) * (M.frame_h + 2LL * M.pad_h) + M.pad_h + ln % M.frame_h : ln;
     }
     __syncthreads();
-    prefetch(u + gridDim.x);  // next unit's loads in flight behind this unit's stores
+    MS_FUSED_PREFETCH(u + gridDim.x);  // next unit's loads in flight behind this unit's stores
     const int wd = M.width + 2 * M.pad_w;
     if (M.c_dst % 8 != 0) {
       const int gv = M.c_dst / 4;
@@ -1012,6 +1020,9 @@ __global__ void __launch_bounds__(kFusedThreads, 4) compact_fused_kernel(const _
                                   M.plane_vecs, j, M.dst_lines, M.G, 0.0f);
     }
   }
+#undef MS_FUSED_PREFETCH
+#undef MS_FUSED_SRC_ROW
+#undef MS_FUSED_LOCATE
 }
 
 static int gather_pad_launch(const void* src, long long lines, int width, int c_src, int c_dst, int pad_w,
