@@ -433,6 +433,116 @@ def compaction_roofline(model, peak_gbs, n):
             "kernel": "compact_fused_kernel (index + every modality's gather, one persistent launch)"}
 
 
+def c5_arm(args):
+    """configs[4]: 4-modality synthetic sweep -- batch 1..1024, masks over all
+    15 modality subsets -- of the HBM-bound hot-path kernels against the
+    measured HBM peak: the policy step (ms_policy_select, C = 16 candidates),
+    compaction (ms_compact: index + 4 gathers of TBN-clip-sized bf16 rows) and
+    the fusion head (gather-concat FC1 + FC2).  Each point: CUDA-graph timed,
+    median of --steps replays after --warmup.  value = the compaction's
+    fraction of HBM at the largest batch (the kernel with real bytes to move).
+    Runs on rank 0 (replicas only: the other ranks exit)."""
+    import ctypes
+
+    import torch
+    world, rank, local = _dist()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    from paper_2310_18481_b200 import build
+    build.build()
+    from paper_2310_18481_b200 import device as dv
+    from paper_2310_18481_b200.encoders import FEAT_DIM, FusionHead
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    K, C = 4, 16
+    Ns = [1, 4, 16, 64, 256, 1024]
+    L = dv.lib()
+    e0, e1 = dv.Event(), dv.Event()
+
+    def timed(fn, inner=10):
+        for _ in range(max(3, args.warmup)):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(inner):
+                    fn()
+        torch.cuda.current_stream().wait_stream(st)
+        g.replay()
+        ts = []
+        for _ in range(max(3, args.steps)):
+            e0.record()
+            g.replay()
+            e1.record()
+            ts.append(e0.elapsed_us(e1) / inner)
+        return float(np.median(ts))
+
+    rng = np.random.default_rng(0)
+    out = {"policy": [], "compaction": [], "fusion": []}
+    for n in Ns:
+        lat = np.sort(rng.integers(1_000, 200_000, size=(n, C)), axis=1).astype(np.int64) + np.arange(C)
+        lat_d = torch.as_tensor(lat).cuda()
+        nc = torch.full((n,), C, dtype=torch.int32, device="cuda")
+        dl = torch.as_tensor(rng.integers(0, 300_000, size=n).astype(np.int64)).cuda()
+        ch = torch.empty(n, dtype=torch.int32, device="cuda")
+        us = timed(lambda: L.ms_policy_select(lat_d.data_ptr(), None, nc.data_ptr(), C, dl.data_ptr(), 0, 1.0, n,
+                                              ch.data_ptr(), dv.stream_ptr()))
+        b = n * (12 * C + 16)
+        out["policy"].append({"n": n, "us": round(us, 2), "bytes": b, "frac": round(b / us / 1e3 / peak, 4)})
+    row = 3 * 224 * 224 * 3  # one TBN rgb clip of bf16 per (request, modality)
+    slots = 1024
+    pools = [torch.randn(slots, row, device="cuda").to(torch.bfloat16) for _ in range(K)]
+    dst = [torch.empty(slots, row, dtype=torch.bfloat16, device="cuda") for _ in range(K)]
+    X = (ctypes.c_void_p * K)(*[p_.data_ptr() for p_ in pools])
+    G = (ctypes.c_void_p * K)(*[d.data_ptr() for d in dst])
+    rows = (dv.RowDesc * K)(*[dv.RowDesc(1, 1, row, row, 0) for _ in range(K)])
+    idx = torch.empty(K * slots, dtype=torch.int32, device="cuda")
+    inv = torch.empty(K * slots, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(K, dtype=torch.int32, device="cuda")
+    offs = torch.empty((1 << K) + 1, dtype=torch.int32, device="cuda")
+    perm = torch.empty(slots, dtype=torch.int32, device="cuda")
+    for n in Ns:
+        masks = (np.arange(n) % 15 + 1).astype(np.int16)
+        m_d = torch.as_tensor(rng.permutation(masks)).cuda()
+        sl = torch.as_tensor(rng.integers(0, slots, size=n).astype(np.int32)).cuda()
+        us = timed(lambda: L.ms_compact(m_d.data_ptr(), n, K, X, rows, sl.data_ptr(), G, idx.data_ptr(),
+                                        inv.data_ptr(), cnt.data_ptr(), offs.data_ptr(), perm.data_ptr(),
+                                        dv.stream_ptr()))
+        present = sum(int(((masks.astype(np.int64) >> k) & 1).sum()) for k in range(K))
+        b = present * row * 2 * 2 + 2 * n + 4 * present
+        out["compaction"].append({"n": n, "us": round(us, 2), "bytes": b, "frac": round(b / us / 1e3 / peak, 4)})
+    del pools, dst
+    torch.cuda.empty_cache()
+    head = FusionHead(K, max(Ns), 499, FEAT_DIM)
+    feats = [torch.randn(max(Ns), FEAT_DIM, device="cuda").to(torch.bfloat16) for _ in range(K)]
+    wbytes = head.w1.numel() * 2 + head.w2.numel() * 2 + (head.b1.numel() + head.b2.numel()) * 4
+    for n in Ns:
+        masks = np.arange(n) % 15 + 1
+        iv = torch.full((K, n), -1, dtype=torch.int32)
+        for k in range(K):
+            sel = np.flatnonzero((masks >> k) & 1)
+            iv[k, sel] = torch.arange(len(sel), dtype=torch.int32)
+        prog = head.program(n, feats, iv.cuda())
+        us = timed(prog.run)
+        present = sum(int(((masks >> k) & 1).sum()) for k in range(K))
+        b = present * FEAT_DIM * 2 + n * head.n_classes * 4 + wbytes
+        out["fusion"].append({"n": n, "us": round(us, 2), "bytes": b, "frac": round(b / us / 1e3 / peak, 4),
+                              "tflops": round(head.flops(n) / us / 1e6, 1)})
+    top = out["compaction"][-1]
+    line = {"metric": "configs[4] HBM fraction of the hot-path kernels (compaction at the largest batch)",
+            "value": top["frac"], "unit": "fraction of measured HBM peak", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(top["us"] / 1000.0, 4), "higher_is_better": True,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "configs[4]: 4-modality synthetic sweep, batch 1..1024, all 15 modality subsets",
+                       "batches": Ns, "candidates": C, "clip_row_bytes": row * 2, "peak_gbs": peak},
+            "policy": out["policy"], "compaction": out["compaction"], "fusion": out["fusion"]}
+    print(json.dumps(line), flush=True)
+
+
 def our_arm(args):
     import torch
     world, rank, local = _dist()
@@ -697,8 +807,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="tbn", choices=["tbn", "vqa", "mlp"],
-                    help="tbn = configs[1] (the headline); vqa = configs[2]; mlp = configs[0]")
+    ap.add_argument("--workload", default="tbn", choices=["tbn", "vqa", "mlp", "c5"],
+                    help="tbn = configs[1] (the headline); vqa = configs[2]; mlp = configs[0]; "
+                         "c5 = configs[4] (HBM-bound kernel sweep, K = 4)")
     ap.add_argument("--window-s", type=float, default=1.0)
     ap.add_argument("--search-seconds", type=float, default=2.0, help="window per arrival draw in the rate search")
     ap.add_argument("--deadline-ms", type=float, default=15.0,
@@ -733,6 +844,8 @@ def main():
                       mults=MULTS if args.budgets == "varying" else None)
     if args.impl == "reference":
         reference_arm(args)
+    elif args.workload == "c5":
+        c5_arm(args)
     else:
         our_arm(args)
 

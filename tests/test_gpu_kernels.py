@@ -901,3 +901,43 @@ def test_conv_halo_pair_vs_torch(dev, n, H, Cin, Cout):
     ok, err, scale = _close(D[:, col0:col0 + Cout].cpu(), ref)
     assert ok, (err, scale)
     assert torch.all(D[:, :col0] == 3.0) and torch.all(D[:, col0 + Cout:] == 3.0)
+
+
+@pytest.mark.parametrize("N", [1, 37, 256, 1024])
+def test_fusion_head_k4_vs_oracle(dev, N):
+    """configs[4]'s fusion stage at K = 4 modalities: the device head
+    (gather-concat FC1 + ReLU, FC2 -> fp32 logits, split-K with the
+    deterministic finalize) over masks covering all 15 subsets, absent
+    modalities dropped exactly as the reference drops them (profile.py:157-159:
+    zero K blocks), vs the CPU oracle's fusion_forward; rows in request order."""
+    from oracle.forward import fusion_forward, fusion_weights as oracle_fusion_weights
+    from paper_2310_18481_b200.encoders import FEAT_DIM, FusionHead
+    K = 4
+    g = torch.Generator().manual_seed(400 + N)
+    masks = torch.arange(N) % 15 + 1  # every subset, cycled
+    masks = masks[torch.randperm(N, generator=g)]
+    head = FusionHead(K, 1024, 499, FEAT_DIM)
+    full = [_bf(torch.randn(N, FEAT_DIM, generator=g)) for _ in range(K)]
+    feats, invs = [], []
+    for k in range(K):
+        have = ((masks >> k) & 1).bool()
+        nk = int(have.sum())
+        f = torch.zeros(1024, FEAT_DIM, dtype=torch.bfloat16)
+        f[:nk] = full[k][have].to(torch.bfloat16)
+        inv = torch.full((N,), -1, dtype=torch.int32)
+        inv[have] = torch.arange(nk, dtype=torch.int32)
+        feats.append(f.cuda())
+        invs.append(inv)
+    inv = torch.stack(invs).cuda()
+    prog = head.program(N, feats, inv)
+    prog.run()
+    torch.cuda.synchronize()
+    got = head.logits[:N].cpu()
+    w = oracle_fusion_weights(K, FEAT_DIM, 499)
+    ref = fusion_forward([f.float() for f in full], masks, w)
+    ok, err, scale = _close(got, ref)
+    assert ok, (err, scale)
+    assert (got.argmax(1) == ref.argmax(1)).float().mean().item() >= 0.999
+    prog.run()  # deterministic split-K: bitwise identical on a rerun
+    torch.cuda.synchronize()
+    assert torch.equal(head.logits[:N].cpu(), got)
