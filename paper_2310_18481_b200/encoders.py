@@ -610,11 +610,10 @@ class BNInceptionEncoder:
             Tq = self.tp[: pix_in * proj].view(pix_in, proj)
             segs.append((nm, nm + proj, Tq, proj, 0, dv.SEG_NO_RELU))
             nm += proj
-        bn_m = pick_bn(nm)
-        if os.environ.get("MS_DENSE_BN128") is not None and bn_m > 128:  # A/B: narrower tiles (OCC=2 eligible)
-            bn_m = -(-nm // -(-nm // 128) // 32) * 32
+        # (narrower N tiles that would let the wide merged GEMMs run two CTAs per
+        # SM measured slower: 128-wide +3.8 %, <= 224-wide +2 % pass time)
         P.gemm(dv.plan_dense(Xv, self.w[name + "/merged"], self.b[name + "/merged"], Yv, M=pix_in,
-                             K=cin, BN=bn_m, relu=True, segs=segs))
+                             K=cin, BN=pick_bn(nm), relu=True, segs=segs))
         tile_in = pick_conv_tile(n, h, h)
         tile_out = pick_conv_tile(n, o, o)
 
