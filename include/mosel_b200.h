@@ -255,6 +255,13 @@ int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in
  * by ms_pool (same accumulation order); the unpooled map never reaches HBM. */
 int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
                            const void* Wt, int Cout, const float* bias, void* Y, long long ldy, int y_col0);
+/* Fuse a 1x1 conv (64 -> 64, + bias + ReLU; BN-Inception's conv2_red) into a
+ * stem plan (output width <= 112): the pooled rows become the A operand of a
+ * second tcgen05 MMA in the same kernel and Y receives the 1x1's output
+ * (rows of ldy at y_col0); the pooled map itself is not stored.  Wred: the
+ * [64 out, 64 in] bf16 weights pre-swizzled to the SW128 K-major layout
+ * (encoders.pack_sw128_weight). */
+int ms_gemm_plan_stem_set_reduce(void* plan, const void* Wred, const float* bias, void* Y, long long ldy, int y_col0);
 int ms_gemm_plan_gather(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                         int feat_dim, int M, const void* W, int N, int BN, const float* bias, int relu,
                         int out_fp32, void* D, long long ldd, int col0);

@@ -875,7 +875,11 @@ constexpr int kStemRowBuf = 128 * 128;     // <= 128 conv pixels x 64 ch bf16
 #endif
 constexpr int kStemEpiWarps = STEM_EPI_WARPS;  // 2 per TMEM lane quarter, 32 channels each (8: 1.1x over 16 for rgb -- fewer warps competing with the MMA warp for issue slots)
 constexpr int kStemCh = 64 / (kStemEpiWarps / 4);
-constexpr int kStemThreads = 64 + 32 * kStemEpiWarps;
+// + one warp issuing the fused 1x1 conv (conv2_red) on the pooled rows (p.red_w)
+constexpr int kStemThreads = 64 + 32 * kStemEpiWarps + 32;
+constexpr int kStemRedWarp = 2 + kStemEpiWarps;
+constexpr int kStemRedA = 128 * 128;     // one pooled row as the 1x1's A operand (SW128, 128 rows)
+constexpr int kStemRedW = 64 * 128;      // the 1x1's 64 x 64 weights (SW128, pre-swizzled)
 template <int N>
 __device__ __forceinline__ void stem_tmem_ld(uint32_t taddr, uint32_t (&r)[N]) {
   if constexpr (N == 16)
@@ -928,13 +932,23 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   constexpr int kWBytes = kPlanes == 1 ? kStemWBytes : kStemKH * kPlanes * kStemWBlk;
   uint8_t* smA = smW + kWBytes;
   uint8_t* rbuf = smA + stages * a_stride + 256;  // + slack: rows >= OW of the last tap read past a stage
-  uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + (kOverlap ? 0 : kStemRowBuf));
+  // fused 1x1 (red): two pooled-row A tiles + its weights, 1024-B aligned
+  uint8_t* redA = smem + (((rbuf + (kOverlap ? 0 : kStemRowBuf)) - smem + 1023) & ~1023);
+  uint8_t* redW = redA + 2 * kStemRedA;
+  const bool red = kOverlap && p.red_w != nullptr;
+  uint64_t* full = reinterpret_cast<uint64_t*>(red ? redW + kStemRedW : rbuf + (kOverlap ? 0 : kStemRowBuf));
   uint64_t* empty = full + stages;
   uint64_t* wbar = empty + stages;
   uint64_t* tfull = wbar + 1;
   uint64_t* tempty = tfull + kStemSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kStemSlots);
+  uint64_t* a_full = tempty + kStemSlots;  // red: pooled row b written (epilogue warps)
+  uint64_t* r_full = a_full + 2;           // red: 1x1 of row b done (commit)
+  uint64_t* r_empty = r_full + 2;          // red: TMEM result b drained (epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_empty + 2);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+  float* sbias_red = sbias + 64;
+  // TMEM: conv slots of 128 columns (4, or 3 with the fused 1x1) + 2 x 64 for the 1x1
+  const int slots = red ? 3 : kStemSlots;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int OH = p.OH, OW = p.OW, PH = p.PH, PW = p.PW;
@@ -950,19 +964,26 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], kStemEpiWarps);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], kStemEpiWarps);
+      mbar_init(&r_full[b], 1);
+      mbar_init(&r_empty[b], kStemEpiWarps);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x < 64) sbias[threadIdx.x] = p.bias ? p.bias[threadIdx.x] : 0.0f;
+  if (threadIdx.x < 64) sbias_red[threadIdx.x] = (red && p.red_bias) ? p.red_bias[threadIdx.x] : 0.0f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
   if (warp == 0 && lane == 0) {  // weights are constants: load them before waiting on the producer grid
-    mbar_arrive_expect_tx(wbar, kWBytes);
+    mbar_arrive_expect_tx(wbar, kWBytes + (red ? kStemRedW : 0));
     for (int o = 0; o < kWBytes; o += 8192)
       bulk_load(smem_addr(smW + o), p.wraw + o, min(8192, kWBytes - o), wbar);
+    if (red) bulk_load(smem_addr(redW), p.red_w, kStemRedW, wbar);
   }
   pdl_wait();
 
@@ -1004,9 +1025,9 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     int s = 0, k = 0;
     uint32_t phase = 0;
     for (; w.valid(); w.next(), ++k) {
-      const int slot = k & (kStemSlots - 1);
+      const int slot = k % slots;
       const int n = w.nrows();
-      mbar_wait(&tempty[slot], (uint32_t)(((k / kStemSlots) & 1) ^ 1));
+      mbar_wait(&tempty[slot], (uint32_t)(((k / slots) & 1) ^ 1));
       mbar_wait(&full[s], phase);
       tc_fence_after();
       if (lane == 0) trace(k, 0);
@@ -1049,6 +1070,26 @@ __global__ void __launch_bounds__(kStemThreads, 1)
         phase ^= 1;
       }
     }
+  } else if (warp == kStemRedWarp) {  // ----------------- fused 1x1 (conv2_red) issuer
+    if (red) {
+      const uint32_t idesc = umma_idesc_bf16_m128(64);
+      const uint64_t bdesc = umma_desc_sw128(smem_addr(redW));
+      mbar_wait(wbar, 0);
+      int kc = 0;  // CLOSE tiles
+      for (; w.valid(); w.next()) {
+        if (w.open) continue;
+        const int b = kc & 1;
+        mbar_wait(&a_full[b], (uint32_t)((kc >> 1) & 1));        // pooled row written
+        mbar_wait(&r_empty[b], (uint32_t)(((kc >> 1) & 1) ^ 1));  // result b drained
+        tc_fence_after();
+        const uint64_t adesc = umma_desc_sw128(smem_addr(redA + b * kStemRedA));
+        const uint32_t d = tmem_base + (uint32_t)(slots * 128 + 64 * b);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_bf16_elect(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, kk != 0);
+        umma_commit_elect(&r_full[b]);
+        ++kc;
+      }
+    }
   } else if constexpr (kOverlap) {  // ------------- epilogue warps (overlapping row groups)
     const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, kStemCh-channel chunk
     const int x = 7 * (lane >> 3) + (lane & 7);   // this lane's conv pixel within the warp's 29
@@ -1061,10 +1102,41 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     const uint32_t t_lane = tmem_base + (uint32_t)(c * kStemCh) + ((uint32_t)(q * 32) << 16);
     const float* bch = sbias + c * kStemCh;
     uint32_t carry[kStemCh / 2];  // conv row 2i of the open pooled row, bf16(acc + bias), per pixel
+    // fused 1x1: the pooled row of CLOSE tile kc goes to redA[kc & 1]; its 1x1
+    // result is drained (bias, ReLU, bf16 -> p.red_y) while the next tile runs
+    int kc = 0, prev_img = 0, prev_i = 0;
+    const Seg& R = p.seg[1];
+    auto drain = [&](int kd, int img_, int i_) {
+      const int b = kd & 1;
+      mbar_wait(&r_full[b], (uint32_t)((kd >> 1) & 1));
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(slots * 128 + 64 * b + 32 * c), v);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_empty[b]);
+      const int px = 32 * q + lane;  // pooled pixel = TMEM lane
+      if (px < PW) {
+        __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(R.ptr) +
+                            (((long long)img_ * PH + i_) * PW + px) * R.ldd + R.col0 + 32 * c;
+        const float* br = sbias_red + 32 * c;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t o[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int e = 8 * g + 2 * t;
+            o[t] = pack_bf16x2(fmaxf(__uint_as_float(v[e]) + br[e], 0.0f), fmaxf(__uint_as_float(v[e + 1]) + br[e + 1], 0.0f));
+          }
+          *reinterpret_cast<uint4*>(yr + 8 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    };
     for (int k = 0; w.valid(); w.next(), ++k) {
-      const int slot = k & (kStemSlots - 1);
+      const int slot = k % slots;
       const int n = w.nrows();
-      mbar_wait(&tfull[slot], (uint32_t)((k / kStemSlots) & 1));
+      mbar_wait(&tfull[slot], (uint32_t)((k / slots) & 1));
       tc_fence_after();
       if (warp == 2 && lane == 0) trace(k, 2);
       uint32_t v0[kStemCh], v1[kStemCh];
@@ -1085,6 +1157,9 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       // horizontal 3-max across lanes; row 2i+2 opens pooled row i+1
       __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(Y.ptr) +
                          (((long long)w.img * PH + w.i) * PW + 14 * q + jj) * Y.ldd + Y.col0 + c * kStemCh;
+      const int pp = 14 * q + jj;  // pooled pixel = the 1x1's A row
+      uint8_t* arow = redA + (kc & 1) * kStemRedA + pp * 128;
+      if (red && kc >= 1) drain(kc - 1, prev_img, prev_i);  // frees redA[kc & 1] (the 1x1 of kc - 2 read it)
 #pragma unroll
       for (int g = 0; g < kStemCh / 8; ++g) {
         uint32_t o[4];
@@ -1105,10 +1180,24 @@ __global__ void __launch_bounds__(kStemThreads, 1)
           if (three) h = bf16x2_max(h, m2);
           o[t] = bf16x2_max(h, 0u);  // ReLU
         }
-        if (owner) *reinterpret_cast<uint4*>(y + 8 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+        if (owner) {
+          if (red)
+            *reinterpret_cast<uint4*>(arow + (((c * (kStemCh / 8) + g) ^ (pp & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+          else
+            *reinterpret_cast<uint4*>(y + 8 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      if (red) {  // this tile's pooled row -> the 1x1 issuer
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[kc & 1]);
+        prev_img = w.img;
+        prev_i = w.i;
+        ++kc;
       }
       if (warp == 2 && lane == 0) trace(k, 3);
     }
+    if (red && kc >= 1) drain(kc - 1, prev_img, prev_i);
   } else {  // ----------------------------- epilogue warps (linear rows, smem horizontal pool)
     const int q = warp & 3, c = (warp - 2) >> 2;  // TMEM lane quarter, kStemCh-channel chunk
     const int ow = q * 32 + lane;
@@ -1119,9 +1208,9 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     const float* bch = sbias + c * kStemCh;
     uint32_t carry[kStemCh / 2];
     for (int k = 0; w.valid(); w.next(), ++k) {
-      const int slot = k & (kStemSlots - 1);
+      const int slot = k % slots;
       const int n = w.nrows();
-      mbar_wait(&tfull[slot], (uint32_t)((k / kStemSlots) & 1));
+      mbar_wait(&tfull[slot], (uint32_t)((k / slots) & 1));
       tc_fence_after();
       uint32_t v0[kStemCh], v1[kStemCh];
       // OPEN: row 2i is the pair's second row (columns 64..127)
@@ -1854,6 +1943,32 @@ int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in
   P->grid_x = p.units < sm_count() ? p.units : sm_count();
   P->grid_y = 1;
   P->tmem_cols = 512;
+  return MS_OK;
+}
+
+int ms_gemm_plan_stem_set_reduce(void* plan, const void* Wred, const float* bias, void* Y, long long ldy, int y_col0) {
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  if (P == nullptr || Wred == nullptr || Y == nullptr) return set_error(MS_ERR_INVALID, "null pointer");
+  GemmParams& p = P->p;
+  if (p.mode != MODE_STEM_POOL || p.OW > 112)
+    return set_error(MS_ERR_INVALID, "stem reduce: needs a stem_pool plan with output width <= 112");
+  if ((reinterpret_cast<uintptr_t>(Wred) & 15) != 0 || (reinterpret_cast<uintptr_t>(Y) & 15) != 0 || ldy % 8 != 0 ||
+      y_col0 % 8 != 0)
+    return set_error(MS_ERR_INVALID, "stem reduce: weights and output rows must be 16-B aligned");
+  p.red_w = reinterpret_cast<const uint8_t*>(Wred);
+  p.red_bias = bias;
+  p.seg[1] = Seg{0, 64, Y, ldy, y_col0, 0};
+  // shared memory: + two pooled-row A tiles + the 1x1 weights (1 KB aligned) + barriers
+  const int w_bytes = p.planes == 1 ? kStemWBytes : kStemKH * p.planes * kStemWBlk;
+  const int extra = 1024 + 2 * kStemRedA + kStemRedW + 6 * 8 + 256;
+  int stages = p.stages;
+  while (stages > 1 && 1024 + w_bytes + 256 + stages * p.b_bytes + extra + (2 * stages + 1 + 2 * kStemSlots) * 8 +
+                            16 + 512 > 227 * 1024)
+    --stages;
+  const int bytes = 1024 + w_bytes + 256 + stages * p.b_bytes + extra + (2 * stages + 1 + 2 * kStemSlots) * 8 + 16 + 512;
+  if (stages < 2 || bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "stem reduce: does not fit in shared memory");
+  p.stages = stages;
+  P->smem_bytes = bytes;
   return MS_OK;
 }
 

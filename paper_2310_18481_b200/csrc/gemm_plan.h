@@ -121,6 +121,8 @@ struct GemmParams {
   const uint8_t* wraw;  // MODE_STEM_POOL: row-pair weights (encoders.pack_stem_weight)
   long long x_plane;    // MODE_STEM_POOL with planes: bytes between 4-channel input planes
   int planes, plane_bytes;
+  const uint8_t* red_w;   // MODE_STEM_POOL: fused 1x1 (64 -> 64) on the pooled rows, SW128 pre-swizzled weights
+  const float* red_bias;  //   its bias; output = seg[1] (the pooled map itself is then not stored)
   long long x_pitch;   // bytes of one padded input row
   int Hp, PH, PW, units;
 };

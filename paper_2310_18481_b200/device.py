@@ -93,6 +93,7 @@ _SIGS = {
     "ms_gemm_plan_conv_halo": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _I, _P, _I, _P, _LL, _I, _I, _P], C.c_int),
     "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _I, _LL, _P, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_conv_pool": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _P, _P, _LL, _I], C.c_int),
+    "ms_gemm_plan_stem_set_reduce": ([_P, _P, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -435,6 +436,18 @@ def plan_stem_pool(X, n_img, H, W_in, KH, pad, Wt, bias, Y, *, ldy, col0=0, plan
     ow = (W_in + 2 * pad - KH) // 2 + 1
     p.flops = 2 * n_img * oh * ow * 64 * KH * KH * 4 * planes
     p.label = f"stem conv {KH}x{KH}/2 {4 * planes}->64 {n_img}x{oh}x{ow} + maxpool"
+    return p
+
+
+def stem_set_reduce(p, Wred, bias, Y, *, ldy, col0=0):
+    """Fuse the 64 -> 64 1x1 conv (+ bias + ReLU) into stem plan ``p``
+    (``ms_gemm_plan_stem_set_reduce``); ``Wred`` from
+    ``encoders.pack_sw128_weight``.  The plan then writes Y instead of the
+    pooled map."""
+    check(lib().ms_gemm_plan_stem_set_reduce(p.addr, ptr(Wred), ptr(bias), ptr(Y), ldy, col0),
+          "ms_gemm_plan_stem_set_reduce")
+    p.keep += [Wred, bias, Y]
+    p.label += " + 1x1 64->64"
     return p
 
 

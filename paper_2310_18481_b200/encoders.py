@@ -330,6 +330,21 @@ def pack_dense_weight(w):
     return out.contiguous()
 
 
+def pack_sw128_weight(w):
+    """[N, 64] bf16 K-major -> the same bytes in the UMMA SW128 K-major layout
+    (16-B chunk j of row n at chunk j ^ (n & 7)), so one linear bulk copy puts
+    the weights in shared memory ready as a B operand (the stem's fused 1x1)."""
+    import torch
+    w = w.reshape(w.shape[0], -1).to(torch.bfloat16)
+    assert w.shape[1] == 64, "one 128-B swizzle row per output channel"
+    n = w.shape[0]
+    chunks = w.reshape(n, 8, 8)
+    out = torch.empty_like(chunks)
+    for r in range(n):
+        out[r, [(j ^ (r & 7)) for j in range(8)]] = chunks[r]
+    return out.reshape(n, 64).contiguous()
+
+
 def pick_bn(n: int, m_tiles: int | None = None, target_ctas: int = 96) -> int:
     """Tile width for N output columns: one tile when N <= 256, else the
     fewest equal-ish tiles (multiples of 32).  With ``m_tiles`` given and too
@@ -393,6 +408,9 @@ class BNInceptionEncoder:
         self.fused_stem = os.environ.get("MS_NO_FUSED_STEM") is None
         # conv2 + pool2 as one kernel (MS_NO_FUSED_POOL2=1: the conv + pool pair, for A/B)
         self.fused_pool2 = os.environ.get("MS_NO_FUSED_POOL2") is None
+        # conv2_red fused into the stem (overlapping-row stems, output width <= 112;
+        # MS_NO_STEM_RED=1: the separate 1x1 GEMM, for A/B)
+        self.stem_red_env = os.environ.get("MS_NO_STEM_RED") is None
         self._pack()
         self._alloc()
         self._programs = {}
@@ -416,6 +434,8 @@ class BNInceptionEncoder:
                     self.w["stem"] = pack_stem_weight_planes(w).to(d)
             elif w.shape[-1] == 1:
                 self.w[name] = pack_dense_weight(w.reshape(w.shape[0], -1)).to(d)
+                if name == "conv2_red":
+                    self.w["conv2_red_sw"] = pack_sw128_weight(w.reshape(w.shape[0], -1)).to(d)
             elif w.shape[1] % 64 and w.shape[1] % 32 == 0:
                 # 96/160/224 input channels: K = 9*C without per-tap padding
                 # (MODE_CONV_K32, 1.04-1.14x, profiles/r01_k32_bench.txt)
@@ -500,6 +520,7 @@ class BNInceptionEncoder:
         elif self.fused_stem and cp == 12 and h1 <= 112:
             self.stem_planes = 3
         self.x_plane_stride = n_img * (size + 2 * rp) * (size + 2 * CONV1_PAD) * 4 if self.stem_planes == 3 else 0
+        self.stem_red = bool(self.stem_planes) and self.stem_red_env and h1 <= 112
 
     # features of pass parity p land in outs[p]: with passes pipelined the next
     # pass's encoder may finish before the previous pass's fusion head has read
@@ -548,8 +569,15 @@ class BNInceptionEncoder:
         P = dv.Program()
         if not self.stem_planes:
             P.pool(self.a_c1, n, h1, h1, 64, 64, 3, 2, 0, True, True, self.a_p1, 64, 0)
-        P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
-                             M=n * h2 * h2, K=64, BN=64, relu=True))
+        if self.stem_red:
+            # conv2_red (1x1 64->64) fused into the stem: the pooled rows are the
+            # A operand of a second MMA in the stem kernel (pool1's map never stored)
+            dv.stem_set_reduce(SP.stages[0][0].ops[0][1], self.w["conv2_red_sw"], self.b["conv2_red"],
+                               self.a_c2r, ldy=64)
+            SP.stages[0][0].ops[0][1].flops += 2 * n * h2 * h2 * 64 * 64
+        else:
+            P.gemm(dv.plan_dense(self.a_p1, self.w["conv2_red"], self.b["conv2_red"], self.a_c2r,
+                                 M=n * h2 * h2, K=64, BN=64, relu=True))
         # conv2 (56x56 rgb/flow): halo reuse measured 1.08-1.09x faster than the
         # tap-box 2-SM kernel (tools/halo_bench.py); narrower layers lose more to
         # the ceil8(W+2)-wide tiles than they gain, audio's 64+2 does not tile 128

@@ -941,3 +941,49 @@ def test_fusion_head_k4_vs_oracle(dev, N):
     prog.run()  # deterministic split-K: bitwise identical on a rerun
     torch.cuda.synchronize()
     assert torch.equal(head.logits[:N].cpu(), got)
+
+
+@pytest.mark.parametrize("n,H,Cin,planes", [(2, 32, 3, 1), (3, 224, 3, 1), (1, 30, 3, 1), (2, 224, 10, 3),
+                                            (3, 64, 10, 3)])
+def test_stem_fused_1x1_bitwise_vs_stem_then_dense(dev, n, H, Cin, planes):
+    """The stem with conv2_red fused (ms_gemm_plan_stem_set_reduce: the pooled
+    rows become the A operand of a second MMA in the same kernel) is BITWISE
+    equal to the stem writing the pooled map followed by the dense 1x1 GEMM
+    (same bf16 pooled values, same K order), for 4-channel and three-plane
+    stems, odd pooled widths included."""
+    from paper_2310_18481_b200.encoders import (pack_dense_weight, pack_stem_weight, pack_stem_weight_planes,
+                                                pack_sw128_weight)
+    g = torch.Generator().manual_seed(H + Cin + 29)
+    x = _bf(torch.randn(n, Cin, H, H, generator=g))
+    w = _bf(torch.randn(64, Cin, 7, 7, generator=g) * (2.0 / (Cin * 49)) ** 0.5)
+    b = torch.randn(64, generator=g) * 0.1
+    wr = _bf(torch.randn(64, 64, generator=g) * (2.0 / 64) ** 0.5)
+    br = torch.randn(64, generator=g) * 0.1
+    Hp = H + 6
+    if planes == 1:
+        X = torch.zeros(n, Hp, Hp, 4, dtype=torch.bfloat16)
+        X[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+        Wst, kw = pack_stem_weight(w), {}
+    else:
+        X = torch.zeros(3, n, Hp, Hp, 4, dtype=torch.bfloat16)
+        xp = torch.zeros(n, Hp, Hp, 12, dtype=torch.bfloat16)
+        xp[:, 3:H + 3, 3:H + 3, :Cin] = x.permute(0, 2, 3, 1)
+        for q in range(3):
+            X[q] = xp[..., 4 * q:4 * q + 4]
+        Wst, kw = pack_stem_weight_planes(w), {"planes": 3, "plane_stride": n * Hp * Hp * 4}
+    Xd, Wd, bd = X.cuda(), Wst.cuda(), b.cuda()
+    OH = (H + 6 - 7) // 2 + 1
+    PH = -(-(OH - 3) // 2) + 1
+    P1 = torch.empty(n * PH * PH, 64, dtype=torch.bfloat16, device="cuda")
+    dev.plan_stem_pool(Xd, n, H, H, 7, 3, Wd, bd, P1, ldy=64, **kw).run()
+    R0 = torch.empty(n * PH * PH, 64, dtype=torch.bfloat16, device="cuda")
+    dev.plan_dense(P1, pack_dense_weight(wr).cuda(), br.cuda(), R0, M=n * PH * PH, K=64, BN=64, relu=True).run()
+    ldr, col0 = 96, 16
+    R1 = torch.full((n * PH * PH, ldr), 7.0, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_stem_pool(Xd, n, H, H, 7, 3, Wd, bd, P1, ldy=64, **kw)
+    dev.stem_set_reduce(p, pack_sw128_weight(wr).cuda(), br.cuda(), R1[:, col0:], ldy=ldr)
+    p.run()
+    p.run()
+    torch.cuda.synchronize()
+    assert torch.equal(R1[:, col0:col0 + 64], R0), (R1[:, col0:col0 + 64].float() - R0.float()).abs().max().item()
+    assert torch.all(R1[:, :col0] == 7.0) and torch.all(R1[:, col0 + 64:] == 7.0)
