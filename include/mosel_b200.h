@@ -350,6 +350,11 @@ int ms_event_record(void* ev, void* stream);
 int ms_event_elapsed_us(void* start, void* stop, double* us);
 /* 0 = completed, 1 = not yet, -1 = error (see ms_last_error) */
 int ms_event_query(void* ev);
+/* serving-loop plumbing without framework overhead: make `stream` wait for
+ * `ev` (an ms_event), and launch an instantiated CUDA graph (the executor's
+ * captured encoder / head graphs) on `stream` */
+int ms_stream_wait_event(void* stream, void* ev);
+int ms_graph_launch(void* graph_exec, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

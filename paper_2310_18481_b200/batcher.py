@@ -195,17 +195,17 @@ class DevicePassSelector:
         pr[1] = now_us
         pr.view(np.float64)[2] = factor
         base = self._prob.data_ptr()
-        torch = self.torch
-        with torch.cuda.stream(self.stream):
-            if slot_free is not None:
-                self.stream.wait_event(slot_free)
-            self.ev0.record(self.stream)
-            dv.pass_select(1, base, base + 4, base + 8, base + 16, self._size.data_ptr(), self._dl.data_ptr(),
-                           self._ncand.data_ptr(), self._coff.data_ptr(), self._moff.data_ptr(), self._cc.data_ptr(),
-                           self._rm.data_ptr(), self.cost, self.cap, self.max_pass_ns, self._choice.data_ptr(),
-                           self._summary.data_ptr(), self._est.data_ptr(), self.mask_ring[slot].data_ptr(),
-                           self.mask_ring.shape[1], stream=self.stream, out_clock=self._clock.data_ptr())
-            self.ev1.record(self.stream)
+        # every launch names the selection stream explicitly (no stream context:
+        # a framework stream switch costs tens of microseconds of host time per pass)
+        if slot_free is not None:
+            self.stream.wait_event(slot_free)
+        self.ev0.record(self.stream)
+        dv.pass_select(1, base, base + 4, base + 8, base + 16, self._size.data_ptr(), self._dl.data_ptr(),
+                       self._ncand.data_ptr(), self._coff.data_ptr(), self._moff.data_ptr(), self._cc.data_ptr(),
+                       self._rm.data_ptr(), self.cost, self.cap, self.max_pass_ns, self._choice.data_ptr(),
+                       self._summary.data_ptr(), self._est.data_ptr(), self.mask_ring[slot].data_ptr(),
+                       self.mask_ring.shape[1], stream=self.stream, out_clock=self._clock.data_ptr())
+        self.ev1.record(self.stream)
         self.ev1.synchronize()
         self.launches += 1
         self.device_us += self.ev0.elapsed_time(self.ev1) * 1000.0

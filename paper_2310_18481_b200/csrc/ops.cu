@@ -911,6 +911,18 @@ int ms_event_query(void* ev) {
   return -1;
 }
 
+int ms_stream_wait_event(void* stream, void* ev) {
+  if (cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<cudaEvent_t>(ev), 0) != cudaSuccess)
+    return set_error(MS_ERR_CUDA, "cudaStreamWaitEvent failed");
+  return MS_OK;
+}
+int ms_graph_launch(void* graph_exec, void* stream) {
+  if (cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), reinterpret_cast<cudaStream_t>(stream)) !=
+      cudaSuccess)
+    return set_error(MS_ERR_CUDA, "cudaGraphLaunch failed");
+  return MS_OK;
+}
+
 int ms_event_elapsed_us(void* start, void* stop, double* us) {
   float ms = 0.0f;
   if (cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)) != cudaSuccess ||

@@ -94,6 +94,8 @@ _SIGS = {
     "ms_gemm_plan_stem_pool": ([_P, _P, _I, _I, _I, _I, _I, _I, _LL, _P, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_conv_pool": ([_P, _P, _I, _I, _I, _I, _LL, _P, _I, _P, _P, _LL, _I], C.c_int),
     "ms_gemm_plan_stem_set_reduce": ([_P, _P, _P, _P, _LL, _I], C.c_int),
+    "ms_stream_wait_event": ([_P, _P], C.c_int),
+    "ms_graph_launch": ([_P, _P], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
@@ -168,9 +170,21 @@ def _torch():
 
 
 def stream_ptr(stream=None) -> int:
+    """Raw cudaStream_t of ``stream`` (default: the current stream, read through
+    the C binding: torch.cuda.current_stream() costs ~14 us of Python per call,
+    which the serving loop pays several times per pass)."""
+    if stream is not None:
+        return stream.cuda_stream
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+
+
+def stream_wait(stream_p: int, ev: "Event") -> None:
+    check(lib().ms_stream_wait_event(stream_p, ev.h), "ms_stream_wait_event")
+
+
+def graph_launch(graph_exec: int, stream_p: int) -> None:
+    check(lib().ms_graph_launch(graph_exec, stream_p), "ms_graph_launch")
 
 
 def ptr(t) -> int | None:
@@ -650,6 +664,10 @@ class Event:
 
     def record(self, stream=None):
         check(lib().ms_event_record(self.h, stream_ptr(stream)), "ms_event_record")
+
+    def record_on(self, stream_p: int):
+        """Record on a raw cudaStream_t (no stream object lookup)."""
+        check(lib().ms_event_record(self.h, stream_p), "ms_event_record")
 
     def done(self) -> bool:
         """True once the device has passed this event (non-blocking)."""

@@ -99,6 +99,7 @@ class MaskedModel:
         self._G = (ctypes.c_void_p * K)(*[e.x.data_ptr() for e in encoders])
         self._ROWS = (dv.RowDesc * K)(*[dv.RowDesc(*r) for r in self.rows])
         self._graphs = {}
+        self._gexec = {}
         self.use_graphs = True
         self.parallel_modalities = True
         self._side = [torch.cuda.Stream() for _ in range(K)]
@@ -109,8 +110,13 @@ class MaskedModel:
         self._pipeline = os.environ.get("MS_PIPELINE", "1") != "0"
         self._parity = 0
         self._cstream = torch.cuda.Stream()
-        self._ev_stem = [torch.cuda.Event() for _ in range(K)]
-        self._ev_cpar = [torch.cuda.Event() for _ in range(2)]
+        # raw stream pointers + native events for the per-pass launch path
+        self._side_p = [s.cuda_stream for s in self._side]
+        self._cstream_p = self._cstream.cuda_stream
+        self._nev_stem = [dv.Event() for _ in range(K)]
+        self._nev_cpar = [dv.Event() for _ in range(2)]
+        self._nev_k = [dv.Event() for _ in range(K)]
+        self._nev_c = dv.Event()
 
     @property
     def n_slots(self) -> int:
@@ -153,7 +159,7 @@ class MaskedModel:
                               self.inv.data_ptr(), self.counts.data_ptr(), self.offs.data_ptr(),
                               self.perm.data_ptr(), dv.stream_ptr()), "ms_compact")
 
-    def _compact_ring(self, n: int, mask_ptr: int, bases, parity: int = 0, stream=None):
+    def _compact_ring(self, n: int, mask_ptr: int, bases, parity: int = 0, stream=None, stream_p=None):
         """Compaction of a pass whose masks are already on the device
         (``mask_ptr``), modality k's compacted rows read from the pool ring
         at ``bases[k]`` (ms_compact_ring), index outputs of ``parity``."""
@@ -163,7 +169,8 @@ class MaskedModel:
         idx, inv, counts, offs, perm = self._ix[parity]
         dv.check(L.ms_compact_ring(mask_ptr, n, self.K, self._X, self._ROWS, rb, self.n_slots, self._G,
                                    idx.data_ptr(), inv.data_ptr(), counts.data_ptr(), offs.data_ptr(),
-                                   perm.data_ptr(), dv.stream_ptr(stream)), "ms_compact_ring")
+                                   perm.data_ptr(), stream_p if stream_p is not None else dv.stream_ptr(stream)),
+                 "ms_compact_ring")
 
     def _head(self, n: int, parity: int = 0):
         inv = self._ix[parity][1][: self.K * n].view(self.K, n)
@@ -198,7 +205,18 @@ class MaskedModel:
                     fn()
             torch.cuda.current_stream().wait_stream(s)
             self._graphs[key] = g
+            self._gexec[key] = g.raw_cuda_graph_exec()
         return g
+
+    def _exec(self, key, make_fn):
+        """The instantiated graph (cudaGraphExec_t) of ``key``, captured from
+        ``make_fn()``'s launches on first use -- launched by the serving paths
+        with ms_graph_launch on a raw stream (no framework stream switching)."""
+        e = self._gexec.get(key)
+        if e is None:
+            self._graph(key, make_fn())
+            e = self._gexec[key]
+        return e
 
     def ring_upload(self, host_pools, counts, bases, stream):
         """Host-IO path: DMA modality k's next ``counts[k]`` ring rows (from
@@ -253,34 +271,33 @@ class MaskedModel:
         by pass parity; only the fusion head runs on the calling stream, after
         its pass's encoders.  So P+1's gather overlaps P's encoders and P+1's
         encoders start while P's last layers and head still run."""
-        torch = self.torch
         par = self._parity
         self._parity ^= 1
-        main = torch.cuda.current_stream()
-        cs = self._cstream
-        for ev in self._ev_stem:  # every gathered input consumed by its stem
-            cs.wait_event(ev)
+        main_p = dv.stream_ptr()
+        cs_p = self._cstream_p
+        for ev in self._nev_stem:  # every gathered input consumed by its stem
+            dv.stream_wait(cs_p, ev)
         if upload_ev is not None:
-            cs.wait_event(upload_ev)
-        self._compact_ring(n, mask_ptr, bases, parity=par, stream=cs)
-        self._ev_cpar[par].record(cs)
-        self.ring_ev[slot].record(cs)
+            dv.stream_wait(cs_p, upload_ev)
+        self._compact_ring(n, mask_ptr, bases, parity=par, stream_p=cs_p)
+        self._nev_cpar[par].record_on(cs_p)
+        self.ring_ev[slot].record(self._cstream)
         self.ring_used[slot] = True
         present = [k for k, nk in enumerate(counts) if nk]
         for k in present:
-            sp = self.encoders[k].program(counts[k], par)
-            ga = self._graph(("stem", k, counts[k], par), sp.first().run)
-            gb = self._graph(("rest", k, counts[k], par), sp.tail().run)
-            side = self._side[k]
-            side.wait_event(self._ev_cpar[par])
-            with torch.cuda.stream(side):
-                ga.replay()
-                self._ev_stem[k].record(side)
-                gb.replay()
-            self._ev_k[k].record(side)
+            nk = counts[k]
+            enc = self.encoders[k]
+            ga = self._exec(("stem", k, nk, par), lambda: enc.program(nk, par).first().run)
+            gb = self._exec(("rest", k, nk, par), lambda: enc.program(nk, par).tail().run)
+            sp = self._side_p[k]
+            dv.stream_wait(sp, self._nev_cpar[par])
+            dv.graph_launch(ga, sp)
+            self._nev_stem[k].record_on(sp)
+            dv.graph_launch(gb, sp)
+            self._nev_k[k].record_on(sp)
         for k in present:
-            main.wait_event(self._ev_k[k])
-        self._graph(("head", n, par), self._head(n, par).run).replay()
+            dv.stream_wait(main_p, self._nev_k[k])
+        dv.graph_launch(self._exec(("head", n, par), lambda: self._head(n, par).run), main_p)
 
     def run_staged(self, n: int, counts, compact=None):
         """Compaction (direct launches), then one graph per present
@@ -296,28 +313,26 @@ class MaskedModel:
             self._head(n).run()
             return
         compact()
-        torch = self.torch
-        main = torch.cuda.current_stream()
+        main_p = dv.stream_ptr()
         present = [k for k, nk in enumerate(counts) if nk]
-        graphs = [self._graph(("enc", k, counts[k]), self.encoders[k].program(counts[k]).run)
-                  for k in present]
-        head = self._graph(("head", n), self._head(n).run)
+        execs = [self._exec(("enc", k, counts[k]), lambda k=k: self.encoders[k].program(counts[k]).run)
+                 for k in present]
+        head = self._exec(("head", n), lambda: self._head(n).run)
         if not self.parallel_modalities or len(present) < 2:
-            for g in graphs:
-                g.replay()
+            for e in execs:
+                dv.graph_launch(e, main_p)
         else:
             # independent encoders run concurrently: fork after compaction,
             # join before the fusion head
-            self._ev_c.record(main)
-            for k, g in zip(present, graphs):
-                side = self._side[k]
-                side.wait_event(self._ev_c)
-                with torch.cuda.stream(side):
-                    g.replay()
-                self._ev_k[k].record(side)
+            self._nev_c.record_on(main_p)
+            for k, e in zip(present, execs):
+                sp = self._side_p[k]
+                dv.stream_wait(sp, self._nev_c)
+                dv.graph_launch(e, sp)
+                self._nev_k[k].record_on(sp)
             for k in present:
-                main.wait_event(self._ev_k[k])
-        head.replay()
+                dv.stream_wait(main_p, self._nev_k[k])
+        dv.graph_launch(head, main_p)
 
     def ensure_warm(self, max_n: int | None = None):
         """warm_graphs once per model (a graph captured lazily while passes are

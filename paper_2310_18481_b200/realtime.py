@@ -268,7 +268,7 @@ def _serve_realtime(model, profile: ModelProfile, matrix: StrategyMatrix, templa
         upload_ev = None
         if host_clips is not None:
             stats.h2d_bytes += model.ring_upload(host_clips.host, counts, bases, copy_stream)
-            upload_ev = model.torch.cuda.Event()
+            upload_ev = dv.Event()
             upload_ev.record(copy_stream)
             stream.wait_stream(copy_stream)
         for k in range(model.K):
