@@ -130,12 +130,16 @@ def frontier(cells, slo_scaled: int):
 
 def parts_for_requests(parts, size: int):
     """G2(i): requests 0..size-1, in index order, fill the job's canonical
-    parts (strategy.py:54-60) in order; a part past the true size is
-    truncated, an empty one skipped (rounded-up strategies,
-    scheduler.py:138-167).  Returns (mask per request, [(mask, lo, hi)])."""
+    parts (strategy.py:54-60) in order; for a rounded-up strategy
+    (scheduler.py:138-167: more part rows than requests) the parts are taken
+    in order of decreasing modality count, so the rows truncated are the
+    least-informed subsets; an empty part is skipped.  Returns (mask per
+    request, [(mask, lo, hi)])."""
     masks = np.zeros(size, dtype=np.uint16)
     spans = []
     lo = 0
+    if sum(b for _, b in parts) > size:  # rounded up: the most-modality parts first (stable)
+        parts = sorted(parts, key=lambda pb: -bin(int(pb[0])).count("1"))
     for mask, batch in parts:
         hi = min(size, lo + batch)
         if hi > lo:

@@ -35,9 +35,14 @@ from .encoders import (CONV1_PAD, FEAT_DIM, SEGMENTS, TBN_MODALITIES, U8_BIAS, U
 
 def request_masks(parts, size: int) -> np.ndarray:
     """G2(i): requests 0..size-1 in index order fill the job's canonical
-    parts in order; parts past the true size (rounded-up strategies,
-    scheduler.py:138-167) are truncated."""
+    parts in order.  A rounded-up strategy (scheduler.py:138-167) has more
+    part rows than the job has requests: then the parts are taken in order
+    of decreasing modality count (stable), so the rows left over are the
+    least-informed subsets rather than, by the canonical bitmask order, the
+    all-modality ones (oracle/selection.parts_for_requests, same rule)."""
     out = np.zeros(size, dtype=np.int16)
+    if sum(b for _, b in parts) > size:
+        parts = sorted(parts, key=lambda pb: -bin(int(pb[0])).count("1"))
     lo = 0
     for mask, batch in parts:
         hi = min(size, lo + batch)

@@ -79,9 +79,11 @@ def test_grouping_rules_pinned_to_reference_canonical_order():
     assert [(m, n) for m, _, n in chunks] == [(3, 1), (3, 2), (3, 2)]
     masks, spans = orc.parts_for_requests(((1, 1), (3, 1)), 2)
     assert masks.tolist() == [1, 3] and spans == [(1, 0, 1), (3, 1, 2)]
-    # rounded-up strategy covering more requests than the job has
+    # rounded-up strategy covering more requests than the job has (builder
+    # contract, not in the reference): the most-modality parts are filled
+    # first, so the row left over is the least-informed subset's
     masks, spans = orc.parts_for_requests(((1, 2), (3, 2)), 3)
-    assert masks.tolist() == [1, 1, 3]
+    assert masks.tolist() == [3, 3, 1]
 
 
 def test_compaction_restatement_properties():
