@@ -814,7 +814,9 @@ def main():
     ap.add_argument("--search-seconds", type=float, default=2.0, help="window per arrival draw in the rate search")
     ap.add_argument("--deadline-ms", type=float, default=15.0,
                     help="fixed per-request latency budget (deadline - arrival)")
-    ap.add_argument("--max-req", type=int, default=96, help="device pass capacity (requests)")
+    ap.add_argument("--max-req", type=int, default=None,
+                    help="device pass capacity (requests); default 96 (tbn, vqa), 1024 (mlp: the tiny towers "
+                         "need big passes to amortise the per-pass host work -- 157k req/s at 96, 467k at 1024)")
     ap.add_argument("--max-job", type=int, default=24, help="job size cap (matrix sizes 1..max_job)")
     ap.add_argument("--no-batching", action="store_true", help="one job per device pass")
     ap.add_argument("--selection", default="pass", choices=["pass", "policy"],
@@ -839,6 +841,8 @@ def main():
     ap.add_argument("--profile-batch", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.max_req is None:
+        args.max_req = 1024 if args.workload == "mlp" else 96
     SERVE_OPTS.update(sched_margin_us=int(args.sched_margin_ms * 1000), policy_grid_us=int(args.policy_grid_us),
                       selection=args.selection, pass_frac=args.pass_frac, arrivals=args.arrivals,
                       mults=MULTS if args.budgets == "varying" else None)
