@@ -669,6 +669,7 @@ class BNInceptionEncoder:
                                   ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, halo=True)
                 return p_.set_pair(True)
             wt = self._w64(wname) if (no_k32 and cin_ % 64) else self.w[wname]
+            # (two N tiles for the under-filled 7x7 layers measured +1.4 % pass time)
             return dv.plan_conv(X_, n, h, h, cin_, cin_, 3, 3, stride_, 1, wt, cout_, self.b[wname], D_,
                                 ldd=ldd_, col0=col0_, BN=pick_bn(cout_), relu=True, tile=tile_, k32=k32(cin_))
 
