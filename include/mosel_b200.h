@@ -255,6 +255,18 @@ int ms_gemm_plan_stem_pool(void* plan, const void* X, int n_img, int H, int W_in
  * by ms_pool (same accumulation order); the unpooled map never reaches HBM. */
 int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int H, int W_in, int C, long long c_stride,
                            const void* Wt, int Cout, const float* bias, void* Y, long long ldy, int y_col0);
+/* The whole late-fusion head in one launch (replaces ms_gemm_plan_gather +
+ * the FC2 dense plan + its split-K finalize; reference: the fusion MLP over
+ * the concatenated encoder outputs, absent modalities zero -- profile.py:
+ * 157-159).  logits[M, n_classes] (fp32, row stride ldo) = FC2(ReLU(FC1(
+ * concat_k feat[k][inv[k, r]] or 0))): W1 [512, n_mod * feat_dim] bf16
+ * K-major, b1 [512], W2 [n_classes, 512] bf16 K-major, b2 [n_classes].
+ * Needs n_mod * feat_dim % 512 == 0 and n_classes <= 512.  8-CTA clusters per
+ * 128 requests; FC1 and FC2 partials reduce-scatter over distributed shared
+ * memory in a fixed order (bitwise reproducible). */
+int ms_gemm_plan_fused_head(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
+                            int feat_dim, int M, const void* W1, const float* b1, const void* W2, const float* b2,
+                            int n_classes, float* logits, long long ldo);
 /* Fuse a 1x1 conv (64 -> 64, + bias + ReLU; BN-Inception's conv2_red) into a
  * stem plan (output width <= 112): the pooled rows become the A operand of a
  * second tcgen05 MMA in the same kernel and Y receives the 1x1's output

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmosel_b200.so"
-SOURCES = ["select.cu", "gemm.cu", "convpool.cu", "ops.cu", "transformer.cu", "policy.cu", "strategy.cu"]
+SOURCES = ["select.cu", "gemm.cu", "convpool.cu", "head.cu", "ops.cu", "transformer.cu", "policy.cu", "strategy.cu"]
 HEADERS = ["ptx.cuh", "runtime.h", "gemm_plan.h"]
 
 NVCC_FLAGS = [

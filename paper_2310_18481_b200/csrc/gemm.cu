@@ -1489,6 +1489,7 @@ static void set_segments(GemmParams& p, int nseg, const MsSegment* segs, void* D
 static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
   const GemmParams& p = P->p;
   if (p.mode == MODE_CONV_POOL) return launch_conv_pool(P, stream);
+  if (p.mode == MODE_FUSED_HEAD) return launch_fused_head(P, stream);
   if (p.mode == MODE_STEM_POOL) {
     static int stem_attr = 0;
     if (!stem_attr) {

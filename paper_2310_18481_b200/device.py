@@ -98,6 +98,7 @@ _SIGS = {
     "ms_graph_launch": ([_P, _P], C.c_int),
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
+    "ms_gemm_plan_fused_head": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _LL], C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
     "ms_gemm_plan_info": ([_P, _P, _P, _P, _P], C.c_int),
     "ms_pool2d": ([_P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P], C.c_int),
@@ -490,6 +491,20 @@ def plan_gather(feats, inv, W, bias, D, *, M, feat_dim, BN=128, relu=True, out_f
     p.flops = 2 * M * W.shape[0] * len(feats) * feat_dim
     p.label = f"gather-concat M={M} N={W.shape[0]} K={len(feats) * feat_dim}"
     _auto_splitk(p, M, W.shape[0], BN, len(feats) * feat_dim // 64, split_k, W.device)
+    return p
+
+
+def plan_fused_head(feats, inv, W1, b1, W2, b2, logits, *, M, feat_dim):
+    """The late-fusion head in one cluster launch (ms_gemm_plan_fused_head):
+    gather-concat FC1 + ReLU + FC2 -> fp32 logits[:M]."""
+    p = GemmPlan()
+    arr = (C.c_void_p * len(feats))(*[ptr(f) for f in feats])
+    check(lib().ms_gemm_plan_fused_head(p.addr, arr, ptr(inv), inv.stride(0), len(feats), feat_dim, M, ptr(W1),
+                                        ptr(b1), ptr(W2), ptr(b2), W2.shape[0], ptr(logits), logits.stride(0)),
+          "ms_gemm_plan_fused_head")
+    p.keep = [feats, inv, W1, b1, W2, b2, logits, arr]
+    p.flops = 2 * M * W1.shape[0] * len(feats) * feat_dim + 2 * M * W1.shape[0] * W2.shape[0]
+    p.label = f"fused_head_kernel M={M} K={len(feats) * feat_dim} -> {W1.shape[0]} -> {W2.shape[0]}"
     return p
 
 

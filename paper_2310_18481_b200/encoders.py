@@ -764,13 +764,34 @@ class FusionHead:
         self.logits = torch.empty(max_req, n_classes, dtype=torch.float32, device=self.dev)
         self._programs = {}
 
-    def program(self, n_req: int, feats, inv):
-        """feats: per-modality compacted feature buffers; inv [n_mod, >=n_req]."""
+    # the one-launch head wins up to ~48 requests per 128-request tile
+    # (tools/head_time.py, profiles/r02_head_time.txt: 10.9 vs 13.6 us at 1
+    # request, K = 3); above that its DSMEM reduce-scatter (~20 B/clk per SM)
+    # costs more than the split-K round trip through L2
+    FUSED_MAX_REQ = int(os.environ.get("MS_FUSED_HEAD_MAX", "48"))
+
+    @property
+    def fusable(self) -> bool:
+        """The one-launch cluster head applies (K % 512, classes <= 512);
+        MS_FUSED_HEAD=0 keeps the three-launch path (A/B switch)."""
+        return (os.environ.get("MS_FUSED_HEAD", "1") != "0" and self.n_classes <= FUSION_HIDDEN
+                and (self.n_mod * self.feat_dim) % 512 == 0 and self.feat_dim % 64 == 0)
+
+    def program(self, n_req: int, feats, inv, fused=None):
+        """feats: per-modality compacted feature buffers; inv [n_mod, >=n_req].
+        fused: None = the one-launch cluster head when it applies and n_req <=
+        FUSED_MAX_REQ, else the gather GEMM + FC2 split-K path."""
         from . import device as dv
-        key = (n_req, tuple(f.data_ptr() for f in feats), inv.data_ptr())
+        fused = (self.fusable and n_req <= self.FUSED_MAX_REQ) if fused is None else fused
+        key = (n_req, tuple(f.data_ptr() for f in feats), inv.data_ptr(), fused)
         if key in self._programs:
             return self._programs[key]
         P = dv.Program()
+        if fused:
+            P.gemm(dv.plan_fused_head(list(feats), inv, self.w1, self.b1, self.w2, self.b2, self.logits, M=n_req,
+                                      feat_dim=self.feat_dim))
+            self._programs[key] = P.seal()
+            return self._programs[key]
         P.gemm(dv.plan_gather(list(feats), inv, self.w1, self.b1, self.h, M=n_req,
                               feat_dim=self.feat_dim, BN=256, relu=True))
         # the fp32 logits leave through the split-K finalize (coalesced rows)
