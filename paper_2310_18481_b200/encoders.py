@@ -520,7 +520,13 @@ class BNInceptionEncoder:
         elif self.fused_stem and cp == 12 and h1 <= 112:
             self.stem_planes = 3
         self.x_plane_stride = n_img * (size + 2 * rp) * (size + 2 * CONV1_PAD) * 4 if self.stem_planes == 3 else 0
-        self.stem_red = bool(self.stem_planes) and self.stem_red_env and h1 <= 112
+        # for the 4-channel (rgb) stem the fused 1x1 is slower timed alone
+        # (117.6 us vs 74.3 + 27.0) but equal on the served path, where the
+        # separate GEMM's HBM round trip competes with the other encoders
+        # (tools/ringab.sh, profiles/r02_ringab_stemred.txt); MS_STEM_RED_RGB=0
+        # keeps it separate
+        self.stem_red = (bool(self.stem_planes) and self.stem_red_env and h1 <= 112
+                         and (self.stem_planes == 3 or os.environ.get("MS_STEM_RED_RGB", "1") == "1"))
 
     # features of pass parity p land in outs[p]: with passes pipelined the next
     # pass's encoder may finish before the previous pass's fusion head has read
