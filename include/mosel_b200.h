@@ -63,6 +63,11 @@ int ms_abi_version(void);
  * next kernel's prologue overlaps the previous kernel's tail.  Returns the
  * previous setting. */
 int ms_set_pdl(int enable);
+/* Grid policy of the two-CTAs-per-SM GEMM plans built afterwards: 0 = one
+ * CTA per SM, 1 = up to two (the kernel fills the GPU alone), 2 = two only
+ * with >= 4 tiles per SM (leaves room for kernels running beside it), < 0 =
+ * MS_OCC2_GRID / default 1.  Returns the previous setting. */
+int ms_set_occ2_grid(int mode);
 const char* ms_last_error(void);
 int ms_device_sync(void);
 

@@ -1340,6 +1340,8 @@ int encode_bf16_map(CUtensorMap* m, int rank, const void* base, const cuuint64_t
   return encode_map(m, rank, base, dims, strides_bytes, box, estride, swz);
 }
 
+int g_occ2_grid = -1;  // ms_set_occ2_grid (< 0: MS_OCC2_GRID / default)
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -1412,11 +1414,13 @@ static int finish_plan(GemmPlan* P, const void* W, int K_pad, int N_rows_w, int 
   if (P->smem_bytes > 227 * 1024) return set_error(MS_ERR_INVALID, "GEMM plan exceeds 227 KB shared memory");
   p.m_tiles = grid_x;
   const int tiles = grid_x * ((p.N + BN - 1) / BN);
-  // up to two of this kernel's own CTAs per SM (MS_OCC2_GRID: 0 never, 2 only
-  // with >= 4 tiles per SM, default 1 always: a kernel with no concurrent
-  // partner still fills both slots -- single-encoder passes 3-6 % faster,
-  // profiles/r02_abn_occ2.txt)
-  static const int occ2_grid = getenv("MS_OCC2_GRID") ? atoi(getenv("MS_OCC2_GRID")) : 1;
+  // up to two of this kernel's own CTAs per SM (MS_OCC2_GRID / ms_set_occ2_grid:
+  // 0 never, 2 only with >= 4 tiles per SM, default 1 always: a kernel with no
+  // concurrent partner still fills both slots -- single-encoder passes 3-6 %
+  // faster, profiles/r02_abn_occ2.txt; with other encoders running beside it,
+  // 2 leaves them the second slot -- mixed passes 0.7-3.4 % faster,
+  // profiles/r02_ringab_grid2.txt; the executor plans both variants)
+  const int occ2_grid = g_occ2_grid >= 0 ? g_occ2_grid : (getenv("MS_OCC2_GRID") ? atoi(getenv("MS_OCC2_GRID")) : 1);
   const bool grid2 = p.occ2 && (occ2_grid == 1 || (occ2_grid == 2 && tiles >= 4 * sm_count()));
   const int max_ctas = grid2 ? 2 * sm_count() : sm_count();
   P->grid_x = tiles < max_ctas ? tiles : max_ctas;
@@ -1863,6 +1867,12 @@ int ms_gemm_plan_set_pair(void* plan, int enable) {
   P->grid_x = 2 * clusters;
   P->grid_y = 1;
   return MS_OK;
+}
+
+int ms_set_occ2_grid(int mode) {
+  const int prev = g_occ2_grid;
+  g_occ2_grid = mode;
+  return prev;
 }
 
 int ms_gemm_plan_set_trace(void* plan, unsigned long long* buf) {

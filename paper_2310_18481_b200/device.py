@@ -70,6 +70,7 @@ class PassCost(C.Structure):
 _SIGS = {
     "ms_abi_version": ([], C.c_int),
     "ms_set_pdl": ([_I], C.c_int),
+    "ms_set_occ2_grid": ([_I], C.c_int),
     "ms_strategy_dp": ([_I, _P, _P, _P, _I, _I, _P, _P, _P], C.c_int),
     "ms_policy_apply": ([_I, _I, _P, _P, _P, _P, _P, _P, C.c_int64, C.c_int64, _I, _D, C.c_int64, _P, _LL,
                          _P, _P], C.c_int),
@@ -155,6 +156,12 @@ def set_pdl(enable: bool) -> bool:
     """Programmatic dependent launch for op-program kernels (default on);
     returns the previous setting.  Affects plans launched afterwards."""
     return bool(lib().ms_set_pdl(int(bool(enable))))
+
+
+def set_occ2_grid(mode: int) -> int:
+    """Grid policy of two-CTAs-per-SM GEMM plans built afterwards (see
+    ms_set_occ2_grid); returns the previous setting."""
+    return int(lib().ms_set_occ2_grid(int(mode)))
 
 
 def check(rc: int, what: str) -> None:

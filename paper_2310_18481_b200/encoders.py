@@ -533,13 +533,25 @@ class BNInceptionEncoder:
     # its features (executor.MaskedModel.run_ring)
     supports_parity = True
 
-    def program(self, n_req: int, parity: int = 0):
-        key = (n_req, parity)
+    # shared=True: plans for a pass where other encoders run beside this one
+    # (two-CTAs-per-SM GEMMs take the second slot only with >= 4 tiles per
+    # SM, leaving it to the partners; ms_set_occ2_grid); same buffers
+    supports_shared = True
+    SHARED_OCC2_GRID = int(os.environ.get("MS_SHARED_OCC2_GRID", "2"))
+
+    def program(self, n_req: int, parity: int = 0, shared: bool = False):
+        key = (n_req, parity, bool(shared))
         if key in self._programs:
             return self._programs[key]
         if not 1 <= n_req <= self.max_req:
             raise ValueError(f"n_req {n_req} outside 1..{self.max_req}")
-        prog = self._build(n_req, parity)
+        from . import device as dv
+        prev = dv.set_occ2_grid(self.SHARED_OCC2_GRID) if shared else None
+        try:
+            prog = self._build(n_req, parity)
+        finally:
+            if shared:
+                dv.set_occ2_grid(prev)
         self._programs[key] = prog
         return prog
 

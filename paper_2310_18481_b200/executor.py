@@ -289,11 +289,16 @@ class MaskedModel:
         self.ring_ev[slot].record(self._cstream)
         self.ring_used[slot] = True
         present = [k for k, nk in enumerate(counts) if nk]
+        # the encoders of a multi-modality pass share the GPU: their "rest"
+        # graphs come from the shared plans (encoders.BNInception.program)
+        sh = len(present) > 1
         for k in present:
             nk = counts[k]
             enc = self.encoders[k]
+            shk = sh and getattr(enc, "supports_shared", False)
             ga = self._exec(("stem", k, nk, par), lambda: enc.program(nk, par).first().run)
-            gb = self._exec(("rest", k, nk, par), lambda: enc.program(nk, par).tail().run)
+            gb = self._exec(("rest", k, nk, par, shk), lambda: enc.program(nk, par, shared=True).tail().run
+                            if shk else enc.program(nk, par).tail().run)
             sp = self._side_p[k]
             dv.stream_wait(sp, self._nev_cpar[par])
             dv.graph_launch(ga, sp)
@@ -361,7 +366,9 @@ class MaskedModel:
                     for nk in range(1, top + 1):
                         sp = enc.program(nk, par)
                         self._graph(("stem", k, nk, par), sp.first().run)
-                        self._graph(("rest", k, nk, par), sp.tail().run)
+                        self._graph(("rest", k, nk, par, False), sp.tail().run)
+                        if getattr(enc, "supports_shared", False) and self.K > 1:
+                            self._graph(("rest", k, nk, par, True), enc.program(nk, par, shared=True).tail().run)
                 for n in range(1, top + 1):
                     self._graph(("head", n, par), self._head(n, par).run)
         self.torch.cuda.synchronize()

@@ -33,10 +33,15 @@ rng = np.random.default_rng(0)
 masks = np.zeros(n, dtype=np.int16)
 for k, c in enumerate(counts):
     masks[rng.permutation(n)[:c]] |= 1 << k
+assert (masks != 0).all(), "every request needs a modality: max(counts) rows, rgb first"
 for s in range(len(m.ring_ev)):
     m.mask_ring[s, :n].copy_(torch.as_tensor(masks))
+import time  # noqa: E402
+
+t_w = time.perf_counter()
 m.ensure_warm()
 torch.cuda.synchronize()
+t_w = time.perf_counter() - t_w
 rings = [0] * m.K
 i = 0
 
@@ -63,5 +68,5 @@ for _ in range(a.reps):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_us(e1) / a.passes)
-print(f"served-path pass {counts}: {np.median(ts):8.1f} us/pass (reps {', '.join(f'{t:.1f}' for t in ts)})",
+print(f"served-path pass {counts}: {np.median(ts):8.1f} us/pass (reps {', '.join(f'{t:.1f}' for t in ts)}; warm {t_w:.1f} s)",
       flush=True)
