@@ -272,6 +272,16 @@ int ms_gemm_plan_conv_pool(void* plan, const void* X, int n_img, int H, int W_in
 int ms_gemm_plan_fused_head(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
                             int feat_dim, int M, const void* W1, const float* b1, const void* W2, const float* b2,
                             int n_classes, float* logits, long long ldo);
+/* The same head for small passes as ONE weight-streaming launch
+ * (MODE_HEAD_GEMV): FC1 over 128 CTAs (4 hidden rows each, W1 chunks held in
+ * registers, features gathered through inv, absent modality = zero K block)
+ * -> bf16 h[M, 512] in `h` -> grid barrier on `sync` (two zeroed uint32
+ * words, left zeroed/advanced for the next launch) -> FC2, one warp per
+ * class.  Replaces the same reference fusion step as ms_gemm_plan_fused_head
+ * (profile.py:157-159 drop rule, profile.py:170-174 head); K <= 4096. */
+int ms_gemm_plan_head_gemv(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
+                           int feat_dim, int M, const void* W1, const float* b1, const void* W2, const float* b2,
+                           int n_classes, float* logits, long long ldo, void* h, void* sync);
 /* Fuse a 1x1 conv (64 -> 64, + bias + ReLU; BN-Inception's conv2_red) into a
  * stem plan (output width <= 112): the pooled rows become the A operand of a
  * second tcgen05 MMA in the same kernel and Y receives the 1x1's output

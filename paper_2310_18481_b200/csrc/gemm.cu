@@ -1494,6 +1494,7 @@ static int launch_plan(const GemmPlan* P, cudaStream_t stream) {
   const GemmParams& p = P->p;
   if (p.mode == MODE_CONV_POOL) return launch_conv_pool(P, stream);
   if (p.mode == MODE_FUSED_HEAD) return launch_fused_head(P, stream);
+  if (p.mode == MODE_HEAD_GEMV) return launch_head_gemv(P, stream);
   if (p.mode == MODE_STEM_POOL) {
     static int stem_attr = 0;
     if (!stem_attr) {

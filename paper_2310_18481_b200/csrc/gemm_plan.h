@@ -25,7 +25,7 @@ constexpr int kABytes = kBM * kBK * 2;  // 16 KB per stage
 enum GemmMode : int {
   MODE_DENSE = 0, MODE_CONV = 1, MODE_GATHER = 2, MODE_CONV_SMALLC = 3, MODE_CONV_C4 = 5,
   MODE_CONV_HALO = 6, MODE_CONV_C12 = 7, MODE_CONV_K32 = 8, MODE_STEM_POOL = 9, MODE_CONV_POOL = 10,
-  MODE_FUSED_HEAD = 11
+  MODE_FUSED_HEAD = 11, MODE_HEAD_GEMV = 12
 };
 // MODE_CONV_K32: implicit-GEMM conv whose input channel count is a multiple
 // of 32 but not of 64 (96, 160, 224): K runs over (tap, 32-channel part)
@@ -126,6 +126,7 @@ struct GemmParams {
   const float* red_bias;  //   its bias; output = seg[1] (the pooled map itself is then not stored)
   long long x_pitch;   // bytes of one padded input row
   int Hp, PH, PW, units;
+  __nv_bfloat16* hbuf;  // MODE_HEAD_GEMV: bf16 hidden rows [M, 512] between the two launches
 };
 
 // One bf16 output tensor map per epilogue segment (TMA stores, SWIZZLE_64B):
@@ -163,5 +164,6 @@ struct alignas(64) GemmPlan {
 int sm_count();
 int launch_conv_pool(const GemmPlan* P, cudaStream_t stream);
 int launch_fused_head(const GemmPlan* P, cudaStream_t stream);
+int launch_head_gemv(const GemmPlan* P, cudaStream_t stream);
 
 }  // namespace mosel

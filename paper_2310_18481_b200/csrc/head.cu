@@ -352,6 +352,200 @@ __global__ void __launch_bounds__(kHdThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Small-pass head (MODE_HEAD_GEMV): with few requests the head is a weight
+// stream -- W1 (512 x K bf16, 4 MB at K = 4096) dwarfs the features -- and the
+// cluster head above reads it with 8 SMs.  Here ONE launch of 128 CTAs
+// streams it: FC1 gives each CTA 4 hidden rows (every thread holds its
+// 8-element K chunks of those rows in registers, loaded -- with the CTA's FC2
+// rows -- before griddepcontrol.wait, so the stream overlaps the previous
+// kernel's tail), gathers each request's concatenated features through inv
+// (absent modality = zero K block, profile.py:157-159) with all of a group's
+// loads in flight, and reduces 4 rows x 8 requests per pass with a butterfly
+// transpose-reduce (31 shuffles for 32 sums).  h is rounded to bf16 (the
+// unfused path's rounding point).  A grid barrier (all 128 CTAs co-resident)
+// replaces a second launch; FC2 then gives each warp one class and reduces 32
+// requests per butterfly.  Every output has one producer in a fixed order:
+// reruns are bitwise identical.
+constexpr int kGvThreads = 256;
+constexpr int kGvRows = 4;      // hidden rows per FC1 CTA
+constexpr int kGvMaxCh = 2;     // K <= 2 * 256 * 8 = 4096
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+// v[j] on entry: this lane's partial of sum j (V sums, V a power of two <=
+// 32); on return v[0] = the warp's total of sum (lane & (V - 1)): plain xor
+// reductions over the lane bits >= V, then a butterfly transpose-reduce over
+// the low bits (V - 1 shuffles instead of V * 5)
+template <int V>
+__device__ __forceinline__ float warp_reduce_multi(float (&v)[V], int lane) {
+#pragma unroll
+  for (int off = 16; off >= V; off >>= 1)
+#pragma unroll
+    for (int j = 0; j < V; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], off);
+#pragma unroll
+  for (int off = V / 2; off >= 1; off >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float keep = hi ? v[j + off] : v[j];
+      const float send = hi ? v[j] : v[j + off];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+// grid-wide barrier for a grid whose CTAs are all co-resident (128 CTAs of
+// one 256-thread block per SM at most): arrive on a counter, the last
+// arriver resets it and bumps the generation word the others spin on, so the
+// two words are ready for the next launch (graph replays) without a memset
+__device__ __forceinline__ void grid_barrier(unsigned* sync) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = sync + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(sync, 1u) == gridDim.x - 1) {
+      atomicExch(sync, 0u);
+      __threadfence();
+      atomicAdd(sync + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Q: requests per reduction pass (1, 2, 4 or 8, picked from M at launch so a
+// one-request head does one request's FMAs)
+template <int Q>
+__global__ void __launch_bounds__(kGvThreads) head_gemv_kernel(const GemmParams p, const __nv_bfloat16* __restrict__ W1,
+                                                               const __nv_bfloat16* __restrict__ W2, unsigned* sync) {
+  __shared__ float red[kGvThreads / 32][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // FC2 rows of this CTA: warp w takes class blockIdx.x + w * gridDim.x
+  // (lane covers K = [8 lane, 8 lane + 8) and [256 + 8 lane, ...))
+  const int cls = blockIdx.x + warp * gridDim.x;
+  const bool live = cls < p.N;
+  uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+  float bias2 = 0.f;
+  if (live) {
+    const uint4* wr = reinterpret_cast<const uint4*>(W2 + (long long)cls * kHdHidden);
+    v0 = __ldg(wr + lane);
+    v1 = __ldg(wr + 32 + lane);
+    bias2 = __ldg(p.red_bias + cls);
+  }
+  const int K = p.n_mod * p.feat_dim, nch = K / 8, row0 = blockIdx.x * kGvRows;
+  uint4 w[kGvMaxCh][kGvRows];
+#pragma unroll
+  for (int i = 0; i < kGvMaxCh; ++i) {
+    const int c = tid + i * kGvThreads;
+#pragma unroll
+    for (int rr = 0; rr < kGvRows; ++rr)
+      w[i][rr] = c < nch ? __ldg(reinterpret_cast<const uint4*>(W1 + (long long)(row0 + rr) * K) + c)
+                         : make_uint4(0, 0, 0, 0);
+  }
+  pdl_wait();  // features / inv come from the encoders and the compaction
+  pdl_trigger();
+  int mch[kGvMaxCh], dch[kGvMaxCh];
+#pragma unroll
+  for (int i = 0; i < kGvMaxCh; ++i) {
+    const int c = min(tid + i * kGvThreads, nch - 1);
+    mch[i] = (c * 8) / p.feat_dim;
+    dch[i] = c * 8 - mch[i] * p.feat_dim;
+  }
+  constexpr int V1 = kGvRows * Q;
+  for (int g0 = 0; g0 < p.M; g0 += Q) {
+    // every gather of the group in flight at once: inv rows, then feature chunks
+    int src[kGvMaxCh][Q];
+#pragma unroll
+    for (int i = 0; i < kGvMaxCh; ++i)
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        src[i][q] = (g0 + q < p.M && tid + i * kGvThreads < nch) ? __ldg(p.inv + (long long)mch[i] * p.inv_ld + g0 + q)
+                                                                 : -1;
+    uint4 xv[kGvMaxCh][Q];
+#pragma unroll
+    for (int i = 0; i < kGvMaxCh; ++i)
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        xv[i][q] = src[i][q] >= 0 ? __ldg(reinterpret_cast<const uint4*>(p.feat[mch[i]] + (long long)src[i][q] * p.feat_dim +
+                                                                         dch[i]))
+                                  : make_uint4(0, 0, 0, 0);  // absent modality: a zero K block
+    float acc[V1];
+#pragma unroll
+    for (int j = 0; j < V1; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < kGvMaxCh; ++i) {
+      float wf[kGvRows][8];
+#pragma unroll
+      for (int rr = 0; rr < kGvRows; ++rr) bf16x8_to_f32(w[i][rr], wf[rr]);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        float x[8];
+        bf16x8_to_f32(xv[i][q], x);
+#pragma unroll
+        for (int rr = 0; rr < kGvRows; ++rr)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[rr * Q + q] = fmaf(wf[rr][e], x[e], acc[rr * Q + q]);
+      }
+    }
+    const float part = warp_reduce_multi<V1>(acc, lane);
+    if (lane < V1) red[warp][lane] = part;
+    __syncthreads();
+    if (warp == 0 && lane < V1) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < kGvThreads / 32; ++k) s += red[k][lane];
+      const int rr = lane / Q, r = g0 + lane % Q, row = row0 + rr;
+      if (r < p.M) p.hbuf[(long long)r * kHdHidden + row] = __float2bfloat16_rn(fmaxf(s + p.bias[row], 0.f));
+    }
+    __syncthreads();
+  }
+  grid_barrier(sync);  // every h row complete (and visible at L2)
+  if (!live) return;
+  const float bias = bias2;
+  float wa[8], wb[8];
+  bf16x8_to_f32(v0, wa);
+  bf16x8_to_f32(v1, wb);
+  float* out = reinterpret_cast<float*>(p.seg[0].ptr);
+  for (int g0 = 0; g0 < p.M; g0 += Q) {
+    uint4 hv[Q][2];  // the group's h chunks in flight at once
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int r = g0 + q;
+      const uint4* hr = reinterpret_cast<const uint4*>(p.hbuf + (long long)r * kHdHidden);
+      hv[q][0] = r < p.M ? __ldcg(hr + lane) : make_uint4(0, 0, 0, 0);  // L2: written by other CTAs
+      hv[q][1] = r < p.M ? __ldcg(hr + 32 + lane) : make_uint4(0, 0, 0, 0);
+    }
+    float acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      float ha[8], hb[8];
+      bf16x8_to_f32(hv[q][0], ha);
+      bf16x8_to_f32(hv[q][1], hb);
+      float a = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a = fmaf(wa[e], ha[e], a);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a = fmaf(wb[e], hb[e], a);
+      acc[q] = a;
+    }
+    const float s = warp_reduce_multi<Q>(acc, lane);
+    if (lane < Q && g0 + lane < p.M) out[(long long)(g0 + lane) * p.seg[0].ldd + cls] = s + bias;
+  }
+}
+
 }  // namespace
 
 int launch_fused_head(const GemmPlan* P, cudaStream_t stream) {
@@ -362,6 +556,16 @@ int launch_fused_head(const GemmPlan* P, cudaStream_t stream) {
   }
   launch_k(fused_head_kernel, dim3(P->grid_x), dim3(kHdThreads), kHdSmem, stream, kHdCL, P->tmA, P->tmB, P->p);
   return check_launch("fused_head_kernel");
+}
+
+
+int launch_head_gemv(const GemmPlan* P, cudaStream_t stream) {
+  const GemmParams& p = P->p;
+  auto* kern = p.M <= 1 ? head_gemv_kernel<1> : p.M <= 2 ? head_gemv_kernel<2> : p.M <= 4 ? head_gemv_kernel<4>
+                                                                                    : head_gemv_kernel<8>;
+  launch_k(kern, dim3(P->grid_x), dim3(kGvThreads), 0, stream, 1, p, reinterpret_cast<const __nv_bfloat16*>(P->w_ptr),
+           p.residual, reinterpret_cast<unsigned*>(p.ws));
+  return check_launch("head_gemv_kernel");
 }
 
 }  // namespace mosel
@@ -413,5 +617,42 @@ extern "C" int ms_gemm_plan_fused_head(void* plan, const void* const* feat, cons
   P->grid_y = 1;
   P->smem_bytes = kHdSmem;
   P->tmem_cols = 512;
+  return MS_OK;
+}
+
+extern "C" int ms_gemm_plan_head_gemv(void* plan, const void* const* feat, const int32_t* inv, int inv_ld, int n_mod,
+                                      int feat_dim, int M, const void* W1, const float* b1, const void* W2,
+                                      const float* b2, int n_classes, float* logits, long long ldo, void* h,
+                                      void* sync) {
+  if (plan == nullptr || feat == nullptr || inv == nullptr || W1 == nullptr || W2 == nullptr || b1 == nullptr ||
+      b2 == nullptr || logits == nullptr || h == nullptr || sync == nullptr)
+    return set_error(MS_ERR_INVALID, "null pointer");
+  if (n_mod < 1 || n_mod > 4 || feat_dim % 8 != 0 || M <= 0 || ldo < n_classes || n_classes < 1)
+    return set_error(MS_ERR_INVALID, "gemv head needs 1..4 modalities, feat_dim % 8 == 0, M > 0, classes >= 1");
+  if (n_mod * feat_dim > kGvMaxCh * kGvThreads * 8 || n_classes > kHdHidden / kGvRows * (kGvThreads / 32))
+    return set_error(MS_ERR_INVALID, "gemv head needs K <= 4096 and classes <= 1024");
+  GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
+  memset(P, 0, sizeof(GemmPlan));
+  GemmParams& p = P->p;
+  p.mode = MODE_HEAD_GEMV;
+  p.M = M;
+  p.N = n_classes;
+  p.bias = b1;
+  p.red_bias = b2;
+  p.inv = inv;
+  p.inv_ld = inv_ld;
+  p.n_mod = n_mod;
+  p.feat_dim = feat_dim;
+  for (int k = 0; k < n_mod; ++k) p.feat[k] = reinterpret_cast<const __nv_bfloat16*>(feat[k]);
+  for (int k = n_mod; k < 4; ++k) p.feat[k] = p.feat[0];
+  p.nseg = 1;
+  p.seg[0] = Seg{0, n_classes, logits, ldo, 0, 0};
+  p.out_fp32 = 1;
+  p.hbuf = reinterpret_cast<__nv_bfloat16*>(h);
+  p.ws = reinterpret_cast<float*>(sync);  // two zeroed 32-bit words: barrier count, generation
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(W2);  // [classes, 512] rows
+  P->w_ptr = W1;                                            // [512, K] rows
+  P->grid_x = kHdHidden / kGvRows;
+  P->grid_y = 1;
   return MS_OK;
 }

@@ -100,6 +100,7 @@ _SIGS = {
     "ms_gemm_plan_gather": ([_P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I, _P, _LL, _I],
                             C.c_int),
     "ms_gemm_plan_fused_head": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _LL], C.c_int),
+    "ms_gemm_plan_head_gemv": ([_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P, _LL, _P, _P], C.c_int),
     "ms_gemm_run": ([_P, _P], C.c_int),
     "ms_gemm_plan_info": ([_P, _P, _P, _P, _P], C.c_int),
     "ms_pool2d": ([_P, _I, _I, _I, _I, _LL, _I, _I, _I, _I, _I, _P, _LL, _I, _P], C.c_int),
@@ -512,6 +513,22 @@ def plan_fused_head(feats, inv, W1, b1, W2, b2, logits, *, M, feat_dim):
     p.keep = [feats, inv, W1, b1, W2, b2, logits, arr]
     p.flops = 2 * M * W1.shape[0] * len(feats) * feat_dim + 2 * M * W1.shape[0] * W2.shape[0]
     p.label = f"fused_head_kernel M={M} K={len(feats) * feat_dim} -> {W1.shape[0]} -> {W2.shape[0]}"
+    return p
+
+
+def plan_head_gemv(feats, inv, W1, b1, W2, b2, logits, h, *, M, feat_dim):
+    """The late-fusion head for small passes (ms_gemm_plan_head_gemv): FC1 as
+    a weight stream over 128 CTAs -> bf16 h -> grid barrier -> FC2, one launch."""
+    import torch
+    p = GemmPlan()
+    sync = torch.zeros(2, dtype=torch.int32, device=W1.device)  # barrier count + generation
+    arr = (C.c_void_p * len(feats))(*[ptr(f) for f in feats])
+    check(lib().ms_gemm_plan_head_gemv(p.addr, arr, ptr(inv), inv.stride(0), len(feats), feat_dim, M, ptr(W1),
+                                       ptr(b1), ptr(W2), ptr(b2), W2.shape[0], ptr(logits), logits.stride(0),
+                                       ptr(h), ptr(sync)), "ms_gemm_plan_head_gemv")
+    p.keep = [feats, inv, W1, b1, W2, b2, logits, h, sync, arr]
+    p.flops = 2 * M * W1.shape[0] * len(feats) * feat_dim + 2 * M * W1.shape[0] * W2.shape[0]
+    p.label = f"head_gemv_kernel M={M} K={len(feats) * feat_dim} -> {W1.shape[0]} -> {W2.shape[0]}"
     return p
 
 

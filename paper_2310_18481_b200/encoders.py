@@ -795,16 +795,34 @@ class FusionHead:
         return (os.environ.get("MS_FUSED_HEAD", "1") != "0" and self.n_classes <= FUSION_HIDDEN
                 and (self.n_mod * self.feat_dim) % 512 == 0 and self.feat_dim % 64 == 0)
 
-    def program(self, n_req: int, feats, inv, fused=None):
+    # the one-launch weight-streaming head (ms_gemm_plan_head_gemv) below
+    # GEMV_MAX_REQ requests: the head is then a 4 MB W1 stream that the
+    # cluster head reads with 8 SMs and the GEMV kernel with 128
+    GEMV_MAX_REQ = int(os.environ.get("MS_HEAD_GEMV_MAX", "16"))
+
+    @property
+    def gemv_ok(self) -> bool:
+        return self.feat_dim % 8 == 0 and self.n_mod * self.feat_dim <= 4096
+
+    def program(self, n_req: int, feats, inv, fused=None, gemv=None):
         """feats: per-modality compacted feature buffers; inv [n_mod, >=n_req].
-        fused: None = the one-launch cluster head when it applies and n_req <=
-        FUSED_MAX_REQ, else the gather GEMM + FC2 split-K path."""
+        gemv: None = the weight-streaming GEMV head up to GEMV_MAX_REQ requests
+        (when fused is not forced); fused: None = the one-launch cluster head
+        when it applies and n_req <= FUSED_MAX_REQ, else the gather GEMM + FC2
+        split-K path."""
         from . import device as dv
+        if gemv is None:
+            gemv = fused is None and self.gemv_ok and n_req <= self.GEMV_MAX_REQ
         fused = (self.fusable and n_req <= self.FUSED_MAX_REQ) if fused is None else fused
-        key = (n_req, tuple(f.data_ptr() for f in feats), inv.data_ptr(), fused)
+        key = (n_req, tuple(f.data_ptr() for f in feats), inv.data_ptr(), fused, gemv)
         if key in self._programs:
             return self._programs[key]
         P = dv.Program()
+        if gemv:
+            P.gemm(dv.plan_head_gemv(list(feats), inv, self.w1, self.b1, self.w2, self.b2, self.logits, self.h,
+                                     M=n_req, feat_dim=self.feat_dim))
+            self._programs[key] = P.seal()
+            return self._programs[key]
         if fused:
             P.gemm(dv.plan_fused_head(list(feats), inv, self.w1, self.b1, self.w2, self.b2, self.logits, M=n_req,
                                       feat_dim=self.feat_dim))

@@ -1034,3 +1034,53 @@ def test_fused_head_cluster_vs_unfused_and_oracle(dev, K, N):
     p.run()
     torch.cuda.synchronize()
     assert torch.equal(out[:N].cpu(), got)
+
+
+@pytest.mark.parametrize("K,N", [(4, 1), (3, 5), (4, 16), (3, 33), (4, 70)])
+def test_head_gemv_vs_unfused_and_oracle(dev, K, N):
+    """The small-pass head (ms_gemm_plan_head_gemv: FC1 weight stream over 128
+    CTAs -> bf16 h -> PDL-chained FC2) vs the unfused three-launch head and the
+    CPU oracle's fusion_forward over all 2^K - 1 modality subsets; no row past
+    M written; bitwise identical on rerun."""
+    from oracle.forward import fusion_forward, fusion_weights as oracle_fusion_weights
+    from paper_2310_18481_b200.encoders import FEAT_DIM, FusionHead
+    g = torch.Generator().manual_seed(900 + N + K)
+    nsub = (1 << K) - 1
+    masks = (torch.arange(N) % nsub + 1)[torch.randperm(N, generator=g)]
+    head = FusionHead(K, 1024, 499, FEAT_DIM)
+    full = [_bf(torch.randn(N, FEAT_DIM, generator=g)) for _ in range(K)]
+    feats, invs = [], []
+    for k in range(K):
+        have = ((masks >> k) & 1).bool()
+        nk = int(have.sum())
+        f = torch.zeros(1024, FEAT_DIM, dtype=torch.bfloat16)
+        f[:nk] = full[k][have].to(torch.bfloat16)
+        inv = torch.full((N,), -1, dtype=torch.int32)
+        inv[have] = torch.arange(nk, dtype=torch.int32)
+        feats.append(f.cuda())
+        invs.append(inv)
+    inv = torch.stack(invs).cuda()
+    prog = head.program(N, feats, inv, fused=False, gemv=False)
+    prog.run()
+    torch.cuda.synchronize()
+    unfused = head.logits[:N].cpu().clone()
+    out = torch.full((N + 1, head.n_classes), 7.0, device="cuda")
+    h = torch.empty(N, 512, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_head_gemv(feats, inv, head.w1, head.b1, head.w2, head.b2, out, h, M=N, feat_dim=FEAT_DIM)
+    p.run()
+    torch.cuda.synchronize()
+    got = out[:N].cpu()
+    assert torch.all(out[N] == 7.0)
+    w = oracle_fusion_weights(K, FEAT_DIM, 499)
+    ref = fusion_forward([f.float() for f in full], masks, w)
+    ok, err, scale = _close(got, ref)
+    assert ok, (err, scale)
+    ok, err, scale = _close(got, unfused, tol=1e-2)
+    assert ok, (err, scale)
+    assert (got.argmax(1) == unfused.argmax(1)).float().mean().item() >= 0.99
+    p.run()
+    torch.cuda.synchronize()
+    assert torch.equal(out[:N].cpu(), got)
+    # the served dispatch picks it for small passes
+    if N <= head.GEMV_MAX_REQ:
+        assert "head_gemv" in head.program(N, feats, inv).ops[0][1].label

@@ -1,5 +1,6 @@
 """Late-fusion head: the one-launch cluster kernel vs the three-launch path
-(gather GEMM, FC2 split-K GEMM, finalize), graph-timed per request count.
+(gather GEMM, FC2 split-K GEMM, finalize) vs the two-launch GEMV head,
+graph-timed per request count.
 
     python tools/head_time.py
 """
@@ -44,15 +45,18 @@ def timed(fn, inner=20):
 for K in (3, 4):
     head = FusionHead(K, 1024, 499, FEAT_DIM)
     feats = [torch.randn(1024, FEAT_DIM, device="cuda").to(torch.bfloat16) for _ in range(K)]
-    for n in (1, 16, 64, 96, 128, 256, 1024):
+    for n in (1, 4, 8, 16, 24, 32, 48, 64, 1024):
         masks = np.arange(n) % ((1 << K) - 1) + 1
         iv = torch.full((K, n), -1, dtype=torch.int32)
         for k in range(K):
             sel = np.flatnonzero((masks >> k) & 1)
             iv[k, sel] = torch.arange(len(sel), dtype=torch.int32)
         iv = iv.cuda()
-        pu = head.program(n, feats, iv, fused=False)
-        pf = head.program(n, feats, iv, fused=True)
-        tu, tf = timed(pu.run), timed(pf.run)
-        print(f"K={K} n={n:5d}  unfused {tu:6.2f} us ({pu.n_launches} launches)  fused {tf:6.2f} us  x{tu / tf:4.2f}",
+        pu = head.program(n, feats, iv, fused=False, gemv=False)
+        pf = head.program(n, feats, iv, fused=True, gemv=False)
+        pg = head.program(n, feats, iv, gemv=True)
+        tu, tf, tg = timed(pu.run), timed(pf.run), timed(pg.run)
+        wb = head.w1.numel() * 2 + head.w2.numel() * 2
+        print(f"K={K} n={n:5d}  unfused {tu:6.2f} us ({pu.n_launches} launches)  fused {tf:6.2f} us  "
+              f"gemv {tg:6.2f} us ({wb / tg / 1e3:5.0f} GB/s of weights)  best {min((tu, 'unfused'), (tf, 'fused'), (tg, 'gemv'))[1]}",
               flush=True)
