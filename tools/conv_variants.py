@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=183)
 ap.add_argument("--inner", type=int, default=10)
 ap.add_argument("--only", default="")
+ap.add_argument("--tap-pair", action="store_true", help="tap-box / K32 plan vs the same plan on CTA pairs")
 a = ap.parse_args()
 import torch  # noqa: E402
 
@@ -73,6 +74,22 @@ for H, cin, cout in SHAPES:
     ref = D0.clone()
     fl = p0.flops
     line = f"{H:2d}x{H} {cin:3d}->{cout:3d} {'k32' if k32 else 'tap'} {t0:6.1f} us {fl / t0 / 1e6:5.0f} TF/s"
+    if a.tap_pair:  # the same tap-box / K32 plan on CTA pairs (M = 256 tiles, half of each weight box per SM)
+        D1 = torch.empty_like(D0)
+        try:
+            p1 = dv.plan_conv(X, n, H, H, cin, cin, 3, 3, 1, 1, Wk, cout, b, D1, ldd=cout, BN=BN, tile=tile, k32=k32)
+            p1.set_pair(True)
+            t1 = timed(p1.run)
+            p1.run()
+            torch.cuda.synchronize()
+            err = (D1.float() - ref.float()).abs().max().item()
+            inf = p1.info()
+            line += (f" | tap-pair {t1:6.1f} us {fl / t1 / 1e6:5.0f} TF/s x{t0 / t1:4.2f} st{inf['stages']} "
+                     f"g{inf['grid_x']} maxdiff {err:.3g}")
+        except Exception as ex:  # noqa: BLE001
+            line += f" | tap-pair n/a ({str(ex)[:60]})"
+        print(line, flush=True)
+        continue
     cc = -(-cin // 64)
     bns = -(-cout // 32) * 32
     while bns > 32 and 9 * cc * (bns // 2) * 128 > 150 * 1024:  # half of the weights resident per CTA
