@@ -34,10 +34,30 @@
 
 namespace mosel {
 
+// exact-form GELU, 0.5 x (1 + erf(x / sqrt 2)), with erf from Abramowitz &
+// Stegun 7.1.26 (|error| <= 1.5e-7, below bf16 output rounding by ~4 orders):
+// one MUFU reciprocal + one MUFU exp2 + 9 FMA-class ops and no branches,
+// where libdevice erff took ~25 instructions with divergent ranges and made
+// the ViT/BERT FC1 epilogue-bound (tools/vqa_gemm.py: 729 vs 1151 TF/s
+// without the activation at M=18912 N=3072 K=768)
+__device__ __forceinline__ float gelu_erf(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  float t, e;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  float q = fmaf(t, 1.061405429f, -1.453152027f);
+  q = fmaf(t, q, 1.421413741f);
+  q = fmaf(t, q, -0.284496736f);
+  q = fmaf(t, q, 0.254829592f);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float erf_abs = fmaf(-q * t, e, 1.0f);
+  const float erf_x = copysignf(erf_abs, x);
+  return 0.5f * x * (1.0f + erf_x);
+}
+
 __device__ __forceinline__ float activate(float x, int act) {
   switch (act) {
     case MS_ACT_RELU: return fmaxf(x, 0.0f);
-    case MS_ACT_GELU: return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+    case MS_ACT_GELU: return gelu_erf(x);
     case MS_ACT_TANH: return tanhf(x);
     default: return x;
   }

@@ -362,12 +362,12 @@ __global__ void __launch_bounds__(kHdThreads, 1)
 // rows -- before griddepcontrol.wait, so the stream overlaps the previous
 // kernel's tail), gathers each request's concatenated features through inv
 // (absent modality = zero K block, profile.py:157-159) with all of a group's
-// loads in flight, and reduces 4 rows x 8 requests per pass with a butterfly
-// transpose-reduce (31 shuffles for 32 sums).  h is rounded to bf16 (the
+// loads in flight, and reduces 4 rows x Q requests per pass with a
+// multi-sum butterfly (warp_reduce_multi).  h is rounded to bf16 (the
 // unfused path's rounding point).  A grid barrier (all 128 CTAs co-resident)
-// replaces a second launch; FC2 then gives each warp one class and reduces 32
-// requests per butterfly.  Every output has one producer in a fixed order:
-// reruns are bitwise identical.
+// replaces a second launch; FC2 then gives each warp one class at a time.
+// Every output has one producer in a fixed order: reruns are bitwise
+// identical.
 constexpr int kGvThreads = 256;
 constexpr int kGvRows = 4;      // hidden rows per FC1 CTA
 constexpr int kGvMaxCh = 2;     // K <= 2 * 256 * 8 = 4096
@@ -513,36 +513,44 @@ __global__ void __launch_bounds__(kGvThreads) head_gemv_kernel(const GemmParams 
     __syncthreads();
   }
   grid_barrier(sync);  // every h row complete (and visible at L2)
-  if (!live) return;
-  const float bias = bias2;
-  float wa[8], wb[8];
-  bf16x8_to_f32(v0, wa);
-  bf16x8_to_f32(v1, wb);
   float* out = reinterpret_cast<float*>(p.seg[0].ptr);
-  for (int g0 = 0; g0 < p.M; g0 += Q) {
-    uint4 hv[Q][2];  // the group's h chunks in flight at once
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int r = g0 + q;
-      const uint4* hr = reinterpret_cast<const uint4*>(p.hbuf + (long long)r * kHdHidden);
-      hv[q][0] = r < p.M ? __ldcg(hr + lane) : make_uint4(0, 0, 0, 0);  // L2: written by other CTAs
-      hv[q][1] = r < p.M ? __ldcg(hr + 32 + lane) : make_uint4(0, 0, 0, 0);
+  // classes cls, cls + 8 * grid, ... (the first one's row was prefetched)
+  for (int c = cls; c < p.N; c += kGvThreads / 32 * gridDim.x) {
+    float bias = bias2;
+    if (c != cls) {
+      const uint4* wr = reinterpret_cast<const uint4*>(W2 + (long long)c * kHdHidden);
+      v0 = __ldg(wr + lane);
+      v1 = __ldg(wr + 32 + lane);
+      bias = __ldg(p.red_bias + c);
     }
-    float acc[Q];
+    float wa[8], wb[8];
+    bf16x8_to_f32(v0, wa);
+    bf16x8_to_f32(v1, wb);
+    for (int g0 = 0; g0 < p.M; g0 += Q) {
+      uint4 hv[Q][2];  // the group's h chunks in flight at once
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      float ha[8], hb[8];
-      bf16x8_to_f32(hv[q][0], ha);
-      bf16x8_to_f32(hv[q][1], hb);
-      float a = 0.f;
+      for (int q = 0; q < Q; ++q) {
+        const int r = g0 + q;
+        const uint4* hr = reinterpret_cast<const uint4*>(p.hbuf + (long long)r * kHdHidden);
+        hv[q][0] = r < p.M ? __ldcg(hr + lane) : make_uint4(0, 0, 0, 0);  // L2: written by other CTAs
+        hv[q][1] = r < p.M ? __ldcg(hr + 32 + lane) : make_uint4(0, 0, 0, 0);
+      }
+      float acc[Q];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a = fmaf(wa[e], ha[e], a);
+      for (int q = 0; q < Q; ++q) {
+        float ha[8], hb[8];
+        bf16x8_to_f32(hv[q][0], ha);
+        bf16x8_to_f32(hv[q][1], hb);
+        float a = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a = fmaf(wb[e], hb[e], a);
-      acc[q] = a;
+        for (int e = 0; e < 8; ++e) a = fmaf(wa[e], ha[e], a);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a = fmaf(wb[e], hb[e], a);
+        acc[q] = a;
+      }
+      const float s = warp_reduce_multi<Q>(acc, lane);
+      if (lane < Q && g0 + lane < p.M) out[(long long)(g0 + lane) * p.seg[0].ldd + c] = s + bias;
     }
-    const float s = warp_reduce_multi<Q>(acc, lane);
-    if (lane < Q && g0 + lane < p.M) out[(long long)(g0 + lane) * p.seg[0].ldd + cls] = s + bias;
   }
 }
 
@@ -629,8 +637,7 @@ extern "C" int ms_gemm_plan_head_gemv(void* plan, const void* const* feat, const
     return set_error(MS_ERR_INVALID, "null pointer");
   if (n_mod < 1 || n_mod > 4 || feat_dim % 8 != 0 || M <= 0 || ldo < n_classes || n_classes < 1)
     return set_error(MS_ERR_INVALID, "gemv head needs 1..4 modalities, feat_dim % 8 == 0, M > 0, classes >= 1");
-  if (n_mod * feat_dim > kGvMaxCh * kGvThreads * 8 || n_classes > kHdHidden / kGvRows * (kGvThreads / 32))
-    return set_error(MS_ERR_INVALID, "gemv head needs K <= 4096 and classes <= 1024");
+  if (n_mod * feat_dim > kGvMaxCh * kGvThreads * 8) return set_error(MS_ERR_INVALID, "gemv head needs K <= 4096");
   GemmPlan* P = reinterpret_cast<GemmPlan*>(plan);
   memset(P, 0, sizeof(GemmPlan));
   GemmParams& p = P->p;
