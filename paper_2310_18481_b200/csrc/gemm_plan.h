@@ -126,7 +126,7 @@ struct GemmParams {
   const float* red_bias;  //   its bias; output = seg[1] (the pooled map itself is then not stored)
   long long x_pitch;   // bytes of one padded input row
   int Hp, PH, PW, units;
-  __nv_bfloat16* hbuf;  // MODE_HEAD_GEMV: bf16 hidden rows [M, 512] between the two launches
+  __nv_bfloat16* hbuf;  // MODE_HEAD_GEMV: bf16 hidden rows [M, 512] (caller buffer)
 };
 
 // One bf16 output tensor map per epilogue segment (TMA stores, SWIZZLE_64B):
