@@ -743,8 +743,20 @@ __global__ void __launch_bounds__(kThreads, OCC)
           }
         }
       };
-      uint32_t va[32], vb[32];
       int c = tg ? 0 : grp;
+      if constexpr (OCC == 2) {
+        // 96-register instantiation: one TMEM buffer (the double-buffered
+        // loads below spilled 280 B per thread here; the OCC=2 epilogue waits
+        // on its accumulator anyway, so the load latency is not exposed)
+        uint32_t va[32];
+        for (; c < n_chunks; c += cs) {
+          tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), va);
+          tmem_wait_ld();
+          if (c + cs >= n_chunks) release_acc();
+          process(va, c);
+        }
+      } else {
+      uint32_t va[32], vb[32];
       if (c < n_chunks) tmem_ld_32x32b_x32(t_base + (uint32_t)(c * 32), va);
       while (c < n_chunks) {
         tmem_wait_ld();
@@ -762,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, OCC)
           release_acc();
         process(vb, c);
         c += cs;
+      }
       }
       if (!tg && grp >= n_chunks) release_acc();  // no chunk for this group in a narrow tile
       if (warp == 2 && lane == 0 && t == cta0) GEMM_TRACE(11);
