@@ -272,29 +272,38 @@ __global__ void __launch_bounds__(kCPThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[slot]);
         named_bar_sync(1 + grp, 128);  // exchange rows written
-        named_bar_sync(3 + grp, 128);  // ... and read (before the next tile rewrites them)
+#pragma unroll
+        for (int c = 0; c < CPG; ++c)
+          named_bar_sync(3 + grp, 128);  // ... and read, one channel chunk at a time (before the next tile rewrites them)
         continue;
       }
-      // y == 1: rows 2i (carry), 2i+1 (exchange), 2i+2 (TMEM, when inside the map)
-      uint32_t m[CPG][16];
-      if (two) {
-#pragma unroll
-        for (int h = 0; h < 2 * CPG; ++h) {  // 16-column halves keep the live registers down
-          uint32_t v[16];
-          tmem_ld_32x32b_x16(ts + (uint32_t)(h * 16), v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            m[h >> 1][(h & 1) * 8 + e] = pack_bf16x2(__uint_as_float(v[2 * e]) + bch[h * 16 + 2 * e],
-                                                     __uint_as_float(v[2 * e + 1]) + bch[h * 16 + 2 * e + 1]);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[slot]);
-      named_bar_sync(1 + grp, 128);
+      // y == 1: rows 2i (carry), 2i+1 (exchange), 2i+2 (TMEM, when inside the map),
+      // one 32-channel chunk at a time: only that chunk's maxima are live (all
+      // CPG chunks at once kept 16 * CPG more registers and spilled the carry)
+      named_bar_sync(1 + grp, 128);  // the exchange rows are written
+      __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(Y.ptr) +
+                          (((long long)w.img * p.PH + w.i) * p.PW + j) * Y.ldd + Y.col0 + cbase;
 #pragma unroll
       for (int c = 0; c < CPG; ++c) {
+        uint32_t m[16];
+        if (two) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // 16-column halves keep the live registers down
+            const int h = 2 * c + hh;
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(ts + (uint32_t)(h * 16), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              m[hh * 8 + e] = pack_bf16x2(__uint_as_float(v[2 * e]) + bch[h * 16 + 2 * e],
+                                          __uint_as_float(v[2 * e + 1]) + bch[h * 16 + 2 * e + 1]);
+          }
+        }
+        if (c == CPG - 1) {  // every TMEM read of this slot is done
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[slot]);
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const uint4 r1 = *reinterpret_cast<const uint4*>(xrow + c * 64 + g * 16);
@@ -304,34 +313,27 @@ __global__ void __launch_bounds__(kCPThreads, 1)
             const int e = 4 * g + t;
             const uint32_t vm = bmax2(carry[c][e], r1w[t]);
             if (two) {
-              const uint32_t r2 = m[c][e];
-              m[c][e] = bmax2(vm, r2);
+              const uint32_t r2 = m[e];
+              m[e] = bmax2(vm, r2);
               carry[c][e] = r2;
             } else {
-              m[c][e] = vm;
+              m[e] = vm;
             }
           }
         }
-      }
-      // the window of pooled column 15 (x = 30, 31, 32) crosses into the x >= 32 warp
-      if (q == 3 && lane == 0) {
+        // the window of pooled column 15 (x = 30, 31, 32) crosses into the x >= 32 warp
+        if (q == 3 && lane == 0) {
 #pragma unroll
-        for (int c = 0; c < CPG; ++c)
-#pragma unroll
-          for (int e = 0; e < 16; ++e) gbnd[c * 16 + e] = m[c][e];
-      }
-      named_bar_sync(3 + grp, 128);
-      __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(Y.ptr) +
-                          (((long long)w.img * p.PH + w.i) * p.PW + j) * Y.ldd + Y.col0 + cbase;
-#pragma unroll
-      for (int c = 0; c < CPG; ++c) {
+          for (int e = 0; e < 16; ++e) gbnd[c * 16 + e] = m[e];
+        }
+        named_bar_sync(3 + grp, 128);
         uint32_t o[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const uint32_t m1 = __shfl_down_sync(0xffffffffu, m[c][e], 1);
-          uint32_t m2 = __shfl_down_sync(0xffffffffu, m[c][e], 2);
+          const uint32_t m1 = __shfl_down_sync(0xffffffffu, m[e], 1);
+          uint32_t m2 = __shfl_down_sync(0xffffffffu, m[e], 2);
           if (q == 2 && lane == 30) m2 = gbnd[c * 16 + e];
-          uint32_t h = bmax2(m[c][e], m1);
+          uint32_t h = bmax2(m[e], m1);
           if (three) h = bmax2(h, m2);
           o[e] = bmax2(h, 0u);  // ReLU
         }
