@@ -851,7 +851,7 @@ struct FusedArgs {
   FusedMod m[kMaxK];
 };
 
-__global__ void __launch_bounds__(kFusedThreads, 4) compact_fused_kernel(const __grid_constant__ FusedArgs a) {
+__global__ void __launch_bounds__(kFusedThreads, 3) compact_fused_kernel(const __grid_constant__ FusedArgs a) {
   __shared__ __align__(16) unsigned char line_buf[kMaxLineBytes];
   __shared__ long long s_dline[32];
   __shared__ int16_t s_idx[kMaxK][kFusedMaxN];
@@ -1256,7 +1256,9 @@ static int compact_fused(const uint16_t* mask, int N, int K, const void* const* 
   }
   // a few CTAs per SM, no more than the work needs at max occupancy
   long long blocks = (work * N / 2 + kMaxLineBytes - 1) / kMaxLineBytes;
-  if (blocks > 148LL * 4) blocks = 148LL * 4;  // one resident wave (<= 64 registers x 256 threads: 4 CTAs per SM)
+  // one resident wave: 3 CTAs per SM (<= 85 registers x 256 threads; the 4-CTA
+  // bound of 64 registers spilled 160 B per thread)
+  if (blocks > 148LL * 3) blocks = 148LL * 3;
   if (blocks < 1) blocks = 1;
   launch_k(compact_fused_kernel, dim3((unsigned)blocks), dim3(kFusedThreads), 0, st, 1, a);
   *done = true;
