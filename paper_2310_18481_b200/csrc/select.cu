@@ -984,7 +984,16 @@ __global__ void __launch_bounds__(kFusedThreads, 3) compact_fused_kernel(const _
       const long long v0 = (long long)c * M.per, v1 = min(M.row_vecs, v0 + M.per);
       const uint4* s4 = reinterpret_cast<const uint4*>(M.X) + MS_FUSED_SRC_ROW(k, j) * M.row_vecs;
       uint4* d4 = reinterpret_cast<uint4*>(M.G) + (long long)j * M.row_vecs;
-      for (long long v = v0 + t; v < v1; v += kFusedThreads) d4[v] = __ldcs(s4 + v);
+      long long v = v0 + t;
+      for (; v + 3 * kFusedThreads < v1; v += 4 * kFusedThreads) {  // four loads in flight per thread
+        const uint4 x0 = __ldcs(s4 + v), x1 = __ldcs(s4 + v + kFusedThreads);
+        const uint4 x2 = __ldcs(s4 + v + 2 * kFusedThreads), x3 = __ldcs(s4 + v + 3 * kFusedThreads);
+        d4[v] = x0;
+        d4[v + kFusedThreads] = x1;
+        d4[v + 2 * kFusedThreads] = x2;
+        d4[v + 3 * kFusedThreads] = x3;
+      }
+      for (; v < v1; v += kFusedThreads) d4[v] = __ldcs(s4 + v);
       MS_FUSED_PREFETCH(u + gridDim.x);
       continue;
     }
