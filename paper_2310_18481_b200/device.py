@@ -345,10 +345,13 @@ def _auto_splitk(p, M, N, BN, num_kb, split_k, dev):
     return p
 
 
-def _auto_pair(p, n_m_tiles, BN, allowed):
-    """Use 2-SM CTA pairs where they measured faster (tools/gemm_bench.py):
-    wide tiles (BN >= 128) with at least two waves of 256-row tiles."""
-    if allowed and BN >= 128 and n_m_tiles >= 4 * SM_COUNT and getattr(p, "split_k", 1) == 1:
+def _auto_pair(p, n_m_tiles, BN, allowed, N=0):
+    """Use 2-SM CTA pairs where they measured faster (tools/gemm_bench.py,
+    tools/pair_sweep.py): wide tiles (BN >= 128) with at least two waves of
+    256-row tiles, or one wave of 128-row tiles with N >= 2048 (the ViT/BERT
+    QKV and FC1 GEMMs: 1.02-1.06x)."""
+    if allowed and BN >= 128 and getattr(p, "split_k", 1) == 1 and \
+            (n_m_tiles >= 4 * SM_COUNT or (n_m_tiles >= SM_COUNT and N >= 2048)):
         p.set_pair()
     return p
 
@@ -378,7 +381,7 @@ def plan_dense(A, W, bias, D, *, K=None, BN=128, relu=False, out_fp32=False, col
         if pair:
             p.set_pair()
         else:
-            _auto_pair(p, -(-m // 128), BN, True)
+            _auto_pair(p, -(-m // 128), BN, True, W.shape[0])
     return p
 
 

@@ -610,6 +610,29 @@ def test_gemm_cta_pair_dense_vs_torch(dev, M, K, N, BN):
     assert ok, (err, scale)
 
 
+@pytest.mark.parametrize("N,act", [(3072, 2), (2304, 0)])
+def test_gemm_auto_pair_wide_n_vs_torch(dev, N, act):
+    """ViT/BERT-shaped GEMMs (one wave of 128-row tiles, N >= 2048) take the
+    CTA-pair kernel automatically; GELU (exact-form erf) and plain epilogues
+    vs a torch fp32 reference."""
+    M, K = 148 * 128 + 77, 768
+    g = torch.Generator().manual_seed(N + act)
+    A = _bf(torch.randn(M, K, generator=g)).cuda()
+    W = _bf(torch.randn(N, K, generator=g) * 0.05).cuda()
+    b = (torch.randn(N, generator=g) * 0.1).cuda()
+    D = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    p = dev.plan_dense(A, W, b, D, BN=256, act=act)
+    assert p.info()["grid_x"] % 2 == 0 and p.info()["stages"] != dev.plan_dense(A, W, b, D, BN=256, act=act,
+                                                                                  pair=False).info()["stages"]
+    p.run()
+    torch.cuda.synchronize()
+    ref = A.float() @ W.float().T + b
+    if act == 2:
+        ref = torch.nn.functional.gelu(ref)
+    ok, err, scale = _close(D.float(), ref)
+    assert ok, (err, scale)
+
+
 @pytest.mark.parametrize("n,H,Cin,Cout,k,s,pad,tile,BN", [
     (4, 56, 64, 192, 3, 1, 1, (1, 8, 16), 192), (3, 28, 96, 96, 3, 2, 1, (1, 7, 14), 96),
     (5, 7, 160, 224, 3, 1, 1, (2, 7, 7), 224),
